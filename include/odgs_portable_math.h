@@ -1,0 +1,351 @@
+/*
+ * odgs_portable_math.h — bit-reproducible transcendental functions shared by the
+ * sm_100a kernels and the CPU oracle's `PortableMath` policy.
+ *
+ * Why this exists. The reference rasterizer calls libm `std::atan2`, `std::hypot`,
+ * `std::sin`, `std::cos` and `std::exp` on float on the path to pixel means, radii
+ * and per-pixel alphas (reference proj/include/odgs/projection.hpp:25-27,45-46,84-85,
+ * covariance.hpp:35, types.hpp:30, rasterizer.hpp:249). Tile membership, tile ranges
+ * and the per-pixel walk length depend on those bits, and CUDA's libdevice and
+ * glibc round differently in the last place. Every function below is therefore built
+ * only from IEEE-754 correctly rounded operations (+, -, *, /, sqrt, fma, integer
+ * bit manipulation), so the host and the device produce the SAME bits.
+ *
+ * Precision:
+ *   pm_expf, pm_sinf, pm_cosf, pm_atan2f, pm_hypotf evaluate in binary64 and round
+ *   once to binary32: nearly always the correctly rounded float result (they agree
+ *   with glibc's float functions except in rare last-place cases).
+ *   pm_expf_blend evaluates in binary32 (7th-degree Horner), <= ~1 ulp, and is the
+ *   per-pixel exponential of the blend and backward loops, where throughput matters.
+ *
+ * Build rules (both sides): no floating-point contraction — the host oracle is
+ * compiled with -ffp-contract=off; on the device every operation here is an explicit
+ * round-to-nearest intrinsic (__dmul_rn, __fadd_rn, ...) or an explicit fma, which
+ * nvcc never re-associates or contracts. Round-to-nearest-even mode is assumed.
+ */
+#ifndef ODGS_PORTABLE_MATH_H
+#define ODGS_PORTABLE_MATH_H
+
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#if defined(__CUDACC__)
+#define PM_HD __host__ __device__ __forceinline__
+#else
+#define PM_HD static inline
+#endif
+
+/* ---------------------------------------------------------------- primitives */
+
+PM_HD double pm_dadd(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+PM_HD double pm_dsub(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+PM_HD double pm_dmul(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __dmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+PM_HD double pm_ddiv(double a, double b) {
+#if defined(__CUDA_ARCH__)
+  return __ddiv_rn(a, b);
+#else
+  return a / b;
+#endif
+}
+PM_HD double pm_dsqrt(double a) {
+#if defined(__CUDA_ARCH__)
+  return __dsqrt_rn(a);
+#else
+  return sqrt(a);
+#endif
+}
+PM_HD double pm_dfma(double a, double b, double c) { return fma(a, b, c); }
+
+PM_HD float pm_fadd(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+PM_HD float pm_fsub(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fsub_rn(a, b);
+#else
+  return a - b;
+#endif
+}
+PM_HD float pm_fmul(float a, float b) {
+#if defined(__CUDA_ARCH__)
+  return __fmul_rn(a, b);
+#else
+  return a * b;
+#endif
+}
+PM_HD float pm_ffma(float a, float b, float c) { return fmaf(a, b, c); }
+
+PM_HD float pm_d2f(double x) {
+#if defined(__CUDA_ARCH__)
+  return __double2float_rn(x);
+#else
+  return (float)x;
+#endif
+}
+
+/* 2^k as a binary64, -1022 <= k <= 1023. */
+PM_HD double pm_pow2i_d(int k) {
+  const uint64_t bits = (uint64_t)(int64_t)(k + 1023) << 52;
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double((long long)bits);
+#else
+  double d;
+  memcpy(&d, &bits, sizeof d);
+  return d;
+#endif
+}
+
+/* 2^k as a binary32, -126 <= k <= 127. */
+PM_HD float pm_pow2i_f(int k) {
+  const uint32_t bits = (uint32_t)(k + 127) << 23;
+#if defined(__CUDA_ARCH__)
+  return __uint_as_float(bits);
+#else
+  float f;
+  memcpy(&f, &bits, sizeof f);
+  return f;
+#endif
+}
+
+PM_HD int pm_isnan_d(double x) { return x != x; }
+PM_HD int pm_isinf_d(double x) { return x == x && (x - x) != (x - x); }
+
+/* Round-to-nearest-even integer of |x| < 2^51, via the 1.5*2^52 shifter. */
+PM_HD double pm_rint_d(double x) {
+  const double shifter = 0x1.8p52;
+  return pm_dsub(pm_dadd(x, shifter), shifter);
+}
+
+/* ---------------------------------------------------------------- exp */
+
+/* e^x in binary64 for -745 < x < 709 (only used on float-derived arguments). */
+PM_HD double pm_exp_core_d(double x) {
+  const double inv_ln2 = 0x1.71547652b82fep+0;
+  const double ln2_hi = 0x1.62e42fefa39efp-1;
+  const double ln2_lo = 0x1.abc9e3b39803fp-56;
+  const double kd = pm_rint_d(pm_dmul(x, inv_ln2));
+  double r = pm_dfma(-kd, ln2_hi, x);
+  r = pm_dfma(-kd, ln2_lo, r);
+  /* Taylor to degree 13 on |r| <= 0.347: truncation < 5e-18 relative. */
+  double p = 0x1.6124613a86d09p-33;
+  p = pm_dfma(p, r, 0x1.1eed8eff8d898p-29);
+  p = pm_dfma(p, r, 0x1.ae64567f544e4p-26);
+  p = pm_dfma(p, r, 0x1.27e4fb7789f5cp-22);
+  p = pm_dfma(p, r, 0x1.71de3a556c734p-19);
+  p = pm_dfma(p, r, 0x1.a01a01a01a01ap-16);
+  p = pm_dfma(p, r, 0x1.a01a01a01a01ap-13);
+  p = pm_dfma(p, r, 0x1.6c16c16c16c17p-10);
+  p = pm_dfma(p, r, 0x1.1111111111111p-7);
+  p = pm_dfma(p, r, 0x1.5555555555555p-5);
+  p = pm_dfma(p, r, 0x1.5555555555555p-3);
+  p = pm_dfma(p, r, 0x1.0p-1);
+  p = pm_dfma(p, r, 0x1.0p+0);
+  p = pm_dfma(p, r, 0x1.0p+0);
+  return pm_dmul(p, pm_pow2i_d((int)kd));
+}
+
+/* expf(x), binary64 evaluation rounded once. */
+PM_HD float pm_expf(float x) {
+  if (x != x) return x;
+  if (x < -104.0f) return 0.0f;          /* true value < half the least subnormal */
+  if (x > 89.0f) return INFINITY;        /* true value > FLT_MAX */
+  return pm_d2f(pm_exp_core_d((double)x));
+}
+
+/*
+ * expf(x) in binary32 for the per-pixel loops (argument -d2/2 <= 0). Results
+ * below 2^-126 (x < -87) are flushed to +0 — the alpha they would produce is
+ * < 1e-38 and can change neither the transmittance nor the colour.
+ */
+PM_HD float pm_expf_blend(float x) {
+  if (!(x >= -87.0f)) return (x != x) ? x : 0.0f;
+  if (x > 88.0f) return pm_expf(x);
+  const float shifter = 12582912.0f; /* 1.5 * 2^23 */
+  const float t = pm_ffma(x, 0x1.715476p+0f, shifter);
+  const float n = pm_fsub(t, shifter);
+  float r = pm_ffma(n, -0x1.62e400p-1f, x); /* n * ln2_hi is exact for |n| < 2^8 */
+  r = pm_ffma(n, -0x1.7f7d1cp-20f, r);
+  float p = 0x1.a01a02p-13f;
+  p = pm_ffma(p, r, 0x1.6c16c2p-10f);
+  p = pm_ffma(p, r, 0x1.111112p-7f);
+  p = pm_ffma(p, r, 0x1.555556p-5f);
+  p = pm_ffma(p, r, 0x1.555556p-3f);
+  p = pm_ffma(p, r, 0x1.0p-1f);
+  p = pm_ffma(p, r, 0x1.0p+0f);
+  p = pm_ffma(p, r, 0x1.0p+0f);
+  return pm_fmul(p, pm_pow2i_f((int)n));
+}
+
+/* ---------------------------------------------------------------- sin / cos */
+
+/* Reduces x to r in [-pi/4, pi/4] and the quadrant q = k mod 4 (|x| < 2^40). */
+PM_HD double pm_reduce_pio2(double x, int* q) {
+  const double two_over_pi = 0x1.45f306dc9c883p-1;
+  const double p1 = 0x1.921fb54442d18p+0;
+  const double p2 = 0x1.1a62633145c07p-54;
+  const double p3 = -0x1.f1976b7ed8fbcp-110;
+  const double kd = pm_rint_d(pm_dmul(x, two_over_pi));
+  double r = pm_dfma(-kd, p1, x);
+  r = pm_dfma(-kd, p2, r);
+  r = pm_dfma(-kd, p3, r);
+  *q = (int)((int64_t)kd & 3);
+  return r;
+}
+
+PM_HD double pm_sin_poly(double r) {
+  const double s = pm_dmul(r, r);
+  double p = 0x1.952c77030ad4ap-49;
+  p = pm_dfma(p, s, -0x1.ae7f3e733b81fp-41);
+  p = pm_dfma(p, s, 0x1.6124613a86d09p-33);
+  p = pm_dfma(p, s, -0x1.ae64567f544e4p-26);
+  p = pm_dfma(p, s, 0x1.71de3a556c734p-19);
+  p = pm_dfma(p, s, -0x1.a01a01a01a01ap-13);
+  p = pm_dfma(p, s, 0x1.1111111111111p-7);
+  p = pm_dfma(p, s, -0x1.5555555555555p-3);
+  return pm_dfma(pm_dmul(r, s), p, r);
+}
+
+PM_HD double pm_cos_poly(double r) {
+  const double s = pm_dmul(r, r);
+  double p = -0x1.6827863b97d97p-53;
+  p = pm_dfma(p, s, 0x1.ae7f3e733b81fp-45);
+  p = pm_dfma(p, s, -0x1.93974a8c07c9dp-37);
+  p = pm_dfma(p, s, 0x1.1eed8eff8d898p-29);
+  p = pm_dfma(p, s, -0x1.27e4fb7789f5cp-22);
+  p = pm_dfma(p, s, 0x1.a01a01a01a01ap-16);
+  p = pm_dfma(p, s, -0x1.6c16c16c16c17p-10);
+  p = pm_dfma(p, s, 0x1.5555555555555p-5);
+  p = pm_dfma(p, s, -0x1.0p-1);
+  return pm_dfma(s, p, 1.0);
+}
+
+PM_HD float pm_sinf(float x) {
+  if (x != x || x - x != 0.0f) return x - x; /* NaN for NaN and +-inf */
+  int q;
+  const double r = pm_reduce_pio2((double)x, &q);
+  double v;
+  switch (q) {
+    case 0: v = pm_sin_poly(r); break;
+    case 1: v = pm_cos_poly(r); break;
+    case 2: v = -pm_sin_poly(r); break;
+    default: v = -pm_cos_poly(r); break;
+  }
+  return pm_d2f(v);
+}
+
+PM_HD float pm_cosf(float x) {
+  if (x != x || x - x != 0.0f) return x - x;
+  int q;
+  const double r = pm_reduce_pio2((double)x, &q);
+  double v;
+  switch (q) {
+    case 0: v = pm_cos_poly(r); break;
+    case 1: v = -pm_sin_poly(r); break;
+    case 2: v = -pm_cos_poly(r); break;
+    default: v = pm_sin_poly(r); break;
+  }
+  return pm_d2f(v);
+}
+
+/* ---------------------------------------------------------------- atan2 / hypot */
+
+/* atan(t) for 0 <= t <= 1 in binary64. */
+PM_HD double pm_atan_unit_d(double t) {
+  const double tan_pi_8 = 0x1.a827999fcef32p-2;
+  const double pi_4 = 0x1.921fb54442d18p-1;
+  double base = 0.0, u = t;
+  if (t > tan_pi_8) {
+    u = pm_ddiv(pm_dsub(t, 1.0), pm_dadd(t, 1.0));
+    base = pi_4;
+  }
+  /* Taylor in s = u^2 to u^45 on |u| <= tan(pi/8): truncation < 2e-19. */
+  const double s = pm_dmul(u, u);
+  double p = 0x1.6c16c16c16c17p-6;
+  p = pm_dfma(p, s, -0x1.7d05f417d05f4p-6);
+  p = pm_dfma(p, s, 0x1.8f9c18f9c18fap-6);
+  p = pm_dfma(p, s, -0x1.a41a41a41a41ap-6);
+  p = pm_dfma(p, s, 0x1.bacf914c1bad0p-6);
+  p = pm_dfma(p, s, -0x1.d41d41d41d41dp-6);
+  p = pm_dfma(p, s, 0x1.f07c1f07c1f08p-6);
+  p = pm_dfma(p, s, -0x1.0842108421084p-5);
+  p = pm_dfma(p, s, 0x1.1a7b9611a7b96p-5);
+  p = pm_dfma(p, s, -0x1.2f684bda12f68p-5);
+  p = pm_dfma(p, s, 0x1.47ae147ae147bp-5);
+  p = pm_dfma(p, s, -0x1.642c8590b2164p-5);
+  p = pm_dfma(p, s, 0x1.8618618618618p-5);
+  p = pm_dfma(p, s, -0x1.af286bca1af28p-5);
+  p = pm_dfma(p, s, 0x1.e1e1e1e1e1e1ep-5);
+  p = pm_dfma(p, s, -0x1.1111111111111p-4);
+  p = pm_dfma(p, s, 0x1.3b13b13b13b14p-4);
+  p = pm_dfma(p, s, -0x1.745d1745d1746p-4);
+  p = pm_dfma(p, s, 0x1.c71c71c71c71cp-4);
+  p = pm_dfma(p, s, -0x1.2492492492492p-3);
+  p = pm_dfma(p, s, 0x1.999999999999ap-3);
+  p = pm_dfma(p, s, -0x1.5555555555555p-2);
+  return pm_dadd(base, pm_dfma(pm_dmul(u, s), p, u));
+}
+
+/* atan2f(y, x) with the C99 special-value conventions. */
+PM_HD float pm_atan2f(float y, float x) {
+  const double pi = 0x1.921fb54442d18p+1;
+  const double pi_2 = 0x1.921fb54442d18p+0;
+  const double pi_4 = 0x1.921fb54442d18p-1;
+  if (x != x || y != y) return x + y;
+  const int y_neg = signbit(y) != 0;
+  const int x_neg = signbit(x) != 0;
+  const double ax = fabs((double)x), ay = fabs((double)y);
+  double a;
+  if (ay == 0.0) {
+    a = x_neg ? pi : 0.0;
+  } else if (ax == 0.0) {
+    a = pi_2;
+  } else if (pm_isinf_d(ax) || pm_isinf_d(ay)) {
+    if (pm_isinf_d(ax) && pm_isinf_d(ay))
+      a = x_neg ? 3.0 * pi_4 : pi_4;
+    else if (pm_isinf_d(ax))
+      a = x_neg ? pi : 0.0;
+    else
+      a = pi_2;
+  } else {
+    if (ay <= ax)
+      a = pm_atan_unit_d(pm_ddiv(ay, ax));
+    else
+      a = pm_dsub(pi_2, pm_atan_unit_d(pm_ddiv(ax, ay)));
+    if (x_neg) a = pm_dsub(pi, a);
+  }
+  const float f = pm_d2f(a);
+  return y_neg ? -f : f;
+}
+
+/* hypotf(x, y) as glibc computes it: sqrt(x*x + y*y) in binary64, rounded once. */
+PM_HD float pm_hypotf(float x, float y) {
+  const double ax = fabs((double)x), ay = fabs((double)y);
+  if (pm_isinf_d(ax) || pm_isinf_d(ay)) return INFINITY;
+  if (ax != ax || ay != ay) return x + y;
+  return pm_d2f(pm_dsqrt(pm_dadd(pm_dmul(ax, ax), pm_dmul(ay, ay))));
+}
+
+#endif /* ODGS_PORTABLE_MATH_H */

@@ -1,0 +1,1369 @@
+// ref_tests.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Ports of the reference's hot-path test suites to the Eigen-free oracle, so the
+// restatement is pinned by the reference's own known answers, finite-difference
+// checks and tolerances before anything is compared against it:
+//   proj/tests/test_core.cpp        (build_covariance, sigmoid/logit)
+//   proj/tests/test_projection.cpp  (all cases)
+//   proj/tests/test_rasterizer.cpp  (all cases, incl. brute-force oracle equivalence)
+//   proj/tests/test_backward.cpp    (all cases)
+//   proj/tests/acceptance.cpp       criteria 1-5 (3 = include/odgs/gradcheck.hpp:78-164)
+// plus the PortableMath checks this build adds (portable transcendentals vs libm,
+// and the Portable float oracle passing the same rasterizer contracts).
+//
+// doctest is not available (vendor/ is not shipped), so a minimal CHECK runner is
+// used. Exit status 0 iff every check passed. Run: oracle/_build/ref_tests [filter]
+#include <cfloat>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <map>
+
+#include "odgs_oracle.hpp"
+
+using namespace oracle;
+
+// ------------------------------------------------------------------ mini runner
+namespace {
+struct Registry {
+  std::vector<std::pair<std::string, std::function<void()>>> tests;
+  static Registry& get() { static Registry r; return r; }
+};
+struct Reg { Reg(const char* n, std::function<void()> f) { Registry::get().tests.push_back({n, f}); } };
+int g_failures = 0, g_checks = 0;
+std::string g_current;
+void fail(const char* file, int line, const char* expr) {
+  ++g_failures;
+  std::printf("  FAIL [%s] %s:%d: %s\n", g_current.c_str(), file, line, expr);
+}
+struct Approx {
+  double v, eps = 1e-5 * 100;  // doctest default epsilon: scale * FLT_EPSILON * 100
+  explicit Approx(double x) : v(x), eps(std::numeric_limits<float>::epsilon() * 100) {}
+  Approx& epsilon(double e) { eps = e; return *this; }
+  friend bool operator==(double a, const Approx& b) {
+    return std::abs(a - b.v) < b.eps * (1.0 + std::max(std::abs(a), std::abs(b.v)));
+  }
+};
+}  // namespace
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CASE(name) \
+  static void CAT(test_, __LINE__)(); \
+  static Reg CAT(reg_, __LINE__)(name, CAT(test_, __LINE__)); \
+  static void CAT(test_, __LINE__)()
+#define CHECK(...) do { ++g_checks; if (!(__VA_ARGS__)) fail(__FILE__, __LINE__, #__VA_ARGS__); } while (0)
+#define CHECK_FALSE(...) CHECK(!(__VA_ARGS__))
+#define REQUIRE(...) do { ++g_checks; if (!(__VA_ARGS__)) { fail(__FILE__, __LINE__, #__VA_ARGS__); return; } } while (0)
+#define CHECK_THROWS_AS(expr, type) do { ++g_checks; bool ok_ = false; \
+  try { (void)(expr); } catch (const type&) { ok_ = true; } catch (...) {} \
+  if (!ok_) fail(__FILE__, __LINE__, "throws " #type ": " #expr); } while (0)
+
+// ------------------------------------------------------------------ helpers
+namespace {
+constexpr double kPi = pi_v<double>;
+using V3d = V3<double>;
+using M23d = M23<double>;
+using M3d = M3<double>;
+using M2d = M2<double>;
+
+template <class S, int R, int C> double maxabs(const Mat<S, R, C>& a) {
+  double m = 0;
+  for (int r = 0; r < R; ++r) for (int c = 0; c < C; ++c) m = std::max(m, (double)std::abs(a(r, c)));
+  return m;
+}
+template <class S, int R, int C> Mat<S, R, C> sub(const Mat<S, R, C>& a, const Mat<S, R, C>& b) {
+  Mat<S, R, C> o;
+  for (int r = 0; r < R; ++r) for (int c = 0; c < C; ++c) o(r, c) = a(r, c) - b(r, c);
+  return o;
+}
+template <class S, int R, int C> double fro(const Mat<S, R, C>& a) {
+  double s = 0;
+  for (int r = 0; r < R; ++r) for (int c = 0; c < C; ++c) s += (double)a(r, c) * a(r, c);
+  return std::sqrt(s);
+}
+double rel_frobenius(const M23d& a, const M23d& b) { return fro(sub(a, b)) / std::max(fro(a), fro(b)); }
+V3d scale3(double k, const V3d& v) { return {{k * v[0], k * v[1], k * v[2]}}; }
+double vnorm(const V3d& v) { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
+M3d identity3() { return {{{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}}; }
+
+V3d sample_position(std::mt19937& rng, double max_elev, double seam_margin) {  // test_projection.cpp:20-28
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  const double phi = (2.0 * u01(rng) - 1.0) * (kPi - seam_margin);
+  const double theta = (2.0 * u01(rng) - 1.0) * max_elev;
+  const double r = std::pow(10.0, -1.0 + 3.0 * u01(rng));
+  return scale3(r, {{std::cos(theta) * std::sin(phi), -std::sin(theta), std::cos(theta) * std::cos(phi)}});
+}
+
+// Eigen::AngleAxis<double>::toRotationMatrix().
+M3d angle_axis(double angle, V3d axis) {
+  const double n = vnorm(axis);
+  for (int k = 0; k < 3; ++k) axis[k] /= n;
+  const V3d sin_axis = scale3(std::sin(angle), axis);
+  const double c = std::cos(angle);
+  const V3d cos1_axis = scale3(1.0 - c, axis);
+  M3d res;
+  double tmp = cos1_axis[0] * axis[1];
+  res(0, 1) = tmp - sin_axis[2]; res(1, 0) = tmp + sin_axis[2];
+  tmp = cos1_axis[0] * axis[2];
+  res(0, 2) = tmp + sin_axis[1]; res(2, 0) = tmp - sin_axis[1];
+  tmp = cos1_axis[1] * axis[2];
+  res(1, 2) = tmp - sin_axis[0]; res(2, 1) = tmp + sin_axis[0];
+  for (int k = 0; k < 3; ++k) res(k, k) = cos1_axis[k] * axis[k] + c;
+  return res;
+}
+
+// Smallest eigenvalue of a symmetric 3x3 by cyclic Jacobi (verification only).
+double min_eig_sym3(M3d a) {
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    for (int p = 0; p < 3; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        if (std::abs(a(p, q)) < 1e-300) continue;
+        const double theta = (a(q, q) - a(p, p)) / (2 * a(p, q));
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1));
+        const double c = 1 / std::sqrt(t * t + 1), s = t * c;
+        for (int k = 0; k < 3; ++k) {
+          const double akp = a(k, p), akq = a(k, q);
+          a(k, p) = c * akp - s * akq; a(k, q) = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double apk = a(p, k), aqk = a(q, k);
+          a(p, k) = c * apk - s * aqk; a(q, k) = s * apk + c * aqk;
+        }
+      }
+  }
+  return std::min({a(0, 0), a(1, 1), a(2, 2)});
+}
+
+template <class S> double image_max_abs_diff(const std::vector<S>& a, const std::vector<S>& b) {
+  double w = 0;
+  for (std::size_t k = 0; k < a.size(); ++k) w = std::max(w, (double)std::abs(a[k] - b[k]));
+  return w;
+}
+}  // namespace
+
+// ================================================================== test_core.cpp
+TEST_CASE("core: sigmoid and logit invert each other") {  // test_core.cpp:27-37
+  std::mt19937 rng(7);
+  std::uniform_real_distribution<double> dist(-8.0, 8.0);
+  for (int i = 0; i < 100; ++i) {
+    const double x = dist(rng);
+    CHECK(logit(sigmoid(x)) == Approx(x).epsilon(1e-9));
+  }
+  CHECK_THROWS_AS(logit(0.0), std::invalid_argument);
+  CHECK_THROWS_AS(logit(1.0), std::invalid_argument);
+  CHECK_THROWS_AS(logit(-0.5), std::invalid_argument);
+}
+
+TEST_CASE("core: build_covariance identity rotation cases") {  // test_core.cpp:39-51
+  const V4<double> identity{{1, 0, 0, 0}};
+  CHECK(maxabs(sub(build_covariance<double>(identity, {{0, 0, 0}}), identity3())) < 1e-15);
+  M3d expected = identity3();
+  expected(0, 0) = 4.0;
+  CHECK(maxabs(sub(build_covariance<double>(identity, {{std::log(2.0), 0.0, 0.0}}), expected)) < 1e-14);
+}
+
+TEST_CASE("core: build_covariance matches the independent rotation oracle") {  // test_core.cpp:53-81
+  std::mt19937 rng(11);
+  std::normal_distribution<double> gauss;
+  auto rotation_oracle = [](V4<double> q) {
+    const double n = norm4(q);
+    for (int k = 0; k < 4; ++k) q[k] /= n;
+    const double w = q[0];
+    M3d vx{{{0, -q[3], q[2]}, {q[3], 0, -q[1]}, {-q[2], q[1], 0}}};
+    M3d vx2 = mul(vx, vx);
+    M3d r;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) r(i, j) = (i == j ? 1.0 : 0.0) + 2.0 * w * vx(i, j) + 2.0 * vx2(i, j);
+    return r;
+  };
+  for (int trial = 0; trial < 200; ++trial) {
+    V4<double> q;
+    for (int c = 3; c >= 0; --c) q[c] = gauss(rng);  // GCC right-to-left argument order
+    if (norm4(q) < 1e-3) continue;
+    V3<double> s;
+    for (int c = 2; c >= 0; --c) s[c] = gauss(rng) * 0.5;
+    const M3d sigma = build_covariance<double>(q, s);
+    const M3d r = rotation_oracle(q);
+    M3d d;
+    for (int i = 0; i < 3; ++i) for (int j = 0; j < 3; ++j) d(i, j) = (i == j) ? std::exp(2.0 * s[i]) : 0.0;
+    const M3d expected = mul(mul(r, d), transpose(r));
+    CHECK(maxabs(sub(sigma, expected)) < 1e-12);
+    CHECK(maxabs(sub(sigma, transpose(sigma))) < 1e-14);
+    CHECK(min_eig_sym3(sigma) >= -1e-14);
+    CHECK(sigma(0, 0) + sigma(1, 1) + sigma(2, 2) ==
+          Approx(std::exp(2 * s[0]) + std::exp(2 * s[1]) + std::exp(2 * s[2])).epsilon(1e-12));
+    V4<double> nq{{-q[0], -q[1], -q[2], -q[3]}};
+    CHECK(maxabs(sub(sigma, build_covariance<double>(nq, s))) < 1e-13);
+  }
+}
+
+TEST_CASE("core: build_covariance rejects bad quaternions") {  // test_core.cpp:83-90
+  CHECK_THROWS_AS(build_covariance<double>({{0, 0, 0, 0}}, {{0, 0, 0}}), std::invalid_argument);
+  CHECK_THROWS_AS(build_covariance<double>({{1, 0, 0, 0}}, {{0, 0, std::numeric_limits<double>::quiet_NaN()}}),
+                  std::invalid_argument);
+}
+
+// ================================================================== test_projection.cpp
+TEST_CASE("projection: to_spherical axis cases") {  // :32-46
+  auto a = to_spherical<double>({{0, 0, 1}});
+  CHECK(a.azimuth == Approx(0.0));
+  CHECK(a.elevation == Approx(0.0));
+  auto b = to_spherical<double>({{1, 0, 0}});
+  CHECK(b.azimuth == Approx(kPi / 2));
+  CHECK(b.elevation == Approx(0.0));
+  auto c = to_spherical<double>({{0, -1, 0}});
+  CHECK(c.elevation == Approx(kPi / 2));
+  CHECK(c.azimuth == Approx(0.0));
+  CHECK_THROWS_AS(to_spherical<double>({{0, 0, 0}}), std::domain_error);
+}
+
+TEST_CASE("projection: project_center axis cases") {  // :48-57
+  const double width = 1000, height = 500;
+  auto p = project_center<double>({{0, 0, 1}}, width, height);
+  CHECK(p[0] == Approx(500)); CHECK(p[1] == Approx(250));
+  p = project_center<double>({{1, 0, 0}}, width, height);
+  CHECK(p[0] == Approx(750)); CHECK(p[1] == Approx(250));
+  p = project_center<double>({{0, -1, 0}}, width, height);
+  CHECK(p[0] == Approx(500.0));
+  CHECK(std::abs(p[1]) < 1e-9);
+}
+
+TEST_CASE("projection: tangent_rotation sends the viewing ray to +z") {  // :59-79
+  CHECK(maxabs(sub(tangent_rotation<double>({0.0, 0.0}), identity3())) < 1e-15);
+  M3d expected{{{0, 0, -1}, {0, 1, 0}, {1, 0, 0}}};
+  CHECK(maxabs(sub(tangent_rotation<double>({kPi / 2, 0.0}), expected)) < 1e-15);
+  std::mt19937 rng(23);
+  int bad = 0;
+  for (int i = 0; i < 10000; ++i) {
+    const V3d mu = sample_position(rng, kPi / 2 * 0.999, 1e-6);
+    const M3d t = tangent_rotation(to_spherical(mu));
+    if (!(maxabs(sub(mul(t, transpose(t)), identity3())) < 1e-14)) ++bad;
+    const V3d aligned = mulv(t, mu);
+    const double n = vnorm(mu);
+    if (!(vnorm({{aligned[0], aligned[1], aligned[2] - n}}) < 1e-12 * n)) ++bad;
+  }
+  CHECK(bad == 0);
+}
+
+TEST_CASE("projection: perspective_jacobian") {  // :81-104
+  M23d e{{{0.5, 0, 0}, {0, 0.5, 0}}};
+  CHECK(maxabs(sub(perspective_jacobian<double>({{0, 0, 2}}, 1.0, 1.0), e)) < 1e-15);
+  M23d e2{{{1, 0, -1}, {0, 1, -1}}};
+  CHECK(maxabs(sub(perspective_jacobian<double>({{1, 1, 1}}, 1.0, 1.0), e2)) < 1e-15);
+  const double r = 3.7;
+  M23d e3{{{1 / r, 0, 0}, {0, 1 / r, 0}}};
+  CHECK(maxabs(sub(perspective_jacobian<double>({{0, 0, r}}, 1.0, 1.0), e3)) < 1e-15);
+  CHECK_THROWS_AS(perspective_jacobian<double>({{0, 0, -1}}, 1.0, 1.0), std::domain_error);
+  CHECK_THROWS_AS(perspective_jacobian<double>({{1, 1, 0}}, 1.0, 1.0), std::domain_error);
+}
+
+TEST_CASE("projection: jacobian_omni zero-angle case") {  // :106-113
+  const double width = 512, height = 256, r = 2.5;
+  M23d e{{{width / (2 * kPi * r), 0, 0}, {0, height / (kPi * r), 0}}};
+  CHECK(maxabs(sub(jacobian_omni<double>({{0, 0, r}}, width, height), e)) < 1e-12);
+}
+
+TEST_CASE("projection: factored, expanded, and direct Jacobians agree") {  // :115-130
+  const double width = 1600, height = 800;
+  std::mt19937 rng(31);
+  const double max_elev = 85.0 * kPi / 180.0;
+  double worst = 0;
+  for (int i = 0; i < 10000; ++i) {
+    const V3d mu = sample_position(rng, max_elev * 0.9999, 1e-9);
+    const M23d f = jacobian_omni_factored(mu, width, height);
+    const M23d c = jacobian_omni_closed(mu, width, height);
+    const M23d d = jacobian_omni_direct(mu, width, height);
+    worst = std::max({worst, rel_frobenius(f, c), rel_frobenius(f, d), rel_frobenius(c, d)});
+  }
+  CHECK(worst <= 1e-12);
+}
+
+TEST_CASE("projection: jacobian_omni matches finite differences of project_center") {  // :132-154
+  const double width = 1600, height = 800, step = 1e-5;
+  std::mt19937 rng(37);
+  const double max_elev = 85.0 * kPi / 180.0;
+  double worst = 0;
+  for (int i = 0; i < 10000; ++i) {
+    const V3d mu = sample_position(rng, max_elev, 0.01);
+    M23d fd;
+    for (int axis = 0; axis < 3; ++axis) {
+      V3d lo = mu, hi = mu;
+      lo[axis] -= step; hi[axis] += step;
+      const auto ph = project_center(hi, width, height), pl = project_center(lo, width, height);
+      fd(0, axis) = (ph[0] - pl[0]) / (2 * step);
+      fd(1, axis) = (ph[1] - pl[1]) / (2 * step);
+    }
+    worst = std::max(worst, rel_frobenius(jacobian_omni(mu, width, height), fd));
+  }
+  CHECK(worst < 1e-6);
+}
+
+TEST_CASE("projection: jacobian_omni clamps the polar stretch") {  // :156-172
+  const double width = 1000, height = 500;
+  const double theta = 88.0 * kPi / 180.0;
+  bool clamped = false;
+  const M23d j = jacobian_omni<double>({{0, -std::sin(theta), std::cos(theta)}}, width, height,
+                                       kDefaultMaxElevation, &clamped);
+  CHECK(clamped);
+  const double expected = width / (2 * kPi) / std::cos(85.0 * kPi / 180.0);
+  const double row0 = std::sqrt(j(0, 0) * j(0, 0) + j(0, 1) * j(0, 1) + j(0, 2) * j(0, 2));
+  CHECK(row0 == Approx(expected).epsilon(1e-9));
+  bool clamped_low = true;
+  jacobian_omni<double>({{0, 0, 1}}, width, height, kDefaultMaxElevation, &clamped_low);
+  CHECK_FALSE(clamped_low);
+}
+
+TEST_CASE("projection: project_covariance trivial and property cases") {  // :174-223
+  const double k = 7.0;
+  const double width = 2 * kPi * k, height = kPi * k;
+  const M23d j = jacobian_omni<double>({{0, 0, 1}}, width, height);
+  const double eps_lp = 0.3;
+  const M2d iso = project_covariance<double>(identity3(), identity3(), j, eps_lp);
+  M2d expected{{{k * k + eps_lp, 0}, {0, k * k + eps_lp}}};
+  CHECK(maxabs(sub(iso, expected)) < 1e-10);
+  const M2d zero = project_covariance<double>(M3d{}, identity3(), j, eps_lp);
+  M2d lp{{{eps_lp, 0}, {0, eps_lp}}};
+  CHECK(maxabs(sub(zero, lp)) < 1e-15);
+  std::mt19937 rng(41);
+  std::normal_distribution<double> gauss;
+  int bad = 0;
+  for (int i = 0; i < 10000; ++i) {
+    const V3d mu = sample_position(rng, 1.4, 1e-3);
+    const M23d jac = jacobian_omni(mu, 1024.0, 512.0);
+    M3d a;
+    for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) a(r, c) = gauss(rng);
+    const M3d sigma = mul(a, transpose(a));
+    V4<double> q;
+    for (int c = 3; c >= 0; --c) q[c] = gauss(rng);
+    const M3d rot = norm4(q) > 1e-3 ? rotation_from_quaternion(q) : identity3();
+    const M2d cov = project_covariance(sigma, rot, jac, eps_lp);
+    if (!(cov(0, 1) == cov(1, 0))) ++bad;
+    const double mid = (cov(0, 0) + cov(1, 1)) / 2;
+    const double disc = std::sqrt(std::max(0.0, mid * mid - (cov(0, 0) * cov(1, 1) - cov(0, 1) * cov(0, 1))));
+    if (!(mid - disc >= eps_lp * (1 - 1e-9))) ++bad;
+    V4<double> q2;
+    for (int c = 3; c >= 0; --c) q2[c] = gauss(rng);
+    const M3d extra = rotation_from_quaternion(norm4(q2) > 1e-3 ? V4<double>{{1, 0.3, -0.2, 0.5}}
+                                                                : V4<double>{{1, 0, 0, 0}});
+    const M2d cov2 = project_covariance<double>(mul(mul(extra, sigma), transpose(extra)),
+                                                mul(rot, transpose(extra)), jac, eps_lp);
+    if (!(maxabs(sub(cov, cov2)) < 1e-9 * fro(cov))) ++bad;
+  }
+  CHECK(bad == 0);
+}
+
+TEST_CASE("projection: project_gaussian basics") {  // :225-251
+  Cloud<double> cloud;
+  cloud.resize(1);
+  cloud.mean(0, 2) = 1;
+  for (int c = 0; c < 3; ++c) cloud.ls(0, c) = std::log(0.01);
+  Camera<double> camera = identity_camera<double>(256, 128);
+  Settings<double> settings;
+  auto splat = project_gaussian(cloud, 0, camera, settings);
+  REQUIRE(splat.has_value());
+  CHECK(splat->pixel_mean[0] == Approx(128));
+  CHECK(splat->pixel_mean[1] == Approx(64));
+  CHECK(splat->depth == Approx(1.0));
+  CHECK(splat->index == 0);
+  M2d prod = mul(splat->cov2d, splat->cov2d_inv);
+  CHECK(maxabs(sub(prod, M2d{{{1, 0}, {0, 1}}})) < 1e-4);
+  cloud.mean(0, 2) = 0.001;
+  CHECK_FALSE(project_gaussian(cloud, 0, camera, settings).has_value());
+  cloud.mean(0, 2) = 2000;
+  CHECK_FALSE(project_gaussian(cloud, 0, camera, settings).has_value());
+}
+
+TEST_CASE("projection: horizontal footprint grows as sec(theta)") {  // :253-292
+  const double width = 1024, height = 512;
+  const double s = 6.0 * 2.0 * kPi / width;
+  Cloud<double> cloud;
+  cloud.resize(1);
+  for (int c = 0; c < 3; ++c) cloud.ls(0, c) = std::log(s);
+  Camera<double> camera = identity_camera<double>((int)width, (int)height);
+  Settings<double> settings;
+  auto fitted_sigma_x = [&](double theta) {
+    cloud.mean(0, 0) = 0; cloud.mean(0, 1) = -std::sin(theta); cloud.mean(0, 2) = std::cos(theta);
+    auto splat = project_gaussian(cloud, 0, camera, settings);
+    double mass = 0, m1 = 0, m2 = 0;
+    const double cy = splat->pixel_mean[1];
+    for (int x = 0; x < camera.width; ++x) {
+      const double w = eval_splat(*splat, V2<double>{{x + 0.5, cy}});
+      mass += w; m1 += w * (x + 0.5);
+    }
+    m1 /= mass;
+    for (int x = 0; x < camera.width; ++x) {
+      const double w = eval_splat(*splat, V2<double>{{x + 0.5, cy}});
+      m2 += w * (x + 0.5 - m1) * (x + 0.5 - m1);
+    }
+    return std::sqrt(m2 / mass);
+  };
+  CHECK(fitted_sigma_x(kPi / 3) / fitted_sigma_x(0.0) == Approx(2.0).epsilon(0.05));
+}
+
+TEST_CASE("projection: project_center is 2-pi periodic in azimuth") {  // :294-307
+  std::mt19937 rng(53);
+  const double two_pi = 2 * kPi;
+  M3d full_turn{{{std::cos(two_pi), 0, std::sin(two_pi)}, {0, 1, 0}, {-std::sin(two_pi), 0, std::cos(two_pi)}}};
+  int bad = 0;
+  for (int i = 0; i < 1000; ++i) {
+    const V3d mu = sample_position(rng, 1.45, 0.02);
+    const auto a = project_center(mu, 1000.0, 500.0), b = project_center(mulv(full_turn, mu), 1000.0, 500.0);
+    if (!(std::max(std::abs(a[0] - b[0]), std::abs(a[1] - b[1])) < 1e-9)) ++bad;
+  }
+  CHECK(bad == 0);
+}
+
+// ================================================================== test_rasterizer.cpp
+namespace {
+Splat2D<double> unit_splat(double mx, double my, double opacity, V3<double> color, double depth) {  // :13-26
+  Splat2D<double> s;
+  s.pixel_mean = {{mx, my}};
+  s.cov2d = {{{1, 0}, {0, 1}}};
+  s.cov2d_inv = {{{1, 0}, {0, 1}}};
+  s.depth = depth;
+  s.radius = 3.0;
+  s.opacity = opacity;
+  s.color = color;
+  s.index = 0;
+  return s;
+}
+}  // namespace
+
+TEST_CASE("rasterizer: cull keeps the spherical shell") {  // :30-51
+  Cloud<double> cloud;
+  cloud.resize(3);
+  cloud.mean(0, 2) = 0.05;
+  cloud.mean(1, 1) = 1;
+  cloud.mean(2, 0) = 500;
+  auto cam = identity_camera<double>(64, 32);
+  const auto visible = cull(cloud, cam, 0.1, 100.0);
+  REQUIRE(visible.size() == 1);
+  CHECK(visible[0] == 1);
+  Cloud<double> empty;
+  CHECK(cull(empty, cam, 0.1, 100.0).empty());
+  cloud.mean(0, 2) = 1;
+  cloud.mean(2, 0) = 5;
+  CHECK(cull(cloud, cam, 0.1, 100.0) == std::vector<int64_t>{0, 1, 2});
+  CHECK_THROWS_AS(cull(cloud, cam, 1.0, 0.5), std::invalid_argument);
+}
+
+TEST_CASE("rasterizer: eval_splat unit peak and falloff") {  // :53-60
+  const auto s = unit_splat(10, 10, 1.0, {{1, 0, 0}}, 1.0);
+  CHECK(eval_splat(s, V2<double>{{10, 10}}) == Approx(1.0));
+  CHECK(eval_splat(s, V2<double>{{11, 10}}) == Approx(std::exp(-0.5)).epsilon(1e-12));
+  CHECK(eval_splat(s, V2<double>{{13, 10}}) == Approx(std::exp(-4.5)).epsilon(1e-12));
+}
+
+TEST_CASE("rasterizer: composite_pixel follows the blending recursion") {  // :62-108
+  Settings<double> settings;
+  const V2<double> x{{10, 10}};
+  {
+    std::vector<std::pair<Splat2D<double>, double>> stack = {{unit_splat(10, 10, 0.5, {{1, 0, 0}}, 1.0), 0.0}};
+    const auto out = composite_pixel(stack, x, settings);
+    CHECK(out.color[0] == Approx(0.5));
+    CHECK(out.color[1] == Approx(0.0));
+    CHECK(out.transmittance == Approx(0.5));
+    CHECK(out.composited == 1);
+  }
+  {
+    std::vector<std::pair<Splat2D<double>, double>> stack = {{unit_splat(10, 10, 0.5, {{1, 0, 0}}, 1.0), 0.0},
+                                                             {unit_splat(10, 10, 0.5, {{1, 0, 0}}, 2.0), 0.0}};
+    const auto out = composite_pixel(stack, x, settings);
+    CHECK(out.color[0] == Approx(0.75));
+    CHECK(out.transmittance == Approx(0.25));
+  }
+  {
+    const auto out = composite_pixel<double>({}, x, settings);
+    CHECK(out.color[0] == 0.0); CHECK(out.color[1] == 0.0); CHECK(out.color[2] == 0.0);
+    CHECK(out.transmittance == Approx(1.0));
+  }
+  {
+    std::vector<std::pair<Splat2D<double>, double>> stack = {{unit_splat(10, 10, 0.9999, {{0, 1, 0}}, 1.0), 0.0}};
+    const auto out = composite_pixel(stack, x, settings);
+    CHECK(out.color[1] == Approx(0.99));
+    CHECK(out.transmittance == Approx(0.01));
+  }
+  {
+    std::vector<std::pair<Splat2D<double>, double>> stack;
+    for (int i = 0; i < 6; ++i) stack.push_back({unit_splat(10, 10, 0.9999, {{0, 0, 1}}, 1.0 + i), 0.0});
+    const auto out = composite_pixel(stack, x, settings);
+    CHECK(out.composited == 2);
+    CHECK(out.transmittance == Approx(1e-4));
+  }
+}
+
+template <class M> static void empty_render_case() {  // :110-116
+  Cloud<float> cloud;
+  auto cam = identity_camera<float>(64, 32);
+  const auto out = render<float, M>(cloud, cam, Settings<float>{});
+  CHECK(image_max_abs_diff(out.image, std::vector<float>(out.image.size(), 0.f)) == 0.0);
+  CHECK(*std::min_element(out.transmittance.begin(), out.transmittance.end()) == 1.0f);
+}
+TEST_CASE("rasterizer: empty cloud is black with unit transmittance") {
+  empty_render_case<StdMath>();
+  empty_render_case<PortableMath>();
+}
+
+TEST_CASE("rasterizer: render rejects non-finite parameters with the culprit index") {  // :118-129
+  std::mt19937 rng(5);
+  auto cloud = random_cloud<float>(rng, 4);
+  cloud.mean(2, 1) = std::numeric_limits<float>::quiet_NaN();
+  auto cam = identity_camera<float>(64, 32);
+  bool threw = false;
+  try {
+    render(cloud, cam, Settings<float>{});
+  } catch (const std::runtime_error& e) {
+    threw = true;
+    CHECK(std::string(e.what()).find("2") != std::string::npos);
+  }
+  CHECK(threw);
+}
+
+template <class M> static void oracle_equivalence_case() {  // :131-158
+  Settings<float> settings;
+  {
+    Cloud<float> cloud;
+    cloud.resize(1);
+    cloud.mean(0, 2) = 2;
+    for (int c = 0; c < 3; ++c) cloud.ls(0, c) = std::log(0.05f);
+    cloud.raw_opacities[0] = logit(0.95f);
+    cloud.col(0, 0) = 1; cloud.col(0, 1) = 0.5; cloud.col(0, 2) = 0.25;
+    auto cam = identity_camera<float>(256, 128);
+    const auto tiled = render<float, M>(cloud, cam, settings);
+    CHECK(image_max_abs_diff(tiled.image, brute_force_render<float, M>(cloud, cam, settings)) <= 1e-5);
+  }
+  std::mt19937 rng(77);
+  for (int scene = 0; scene < 3; ++scene) {
+    const auto cloud = random_cloud<float>(rng, 100);
+    auto cam = identity_camera<float>(256, 128);
+    const auto tiled = render<float, M>(cloud, cam, settings);
+    CHECK(image_max_abs_diff(tiled.image, brute_force_render<float, M>(cloud, cam, settings)) <= 1e-5);
+  }
+}
+TEST_CASE("rasterizer: tiled render equals the brute-force oracle") {
+  oracle_equivalence_case<StdMath>();
+  oracle_equivalence_case<PortableMath>();
+}
+
+template <class M> static void permutation_case() {  // :160-173
+  std::mt19937 rng(83);
+  auto cloud = random_cloud<float>(rng, 60);
+  auto cam = identity_camera<float>(128, 64);
+  Settings<float> settings;
+  const auto base = render<float, M>(cloud, cam, settings);
+  std::vector<int64_t> perm(60);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::shuffle(perm.begin(), perm.end(), rng);
+  Cloud<float> sh;
+  sh.resize(60);
+  for (int k = 0; k < 60; ++k) {
+    const int64_t i = perm[k];
+    for (int c = 0; c < 3; ++c) { sh.mean(k, c) = cloud.mean(i, c); sh.ls(k, c) = cloud.ls(i, c); sh.col(k, c) = cloud.col(i, c); }
+    for (int c = 0; c < 4; ++c) sh.rot(k, c) = cloud.rot(i, c);
+    sh.raw_opacities[k] = cloud.raw_opacities[i];
+  }
+  const auto shuffled = render<float, M>(sh, cam, settings);
+  CHECK(image_max_abs_diff(base.image, shuffled.image) <= 1e-6);
+}
+TEST_CASE("rasterizer: render is invariant under cloud permutation") {
+  permutation_case<StdMath>();
+  permutation_case<PortableMath>();
+}
+
+template <class M> static void yaw_case() {  // :175-196
+  std::mt19937 rng(89);
+  const auto cloud = random_cloud<float>(rng, 80);
+  auto cam = identity_camera<float>(256, 128);
+  Settings<float> settings;
+  const auto base = render<float, M>(cloud, cam, settings);
+  for (const int k : {1, 17, 64, 200}) {
+    const float delta = float(k) * 2.0f * pi_v<float> / float(cam.width);
+    const auto yawed = render<float, M>(cloud, yawed_camera(cam, delta), settings);
+    float worst = 0;
+    for (int c = 0; c < 3; ++c)
+      for (int y = 0; y < cam.height; ++y)
+        for (int x = 0; x < cam.width; ++x) {
+          const int src = (x - k % cam.width + cam.width) % cam.width;
+          worst = std::max(worst, std::abs(yawed.img(c, y, x) - base.img(c, y, src)));
+        }
+    CHECK(worst <= 1e-4f);
+  }
+}
+TEST_CASE("rasterizer: camera yaw by whole pixels circularly shifts the image") {
+  yaw_case<StdMath>();
+  yaw_case<PortableMath>();
+}
+
+TEST_CASE("rasterizer: raising opacity never reduces a splat's own composited term") {  // :198-238
+  std::mt19937 rng(97);
+  std::uniform_real_distribution<double> u01(0.0, 1.0);
+  Settings<double> settings;
+  const V2<double> x{{10, 10}};
+  int bad = 0;
+  for (int trial = 0; trial < 200; ++trial) {
+    const int n = 1 + static_cast<int>(u01(rng) * 4);
+    std::vector<std::pair<Splat2D<double>, double>> stack;
+    for (int i = 0; i < n; ++i) {
+      // unit_splat(10 + u01, 10 - u01, 0.05 + 0.65 u01, ...): GCC evaluates the three
+      // draws right to left.
+      const double a3 = u01(rng), a2 = u01(rng), a1 = u01(rng);
+      stack.push_back({unit_splat(10 + a1, 10 - a2, 0.05 + 0.65 * a3, {{1, 1, 1}}, 1.0 + i), 0.0});
+    }
+    const int target = static_cast<int>(u01(rng) * n);
+    auto own_term = [&](double opacity) {
+      stack[target].first.opacity = opacity;
+      double t = 1.0, term = 0.0;
+      int done = 0;
+      for (const auto& [splat, shift] : stack) {
+        const double w = eval_splat(splat, x, shift);
+        const double alpha = std::min(settings.alpha_clamp, splat.opacity * w);
+        const double t_next = t * (1.0 - alpha);
+        if (t_next < settings.transmittance_floor) break;
+        if (done == target) term = alpha * t;
+        t = t_next;
+        ++done;
+      }
+      return term;
+    };
+    const double base_opacity = stack[target].first.opacity;
+    const double lower = own_term(base_opacity);
+    const double higher = own_term(std::min(0.9, base_opacity * 1.2));
+    if (!(higher >= lower - 1e-12)) ++bad;
+  }
+  CHECK(bad == 0);
+}
+
+// ================================================================== test_backward.cpp
+namespace {
+M23d random_mat23(std::mt19937& rng) {
+  std::normal_distribution<double> gauss;
+  M23d m;
+  for (int r = 0; r < 2; ++r) for (int c = 0; c < 3; ++c) m(r, c) = gauss(rng);
+  return m;
+}
+M3d random_spd3(std::mt19937& rng) {
+  std::normal_distribution<double> gauss;
+  M3d a;
+  for (int r = 0; r < 3; ++r) for (int c = 0; c < 3; ++c) a(r, c) = gauss(rng);
+  M3d s = mul(a, transpose(a));
+  for (int k = 0; k < 3; ++k) s(k, k) += 0.1;
+  return s;
+}
+M2d random_sym2(std::mt19937& rng) {
+  std::normal_distribution<double> gauss;
+  M2d m;
+  m(0, 0) = gauss(rng);
+  m(1, 1) = gauss(rng);
+  m(0, 1) = m(1, 0) = gauss(rng);
+  return m;
+}
+Settings<double> fd_settings() { Settings<double> s; s.cutoff_sigma = 8.0; return s; }
+Cloud<double> fd_cloud(std::mt19937& rng, int n) {  // test_backward.cpp:53-63
+  CloudBounds b;
+  b.depth_min = 0.8; b.depth_max = 10.0;
+  b.max_elevation = 75.0 * kPi / 180.0;
+  b.opacity_min = 0.1; b.opacity_max = 0.7;
+  b.scale_min = 0.02; b.scale_max = 0.12;
+  return random_cloud<double>(rng, n, b);
+}
+std::vector<double> random_probe(std::mt19937& rng, int height, int width) {  // :80-87
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  std::vector<double> probe((std::size_t)3 * height * width);
+  for (int c = 0; c < 3; ++c)
+    for (int y = 0; y < height; ++y)
+      for (int x = 0; x < width; ++x) probe[(std::size_t)c * width * height + (std::size_t)x * height + y] = u(rng);
+  return probe;
+}
+double probe_loss(const Cloud<double>& cloud, const Camera<double>& cam, const Settings<double>& settings,
+                  const std::vector<double>& probe) {
+  const auto out = render(cloud, cam, settings);
+  double loss = 0;
+  for (std::size_t k = 0; k < probe.size(); ++k) loss += out.image[k] * probe[k];
+  return loss;
+}
+}  // namespace
+
+TEST_CASE("backward: grad_T trivial, worked, and finite-difference cases") {  // :91-153
+  std::mt19937 rng(101);
+  {
+    const M23d t = random_mat23(rng);
+    CHECK(maxabs(grad_T<double>(t, random_spd3(rng), M2d{})) == 0.0);
+  }
+  {
+    M23d t{{{1, 0, 0}, {0, 1, 0}}};
+    M23d e{{{2, 0, 0}, {0, 2, 0}}};
+    CHECK(maxabs(sub(grad_T<double>(t, identity3(), M2d{{{1, 0}, {0, 1}}}), e)) < 1e-15);
+  }
+  {
+    const double h = 1e-6;
+    double worst = 0;
+    for (int trial = 0; trial < 200; ++trial) {
+      const M23d t = random_mat23(rng);
+      const M3d v = random_spd3(rng);
+      const M2d g2 = random_sym2(rng);
+      const M23d analytic = grad_T(t, v, g2);
+      auto value = [&](const M23d& tt) {
+        const M2d p = mul(mul(tt, v), transpose(tt));
+        const M2d gp = mul(transpose(g2), p);
+        return gp(0, 0) + gp(1, 1);
+      };
+      M23d fd;
+      for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 3; ++c) {
+          M23d hi = t, lo = t;
+          hi(r, c) += h; lo(r, c) -= h;
+          fd(r, c) = (value(hi) - value(lo)) / (2 * h);
+        }
+      worst = std::max(worst, fro(sub(analytic, fd)) / fro(fd));
+    }
+    CHECK(worst < 1e-8);
+  }
+  {
+    for (int term = 0; term < 12; ++term) {
+      GradTSigns signs;
+      signs.sign[(std::size_t)term] = -1;
+      double deviation = 0;
+      for (int draw = 0; draw < 3; ++draw) {
+        const M23d t = random_mat23(rng);
+        const M3d v = random_spd3(rng);
+        const M2d g2 = random_sym2(rng);
+        const M23d truth = grad_T(t, v, g2);
+        const M23d mutated = grad_T(t, v, g2, &signs);
+        deviation = std::max(deviation, fro(sub(mutated, truth)) / fro(truth));
+      }
+      CHECK(deviation > 1e-4);
+    }
+  }
+}
+
+TEST_CASE("backward: grad_position worked case and finite differences") {  // :155-241
+  const double width = 1024, height = 512;
+  CHECK(vnorm(grad_position<double>({{0.3, -0.2, 1.1}}, M23d{}, width, height)) == 0.0);
+  {
+    M23d dl_dj{};
+    dl_dj(0, 0) = 1.0;
+    const V3d g = grad_position<double>({{0, 0, 1}}, dl_dj, width, height);
+    CHECK(g[0] == Approx(0.0));
+    CHECK(g[1] == Approx(0.0));
+    CHECK(g[2] == Approx(-width / (2 * kPi)).epsilon(1e-12));
+  }
+  {
+    std::mt19937 rng(103);
+    std::uniform_real_distribution<double> u01(0.0, 1.0);
+    const double h = 1e-6;
+    double worst = 0;
+    for (int trial = 0; trial < 500; ++trial) {
+      const double phi = (2 * u01(rng) - 1) * (kPi - 0.05);
+      const double theta = (2 * u01(rng) - 1) * 1.4;
+      const double r = 0.3 + 5 * u01(rng);
+      const V3d t{{r * std::cos(theta) * std::sin(phi), -r * std::sin(theta), r * std::cos(theta) * std::cos(phi)}};
+      const M23d dl_dj = random_mat23(rng);
+      const V3d analytic = grad_position(t, dl_dj, width, height);
+      V3d fd;
+      for (int axis = 0; axis < 3; ++axis) {
+        V3d hi = t, lo = t;
+        hi[axis] += h; lo[axis] -= h;
+        auto val = [&](const V3d& p) {
+          const M23d jd = jacobian_omni_direct(p, width, height);
+          double s = 0;
+          for (int a = 0; a < 2; ++a) for (int b = 0; b < 3; ++b) s += dl_dj(a, b) * jd(a, b);
+          return s;
+        };
+        fd[axis] = (val(hi) - val(lo)) / (2 * h);
+      }
+      worst = std::max(worst, vnorm({{analytic[0] - fd[0], analytic[1] - fd[1], analytic[2] - fd[2]}}) / vnorm(fd));
+    }
+    CHECK(worst < 1e-6);
+  }
+  {
+    std::mt19937 rng(107);
+    std::uniform_real_distribution<double> u01(0.0, 1.0);
+    const double max_elev = kDefaultMaxElevation, h = 1e-7;
+    double worst = 0;
+    for (int trial = 0; trial < 200; ++trial) {
+      const double phi = (2 * u01(rng) - 1) * (kPi - 0.05);
+      const double sgn = u01(rng) < 0.5 ? -1.0 : 1.0;
+      const double theta = sgn * (85.5 + 2.5 * u01(rng)) * kPi / 180.0;
+      const double r = 0.5 + 2 * u01(rng);
+      const V3d t{{r * std::cos(theta) * std::sin(phi), -r * std::sin(theta), r * std::cos(theta) * std::cos(phi)}};
+      const M23d dl_dj = random_mat23(rng);
+      const V3d analytic = grad_position_clamped(t, dl_dj, width, height, max_elev);
+      auto value = [&](const V3d& p) {
+        const M23d jf = jacobian_omni_factored(p, width, height, max_elev);
+        double s = 0;
+        for (int a = 0; a < 2; ++a) for (int b = 0; b < 3; ++b) s += dl_dj(a, b) * jf(a, b);
+        return s;
+      };
+      V3d fd;
+      for (int axis = 0; axis < 3; ++axis) {
+        V3d hi = t, lo = t;
+        hi[axis] += h; lo[axis] -= h;
+        fd[axis] = (value(hi) - value(lo)) / (2 * h);
+      }
+      worst = std::max(worst, vnorm({{analytic[0] - fd[0], analytic[1] - fd[1], analytic[2] - fd[2]}}) / vnorm(fd));
+    }
+    CHECK(worst < 1e-5);
+  }
+}
+
+TEST_CASE("backward: grad_cov3d_params") {  // :243-300
+  std::mt19937 rng(109);
+  std::normal_distribution<double> gauss;
+  {
+    const auto [dq, ds] = grad_cov3d_params<double>(M3d{}, {{1, 0.2, -0.1, 0.4}}, {{0.1, -0.3, 0.0}});
+    CHECK(norm4(dq) == 0.0);
+    CHECK(vnorm(ds) == 0.0);
+  }
+  {
+    int bad = 0;
+    for (int trial = 0; trial < 100; ++trial) {
+      V4<double> q;
+      for (int c = 3; c >= 0; --c) q[c] = gauss(rng);
+      if (norm4(q) < 1e-3) continue;
+      V3d ls;
+      for (int c = 2; c >= 0; --c) ls[c] = 0.3 * gauss(rng);
+      M3d g = random_spd3(rng);
+      const double tr = g(0, 0) + g(1, 1) + g(2, 2);
+      for (int k = 0; k < 3; ++k) g(k, k) -= 0.5 * tr;
+      const auto [dq, ds] = grad_cov3d_params<double>(g, q, ls);
+      const double dot = dq[0] * q[0] + dq[1] * q[1] + dq[2] * q[2] + dq[3] * q[3];
+      if (!(std::abs(dot) <= 1e-10 * std::max(1.0, norm4(dq) * norm4(q)))) ++bad;
+    }
+    CHECK(bad == 0);
+  }
+  {
+    const double h = 1e-6;
+    double worst = 0;
+    for (int trial = 0; trial < 200; ++trial) {
+      V4<double> q;
+      for (int c = 3; c >= 0; --c) q[c] = gauss(rng);
+      if (norm4(q) < 0.1) continue;
+      V3d ls;
+      for (int c = 2; c >= 0; --c) ls[c] = 0.4 * gauss(rng);
+      // random_spd3(rng) - random_spd3(rng): GCC evaluates the right operand first.
+      const M3d b = random_spd3(rng);
+      const M3d a = random_spd3(rng);
+      const M3d sym = sub(a, b);
+      auto value = [&](const V4<double>& qq, const V3d& ss) {
+        const M3d c = build_covariance(qq, ss);
+        double s = 0;
+        for (int r = 0; r < 3; ++r) for (int k = 0; k < 3; ++k) s += sym(r, k) * c(r, k);
+        return s;
+      };
+      const auto [dq, ds] = grad_cov3d_params(sym, q, ls);
+      V4<double> fdq;
+      for (int k = 0; k < 4; ++k) {
+        V4<double> hi = q, lo = q;
+        hi[k] += h; lo[k] -= h;
+        fdq[k] = (value(hi, ls) - value(lo, ls)) / (2 * h);
+      }
+      V3d fds;
+      for (int k = 0; k < 3; ++k) {
+        V3d hi = ls, lo = ls;
+        hi[k] += h; lo[k] -= h;
+        fds[k] = (value(q, hi) - value(q, lo)) / (2 * h);
+      }
+      V4<double> eq{{dq[0] - fdq[0], dq[1] - fdq[1], dq[2] - fdq[2], dq[3] - fdq[3]}};
+      worst = std::max(worst, norm4(eq) / std::max(1e-12, norm4(fdq)));
+      worst = std::max(worst, vnorm({{ds[0] - fds[0], ds[1] - fds[1], ds[2] - fds[2]}}) / std::max(1e-12, vnorm(fds)));
+    }
+    CHECK(worst < 1e-6);
+  }
+}
+
+TEST_CASE("backward: grad_pixels_to_splats") {  // :302-432
+  {
+    std::mt19937 rng(113);
+    const auto cloud = fd_cloud(rng, 5);
+    const auto cam = identity_camera<double>(64, 32);
+    const auto settings = fd_settings();
+    const auto fwd = render(cloud, cam, settings);
+    const auto grads = grad_pixels_to_splats(fwd, std::vector<double>((std::size_t)3 * 32 * 64, 0.0), settings);
+    bool all_zero = true;
+    for (const auto& g : grads) {
+      all_zero = all_zero && g.pixel_mean[0] == 0 && g.pixel_mean[1] == 0 && maxabs(g.cov2d) == 0 && g.opacity == 0 &&
+                 g.color[0] == 0 && g.color[1] == 0 && g.color[2] == 0;
+    }
+    CHECK(all_zero);
+  }
+  {
+    Cloud<double> cloud;
+    cloud.resize(1);
+    cloud.mean(0, 2) = 1;
+    for (int c = 0; c < 3; ++c) cloud.ls(0, c) = std::log(0.05);
+    cloud.raw_opacities[0] = logit(0.6);
+    cloud.col(0, 0) = 0.2; cloud.col(0, 1) = 0.4; cloud.col(0, 2) = 0.8;
+    const auto cam = identity_camera<double>(64, 32);
+    Settings<double> settings;
+    const auto fwd = render(cloud, cam, settings);
+    std::vector<double> probe((std::size_t)3 * 32 * 64, 0.0);
+    probe[(std::size_t)1 * 32 * 64 + (std::size_t)31 * 32 + 15] = 1.0;
+    const auto grads = grad_pixels_to_splats(fwd, probe, settings);
+    REQUIRE(grads.size() == 1);
+    const double w = eval_splat(fwd.splats[0], V2<double>{{31.5, 15.5}});
+    const double alpha = 0.6 * w;
+    CHECK(grads[0].color[0] == Approx(0.0));
+    CHECK(grads[0].color[1] == Approx(alpha).epsilon(1e-12));
+    CHECK(grads[0].color[2] == Approx(0.0));
+    CHECK(grads[0].opacity == Approx(w * cloud.col(0, 1)).epsilon(1e-12));
+    CHECK(std::abs(grads[0].cov2d(0, 1) - grads[0].cov2d(1, 0)) <= 1e-12 * std::max(1.0, std::abs(grads[0].cov2d(0, 1))));
+  }
+  {
+    std::mt19937 rng(127);
+    const auto settings = fd_settings();
+    const auto cam = identity_camera<double>(64, 32);
+    const auto cloud = fd_cloud(rng, 5);
+    const auto probe = random_probe(rng, 32, 64);
+    const auto fwd = render(cloud, cam, settings);
+    const auto grads = grad_pixels_to_splats(fwd, probe, settings);
+    auto value = [&](std::vector<Splat2D<double>> splats) {
+      for (auto& s : splats) {
+        const double det = s.cov2d(0, 0) * s.cov2d(1, 1) - s.cov2d(1, 0) * s.cov2d(0, 1);
+        s.cov2d_inv = {{{s.cov2d(1, 1) / det, -s.cov2d(0, 1) / det}, {-s.cov2d(0, 1) / det, s.cov2d(0, 0) / det}}};
+      }
+      double loss = 0;
+      const double cutoff2 = settings.cutoff_sigma * settings.cutoff_sigma;
+      for (int py = 0; py < cam.height; ++py)
+        for (int px = 0; px < cam.width; ++px) {
+          double t = 1.0, color[3] = {0, 0, 0};
+          for (const auto& inst : fwd.instances) {
+            const auto& s = splats[(std::size_t)inst.splat];
+            const double dx = px + 0.5 - (s.pixel_mean[0] + inst.shift);
+            const double dy = py + 0.5 - s.pixel_mean[1];
+            const double d2 = s.cov2d_inv(0, 0) * dx * dx + 2 * s.cov2d_inv(0, 1) * dx * dy + s.cov2d_inv(1, 1) * dy * dy;
+            if (d2 > cutoff2) continue;
+            const double alpha = std::min(settings.alpha_clamp, s.opacity * std::exp(-d2 / 2));
+            const double t_next = t * (1 - alpha);
+            if (t_next < settings.transmittance_floor) break;
+            for (int c = 0; c < 3; ++c) color[c] += s.color[c] * (alpha * t);
+            t = t_next;
+          }
+          for (int c = 0; c < 3; ++c) loss += probe[(std::size_t)c * 32 * 64 + (std::size_t)px * 32 + py] * color[c];
+        }
+      return loss;
+    };
+    const double h = 1e-5;
+    double worst = 0;
+    for (std::size_t s = 0; s < fwd.splats.size(); ++s) {
+      auto fd_against = [&](auto&& mutate, double analytic, double scale) {
+        auto hi = fwd.splats, lo = fwd.splats;
+        mutate(hi[s], +h);
+        mutate(lo[s], -h);
+        const double fd = (value(hi) - value(lo)) / (2 * h);
+        worst = std::max(worst, std::abs(fd - analytic) / std::max(scale, std::abs(fd)));
+      };
+      const double scale = 1e-6;
+      fd_against([](Splat2D<double>& sp, double d) { sp.pixel_mean[0] += d; }, grads[s].pixel_mean[0], scale);
+      fd_against([](Splat2D<double>& sp, double d) { sp.pixel_mean[1] += d; }, grads[s].pixel_mean[1], scale);
+      fd_against([](Splat2D<double>& sp, double d) { sp.opacity += d; }, grads[s].opacity, scale);
+      for (int c = 0; c < 3; ++c)
+        fd_against([c](Splat2D<double>& sp, double d) { sp.color[c] += d; }, grads[s].color[c], scale);
+      fd_against([](Splat2D<double>& sp, double d) { sp.cov2d(0, 0) += d; }, grads[s].cov2d(0, 0), scale);
+      fd_against([](Splat2D<double>& sp, double d) { sp.cov2d(1, 1) += d; }, grads[s].cov2d(1, 1), scale);
+      fd_against([](Splat2D<double>& sp, double d) { sp.cov2d(0, 1) += d; sp.cov2d(1, 0) += d; },
+                 grads[s].cov2d(0, 1) + grads[s].cov2d(1, 0), scale);
+    }
+    CHECK(worst < 1e-4);
+  }
+}
+
+TEST_CASE("backward: end to end") {  // :434-557
+  {
+    std::mt19937 rng(131);
+    const auto cloud = fd_cloud(rng, 6);
+    const auto cam = identity_camera<double>(64, 32);
+    const auto settings = fd_settings();
+    const auto fwd = render(cloud, cam, settings);
+    const auto g = backward(cloud, cam, fwd, std::vector<double>((std::size_t)3 * 32 * 64, 0.0), settings);
+    double m = 0;
+    for (auto* v : {&g.means, &g.rotations, &g.log_scales, &g.raw_opacities, &g.colors})
+      for (double x : *v) m = std::max(m, std::abs(x));
+    CHECK(m == 0.0);
+  }
+  {
+    Cloud<double> cloud;
+    cloud.resize(1);
+    cloud.mean(0, 2) = 2;
+    for (int c = 0; c < 3; ++c) cloud.ls(0, c) = std::log(0.08);
+    cloud.raw_opacities[0] = logit(0.7);
+    for (int c = 0; c < 3; ++c) cloud.col(0, c) = 0.9;
+    const auto cam = identity_camera<double>(128, 64);
+    Settings<double> settings;
+    Cloud<double> shifted = cloud;
+    shifted.mean(0, 0) += 0.02;
+    const auto target = render(shifted, cam, settings).image;
+    const auto fwd = render(cloud, cam, settings);
+    std::vector<double> dl(fwd.image.size());
+    for (std::size_t k = 0; k < dl.size(); ++k) dl[k] = fwd.image[k] - target[k];
+    const auto g = backward(cloud, cam, fwd, dl, settings);
+    CHECK(g.means[0] < 0.0);
+  }
+  {
+    std::mt19937 rng(137);
+    const auto cam = identity_camera<double>(64, 32);
+    const auto settings = fd_settings();
+    int checked = 0;
+    for (int scene = 0; scene < 3; ++scene) {
+      Cloud<double> cloud = fd_cloud(rng, 8);
+      auto fwd = render(cloud, cam, settings);
+      if (*std::min_element(fwd.transmittance.begin(), fwd.transmittance.end()) < 1e-2) continue;
+      ++checked;
+      const auto probe = random_probe(rng, 32, 64);
+      const auto grads = backward(cloud, cam, fwd, probe, settings);
+      auto group_rel = [&](std::vector<double> Cloud<double>::*field, const std::vector<double>& an_vec) {
+        double max_abs_fd = 0, max_abs_an = 0, max_diff = 0;
+        for (std::size_t k = 0; k < an_vec.size(); ++k) {
+          const double an = an_vec[k];
+          Cloud<double> hi = cloud, lo = cloud;
+          const double h = 1e-4;
+          (hi.*field)[k] += h;
+          (lo.*field)[k] -= h;
+          const double fd = (probe_loss(hi, cam, settings, probe) - probe_loss(lo, cam, settings, probe)) / (2 * h);
+          max_abs_fd = std::max(max_abs_fd, std::abs(fd));
+          max_abs_an = std::max(max_abs_an, std::abs(an));
+          max_diff = std::max(max_diff, std::abs(fd - an));
+        }
+        return max_diff / std::max({max_abs_fd, max_abs_an, 1e-12});
+      };
+      const double tol = 1e-3;
+      CHECK(group_rel(&Cloud<double>::means, grads.means) < tol);
+      CHECK(group_rel(&Cloud<double>::rotations, grads.rotations) < tol);
+      CHECK(group_rel(&Cloud<double>::log_scales, grads.log_scales) < tol);
+      CHECK(group_rel(&Cloud<double>::raw_opacities, grads.raw_opacities) < tol);
+      CHECK(group_rel(&Cloud<double>::colors, grads.colors) < tol);
+    }
+    CHECK(checked > 0);
+  }
+  {
+    std::mt19937 rng(139);
+    const auto cloud = fd_cloud(rng, 6);
+    const auto settings = fd_settings();
+    const auto cam_a = identity_camera<double>(64, 32);
+    Camera<double> cam_b = cam_a;
+    cam_b.translation = {{0.1, 0.0, -0.2}};
+    const auto probe = random_probe(rng, 32, 64);
+    const auto fwd_a = render(cloud, cam_a, settings);
+    const auto fwd_b = render(cloud, cam_b, settings);
+    auto sum = backward(cloud, cam_a, fwd_a, probe, settings);
+    const auto gb = backward(cloud, cam_b, fwd_b, probe, settings);
+    sum.accumulate(gb);
+    const auto only_a = backward(cloud, cam_a, fwd_a, probe, settings);
+    double worst = 0;
+    for (std::size_t k = 0; k < sum.means.size(); ++k) worst = std::max(worst, std::abs((sum.means[k] - gb.means[k]) - only_a.means[k]));
+    CHECK(worst < 1e-12);
+    CHECK(*std::max_element(sum.observed.begin(), sum.observed.end()) <= 2);
+  }
+}
+
+// ================================================================== acceptance.cpp 1-5
+namespace {
+V3d acc_sample_position(std::mt19937& rng, double margin_rad = 0.0) {  // acceptance.cpp:48-57
+  std::uniform_real_distribution<double> uni(0.0, 1.0);
+  const double max_el = 85.0 * kPi / 180.0;
+  const double elevation = (2 * uni(rng) - 1) * max_el;
+  const double azimuth = (2 * uni(rng) - 1) * (kPi - margin_rad);
+  const double r = std::pow(10.0, -1.0 + 3.0 * uni(rng));
+  const double cos_el = std::cos(elevation);
+  return {{r * cos_el * std::sin(azimuth), -r * std::sin(elevation), r * cos_el * std::cos(azimuth)}};
+}
+Cloud<double> oracle_scene(std::mt19937& rng, int n) {  // acceptance.cpp:63-85
+  std::uniform_real_distribution<double> uni(0.0, 1.0);
+  std::normal_distribution<double> normal(0.0, 1.0);
+  Cloud<double> cloud;
+  cloud.resize(n);
+  for (int i = 0; i < n; ++i) {
+    const double azimuth = (2 * uni(rng) - 1) * kPi;
+    const double elevation = (2 * uni(rng) - 1) * 1.4;
+    const double depth = 1.0 + 7.0 * uni(rng);
+    const double cos_el = std::cos(elevation);
+    cloud.mean(i, 0) = depth * cos_el * std::sin(azimuth);
+    cloud.mean(i, 1) = -depth * std::sin(elevation);
+    cloud.mean(i, 2) = depth * cos_el * std::cos(azimuth);
+    for (int c = 0; c < 3; ++c) cloud.ls(i, c) = std::log(depth * (0.03 + 0.15 * uni(rng)));
+    V4<double> q;
+    for (int c = 0; c < 4; ++c) q[c] = normal(rng);
+    const double qn = norm4(q);
+    for (int c = 0; c < 4; ++c) cloud.rot(i, c) = q[c] / qn;
+    cloud.raw_opacities[i] = logit(0.05 + 0.9 * uni(rng));
+    for (int c = 0; c < 3; ++c) cloud.col(i, c) = uni(rng);
+  }
+  return cloud;
+}
+Cloud<double> gradcheck_cloud(std::mt19937& rng, int n, const Camera<double>& camera) {  // gradcheck.hpp:48-74
+  std::uniform_real_distribution<double> uni(0.0, 1.0);
+  std::normal_distribution<double> normal(0.0, 1.0);
+  Cloud<double> cloud;
+  cloud.resize(n);
+  for (int i = 0; i < n; ++i) {
+    const double azimuth = 2.8 * (2 * uni(rng) - 1);
+    const double elevation = 1.3 * (2 * uni(rng) - 1);
+    const double depth = 0.8 + 9.2 * uni(rng);
+    const double cos_el = std::cos(elevation);
+    const V3d in_cam{{depth * cos_el * std::sin(azimuth), -depth * std::sin(elevation), depth * cos_el * std::cos(azimuth)}};
+    const V3d d{{in_cam[0] - camera.translation[0], in_cam[1] - camera.translation[1], in_cam[2] - camera.translation[2]}};
+    const V3d w = mulv(transpose(camera.rotation), d);
+    for (int c = 0; c < 3; ++c) cloud.mean(i, c) = w[c];
+    for (int c = 0; c < 3; ++c) cloud.ls(i, c) = std::log(depth * (0.02 + 0.10 * uni(rng)));
+    V4<double> q;
+    for (int c = 0; c < 4; ++c) q[c] = normal(rng);
+    const double qn = norm4(q);
+    for (int c = 0; c < 4; ++c) cloud.rot(i, c) = q[c] / qn;
+    cloud.raw_opacities[i] = logit(0.1 + 0.6 * uni(rng));
+    for (int c = 0; c < 3; ++c) cloud.col(i, c) = uni(rng);
+  }
+  return cloud;
+}
+struct GradcheckReport { double worst = 0; int scenes = 0; bool pass = false; };
+GradcheckReport run_gradcheck(int scenes_wanted = 20, int mutate_term = -1) {  // gradcheck.hpp:78-164
+  const unsigned seed = 1;
+  const int max_gaussians = 10, width = 64, height = 32;
+  const double lambda_ssim = 0.2, tolerance = 1e-3, step = 1e-4;
+  Settings<double> settings;
+  settings.threads = 1;
+  settings.cutoff_sigma = 8;
+  GradTSigns signs;
+  if (mutate_term >= 0 && mutate_term < 12) signs.sign[(std::size_t)mutate_term] = -1;
+  Camera<double> camera;
+  camera.rotation = angle_axis(0.8, {{1, 2, 3}});
+  camera.translation = {{0.1, -0.2, 0.15}};
+  camera.width = width;
+  camera.height = height;
+  GradcheckReport report;
+  double groups[5] = {0, 0, 0, 0, 0};
+  std::mt19937 rng(seed);
+  std::uniform_int_distribution<int> size_dist(3, max_gaussians);
+  while (report.scenes < scenes_wanted) {
+    Cloud<double> cloud = gradcheck_cloud(rng, size_dist(rng), camera);
+    const auto target = render(gradcheck_cloud(rng, size_dist(rng), camera), camera, settings).image;
+    const auto probe = render(cloud, camera, settings);
+    if (*std::min_element(probe.transmittance.begin(), probe.transmittance.end()) < 1e-2) continue;
+    ++report.scenes;
+    std::vector<double> lgrad;
+    photometric_loss(probe.image, target, height, width, lambda_ssim, &lgrad);
+    const auto analytic = backward(cloud, camera, probe, lgrad, settings, &signs);
+    auto loss_at = [&](const Cloud<double>& c) {
+      std::vector<double> g;
+      return photometric_loss(render(c, camera, settings).image, target, height, width, lambda_ssim, &g);
+    };
+    auto fd = [&](double& param) {
+      const double saved = param;
+      const double h = step * std::max(1.0, std::abs(saved));
+      param = saved + h;
+      const double up = loss_at(cloud);
+      param = saved - h;
+      const double down = loss_at(cloud);
+      param = saved;
+      return (up - down) / (2 * h);
+    };
+    // Row-major traversal (i, c) of the reference's check_group.
+    auto check_group = [&](double& group, std::vector<double>& params, const std::vector<double>& grads, int cols) {
+      double max_diff = 0, max_scale = 1e-12;
+      const int64_t n = cloud.n;
+      for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < cols; ++c) {
+          const double numeric = fd(params[c * n + i]);
+          max_diff = std::max(max_diff, std::abs(numeric - grads[c * n + i]));
+          max_scale = std::max({max_scale, std::abs(numeric), std::abs(grads[c * n + i])});
+        }
+      group = std::max(group, max_diff / max_scale);
+    };
+    check_group(groups[0], cloud.means, analytic.means, 3);
+    check_group(groups[1], cloud.rotations, analytic.rotations, 4);
+    check_group(groups[2], cloud.log_scales, analytic.log_scales, 3);
+    check_group(groups[3], cloud.raw_opacities, analytic.raw_opacities, 1);
+    check_group(groups[4], cloud.colors, analytic.colors, 3);
+  }
+  for (double g : groups) report.worst = std::max(report.worst, g);
+  report.pass = report.worst < tolerance;
+  return report;
+}
+}  // namespace
+
+TEST_CASE("acceptance 1: the three jacobian derivations agree") {  // acceptance.cpp:144-164
+  std::mt19937 rng(101);
+  double worst = 0;
+  for (int k = 0; k < 10000; ++k) {
+    const V3d mu = acc_sample_position(rng);
+    const M23d f = jacobian_omni_factored(mu, 1024.0, 512.0);
+    const M23d c = jacobian_omni_closed(mu, 1024.0, 512.0);
+    const M23d d = jacobian_omni_direct(mu, 1024.0, 512.0);
+    worst = std::max({worst, rel_frobenius(f, c), rel_frobenius(c, d), rel_frobenius(f, d)});
+  }
+  std::printf("  [1] jacobian three-way agreement: max rel %.2e vs 1e-12\n", worst);
+  CHECK(worst <= 1e-12);
+}
+
+TEST_CASE("acceptance 2: jacobian matches finite differences of the projection") {  // :166-194
+  std::mt19937 rng(202);
+  const double h = 1e-5;
+  double worst = 0;
+  for (int k = 0; k < 10000; ++k) {
+    const V3d mu = acc_sample_position(rng, 0.01);
+    M23d fd;
+    for (int c = 0; c < 3; ++c) {
+      V3d up = mu, down = mu;
+      up[c] += h; down[c] -= h;
+      const auto pu = project_center(up, 1024.0, 512.0), pd = project_center(down, 1024.0, 512.0);
+      fd(0, c) = (pu[0] - pd[0]) / (2 * h);
+      fd(1, c) = (pu[1] - pd[1]) / (2 * h);
+    }
+    worst = std::max(worst, rel_frobenius(jacobian_omni(mu, 1024.0, 512.0), fd));
+  }
+  std::printf("  [2] jacobian vs finite differences: max rel %.2e vs 1e-6\n", worst);
+  CHECK(worst < 1e-6);
+}
+
+TEST_CASE("acceptance 3: analytic gradients of the photometric loss") {  // :196-217
+  const auto clean = run_gradcheck();
+  REQUIRE(clean.scenes == 20);
+  int caught = 0;
+  for (int term = 0; term < 12; ++term)
+    if (!run_gradcheck(2, term).pass) ++caught;
+  std::printf("  [3] backward finite differences: worst rel %.2e vs 1e-3 on 20 scenes, %d/12 sign flips caught\n",
+              clean.worst, caught);
+  CHECK(clean.pass);
+  CHECK(caught == 12);
+}
+
+TEST_CASE("acceptance 4: tiled rendering equals the brute-force oracle") {  // :219-242
+  std::mt19937 rng(404);
+  Settings<double> settings;
+  settings.threads = 1;
+  auto camera = identity_camera<double>(256, 128);
+  double worst = 0;
+  for (int scene = 0; scene < 10; ++scene) {
+    const auto cloud = oracle_scene(rng, 100);
+    worst = std::max(worst, image_max_abs_diff(render(cloud, camera, settings).image,
+                                               brute_force_render(cloud, camera, settings)));
+  }
+  std::printf("  [4] rasterizer oracle equivalence: max channel diff %.2e vs 1e-5\n", worst);
+  CHECK(worst <= 1e-5);
+}
+
+TEST_CASE("acceptance 5: a yaw by whole pixels circularly shifts the panorama") {  // :244-282
+  std::mt19937 rng(505);
+  Settings<double> settings;
+  settings.threads = 1;
+  const int width = 256, height = 128;
+  const auto cloud = oracle_scene(rng, 60);
+  Camera<double> base;
+  base.rotation = angle_axis(0.4, {{0.2, 1, -0.1}});
+  base.translation = {{0.2, -0.1, 0.3}};
+  base.width = width;
+  base.height = height;
+  const auto original = render(cloud, base, settings);
+  double worst = 0;
+  for (const int k : {1, 37, 128}) {
+    const double yaw = 2 * kPi * k / width;
+    M3d spin{{{std::cos(yaw), 0, -std::sin(yaw)}, {0, 1, 0}, {std::sin(yaw), 0, std::cos(yaw)}}};
+    Camera<double> turned = base;
+    turned.rotation = mul(spin, base.rotation);
+    turned.translation = mulv(spin, base.translation);
+    const auto shifted = render(cloud, turned, settings);
+    for (int c = 0; c < 3; ++c)
+      for (int y = 0; y < height; ++y)
+        for (int x = 0; x < width; ++x)
+          worst = std::max(worst, std::abs(shifted.img(c, y, (x - k + width) % width) - original.img(c, y, x)));
+  }
+  std::printf("  [5] yaw-shift invariance: max channel diff %.2e vs 1e-4\n", worst);
+  CHECK(worst <= 1e-4);
+}
+
+// ================================================================== PortableMath (this build)
+namespace {
+int64_t ulp_diff(float a, float b) {
+  if (a == b) return 0;
+  if (a != a || b != b) return (a != a && b != b) ? 0 : INT64_MAX;
+  int32_t ia, ib;
+  std::memcpy(&ia, &a, 4);
+  std::memcpy(&ib, &b, 4);
+  if (ia < 0) ia = INT32_MIN - ia;
+  if (ib < 0) ib = INT32_MIN - ib;
+  return std::abs((int64_t)ia - (int64_t)ib);
+}
+}  // namespace
+
+TEST_CASE("portable math: within 1 ulp of libm on the arguments the path sees") {
+  std::mt19937 rng(2024);
+  std::uniform_real_distribution<float> ang(-3.2f, 3.2f), ex(-40.f, 10.f), bl(-50.f, 0.f), co(-30.f, 30.f);
+  int64_t w_exp = 0, w_blend = 0, w_sin = 0, w_cos = 0, w_atan2 = 0, w_hypot = 0;
+  int64_t diff_exp = 0, diff_atan2 = 0;
+  const int n = 2000000;
+  for (int k = 0; k < n; ++k) {
+    const float a = ang(rng), e = ex(rng), b = bl(rng), y = co(rng), x = co(rng);
+    const int64_t de = ulp_diff(pm_expf(e), std::exp(e));
+    w_exp = std::max(w_exp, de);
+    diff_exp += de != 0;
+    w_blend = std::max(w_blend, ulp_diff(pm_expf_blend(b), std::exp(b)));
+    w_sin = std::max(w_sin, ulp_diff(pm_sinf(a), std::sin(a)));
+    w_cos = std::max(w_cos, ulp_diff(pm_cosf(a), std::cos(a)));
+    const int64_t da = ulp_diff(pm_atan2f(y, x), std::atan2(y, x));
+    w_atan2 = std::max(w_atan2, da);
+    diff_atan2 += da != 0;
+    w_hypot = std::max(w_hypot, ulp_diff(pm_hypotf(x, y), std::hypot(x, y)));
+  }
+  std::printf("  max ulp vs glibc over %d samples: exp %lld (differs %lld), exp_blend %lld, sin %lld, cos %lld, "
+              "atan2 %lld (differs %lld), hypot %lld\n",
+              n, (long long)w_exp, (long long)diff_exp, (long long)w_blend, (long long)w_sin, (long long)w_cos,
+              (long long)w_atan2, (long long)diff_atan2, (long long)w_hypot);
+  CHECK(w_exp <= 1);
+  CHECK(w_blend <= 2);
+  CHECK(w_sin <= 1);
+  CHECK(w_cos <= 1);
+  CHECK(w_atan2 <= 1);
+  CHECK(w_hypot <= 1);
+  // Special values.
+  CHECK(pm_atan2f(0.0f, -1.0f) == std::atan2(0.0f, -1.0f));
+  CHECK(pm_atan2f(-0.0f, -1.0f) == std::atan2(-0.0f, -1.0f));
+  CHECK(pm_atan2f(1.0f, 0.0f) == std::atan2(1.0f, 0.0f));
+  CHECK(pm_atan2f(0.0f, 0.0f) == 0.0f);
+  CHECK(pm_expf(0.0f) == 1.0f);
+  CHECK(pm_expf_blend(0.0f) == 1.0f);
+  CHECK(pm_expf_blend(-100.0f) == 0.0f);
+  CHECK(pm_cosf(0.0f) == 1.0f);
+  CHECK(pm_sinf(0.0f) == 0.0f);
+}
+
+TEST_CASE("portable oracle: float images agree with the libm oracle, walks nearly always") {
+  std::mt19937 rng(77);
+  Settings<float> settings;
+  int64_t walked_diff = 0, pixels = 0;
+  double worst = 0;
+  for (int scene = 0; scene < 3; ++scene) {
+    const auto cloud = random_cloud<float>(rng, 2000);
+    auto cam = identity_camera<float>(512, 256);
+    const auto a = render<float, StdMath>(cloud, cam, settings);
+    const auto b = render<float, PortableMath>(cloud, cam, settings);
+    worst = std::max(worst, image_max_abs_diff(a.image, b.image));
+    for (std::size_t p = 0; p < a.walked.size(); ++p) walked_diff += a.walked[p] != b.walked[p];
+    pixels += (int64_t)a.walked.size();
+    CHECK(a.tile_offsets.size() == b.tile_offsets.size());
+  }
+  std::printf("  Std vs Portable float: image max diff %.2e, walked differs on %lld / %lld pixels\n", worst,
+              (long long)walked_diff, (long long)pixels);
+  CHECK(worst <= 1e-4);
+  CHECK(walked_diff * 1000 <= pixels);
+}
+
+int main(int argc, char** argv) {
+  const char* filter = argc > 1 ? argv[1] : nullptr;
+  int run = 0;
+  for (auto& [name, fn] : Registry::get().tests) {
+    if (filter && name.find(filter) == std::string::npos) continue;
+    g_current = name;
+    const int before = g_failures;
+    std::printf("[ RUN  ] %s\n", name.c_str());
+    std::fflush(stdout);
+    try {
+      fn();
+    } catch (const std::exception& e) {
+      ++g_failures;
+      std::printf("  FAIL [%s] unexpected exception: %s\n", name.c_str(), e.what());
+    }
+    std::printf("[ %s ] %s\n", g_failures == before ? " OK " : "FAIL", name.c_str());
+    ++run;
+  }
+  std::printf("%d test cases, %d checks, %d failures\n", run, g_checks, g_failures);
+  return g_failures == 0 ? 0 : 1;
+}
