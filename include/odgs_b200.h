@@ -1,0 +1,191 @@
+/*
+ * odgs_b200.h — C ABI of the B200-native ODGS rasterizer (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's rasterizer API
+ * (reference tree proj/include/odgs/). Each entry point names the reference
+ * function it replaces. Plain pointers and sizes only; no C++ or torch types.
+ *
+ * Data layouts are the reference's own (Eigen column-major storage), so an Eigen
+ * caller can pass .data() directly:
+ *   cloud members  SoA: means[c*n + i] (MatX3), rotations (w,x,y,z) [4][n], log_scales
+ *                  [3][n], raw_opacities [n], colors [3][n]   (types.hpp:53-143)
+ *   images         planar channels, each H x W column-major: img[c*W*H + x*H + y]
+ *                  (ErpImage, types.hpp:184-224)
+ *   per-pixel maps transmittance/walked [x*H + y]               (rasterizer.hpp:95-96)
+ * Camera rotation is passed row-major here (the C++ wrapper transposes Eigen's
+ * column-major Mat3).
+ *
+ * Errors mirror the reference's exceptions (see odgs_status); the failing Gaussian
+ * index and message are available from odgs_last_error(). Calls on one context are
+ * ordered on that context's CUDA stream; use one context per host thread.
+ */
+#ifndef ODGS_B200_H
+#define ODGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ODGS_ABI_VERSION 1
+
+typedef enum {
+  ODGS_OK = 0,
+  /* std::invalid_argument: bad camera (types.hpp:160-168), near-zero quaternion
+     (covariance.hpp:14-15), bad settings/arguments. */
+  ODGS_ERR_INVALID_ARGUMENT = 1,
+  /* std::runtime_error: non-finite parameter (rasterizer.hpp:134-136) or non-finite
+     gradient (backward.hpp:440-446); index = first offending Gaussian. */
+  ODGS_ERR_RUNTIME = 2,
+  /* std::domain_error: derivative undefined on the pole axis (backward.hpp:79-80,
+     projection.hpp:123-124) or zero-length direction (projection.hpp:23-24). */
+  ODGS_ERR_DOMAIN = 3,
+  ODGS_ERR_CUDA = 4,
+  ODGS_ERR_OUT_OF_MEMORY = 5
+} odgs_status;
+
+typedef enum { ODGS_MEM_HOST = 0, ODGS_MEM_DEVICE = 1 } odgs_memory;
+
+/* RenderSettings (types.hpp:229-255). `threads` is accepted and ignored on the GPU. */
+typedef struct {
+  float near_radius;
+  float far_radius;
+  int32_t tile_size;
+  float alpha_clamp;
+  float transmittance_floor;
+  float cutoff_sigma;
+  float lowpass_dilation;
+  float max_elevation;
+  int32_t threads;
+} odgs_settings;
+
+/* CameraPose (types.hpp:148-180): p_cam = R p_world + t, y-down, z-forward. */
+typedef struct {
+  float rotation[9]; /* row-major */
+  float translation[3];
+  int32_t width;
+  int32_t height;
+} odgs_camera;
+
+/* GaussianCloud<float> (types.hpp:53-143). All five arrays live in `memory`. */
+typedef struct {
+  int64_t n;
+  const float* means;
+  const float* rotations;
+  const float* log_scales;
+  const float* raw_opacities;
+  const float* colors;
+  int32_t memory;
+} odgs_cloud;
+
+/* GradBuffers<float> (backward.hpp:342-374), same SoA layout as the cloud. */
+typedef struct {
+  float* means;
+  float* rotations;
+  float* log_scales;
+  float* raw_opacities;
+  float* colors;
+  float* pixel_grad_norm;
+  float* one_minus_cos;
+  int32_t* observed;
+  int32_t memory;
+} odgs_grads;
+
+typedef struct odgs_ctx odgs_ctx;
+typedef struct odgs_frame odgs_frame;
+
+typedef struct {
+  int32_t width, height, tiles_x, tiles_y;
+  int64_t n_gaussians; /* cloud size */
+  int64_t n_splats;    /* projected (RenderOutput::splats.size()) */
+  int64_t n_instances; /* seam instances (RenderOutput::instances.size()) */
+  int64_t n_entries;   /* tile entries (RenderOutput::tile_entries.size()) */
+} odgs_frame_info;
+
+/* Fields of a rendered frame (RenderOutput, rasterizer.hpp:92-102). */
+typedef enum {
+  ODGS_FRAME_IMAGE = 0,          /* float [3][W][H]                                        */
+  ODGS_FRAME_TRANSMITTANCE = 1,  /* float [W][H]                                           */
+  ODGS_FRAME_WALKED = 2,         /* int32 [W][H] entries examined, exclusive               */
+  ODGS_FRAME_TILE_OFFSETS = 3,   /* int32 [tiles+1]                                        */
+  ODGS_FRAME_TILE_ENTRIES = 4,   /* int32 [n_entries] instance ids, per tile, global order */
+  ODGS_FRAME_INSTANCE_SPLAT = 5, /* int32 [n_instances] splat ids, sorted (depth,index,shift) */
+  ODGS_FRAME_INSTANCE_SHIFT = 6, /* float [n_instances] -W, 0 or +W                        */
+  ODGS_FRAME_SPLAT_INDEX = 7,    /* int64 [n_splats] cloud row, ascending                  */
+  ODGS_FRAME_SPLAT_MEAN = 8,     /* float [n_splats][2]                                    */
+  ODGS_FRAME_SPLAT_COV2D = 9,    /* float [n_splats][4] row-major (needs ODGS_FRAME_KEEP_COV2D) */
+  ODGS_FRAME_SPLAT_INV = 10,     /* float [n_splats][4] row-major                          */
+  ODGS_FRAME_SPLAT_DEPTH = 11,   /* float [n_splats]                                       */
+  ODGS_FRAME_SPLAT_RADIUS = 12,  /* float [n_splats]                                       */
+  ODGS_FRAME_SPLAT_OPACITY = 13, /* float [n_splats]                                       */
+  ODGS_FRAME_SPLAT_COLOR = 14,   /* float [n_splats][3]                                    */
+  ODGS_FRAME_SPLAT_CLAMPED = 15, /* int32 [n_splats] pole clamp engaged                    */
+  /* SplatGrads (backward.hpp:19-25) of the last odgs_backward on this frame: */
+  ODGS_FRAME_SPLATGRAD_MEAN = 16,    /* float [n_splats][2]                                */
+  ODGS_FRAME_SPLATGRAD_COV2D = 17,   /* float [n_splats][4] full-matrix convention          */
+  ODGS_FRAME_SPLATGRAD_OPACITY = 18, /* float [n_splats] w.r.t. activated opacity           */
+  ODGS_FRAME_SPLATGRAD_COLOR = 19,   /* float [n_splats][3]                                */
+  ODGS_FRAME_FIELD_COUNT = 20
+} odgs_frame_field;
+
+/* odgs_frame_set_flags */
+#define ODGS_FRAME_KEEP_COV2D 0x1u /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
+
+/* odgs_backward flags */
+#define ODGS_ACCUMULATE 0x1u /* add into the gradient buffers (GradBuffers::accumulate) */
+
+/* ------------------------------------------------------------------ context */
+odgs_settings odgs_default_settings(void);
+int odgs_abi_version(void);
+
+/* Creates a context on `device`. stream: a cudaStream_t, or NULL for a private one. */
+odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out);
+void odgs_ctx_destroy(odgs_ctx* ctx);
+odgs_status odgs_ctx_set_stream(odgs_ctx* ctx, void* stream);
+void* odgs_ctx_stream(odgs_ctx* ctx);
+odgs_status odgs_synchronize(odgs_ctx* ctx);
+/* Code of the last failed call on ctx; *gaussian_index = offending row or -1. */
+odgs_status odgs_last_error(const odgs_ctx* ctx, int64_t* gaussian_index, char* message, size_t message_len);
+/* Number of kernels this context has launched since creation. */
+int64_t odgs_ctx_launch_count(const odgs_ctx* ctx);
+
+/* ------------------------------------------------------------------ frames */
+odgs_status odgs_frame_create(odgs_ctx* ctx, odgs_frame** out);
+void odgs_frame_destroy(odgs_frame* frame);
+odgs_status odgs_frame_set_flags(odgs_frame* frame, uint32_t flags);
+odgs_status odgs_frame_get_info(const odgs_frame* frame, odgs_frame_info* info);
+/* Copies a field to host memory (bytes must be >= the field's size). Synchronizes. */
+odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, void* host_dst, size_t bytes);
+/* Device pointer of a resident field (IMAGE, TRANSMITTANCE, WALKED, TILE_OFFSETS). */
+odgs_status odgs_frame_device_ptr(odgs_frame* frame, int field, void** device_ptr);
+
+/* ------------------------------------------------------------------ hot path */
+/* prepare_render (rasterizer.hpp:129-207): validate, project, seam-duplicate, sort,
+   bin. Returns after the device has finished projection (errors are reported
+   synchronously, as the reference throws); the rest is enqueued on the stream. */
+odgs_status odgs_prepare_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                                const odgs_settings* settings, odgs_frame* frame);
+
+/* render (rasterizer.hpp:211-267): prepare_render + front-to-back tile blending. */
+odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                        const odgs_settings* settings, odgs_frame* frame);
+
+/* backward (backward.hpp:380-448) incl. grad_pixels_to_splats (:208-339) for the view
+   rendered into `frame` (same cloud, camera, settings — unchecked, as in the
+   reference). dl_dimage: [3][W][H] in dl_memory. grad_t_signs: NULL or 12 signs
+   (GradTSigns, backward.hpp:32-34). flags: ODGS_ACCUMULATE. */
+odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, odgs_frame* frame,
+                          const float* dl_dimage, int32_t dl_memory, const odgs_settings* settings,
+                          const odgs_grads* grads, const double* grad_t_signs, uint32_t flags);
+
+/* cull (rasterizer.hpp:15-28): host output of the kept rows, ascending. */
+odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, float near_radius,
+                      float far_radius, int64_t* out_indices, int64_t* out_count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ODGS_B200_H */

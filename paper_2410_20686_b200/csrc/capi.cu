@@ -1,0 +1,852 @@
+// capi.cu — the C ABI (include/odgs_b200.h): contexts, frames, and the host-side
+// orchestration of the forward and backward kernels on one CUDA stream.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "odgs_b200.h"
+
+using namespace odgs_b200;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace
+
+struct odgs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  odgs_status last_code = ODGS_OK;
+  int64_t last_index = -1;
+  std::string last_msg;
+  DevErrors* d_err = nullptr;
+  DevErrors* h_err = nullptr;       // pinned readback
+  DevErrors* h_err_init = nullptr;  // pinned reset template
+  uint32_t* h_scratch = nullptr;    // pinned
+  DevBuf cloud_buf, dl_buf, grads_buf, signs_buf, cull_buf;
+  float* d_unit_signs = nullptr;
+  int64_t launches = 0;
+};
+
+struct odgs_frame {
+  odgs_ctx* ctx = nullptr;
+  uint32_t flags = 0;
+  int width = 0, height = 0, tile_size = 16, tiles_x = 0, tiles_y = 0;
+  int64_t n = 0;
+  uint32_t n_entries = 0;
+  int64_t n_splats = 0, n_instances = 0;
+  bool prepared = false, rendered = false, have_splat_grads = false;
+  DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
+  DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, splat_grads;
+  int depth_which = 0, tile_which = 0;
+  DevCamera cam{};
+  DevSettings settings{};
+};
+
+namespace {
+
+struct LaunchScope {
+  odgs_ctx* ctx;
+  int64_t start;
+  explicit LaunchScope(odgs_ctx* c) : ctx(c), start(g_launches) {}
+  ~LaunchScope() {
+    if (ctx) ctx->launches += g_launches - start;
+  }
+};
+
+odgs_status set_error(odgs_ctx* ctx, odgs_status code, int64_t index, const std::string& msg) {
+  if (ctx) {
+    ctx->last_code = code;
+    ctx->last_index = index;
+    ctx->last_msg = msg;
+  }
+  return code;
+}
+
+odgs_status ok(odgs_ctx* ctx) {
+  if (ctx) {
+    ctx->last_code = ODGS_OK;
+    ctx->last_index = -1;
+    ctx->last_msg.clear();
+  }
+  return ODGS_OK;
+}
+
+odgs_status cuda_fail(odgs_ctx* ctx, cudaError_t e, const char* where) {
+  return set_error(ctx, e == cudaErrorMemoryAllocation ? ODGS_ERR_OUT_OF_MEMORY : ODGS_ERR_CUDA, -1,
+                   std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define ODGS_CUDA(ctx, expr)                                  \
+  do {                                                        \
+    cudaError_t e_ = (expr);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #expr);  \
+  } while (0)
+
+cudaError_t ensure(DevBuf& b, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  if (b.cap >= bytes) return cudaSuccess;
+  if (b.p) {
+    cudaError_t e = cudaFreeAsync(b.p, s);
+    if (e != cudaSuccess) return e;
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  const size_t nb = ((bytes + bytes / 4) + 255) / 256 * 256;
+  cudaError_t e = cudaMallocAsync(&b.p, nb, s);
+  if (e != cudaSuccess) return e;
+  b.cap = nb;
+  return cudaSuccess;
+}
+
+void release(DevBuf& b, cudaStream_t s) {
+  if (b.p) cudaFreeAsync(b.p, s);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+int bits_for(uint32_t n_tiles) {
+  int b = 0;
+  while (b < 32 && (1ull << b) < (unsigned long long)n_tiles) ++b;
+  return b;
+}
+
+// Host-side argument checks that the reference performs before any work.
+odgs_status check_settings(odgs_ctx* ctx, const odgs_settings* s) {
+  if (!s) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "settings: null");
+  if (s->tile_size <= 0)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "RenderSettings: tile_size must be positive");
+  if (s->tile_size > 64)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "RenderSettings: tile_size > 64 is not supported on the GPU");
+  return ODGS_OK;
+}
+
+// CameraPose::validate (types.hpp:159-169), evaluated in float like the reference.
+odgs_status check_camera(odgs_ctx* ctx, const odgs_camera* c) {
+  if (!c) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "camera: null");
+  if (c->width <= 0 || c->height <= 0 || c->width != 2 * c->height)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1,
+                     "CameraPose: equirectangular image needs width == 2 * height > 0");
+  float err = 0.0f;
+  const float* R = c->rotation;
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) {
+      const float v = sum3(R[3 * r] * R[3 * k], R[3 * r + 1] * R[3 * k + 1], R[3 * r + 2] * R[3 * k + 2]);
+      err = std::max(err, std::fabs(v - (r == k ? 1.0f : 0.0f)));
+    }
+  if (!(err < 1e-5f)) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "CameraPose: rotation is not orthonormal");
+  if ((int64_t)c->width * c->height > (int64_t)1 << 31)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "CameraPose: image too large");
+  return ODGS_OK;
+}
+
+DevCamera to_dev(const odgs_camera& c) {
+  DevCamera d;
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) d.R[r][k] = c.rotation[3 * r + k];
+  for (int k = 0; k < 3; ++k) d.t[k] = c.translation[k];
+  d.width = c.width;
+  d.height = c.height;
+  return d;
+}
+
+DevSettings to_dev(const odgs_settings& s) {
+  DevSettings d;
+  d.near_radius = s.near_radius;
+  d.far_radius = s.far_radius;
+  d.tile_size = s.tile_size;
+  d.alpha_clamp = s.alpha_clamp;
+  d.transmittance_floor = s.transmittance_floor;
+  d.cutoff_sigma = s.cutoff_sigma;
+  d.lowpass_dilation = s.lowpass_dilation;
+  d.max_elevation = s.max_elevation;
+  return d;
+}
+
+// Resolves the cloud to device pointers, copying host arrays into the context.
+struct CloudPtrs {
+  const float *means, *rotations, *log_scales, *raw_opacities, *colors;
+};
+
+odgs_status resolve_cloud(odgs_ctx* ctx, const odgs_cloud* c, CloudPtrs* out) {
+  if (!c) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cloud: null");
+  if (c->n < 0 || c->n >= ((int64_t)1 << 30))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cloud: size must be in [0, 2^30)");
+  if (c->memory == ODGS_MEM_DEVICE || c->n == 0) {
+    *out = {c->means, c->rotations, c->log_scales, c->raw_opacities, c->colors};
+    return ODGS_OK;
+  }
+  const int64_t n = c->n;
+  ODGS_CUDA(ctx, ensure(ctx->cloud_buf, sizeof(float) * 14 * n, ctx->stream));
+  float* b = ctx->cloud_buf.as<float>();
+  float* dst[5] = {b, b + 3 * n, b + 7 * n, b + 10 * n, b + 11 * n};
+  const float* src[5] = {c->means, c->rotations, c->log_scales, c->raw_opacities, c->colors};
+  const int64_t width[5] = {3, 4, 3, 1, 3};
+  for (int k = 0; k < 5; ++k)
+    ODGS_CUDA(ctx, cudaMemcpyAsync(dst[k], src[k], sizeof(float) * width[k] * n, cudaMemcpyHostToDevice, ctx->stream));
+  *out = {dst[0], dst[1], dst[2], dst[3], dst[4]};
+  return ODGS_OK;
+}
+
+// Reads the device error words (synchronizing the stream).
+odgs_status read_errors(odgs_ctx* ctx) {
+  ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(DevErrors), cudaMemcpyDeviceToHost, ctx->stream));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return ODGS_OK;
+}
+
+odgs_status reset_errors(odgs_ctx* ctx) {
+  ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->d_err, ctx->h_err_init, sizeof(DevErrors), cudaMemcpyHostToDevice, ctx->stream));
+  return ODGS_OK;
+}
+
+odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                         const odgs_settings* settings, odgs_frame* f) {
+  if (!ctx || !f) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "null context or frame");
+  odgs_status st;
+  if ((st = check_camera(ctx, camera)) != ODGS_OK) return st;
+  if ((st = check_settings(ctx, settings)) != ODGS_OK) return st;
+  CloudPtrs cp;
+  if ((st = resolve_cloud(ctx, cloud, &cp)) != ODGS_OK) return st;
+  cudaStream_t s = ctx->stream;
+  f->prepared = f->rendered = f->have_splat_grads = false;
+  f->width = camera->width;
+  f->height = camera->height;
+  f->tile_size = settings->tile_size;
+  f->tiles_x = (f->width + f->tile_size - 1) / f->tile_size;
+  f->tiles_y = (f->height + f->tile_size - 1) / f->tile_size;
+  f->n = cloud->n;
+  f->cam = to_dev(*camera);
+  f->settings = to_dev(*settings);
+  const int64_t n = f->n;
+  const uint32_t n_tiles = (uint32_t)(f->tiles_x * f->tiles_y);
+
+  ODGS_CUDA(ctx, ensure(f->sp_ab, sizeof(float4) * 2 * n, s));
+  ODGS_CUDA(ctx, ensure(f->sp_c, sizeof(float4) * n, s));
+  if (f->flags & ODGS_FRAME_KEEP_COV2D) ODGS_CUDA(ctx, ensure(f->cov, sizeof(float4) * n, s));
+  for (int k = 0; k < 2; ++k) {
+    ODGS_CUDA(ctx, ensure(f->keys[k], sizeof(uint32_t) * n, s));
+    ODGS_CUDA(ctx, ensure(f->vals[k], sizeof(uint32_t) * n, s));
+  }
+  ODGS_CUDA(ctx, ensure(f->cnt, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->cnt_sorted, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->off_sorted, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->ent_off_idx, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->scan_tmp, scan_temp_bytes(n) + 256, s));
+  ODGS_CUDA(ctx, ensure(f->offsets, sizeof(int32_t) * (n_tiles + 1), s));
+  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+
+  PreprocessArgs pa;
+  pa.n = n;
+  pa.means = cp.means;
+  pa.rotations = cp.rotations;
+  pa.log_scales = cp.log_scales;
+  pa.raw_opacities = cp.raw_opacities;
+  pa.colors = cp.colors;
+  pa.cam = f->cam;
+  pa.settings = f->settings;
+  pa.sp_ab = f->sp_ab.as<float4>();
+  pa.sp_c = f->sp_c.as<float4>();
+  pa.cov_out = (f->flags & ODGS_FRAME_KEEP_COV2D) ? f->cov.as<float4>() : nullptr;
+  pa.keys = f->keys[0].as<uint32_t>();
+  pa.vals = f->vals[0].as<uint32_t>();
+  pa.cnt = f->cnt.as<uint32_t>();
+  pa.err = ctx->d_err;
+  launch_preprocess(pa, s);
+
+  // Depth sort of the Gaussians (key: depth bits; culled sort last).
+  ODGS_CUDA(ctx, ensure(f->sort_tmp, std::max(radix_sort_temp_bytes(n), (size_t)16), s));
+  uint32_t* dk[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
+  uint32_t* dv[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
+  radix_sort_pairs(dk, dv, n, 0, 32, f->sort_tmp.p, &f->depth_which, s);
+  const uint32_t* sorted_idx = dv[f->depth_which];
+  launch_gather_counts(n, sorted_idx, f->cnt.as<uint32_t>(), f->cnt_sorted.as<uint32_t>(), s);
+  exclusive_scan_u32(f->cnt_sorted.as<uint32_t>(), f->off_sorted.as<uint32_t>(), n, f->scan_tmp.p,
+                     &ctx->d_err->n_entries, s);
+  if ((st = read_errors(ctx)) != ODGS_OK) return st;
+  const DevErrors& he = *ctx->h_err;
+  if (he.nonfinite != kNoError) {
+    const int64_t idx = (int64_t)(he.nonfinite >> 4);
+    return set_error(ctx, ODGS_ERR_RUNTIME, idx, "render: non-finite parameter in Gaussian " + std::to_string(idx));
+  }
+  if (he.project != kNoError) {
+    const int64_t idx = (int64_t)(he.project >> 4);
+    const int code = (int)(he.project & 15);
+    if (code == 3)
+      return set_error(ctx, ODGS_ERR_DOMAIN, idx, "to_spherical: degenerate zero-length direction");
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "normalize_quaternion: near-zero quaternion");
+  }
+  const unsigned long long total = n > 0 ? he.n_entries : 0ull;
+  if (total >= (1ull << 31))
+    return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: more than 2^31 tile entries");
+  f->n_entries = (uint32_t)total;
+  f->n_splats = n > 0 ? (int64_t)he.n_visible : 0;
+  f->n_instances = n > 0 ? (int64_t)he.n_instances : 0;
+  const uint32_t K = f->n_entries;
+
+  for (int k = 0; k < 2; ++k) {
+    ODGS_CUDA(ctx, ensure(f->ekeys[k], sizeof(uint32_t) * K, s));
+    ODGS_CUDA(ctx, ensure(f->evals[k], sizeof(uint32_t) * K, s));
+  }
+  EmitArgs ea;
+  ea.n = n;
+  ea.sorted_idx = sorted_idx;
+  ea.cnt_sorted = f->cnt_sorted.as<uint32_t>();
+  ea.off_sorted = f->off_sorted.as<uint32_t>();
+  ea.sp_ab = f->sp_ab.as<float4>();
+  ea.sp_c = f->sp_c.as<float4>();
+  ea.width = f->width;
+  ea.height = f->height;
+  ea.tile_size = f->tile_size;
+  ea.tiles_x = f->tiles_x;
+  ea.out_keys = f->ekeys[0].as<uint32_t>();
+  ea.out_vals = f->evals[0].as<uint32_t>();
+  ea.ent_off_idx = f->ent_off_idx.as<uint32_t>();
+  launch_emit(ea, s);
+
+  ODGS_CUDA(ctx, ensure(f->sort_tmp, std::max(radix_sort_temp_bytes(K), radix_sort_temp_bytes(n)), s));
+  uint32_t* ek[2] = {f->ekeys[0].as<uint32_t>(), f->ekeys[1].as<uint32_t>()};
+  uint32_t* ev[2] = {f->evals[0].as<uint32_t>(), f->evals[1].as<uint32_t>()};
+  radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s);
+  launch_tile_ranges(K, ek[f->tile_which], n_tiles, f->offsets.as<int32_t>(), s);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  f->prepared = true;
+  return ok(ctx);
+}
+
+odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
+  cudaStream_t s = ctx->stream;
+  const int64_t px = (int64_t)f->width * f->height;
+  ODGS_CUDA(ctx, ensure(f->image, sizeof(float) * 3 * px, s));
+  ODGS_CUDA(ctx, ensure(f->trans, sizeof(float) * px, s));
+  ODGS_CUDA(ctx, ensure(f->walked, sizeof(int32_t) * px, s));
+  BlendArgs ba;
+  ba.offsets = f->offsets.as<int32_t>();
+  ba.vals = f->evals[f->tile_which].as<uint32_t>();
+  ba.sp_ab = f->sp_ab.as<float4>();
+  ba.sp_c = f->sp_c.as<float4>();
+  ba.width = f->width;
+  ba.height = f->height;
+  ba.tile_size = f->tile_size;
+  ba.tiles_x = f->tiles_x;
+  ba.tiles_y = f->tiles_y;
+  ba.alpha_clamp = f->settings.alpha_clamp;
+  ba.transmittance_floor = f->settings.transmittance_floor;
+  ba.cutoff_sigma = f->settings.cutoff_sigma;
+  ba.image = f->image.as<float>();
+  ba.transmittance = f->trans.as<float>();
+  ba.walked = f->walked.as<int32_t>();
+  launch_blend(ba, s);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  f->rendered = true;
+  return ok(ctx);
+}
+
+size_t field_elem_bytes(int field) {
+  switch (field) {
+    case ODGS_FRAME_SPLAT_INDEX: return 8;
+    default: return 4;
+  }
+}
+
+// Splat-order (visible Gaussians ascending) host views of per-Gaussian device data.
+struct HostViews {
+  std::vector<float4> ab, c;
+  std::vector<int64_t> splat_of;  // Gaussian -> splat position or -1
+  std::vector<int64_t> visible;   // splat position -> Gaussian
+};
+
+odgs_status load_views(odgs_ctx* ctx, odgs_frame* f, HostViews* v) {
+  const int64_t n = f->n;
+  v->ab.resize(2 * n);
+  v->c.resize(n);
+  if (n > 0) {
+    ODGS_CUDA(ctx, cudaMemcpyAsync(v->ab.data(), f->sp_ab.p, sizeof(float4) * 2 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(v->c.data(), f->sp_c.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  v->splat_of.assign(n, -1);
+  v->visible.clear();
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t fl;
+    std::memcpy(&fl, &v->c[i].w, 4);
+    if (fl & kFlagVisible) {
+      v->splat_of[i] = (int64_t)v->visible.size();
+      v->visible.push_back(i);
+    }
+  }
+  return ODGS_OK;
+}
+
+uint32_t flags_of(const float4& c) {
+  uint32_t fl;
+  std::memcpy(&fl, &c.w, 4);
+  return fl;
+}
+
+}  // namespace
+
+extern "C" {
+
+odgs_settings odgs_default_settings(void) {
+  odgs_settings s;
+  s.near_radius = 0.01f;
+  s.far_radius = 1000.0f;
+  s.tile_size = 16;
+  s.alpha_clamp = 0.99f;
+  s.transmittance_floor = 1e-4f;
+  s.cutoff_sigma = 3.0f;
+  s.lowpass_dilation = 0.3f;
+  s.max_elevation = 85.0f * kPiF / 180.0f;
+  s.threads = 0;
+  return s;
+}
+
+int odgs_abi_version(void) { return ODGS_ABI_VERSION; }
+
+odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out) {
+  if (!out) return ODGS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  odgs_ctx* ctx = new (std::nothrow) odgs_ctx();
+  if (!ctx) return ODGS_ERR_OUT_OF_MEMORY;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) {
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+      ctx->own_stream = true;
+    }
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_err, sizeof(DevErrors));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err, sizeof(DevErrors));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_err_init, sizeof(DevErrors));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_scratch, 256);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_unit_signs, 12 * sizeof(float));
+  if (e == cudaSuccess) {
+    const float ones[12] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+    e = cudaMemcpy(ctx->d_unit_signs, ones, sizeof ones, cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    odgs_ctx_destroy(ctx);
+    return e == cudaErrorMemoryAllocation ? ODGS_ERR_OUT_OF_MEMORY : ODGS_ERR_CUDA;
+  }
+  ctx->h_err_init->nonfinite = kNoError;
+  ctx->h_err_init->project = kNoError;
+  ctx->h_err_init->bwd_domain = kNoError;
+  ctx->h_err_init->bwd_nonfinite = kNoError;
+  ctx->h_err_init->n_entries = 0;
+  ctx->h_err_init->n_visible = 0;
+  ctx->h_err_init->n_instances = 0;
+  *out = ctx;
+  return ODGS_OK;
+}
+
+void odgs_ctx_destroy(odgs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) {
+    release(ctx->cloud_buf, ctx->stream);
+    release(ctx->dl_buf, ctx->stream);
+    release(ctx->grads_buf, ctx->stream);
+    release(ctx->signs_buf, ctx->stream);
+    release(ctx->cull_buf, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+  }
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->d_unit_signs) cudaFree(ctx->d_unit_signs);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->h_err_init) cudaFreeHost(ctx->h_err_init);
+  if (ctx->h_scratch) cudaFreeHost(ctx->h_scratch);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+odgs_status odgs_ctx_set_stream(odgs_ctx* ctx, void* stream) {
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->own_stream = false;
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  return ok(ctx);
+}
+
+void* odgs_ctx_stream(odgs_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+odgs_status odgs_synchronize(odgs_ctx* ctx) {
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return ok(ctx);
+}
+
+odgs_status odgs_last_error(const odgs_ctx* ctx, int64_t* gaussian_index, char* message, size_t message_len) {
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  if (gaussian_index) *gaussian_index = ctx->last_index;
+  if (message && message_len > 0) std::snprintf(message, message_len, "%s", ctx->last_msg.c_str());
+  return ctx->last_code;
+}
+
+int64_t odgs_ctx_launch_count(const odgs_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+odgs_status odgs_frame_create(odgs_ctx* ctx, odgs_frame** out) {
+  if (!ctx || !out) return ODGS_ERR_INVALID_ARGUMENT;
+  odgs_frame* f = new (std::nothrow) odgs_frame();
+  if (!f) return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "frame allocation");
+  f->ctx = ctx;
+  *out = f;
+  return ok(ctx);
+}
+
+void odgs_frame_destroy(odgs_frame* f) {
+  if (!f) return;
+  cudaStream_t s = f->ctx->stream;
+  DevBuf* bufs[] = {&f->sp_ab, &f->sp_c, &f->cov, &f->keys[0], &f->keys[1], &f->vals[0], &f->vals[1], &f->cnt,
+                    &f->cnt_sorted, &f->off_sorted, &f->ent_off_idx, &f->sort_tmp, &f->scan_tmp, &f->ekeys[0],
+                    &f->ekeys[1], &f->evals[0], &f->evals[1], &f->offsets, &f->image, &f->trans, &f->walked,
+                    &f->records, &f->splat_grads};
+  for (DevBuf* b : bufs) release(*b, s);
+  cudaStreamSynchronize(s);
+  delete f;
+}
+
+odgs_status odgs_frame_set_flags(odgs_frame* f, uint32_t flags) {
+  if (!f) return ODGS_ERR_INVALID_ARGUMENT;
+  f->flags = flags;
+  return ODGS_OK;
+}
+
+odgs_status odgs_frame_get_info(const odgs_frame* f, odgs_frame_info* info) {
+  if (!f || !info) return ODGS_ERR_INVALID_ARGUMENT;
+  info->width = f->width;
+  info->height = f->height;
+  info->tiles_x = f->tiles_x;
+  info->tiles_y = f->tiles_y;
+  info->n_gaussians = f->n;
+  info->n_entries = f->n_entries;
+  info->n_splats = f->n_splats;
+  info->n_instances = f->n_instances;
+  return ODGS_OK;
+}
+
+odgs_status odgs_prepare_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                                const odgs_settings* settings, odgs_frame* frame) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  return prepare_impl(ctx, cloud, camera, settings, frame);
+}
+
+odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                        const odgs_settings* settings, odgs_frame* frame) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  odgs_status st = prepare_impl(ctx, cloud, camera, settings, frame);
+  if (st != ODGS_OK) return st;
+  return blend_impl(ctx, frame);
+}
+
+odgs_status odgs_frame_device_ptr(odgs_frame* f, int field, void** device_ptr) {
+  if (!f || !device_ptr || !f->prepared) return ODGS_ERR_INVALID_ARGUMENT;
+  switch (field) {
+    case ODGS_FRAME_IMAGE: *device_ptr = f->rendered ? f->image.p : nullptr; break;
+    case ODGS_FRAME_TRANSMITTANCE: *device_ptr = f->rendered ? f->trans.p : nullptr; break;
+    case ODGS_FRAME_WALKED: *device_ptr = f->rendered ? f->walked.p : nullptr; break;
+    case ODGS_FRAME_TILE_OFFSETS: *device_ptr = f->offsets.p; break;
+    default: return ODGS_ERR_INVALID_ARGUMENT;
+  }
+  return *device_ptr ? ODGS_OK : ODGS_ERR_INVALID_ARGUMENT;
+}
+
+odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* f, int field, void* host_dst, size_t bytes) {
+  if (!ctx || !f || !f->prepared) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not prepared");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = ctx->stream;
+  const int64_t px = (int64_t)f->width * f->height;
+  const int64_t n_tiles = (int64_t)f->tiles_x * f->tiles_y;
+  auto need = [&](size_t want) -> odgs_status {
+    if (bytes < want) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "download: buffer too small");
+    return ODGS_OK;
+  };
+  odgs_status st;
+  auto copy_dev = [&](const void* src, size_t sz) -> odgs_status {
+    if ((st = need(sz)) != ODGS_OK) return st;
+    if (sz) ODGS_CUDA(ctx, cudaMemcpyAsync(host_dst, src, sz, cudaMemcpyDeviceToHost, s));
+    ODGS_CUDA(ctx, cudaStreamSynchronize(s));
+    return ok(ctx);
+  };
+  if ((field == ODGS_FRAME_IMAGE || field == ODGS_FRAME_TRANSMITTANCE || field == ODGS_FRAME_WALKED) && !f->rendered)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not rendered");
+  switch (field) {
+    case ODGS_FRAME_IMAGE: return copy_dev(f->image.p, sizeof(float) * 3 * px);
+    case ODGS_FRAME_TRANSMITTANCE: return copy_dev(f->trans.p, sizeof(float) * px);
+    case ODGS_FRAME_WALKED: return copy_dev(f->walked.p, sizeof(int32_t) * px);
+    case ODGS_FRAME_TILE_OFFSETS: return copy_dev(f->offsets.p, sizeof(int32_t) * (n_tiles + 1));
+    default: break;
+  }
+  if (field < 0 || field >= ODGS_FRAME_FIELD_COUNT) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "bad field");
+  if (field == ODGS_FRAME_SPLAT_COV2D && !(f->flags & ODGS_FRAME_KEEP_COV2D))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "SPLAT_COV2D needs ODGS_FRAME_KEEP_COV2D");
+  if (field >= ODGS_FRAME_SPLATGRAD_MEAN && !f->have_splat_grads)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "no backward on this frame");
+
+  // Reference-format views, materialised on the host from the device arrays.
+  HostViews v;
+  if ((st = load_views(ctx, f, &v)) != ODGS_OK) return st;
+  const int64_t ns = (int64_t)v.visible.size();
+  if (field >= ODGS_FRAME_SPLAT_INDEX && field <= ODGS_FRAME_SPLAT_CLAMPED) {
+    const int width = (field == ODGS_FRAME_SPLAT_MEAN) ? 2
+                      : (field == ODGS_FRAME_SPLAT_COV2D || field == ODGS_FRAME_SPLAT_INV) ? 4
+                      : (field == ODGS_FRAME_SPLAT_COLOR) ? 3 : 1;
+    if ((st = need(field_elem_bytes(field) * width * ns)) != ODGS_OK) return st;
+    std::vector<float4> cov;
+    if (field == ODGS_FRAME_SPLAT_COV2D) {
+      cov.resize(f->n);
+      if (f->n) ODGS_CUDA(ctx, cudaMemcpy(cov.data(), f->cov.p, sizeof(float4) * f->n, cudaMemcpyDeviceToHost));
+    }
+    for (int64_t sidx = 0; sidx < ns; ++sidx) {
+      const int64_t i = v.visible[sidx];
+      const float4 a = v.ab[2 * i], b = v.ab[2 * i + 1], c = v.c[i];
+      float* o = static_cast<float*>(host_dst) + sidx * width;
+      switch (field) {
+        case ODGS_FRAME_SPLAT_INDEX: static_cast<int64_t*>(host_dst)[sidx] = i; break;
+        case ODGS_FRAME_SPLAT_MEAN: o[0] = a.x; o[1] = a.y; break;
+        case ODGS_FRAME_SPLAT_COV2D: o[0] = cov[i].x; o[1] = cov[i].y; o[2] = cov[i].z; o[3] = cov[i].w; break;
+        case ODGS_FRAME_SPLAT_INV: o[0] = a.z; o[1] = a.w; o[2] = a.w; o[3] = b.x; break;
+        case ODGS_FRAME_SPLAT_DEPTH: o[0] = c.y; break;
+        case ODGS_FRAME_SPLAT_RADIUS: o[0] = c.z; break;
+        case ODGS_FRAME_SPLAT_OPACITY: o[0] = b.y; break;
+        case ODGS_FRAME_SPLAT_COLOR: o[0] = b.z; o[1] = b.w; o[2] = c.x; break;
+        case ODGS_FRAME_SPLAT_CLAMPED: static_cast<int32_t*>(host_dst)[sidx] = (flags_of(c) & kFlagClamped) ? 1 : 0; break;
+      }
+    }
+    return ok(ctx);
+  }
+  if (field >= ODGS_FRAME_SPLATGRAD_MEAN) {
+    const int width = field == ODGS_FRAME_SPLATGRAD_MEAN ? 2 : field == ODGS_FRAME_SPLATGRAD_COV2D ? 4
+                      : field == ODGS_FRAME_SPLATGRAD_OPACITY ? 1 : 3;
+    const int first = field == ODGS_FRAME_SPLATGRAD_MEAN ? 0 : field == ODGS_FRAME_SPLATGRAD_COV2D ? 2
+                      : field == ODGS_FRAME_SPLATGRAD_OPACITY ? 6 : 7;
+    if ((st = need(sizeof(float) * width * ns)) != ODGS_OK) return st;
+    std::vector<float> sg((size_t)f->n * 10);
+    if (f->n) ODGS_CUDA(ctx, cudaMemcpy(sg.data(), f->splat_grads.p, sizeof(float) * 10 * f->n, cudaMemcpyDeviceToHost));
+    for (int64_t sidx = 0; sidx < ns; ++sidx)
+      for (int k = 0; k < width; ++k)
+        static_cast<float*>(host_dst)[sidx * width + k] = sg[(size_t)v.visible[sidx] * 10 + first + k];
+    return ok(ctx);
+  }
+  // Instances sorted by (depth, index, shift) and the tile entries as instance ids.
+  std::vector<uint32_t> sorted_idx(f->n);
+  if (f->n)
+    ODGS_CUDA(ctx, cudaMemcpy(sorted_idx.data(), f->vals[f->depth_which].p, sizeof(uint32_t) * f->n,
+                              cudaMemcpyDeviceToHost));
+  std::vector<int32_t> inst_splat;
+  std::vector<float> inst_shift;
+  std::vector<int32_t> inst_id(3 * (size_t)f->n, -1);
+  for (int64_t r = 0; r < f->n; ++r) {
+    const uint32_t i = sorted_idx[r];
+    const uint32_t fl = flags_of(v.c[i]);
+    if (!(fl & kFlagVisible)) continue;
+    for (int k = 0; k < 3; ++k)
+      if (fl & (kFlagShiftBase << k)) {
+        inst_id[3 * (size_t)i + k] = (int32_t)inst_splat.size();
+        inst_splat.push_back((int32_t)v.splat_of[i]);
+        inst_shift.push_back(k == 0 ? -(float)f->width : (k == 1 ? 0.0f : (float)f->width));
+      }
+  }
+  if (field == ODGS_FRAME_INSTANCE_SPLAT) {
+    if ((st = need(sizeof(int32_t) * inst_splat.size())) != ODGS_OK) return st;
+    std::memcpy(host_dst, inst_splat.data(), sizeof(int32_t) * inst_splat.size());
+    return ok(ctx);
+  }
+  if (field == ODGS_FRAME_INSTANCE_SHIFT) {
+    if ((st = need(sizeof(float) * inst_shift.size())) != ODGS_OK) return st;
+    std::memcpy(host_dst, inst_shift.data(), sizeof(float) * inst_shift.size());
+    return ok(ctx);
+  }
+  if (field == ODGS_FRAME_TILE_ENTRIES) {
+    const uint32_t K = f->n_entries;
+    if ((st = need(sizeof(int32_t) * K)) != ODGS_OK) return st;
+    std::vector<uint32_t> vals(K);
+    if (K) ODGS_CUDA(ctx, cudaMemcpy(vals.data(), f->evals[f->tile_which].p, sizeof(uint32_t) * K, cudaMemcpyDeviceToHost));
+    for (uint32_t e = 0; e < K; ++e)
+      static_cast<int32_t*>(host_dst)[e] = inst_id[3 * (size_t)(vals[e] >> 2) + (vals[e] & 3u)];
+    return ok(ctx);
+  }
+  return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "bad field");
+}
+
+odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, odgs_frame* f,
+                          const float* dl_dimage, int32_t dl_memory, const odgs_settings* settings,
+                          const odgs_grads* grads, const double* grad_t_signs, uint32_t flags) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: frame not rendered");
+  if (!grads || !dl_dimage) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: null buffers");
+  odgs_status st;
+  if ((st = check_camera(ctx, camera)) != ODGS_OK) return st;
+  if ((st = check_settings(ctx, settings)) != ODGS_OK) return st;
+  if (!cloud || cloud->n != f->n)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: cloud does not match the frame");
+  CloudPtrs cp;
+  if ((st = resolve_cloud(ctx, cloud, &cp)) != ODGS_OK) return st;
+  cudaStream_t s = ctx->stream;
+  const int64_t n = f->n;
+  const int64_t px = (int64_t)f->width * f->height;
+  const uint32_t K = f->n_entries;
+
+  const float* dl = dl_dimage;
+  if (dl_memory != ODGS_MEM_DEVICE) {
+    ODGS_CUDA(ctx, ensure(ctx->dl_buf, sizeof(float) * 3 * px, s));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->dl_buf.p, dl_dimage, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, s));
+    dl = ctx->dl_buf.as<float>();
+  }
+  const float* signs = ctx->d_unit_signs;
+  if (grad_t_signs) {
+    float sf[12];
+    for (int k = 0; k < 12; ++k) sf[k] = (float)grad_t_signs[k];
+    ODGS_CUDA(ctx, ensure(ctx->signs_buf, sizeof sf, s));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->signs_buf.p, sf, sizeof sf, cudaMemcpyHostToDevice, s));
+    ODGS_CUDA(ctx, cudaStreamSynchronize(s));
+    signs = ctx->signs_buf.as<float>();
+  }
+  // Gradient destinations.
+  const bool host_out = grads->memory != ODGS_MEM_DEVICE;
+  float *gm = grads->means, *gq = grads->rotations, *gls = grads->log_scales, *gop = grads->raw_opacities,
+        *gcol = grads->colors, *gpn = grads->pixel_grad_norm, *gomc = grads->one_minus_cos;
+  int32_t* gobs = grads->observed;
+  if (host_out && n > 0) {
+    ODGS_CUDA(ctx, ensure(ctx->grads_buf, sizeof(float) * 17 * n, s));
+    float* b = ctx->grads_buf.as<float>();
+    float* dst[8] = {b, b + 3 * n, b + 7 * n, b + 10 * n, b + 11 * n, b + 14 * n, b + 15 * n, b + 16 * n};
+    const void* src[8] = {gm, gq, gls, gop, gcol, gpn, gomc, gobs};
+    const int64_t width[8] = {3, 4, 3, 1, 3, 1, 1, 1};
+    for (int k = 0; k < 8; ++k) {
+      if (!src[k] && k < 5) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: null gradient buffer");
+      if ((flags & ODGS_ACCUMULATE) && src[k])
+        ODGS_CUDA(ctx, cudaMemcpyAsync(dst[k], src[k], 4 * width[k] * n, cudaMemcpyHostToDevice, s));
+    }
+    gm = dst[0]; gq = dst[1]; gls = dst[2]; gop = dst[3]; gcol = dst[4];
+    gpn = gpn ? dst[5] : nullptr;
+    gomc = gomc ? dst[6] : nullptr;
+    gobs = gobs ? reinterpret_cast<int32_t*>(dst[7]) : nullptr;
+  }
+  ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
+  if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->records.p, 0, sizeof(float) * 9 * (size_t)K, s));
+  ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
+  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+
+  BwdRasterArgs ra;
+  ra.offsets = f->offsets.as<int32_t>();
+  ra.vals = f->evals[f->tile_which].as<uint32_t>();
+  ra.sp_ab = f->sp_ab.as<float4>();
+  ra.sp_c = f->sp_c.as<float4>();
+  ra.ent_off_idx = f->ent_off_idx.as<uint32_t>();
+  ra.transmittance = f->trans.as<float>();
+  ra.walked = f->walked.as<int32_t>();
+  ra.dl_dimage = dl;
+  ra.width = f->width;
+  ra.height = f->height;
+  ra.tile_size = f->tile_size;
+  ra.tiles_x = f->tiles_x;
+  ra.tiles_y = f->tiles_y;
+  ra.alpha_clamp = f->settings.alpha_clamp;
+  ra.cutoff_sigma = f->settings.cutoff_sigma;
+  ra.records = f->records.as<float>();
+  launch_bwd_raster(ra, s);
+
+  BwdSplatArgs sa;
+  sa.n = n;
+  sa.means = cp.means;
+  sa.rotations = cp.rotations;
+  sa.log_scales = cp.log_scales;
+  sa.raw_opacities = cp.raw_opacities;
+  sa.cam = f->cam;
+  sa.settings = f->settings;
+  sa.sp_ab = f->sp_ab.as<float4>();
+  sa.sp_c = f->sp_c.as<float4>();
+  sa.cnt = f->cnt.as<uint32_t>();
+  sa.ent_off_idx = f->ent_off_idx.as<uint32_t>();
+  sa.records = f->records.as<float>();
+  sa.signs = signs;
+  sa.accumulate = (flags & ODGS_ACCUMULATE) ? 1 : 0;
+  sa.g_means = gm;
+  sa.g_rotations = gq;
+  sa.g_log_scales = gls;
+  sa.g_raw_opacities = gop;
+  sa.g_colors = gcol;
+  sa.g_pixel_grad_norm = gpn;
+  sa.g_one_minus_cos = gomc;
+  sa.g_observed = gobs;
+  sa.splat_grads = f->splat_grads.as<float>();
+  sa.err = ctx->d_err;
+  launch_bwd_splat(sa, s);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  f->have_splat_grads = true;
+
+  if (host_out && n > 0) {
+    float* b = ctx->grads_buf.as<float>();
+    void* dsth[8] = {grads->means, grads->rotations, grads->log_scales, grads->raw_opacities, grads->colors,
+                     grads->pixel_grad_norm, grads->one_minus_cos, grads->observed};
+    const float* srcd[8] = {b, b + 3 * n, b + 7 * n, b + 10 * n, b + 11 * n, b + 14 * n, b + 15 * n, b + 16 * n};
+    const int64_t width[8] = {3, 4, 3, 1, 3, 1, 1, 1};
+    for (int k = 0; k < 8; ++k)
+      if (dsth[k]) ODGS_CUDA(ctx, cudaMemcpyAsync(dsth[k], srcd[k], 4 * width[k] * n, cudaMemcpyDeviceToHost, s));
+  }
+  if ((st = read_errors(ctx)) != ODGS_OK) return st;
+  const DevErrors& he = *ctx->h_err;
+  if (he.bwd_domain != kNoError) {
+    const int64_t idx = (int64_t)(he.bwd_domain >> 4);
+    return set_error(ctx, ODGS_ERR_DOMAIN, idx, "grad_position: undefined at the pole axis");
+  }
+  if (he.bwd_nonfinite != kNoError) {
+    const int64_t idx = (int64_t)(he.bwd_nonfinite >> 4);
+    return set_error(ctx, ODGS_ERR_RUNTIME, idx, "backward: non-finite gradient for Gaussian " + std::to_string(idx));
+  }
+  return ok(ctx);
+}
+
+odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, float near_radius,
+                      float far_radius, int64_t* out_indices, int64_t* out_count) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!(0.0f < near_radius && near_radius < far_radius))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cull: need 0 < near < far");
+  if (!camera || !out_count) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cull: null argument");
+  CloudPtrs cp;
+  odgs_status st;
+  if ((st = resolve_cloud(ctx, cloud, &cp)) != ODGS_OK) return st;
+  const int64_t n = cloud->n;
+  *out_count = 0;
+  if (n == 0) return ok(ctx);
+  ODGS_CUDA(ctx, ensure(ctx->cull_buf, n, ctx->stream));
+  launch_cull(n, cp.means, to_dev(*camera), near_radius, far_radius, ctx->cull_buf.as<uint8_t>(), ctx->stream);
+  std::vector<uint8_t> keep(n);
+  ODGS_CUDA(ctx, cudaMemcpyAsync(keep.data(), ctx->cull_buf.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  int64_t c = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (keep[i]) {
+      if (out_indices) out_indices[c] = i;
+      ++c;
+    }
+  *out_count = c;
+  return ok(ctx);
+}
+
+}  // extern "C"

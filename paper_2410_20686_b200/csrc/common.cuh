@@ -1,0 +1,188 @@
+// common.cuh — shared device code of the B200 ODGS rasterizer.
+//
+// Numerics contract: every translation unit of the rasterizer is compiled with
+// --fmad=false (no contraction) and IEEE division/sqrt, and every operation below
+// follows the reference's (and the oracle's) operation order, so a float render on
+// the GPU is bit-identical to oracle::render<float, PortableMath>: splat records,
+// instance order, tile CSR, walk lengths, transmittance and image.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "odgs_portable_math.h"
+
+namespace odgs_b200 {
+
+constexpr float kPiF = 3.14159274101257324f;  // std::numbers::pi_v<float>
+constexpr uint32_t kCulledKey = 0xFFFFFFFFu;
+
+// Per-call device error words. Each holds min over offenders of (index << 4 | code)
+// so the lowest Gaussian index wins, as in the reference's serial loops.
+struct DevErrors {
+  unsigned long long nonfinite;    // first_non_finite (rasterizer.hpp:134-136)
+  unsigned long long project;      // project_gaussian throws (code 1 invalid_argument, 3 domain)
+  unsigned long long bwd_domain;   // grad_position*/jacobian_omni_direct pole axis (backward.hpp:79-80)
+  unsigned long long bwd_nonfinite;  // non-finite gradient (backward.hpp:440-446)
+  unsigned long long n_entries;    // total tile entries K (written by the offsets scan)
+  unsigned long long n_visible;    // projected splats (RenderOutput::splats.size())
+  unsigned long long n_instances;  // seam instances (RenderOutput::instances.size())
+};
+constexpr unsigned long long kNoError = ~0ull;
+
+struct DevCamera {
+  float R[3][3];
+  float t[3];
+  int width, height;
+};
+
+struct DevSettings {
+  float near_radius, far_radius;
+  int tile_size;
+  float alpha_clamp, transmittance_floor, cutoff_sigma, lowpass_dilation, max_elevation;
+};
+
+// Splat flags (sp_c.w as bits).
+constexpr uint32_t kFlagVisible = 1u;
+constexpr uint32_t kFlagClamped = 2u;
+constexpr uint32_t kFlagShiftBase = 4u;  // bit (2 + k): instance for shift k in {-W, 0, +W} exists
+
+// ------------------------------------------------------------------ small matrices
+struct M2 { float a[2][2]; };
+struct M3 { float a[3][3]; };
+struct M23 { float a[2][3]; };
+
+__host__ __device__ __forceinline__ float sum2(float a, float b) { return a + b; }
+__host__ __device__ __forceinline__ float sum3(float a, float b, float c) { return a + (b + c); }
+__host__ __device__ __forceinline__ float sum4(float a, float b, float c, float d) { return (a + b) + (c + d); }
+
+// Lazy coefficient products with the halving sum order of the oracle (odgs_oracle.hpp mul()).
+__device__ __forceinline__ M2 mul22(const M2& x, const M2& y) {
+  M2 o;
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) o.a[r][c] = sum2(x.a[r][0] * y.a[0][c], x.a[r][1] * y.a[1][c]);
+  return o;
+}
+__device__ __forceinline__ M23 mul2_23(const M2& x, const M23& y) {
+  M23 o;
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c) o.a[r][c] = sum2(x.a[r][0] * y.a[0][c], x.a[r][1] * y.a[1][c]);
+  return o;
+}
+__device__ __forceinline__ M23 mul23_3(const M23& x, const M3& y) {
+  M23 o;
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 3; ++c)
+      o.a[r][c] = sum3(x.a[r][0] * y.a[0][c], x.a[r][1] * y.a[1][c], x.a[r][2] * y.a[2][c]);
+  return o;
+}
+__device__ __forceinline__ M3 mul33(const M3& x, const M3& y) {
+  M3 o;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      o.a[r][c] = sum3(x.a[r][0] * y.a[0][c], x.a[r][1] * y.a[1][c], x.a[r][2] * y.a[2][c]);
+  return o;
+}
+// x * y^T for 2x3 x 2x3 -> 2x2.
+__device__ __forceinline__ M2 mul23_32t(const M23& x, const M23& y) {
+  M2 o;
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c)
+      o.a[r][c] = sum3(x.a[r][0] * y.a[c][0], x.a[r][1] * y.a[c][1], x.a[r][2] * y.a[c][2]);
+  return o;
+}
+// m * m^T for 3x3.
+__device__ __forceinline__ M3 mul33_t(const M3& m) {
+  M3 o;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c)
+      o.a[r][c] = sum3(m.a[r][0] * m.a[c][0], m.a[r][1] * m.a[c][1], m.a[r][2] * m.a[c][2]);
+  return o;
+}
+
+// Eigen::Quaternion(w,x,y,z).toRotationMatrix() on a normalised quaternion (covariance.hpp:22).
+__device__ __forceinline__ M3 quaternion_matrix(float w, float x, float y, float z) {
+  const float tx = 2.0f * x, ty = 2.0f * y, tz = 2.0f * z;
+  const float twx = tx * w, twy = ty * w, twz = tz * w;
+  const float txx = tx * x, txy = ty * x, txz = tz * x;
+  const float tyy = ty * y, tyz = tz * y, tzz = tz * z;
+  M3 r;
+  r.a[0][0] = 1.0f - (tyy + tzz); r.a[0][1] = txy - twz;          r.a[0][2] = txz + twy;
+  r.a[1][0] = txy + twz;          r.a[1][1] = 1.0f - (txx + tzz); r.a[1][2] = tyz - twx;
+  r.a[2][0] = txz - twy;          r.a[2][1] = tyz + twx;          r.a[2][2] = 1.0f - (txx + tyy);
+  return r;
+}
+
+__device__ __forceinline__ void to_camera(const DevCamera& cam, const float p[3], float mu[3]) {
+  for (int r = 0; r < 3; ++r) mu[r] = sum3(cam.R[r][0] * p[0], cam.R[r][1] * p[1], cam.R[r][2] * p[2]) + cam.t[r];
+}
+
+// jacobian_omni_factored (projection.hpp:75-96) given the spherical angles and r.
+__device__ __forceinline__ M23 jacobian_factored(float phi, float theta, float r, float W, float H,
+                                                 float max_elevation, bool* clamped) {
+  const bool clamp = fabsf(theta) > max_elevation;
+  *clamped = clamp;
+  const float sec = 1.0f / pm_cosf(clamp ? max_elevation : fabsf(theta));
+  M23 j_o;
+  j_o.a[0][0] = 1.0f / r; j_o.a[0][1] = 0.0f; j_o.a[0][2] = 0.0f;
+  j_o.a[1][0] = 0.0f; j_o.a[1][1] = 1.0f / r; j_o.a[1][2] = 0.0f;
+  M2 q_o;
+  q_o.a[0][0] = sec; q_o.a[0][1] = 0.0f; q_o.a[1][0] = 0.0f; q_o.a[1][1] = 1.0f;
+  M2 s_o;
+  s_o.a[0][0] = W / (2.0f * kPiF); s_o.a[0][1] = 0.0f; s_o.a[1][0] = 0.0f; s_o.a[1][1] = H / kPiF;
+  const float cp = pm_cosf(phi), sp = pm_sinf(phi);
+  const float ct = pm_cosf(theta), st = pm_sinf(theta);
+  M3 t_phi, t_theta;
+  t_phi.a[0][0] = cp;   t_phi.a[0][1] = 0.0f; t_phi.a[0][2] = -sp;
+  t_phi.a[1][0] = 0.0f; t_phi.a[1][1] = 1.0f; t_phi.a[1][2] = 0.0f;
+  t_phi.a[2][0] = sp;   t_phi.a[2][1] = 0.0f; t_phi.a[2][2] = cp;
+  t_theta.a[0][0] = 1.0f; t_theta.a[0][1] = 0.0f; t_theta.a[0][2] = 0.0f;
+  t_theta.a[1][0] = 0.0f; t_theta.a[1][1] = ct;   t_theta.a[1][2] = st;
+  t_theta.a[2][0] = 0.0f; t_theta.a[2][1] = -st;  t_theta.a[2][2] = ct;
+  const M3 tmu = mul33(t_theta, t_phi);
+  return mul23_3(mul2_23(mul22(s_o, q_o), j_o), tmu);
+}
+
+// Saturating floor-to-int (matches oracle::floor_to_int).
+__device__ __forceinline__ int floor_to_int(float v) {
+  float f = floorf(v);
+  if (!(f >= -1073741824.0f)) f = -1073741824.0f;
+  if (f > 1073741824.0f) f = 1073741824.0f;
+  return (int)f;
+}
+
+// instance_box (rasterizer.hpp:107-122). Returns false if the clipped box is empty.
+__device__ __forceinline__ bool instance_box(float mx, float my, float radius, float shift, int width, int height,
+                                             int box[4]) {
+  const float cx = mx + shift;
+  const float cy = my;
+  const int x0 = max(0, floor_to_int(cx - radius - 0.5f) + 1);
+  const int x1 = min(width - 1, floor_to_int(cx + radius - 0.5f));
+  const int y0 = max(0, floor_to_int(cy - radius - 0.5f) + 1);
+  const int y1 = min(height - 1, floor_to_int(cy + radius - 0.5f));
+  if (x0 > x1 || y0 > y1) return false;
+  box[0] = x0; box[1] = x1; box[2] = y0; box[3] = y1;
+  return true;
+}
+
+__device__ __forceinline__ float shift_of(int k, int width) {
+  return k == 0 ? -(float)width : (k == 1 ? 0.0f : (float)width);
+}
+
+// Tile span of shift k of a splat (box / tile_size); false if no instance.
+__device__ __forceinline__ bool instance_tiles(float mx, float my, float radius, int k, int width, int height,
+                                               int tile_size, int span[4]) {
+  int box[4];
+  if (!instance_box(mx, my, radius, shift_of(k, width), width, height, box)) return false;
+  for (int q = 0; q < 4; ++q) span[q] = box[q] / tile_size;
+  return true;
+}
+
+__device__ __forceinline__ void atomic_min_error(unsigned long long* word, long long index, int code) {
+  atomicMin(word, ((unsigned long long)index << 4) | (unsigned long long)code);
+}
+
+__device__ __forceinline__ float std_min(float a, float b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ float std_max(float a, float b) { return (a < b) ? b : a; }  // std::max
+
+}  // namespace odgs_b200

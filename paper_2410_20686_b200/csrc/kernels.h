@@ -1,0 +1,106 @@
+// kernels.h — host-side launch interface of the device kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace odgs_b200 {
+
+// Every launch_* below increments this counter once per kernel it launches, so the
+// host can report how many of its own kernels ran (bench.py "gpu_launches").
+extern thread_local int64_t g_launches;
+
+struct PreprocessArgs {
+  int64_t n;
+  const float *means, *rotations, *log_scales, *raw_opacities, *colors;
+  DevCamera cam;
+  DevSettings settings;
+  float4* sp_ab;   // [2n] {mx,my,i00,i01},{i11,opacity,r,g}
+  float4* sp_c;    // [n] {b, depth, radius, flags}
+  float4* cov_out; // [n] or null
+  uint32_t* keys;  // [n] depth bits or kCulledKey
+  uint32_t* vals;  // [n] iota
+  uint32_t* cnt;   // [n] tile entries of the Gaussian
+  DevErrors* err;
+};
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
+
+void launch_gather_counts(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt, uint32_t* cnt_sorted,
+                          cudaStream_t stream);
+
+struct EmitArgs {
+  int64_t n;
+  const uint32_t *sorted_idx, *cnt_sorted, *off_sorted;
+  const float4 *sp_ab, *sp_c;
+  int width, height, tile_size, tiles_x;
+  uint32_t *out_keys, *out_vals, *ent_off_idx;
+};
+void launch_emit(const EmitArgs& a, cudaStream_t stream);
+
+void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, float far_r, uint8_t* keep,
+                 cudaStream_t stream);
+
+void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, int32_t* offsets,
+                        cudaStream_t stream);
+
+struct BlendArgs {
+  const int32_t* offsets;
+  const uint32_t* vals;
+  const float4 *sp_ab, *sp_c;
+  int width, height, tile_size, tiles_x, tiles_y;
+  float alpha_clamp, transmittance_floor, cutoff_sigma;
+  float* image;
+  float* transmittance;
+  int32_t* walked;
+};
+void launch_blend(const BlendArgs& a, cudaStream_t stream);
+
+// ------------------------------------------------------------------ sort / scan
+// Scratch needed by exclusive_scan_u32 for n items.
+size_t scan_temp_bytes(int64_t n);
+// out[k] = sum_{j<k} in[k]; optionally atomically adds the 64-bit total to *total64.
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp, unsigned long long* total64,
+                        cudaStream_t stream);
+
+size_t radix_sort_temp_bytes(int64_t n);
+// Stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit).
+// keys/vals: [2] ping-pong buffers of n each; on return *which (0/1) holds the result.
+void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
+                      int* which, cudaStream_t stream);
+
+// ------------------------------------------------------------------ backward
+struct BwdRasterArgs {
+  const int32_t* offsets;
+  const uint32_t* vals;
+  const float4 *sp_ab, *sp_c;
+  const uint32_t* ent_off_idx;
+  const float* transmittance;
+  const int32_t* walked;
+  const float* dl_dimage;
+  int width, height, tile_size, tiles_x, tiles_y;
+  float alpha_clamp, cutoff_sigma;
+  float* records;  // [K][9] per tile entry, at the entry's emit position
+};
+void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
+
+struct BwdSplatArgs {
+  int64_t n;
+  const float *means, *rotations, *log_scales, *raw_opacities;
+  DevCamera cam;
+  DevSettings settings;
+  const float4 *sp_ab, *sp_c;
+  const uint32_t *cnt, *ent_off_idx;
+  const float* records;
+  const float* signs;  // [12] GradTSigns
+  int accumulate;
+  float *g_means, *g_rotations, *g_log_scales, *g_raw_opacities, *g_colors, *g_pixel_grad_norm, *g_one_minus_cos;
+  int32_t* g_observed;
+  float* splat_grads;  // [n][10] SplatGrads per Gaussian (mean2, cov4, opacity, color3) or null
+  DevErrors* err;
+};
+void launch_bwd_splat(const BwdSplatArgs& a, cudaStream_t stream);
+
+}  // namespace odgs_b200

@@ -1,0 +1,418 @@
+// raster_bwd.cu — backward hot path of the B200 ODGS rasterizer.
+//
+//   k_bwd_raster  one CTA per tile, back to front over the tile list. Each pixel starts
+//                 from its stored final transmittance (bit-identical to the reference's
+//                 forward replay, backward.hpp:250-269) and runs the suffix recursion
+//                 (:271-305). Per entry, the 9 accumulators (EntryGrad, :218-224) are
+//                 summed over the tile's pixels in a fixed order (pixel -> warp xor tree
+//                 -> warps in index order) and written to the entry's EMIT position, so
+//                 every Gaussian's records are contiguous. Deterministic, no atomics.
+//   k_bwd_splat   one thread per Gaussian: ordered fold of its records (:310-327),
+//                 Sigma_2D transport (:329-337), then the per-splat chain rule
+//                 (:393-438) incl. the densify statistics, plus the error checks
+//                 (pole axis :79-80, non-finite gradient :440-446).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace odgs_b200 {
+
+constexpr int kBwdThreads = 256;
+constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kBwdBatch = 128;
+constexpr int kRec = 9;  // mx, my, m00, m01, m11, op, c0, c1, c2
+
+template <int PPT>
+__global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
+    const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
+    const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
+    const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
+    const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
+    float cutoff2, float* __restrict__ records) {
+  __shared__ float s_cx[kBwdBatch], s_cy[kBwdBatch], s_i00[kBwdBatch], s_i01[kBwdBatch], s_i11[kBwdBatch],
+      s_op[kBwdBatch], s_col[3][kBwdBatch];
+  __shared__ uint32_t s_pos[kBwdBatch];
+  __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];
+  __shared__ int s_maxw[kBwdWarps];
+
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int e0 = offsets[tile];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int area = tile_size * tile_size;
+  const int64_t plane = (int64_t)width * height;
+
+  float px[PPT], py[PPT], t[PPT], d0[PPT], d1[PPT], d2v[PPT], suf0[PPT], suf1[PPT], suf2[PPT];
+  int wk[PPT];
+  int my_max = 0;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int lp = tid + q * kBwdThreads;
+    const int lx = lp / tile_size, ly = lp - lx * tile_size;
+    const int x = tx * tile_size + lx, y = ty * tile_size + ly;
+    const bool valid = lp < area && x < width && y < height;
+    px[q] = (float)x + 0.5f;
+    py[q] = (float)y + 0.5f;
+    wk[q] = 0;
+    t[q] = 1.0f;
+    d0[q] = d1[q] = d2v[q] = 0.0f;
+    suf0[q] = suf1[q] = suf2[q] = 0.0f;
+    if (valid) {
+      const int64_t p = (int64_t)x * height + y;
+      d0[q] = dl_dimage[p];
+      d1[q] = dl_dimage[plane + p];
+      d2v[q] = dl_dimage[2 * plane + p];
+      // Only exact zeros are skipped (the reference's float isZero() also skips
+      // |g| <= 1e-5, which would silently drop small L1 gradients).
+      if (d0[q] != 0.0f || d1[q] != 0.0f || d2v[q] != 0.0f) {
+        wk[q] = walked_in[p];
+        t[q] = transmittance[p];
+      }
+    }
+    my_max = max(my_max, wk[q]);
+  }
+  // CTA-wide max walk: entries at or beyond it are never replayed.
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, d));
+  if (lane == 0) s_maxw[warp] = my_max;
+  __syncthreads();
+  int max_walked = 0;
+  for (int w = 0; w < kBwdWarps; ++w) max_walked = max(max_walked, s_maxw[w]);
+
+  for (int hi = max_walked; hi > 0; hi -= kBwdBatch) {
+    const int lo = max(0, hi - kBwdBatch);
+    const int count = hi - lo;
+    if (tid < count) {
+      const int e = e0 + lo + tid;
+      const uint32_t v = vals[e];
+      const uint32_t g = v >> 2;
+      const int k = (int)(v & 3u);
+      const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+      const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+      const float4 c = __ldg(sp_c + g);
+      s_cx[tid] = a.x + shift_of(k, width);
+      s_cy[tid] = a.y;
+      s_i00[tid] = a.z;
+      s_i01[tid] = a.w;
+      s_i11[tid] = b.x;
+      s_op[tid] = b.y;
+      s_col[0][tid] = b.z;
+      s_col[1][tid] = b.w;
+      s_col[2][tid] = c.x;
+      // Emit position of (tile, g, k): the Gaussian's first entry + areas of its
+      // earlier shifts + row-major offset inside this shift's tile rectangle.
+      uint32_t pos = __ldg(ent_off_idx + g);
+      for (int kk = 0; kk <= k; ++kk) {
+        int span[4];
+        if (!instance_tiles(a.x, a.y, c.z, kk, width, height, tile_size, span)) continue;
+        const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
+        if (kk < k) pos += w * (uint32_t)(span[3] - span[2] + 1);
+        else pos += (uint32_t)(ty - span[2]) * w + (uint32_t)(tx - span[0]);
+      }
+      s_pos[tid] = pos;
+    }
+    __syncthreads();
+    for (int j = count - 1; j >= 0; --j) {
+      const int rel = lo + j;  // entry index inside the tile list
+      float acc[kRec];
+#pragma unroll
+      for (int c = 0; c < kRec; ++c) acc[c] = 0.0f;
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        if (rel >= wk[q]) continue;
+        const float dx = px[q] - s_cx[j];
+        const float dy = py[q] - s_cy[j];
+        const float i00 = s_i00[j], i01 = s_i01[j], i11 = s_i11[j];
+        const float dd = i00 * dx * dx + 2.0f * i01 * dx * dy + i11 * dy * dy;
+        if (dd > cutoff2) continue;
+        const float op = s_op[j];
+        const float G = pm_expf_blend(-dd / 2.0f);
+        const float raw_alpha = op * G;
+        const float alpha = std_min(alpha_clamp, raw_alpha);
+        const float one_m = 1.0f - alpha;
+        const float t_here = t[q] / one_m;
+        const float c0 = s_col[0][j], c1 = s_col[1][j], c2 = s_col[2][j];
+        acc[6] += d0[q] * alpha * t_here;
+        acc[7] += d1[q] * alpha * t_here;
+        acc[8] += d2v[q] * alpha * t_here;
+        const float v0 = c0 * t_here - suf0[q] / one_m;
+        const float v1 = c1 * t_here - suf1[q] / one_m;
+        const float v2 = c2 * t_here - suf2[q] / one_m;
+        const float dl_dalpha = d0[q] * v0 + (d1[q] * v1 + d2v[q] * v2);
+        const float at = alpha * t_here;
+        suf0[q] += c0 * at;
+        suf1[q] += c1 * at;
+        suf2[q] += c2 * at;
+        t[q] = t_here;
+        any = true;
+        if (raw_alpha > alpha_clamp) continue;  // clamped: no alpha gradient (:289)
+        acc[5] += dl_dalpha * G;
+        const float dl_dd2 = dl_dalpha * op * (-G / 2.0f);
+        const float gx = i00 * dx + i01 * dy;
+        const float gy = i01 * dx + i11 * dy;
+        acc[0] += dl_dd2 * (-2.0f) * gx;
+        acc[1] += dl_dd2 * (-2.0f) * gy;
+        acc[2] += dl_dd2 * dx * dx;
+        acc[3] += dl_dd2 * dx * dy;
+        acc[4] += dl_dd2 * dy * dy;
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) {
+          float v = acc[c];
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+          acc[c] = v;
+        }
+      }
+      if (lane < kRec) {
+        float v = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) v = (lane == c) ? acc[c] : v;
+        s_part[warp][j][lane] = v;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < count * kRec; idx += kBwdThreads) {
+      const int j = idx / kRec, c = idx - j * kRec;
+      float s = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kBwdWarps; ++w) s += s_part[w][j][c];
+      records[(int64_t)s_pos[j] * kRec + c] = s;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  if (n_tiles == 0) return;
+  const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
+  const int area = a.tile_size * a.tile_size;
+#define ODGS_BWD(PPT)                                                                                             \
+  k_bwd_raster<PPT><<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,       \
+                                                         a.transmittance, a.walked, a.dl_dimage, a.width, a.height, \
+                                                         a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2, a.records)
+  if (area <= kBwdThreads) ODGS_BWD(1);
+  else if (area <= 4 * kBwdThreads) ODGS_BWD(4);
+  else ODGS_BWD(16);
+#undef ODGS_BWD
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ per-splat chain rule
+__device__ __forceinline__ bool all_finite(const float* v, int n) {
+  bool ok = true;
+  for (int k = 0; k < n; ++k) ok = ok && isfinite(v[k]);
+  return ok;
+}
+
+__global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = a.n;
+  if (i >= n) return;
+  const float4 c4 = a.sp_c[i];
+  const uint32_t flags = __float_as_uint(c4.w);
+  float gm[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gls[3] = {0, 0, 0}, gop = 0, gcol[3] = {0, 0, 0};
+  float pgn = 0, omc = 0;
+  int observed = 0;
+  if (flags & kFlagVisible) {
+    observed = 1;
+    // Ordered fold of this Gaussian's entry records (contiguous, emit order).
+    float r[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const uint32_t off = a.ent_off_idx[i], cnt = a.cnt[i];
+    for (uint32_t e = 0; e < cnt; ++e) {
+      const float* rec = a.records + (int64_t)(off + e) * kRec;
+#pragma unroll
+      for (int c = 0; c < kRec; ++c) r[c] += rec[c];
+    }
+    const float4 ab0 = a.sp_ab[2 * i], ab1 = a.sp_ab[2 * i + 1];
+    const float inv[2][2] = {{ab0.z, ab0.w}, {ab0.w, ab1.x}};
+    const float ginv[2][2] = {{r[2], r[3]}, {r[3], r[4]}};
+    // dL/dSigma2D = -inv * G_inv * inv (backward.hpp:336)
+    float tmp[2][2], dcov[2][2];
+    for (int p = 0; p < 2; ++p)
+      for (int q = 0; q < 2; ++q) tmp[p][q] = (-inv[p][0]) * ginv[0][q] + (-inv[p][1]) * ginv[1][q];
+    for (int p = 0; p < 2; ++p)
+      for (int q = 0; q < 2; ++q) dcov[p][q] = tmp[p][0] * inv[0][q] + tmp[p][1] * inv[1][q];
+    const float sg_mean[2] = {r[0], r[1]};
+    const float sg_op = r[5];
+    if (a.splat_grads) {
+      float* o = a.splat_grads + i * 10;
+      o[0] = r[0]; o[1] = r[1];
+      o[2] = dcov[0][0]; o[3] = dcov[0][1]; o[4] = dcov[1][0]; o[5] = dcov[1][1];
+      o[6] = r[5]; o[7] = r[6]; o[8] = r[7]; o[9] = r[8];
+    }
+
+    // Reconstruct the forward intermediates (backward.hpp:400-410).
+    const float p[3] = {a.means[i], a.means[n + i], a.means[2 * n + i]};
+    const float qraw[4] = {a.rotations[i], a.rotations[n + i], a.rotations[2 * n + i], a.rotations[3 * n + i]};
+    const float ls[3] = {a.log_scales[i], a.log_scales[n + i], a.log_scales[2 * n + i]};
+    float mu[3];
+    to_camera(a.cam, p, mu);
+    const float x = mu[0], y = mu[1], z = mu[2];
+    const float W = (float)a.cam.width, H = (float)a.cam.height;
+    const float phi = pm_atan2f(x, z);
+    const float rho_h = pm_hypotf(x, z);
+    const float theta = pm_atan2f(-y, rho_h);
+    omc = 1.0f - pm_cosf(theta);
+    const float depth = sqrtf(sum3(x * x, y * y, z * z));
+    bool clamped;
+    const M23 J = jacobian_factored(phi, theta, depth, W, H, a.settings.max_elevation, &clamped);
+    const float qn = sqrtf(sum4(qraw[0] * qraw[0], qraw[1] * qraw[1], qraw[2] * qraw[2], qraw[3] * qraw[3]));
+    const float qq[4] = {qraw[0] / qn, qraw[1] / qn, qraw[2] / qn, qraw[3] / qn};
+    const M3 Rq = quaternion_matrix(qq[0], qq[1], qq[2], qq[3]);
+    const float sc[3] = {pm_expf(ls[0]), pm_expf(ls[1]), pm_expf(ls[2])};
+    M3 m;
+    for (int rr = 0; rr < 3; ++rr)
+      for (int k = 0; k < 3; ++k) m.a[rr][k] = Rq.a[rr][k] * sc[k];
+    const M3 V = mul33_t(m);
+    M3 Rc;
+    for (int rr = 0; rr < 3; ++rr)
+      for (int k = 0; k < 3; ++k) Rc.a[rr][k] = a.cam.R[rr][k];
+    const M23 T = mul23_3(J, Rc);
+
+    // grad_T (backward.hpp:42-68)
+    const float* s = a.signs;
+    const float d11 = dcov[0][0], d22 = dcov[1][1], d12 = dcov[0][1] + dcov[1][0];
+    float av[3], bv[3];
+    for (int c = 0; c < 3; ++c) {
+      av[c] = T.a[0][0] * V.a[c][0] + T.a[0][1] * V.a[c][1] + T.a[0][2] * V.a[c][2];
+      bv[c] = T.a[1][0] * V.a[c][0] + T.a[1][1] * V.a[c][1] + T.a[1][2] * V.a[c][2];
+    }
+    float dT[2][3];
+    for (int c = 0; c < 3; ++c) {
+      dT[0][c] = s[2 * c] * 2.0f * av[c] * d11 + s[2 * c + 1] * bv[c] * d12;
+      dT[1][c] = s[6 + 2 * c] * 2.0f * bv[c] * d22 + s[6 + 2 * c + 1] * av[c] * d12;
+    }
+    // dl_dj = dl_dt * R^T
+    float dJ[2][3];
+    for (int rr = 0; rr < 2; ++rr)
+      for (int c = 0; c < 3; ++c)
+        dJ[rr][c] = dT[rr][0] * Rc.a[c][0] + dT[rr][1] * Rc.a[c][1] + dT[rr][2] * Rc.a[c][2];
+
+    float dmu[3] = {0, 0, 0};
+    const float rho2 = x * x + z * z;
+    if (!(rho2 > 0.0f)) {
+      atomic_min_error(&a.err->bwd_domain, i, 3);
+    } else {
+      const float rho = sqrtf(rho2);
+      const float r2 = rho2 + y * y;
+      const float kw0 = W / (2.0f * kPiF), kh0 = H / kPiF;
+      if (!clamped) {  // grad_position (backward.hpp:73-105)
+        const float r4 = r2 * r2;
+        const float g11 = dJ[0][0], g13 = dJ[0][2], g21 = dJ[1][0], g22 = dJ[1][1], g23 = dJ[1][2];
+        const float xz_over_rho4 = x * z / (rho2 * rho2);
+        const float xx_minus_zz = (x * x - z * z) / (rho2 * rho2);
+        const float mixed = x * y * z * (2.0f * rho2 + r2) / (r4 * rho2 * rho);
+        const float straight = (r2 - 2.0f * y * y) / (r4 * rho);
+        dmu[0] = -2.0f * kw0 * xz_over_rho4 * g11 + kw0 * xx_minus_zz * g13 -
+                 kh0 * y * (z * z * r2 - 2.0f * x * x * rho2) / (r4 * rho2 * rho) * g21 - kh0 * x * straight * g22 +
+                 kh0 * mixed * g23;
+        dmu[1] = -kh0 * x * straight * g21 - 2.0f * kh0 * y * rho / r4 * g22 - kh0 * z * straight * g23;
+        dmu[2] = kw0 * xx_minus_zz * g11 + 2.0f * kw0 * xz_over_rho4 * g13 + kh0 * mixed * g21 -
+                 kh0 * z * straight * g22 - kh0 * y * (x * x * r2 - 2.0f * z * z * rho2) / (r4 * rho2 * rho) * g23;
+      } else {  // grad_position_clamped (backward.hpp:111-150)
+        const float r = sqrtf(r2);
+        const float cp = pm_cosf(phi), sp = pm_sinf(phi), ct = pm_cosf(theta), st = pm_sinf(theta);
+        const float sec = 1.0f / pm_cosf(a.settings.max_elevation);
+        const float kw = W / (2.0f * kPiF) * sec / r;
+        const float kh = H / kPiF / r;
+        const float djr[2][3] = {{-kw * cp / r, 0.0f, kw * sp / r}, {-kh * st * sp / r, -kh * ct / r, -kh * st * cp / r}};
+        const float djp[2][3] = {{-kw * sp, 0.0f, -kw * cp}, {kh * st * cp, 0.0f, -kh * st * sp}};
+        const float djt[2][3] = {{0.0f, 0.0f, 0.0f}, {kh * ct * sp, -kh * st, kh * ct * cp}};
+        float cr = 0, cph = 0, cth = 0;
+        for (int c = 0; c < 3; ++c)
+          for (int rr = 0; rr < 2; ++rr) {
+            cr += dJ[rr][c] * djr[rr][c];
+            cph += dJ[rr][c] * djp[rr][c];
+            cth += dJ[rr][c] * djt[rr][c];
+          }
+        const float drdt[3] = {x / r, y / r, z / r};
+        const float dphidt[3] = {z / rho2, 0.0f, -x / rho2};
+        const float dthdt[3] = {x * y / (rho * r2), -rho / r2, z * y / (rho * r2)};
+        for (int c = 0; c < 3; ++c) dmu[c] = cr * drdt[c] + cph * dphidt[c] + cth * dthdt[c];
+      }
+      // Mean path: unclamped direct Jacobian (projection.hpp:118-133, backward.hpp:420-423)
+      const float jd[2][3] = {{kw0 * z / rho2, 0.0f, -kw0 * x / rho2},
+                              {-kh0 * x * y / (rho * r2), kh0 * rho / r2, -kh0 * y * z / (rho * r2)}};
+      for (int c = 0; c < 3; ++c) dmu[c] += jd[0][c] * sg_mean[0] + jd[1][c] * sg_mean[1];
+    }
+    // means = R^T dmu
+    for (int c = 0; c < 3; ++c) gm[c] = Rc.a[0][c] * dmu[0] + (Rc.a[1][c] * dmu[1] + Rc.a[2][c] * dmu[2]);
+    pgn = sqrtf(sg_mean[0] * sg_mean[0] + sg_mean[1] * sg_mean[1]);
+
+    // dL/dSigma3D = T^T dcov T; grad_cov3d_params (backward.hpp:156-201)
+    float tg[3][2];
+    for (int c = 0; c < 3; ++c)
+      for (int q = 0; q < 2; ++q) tg[c][q] = T.a[0][c] * dcov[0][q] + T.a[1][c] * dcov[1][q];
+    float ds[3][3];
+    for (int c = 0; c < 3; ++c)
+      for (int d = 0; d < 3; ++d) ds[c][d] = tg[c][0] * T.a[0][d] + tg[c][1] * T.a[1][d];
+    float dm[3][3];  // 2 * dSigma * M
+    for (int rr = 0; rr < 3; ++rr)
+      for (int k = 0; k < 3; ++k)
+        dm[rr][k] = 2.0f * (ds[rr][0] * m.a[0][k] + ds[rr][1] * m.a[1][k] + ds[rr][2] * m.a[2][k]);
+    float drot[3][3];
+    for (int rr = 0; rr < 3; ++rr)
+      for (int k = 0; k < 3; ++k) drot[rr][k] = dm[rr][k] * sc[k];
+    for (int k = 0; k < 3; ++k)
+      gls[k] = (Rq.a[0][k] * dm[0][k] + Rq.a[1][k] * dm[1][k] + Rq.a[2][k] * dm[2][k]) * sc[k];
+    const float w = qq[0], qx = qq[1], qy = qq[2], qz = qq[3];
+    const float dw[3][3] = {{0, -qz, qy}, {qz, 0, -qx}, {-qy, qx, 0}};
+    const float dx[3][3] = {{0, qy, qz}, {qy, -2 * qx, -w}, {qz, w, -2 * qx}};
+    const float dy[3][3] = {{-2 * qy, qx, w}, {qx, 0, qz}, {-w, qz, -2 * qy}};
+    const float dz[3][3] = {{-2 * qz, -w, qx}, {w, -2 * qz, qy}, {qx, qy, 0}};
+    float gu[4] = {0, 0, 0, 0};
+    for (int rr = 0; rr < 3; ++rr)
+      for (int k = 0; k < 3; ++k) {
+        gu[0] += drot[rr][k] * dw[rr][k];
+        gu[1] += drot[rr][k] * dx[rr][k];
+        gu[2] += drot[rr][k] * dy[rr][k];
+        gu[3] += drot[rr][k] * dz[rr][k];
+      }
+    for (int k = 0; k < 4; ++k) gu[k] *= 2.0f;
+    const float qd = (qq[0] * gu[0] + qq[1] * gu[1]) + (qq[2] * gu[2] + qq[3] * gu[3]);
+    for (int k = 0; k < 4; ++k) gq[k] = (gu[k] - qq[k] * qd) / qn;
+
+    const float o = ab1.y;
+    gop = sg_op * o * (1.0f - o);
+    gcol[0] = r[6];
+    gcol[1] = r[7];
+    gcol[2] = r[8];
+    float all[14];
+    for (int k = 0; k < 3; ++k) all[k] = gm[k];
+    for (int k = 0; k < 4; ++k) all[3 + k] = gq[k];
+    for (int k = 0; k < 3; ++k) all[7 + k] = gls[k];
+    all[10] = gop;
+    for (int k = 0; k < 3; ++k) all[11 + k] = gcol[k];
+    if (!all_finite(all, 14)) atomic_min_error(&a.err->bwd_nonfinite, i, 2);
+  }
+  if (a.accumulate) {
+    for (int k = 0; k < 3; ++k) a.g_means[k * n + i] += gm[k];
+    for (int k = 0; k < 4; ++k) a.g_rotations[k * n + i] += gq[k];
+    for (int k = 0; k < 3; ++k) a.g_log_scales[k * n + i] += gls[k];
+    a.g_raw_opacities[i] += gop;
+    for (int k = 0; k < 3; ++k) a.g_colors[k * n + i] += gcol[k];
+    if (a.g_pixel_grad_norm) a.g_pixel_grad_norm[i] += pgn;
+    if (a.g_one_minus_cos) a.g_one_minus_cos[i] += omc;
+    if (a.g_observed) a.g_observed[i] += observed;
+  } else {
+    for (int k = 0; k < 3; ++k) a.g_means[k * n + i] = gm[k];
+    for (int k = 0; k < 4; ++k) a.g_rotations[k * n + i] = gq[k];
+    for (int k = 0; k < 3; ++k) a.g_log_scales[k * n + i] = gls[k];
+    a.g_raw_opacities[i] = gop;
+    for (int k = 0; k < 3; ++k) a.g_colors[k * n + i] = gcol[k];
+    if (a.g_pixel_grad_norm) a.g_pixel_grad_norm[i] = pgn;
+    if (a.g_one_minus_cos) a.g_one_minus_cos[i] = omc;
+    if (a.g_observed) a.g_observed[i] = observed;
+  }
+}
+
+void launch_bwd_splat(const BwdSplatArgs& a, cudaStream_t stream) {
+  if (a.n == 0) return;
+  k_bwd_splat<<<(unsigned)((a.n + 255) / 256), 256, 0, stream>>>(a);
+  ++g_launches;
+}
+
+}  // namespace odgs_b200

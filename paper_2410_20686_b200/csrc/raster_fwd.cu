@@ -1,0 +1,414 @@
+// raster_fwd.cu — forward hot path of the B200 ODGS rasterizer.
+//
+//   k_preprocess  one thread per Gaussian: shell cull, ERP centre, tangent-plane
+//                 Jacobian, Sigma -> Sigma_2D, inverse, radius, opacity, seam-instance
+//                 tile counts, depth sort key           (projection.hpp:178-216,
+//                                                         rasterizer.hpp:133-156)
+//   k_emit        one warp per 32 depth-ranked splats: writes (tile, gaussian|shift)
+//                 entries in global (depth, index, shift) order, load-balanced over the
+//                 warp                                   (rasterizer.hpp:158-205)
+//   k_tile_ranges CSR tile offsets from the tile-sorted entries, empty tiles included
+//   k_blend       one CTA per tile: front-to-back compositing with batches of splats
+//                 staged in shared memory and CTA-wide early exit (rasterizer.hpp:211-267)
+//
+// Compiled with --fmad=false: see common.cuh for the numerics contract.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace odgs_b200 {
+
+// ------------------------------------------------------------------ preprocess
+// Projects Gaussian i; returns the number of seam instances (0 if culled) and sets
+// *visible. Error words get the lowest offending index.
+__device__ __forceinline__ uint32_t preprocess_one(
+    int64_t i, int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
+    const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
+    const float* __restrict__ colors, const DevCamera& cam, const DevSettings& s, float4* __restrict__ sp_ab,
+    float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, bool* visible) {
+  *visible = false;
+  const float p[3] = {__ldg(means + i), __ldg(means + n + i), __ldg(means + 2 * n + i)};
+  const float q[4] = {__ldg(rotations + i), __ldg(rotations + n + i), __ldg(rotations + 2 * n + i),
+                      __ldg(rotations + 3 * n + i)};
+  const float ls[3] = {__ldg(log_scales + i), __ldg(log_scales + n + i), __ldg(log_scales + 2 * n + i)};
+  const float raw = __ldg(raw_opacities + i);
+  const float col[3] = {__ldg(colors + i), __ldg(colors + n + i), __ldg(colors + 2 * n + i)};
+
+  keys[i] = kCulledKey;
+  vals[i] = (uint32_t)i;
+  cnt[i] = 0;
+  sp_c[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+
+  bool finite = isfinite(raw);
+  for (int c = 0; c < 3; ++c) finite = finite && isfinite(p[c]) && isfinite(ls[c]) && isfinite(col[c]);
+  for (int c = 0; c < 4; ++c) finite = finite && isfinite(q[c]);
+  if (!finite) {
+    atomic_min_error(&err->nonfinite, i, 2);
+    return 0;
+  }
+
+  float mu[3];
+  to_camera(cam, p, mu);
+  const float sq = sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]);
+  const float depth = sqrtf(sq);
+  if (!(depth >= s.near_radius && depth <= s.far_radius)) return 0;  // shell cull
+  if (!(sq > 0.0f)) {
+    atomic_min_error(&err->project, i, 3);  // to_spherical domain_error
+    return 0;
+  }
+  const float phi = pm_atan2f(mu[0], mu[2]);
+  const float rho = pm_hypotf(mu[0], mu[2]);
+  const float theta = pm_atan2f(-mu[1], rho);
+  const float W = (float)cam.width, H = (float)cam.height;
+  const float mx = W / (2.0f * kPiF) * phi + W / 2.0f;
+  const float my = -H / kPiF * theta + H / 2.0f;
+  bool clamped;
+  const M23 J = jacobian_factored(phi, theta, depth, W, H, s.max_elevation, &clamped);
+
+  // build_covariance (covariance.hpp:28-37)
+  const float qn = sqrtf(sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]));
+  if (!(qn > 1e-12f)) {
+    atomic_min_error(&err->project, i, 1);  // normalize_quaternion invalid_argument
+    return 0;
+  }
+  const M3 Rq = quaternion_matrix(q[0] / qn, q[1] / qn, q[2] / qn, q[3] / qn);
+  const float sc[3] = {pm_expf(ls[0]), pm_expf(ls[1]), pm_expf(ls[2])};
+  M3 m;
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) m.a[r][k] = Rq.a[r][k] * sc[k];
+  const M3 sigma = mul33_t(m);
+
+  // project_covariance (projection.hpp:146-158)
+  M3 Rc;
+  for (int r = 0; r < 3; ++r)
+    for (int k = 0; k < 3; ++k) Rc.a[r][k] = cam.R[r][k];
+  const M23 t = mul23_3(J, Rc);
+  const M23 tmp = mul23_3(t, sigma);
+  M2 cov = mul23_32t(tmp, t);
+  const float off = (cov.a[0][1] + cov.a[1][0]) / 2.0f;
+  const float c00 = cov.a[0][0] + s.lowpass_dilation;
+  const float c11 = cov.a[1][1] + s.lowpass_dilation;
+  const float det = c00 * c11 - off * off;
+  const bool cov_finite = isfinite(c00) && isfinite(off) && isfinite(c11);
+  if (!(det > 0.0f) || !cov_finite) return 0;  // dropped, not an error (projection.hpp:199-200)
+  const float i00 = c11 / det;
+  const float i01 = -off / det;
+  const float i11 = c00 / det;
+  const float mid = (c00 + c11) / 2.0f;
+  const float lambda_max = mid + sqrtf(std_max(0.0f, mid * mid - det));
+  const float radius = s.cutoff_sigma * sqrtf(lambda_max);
+  const float opacity = 1.0f / (1.0f + pm_expf(-raw));
+
+  // Seam instances (rasterizer.hpp:146-156) and their tile counts (:187-193).
+  uint32_t flags = kFlagVisible | (clamped ? kFlagClamped : 0u);
+  uint32_t total = 0, n_inst = 0;
+  for (int k = 0; k < 3; ++k) {
+    int span[4];
+    if (instance_tiles(mx, my, radius, k, cam.width, cam.height, s.tile_size, span)) {
+      flags |= kFlagShiftBase << k;
+      total += (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
+      ++n_inst;
+    }
+  }
+  sp_ab[2 * i] = make_float4(mx, my, i00, i01);
+  sp_ab[2 * i + 1] = make_float4(i11, opacity, col[0], col[1]);
+  sp_c[i] = make_float4(col[2], depth, radius, __uint_as_float(flags));
+  if (cov_out) cov_out[i] = make_float4(c00, off, off, c11);
+  keys[i] = __float_as_uint(depth);  // positive floats order like their bit patterns
+  cnt[i] = total;
+  *visible = true;
+  return n_inst;
+}
+
+__global__ void __launch_bounds__(256) k_preprocess(
+    int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
+    const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
+    const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
+    float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool visible = false;
+  uint32_t n_inst = 0;
+  if (i < n)
+    n_inst = preprocess_one(i, n, means, rotations, log_scales, raw_opacities, colors, cam, s, sp_ab, sp_c, cov_out,
+                            keys, vals, cnt, err, &visible);
+  const uint32_t v_sum = __reduce_add_sync(0xffffffffu, visible ? 1u : 0u);
+  const uint32_t i_sum = __reduce_add_sync(0xffffffffu, n_inst);
+  if ((threadIdx.x & 31) == 0 && (v_sum | i_sum)) {
+    atomicAdd(&err->n_visible, (unsigned long long)v_sum);
+    atomicAdd(&err->n_instances, (unsigned long long)i_sum);
+  }
+}
+
+void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
+  if (a.n == 0) return;
+  const int block = 256;
+  const int64_t grid = (a.n + block - 1) / block;
+  k_preprocess<<<(unsigned)grid, block, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
+                                                     a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
+                                                     a.vals, a.cnt, a.err);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ gather counts into rank order
+__global__ void k_gather_counts(int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt,
+                                uint32_t* __restrict__ cnt_sorted) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) cnt_sorted[r] = cnt[sorted_idx[r]];
+}
+
+void launch_gather_counts(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt, uint32_t* cnt_sorted,
+                          cudaStream_t stream) {
+  if (n == 0) return;
+  k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, sorted_idx, cnt, cnt_sorted);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ emit tile entries
+constexpr int kEmitWarps = 8;
+
+__global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
+    int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
+    const uint32_t* __restrict__ off_sorted, const float4* __restrict__ sp_ab, const float4* __restrict__ sp_c,
+    int width, int height, int tile_size, int tiles_x, uint32_t* __restrict__ out_keys,
+    uint32_t* __restrict__ out_vals, uint32_t* __restrict__ ent_off_idx) {
+  __shared__ int s_span[kEmitWarps][32][12];
+  __shared__ uint32_t s_area[kEmitWarps][32][3];
+  __shared__ uint32_t s_excl[kEmitWarps][32];
+  __shared__ uint32_t s_gid[kEmitWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = ((int64_t)blockIdx.x * kEmitWarps + warp) * 32;
+  if (base >= n) return;
+  const int64_t r = base + lane;
+  const bool valid = r < n;
+  uint32_t c = 0, gid = 0, off = 0;
+  if (valid) {
+    c = cnt_sorted[r];
+    gid = sorted_idx[r];
+    off = off_sorted[r];
+    ent_off_idx[gid] = off;
+  }
+  uint32_t areas[3] = {0, 0, 0};
+  if (c > 0) {
+    const float4 a = sp_ab[2 * (int64_t)gid];
+    const float radius = sp_c[gid].z;
+    for (int k = 0; k < 3; ++k) {
+      int span[4];
+      if (instance_tiles(a.x, a.y, radius, k, width, height, tile_size, span)) {
+        areas[k] = (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
+        for (int q = 0; q < 4; ++q) s_span[warp][lane][4 * k + q] = span[q];
+      }
+    }
+  }
+  s_area[warp][lane][0] = areas[0];
+  s_area[warp][lane][1] = areas[1];
+  s_area[warp][lane][2] = areas[2];
+  s_gid[warp][lane] = gid;
+  uint32_t incl = c;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  s_excl[warp][lane] = incl - c;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t base_off = __shfl_sync(0xffffffffu, off, 0);
+  __syncwarp();
+  for (uint32_t p = lane; p < total; p += 32) {
+    int lo = 0, hi = 31;  // largest owner with excl <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_excl[warp][mid] <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    uint32_t j = p - s_excl[warp][lo];
+    int k = 0;
+    while (j >= s_area[warp][lo][k]) {
+      j -= s_area[warp][lo][k];
+      ++k;
+    }
+    const int* span = s_span[warp][lo] + 4 * k;
+    const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
+    const int ty = span[2] + (int)(j / w), tx = span[0] + (int)(j % w);
+    out_keys[base_off + p] = (uint32_t)(ty * tiles_x + tx);
+    out_vals[base_off + p] = (s_gid[warp][lo] << 2) | (uint32_t)k;
+  }
+}
+
+void launch_emit(const EmitArgs& a, cudaStream_t stream) {
+  if (a.n == 0) return;
+  const int64_t warps = (a.n + 31) / 32;
+  const int64_t grid = (warps + kEmitWarps - 1) / kEmitWarps;
+  k_emit<<<(unsigned)grid, kEmitWarps * 32, 0, stream>>>(a.n, a.sorted_idx, a.cnt_sorted, a.off_sorted, a.sp_ab,
+                                                         a.sp_c, a.width, a.height, a.tile_size, a.tiles_x,
+                                                         a.out_keys, a.out_vals, a.ent_off_idx);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ tile ranges
+__global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ keys, uint32_t n_tiles,
+                              int32_t* __restrict__ offsets) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e > k_entries) return;
+  const uint32_t prev = e == 0 ? 0u : keys[e - 1] + 1u;  // first tile whose range starts at e
+  const uint32_t cur = e == k_entries ? n_tiles : keys[e];
+  if (e != 0 && e != k_entries && keys[e - 1] == cur) return;
+  for (uint32_t t = prev; t <= cur; ++t) offsets[t] = (int32_t)e;
+}
+
+void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, int32_t* offsets,
+                        cudaStream_t stream) {
+  if (k_entries == 0) {
+    cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), stream);
+    return;
+  }
+  const uint32_t threads = k_entries + 1;
+  k_tile_ranges<<<(threads + 255) / 256, 256, 0, stream>>>(k_entries, keys, n_tiles, offsets);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ blend
+constexpr int kBlendThreads = 256;
+
+template <int PPT>
+__global__ void __launch_bounds__(kBlendThreads) k_blend(
+    const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
+    const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
+    float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
+    int32_t* __restrict__ walked_out) {
+  __shared__ float s_cx[kBlendThreads], s_cy[kBlendThreads], s_i00[kBlendThreads], s_i01x2[kBlendThreads],
+      s_i11[kBlendThreads], s_op[kBlendThreads], s_r[kBlendThreads], s_g[kBlendThreads], s_b[kBlendThreads];
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int e0 = offsets[tile], e1 = offsets[tile + 1];
+  const int tid = threadIdx.x;
+
+  float px[PPT], py[PPT], t[PPT], cr[PPT], cg[PPT], cb[PPT];
+  int walked[PPT];
+  bool done[PPT];
+  int64_t pix[PPT];
+  const int area = tile_size * tile_size;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int lp = tid + q * kBlendThreads;
+    // Column-major pixel order inside the tile so a warp writes runs of y (the
+    // images are column-major, y + x*H).
+    const int lx = lp / tile_size, ly = lp - lx * tile_size;
+    const int x = tx * tile_size + lx, y = ty * tile_size + ly;
+    const bool valid = lp < area && x < width && y < height;
+    px[q] = (float)x + 0.5f;
+    py[q] = (float)y + 0.5f;
+    t[q] = 1.0f;
+    cr[q] = cg[q] = cb[q] = 0.0f;
+    walked[q] = e1 - e0;
+    done[q] = !valid;
+    pix[q] = valid ? (int64_t)x * height + y : -1;
+  }
+
+  const float W = (float)width;
+  for (int base = e0; base < e1; base += kBlendThreads) {
+    bool any_alive = false;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) any_alive |= !done[q];
+    if (__syncthreads_count(any_alive) == 0) break;
+    const int e = base + tid;
+    if (e < e1) {
+      const uint32_t v = vals[e];
+      const uint32_t g = v >> 2;
+      const int k = (int)(v & 3u);
+      const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+      const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+      const float c2 = __ldg(&sp_c[g].x);
+      const float shift = k == 0 ? -W : (k == 1 ? 0.0f : W);
+      s_cx[tid] = a.x + shift;
+      s_cy[tid] = a.y;
+      s_i00[tid] = a.z;
+      s_i01x2[tid] = 2.0f * a.w;
+      s_i11[tid] = b.x;
+      s_op[tid] = b.y;
+      s_r[tid] = b.z;
+      s_g[tid] = b.w;
+      s_b[tid] = c2;
+    }
+    __syncthreads();
+    const int count = min(kBlendThreads, e1 - base);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+      if (done[q]) continue;
+      float tq = t[q], r = cr[q], gg = cg[q], bb = cb[q];
+      const float x0 = px[q], y0 = py[q];
+      int j = 0;
+      for (; j < count; ++j) {
+        const float dx = x0 - s_cx[j];
+        const float dy = y0 - s_cy[j];
+        const float d2 = s_i00[j] * dx * dx + s_i01x2[j] * dx * dy + s_i11[j] * dy * dy;
+        if (d2 > cutoff2) continue;
+        const float alpha = std_min(alpha_clamp, s_op[j] * pm_expf_blend(-d2 / 2.0f));
+        const float t_next = tq * (1.0f - alpha);
+        if (t_next < transmittance_floor) {
+          walked[q] = base + j - e0;
+          done[q] = true;
+          break;
+        }
+        const float w = alpha * tq;
+        r = r + s_r[j] * w;
+        gg = gg + s_g[j] * w;
+        bb = bb + s_b[j] * w;
+        tq = t_next;
+      }
+      t[q] = tq;
+      cr[q] = r;
+      cg[q] = gg;
+      cb[q] = bb;
+    }
+    __syncthreads();
+  }
+
+  const int64_t plane = (int64_t)width * height;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    if (pix[q] < 0) continue;
+    image[pix[q]] = cr[q];
+    image[plane + pix[q]] = cg[q];
+    image[2 * plane + pix[q]] = cb[q];
+    trans_out[pix[q]] = t[q];
+    walked_out[pix[q]] = walked[q];
+  }
+}
+
+void launch_blend(const BlendArgs& a, cudaStream_t stream) {
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  if (n_tiles == 0) return;
+  const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
+  const int area = a.tile_size * a.tile_size;
+#define ODGS_BLEND(PPT)                                                                                          \
+  k_blend<PPT><<<n_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,    \
+                                                      a.tile_size, a.tiles_x, a.alpha_clamp,                    \
+                                                      a.transmittance_floor, cutoff2, a.image, a.transmittance, \
+                                                      a.walked)
+  if (area <= kBlendThreads) ODGS_BLEND(1);
+  else if (area <= 4 * kBlendThreads) ODGS_BLEND(4);
+  else ODGS_BLEND(16);
+#undef ODGS_BLEND
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ cull (rasterizer.hpp:15-28)
+__global__ void k_cull(int64_t n, const float* __restrict__ means, DevCamera cam, float near_r, float far_r,
+                       uint8_t* __restrict__ keep) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float p[3] = {means[i], means[n + i], means[2 * n + i]};
+  float mu[3];
+  to_camera(cam, p, mu);
+  const float d = sqrtf(sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]));
+  keep[i] = (d >= near_r && d <= far_r) ? 1 : 0;
+}
+
+void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, float far_r, uint8_t* keep,
+                 cudaStream_t stream) {
+  if (n == 0) return;
+  k_cull<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, means, cam, near_r, far_r, keep);
+  ++g_launches;
+}
+
+}  // namespace odgs_b200

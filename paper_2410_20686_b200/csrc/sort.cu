@@ -1,0 +1,272 @@
+// sort.cu — device-wide exclusive scan and stable LSD radix sort of (u32 key, u32 value)
+// pairs, hand-written for sm_100a (no CUB).
+//
+// Used twice per frame:
+//   * depth sort of the N projected Gaussians (key = float bits of ||mu_cam||, value =
+//     cloud index) — stability gives the reference's (depth, index) tie-break;
+//   * tile sort of the K tile entries emitted in (depth, index, shift) order (key =
+//     tile id, ceil(log2 T) bits) — stability keeps that order inside every tile, so
+//     the per-tile lists equal the reference's (rasterizer.hpp:158-205).
+//
+// Each pass = upsweep (per-tile digit histogram) + exclusive scan of the digit-major
+// histogram + downsweep (warp-level ballot ranking, block-local scatter through shared
+// memory, then coalesced-run writes). Tiles are 4096 items (256 threads x 16).
+#include "kernels.h"
+
+namespace odgs_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kIPT = 16;
+constexpr int kTile = kThreads * kIPT;  // 4096
+constexpr int kWarpItems = 32 * kIPT;   // 512
+
+__device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += u;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t warp_reduce(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// ------------------------------------------------------------------ scan
+__global__ void __launch_bounds__(kThreads) k_scan_reduce(const uint32_t* __restrict__ in, int64_t n,
+                                                          uint32_t* __restrict__ block_sums,
+                                                          unsigned long long* total64) {
+  __shared__ uint32_t s_warp[kWarps];
+  const int64_t base = (int64_t)blockIdx.x * kTile;
+  uint32_t sum = 0;
+  for (int k = threadIdx.x; k < kTile; k += kThreads) {
+    const int64_t idx = base + k;
+    if (idx < n) sum += in[idx];
+  }
+  sum = warp_reduce(sum);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_warp[warp] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    unsigned long long t64 = 0;
+    for (int w = 0; w < kWarps; ++w) {
+      t += s_warp[w];
+      t64 += s_warp[w];
+    }
+    block_sums[blockIdx.x] = t;
+    if (total64) atomicAdd(total64, t64);
+  }
+}
+
+// Scans one tile per block; block_offsets may be null (single block: adds the total).
+__global__ void __launch_bounds__(kThreads) k_scan_downsweep(const uint32_t* __restrict__ in,
+                                                             uint32_t* __restrict__ out, int64_t n,
+                                                             const uint32_t* __restrict__ block_offsets,
+                                                             unsigned long long* total64) {
+  __shared__ uint32_t s_warp[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)warp * kWarpItems;
+  uint32_t v[kIPT];
+  uint32_t wsum = 0;
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const int64_t idx = base + j * 32 + lane;
+    v[j] = idx < n ? in[idx] : 0u;
+    wsum += v[j];
+  }
+  wsum = warp_reduce(wsum);
+  if (lane == 0) s_warp[warp] = wsum;
+  __syncthreads();
+  uint32_t carry = block_offsets ? block_offsets[blockIdx.x] : 0u;
+  for (int w = 0; w < warp; ++w) carry += s_warp[w];
+  if (!block_offsets && total64 && threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kWarps; ++w) t += s_warp[w];
+    atomicAdd(total64, t);
+  }
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const uint32_t incl = warp_inclusive_scan(v[j], lane);
+    const int64_t idx = base + j * 32 + lane;
+    if (idx < n) out[idx] = carry + incl - v[j];
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// ------------------------------------------------------------------ radix sort
+__global__ void __launch_bounds__(kThreads) k_radix_upsweep(const uint32_t* __restrict__ keys, int64_t n,
+                                                            int shift, int bits, uint32_t* __restrict__ hist,
+                                                            int64_t n_blocks) {
+  __shared__ uint32_t s_cnt[kWarps][256];
+  const int warp = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kWarps * 256; k += kThreads) (&s_cnt[0][0])[k] = 0;
+  __syncthreads();
+  const uint32_t mask = (1u << bits) - 1u;
+  const int64_t base = (int64_t)blockIdx.x * kTile;
+#pragma unroll 4
+  for (int k = threadIdx.x; k < kTile; k += kThreads) {
+    const int64_t idx = base + k;
+    if (idx < n) atomicAdd(&s_cnt[warp][(keys[idx] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  const int radix = 1 << bits;
+  for (int d = threadIdx.x; d < radix; d += kThreads) {
+    uint32_t t = 0;
+    for (int w = 0; w < kWarps; ++w) t += s_cnt[w][d];
+    hist[(int64_t)d * n_blocks + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_radix_downsweep(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ hist_scanned,
+    int64_t n_blocks) {
+  __shared__ uint32_t s_keys[kTile];
+  __shared__ uint32_t s_vals[kTile];
+  __shared__ uint32_t s_wcnt[kWarps][256];
+  __shared__ uint32_t s_start[256];
+  __shared__ uint32_t s_gbase[256];
+  __shared__ uint32_t s_wsum[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int radix = 1 << bits;
+  const uint32_t mask = (uint32_t)radix - 1u;
+  for (int k = threadIdx.x; k < kWarps * 256; k += kThreads) (&s_wcnt[0][0])[k] = 0;
+  __syncthreads();
+
+  const int64_t tile_base = (int64_t)blockIdx.x * kTile;
+  const int64_t base = tile_base + (int64_t)warp * kWarpItems;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t key[kIPT], val[kIPT], rank[kIPT];
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const int64_t idx = base + j * 32 + lane;
+    const bool valid = idx < n;
+    key[j] = valid ? keys_in[idx] : 0u;
+    val[j] = valid ? vals_in[idx] : 0u;
+    // Padding sorts behind every real item of the tile: last digit, largest index.
+    const uint32_t d = valid ? (key[j] >> shift) & mask : mask;
+    uint32_t peers = 0xffffffffu;
+    for (int b = 0; b < bits; ++b) {
+      const uint32_t bit = (d >> b) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? bal : ~bal;
+    }
+    const uint32_t pre = s_wcnt[warp][d];
+    __syncwarp();
+    if ((peers & lt_mask) == 0) s_wcnt[warp][d] = pre + __popc(peers);
+    __syncwarp();
+    rank[j] = pre + __popc(peers & lt_mask);
+  }
+  __syncthreads();
+  // Per digit: exclusive over warps (in place), then exclusive over digits.
+  uint32_t digit_total = 0;
+  if (threadIdx.x < radix) {
+    const int d = threadIdx.x;
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_wcnt[w][d];
+      s_wcnt[w][d] = digit_total;
+      digit_total += c;
+    }
+  }
+  // Block exclusive scan of digit_total over threadIdx (digits), 256 threads.
+  const uint32_t incl = warp_inclusive_scan(digit_total, lane);
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  uint32_t woff = 0;
+  for (int w = 0; w < warp; ++w) woff += s_wsum[w];
+  if (threadIdx.x < radix) {
+    const uint32_t start = woff + incl - digit_total;
+    s_start[threadIdx.x] = start;
+    s_gbase[threadIdx.x] = hist_scanned[(int64_t)threadIdx.x * n_blocks + blockIdx.x] - start;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const int64_t idx = base + j * 32 + lane;
+    const uint32_t d = idx < n ? (key[j] >> shift) & mask : mask;
+    const uint32_t pos = s_start[d] + s_wcnt[warp][d] + rank[j];
+    s_keys[pos] = key[j];
+    s_vals[pos] = val[j];
+  }
+  __syncthreads();
+  const int64_t valid_count = n - tile_base < kTile ? n - tile_base : kTile;
+  for (int k = threadIdx.x; k < valid_count; k += kThreads) {
+    const uint32_t kk = s_keys[k];
+    const uint32_t d = (kk >> shift) & mask;
+    const uint32_t pos = s_gbase[d] + (uint32_t)k;
+    keys_out[pos] = kk;
+    vals_out[pos] = s_vals[k];
+  }
+}
+
+int64_t blocks_for(int64_t n) { return (n + kTile - 1) / kTile; }
+
+}  // namespace
+
+thread_local int64_t g_launches = 0;
+
+size_t scan_temp_bytes(int64_t n) {
+  if (n <= kTile) return 0;
+  const int64_t nb = blocks_for(n);
+  return (size_t)(2 * nb) * sizeof(uint32_t) + 256 + scan_temp_bytes(nb);
+}
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp, unsigned long long* total64,
+                        cudaStream_t stream) {
+  if (n <= 0) return;
+  if (n <= kTile) {
+    k_scan_downsweep<<<1, kThreads, 0, stream>>>(in, out, n, nullptr, total64);
+    ++g_launches;
+    return;
+  }
+  const int64_t nb = blocks_for(n);
+  uint32_t* sums = static_cast<uint32_t*>(temp);
+  uint32_t* offs = sums + nb;
+  void* next = reinterpret_cast<char*>(temp) + (((size_t)(2 * nb) * sizeof(uint32_t) + 255) / 256) * 256;
+  k_scan_reduce<<<(unsigned)nb, kThreads, 0, stream>>>(in, n, sums, total64);
+  ++g_launches;
+  exclusive_scan_u32(sums, offs, nb, next, nullptr, stream);
+  k_scan_downsweep<<<(unsigned)nb, kThreads, 0, stream>>>(in, out, n, offs, nullptr);
+  ++g_launches;
+}
+
+size_t radix_sort_temp_bytes(int64_t n) {
+  const int64_t nb = blocks_for(n > 0 ? n : 1);
+  const int64_t hist = 256 * nb;
+  return (size_t)(2 * hist) * sizeof(uint32_t) + 256 + scan_temp_bytes(hist);
+}
+
+void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
+                      int* which, cudaStream_t stream) {
+  int cur = 0;
+  *which = 0;
+  if (n <= 1 || end_bit <= begin_bit) return;
+  const int64_t nb = blocks_for(n);
+  uint32_t* hist = static_cast<uint32_t*>(temp);
+  uint32_t* hist_scanned = hist + 256 * nb;
+  void* scan_tmp = reinterpret_cast<char*>(temp) + (((size_t)(2 * 256 * nb) * sizeof(uint32_t) + 255) / 256) * 256;
+  int bit = begin_bit;
+  int passes = (end_bit - begin_bit + 7) / 8;
+  while (bit < end_bit) {
+    const int bits = (end_bit - bit + passes - 1) / passes;
+    --passes;
+    k_radix_upsweep<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], n, bit, bits, hist, nb);
+    ++g_launches;
+    exclusive_scan_u32(hist, hist_scanned, (int64_t)(1 << bits) * nb, scan_tmp, nullptr, stream);
+    k_radix_downsweep<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
+                                                             bit, bits, hist_scanned, nb);
+    ++g_launches;
+    cur ^= 1;
+    bit += bits;
+  }
+  *which = cur;
+}
+
+}  // namespace odgs_b200

@@ -1,0 +1,317 @@
+"""Python mirror of the reference rasterizer API over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(proj/include/odgs/{types,rasterizer,backward}.hpp):
+
+    render(cloud, camera, settings)            rasterizer.hpp:211-214
+    prepare_render(cloud, camera, settings)    rasterizer.hpp:129-132
+    backward(cloud, camera, fwd, dl_dimage, settings, signs=None)   backward.hpp:380-386
+    cull(cloud, camera, near, far)             rasterizer.hpp:15-18
+
+Exceptions: InvalidArgument (std::invalid_argument), OdgsRuntimeError
+(std::runtime_error), DomainError (std::domain_error); `.index` carries the
+offending Gaussian row where the reference names one.
+
+Arrays use the reference's storage: cloud members SoA with shape (3, n)/(4, n)/(n,)
+(Eigen column-major MatX3 .data()), images (3, W, H) i.e. planar channels each
+column-major (ErpImage storage). Host inputs are numpy float32; device inputs are
+torch CUDA float32 tensors (no copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _capi as capi
+
+
+class OdgsError(Exception):
+    def __init__(self, message: str, index: int = -1):
+        super().__init__(message)
+        self.index = index
+
+
+class InvalidArgument(OdgsError, ValueError):
+    pass
+
+
+class OdgsRuntimeError(OdgsError, RuntimeError):
+    pass
+
+
+class DomainError(OdgsError, ArithmeticError):
+    pass
+
+
+_EXC = {capi.STATUS_INVALID_ARGUMENT: InvalidArgument, capi.STATUS_RUNTIME: OdgsRuntimeError,
+        capi.STATUS_DOMAIN: DomainError}
+
+
+@dataclass
+class RenderSettings:  # types.hpp:229-255
+    near_radius: float = 0.01
+    far_radius: float = 1000.0
+    tile_size: int = 16
+    alpha_clamp: float = 0.99
+    transmittance_floor: float = 1e-4
+    cutoff_sigma: float = 3.0
+    lowpass_dilation: float = 0.3
+    max_elevation: float = float(np.float32(85.0) * np.float32(math.pi) / np.float32(180.0))
+    threads: int = 0
+
+    def to_c(self) -> capi.Settings:
+        return capi.Settings(self.near_radius, self.far_radius, self.tile_size, self.alpha_clamp,
+                             self.transmittance_floor, self.cutoff_sigma, self.lowpass_dilation,
+                             self.max_elevation, self.threads)
+
+
+@dataclass
+class CameraPose:  # types.hpp:148-180
+    width: int
+    height: int
+    rotation: np.ndarray = field(default_factory=lambda: np.eye(3))
+    translation: np.ndarray = field(default_factory=lambda: np.zeros(3))
+
+    def to_c(self) -> capi.Camera:
+        c = capi.Camera()
+        r = np.asarray(self.rotation, dtype=np.float32).reshape(3, 3)
+        t = np.asarray(self.translation, dtype=np.float32).reshape(3)
+        for k in range(9):
+            c.rotation[k] = float(r.flat[k])
+        for k in range(3):
+            c.translation[k] = float(t[k])
+        c.width = int(self.width)
+        c.height = int(self.height)
+        return c
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+@dataclass
+class GaussianCloud:  # types.hpp:53-143
+    means: object          # (3, n)
+    rotations: object      # (4, n)  (w, x, y, z), unnormalised
+    log_scales: object     # (3, n)
+    raw_opacities: object  # (n,)
+    colors: object         # (3, n)
+
+    @property
+    def n(self) -> int:
+        return int(self.raw_opacities.shape[0])
+
+    @property
+    def on_device(self) -> bool:
+        return _is_torch(self.means) and self.means.is_cuda
+
+    @staticmethod
+    def from_numpy(means, rotations, log_scales, raw_opacities, colors) -> "GaussianCloud":
+        f = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+        return GaussianCloud(f(means), f(rotations), f(log_scales), f(raw_opacities), f(colors))
+
+    def to_c(self) -> capi.Cloud:
+        arrs = (self.means, self.rotations, self.log_scales, self.raw_opacities, self.colors)
+        if self.on_device:
+            for a in arrs:
+                if not (a.is_contiguous() and str(a.dtype) == "torch.float32"):
+                    raise InvalidArgument("cloud tensors must be contiguous float32")
+            ptrs = [a.data_ptr() for a in arrs]
+            mem = capi.MEM_DEVICE
+        elif _is_torch(self.means):
+            ptrs = [a.data_ptr() for a in arrs]
+            mem = capi.MEM_HOST
+        else:
+            for a in arrs:
+                if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
+                    raise InvalidArgument("cloud arrays must be C-contiguous float32")
+            ptrs = [a.ctypes.data for a in arrs]
+            mem = capi.MEM_HOST
+        return capi.Cloud(self.n, *ptrs, mem)
+
+
+class Context:
+    """One CUDA device + stream (odgs_ctx). Not thread-safe; one per host thread."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None):
+        self.lib = capi.load_library()
+        h = C.c_void_p()
+        st = self.lib.odgs_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h))
+        if st != 0:
+            raise OdgsError(f"odgs_ctx_create failed with status {st}")
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            self.lib.odgs_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, status: int):
+        if status == capi.STATUS_OK:
+            return
+        idx = C.c_int64(-1)
+        msg = C.create_string_buffer(512)
+        self.lib.odgs_last_error(self.handle, C.byref(idx), msg, 512)
+        raise _EXC.get(status, OdgsError)(msg.value.decode(), idx.value)
+
+    def synchronize(self):
+        self.check(self.lib.odgs_synchronize(self.handle))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.odgs_ctx_launch_count(self.handle))
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.odgs_ctx_stream(self.handle) or 0)
+
+
+class RenderOutput:
+    """A rendered frame (RenderOutput, rasterizer.hpp:92-102); fields download on access."""
+
+    def __init__(self, ctx: Context, flags: int = 0):
+        self.ctx = ctx
+        h = C.c_void_p()
+        ctx.check(ctx.lib.odgs_frame_create(ctx.handle, C.byref(h)))
+        self.handle = h
+        if flags:
+            ctx.lib.odgs_frame_set_flags(h, flags)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.ctx.lib.odgs_frame_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def info(self) -> capi.FrameInfo:
+        i = capi.FrameInfo()
+        self.ctx.lib.odgs_frame_get_info(self.handle, C.byref(i))
+        return i
+
+    def _download(self, fld: int, dtype, shape) -> np.ndarray:
+        out = np.empty(shape, dtype=dtype)
+        self.ctx.check(self.ctx.lib.odgs_frame_download(self.ctx.handle, self.handle, fld,
+                                                        out.ctypes.data, out.nbytes))
+        return out
+
+    def device_ptr(self, fld: int) -> int:
+        p = C.c_void_p()
+        self.ctx.check(self.ctx.lib.odgs_frame_device_ptr(self.handle, fld, C.byref(p)))
+        return int(p.value)
+
+    @property
+    def image(self) -> np.ndarray:  # (3, W, H)
+        i = self.info()
+        return self._download(capi.FRAME_IMAGE, np.float32, (3, i.width, i.height))
+
+    @property
+    def transmittance(self) -> np.ndarray:  # (W, H)
+        i = self.info()
+        return self._download(capi.FRAME_TRANSMITTANCE, np.float32, (i.width, i.height))
+
+    @property
+    def walked(self) -> np.ndarray:  # (W, H)
+        i = self.info()
+        return self._download(capi.FRAME_WALKED, np.int32, (i.width, i.height))
+
+    @property
+    def tile_offsets(self) -> np.ndarray:
+        i = self.info()
+        return self._download(capi.FRAME_TILE_OFFSETS, np.int32, (i.tiles_x * i.tiles_y + 1,))
+
+    @property
+    def tile_entries(self) -> np.ndarray:
+        return self._download(capi.FRAME_TILE_ENTRIES, np.int32, (self.info().n_entries,))
+
+    @property
+    def instance_splat(self) -> np.ndarray:
+        return self._download(capi.FRAME_INSTANCE_SPLAT, np.int32, (self.info().n_instances,))
+
+    @property
+    def instance_shift(self) -> np.ndarray:
+        return self._download(capi.FRAME_INSTANCE_SHIFT, np.float32, (self.info().n_instances,))
+
+    def splat_field(self, fld: int, width: int = 1, dtype=np.float32) -> np.ndarray:
+        ns = self.info().n_splats
+        shape = (ns,) if width == 1 else (ns, width)
+        return self._download(fld, dtype, shape)
+
+
+@dataclass
+class GradBuffers:  # backward.hpp:342-374
+    means: np.ndarray
+    rotations: np.ndarray
+    log_scales: np.ndarray
+    raw_opacities: np.ndarray
+    colors: np.ndarray
+    pixel_grad_norm: np.ndarray
+    one_minus_cos: np.ndarray
+    observed: np.ndarray
+
+    @staticmethod
+    def zeros(n: int) -> "GradBuffers":
+        z = lambda *s: np.zeros(s, np.float32)
+        return GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n), np.zeros(n, np.int32))
+
+    def to_c(self) -> capi.Grads:
+        arrs = (self.means, self.rotations, self.log_scales, self.raw_opacities, self.colors,
+                self.pixel_grad_norm, self.one_minus_cos, self.observed)
+        if _is_torch(self.means) and self.means.is_cuda:
+            return capi.Grads(*[a.data_ptr() for a in arrs], capi.MEM_DEVICE)
+        return capi.Grads(*[a.ctypes.data for a in arrs], capi.MEM_HOST)
+
+
+def prepare_render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings,
+                   out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
+    out = out or RenderOutput(ctx, flags)
+    cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
+    ctx.check(ctx.lib.odgs_prepare_render(ctx.handle, C.byref(cc), C.byref(cam), C.byref(st), out.handle))
+    return out
+
+
+def render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings,
+           out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
+    out = out or RenderOutput(ctx, flags)
+    cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
+    ctx.check(ctx.lib.odgs_render(ctx.handle, C.byref(cc), C.byref(cam), C.byref(st), out.handle))
+    return out
+
+
+def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: RenderOutput, dl_dimage,
+             settings: RenderSettings, signs=None, grads: Optional[GradBuffers] = None,
+             accumulate: bool = False) -> GradBuffers:
+    grads = grads or GradBuffers.zeros(cloud.n)
+    cc, cam, st, gc = cloud.to_c(), camera.to_c(), settings.to_c(), grads.to_c()
+    if _is_torch(dl_dimage):
+        dptr, dmem = dl_dimage.data_ptr(), (capi.MEM_DEVICE if dl_dimage.is_cuda else capi.MEM_HOST)
+    else:
+        dl_dimage = np.ascontiguousarray(dl_dimage, dtype=np.float32)
+        dptr, dmem = dl_dimage.ctypes.data, capi.MEM_HOST
+    sp = None
+    if signs is not None:
+        sp = (C.c_double * 12)(*[float(s) for s in signs])
+    ctx.check(ctx.lib.odgs_backward(ctx.handle, C.byref(cc), C.byref(cam), fwd.handle, C.c_void_p(dptr), dmem,
+                                    C.byref(st), C.byref(gc), sp, capi.ACCUMULATE if accumulate else 0))
+    return grads
+
+
+def cull(ctx: Context, cloud: GaussianCloud, camera: CameraPose, near: float, far: float) -> np.ndarray:
+    out = np.empty(max(cloud.n, 1), np.int64)
+    count = C.c_int64(0)
+    cc, cam = cloud.to_c(), camera.to_c()
+    ctx.check(ctx.lib.odgs_cull(ctx.handle, C.byref(cc), C.byref(cam), near, far,
+                                out.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(count)))
+    return out[: count.value].copy()

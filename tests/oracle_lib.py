@@ -1,0 +1,132 @@
+"""ctypes access to the CPU oracle (oracle/libodgs_oracle.so) — test infrastructure only.
+
+The oracle is the Eigen-free restatement of the reference hot path
+(oracle/odgs_oracle.hpp); it is built from the repo's own sources with
+oracle/Makefile, here and on the GPU box.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+ORACLE_DIR = ROOT / "oracle"
+LIB = ORACLE_DIR / "_build" / "libodgs_oracle.so"
+REF_TESTS = ORACLE_DIR / "_build" / "ref_tests"
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-C", str(ORACLE_DIR), "-j4", str(LIB), str(REF_TESTS)], check=True,
+                   stdout=subprocess.DEVNULL)
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(str(LIB))
+        dp = C.POINTER(C.c_double)
+        L.oracle_render.restype = C.c_int
+        L.oracle_render.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, dp, dp, dp, dp, dp, dp, dp, C.c_int,
+                                    C.c_int, dp, C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]
+        L.oracle_backward.restype = C.c_int
+        L.oracle_backward.argtypes = [C.c_void_p, dp, C.c_int, C.c_char_p, C.c_int]
+        L.oracle_get.restype = C.c_int64
+        L.oracle_get.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        L.oracle_free.argtypes = [C.c_void_p]
+        L.oracle_random_cloud.argtypes = [C.c_uint32, C.c_int, dp, C.c_int, dp, dp, dp, dp, dp]
+        L.oracle_photometric_loss.restype = C.c_double
+        L.oracle_photometric_loss.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, dp]
+        L.oracle_hardware_concurrency.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ------------------------------------------------------------------ scenes (mt19937, scenes.hpp)
+DEFAULT_BOUNDS = (0.5, 20.0, 1.45, 0.05, 0.95, 0.005, 0.05)
+
+
+def random_cloud(seed: int, n: int, bounds=DEFAULT_BOUNDS, as_float: bool = True):
+    """scenes::random_cloud<float|double>(std::mt19937(seed), n, bounds) as float64 arrays."""
+    b = np.asarray(bounds, dtype=np.float64)
+    means, rot, ls = np.zeros((3, n)), np.zeros((4, n)), np.zeros((3, n))
+    op, col = np.zeros(n), np.zeros((3, n))
+    lib().oracle_random_cloud(seed, n, _dp(b), int(as_float), _dp(means), _dp(rot), _dp(ls), _dp(op), _dp(col))
+    return means, rot, ls, op, col
+
+
+# ------------------------------------------------------------------ render / backward
+@dataclass
+class OracleSettings:
+    near: float = 0.01
+    far: float = 1000.0
+    tile: int = 16
+    alpha_clamp: float = 0.99
+    floor: float = 1e-4
+    cutoff: float = 3.0
+    lowpass: float = 0.3
+    max_elevation: float = float(np.float32(85.0) * np.float32(np.pi) / np.float32(180.0))
+
+    def array(self):
+        return np.array([self.near, self.far, self.tile, self.alpha_clamp, self.floor, self.cutoff,
+                         self.lowpass, self.max_elevation], dtype=np.float64)
+
+
+class OracleError(Exception):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class OracleFrame:
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if self.h:
+            lib().oracle_free(self.h)
+            self.h = None
+
+    def get(self, which: str):
+        L = lib()
+        n = L.oracle_get(self.h, which.encode(), None)
+        if n < 0:
+            raise KeyError(which)
+        dtype = {"walked": np.int32, "tile_offsets": np.int32, "tile_entries": np.int32, "inst_splat": np.int32,
+                 "splat_index": np.int64, "splat_clamped": np.int32, "stats": np.int64,
+                 "g_observed": np.int32}.get(which, np.float64)
+        out = np.empty(n, dtype=dtype)
+        L.oracle_get(self.h, which.encode(), out.ctypes.data)
+        return out
+
+    def backward(self, dl_dimage: np.ndarray, mutate_term: int = -1):
+        g = np.ascontiguousarray(dl_dimage, dtype=np.float64).ravel()
+        err = C.create_string_buffer(512)
+        rc = lib().oracle_backward(self.h, _dp(g), mutate_term, err, 512)
+        if rc != 0:
+            raise OracleError(rc, err.value.decode())
+
+
+def render(cloud, R, t, width, height, settings: OracleSettings = OracleSettings(), dbl=False, portable=False,
+           brute=False, threads=0) -> OracleFrame:
+    means, rot, ls, op, col = [np.ascontiguousarray(a, dtype=np.float64) for a in cloud]
+    R = np.ascontiguousarray(R, dtype=np.float64).reshape(9)
+    t = np.ascontiguousarray(t, dtype=np.float64).reshape(3)
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    rc = lib().oracle_render(int(dbl), int(portable), int(brute), op.shape[0], _dp(means), _dp(rot), _dp(ls),
+                             _dp(op), _dp(col), _dp(R), _dp(t), width, height, _dp(settings.array()), threads,
+                             C.byref(h), err, 512)
+    if rc != 0:
+        raise OracleError(rc, err.value.decode())
+    return OracleFrame(h)

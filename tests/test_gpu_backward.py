@@ -1,0 +1,163 @@
+"""GPU backward parity: gradients through the C ABI vs the fp64 CPU oracle.
+
+Contract (BASELINE north_star): every parameter group within
+group-relative 1e-3 using the reference's own metric (test_backward.cpp:488-504):
+max|g - o| / max(max|g|, max|o|, 1e-12). Cases follow proj/tests/test_backward.cpp.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle_lib
+from helpers import angle_axis, settings_pair, to_cloud32
+from paper_2410_20686_b200 import CameraPose, DomainError, GradBuffers, backward, render
+from paper_2410_20686_b200 import _capi as capi
+
+pytestmark = pytest.mark.gpu
+
+FD_BOUNDS = (0.8, 10.0, 75.0 * math.pi / 180.0, 0.1, 0.7, 0.02, 0.12)  # test_backward.cpp:53-63
+GROUPS = ["means", "rotations", "log_scales", "raw_opacities", "colors"]
+
+
+def group_rel(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return np.abs(a - b).max() / max(np.abs(a).max(), np.abs(b).max(), 1e-12)
+
+
+def probe(seed, W, H):
+    return np.random.default_rng(seed).uniform(-1, 1, (3, W, H)).astype(np.float32)
+
+
+def run_both(ctx, arrs, cam, gs, os_, dl, signs=None):
+    cloud = to_cloud32(arrs)
+    fr = render(ctx, cloud, cam, gs)
+    g = backward(ctx, cloud, cam, fr, dl, gs, signs=signs)
+    of = oracle_lib.render(arrs, cam.rotation, cam.translation, cam.width, cam.height, os_, dbl=True)
+    of.backward(dl.astype(np.float64))
+    n = arrs[3].shape[0]
+    o = {"means": of.get("g_means").reshape(3, n), "rotations": of.get("g_rotations").reshape(4, n),
+         "log_scales": of.get("g_log_scales").reshape(3, n), "raw_opacities": of.get("g_raw_opacities"),
+         "colors": of.get("g_colors").reshape(3, n), "pixel_grad_norm": of.get("g_pixel_grad_norm"),
+         "one_minus_cos": of.get("g_one_minus_cos"), "observed": of.get("g_observed")}
+    return g, o, fr, of
+
+
+CASES = [
+    ("fd_scene_64x32", lambda: oracle_lib.random_cloud(137, 8, FD_BOUNDS), CameraPose(64, 32), {"cutoff_sigma": 8.0}),
+    ("fd_scene_pitched", lambda: oracle_lib.random_cloud(138, 10, FD_BOUNDS),
+     CameraPose(64, 32, angle_axis(0.8, [1, 2, 3]), [0.1, -0.2, 0.15]), {"cutoff_sigma": 8.0}),
+    ("dense_512x256", lambda: oracle_lib.random_cloud(139, 3000), CameraPose(512, 256), {}),
+    ("poles_seam_1024", lambda: oracle_lib.random_cloud(140, 5000, (0.5, 20.0, 1.55, 0.05, 0.95, 0.001, 0.01)),
+     CameraPose(1024, 512), {}),
+]
+
+
+@pytest.mark.parametrize("name,make,cam,kw", CASES, ids=[c[0] for c in CASES])
+def test_gradients_match_fp64_oracle(gpu_ctx, name, make, cam, kw):
+    arrs = make()
+    gs, os_ = settings_pair(**kw)
+    dl = probe(7, cam.width, cam.height)
+    g, o, _, _ = run_both(gpu_ctx, arrs, cam, gs, os_, dl)
+    for k in GROUPS:
+        err = group_rel(getattr(g, k), o[k])
+        assert err < 1e-3, (k, err)
+    assert np.array_equal(g.observed, o["observed"])
+    assert group_rel(g.one_minus_cos, o["one_minus_cos"]) < 1e-5
+    assert group_rel(g.pixel_grad_norm, o["pixel_grad_norm"]) < 1e-3
+
+
+def test_splat_grads_match_oracle(gpu_ctx):
+    arrs = oracle_lib.random_cloud(127, 5, FD_BOUNDS)
+    cam = CameraPose(64, 32)
+    gs, os_ = settings_pair(cutoff_sigma=8.0)
+    dl = probe(3, 64, 32)
+    g, o, fr, of = run_both(gpu_ctx, arrs, cam, gs, os_, dl)
+    pairs = [(capi.FRAME_SPLATGRAD_MEAN, 2, "sg_mean"), (capi.FRAME_SPLATGRAD_COV2D, 4, "sg_cov2d"),
+             (capi.FRAME_SPLATGRAD_OPACITY, 1, "sg_opacity"), (capi.FRAME_SPLATGRAD_COLOR, 3, "sg_color")]
+    for fld, w, key in pairs:
+        a = fr.splat_field(fld, w)
+        b = of.get(key).reshape(a.shape)
+        assert group_rel(a, b) < 1e-4, key
+
+
+def test_zero_image_gradient_gives_zero(gpu_ctx):
+    arrs = oracle_lib.random_cloud(131, 6, FD_BOUNDS)
+    cam = CameraPose(64, 32)
+    gs, _ = settings_pair(cutoff_sigma=8.0)
+    cloud = to_cloud32(arrs)
+    fr = render(gpu_ctx, cloud, cam, gs)
+    g = backward(gpu_ctx, cloud, cam, fr, np.zeros((3, 64, 32), np.float32), gs)
+    for k in GROUPS:
+        assert np.all(getattr(g, k) == 0), k
+
+
+def test_gradients_add_over_views_and_are_deterministic(gpu_ctx):
+    """test_backward.cpp:536-556 (GradBuffers::accumulate) + run-to-run bitwise determinism."""
+    arrs = oracle_lib.random_cloud(139, 2000)
+    cloud = to_cloud32(arrs)
+    gs, _ = settings_pair()
+    cam_a = CameraPose(512, 256)
+    cam_b = CameraPose(512, 256, np.eye(3), [0.1, 0.0, -0.2])
+    dl = probe(11, 512, 256)
+    fa = render(gpu_ctx, cloud, cam_a, gs)
+    ga = backward(gpu_ctx, cloud, cam_a, fa, dl, gs)
+    ga2 = backward(gpu_ctx, cloud, cam_a, fa, dl, gs)
+    for k in GROUPS:
+        assert np.array_equal(getattr(ga, k), getattr(ga2, k)), k
+    fb = render(gpu_ctx, cloud, cam_b, gs)
+    gb = backward(gpu_ctx, cloud, cam_b, fb, dl, gs)
+    acc = backward(gpu_ctx, cloud, cam_a, fa, dl, gs)
+    acc = backward(gpu_ctx, cloud, cam_b, fb, dl, gs, grads=acc, accumulate=True)
+    for k in GROUPS:
+        assert np.array_equal(getattr(acc, k), getattr(ga, k) + getattr(gb, k)), k
+    assert acc.observed.max() <= 2
+
+
+def test_every_grad_t_sign_flip_is_caught(gpu_ctx):
+    """acceptance.cpp:196-217: each of the 12 GradTSigns mutations breaks parity."""
+    arrs = oracle_lib.random_cloud(141, 10, FD_BOUNDS)
+    cam = CameraPose(64, 32, angle_axis(0.8, [1, 2, 3]), [0.1, -0.2, 0.15])
+    gs, os_ = settings_pair(cutoff_sigma=8.0)
+    dl = probe(5, 64, 32)
+    caught = 0
+    for term in range(12):
+        signs = [1.0] * 12
+        signs[term] = -1.0
+        g, o, _, _ = run_both(gpu_ctx, arrs, cam, gs, os_, dl, signs=signs)
+        worst = max(group_rel(getattr(g, k), o[k]) for k in ("means", "rotations", "log_scales"))
+        caught += worst > 1e-3
+    assert caught == 12
+
+
+def test_pole_axis_is_a_domain_error(gpu_ctx):
+    """backward.hpp:79-80: the position gradient is undefined on the pole axis."""
+    arrs = [np.array(a) for a in oracle_lib.random_cloud(142, 3, FD_BOUNDS)]
+    arrs[0][:, 1] = [0.0, -2.0, 0.0]
+    cloud = to_cloud32(arrs)
+    cam = CameraPose(64, 32)
+    gs, _ = settings_pair()
+    fr = render(gpu_ctx, cloud, cam, gs)
+    with pytest.raises(DomainError) as e:
+        backward(gpu_ctx, cloud, cam, fr, probe(1, 64, 32), gs)
+    assert e.value.index == 1
+
+
+def test_device_gradient_buffers(gpu_ctx):
+    import torch
+    arrs = oracle_lib.random_cloud(143, 1500)
+    cloud = to_cloud32(arrs)
+    cam = CameraPose(256, 128)
+    gs, _ = settings_pair()
+    dl = probe(2, 256, 128)
+    fr = render(gpu_ctx, cloud, cam, gs)
+    host = backward(gpu_ctx, cloud, cam, fr, dl, gs)
+    n = cloud.n
+    z = lambda *s: torch.zeros(s, dtype=torch.float32, device="cuda")
+    dev = GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n),
+                      torch.zeros(n, dtype=torch.int32, device="cuda"))
+    backward(gpu_ctx, cloud, cam, fr, torch.from_numpy(dl).cuda(), gs, grads=dev)
+    torch.cuda.synchronize()
+    for k in GROUPS:
+        assert np.array_equal(getattr(dev, k).cpu().numpy(), getattr(host, k)), k
