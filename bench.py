@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ODGS rasterizer (BASELINE.json metric: ERP frames/sec for 1M
+Gaussians at 2048x1024).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one forward render (preprocess -> depth sort -> emit -> tile sort -> tile
+ranges -> blend) of the C3 workload — 1M synthetic Gaussians, 50% uniform, 25% near the
+poles, 25% on the azimuth seam — into a 2048x1024 ERP frame, from a camera yawed by a
+different angle every step. With N > 1 (torchrun, one process per GPU) every rank
+renders its own views (weak scaling; the render path has no exchange step, so there
+is no collective in it). Rank 0 prints one JSON line.
+
+--impl reference times the reference algorithm's CPU implementation (the oracle
+restatement, oracle/odgs_oracle.hpp, StdMath float — the reference itself cannot be
+built in this image) on the host's cores, one full C3 frame per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ERP frames/sec (1M Gaussians, 2048×1024)"
+UNIT = "frames/s"
+W_IMG, H_IMG = 2048, 1024
+N_GAUSS = 1_000_000
+WORKLOAD = ("C3: 1M synthetic Gaussians (50% uniform, 25% poles |elev| 75-89.5 deg, 25% azimuth seam), "
+            "SH0, 2048x1024 ERP, camera yawed per step")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cloud_arrays():
+    from paper_2410_20686_b200 import scenes
+    c = scenes.cloud_c3(N_GAUSS)
+    return [c.means, c.rotations, c.log_scales, c.raw_opacities, c.colors]
+
+
+def camera(step: int, rank: int):
+    from paper_2410_20686_b200 import scenes
+    yaw = 2 * math.pi * ((rank * 7919 + step) % 64) / 64.0
+    return scenes.yaw_camera(yaw, W_IMG, H_IMG)
+
+
+# ------------------------------------------------------------------ CPU reference arm
+def cpu_frames(arrs, max_frames: int, min_seconds: float):
+    """Renders full C3 frames with the oracle (StdMath float, all host threads)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import numpy as np
+    import oracle_lib  # the CPU restatement (only the baseline leg may run it)
+    a64 = [np.asarray(a, dtype=np.float64) for a in arrs]
+    cores = oracle_lib.lib().oracle_hardware_concurrency()
+    times = []
+    t_all = time.perf_counter()
+    for k in range(max_frames):
+        cam = camera(k, 0)
+        t0 = time.perf_counter()
+        oracle_lib.render(a64, cam.rotation, cam.translation, W_IMG, H_IMG, oracle_lib.OracleSettings())
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all >= min_seconds:
+            break
+    return times, cores
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return
+    arrs = cloud_arrays()
+    cpu_frames(arrs, max_frames=max(args.warmup, 0), min_seconds=0.0) if args.warmup > 0 else None
+    times, cores = cpu_frames(arrs, max_frames=args.steps, min_seconds=float("inf"))
+    total = sum(times)
+    value = len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_gaussians": N_GAUSS, "width": W_IMG, "height": H_IMG},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{len(times)} full C3 frames, oracle restatement (StdMath float), "
+                                   f"threads = all {cores} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import ctypes as C
+
+    from paper_2410_20686_b200 import Context, GaussianCloud, RenderOutput, RenderSettings, render
+    from paper_2410_20686_b200 import _capi as capi
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(local_rank, stream=stream.cuda_stream)
+    settings = RenderSettings()
+    arrs = cloud_arrays()
+    dcloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs])
+    frame = RenderOutput(ctx)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    for k in range(args.warmup):
+        render(ctx, dcloud, camera(k, rank), settings, out=frame)
+    torch.cuda.synchronize()
+
+    # Timed region: K renders, L2 flushed between steps (outside the step events).
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    work = []
+    ctx.set_profiling(True)
+    ctx.reset_stage_times()
+    launches0 = ctx.launch_count
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        for k in range(args.steps):
+            flush.zero_()
+            starts[k].record(stream)
+            render(ctx, dcloud, camera(k, rank), settings, out=frame)
+            ends[k].record(stream)
+            work.append(frame.work())
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launch_count - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    stages = ctx.stage_times()
+    ctx.set_profiling(False)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_total_ms = float(t.item())
+    value = world * args.steps / (max_total_ms / 1000.0)
+
+    # Roofline of the dominant stage.
+    hbm_peak, hbm_src = peaks()
+    fp32_peak = ctx.measure_fp32_tflops()
+    e_exam = sum(w[0] for w in work) / len(work)
+    e_contrib = sum(w[1] for w in work) / len(work)
+    info = frame.info()
+    K = info.n_entries
+    stage_ms = {k: v[0] / max(v[1], 1) for k, v in stages.items() if v[1] > 0}
+    dominant = max(stage_ms, key=stage_ms.get)
+    # Algorithmic work per unit: blend 11 flops per examined entry
+    # + 12 per composited entry; preprocess 104 B per Gaussian;
+    # sorts 20 B per item per 8-bit pass.
+    blend_flops = 11 * e_exam + 12 * e_contrib
+    depth_passes = 4
+    tile_bits = math.ceil(math.log2(info.tiles_x * info.tiles_y))
+    tile_passes = math.ceil(tile_bits / 8)
+    bytes_by_stage = {
+        "preprocess": 104.0 * N_GAUSS,
+        "depth_sort": 20.0 * N_GAUSS * depth_passes,
+        "tile_sort": 20.0 * K * tile_passes,
+        "emit": 8.0 * K + 44.0 * N_GAUSS,
+    }
+    stage_roof = {}
+    for k, b in bytes_by_stage.items():
+        if k in stage_ms:
+            gbs = b / (stage_ms[k] * 1e-3) / 1e9
+            stage_roof[k] = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": gbs / hbm_peak, "ms": stage_ms[k]}
+    if "blend" in stage_ms:
+        tf = blend_flops / (stage_ms["blend"] * 1e-3) / 1e12
+        stage_roof["blend"] = {"bound": "fp32", "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                               "frac": tf / fp32_peak, "ms": stage_ms["blend"]}
+    roof = dict(stage_roof[dominant]) if dominant in stage_roof else {"bound": "unknown"}
+    roof["kernel"] = dominant
+    roof["traffic"] = None
+    roof["peak_source"] = (hbm_src if roof.get("unit") == "GB/s"
+                           else "measured FP32 FMA microbenchmark (odgs_measure_fp32_tflops), same run")
+
+    # End to end through the C ABI with host buffers: pinned cloud -> H2D inside
+    # odgs_render, image D2H into pinned memory, every step.
+    hcloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in arrs])
+    himg = torch.empty(3 * W_IMG * H_IMG, dtype=torch.float32).pin_memory()
+    h2d = sum(int(np.asarray(a).nbytes) for a in arrs)
+    d2h = himg.numel() * 4
+    e2e_frame = RenderOutput(ctx)
+
+    def e2e_step(k):
+        render(ctx, hcloud, camera(k, rank), settings, out=e2e_frame)
+        ctx.check(ctx.lib.odgs_frame_download(ctx.handle, e2e_frame.handle, capi.FRAME_IMAGE,
+                                              C.c_void_p(himg.data_ptr()), d2h))
+
+    for k in range(max(args.warmup, 1)):
+        e2e_step(k)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        e2e_step(k)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * args.steps / float(te.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        times, cores = cpu_frames(arrs, max_frames=5, min_seconds=10.0)
+        cpu = {"value": len(times) / sum(times), "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{len(times)} full C3 frame(s) (1M Gaussians, 2048x1024), oracle restatement "
+                         f"(StdMath float), threads = all {cores} host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_gaussians": N_GAUSS, "width": W_IMG, "height": H_IMG,
+                       "tile_entries": K, "entries_examined": e_exam, "entries_composited": e_contrib,
+                       "l2": "flushed between steps (256 MiB write, outside the step events)",
+                       "parallelism": f"view-replicas x{world}"},
+            "roofline": roof,
+            "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "stage_rooflines": stage_roof,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    frame.destroy()
+    e2e_frame.destroy()
+    ctx.close()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,31 @@ odgs_status odgs_last_error(const odgs_ctx* ctx, int64_t* gaussian_index, char* 
 /* Number of kernels this context has launched since creation. */
 int64_t odgs_ctx_launch_count(const odgs_ctx* ctx);
 
+/* ------------------------------------------------------------------ profiling
+   Per-stage CUDA-event timers on the context's stream (the stream every kernel is
+   launched on). Enabling adds one event pair per stage per call and a stream
+   synchronisation at the end of each profiled call. */
+typedef enum {
+  ODGS_STAGE_PREPROCESS = 0, /* k_preprocess                       */
+  ODGS_STAGE_DEPTH_SORT = 1, /* radix sort of the Gaussians by depth */
+  ODGS_STAGE_SCAN = 2,       /* gather counts + exclusive scan     */
+  ODGS_STAGE_EMIT = 3,       /* k_emit tile entries                */
+  ODGS_STAGE_TILE_SORT = 4,  /* radix sort of the entries by tile  */
+  ODGS_STAGE_RANGES = 5,     /* tile CSR offsets                   */
+  ODGS_STAGE_BLEND = 6,      /* k_blend                            */
+  ODGS_STAGE_BWD_RASTER = 7, /* k_bwd_raster (+ record clear)      */
+  ODGS_STAGE_BWD_SPLAT = 8,  /* k_bwd_splat                        */
+  ODGS_STAGE_COUNT = 9
+} odgs_stage;
+odgs_status odgs_ctx_set_profiling(odgs_ctx* ctx, int enable);
+/* Accumulated milliseconds and call counts per stage since the last reset; returns
+   the number of stages written (<= max_stages). */
+int odgs_ctx_stage_times(odgs_ctx* ctx, double* ms, int64_t* calls, int max_stages);
+void odgs_ctx_reset_stage_times(odgs_ctx* ctx);
+const char* odgs_stage_name(int stage);
+/* Measured FP32 FMA throughput of the device (TFLOP/s, 2 flops per FMA). */
+odgs_status odgs_measure_fp32_tflops(odgs_ctx* ctx, double* tflops);
+
 /* ------------------------------------------------------------------ frames */
 odgs_status odgs_frame_create(odgs_ctx* ctx, odgs_frame** out);
 void odgs_frame_destroy(odgs_frame* frame);
@@ -158,6 +183,11 @@ odgs_status odgs_frame_set_flags(odgs_frame* frame, uint32_t flags);
 odgs_status odgs_frame_get_info(const odgs_frame* frame, odgs_frame_info* info);
 /* Copies a field to host memory (bytes must be >= the field's size). Synchronizes. */
 odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, void* host_dst, size_t bytes);
+/* Blend work of the last render into `frame` (for rooflines): pixel-entry
+   evaluations examined (sum over pixels of walked, +1 when the walk stopped early)
+   and entries composited. Synchronizes. */
+odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_examined,
+                            int64_t* entries_composited);
 /* Device pointer of a resident field (IMAGE, TRANSMITTANCE, WALKED, TILE_OFFSETS). */
 odgs_status odgs_frame_device_ptr(odgs_frame* frame, int field, void** device_ptr);
 

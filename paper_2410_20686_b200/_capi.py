@@ -80,11 +80,17 @@ SIGNATURES = {
     "odgs_frame_set_flags": (C.c_int, [_P, C.c_uint32]),
     "odgs_frame_get_info": (C.c_int, [_P, C.POINTER(FrameInfo)]),
     "odgs_frame_download": (C.c_int, [_P, _P, C.c_int, _P, C.c_size_t]),
+    "odgs_frame_work": (C.c_int, [_P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "odgs_frame_device_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "odgs_prepare_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
     "odgs_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
     "odgs_backward": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), _P, _P, C.c_int32,
                                 C.POINTER(Settings), C.POINTER(Grads), C.POINTER(C.c_double), C.c_uint32]),
+    "odgs_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "odgs_ctx_stage_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]),
+    "odgs_ctx_reset_stage_times": (None, [_P]),
+    "odgs_stage_name": (C.c_char_p, [C.c_int]),
+    "odgs_measure_fp32_tflops": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "odgs_cull": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.c_float, C.c_float,
                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }

@@ -24,8 +24,18 @@ struct DevBuf {
 
 }  // namespace
 
+struct StageTimers {
+  bool enabled = false;
+  struct Pending { int stage; cudaEvent_t start, stop; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[ODGS_STAGE_COUNT] = {};
+  int64_t calls[ODGS_STAGE_COUNT] = {};
+};
+
 struct odgs_ctx {
   int device = 0;
+  StageTimers timers;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   odgs_status last_code = ODGS_OK;
@@ -49,7 +59,7 @@ struct odgs_frame {
   int64_t n_splats = 0, n_instances = 0;
   bool prepared = false, rendered = false, have_splat_grads = false;
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
-  DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, splat_grads;
+  DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, splat_grads, work;
   int depth_which = 0, tile_which = 0;
   DevCamera cam{};
   DevSettings settings{};
@@ -82,6 +92,51 @@ odgs_status ok(odgs_ctx* ctx) {
     ctx->last_msg.clear();
   }
   return ODGS_OK;
+}
+
+cudaEvent_t pool_event(StageTimers& t) {
+  if (!t.pool.empty()) {
+    cudaEvent_t e = t.pool.back();
+    t.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII stage timer: records an event pair around the enclosed launches.
+struct StageScope {
+  odgs_ctx* ctx;
+  int stage;
+  cudaEvent_t start = nullptr;
+  StageScope(odgs_ctx* c, int s) : ctx(c), stage(s) {
+    if (ctx->timers.enabled) {
+      start = pool_event(ctx->timers);
+      cudaEventRecord(start, ctx->stream);
+    }
+  }
+  ~StageScope() {
+    if (start) {
+      cudaEvent_t stop = pool_event(ctx->timers);
+      cudaEventRecord(stop, ctx->stream);
+      ctx->timers.pending.push_back({stage, start, stop});
+    }
+  }
+};
+
+void resolve_timers(odgs_ctx* ctx) {
+  StageTimers& t = ctx->timers;
+  for (auto& p : t.pending) {
+    cudaEventSynchronize(p.stop);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, p.start, p.stop);
+    t.ms[p.stage] += ms;
+    t.calls[p.stage] += 1;
+    t.pool.push_back(p.start);
+    t.pool.push_back(p.stop);
+  }
+  t.pending.clear();
 }
 
 odgs_status cuda_fail(odgs_ctx* ctx, cudaError_t e, const char* where) {
@@ -264,17 +319,26 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   pa.vals = f->vals[0].as<uint32_t>();
   pa.cnt = f->cnt.as<uint32_t>();
   pa.err = ctx->d_err;
-  launch_preprocess(pa, s);
+  {
+    StageScope sc(ctx, ODGS_STAGE_PREPROCESS);
+    launch_preprocess(pa, s);
+  }
 
   // Depth sort of the Gaussians (key: depth bits; culled sort last).
   ODGS_CUDA(ctx, ensure(f->sort_tmp, std::max(radix_sort_temp_bytes(n), (size_t)16), s));
   uint32_t* dk[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
   uint32_t* dv[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
-  radix_sort_pairs(dk, dv, n, 0, 32, f->sort_tmp.p, &f->depth_which, s);
+  {
+    StageScope sc(ctx, ODGS_STAGE_DEPTH_SORT);
+    radix_sort_pairs(dk, dv, n, 0, 32, f->sort_tmp.p, &f->depth_which, s);
+  }
   const uint32_t* sorted_idx = dv[f->depth_which];
-  launch_gather_counts(n, sorted_idx, f->cnt.as<uint32_t>(), f->cnt_sorted.as<uint32_t>(), s);
-  exclusive_scan_u32(f->cnt_sorted.as<uint32_t>(), f->off_sorted.as<uint32_t>(), n, f->scan_tmp.p,
-                     &ctx->d_err->n_entries, s);
+  {
+    StageScope sc(ctx, ODGS_STAGE_SCAN);
+    launch_gather_counts(n, sorted_idx, f->cnt.as<uint32_t>(), f->cnt_sorted.as<uint32_t>(), s);
+    exclusive_scan_u32(f->cnt_sorted.as<uint32_t>(), f->off_sorted.as<uint32_t>(), n, f->scan_tmp.p,
+                       &ctx->d_err->n_entries, s);
+  }
   if ((st = read_errors(ctx)) != ODGS_OK) return st;
   const DevErrors& he = *ctx->h_err;
   if (he.nonfinite != kNoError) {
@@ -314,13 +378,22 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   ea.out_keys = f->ekeys[0].as<uint32_t>();
   ea.out_vals = f->evals[0].as<uint32_t>();
   ea.ent_off_idx = f->ent_off_idx.as<uint32_t>();
-  launch_emit(ea, s);
+  {
+    StageScope sc(ctx, ODGS_STAGE_EMIT);
+    launch_emit(ea, s);
+  }
 
   ODGS_CUDA(ctx, ensure(f->sort_tmp, std::max(radix_sort_temp_bytes(K), radix_sort_temp_bytes(n)), s));
   uint32_t* ek[2] = {f->ekeys[0].as<uint32_t>(), f->ekeys[1].as<uint32_t>()};
   uint32_t* ev[2] = {f->evals[0].as<uint32_t>(), f->evals[1].as<uint32_t>()};
-  radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s);
-  launch_tile_ranges(K, ek[f->tile_which], n_tiles, f->offsets.as<int32_t>(), s);
+  {
+    StageScope sc(ctx, ODGS_STAGE_TILE_SORT);
+    radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s);
+  }
+  {
+    StageScope sc(ctx, ODGS_STAGE_RANGES);
+    launch_tile_ranges(K, ek[f->tile_which], n_tiles, f->offsets.as<int32_t>(), s);
+  }
   ODGS_CUDA(ctx, cudaGetLastError());
   f->prepared = true;
   return ok(ctx);
@@ -332,6 +405,8 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ODGS_CUDA(ctx, ensure(f->image, sizeof(float) * 3 * px, s));
   ODGS_CUDA(ctx, ensure(f->trans, sizeof(float) * px, s));
   ODGS_CUDA(ctx, ensure(f->walked, sizeof(int32_t) * px, s));
+  ODGS_CUDA(ctx, ensure(f->work, 2 * sizeof(unsigned long long), s));
+  ODGS_CUDA(ctx, cudaMemsetAsync(f->work.p, 0, 2 * sizeof(unsigned long long), s));
   BlendArgs ba;
   ba.offsets = f->offsets.as<int32_t>();
   ba.vals = f->evals[f->tile_which].as<uint32_t>();
@@ -348,7 +423,11 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ba.image = f->image.as<float>();
   ba.transmittance = f->trans.as<float>();
   ba.walked = f->walked.as<int32_t>();
-  launch_blend(ba, s);
+  ba.work = f->work.as<unsigned long long>();
+  {
+    StageScope sc(ctx, ODGS_STAGE_BLEND);
+    launch_blend(ba, s);
+  }
   ODGS_CUDA(ctx, cudaGetLastError());
   f->rendered = true;
   return ok(ctx);
@@ -458,6 +537,8 @@ odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out) {
 void odgs_ctx_destroy(odgs_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  resolve_timers(ctx);
+  for (cudaEvent_t e : ctx->timers.pool) cudaEventDestroy(e);
   if (ctx->stream) {
     release(ctx->cloud_buf, ctx->stream);
     release(ctx->dl_buf, ctx->stream);
@@ -516,7 +597,7 @@ void odgs_frame_destroy(odgs_frame* f) {
   DevBuf* bufs[] = {&f->sp_ab, &f->sp_c, &f->cov, &f->keys[0], &f->keys[1], &f->vals[0], &f->vals[1], &f->cnt,
                     &f->cnt_sorted, &f->off_sorted, &f->ent_off_idx, &f->sort_tmp, &f->scan_tmp, &f->ekeys[0],
                     &f->ekeys[1], &f->evals[0], &f->evals[1], &f->offsets, &f->image, &f->trans, &f->walked,
-                    &f->records, &f->splat_grads};
+                    &f->records, &f->splat_grads, &f->work};
   for (DevBuf* b : bufs) release(*b, s);
   cudaStreamSynchronize(s);
   delete f;
@@ -556,7 +637,19 @@ odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camer
   cudaSetDevice(ctx->device);
   odgs_status st = prepare_impl(ctx, cloud, camera, settings, frame);
   if (st != ODGS_OK) return st;
-  return blend_impl(ctx, frame);
+  st = blend_impl(ctx, frame);
+  if (ctx->timers.enabled) resolve_timers(ctx);
+  return st;
+}
+
+odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_examined, int64_t* entries_composited) {
+  if (!ctx || !f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not rendered");
+  unsigned long long w[2];
+  ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (entries_examined) *entries_examined = (int64_t)w[0];
+  if (entries_composited) *entries_composited = (int64_t)w[1];
+  return ok(ctx);
 }
 
 odgs_status odgs_frame_device_ptr(odgs_frame* f, int field, void** device_ptr) {
@@ -746,6 +839,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     gobs = gobs ? reinterpret_cast<int32_t*>(dst[7]) : nullptr;
   }
   ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
+  StageScope* bwd_scope = new StageScope(ctx, ODGS_STAGE_BWD_RASTER);
   if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->records.p, 0, sizeof(float) * 9 * (size_t)K, s));
   ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
   if ((st = reset_errors(ctx)) != ODGS_OK) return st;
@@ -768,6 +862,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   ra.cutoff_sigma = f->settings.cutoff_sigma;
   ra.records = f->records.as<float>();
   launch_bwd_raster(ra, s);
+  delete bwd_scope;
 
   BwdSplatArgs sa;
   sa.n = n;
@@ -794,7 +889,10 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.g_observed = gobs;
   sa.splat_grads = f->splat_grads.as<float>();
   sa.err = ctx->d_err;
-  launch_bwd_splat(sa, s);
+  {
+    StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
+    launch_bwd_splat(sa, s);
+  }
   ODGS_CUDA(ctx, cudaGetLastError());
   f->have_splat_grads = true;
 
@@ -808,6 +906,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
       if (dsth[k]) ODGS_CUDA(ctx, cudaMemcpyAsync(dsth[k], srcd[k], 4 * width[k] * n, cudaMemcpyDeviceToHost, s));
   }
   if ((st = read_errors(ctx)) != ODGS_OK) return st;
+  if (ctx->timers.enabled) resolve_timers(ctx);
   const DevErrors& he = *ctx->h_err;
   if (he.bwd_domain != kNoError) {
     const int64_t idx = (int64_t)(he.bwd_domain >> 4);
@@ -817,6 +916,68 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     const int64_t idx = (int64_t)(he.bwd_nonfinite >> 4);
     return set_error(ctx, ODGS_ERR_RUNTIME, idx, "backward: non-finite gradient for Gaussian " + std::to_string(idx));
   }
+  return ok(ctx);
+}
+
+odgs_status odgs_ctx_set_profiling(odgs_ctx* ctx, int enable) {
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  resolve_timers(ctx);
+  ctx->timers.enabled = enable != 0;
+  return ok(ctx);
+}
+
+int odgs_ctx_stage_times(odgs_ctx* ctx, double* ms, int64_t* calls, int max_stages) {
+  if (!ctx) return 0;
+  resolve_timers(ctx);
+  const int n = std::min(max_stages, (int)ODGS_STAGE_COUNT);
+  for (int k = 0; k < n; ++k) {
+    if (ms) ms[k] = ctx->timers.ms[k];
+    if (calls) calls[k] = ctx->timers.calls[k];
+  }
+  return n;
+}
+
+void odgs_ctx_reset_stage_times(odgs_ctx* ctx) {
+  if (!ctx) return;
+  resolve_timers(ctx);
+  for (int k = 0; k < ODGS_STAGE_COUNT; ++k) {
+    ctx->timers.ms[k] = 0;
+    ctx->timers.calls[k] = 0;
+  }
+}
+
+const char* odgs_stage_name(int stage) {
+  static const char* names[ODGS_STAGE_COUNT] = {"preprocess", "depth_sort", "scan", "emit", "tile_sort",
+                                                "ranges", "blend", "bwd_raster", "bwd_splat"};
+  return (stage >= 0 && stage < ODGS_STAGE_COUNT) ? names[stage] : "unknown";
+}
+
+odgs_status odgs_measure_fp32_tflops(odgs_ctx* ctx, double* tflops) {
+  LaunchScope scope(ctx);
+  if (!ctx || !tflops) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  int sms = 0;
+  ODGS_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  DevBuf sink;
+  ODGS_CUDA(ctx, ensure(sink, sizeof(float) * 1024 * 1024, ctx->stream));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int iters = 4096;
+  const int blocks = sms * 8, threads = 256;
+  launch_fp32_peak(blocks, threads, iters, sink.as<float>(), ctx->stream);  // warm-up
+  cudaEventRecord(a, ctx->stream);
+  launch_fp32_peak(blocks, threads, iters, sink.as<float>(), ctx->stream);
+  cudaEventRecord(b, ctx->stream);
+  ODGS_CUDA(ctx, cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  release(sink, ctx->stream);
+  // fp32_peak_flops_per_thread(iters) FMAs x 2 flops per thread.
+  const double flops = (double)blocks * threads * fp32_peak_flops_per_thread(iters);
+  *tflops = flops / (ms * 1e-3) / 1e12;
   return ok(ctx);
 }
 

@@ -55,6 +55,7 @@ struct BlendArgs {
   float* image;
   float* transmittance;
   int32_t* walked;
+  unsigned long long* work;  // [2] += entries examined, entries composited (or null)
 };
 void launch_blend(const BlendArgs& a, cudaStream_t stream);
 
@@ -70,6 +71,10 @@ size_t radix_sort_temp_bytes(int64_t n);
 // keys/vals: [2] ping-pong buffers of n each; on return *which (0/1) holds the result.
 void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
                       int* which, cudaStream_t stream);
+
+// FP32 FMA throughput microbenchmark (for the roofline denominator).
+void launch_fp32_peak(int blocks, int threads, int iters, float* sink, cudaStream_t stream);
+double fp32_peak_flops_per_thread(int iters);
 
 // ------------------------------------------------------------------ backward
 struct BwdRasterArgs {

@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
-    int32_t* __restrict__ walked_out) {
+    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work) {
   __shared__ float s_cx[kBlendThreads], s_cy[kBlendThreads], s_i00[kBlendThreads], s_i01x2[kBlendThreads],
       s_i11[kBlendThreads], s_op[kBlendThreads], s_r[kBlendThreads], s_g[kBlendThreads], s_b[kBlendThreads];
   const int tile = blockIdx.x;
@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
   }
 
   const float W = (float)width;
+  uint32_t contrib = 0;
   for (int base = e0; base < e1; base += kBlendThreads) {
     bool any_alive = false;
 #pragma unroll
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
           break;
         }
         const float w = alpha * tq;
+        ++contrib;
         r = r + s_r[j] * w;
         gg = gg + s_g[j] * w;
         bb = bb + s_b[j] * w;
@@ -364,6 +366,18 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
   }
 
   const int64_t plane = (int64_t)width * height;
+  // Work counters for the roofline: entries examined (walked, plus the terminating
+  // entry when the walk stopped early) and entries composited.
+  uint32_t exam = 0;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q)
+    if (pix[q] >= 0) exam += (uint32_t)min(walked[q] + 1, e1 - e0);
+  const uint32_t w_exam = __reduce_add_sync(0xffffffffu, exam);
+  const uint32_t w_contrib = __reduce_add_sync(0xffffffffu, contrib);
+  if ((tid & 31) == 0 && work) {
+    atomicAdd(work, (unsigned long long)w_exam);
+    atomicAdd(work + 1, (unsigned long long)w_contrib);
+  }
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     if (pix[q] < 0) continue;
@@ -384,7 +398,7 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
   k_blend<PPT><<<n_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,    \
                                                       a.tile_size, a.tiles_x, a.alpha_clamp,                    \
                                                       a.transmittance_floor, cutoff2, a.image, a.transmittance, \
-                                                      a.walked)
+                                                      a.walked, a.work)
   if (area <= kBlendThreads) ODGS_BLEND(1);
   else if (area <= 4 * kBlendThreads) ODGS_BLEND(4);
   else ODGS_BLEND(16);

@@ -1,2 +1,31 @@
 // train.cu — placeholder for the training-step kernels (loss, Adam); filled in later.
 #include "kernels.h"
+
+namespace odgs_b200 {
+
+// 8 independent FMA chains per thread keep the FP32 pipe saturated.
+__global__ void __launch_bounds__(256) k_fp32_peak(int iters, float* sink) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3f + k;
+  const float m = 0.999f, c = 1e-4f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], m, c);
+  }
+  float s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678f) sink[threadIdx.x] = s;
+}
+
+double fp32_peak_flops_per_thread(int iters) { return 2.0 * 8 * 16 * (double)iters; }
+
+void launch_fp32_peak(int blocks, int threads, int iters, float* sink, cudaStream_t stream) {
+  k_fp32_peak<<<blocks, threads, 0, stream>>>(iters, sink);
+  ++g_launches;
+}
+
+}  // namespace odgs_b200

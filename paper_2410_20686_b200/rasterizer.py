@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import weakref
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -145,9 +146,12 @@ class Context:
             raise OdgsError(f"odgs_ctx_create failed with status {st}")
         self.handle = h
         self.device = device
+        self._frames = weakref.WeakSet()
 
     def close(self):
         if self.handle:
+            for fr in list(self._frames):  # frames hold device memory of this context
+                fr.destroy()
             self.lib.odgs_ctx_destroy(self.handle)
             self.handle = None
 
@@ -176,6 +180,24 @@ class Context:
     def stream(self) -> int:
         return int(self.lib.odgs_ctx_stream(self.handle) or 0)
 
+    def set_profiling(self, enable: bool):
+        self.check(self.lib.odgs_ctx_set_profiling(self.handle, int(enable)))
+
+    def reset_stage_times(self):
+        self.lib.odgs_ctx_reset_stage_times(self.handle)
+
+    def stage_times(self) -> dict:
+        """{stage: (milliseconds, calls)} accumulated on the context's stream."""
+        ms = (C.c_double * 16)()
+        calls = (C.c_int64 * 16)()
+        n = self.lib.odgs_ctx_stage_times(self.handle, ms, calls, 16)
+        return {self.lib.odgs_stage_name(k).decode(): (ms[k], calls[k]) for k in range(n)}
+
+    def measure_fp32_tflops(self) -> float:
+        v = C.c_double(0)
+        self.check(self.lib.odgs_measure_fp32_tflops(self.handle, C.byref(v)))
+        return v.value
+
 
 class RenderOutput:
     """A rendered frame (RenderOutput, rasterizer.hpp:92-102); fields download on access."""
@@ -185,14 +207,18 @@ class RenderOutput:
         h = C.c_void_p()
         ctx.check(ctx.lib.odgs_frame_create(ctx.handle, C.byref(h)))
         self.handle = h
+        ctx._frames.add(self)
         if flags:
             ctx.lib.odgs_frame_set_flags(h, flags)
 
+    def destroy(self):
+        if self.handle and self.ctx.handle:
+            self.ctx.lib.odgs_frame_destroy(self.handle)
+        self.handle = None
+
     def __del__(self):
         try:
-            if self.handle:
-                self.ctx.lib.odgs_frame_destroy(self.handle)
-                self.handle = None
+            self.destroy()
         except Exception:
             pass
 
@@ -206,6 +232,12 @@ class RenderOutput:
         self.ctx.check(self.ctx.lib.odgs_frame_download(self.ctx.handle, self.handle, fld,
                                                         out.ctypes.data, out.nbytes))
         return out
+
+    def work(self):
+        """(entries examined, entries composited) of the last blend."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        self.ctx.check(self.ctx.lib.odgs_frame_work(self.ctx.handle, self.handle, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def device_ptr(self, fld: int) -> int:
         p = C.c_void_p()

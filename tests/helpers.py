@@ -58,8 +58,16 @@ def gpu_fields(ctx, cloud: GaussianCloud, cam: CameraPose, settings: RenderSetti
     return out
 
 
+def cam32(cam: CameraPose):
+    """The camera exactly as the GPU sees it (float32), widened for the oracle."""
+    r = np.asarray(cam.rotation, dtype=np.float32).astype(np.float64)
+    t = np.asarray(cam.translation, dtype=np.float32).astype(np.float64)
+    return r, t
+
+
 def oracle_fields(cloud_arrs, cam: CameraPose, osettings, portable: bool, dbl: bool = False, brute=False):
-    fr = oracle_lib.render(cloud_arrs, cam.rotation, cam.translation, cam.width, cam.height, osettings,
+    r, t = cam32(cam)
+    fr = oracle_lib.render(cloud_arrs, r, t, cam.width, cam.height, osettings,
                            dbl=dbl, portable=portable, brute=brute)
     W, H = cam.width, cam.height
     out = {k: fr.get(k) for k in ["tile_offsets", "tile_entries", "inst_splat", "inst_shift", "splat_index",
