@@ -131,7 +131,8 @@ typedef enum {
 } odgs_frame_field;
 
 /* odgs_frame_set_flags */
-#define ODGS_FRAME_KEEP_COV2D 0x1u /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
+#define ODGS_FRAME_KEEP_COV2D 0x1u   /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
+#define ODGS_FRAME_PLAIN_BLEND 0x2u  /* disable warp culling in the blend (A/B checks) */
 
 /* odgs_backward flags */
 #define ODGS_ACCUMULATE 0x1u /* add into the gradient buffers (GradBuffers::accumulate) */

@@ -56,8 +56,10 @@ struct BlendArgs {
   float* transmittance;
   int32_t* walked;
   unsigned long long* work;  // [2] += entries examined, entries composited (or null)
+  bool plain;                // force the un-culled reference kernel (A/B checks)
 };
 void launch_blend(const BlendArgs& a, cudaStream_t stream);
+void launch_blend_plain(const BlendArgs& a, cudaStream_t stream);
 
 // ------------------------------------------------------------------ sort / scan
 // Scratch needed by exclusive_scan_u32 for n items.

@@ -389,7 +389,178 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
   }
 }
 
+// ------------------------------------------------------------------ blend with warp culling
+// Conservative half extents (ex, ey) of an entry's cutoff ellipse such that any pixel
+// whose *computed* offset dx = fl(px - cx) satisfies |dx| > ex (or |dy| > ey) has a
+// computed d2 > cutoff^2, so the reference loop would skip it (rasterizer.hpp:247).
+//   exact:    min_dy Q(dx, dy) = dx^2 / Sigma00 with Sigma00 = i11 / det(conic);
+//   rounding: |fl(d2) - Q| <= 4 eps (|t1|+|t2|+|t3|) <= 4 eps kappa Q with
+//             kappa = (max(i00, i11) + |i01|) * (i00 + i11) / det(conic);
+//   margin:   delta = 64 eps kappa covers that, and the rounding of det and Sigma00
+//             (each <= 3 eps kappa); extents are inflated by (1 + 4 delta) in Q.
+// Ill-conditioned entries (delta >= 0.25) are never culled.
+__device__ __forceinline__ bool cull_extents(float i00, float i01, float i11, float cutoff2, float* ex, float* ey) {
+  const float det = i00 * i11 - i01 * i01;
+  if (!(det > 0.0f) || !(i00 > 0.0f) || !(i11 > 0.0f)) return false;
+  const float kappa = (fmaxf(i00, i11) + fabsf(i01)) * (i00 + i11) / det;
+  const float delta = 64.0f * 1.1920929e-7f * kappa;
+  if (!(delta < 0.25f)) return false;
+  const float f = cutoff2 * (1.0f + 4.0f * delta);
+  *ex = sqrtf(i11 / det * f) * 1.00001f + 1e-4f;
+  *ey = sqrtf(i00 / det * f) * 1.00001f + 1e-4f;
+  return true;
+}
+
+__global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
+    const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
+    const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
+    float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
+    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work) {
+  constexpr int kWarps = kBlendThreads / 32;
+  __shared__ float4 s_geo[kBlendThreads];  // cx, cy, i00, 2*i01
+  __shared__ float4 s_att[kBlendThreads];  // i11, opacity, r, g
+  __shared__ float s_b[kBlendThreads];
+  __shared__ uint8_t s_mask[kBlendThreads];
+  __shared__ uint8_t s_list[kWarps][kBlendThreads];
+  __shared__ float4 s_wbox[kWarps];  // pixel-centre bbox of each warp: xmin, xmax, ymin, ymax
+
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int e0 = offsets[tile], e1 = offsets[tile + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // Pixel of this thread. 16x16 tiles: each warp owns a 4-wide x 8-tall block (lanes
+  // run down a column: the image is column-major, so stores are 32 B runs).
+  int lx, ly;
+  bool valid;
+  if (tile_size == 16) {
+    lx = (warp >> 1) * 4 + (lane >> 3);
+    ly = (warp & 1) * 8 + (lane & 7);
+    valid = true;
+  } else {
+    lx = tid / tile_size;
+    ly = tid - lx * tile_size;
+    valid = tid < tile_size * tile_size;
+  }
+  const int x = tx * tile_size + lx, y = ty * tile_size + ly;
+  valid = valid && x < width && y < height;
+  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  {
+    float xmin = valid ? px : INFINITY, xmax = valid ? px : -INFINITY;
+    float ymin = valid ? py : INFINITY, ymax = valid ? py : -INFINITY;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      xmin = fminf(xmin, __shfl_xor_sync(0xffffffffu, xmin, d));
+      xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, d));
+      ymin = fminf(ymin, __shfl_xor_sync(0xffffffffu, ymin, d));
+      ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, d));
+    }
+    if (lane == 0) s_wbox[warp] = make_float4(xmin, xmax, ymin, ymax);
+  }
+
+  float t = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+  int walked = e1 - e0;
+  bool done = !valid;
+  uint32_t contrib = 0;
+  const float W = (float)width;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  for (int base = e0; base < e1; base += kBlendThreads) {
+    if (__syncthreads_count(!done) == 0) break;  // also orders s_wbox / previous batch
+    const int e = base + tid;
+    uint32_t mask = 0;
+    if (e < e1) {
+      const uint32_t v = vals[e];
+      const uint32_t g = v >> 2;
+      const int k = (int)(v & 3u);
+      const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+      const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+      const float c2 = __ldg(&sp_c[g].x);
+      const float cx = a.x + (k == 0 ? -W : (k == 1 ? 0.0f : W));
+      const float cy = a.y;
+      s_geo[tid] = make_float4(cx, cy, a.z, 2.0f * a.w);
+      s_att[tid] = make_float4(b.x, b.y, b.z, b.w);
+      s_b[tid] = c2;
+      float ex, ey;
+      if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const float4 bx = s_wbox[w];
+          const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
+          mask |= out ? 0u : (1u << w);
+        }
+      } else {
+        mask = 0xFFu;
+      }
+    }
+    s_mask[tid] = (uint8_t)mask;
+    __syncthreads();
+    // Compact this warp's entries (in order) into its list.
+    int n_list = 0;
+#pragma unroll
+    for (int c = 0; c < kBlendThreads / 32; ++c) {
+      const bool mine = (s_mask[c * 32 + lane] >> warp) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+      if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(c * 32 + lane);
+      n_list += __popc(bal);
+    }
+    __syncwarp();
+    if (!done) {
+      for (int q = 0; q < n_list; ++q) {
+        const int j = s_list[warp][q];
+        const float4 geo = s_geo[j];
+        const float dx = px - geo.x;
+        const float dy = py - geo.y;
+        const float4 att = s_att[j];
+        const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
+        if (d2 > cutoff2) continue;
+        const float alpha = std_min(alpha_clamp, att.y * pm_expf_blend(-d2 / 2.0f));
+        const float t_next = t * (1.0f - alpha);
+        if (t_next < transmittance_floor) {
+          walked = base + j - e0;
+          done = true;
+          break;
+        }
+        const float wgt = alpha * t;
+        ++contrib;
+        cr = cr + att.z * wgt;
+        cg = cg + att.w * wgt;
+        cb = cb + s_b[j] * wgt;
+        t = t_next;
+      }
+    }
+  }
+
+  const uint32_t exam = valid ? (uint32_t)min(walked + 1, e1 - e0) : 0u;
+  const uint32_t w_exam = __reduce_add_sync(0xffffffffu, exam);
+  const uint32_t w_contrib = __reduce_add_sync(0xffffffffu, contrib);
+  if (lane == 0 && work) {
+    atomicAdd(work, (unsigned long long)w_exam);
+    atomicAdd(work + 1, (unsigned long long)w_contrib);
+  }
+  if (valid) {
+    const int64_t plane = (int64_t)width * height;
+    const int64_t p = (int64_t)x * height + y;
+    image[p] = cr;
+    image[plane + p] = cg;
+    image[2 * plane + p] = cb;
+    trans_out[p] = t;
+    walked_out[p] = walked;
+  }
+}
+
 void launch_blend(const BlendArgs& a, cudaStream_t stream) {
+  if (!a.plain && a.tile_size <= 16 && a.tiles_x * a.tiles_y > 0) {
+    k_blend_cull<<<a.tiles_x * a.tiles_y, kBlendThreads, 0, stream>>>(
+        a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.alpha_clamp,
+        a.transmittance_floor, a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work);
+    ++g_launches;
+    return;
+  }
+  launch_blend_plain(a, stream);
+}
+
+void launch_blend_plain(const BlendArgs& a, cudaStream_t stream) {
   const int n_tiles = a.tiles_x * a.tiles_y;
   if (n_tiles == 0) return;
   const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
