@@ -211,3 +211,18 @@ def test_full_size_c3_bit_exact(gpu_ctx):
     offs = g["tile_offsets"]
     assert offs[0] == 0 and np.all(np.diff(offs) >= 0) and offs[-1] == g["n_entries"]
     assert np.all(g["transmittance"] >= 1e-4 * (1 - 1e-6))
+
+
+@pytest.mark.parametrize("tile", [8, 16])
+def test_warp_culled_blend_equals_plain_blend(gpu_ctx, tile):
+    """The culled blend (conservative per-warp ellipse test) changes no output bit."""
+    from paper_2410_20686_b200 import _capi as capi
+    c = scenes.cloud_c3(200_000)
+    cam = CameraPose(2048, 1024, rot_yaw(0.3))
+    s = RenderSettings(tile_size=tile)
+    a = render(gpu_ctx, c, cam, s)
+    b = render(gpu_ctx, c, cam, s, flags=capi.FRAME_PLAIN_BLEND)
+    assert np.array_equal(a.image, b.image)
+    assert np.array_equal(a.walked, b.walked)
+    assert np.array_equal(a.transmittance, b.transmittance)
+    assert a.work() == b.work()
