@@ -411,46 +411,26 @@ __device__ __forceinline__ bool cull_extents(float i00, float i01, float i11, fl
   return true;
 }
 
-// One entry of a tile list, staged for a warp.
-struct StagedEntry {
-  float4 geo;  // cx (with seam shift), cy, i00, 2*i01
-  float4 att;  // i11, opacity, r, g
-  float b;
-};
-
-__device__ __forceinline__ void load_entry(const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
-                                           const float4* __restrict__ sp_c, int e, float W, StagedEntry& o) {
-  const uint32_t v = __ldg(vals + e);
-  const uint32_t g = v >> 2;
-  const int k = (int)(v & 3u);
-  const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
-  o.att = __ldg(sp_ab + 2 * (int64_t)g + 1);
-  o.b = __ldg(&sp_c[g].x);
-  o.geo = make_float4(a.x + (k == 0 ? -W : (k == 1 ? 0.0f : W)), a.y, a.z, a.w);
-}
-
-// Warp-independent blend: one CTA per tile (8 warps), each warp owns a 4x8 pixel
-// block (16x16 tiles) and walks the tile list on its own in 32-entry chunks: lane j
-// loads entry chunk+j (the next chunk is prefetched while the current one
-// composites), tests it against the warp's pixel box with cull_extents(), and the
-// surviving entries are compacted, in list order, into the warp's shared slots.
-// No CTA barriers; a warp retires as soon as its 32 pixels are saturated.
-__global__ void __launch_bounds__(kBlendThreads) k_blend_warp(
+__global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
     int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work) {
   constexpr int kWarps = kBlendThreads / 32;
-  __shared__ float4 s_geo[kWarps][32];
-  __shared__ float4 s_att[kWarps][32];
-  __shared__ float s_b[kWarps][32];
-  __shared__ uint8_t s_j[kWarps][32];
+  __shared__ float4 s_geo[kBlendThreads];  // cx, cy, i00, 2*i01
+  __shared__ float4 s_att[kBlendThreads];  // i11, opacity, r, g
+  __shared__ float s_b[kBlendThreads];
+  __shared__ uint8_t s_mask[kBlendThreads];
+  __shared__ uint8_t s_list[kWarps][kBlendThreads];
+  __shared__ float4 s_wbox[kWarps];  // pixel-centre bbox of each warp: xmin, xmax, ymin, ymax
 
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile], e1 = offsets[tile + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
+  // Pixel of this thread. 16x16 tiles: each warp owns a 4-wide x 8-tall block (lanes
+  // run down a column: the image is column-major, so stores are 32 B runs).
   int lx, ly;
   bool valid;
   if (tile_size == 16) {
@@ -465,14 +445,17 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_warp(
   const int x = tx * tile_size + lx, y = ty * tile_size + ly;
   valid = valid && x < width && y < height;
   const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-  float bx0 = valid ? px : INFINITY, bx1 = valid ? px : -INFINITY;
-  float by0 = valid ? py : INFINITY, by1 = valid ? py : -INFINITY;
+  {
+    float xmin = valid ? px : INFINITY, xmax = valid ? px : -INFINITY;
+    float ymin = valid ? py : INFINITY, ymax = valid ? py : -INFINITY;
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, d));
-    bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, d));
-    by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, d));
-    by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, d));
+    for (int d = 16; d > 0; d >>= 1) {
+      xmin = fminf(xmin, __shfl_xor_sync(0xffffffffu, xmin, d));
+      xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, d));
+      ymin = fminf(ymin, __shfl_xor_sync(0xffffffffu, ymin, d));
+      ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, d));
+    }
+    if (lane == 0) s_wbox[warp] = make_float4(xmin, xmax, ymin, ymax);
   }
 
   float t = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
@@ -482,45 +465,59 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_warp(
   const float W = (float)width;
   const uint32_t lt_mask = (1u << lane) - 1u;
 
-  StagedEntry nxt;
-  if (e0 + lane < e1) load_entry(vals, sp_ab, sp_c, e0 + lane, W, nxt);
-  for (int chunk = e0; chunk < e1; chunk += 32) {
-    if (__all_sync(0xffffffffu, done)) break;
-    const StagedEntry cur = nxt;
-    const bool have = chunk + lane < e1;
-    if (chunk + 32 + lane < e1) load_entry(vals, sp_ab, sp_c, chunk + 32 + lane, W, nxt);
-    bool rel = false;
-    if (have) {
+  for (int base = e0; base < e1; base += kBlendThreads) {
+    if (__syncthreads_count(!done) == 0) break;  // also orders s_wbox / previous batch
+    const int e = base + tid;
+    uint32_t mask = 0;
+    if (e < e1) {
+      const uint32_t v = vals[e];
+      const uint32_t g = v >> 2;
+      const int k = (int)(v & 3u);
+      const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+      const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+      const float c2 = __ldg(&sp_c[g].x);
+      const float cx = a.x + (k == 0 ? -W : (k == 1 ? 0.0f : W));
+      const float cy = a.y;
+      s_geo[tid] = make_float4(cx, cy, a.z, 2.0f * a.w);
+      s_att[tid] = make_float4(b.x, b.y, b.z, b.w);
+      s_b[tid] = c2;
       float ex, ey;
-      if (cull_extents(cur.geo.z, cur.geo.w, cur.att.x, cutoff2, &ex, &ey)) {
-        const float cx = cur.geo.x, cy = cur.geo.y;
-        rel = !((bx0 - cx > ex) || (bx1 - cx < -ex) || (by0 - cy > ey) || (by1 - cy < -ey));
+      if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+          const float4 bx = s_wbox[w];
+          const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
+          mask |= out ? 0u : (1u << w);
+        }
       } else {
-        rel = true;
+        mask = 0xFFu;
       }
     }
-    const uint32_t bal = __ballot_sync(0xffffffffu, rel);
-    if (rel) {
-      const int slot = __popc(bal & lt_mask);
-      s_geo[warp][slot] = make_float4(cur.geo.x, cur.geo.y, cur.geo.z, 2.0f * cur.geo.w);
-      s_att[warp][slot] = cur.att;
-      s_b[warp][slot] = cur.b;
-      s_j[warp][slot] = (uint8_t)lane;
+    s_mask[tid] = (uint8_t)mask;
+    __syncthreads();
+    // Compact this warp's entries (in order) into its list.
+    int n_list = 0;
+#pragma unroll
+    for (int c = 0; c < kBlendThreads / 32; ++c) {
+      const bool mine = (s_mask[c * 32 + lane] >> warp) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+      if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(c * 32 + lane);
+      n_list += __popc(bal);
     }
     __syncwarp();
-    const int n = __popc(bal);
     if (!done) {
-      for (int q = 0; q < n; ++q) {
-        const float4 geo = s_geo[warp][q];
+      for (int q = 0; q < n_list; ++q) {
+        const int j = s_list[warp][q];
+        const float4 geo = s_geo[j];
         const float dx = px - geo.x;
         const float dy = py - geo.y;
-        const float4 att = s_att[warp][q];
+        const float4 att = s_att[j];
         const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
         if (d2 > cutoff2) continue;
         const float alpha = std_min(alpha_clamp, att.y * pm_expf_blend(-d2 / 2.0f));
         const float t_next = t * (1.0f - alpha);
         if (t_next < transmittance_floor) {
-          walked = chunk + s_j[warp][q] - e0;
+          walked = base + j - e0;
           done = true;
           break;
         }
@@ -528,11 +525,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_warp(
         ++contrib;
         cr = cr + att.z * wgt;
         cg = cg + att.w * wgt;
-        cb = cb + s_b[warp][q] * wgt;
+        cb = cb + s_b[j] * wgt;
         t = t_next;
       }
     }
-    __syncwarp();
   }
 
   const uint32_t exam = valid ? (uint32_t)min(walked + 1, e1 - e0) : 0u;
@@ -555,7 +551,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_warp(
 
 void launch_blend(const BlendArgs& a, cudaStream_t stream) {
   if (!a.plain && a.tile_size <= 16 && a.tiles_x * a.tiles_y > 0) {
-    k_blend_warp<<<a.tiles_x * a.tiles_y, kBlendThreads, 0, stream>>>(
+    k_blend_cull<<<a.tiles_x * a.tiles_y, kBlendThreads, 0, stream>>>(
         a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.alpha_clamp,
         a.transmittance_floor, a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work);
     ++g_launches;
