@@ -211,6 +211,46 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
                           const float* dl_dimage, int32_t dl_memory, const odgs_settings* settings,
                           const odgs_grads* grads, const double* grad_t_signs, uint32_t flags);
 
+/* ------------------------------------------------------------------ training step
+   (all pointers are device memory) */
+
+/* The optimisable parameters (GaussianCloud<float> with writable device arrays). */
+typedef struct {
+  int64_t n;
+  float* means;
+  float* rotations;
+  float* log_scales;
+  float* raw_opacities;
+  float* colors;
+} odgs_params;
+
+/* TrainState (types.hpp:257-325): Adam moments per group and the densify window. */
+typedef struct {
+  float *means_m, *means_v, *rot_m, *rot_v, *scale_m, *scale_v, *opac_m, *opac_v, *color_m, *color_v;
+  float* grad_accum;
+  float* elev_accum;
+  int32_t* grad_count;
+} odgs_train_state;
+
+/* Learning rates of this step (means: means_lr_at(iteration) * extent,
+   optimizer.hpp:61-69) and the 1-based Adam step. */
+typedef struct {
+  float lr_means, lr_rotation, lr_scale, lr_opacity, lr_color;
+  int64_t step;
+} odgs_adam_params;
+
+/* photometric_loss (metrics.hpp:152-184) for lambda_ssim = 0 (L1): writes the image
+   gradient to dl_dimage and the loss to *loss (synchronizes). lambda_ssim > 0 is
+   rejected with ODGS_ERR_INVALID_ARGUMENT (SSIM is not on the GPU yet). */
+odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
+                                  int32_t height, float lambda_ssim, float* dl_dimage, double* loss);
+
+/* The update half of train_step (optimizer.hpp:114-139): densify-window
+   accumulation, Adam (b1 0.9, b2 0.999, eps 1e-15) on the five groups, quaternion
+   renormalisation. grads must be device buffers (e.g. after an all-reduce). */
+odgs_status odgs_adam_step(odgs_ctx* ctx, const odgs_params* params, const odgs_grads* grads,
+                           const odgs_train_state* state, const odgs_adam_params* adam);
+
 /* cull (rasterizer.hpp:15-28): host output of the kept rows, ascending. */
 odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, float near_radius,
                       float far_radius, int64_t* out_indices, int64_t* out_count);

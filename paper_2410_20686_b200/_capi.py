@@ -58,6 +58,22 @@ class Grads(C.Structure):
                 ("observed", C.c_void_p), ("memory", C.c_int32)]
 
 
+class Params(C.Structure):
+    _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("rotations", C.c_void_p), ("log_scales", C.c_void_p),
+                ("raw_opacities", C.c_void_p), ("colors", C.c_void_p)]
+
+
+class TrainState(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("means_m", "means_v", "rot_m", "rot_v", "scale_m", "scale_v", "opac_m",
+                                          "opac_v", "color_m", "color_v", "grad_accum", "elev_accum",
+                                          "grad_count")]
+
+
+class AdamParams(C.Structure):
+    _fields_ = [("lr_means", C.c_float), ("lr_rotation", C.c_float), ("lr_scale", C.c_float),
+                ("lr_opacity", C.c_float), ("lr_color", C.c_float), ("step", C.c_int64)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("n_gaussians", C.c_int64), ("n_splats", C.c_int64),
@@ -92,6 +108,9 @@ SIGNATURES = {
     "odgs_ctx_reset_stage_times": (None, [_P]),
     "odgs_stage_name": (C.c_char_p, [C.c_int]),
     "odgs_measure_fp32_tflops": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "odgs_photometric_loss": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float, _P, C.POINTER(C.c_double)]),
+    "odgs_adam_step": (C.c_int, [_P, C.POINTER(Params), C.POINTER(Grads), C.POINTER(TrainState),
+                                 C.POINTER(AdamParams)]),
     "odgs_cull": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.c_float, C.c_float,
                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }

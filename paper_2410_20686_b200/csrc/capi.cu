@@ -45,7 +45,7 @@ struct odgs_ctx {
   DevErrors* h_err = nullptr;       // pinned readback
   DevErrors* h_err_init = nullptr;  // pinned reset template
   uint32_t* h_scratch = nullptr;    // pinned
-  DevBuf cloud_buf, dl_buf, grads_buf, signs_buf, cull_buf;
+  DevBuf cloud_buf, dl_buf, grads_buf, signs_buf, cull_buf, loss_buf;
   float* d_unit_signs = nullptr;
   int64_t launches = 0;
 };
@@ -546,6 +546,7 @@ void odgs_ctx_destroy(odgs_ctx* ctx) {
     release(ctx->grads_buf, ctx->stream);
     release(ctx->signs_buf, ctx->stream);
     release(ctx->cull_buf, ctx->stream);
+    release(ctx->loss_buf, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
   }
   if (ctx->d_err) cudaFree(ctx->d_err);
@@ -917,6 +918,60 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     const int64_t idx = (int64_t)(he.bwd_nonfinite >> 4);
     return set_error(ctx, ODGS_ERR_RUNTIME, idx, "backward: non-finite gradient for Gaussian " + std::to_string(idx));
   }
+  return ok(ctx);
+}
+
+odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
+                                  int32_t height, float lambda_ssim, float* dl_dimage, double* loss) {
+  LaunchScope scope(ctx);
+  if (!ctx || !rendered || !target || !dl_dimage) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!(lambda_ssim >= 0.0f) || !(lambda_ssim < 1.0f))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "photometric_loss: lambda must be in [0, 1)");
+  if (lambda_ssim > 0.0f)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "photometric_loss: SSIM term not available on the GPU");
+  if (width <= 0 || height <= 0) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "photometric_loss: bad size");
+  const int64_t count = 3 * (int64_t)width * height;
+  ODGS_CUDA(ctx, ensure(ctx->loss_buf, l1_loss_temp_bytes(count), ctx->stream));
+  launch_l1_loss(rendered, target, count, lambda_ssim, dl_dimage, ctx->loss_buf.as<double>(), ctx->stream);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  if (loss) {
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->loss_buf.p, sizeof(double), cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+    ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(loss, ctx->h_scratch, sizeof(double));
+  }
+  return ok(ctx);
+}
+
+odgs_status odgs_adam_step(odgs_ctx* ctx, const odgs_params* p, const odgs_grads* g, const odgs_train_state* st,
+                           const odgs_adam_params* ap) {
+  LaunchScope scope(ctx);
+  if (!ctx || !p || !g || !st || !ap) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (ap->step < 1) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "adam_step: step must be >= 1");
+  if (g->memory != ODGS_MEM_DEVICE)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "adam_step: gradients must be device buffers");
+  AdamArgs a;
+  a.n = p->n;
+  a.means = p->means; a.rotations = p->rotations; a.log_scales = p->log_scales;
+  a.raw_opacities = p->raw_opacities; a.colors = p->colors;
+  a.means_m = st->means_m; a.means_v = st->means_v; a.rot_m = st->rot_m; a.rot_v = st->rot_v;
+  a.scale_m = st->scale_m; a.scale_v = st->scale_v; a.opac_m = st->opac_m; a.opac_v = st->opac_v;
+  a.color_m = st->color_m; a.color_v = st->color_v;
+  a.grad_accum = st->grad_accum; a.elev_accum = st->elev_accum; a.grad_count = st->grad_count;
+  a.g_means = g->means; a.g_rotations = g->rotations; a.g_log_scales = g->log_scales;
+  a.g_raw_opacities = g->raw_opacities; a.g_colors = g->colors; a.g_pixel_grad_norm = g->pixel_grad_norm;
+  a.g_one_minus_cos = g->one_minus_cos; a.g_observed = g->observed;
+  if ((a.grad_accum && !a.g_pixel_grad_norm) || (a.elev_accum && !a.g_one_minus_cos) || (a.grad_count && !a.g_observed))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "adam_step: densify window needs the statistics");
+  a.lr_means = ap->lr_means; a.lr_rotation = ap->lr_rotation; a.lr_scale = ap->lr_scale;
+  a.lr_opacity = ap->lr_opacity; a.lr_color = ap->lr_color;
+  // c = 1 - pow(b, step) in Scalar, as adam_update computes it (optimizer.hpp:80-81).
+  a.c1 = 1.0f - std::pow(0.9f, (float)ap->step);
+  a.c2 = 1.0f - std::pow(0.999f, (float)ap->step);
+  launch_adam(a, ctx->stream);
+  ODGS_CUDA(ctx, cudaGetLastError());
   return ok(ctx);
 }
 

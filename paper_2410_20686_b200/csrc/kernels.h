@@ -74,6 +74,25 @@ size_t radix_sort_temp_bytes(int64_t n);
 void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
                       int* which, cudaStream_t stream);
 
+// ------------------------------------------------------------------ training step
+size_t l1_loss_temp_bytes(int64_t count);
+// temp[0] <- loss (double); grad <- (1 - lambda) sign(rendered - target) / count.
+void launch_l1_loss(const float* rendered, const float* target, int64_t count, float lambda, float* grad,
+                    double* temp, cudaStream_t stream);
+
+struct AdamArgs {
+  int64_t n;
+  float *means, *rotations, *log_scales, *raw_opacities, *colors;
+  float *means_m, *means_v, *rot_m, *rot_v, *scale_m, *scale_v, *opac_m, *opac_v, *color_m, *color_v;
+  float *grad_accum, *elev_accum;
+  int32_t* grad_count;
+  const float *g_means, *g_rotations, *g_log_scales, *g_raw_opacities, *g_colors, *g_pixel_grad_norm,
+      *g_one_minus_cos;
+  const int32_t* g_observed;
+  float lr_means, lr_rotation, lr_scale, lr_opacity, lr_color, c1, c2;
+};
+void launch_adam(const AdamArgs& a, cudaStream_t stream);
+
 // FP32 FMA throughput microbenchmark (for the roofline denominator).
 void launch_fp32_peak(int blocks, int threads, int iters, float* sink, cudaStream_t stream);
 double fp32_peak_flops_per_thread(int iters);

@@ -1,4 +1,11 @@
-// train.cu — placeholder for the training-step kernels (loss, Adam); filled in later.
+// train.cu — kernels of the training step around the hot path:
+//   k_l1_loss      photometric_loss at lambda = 0 (metrics.hpp:152-184): the image
+//                  gradient (1 - lambda) * sign(diff) / pixels, bit-identical to the
+//                  reference's float expression, and per-block partial |diff| sums
+//                  (double) reduced in a fixed order -> deterministic loss.
+//   k_adam         train_step's update (optimizer.hpp:74-84, 114-139): densify-window
+//                  accumulation, Adam on the five parameter groups, quaternion
+//                  renormalisation — one pass over the cloud, elementwise.
 #include "kernels.h"
 
 namespace odgs_b200 {
@@ -25,6 +32,117 @@ double fp32_peak_flops_per_thread(int iters) { return 2.0 * 8 * 16 * (double)ite
 
 void launch_fp32_peak(int blocks, int threads, int iters, float* sink, cudaStream_t stream) {
   k_fp32_peak<<<blocks, threads, 0, stream>>>(iters, sink);
+  ++g_launches;
+}
+
+}  // namespace odgs_b200
+
+namespace odgs_b200 {
+
+constexpr int kLossThreads = 256;
+constexpr int kLossItems = 8;
+
+__global__ void __launch_bounds__(kLossThreads) k_l1_loss(const float* __restrict__ rendered,
+                                                          const float* __restrict__ target, int64_t count,
+                                                          float scale, float pixels, float* __restrict__ grad,
+                                                          double* __restrict__ partial) {
+  __shared__ double s_warp[kLossThreads / 32];
+  const int64_t base = (int64_t)blockIdx.x * kLossThreads * kLossItems;
+  double sum = 0.0;
+#pragma unroll
+  for (int k = 0; k < kLossItems; ++k) {
+    const int64_t i = base + (int64_t)k * kLossThreads + threadIdx.x;
+    if (i < count) {
+      const float d = rendered[i] - target[i];
+      sum += (double)fabsf(d);
+      const float sign = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
+      grad[i] = scale * sign / pixels;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kLossThreads / 32; ++w) t += s_warp[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partial, int64_t n, double scale, double* out) {
+  __shared__ double s[256];
+  double t = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 256) t += partial[i];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0] * scale;
+}
+
+size_t l1_loss_temp_bytes(int64_t count) {
+  const int64_t blocks = (count + kLossThreads * kLossItems - 1) / (kLossThreads * kLossItems);
+  return (size_t)(blocks + 1) * sizeof(double);
+}
+
+void launch_l1_loss(const float* rendered, const float* target, int64_t count, float lambda, float* grad,
+                    double* temp, cudaStream_t stream) {
+  const int64_t blocks = (count + kLossThreads * kLossItems - 1) / (kLossThreads * kLossItems);
+  const float pixels = (float)count;  // 3 * H * W, formed in Scalar as the reference does
+  k_l1_loss<<<(unsigned)blocks, kLossThreads, 0, stream>>>(rendered, target, count, 1.0f - lambda, pixels, grad,
+                                                          temp + 1);
+  ++g_launches;
+  k_sum_partials<<<1, 256, 0, stream>>>(temp + 1, blocks, (1.0 - (double)lambda) / (double)count, temp);
+  ++g_launches;
+}
+
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float lr, float c1, float c2) {
+  const float b1 = 0.9f, b2 = 0.999f, eps = 1e-15f;
+  m = b1 * m + (1.0f - b1) * g;
+  v = b2 * v + (1.0f - b2) * (g * g);
+  p -= lr * (m / c1) / (sqrtf(v / c2) + eps);
+}
+
+__global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = a.n;
+  if (i >= n) return;
+  // Densify window (optimizer.hpp:114-117), before the parameters move.
+  if (a.grad_accum) a.grad_accum[i] += a.g_pixel_grad_norm[i];
+  if (a.elev_accum) a.elev_accum[i] += a.g_one_minus_cos[i];
+  if (a.grad_count) a.grad_count[i] += a.g_observed[i];
+  for (int k = 0; k < 3; ++k)
+    adam1(a.means[k * n + i], a.means_m[k * n + i], a.means_v[k * n + i], a.g_means[k * n + i], a.lr_means, a.c1,
+          a.c2);
+  float q[4];
+  for (int k = 0; k < 4; ++k) {
+    adam1(a.rotations[k * n + i], a.rot_m[k * n + i], a.rot_v[k * n + i], a.g_rotations[k * n + i], a.lr_rotation,
+          a.c1, a.c2);
+    q[k] = a.rotations[k * n + i];
+  }
+  for (int k = 0; k < 3; ++k)
+    adam1(a.log_scales[k * n + i], a.scale_m[k * n + i], a.scale_v[k * n + i], a.g_log_scales[k * n + i],
+          a.lr_scale, a.c1, a.c2);
+  adam1(a.raw_opacities[i], a.opac_m[i], a.opac_v[i], a.g_raw_opacities[i], a.lr_opacity, a.c1, a.c2);
+  for (int k = 0; k < 3; ++k)
+    adam1(a.colors[k * n + i], a.color_m[k * n + i], a.color_v[k * n + i], a.g_colors[k * n + i], a.lr_color, a.c1,
+          a.c2);
+  // Quaternion renormalisation (optimizer.hpp:133-139).
+  const float norm = sqrtf(sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]));
+  if (norm > 1e-12f) {
+    for (int k = 0; k < 4; ++k) a.rotations[k * n + i] = q[k] / norm;
+  } else {
+    a.rotations[i] = 1.0f;
+    for (int k = 1; k < 4; ++k) a.rotations[k * n + i] = 0.0f;
+  }
+}
+
+void launch_adam(const AdamArgs& a, cudaStream_t stream) {
+  if (a.n == 0) return;
+  k_adam<<<(unsigned)((a.n + 255) / 256), 256, 0, stream>>>(a);
   ++g_launches;
 }
 

@@ -1,0 +1,150 @@
+"""View-sharded training step over the C ABI (BASELINE config 4).
+
+The reference trains on one view per step (optimizer.hpp:99-156). Per-view gradients
+add (GradBuffers::accumulate, backward.hpp:364-373; test_backward.cpp:536-556), so a
+batch of views partitions across GPUs: each rank renders and back-propagates its views
+into one flat gradient buffer, a single all-reduce (sum) exchanges it, and every rank
+applies the identical Adam update — replicas stay bit-identical because the reduced
+buffer is identical everywhere.
+
+Layout of the flat gradient buffer (float32, 16 n): means 3n | rotations 4n |
+log_scales 3n | raw_opacities n | colors 3n | pixel_grad_norm n | one_minus_cos n; the
+int32 `observed` counts travel in a second buffer.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as capi
+from .rasterizer import (CameraPose, Context, GaussianCloud, GradBuffers, RenderOutput, RenderSettings, backward,
+                         render)
+
+FLAT_LAYOUT = (("means", 3), ("rotations", 4), ("log_scales", 3), ("raw_opacities", 1), ("colors", 3),
+               ("pixel_grad_norm", 1), ("one_minus_cos", 1))
+FLAT_WIDTH = sum(w for _, w in FLAT_LAYOUT)  # 16
+
+
+@dataclass
+class TrainConfig:  # optimizer.hpp:23-48 (defaults)
+    iterations: int = 5000
+    lr_means_init: float = 1.6e-4
+    lr_means_final: float = 1.6e-6
+    lr_rotation: float = 1e-3
+    lr_scale: float = 5e-3
+    lr_opacity: float = 0.05
+    lr_color: float = 2.5e-3
+    lambda_ssim: float = 0.0  # the GPU loss is L1 for now (C4 runs at lambda = 0)
+
+
+def means_lr_at(iteration: int, cfg: TrainConfig) -> float:
+    """optimizer.hpp:61-69, evaluated in float like Scalar = float."""
+    f = np.float32
+    lr0, lr1 = f(cfg.lr_means_init), f(cfg.lr_means_final)
+    if cfg.iterations <= 1:
+        return float(lr1)
+    t = min(f(1), f(iteration) / f(cfg.iterations - 1))
+    return float(lr0 * np.power(lr1 / lr0, f(t), dtype=np.float32))
+
+
+def assign_views(n_views: int, rank: int, world: int) -> List[int]:
+    """Views of this rank: v with v % world == rank (every view exactly once)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return list(range(rank, n_views, world))
+
+
+def flat_views(flat, n: int) -> dict:
+    """Splits a flat (16 n) buffer into the GradBuffers members (views, no copies)."""
+    out, off = {}, 0
+    for name, w in FLAT_LAYOUT:
+        seg = flat[off * n:(off + w) * n]
+        out[name] = seg.reshape(w, n) if w > 1 else seg
+        off += w
+    return out
+
+
+def allreduce_grads(flat, observed, group=None):
+    """Sum of the per-rank gradient buffers (the one exchange step of the path)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(observed, op=dist.ReduceOp.SUM, group=group)
+
+
+class ViewShardedTrainer:
+    """C4 training step: render + L1 loss + backward for this rank's views, gradient
+    all-reduce, Adam. Everything stays on the device."""
+
+    def __init__(self, ctx: Context, cloud: GaussianCloud, views: Sequence[CameraPose], targets, settings,
+                 cfg: TrainConfig, extent: float, rank: int = 0, world: int = 1, group=None):
+        import torch
+        self.torch = torch
+        self.ctx, self.cloud, self.views, self.targets = ctx, cloud, list(views), list(targets)
+        self.settings, self.cfg, self.extent = settings, cfg, float(extent)
+        self.rank, self.world, self.group = rank, world, group
+        self.mine = assign_views(len(self.views), rank, world)
+        n = cloud.n
+        dev = cloud.means.device
+        self.n = n
+        self.flat = torch.zeros(FLAT_WIDTH * n, dtype=torch.float32, device=dev)
+        self.observed = torch.zeros(n, dtype=torch.int32, device=dev)
+        fv = flat_views(self.flat, n)
+        self.grads = GradBuffers(fv["means"], fv["rotations"], fv["log_scales"], fv["raw_opacities"],
+                                 fv["colors"], fv["pixel_grad_norm"], fv["one_minus_cos"], self.observed)
+        z = lambda a: torch.zeros_like(a)
+        c = cloud
+        self.state = {k: z(v) for k, v in (("means_m", c.means), ("means_v", c.means), ("rot_m", c.rotations),
+                                            ("rot_v", c.rotations), ("scale_m", c.log_scales),
+                                            ("scale_v", c.log_scales), ("opac_m", c.raw_opacities),
+                                            ("opac_v", c.raw_opacities), ("color_m", c.colors),
+                                            ("color_v", c.colors))}
+        self.state["grad_accum"] = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.state["elev_accum"] = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.state["grad_count"] = torch.zeros(n, dtype=torch.int32, device=dev)
+        H, W = views[0].height, views[0].width
+        self.dl = torch.empty(3 * W * H, dtype=torch.float32, device=dev)
+        self.frame = RenderOutput(ctx)
+        self.iteration = 0
+
+    def step(self) -> float:
+        torch = self.torch
+        ctx, lib = self.ctx, self.ctx.lib
+        self.flat.zero_()
+        self.observed.zero_()
+        loss_sum = 0.0
+        for k, v in enumerate(self.mine):
+            cam = self.views[v]
+            render(ctx, self.cloud, cam, self.settings, out=self.frame)
+            img = self.frame.device_ptr(capi.FRAME_IMAGE)
+            loss = C_double()
+            ctx.check(lib.odgs_photometric_loss(ctx.handle, C_void(img), C_void(self.targets[v].data_ptr()),
+                                                cam.width, cam.height, self.cfg.lambda_ssim,
+                                                C_void(self.dl.data_ptr()), byref(loss)))
+            loss_sum += loss.value
+            backward(ctx, self.cloud, cam, self.frame, self.dl, self.settings, grads=self.grads, accumulate=True)
+        allreduce_grads(self.flat, self.observed, self.group)
+        step = self.iteration + 1
+        p = capi.Params(self.n, self.cloud.means.data_ptr(), self.cloud.rotations.data_ptr(),
+                        self.cloud.log_scales.data_ptr(), self.cloud.raw_opacities.data_ptr(),
+                        self.cloud.colors.data_ptr())
+        st = capi.TrainState(*[self.state[k].data_ptr() for k in (
+            "means_m", "means_v", "rot_m", "rot_v", "scale_m", "scale_v", "opac_m", "opac_v", "color_m", "color_v",
+            "grad_accum", "elev_accum", "grad_count")])
+        ap = capi.AdamParams(means_lr_at(self.iteration, self.cfg) * self.extent, self.cfg.lr_rotation,
+                             self.cfg.lr_scale, self.cfg.lr_opacity, self.cfg.lr_color, step)
+        g = self.grads.to_c()
+        ctx.check(lib.odgs_adam_step(ctx.handle, byref(p), byref(g), byref(st), byref(ap)))
+        self.iteration = step
+        return loss_sum
+
+
+# ctypes shorthands
+import ctypes as _C  # noqa: E402
+
+C_double = _C.c_double
+C_void = _C.c_void_p
+byref = _C.byref

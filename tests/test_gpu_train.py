@@ -1,0 +1,137 @@
+"""GPU training-step kernels vs float32 restatements of the reference formulas:
+photometric_loss at lambda = 0 (metrics.hpp:152-184), adam_update + quaternion
+renormalisation + densify window (optimizer.hpp:74-84, 114-139), and the
+view-sharded step on one GPU (gradients add over views)."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_lib
+from helpers import to_cloud32
+from paper_2410_20686_b200 import CameraPose, GaussianCloud, GradBuffers, RenderSettings, backward, render
+from paper_2410_20686_b200 import _capi as capi
+from paper_2410_20686_b200.train import TrainConfig, ViewShardedTrainer, means_lr_at
+
+pytestmark = pytest.mark.gpu
+f32 = np.float32
+
+
+def test_l1_loss_and_gradient(gpu_ctx):
+    W, H = 256, 128
+    rng = np.random.default_rng(0)
+    a = rng.random(3 * W * H, dtype=np.float32)
+    b = rng.random(3 * W * H, dtype=np.float32)
+    b[:100] = a[:100]  # exact zeros of the difference
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    grad = torch.empty_like(da)
+    loss = C.c_double()
+    gpu_ctx.check(gpu_ctx.lib.odgs_photometric_loss(gpu_ctx.handle, C.c_void_p(da.data_ptr()),
+                                                    C.c_void_p(db.data_ptr()), W, H, 0.0,
+                                                    C.c_void_p(grad.data_ptr()), C.byref(loss)))
+    d = a - b
+    pixels = f32(3 * W * H)
+    expect = (f32(1) * np.sign(d).astype(np.float32)) / pixels
+    assert np.array_equal(grad.cpu().numpy(), expect)
+    ref = float(np.abs(d.astype(np.float64)).sum() / (3 * W * H))
+    assert abs(loss.value - ref) <= 1e-12 * ref
+    g64 = np.empty(3 * W * H)
+    oloss = oracle_lib.lib().oracle_photometric_loss(
+        a.astype(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+        b.astype(np.float64).ctypes.data_as(C.POINTER(C.c_double)), H, W, 0.0,
+        g64.ctypes.data_as(C.POINTER(C.c_double)))
+    assert abs(loss.value - oloss) <= 1e-9 * oloss
+    with pytest.raises(Exception):
+        gpu_ctx.check(gpu_ctx.lib.odgs_photometric_loss(gpu_ctx.handle, C.c_void_p(da.data_ptr()),
+                                                        C.c_void_p(db.data_ptr()), W, H, 0.2,
+                                                        C.c_void_p(grad.data_ptr()), C.byref(loss)))
+
+
+def adam_np(p, m, v, g, lr, step):
+    b1, b2, eps = f32(0.9), f32(0.999), f32(1e-15)
+    m[:] = b1 * m + (f32(1) - b1) * g
+    v[:] = b2 * v + (f32(1) - b2) * (g * g)
+    c1 = f32(1) - np.power(b1, f32(step), dtype=np.float32)
+    c2 = f32(1) - np.power(b2, f32(step), dtype=np.float32)
+    p -= f32(lr) * (m / c1) / (np.sqrt(v / c2) + eps)
+
+
+def test_adam_step_matches_float_restatement(gpu_ctx):
+    n = 5000
+    rng = np.random.default_rng(1)
+    arr = lambda *s: rng.standard_normal(s).astype(np.float32)
+    P = {"means": arr(3, n), "rotations": arr(4, n), "log_scales": arr(3, n), "raw_opacities": arr(n),
+         "colors": arr(3, n)}
+    G = {k: arr(*v.shape) * f32(1e-2) for k, v in P.items()}
+    pgn, omc, obs = np.abs(arr(n)), np.abs(arr(n)), (rng.random(n) < 0.5).astype(np.int32)
+    M = {k: arr(*v.shape) * f32(1e-3) for k, v in P.items()}
+    V = {k: np.abs(arr(*v.shape)) * f32(1e-4) for k, v in P.items()}
+    lrs = {"means": 1.6e-4, "rotations": 1e-3, "log_scales": 5e-3, "raw_opacities": 0.05, "colors": 2.5e-3}
+    step = 7
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    DP, DG, DM, DV = ({k: d(v) for k, v in X.items()} for X in (P, G, M, V))
+    acc = {"grad_accum": d(np.zeros(n, np.float32)), "elev_accum": d(np.zeros(n, np.float32)),
+           "grad_count": d(np.zeros(n, np.int32))}
+    dpgn, domc, dobs = d(pgn), d(omc), d(obs)
+    params = capi.Params(n, *[DP[k].data_ptr() for k in ("means", "rotations", "log_scales", "raw_opacities",
+                                                         "colors")])
+    grads = capi.Grads(*[DG[k].data_ptr() for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")],
+                       dpgn.data_ptr(), domc.data_ptr(), dobs.data_ptr(), capi.MEM_DEVICE)
+    keys = [("means_m", "means", DM), ("means_v", "means", DV), ("rot_m", "rotations", DM),
+            ("rot_v", "rotations", DV), ("scale_m", "log_scales", DM), ("scale_v", "log_scales", DV),
+            ("opac_m", "raw_opacities", DM), ("opac_v", "raw_opacities", DV), ("color_m", "colors", DM),
+            ("color_v", "colors", DV)]
+    st = capi.TrainState(*[src[g].data_ptr() for _, g, src in keys], acc["grad_accum"].data_ptr(),
+                         acc["elev_accum"].data_ptr(), acc["grad_count"].data_ptr())
+    ap = capi.AdamParams(lrs["means"], lrs["rotations"], lrs["log_scales"], lrs["raw_opacities"], lrs["colors"], step)
+    gpu_ctx.check(gpu_ctx.lib.odgs_adam_step(gpu_ctx.handle, C.byref(params), C.byref(grads), C.byref(st),
+                                             C.byref(ap)))
+    torch.cuda.synchronize()
+    for k in P:
+        adam_np(P[k], M[k], V[k], G[k], lrs[k], step)
+    q = P["rotations"]
+    norm = np.sqrt((q[0] * q[0] + q[1] * q[1]) + (q[2] * q[2] + q[3] * q[3]))
+    P["rotations"] = np.where(norm > f32(1e-12), q / norm, np.array([[1], [0], [0], [0]], np.float32))
+    for k in P:
+        assert np.array_equal(DP[k].cpu().numpy(), P[k]), k
+        assert np.array_equal(DM[k].cpu().numpy(), M[k]), k
+        assert np.array_equal(DV[k].cpu().numpy(), V[k]), k
+    assert np.array_equal(acc["grad_accum"].cpu().numpy(), pgn)
+    assert np.array_equal(acc["grad_count"].cpu().numpy(), obs)
+
+
+def test_view_sharded_step_sums_views_on_one_gpu(gpu_ctx):
+    arrs = oracle_lib.random_cloud(301, 4000)
+    host = to_cloud32(arrs)
+    dev = lambda: GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(host, k))).cuda()
+                                  for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")])
+    W, H = 512, 256
+    views = [CameraPose(W, H), CameraPose(W, H, np.eye(3), [0.1, 0.0, -0.2])]
+    tgt = [torch.from_numpy(render(gpu_ctx, to_cloud32(oracle_lib.random_cloud(302, 4000)), v,
+                                   RenderSettings()).image.ravel()).cuda() for v in views]
+    cloud = dev()
+    tr = ViewShardedTrainer(gpu_ctx, cloud, views, tgt, RenderSettings(), TrainConfig(), extent=10.0)
+    # Expected gradient: sum of per-view backward passes of the L1 loss.
+    expected = None
+    for v, t in zip(views, tgt):
+        fr = render(gpu_ctx, cloud, v, RenderSettings())
+        img = torch.from_numpy(fr.image.ravel()).cuda()
+        dl = (torch.sign(img - t) / (3 * W * H)).float()
+        g = backward(gpu_ctx, cloud, v, fr, dl, RenderSettings())
+        expected = g if expected is None else GradBuffers(*[a + b for a, b in zip(
+            (expected.means, expected.rotations, expected.log_scales, expected.raw_opacities, expected.colors,
+             expected.pixel_grad_norm, expected.one_minus_cos, expected.observed),
+            (g.means, g.rotations, g.log_scales, g.raw_opacities, g.colors, g.pixel_grad_norm, g.one_minus_cos,
+             g.observed))])
+    before = cloud.means.clone()
+    losses = [tr.step()]
+    # The trainer's buffer holds the gradient at the pre-update cloud: the view sum.
+    for k in ("means", "rotations", "log_scales", "raw_opacities", "colors", "pixel_grad_norm", "one_minus_cos",
+              "observed"):
+        assert torch.equal(getattr(tr.grads, k), getattr(expected, k)), k
+    losses += [tr.step() for _ in range(2)]
+    assert all(math.isfinite(l) for l in losses)
+    assert losses[-1] < losses[0]
+    assert not torch.equal(before, cloud.means)
