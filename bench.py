@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-steps", type=int, default=5)
     return ap.parse_args()
 
 
@@ -280,6 +282,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * args.steps / float(te.item())
 
+    train = None if args.no_train else run_train(args, ctx, rank, world, local_rank, dev, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         times, cores = cpu_frames(arrs, max_frames=5, min_seconds=10.0)
@@ -301,6 +305,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "stage_rooflines": stage_roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "cpu_baseline": cpu,
+            "train": train,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
@@ -309,6 +314,64 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     frame.destroy()
     e2e_frame.destroy()
     ctx.close()
+
+
+def run_train(args, ctx, rank, world, local_rank, dev, stream):
+    """BASELINE config 4: 3M Gaussians, a batch of 8 views at 2048x1024, views sharded
+    over the ranks, NCCL all-reduce of the gradients, Adam. One step = the whole
+    batch (8 renders + L1 losses + 8 backward passes + all-reduce + Adam)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2410_20686_b200 import GaussianCloud, RenderSettings, render, scenes
+    from paper_2410_20686_b200.train import TrainConfig, ViewShardedTrainer
+
+    n = 3_000_000
+    views = scenes.c4_views(W_IMG, H_IMG, 8)
+    src = scenes.cloud_c4(n, 4001)
+    cloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(src, k))).to(dev)
+                            for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")])
+    tsrc = scenes.cloud_c4(n, 4002)
+    tcloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(tsrc, k))).to(dev)
+                             for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")])
+    settings = RenderSettings()
+    targets = []
+    from paper_2410_20686_b200 import RenderOutput
+    from paper_2410_20686_b200 import _capi as capi
+    tf = RenderOutput(ctx)
+    for v in views:  # targets: renders of a second cloud (SURVEY.md §8d)
+        render(ctx, tcloud, v, settings, out=tf)
+        img = torch.empty(3 * W_IMG * H_IMG, dtype=torch.float32, device=dev)
+        ptr = tf.device_ptr(capi.FRAME_IMAGE)
+        torch.cuda.synchronize()
+        img.copy_(torch.from_numpy(tf.image.ravel()).to(dev))
+        targets.append(img)
+    tf.destroy()
+    del tcloud
+    extent = float(np.sqrt(((src.means - src.means.mean(axis=1, keepdims=True)) ** 2).sum(axis=0).max()))
+    tr = ViewShardedTrainer(ctx, cloud, views, targets, settings, TrainConfig(), extent, rank, world)
+    for _ in range(2):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+    ctx.reset_stage_times()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    losses = [tr.step() for _ in range(args.train_steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    stages = {k: round(v[0] / max(args.train_steps, 1), 4) for k, v in ctx.stage_times().items() if v[1] > 0}
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    return {"metric": "train iters/sec (C4: 3M Gaussians, batch of 8 ERP views at 2048x1024)",
+            "value": args.train_steps / (ms_max / 1000.0), "unit": "iters/s", "ms_per_step": ms_max / args.train_steps,
+            "steps": args.train_steps, "warmup": 2, "views_per_gpu": len(tr.mine), "n_gpus": world,
+            "scaling": "strong", "loss": "L1 (lambda_ssim = 0)", "collective": "NCCL all-reduce (sum) of 16n+n values",
+            "stage_ms_per_step": stages, "first_loss": losses[0], "last_loss": losses[-1]}
 
 
 def main():
