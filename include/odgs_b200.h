@@ -102,6 +102,7 @@ typedef struct {
   int64_t n_splats;    /* projected (RenderOutput::splats.size()) */
   int64_t n_instances; /* seam instances (RenderOutput::instances.size()) */
   int64_t n_entries;   /* tile entries (RenderOutput::tile_entries.size()) */
+  int32_t row_begin, row_end; /* pixel rows rendered (the whole image unless odgs_render_band) */
 } odgs_frame_info;
 
 /* Fields of a rendered frame (RenderOutput, rasterizer.hpp:92-102). */
@@ -202,6 +203,15 @@ odgs_status odgs_prepare_render(odgs_ctx* ctx, const odgs_cloud* cloud, const od
 /* render (rasterizer.hpp:211-267): prepare_render + front-to-back tile blending. */
 odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
                         const odgs_settings* settings, odgs_frame* frame);
+
+/* A row band of a render (large renders split over GPUs): identical to
+   render() on pixel rows [row_begin, row_end) — bit for bit, since per-tile lists depend
+   only on the global (depth, index, shift) order — while only tiles of those rows get
+   entries and are blended. Rows must lie on tile boundaries (row_end may be the image
+   height). Other rows of the frame's image/transmittance/walked are undefined. A
+   backward on a band frame returns that band's share of the gradient (bands add). */
+odgs_status odgs_render_band(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                             const odgs_settings* settings, int32_t row_begin, int32_t row_end, odgs_frame* frame);
 
 /* backward (backward.hpp:380-448) incl. grad_pixels_to_splats (:208-339) for the view
    rendered into `frame` (same cloud, camera, settings — unchecked, as in the

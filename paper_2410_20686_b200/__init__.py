@@ -6,8 +6,8 @@ rasterizer API over that ABI.
 """
 from .rasterizer import (CameraPose, Context, DomainError, GaussianCloud, GradBuffers, InvalidArgument,
                          OdgsError, OdgsRuntimeError, RenderOutput, RenderSettings, backward, cull,
-                         prepare_render, render)
+                         prepare_render, render, render_band)
 
 __all__ = ["CameraPose", "Context", "DomainError", "GaussianCloud", "GradBuffers", "InvalidArgument",
            "OdgsError", "OdgsRuntimeError", "RenderOutput", "RenderSettings", "backward", "cull",
-           "prepare_render", "render"]
+           "prepare_render", "render", "render_band"]

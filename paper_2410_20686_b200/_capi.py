@@ -77,7 +77,8 @@ class AdamParams(C.Structure):
 class FrameInfo(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("n_gaussians", C.c_int64), ("n_splats", C.c_int64),
-                ("n_instances", C.c_int64), ("n_entries", C.c_int64)]
+                ("n_instances", C.c_int64), ("n_entries", C.c_int64), ("row_begin", C.c_int32),
+                ("row_end", C.c_int32)]
 
 
 # Every symbol include/odgs_b200.h declares: name -> (restype, argtypes).
@@ -101,6 +102,8 @@ SIGNATURES = {
     "odgs_frame_device_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "odgs_prepare_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
     "odgs_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
+    "odgs_render_band": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), C.c_int32,
+                                   C.c_int32, _P]),
     "odgs_backward": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), _P, _P, C.c_int32,
                                 C.POINTER(Settings), C.POINTER(Grads), C.POINTER(C.c_double), C.c_uint32]),
     "odgs_ctx_set_profiling": (C.c_int, [_P, C.c_int]),

@@ -57,6 +57,7 @@ struct odgs_frame {
   int64_t n = 0;
   uint32_t n_entries = 0;
   int64_t n_splats = 0, n_instances = 0;
+  int32_t row_begin = 0, row_end = 0;
   bool prepared = false, rendered = false, have_splat_grads = false;
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
   DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, splat_grads, work;
@@ -227,6 +228,8 @@ DevSettings to_dev(const odgs_settings& s) {
   d.cutoff_sigma = s.cutoff_sigma;
   d.lowpass_dilation = s.lowpass_dilation;
   d.max_elevation = s.max_elevation;
+  d.band_ty0 = 0;
+  d.band_ty1 = 1 << 30;
   return d;
 }
 
@@ -268,7 +271,8 @@ odgs_status reset_errors(odgs_ctx* ctx) {
 }
 
 odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
-                         const odgs_settings* settings, odgs_frame* f) {
+                         const odgs_settings* settings, odgs_frame* f, int32_t row_begin = 0,
+                         int32_t row_end = -1) {
   if (!ctx || !f) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "null context or frame");
   odgs_status st;
   if ((st = check_camera(ctx, camera)) != ODGS_OK) return st;
@@ -285,6 +289,15 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   f->n = cloud->n;
   f->cam = to_dev(*camera);
   f->settings = to_dev(*settings);
+  if (row_end < 0) row_end = f->height;
+  if (row_begin < 0 || row_begin >= row_end || row_end > f->height || row_begin % f->tile_size != 0 ||
+      (row_end % f->tile_size != 0 && row_end != f->height))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1,
+                     "render_band: rows must satisfy 0 <= begin < end <= height on tile boundaries");
+  f->row_begin = row_begin;
+  f->row_end = row_end;
+  f->settings.band_ty0 = row_begin / f->tile_size;
+  f->settings.band_ty1 = (row_end + f->tile_size - 1) / f->tile_size;
   const int64_t n = f->n;
   const uint32_t n_tiles = (uint32_t)(f->tiles_x * f->tiles_y);
 
@@ -375,6 +388,8 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   ea.height = f->height;
   ea.tile_size = f->tile_size;
   ea.tiles_x = f->tiles_x;
+  ea.band_ty0 = f->settings.band_ty0;
+  ea.band_ty1 = f->settings.band_ty1;
   ea.out_keys = f->ekeys[0].as<uint32_t>();
   ea.out_vals = f->evals[0].as<uint32_t>();
   ea.ent_off_idx = f->ent_off_idx.as<uint32_t>();
@@ -417,6 +432,8 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ba.tile_size = f->tile_size;
   ba.tiles_x = f->tiles_x;
   ba.tiles_y = f->tiles_y;
+  ba.band_ty0 = f->settings.band_ty0;
+  ba.band_ty1 = f->settings.band_ty1;
   ba.alpha_clamp = f->settings.alpha_clamp;
   ba.transmittance_floor = f->settings.transmittance_floor;
   ba.cutoff_sigma = f->settings.cutoff_sigma;
@@ -621,6 +638,8 @@ odgs_status odgs_frame_get_info(const odgs_frame* f, odgs_frame_info* info) {
   info->n_entries = f->n_entries;
   info->n_splats = f->n_splats;
   info->n_instances = f->n_instances;
+  info->row_begin = f->row_begin;
+  info->row_end = f->row_end;
   return ODGS_OK;
 }
 
@@ -652,6 +671,18 @@ odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_exami
   if (entries_examined) *entries_examined = (int64_t)w[0];
   if (entries_composited) *entries_composited = (int64_t)w[1];
   return ok(ctx);
+}
+
+odgs_status odgs_render_band(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                             const odgs_settings* settings, int32_t row_begin, int32_t row_end, odgs_frame* frame) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  odgs_status st = prepare_impl(ctx, cloud, camera, settings, frame, row_begin, row_end);
+  if (st != ODGS_OK) return st;
+  st = blend_impl(ctx, frame);
+  if (ctx->timers.enabled) resolve_timers(ctx);
+  return st;
 }
 
 odgs_status odgs_frame_device_ptr(odgs_frame* f, int field, void** device_ptr) {
@@ -860,6 +891,8 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   ra.tile_size = f->tile_size;
   ra.tiles_x = f->tiles_x;
   ra.tiles_y = f->tiles_y;
+  ra.band_ty0 = f->settings.band_ty0;
+  ra.band_ty1 = f->settings.band_ty1;
   ra.alpha_clamp = f->settings.alpha_clamp;
   ra.cutoff_sigma = f->settings.cutoff_sigma;
   ra.records = f->records.as<float>();

@@ -40,6 +40,7 @@ struct DevSettings {
   float near_radius, far_radius;
   int tile_size;
   float alpha_clamp, transmittance_floor, cutoff_sigma, lowpass_dilation, max_elevation;
+  int band_ty0, band_ty1;  // tile rows [band_ty0, band_ty1) that get entries (row-band renders)
 };
 
 // Splat flags (sp_c.w as bits).
@@ -176,6 +177,16 @@ __device__ __forceinline__ bool instance_tiles(float mx, float my, float radius,
   if (!instance_box(mx, my, radius, shift_of(k, width), width, height, box)) return false;
   for (int q = 0; q < 4; ++q) span[q] = box[q] / tile_size;
   return true;
+}
+
+// instance_tiles clipped to the tile rows of a row band; false if the instance has
+// no tile inside the band (or does not exist).
+__device__ __forceinline__ bool band_tiles(float mx, float my, float radius, int k, int width, int height,
+                                           int tile_size, int band_ty0, int band_ty1, int span[4]) {
+  if (!instance_tiles(mx, my, radius, k, width, height, tile_size, span)) return false;
+  span[2] = max(span[2], band_ty0);
+  span[3] = min(span[3], band_ty1 - 1);
+  return span[2] <= span[3];
 }
 
 __device__ __forceinline__ void atomic_min_error(unsigned long long* word, long long index, int code) {

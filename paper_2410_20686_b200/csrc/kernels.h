@@ -35,7 +35,7 @@ struct EmitArgs {
   int64_t n;
   const uint32_t *sorted_idx, *cnt_sorted, *off_sorted;
   const float4 *sp_ab, *sp_c;
-  int width, height, tile_size, tiles_x;
+  int width, height, tile_size, tiles_x, band_ty0, band_ty1;
   uint32_t *out_keys, *out_vals, *ent_off_idx;
 };
 void launch_emit(const EmitArgs& a, cudaStream_t stream);
@@ -50,7 +50,7 @@ struct BlendArgs {
   const int32_t* offsets;
   const uint32_t* vals;
   const float4 *sp_ab, *sp_c;
-  int width, height, tile_size, tiles_x, tiles_y;
+  int width, height, tile_size, tiles_x, tiles_y, band_ty0, band_ty1;
   float alpha_clamp, transmittance_floor, cutoff_sigma;
   float* image;
   float* transmittance;
@@ -106,7 +106,7 @@ struct BwdRasterArgs {
   const float* transmittance;
   const int32_t* walked;
   const float* dl_dimage;
-  int width, height, tile_size, tiles_x, tiles_y;
+  int width, height, tile_size, tiles_x, tiles_y, band_ty0, band_ty1;
   float alpha_clamp, cutoff_sigma;
   float* records;  // [K][9] per tile entry, at the entry's emit position
 };

@@ -27,14 +27,14 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
-    float cutoff2, float* __restrict__ records) {
+    float cutoff2, float* __restrict__ records, int band_ty0, int band_ty1) {
   __shared__ float s_cx[kBwdBatch], s_cy[kBwdBatch], s_i00[kBwdBatch], s_i01[kBwdBatch], s_i11[kBwdBatch],
       s_op[kBwdBatch], s_col[3][kBwdBatch];
   __shared__ uint32_t s_pos[kBwdBatch];
   __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];
   __shared__ int s_maxw[kBwdWarps];
 
-  const int tile = blockIdx.x;
+  const int tile = band_ty0 * tiles_x + blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
       uint32_t pos = __ldg(ent_off_idx + g);
       for (int kk = 0; kk <= k; ++kk) {
         int span[4];
-        if (!instance_tiles(a.x, a.y, c.z, kk, width, height, tile_size, span)) continue;
+        if (!band_tiles(a.x, a.y, c.z, kk, width, height, tile_size, band_ty0, band_ty1, span)) continue;
         const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
         if (kk < k) pos += w * (uint32_t)(span[3] - span[2] + 1);
         else pos += (uint32_t)(ty - span[2]) * w + (uint32_t)(tx - span[0]);
@@ -185,14 +185,15 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
 }
 
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
-  const int n_tiles = a.tiles_x * a.tiles_y;
-  if (n_tiles == 0) return;
+  const int n_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
+  if (n_tiles <= 0) return;
   const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
   const int area = a.tile_size * a.tile_size;
 #define ODGS_BWD(PPT)                                                                                             \
   k_bwd_raster<PPT><<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,       \
                                                          a.transmittance, a.walked, a.dl_dimage, a.width, a.height, \
-                                                         a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2, a.records)
+                                                         a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2, a.records, \
+                                                         a.band_ty0, a.band_ty1)
   if (area <= kBwdThreads) ODGS_BWD(1);
   else if (area <= 4 * kBwdThreads) ODGS_BWD(4);
   else ODGS_BWD(16);

@@ -106,8 +106,10 @@ __device__ __forceinline__ uint32_t preprocess_one(
     int span[4];
     if (instance_tiles(mx, my, radius, k, cam.width, cam.height, s.tile_size, span)) {
       flags |= kFlagShiftBase << k;
-      total += (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
       ++n_inst;
+      span[2] = max(span[2], s.band_ty0);
+      span[3] = min(span[3], s.band_ty1 - 1);
+      if (span[2] <= span[3]) total += (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
     }
   }
   sp_ab[2 * i] = make_float4(mx, my, i00, i01);
@@ -170,7 +172,7 @@ constexpr int kEmitWarps = 8;
 __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
     const uint32_t* __restrict__ off_sorted, const float4* __restrict__ sp_ab, const float4* __restrict__ sp_c,
-    int width, int height, int tile_size, int tiles_x, uint32_t* __restrict__ out_keys,
+    int width, int height, int tile_size, int tiles_x, int band_ty0, int band_ty1, uint32_t* __restrict__ out_keys,
     uint32_t* __restrict__ out_vals, uint32_t* __restrict__ ent_off_idx) {
   __shared__ int s_span[kEmitWarps][32][12];
   __shared__ uint32_t s_area[kEmitWarps][32][3];
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     const float radius = sp_c[gid].z;
     for (int k = 0; k < 3; ++k) {
       int span[4];
-      if (instance_tiles(a.x, a.y, radius, k, width, height, tile_size, span)) {
+      if (band_tiles(a.x, a.y, radius, k, width, height, tile_size, band_ty0, band_ty1, span)) {
         areas[k] = (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
         for (int q = 0; q < 4; ++q) s_span[warp][lane][4 * k + q] = span[q];
       }
@@ -240,7 +242,8 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
   const int64_t grid = (warps + kEmitWarps - 1) / kEmitWarps;
   k_emit<<<(unsigned)grid, kEmitWarps * 32, 0, stream>>>(a.n, a.sorted_idx, a.cnt_sorted, a.off_sorted, a.sp_ab,
                                                          a.sp_c, a.width, a.height, a.tile_size, a.tiles_x,
-                                                         a.out_keys, a.out_vals, a.ent_off_idx);
+                                                         a.band_ty0, a.band_ty1, a.out_keys, a.out_vals,
+                                                         a.ent_off_idx);
   ++g_launches;
 }
 
@@ -274,10 +277,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
-    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work) {
+    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base) {
   __shared__ float s_cx[kBlendThreads], s_cy[kBlendThreads], s_i00[kBlendThreads], s_i01x2[kBlendThreads],
       s_i11[kBlendThreads], s_op[kBlendThreads], s_r[kBlendThreads], s_g[kBlendThreads], s_b[kBlendThreads];
-  const int tile = blockIdx.x;
+  const int tile = tile_base + blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile], e1 = offsets[tile + 1];
   const int tid = threadIdx.x;
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
-    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work) {
+    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base) {
   constexpr int kWarps = kBlendThreads / 32;
   __shared__ float4 s_geo[kBlendThreads];  // cx, cy, i00, 2*i01
   __shared__ float4 s_att[kBlendThreads];  // i11, opacity, r, g
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
   __shared__ uint8_t s_list[kWarps][kBlendThreads];
   __shared__ float4 s_wbox[kWarps];  // pixel-centre bbox of each warp: xmin, xmax, ymin, ymax
 
-  const int tile = blockIdx.x;
+  const int tile = tile_base + blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile], e1 = offsets[tile + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -550,10 +553,13 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
 }
 
 void launch_blend(const BlendArgs& a, cudaStream_t stream) {
-  if (!a.plain && a.tile_size <= 16 && a.tiles_x * a.tiles_y > 0) {
-    k_blend_cull<<<a.tiles_x * a.tiles_y, kBlendThreads, 0, stream>>>(
+  const int n_band_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
+  if (n_band_tiles <= 0) return;
+  if (!a.plain && a.tile_size <= 16) {
+    k_blend_cull<<<n_band_tiles, kBlendThreads, 0, stream>>>(
         a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.alpha_clamp,
-        a.transmittance_floor, a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work);
+        a.transmittance_floor, a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work,
+        a.band_ty0 * a.tiles_x);
     ++g_launches;
     return;
   }
@@ -561,15 +567,15 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
 }
 
 void launch_blend_plain(const BlendArgs& a, cudaStream_t stream) {
-  const int n_tiles = a.tiles_x * a.tiles_y;
-  if (n_tiles == 0) return;
+  const int n_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
+  if (n_tiles <= 0) return;
   const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
   const int area = a.tile_size * a.tile_size;
 #define ODGS_BLEND(PPT)                                                                                          \
   k_blend<PPT><<<n_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,    \
                                                       a.tile_size, a.tiles_x, a.alpha_clamp,                    \
                                                       a.transmittance_floor, cutoff2, a.image, a.transmittance, \
-                                                      a.walked, a.work)
+                                                      a.walked, a.work, a.band_ty0 * a.tiles_x)
   if (area <= kBlendThreads) ODGS_BLEND(1);
   else if (area <= 4 * kBlendThreads) ODGS_BLEND(4);
   else ODGS_BLEND(16);

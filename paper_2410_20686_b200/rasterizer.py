@@ -322,6 +322,16 @@ def render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: Ren
     return out
 
 
+def render_band(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings, row_begin: int,
+                row_end: int, out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
+    """Rows [row_begin, row_end) of render(); bit-identical to the full render there."""
+    out = out or RenderOutput(ctx, flags)
+    cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
+    ctx.check(ctx.lib.odgs_render_band(ctx.handle, C.byref(cc), C.byref(cam), C.byref(st), row_begin, row_end,
+                                       out.handle))
+    return out
+
+
 def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: RenderOutput, dl_dimage,
              settings: RenderSettings, signs=None, grads: Optional[GradBuffers] = None,
              accumulate: bool = False) -> GradBuffers:

@@ -45,4 +45,4 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(capi.Settings) == 36
     assert ctypes.sizeof(capi.Camera) == 56
     assert ctypes.sizeof(capi.Cloud) == 56
-    assert ctypes.sizeof(capi.FrameInfo) == 48
+    assert ctypes.sizeof(capi.FrameInfo) == 56
