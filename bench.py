@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--no-large", action="store_true")
     return ap.parse_args()
 
 
@@ -283,6 +284,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e_value = world * args.steps / float(te.item())
 
     train = None if args.no_train else run_train(args, ctx, rank, world, local_rank, dev, stream)
+    large = None if args.no_large else run_large(args, ctx, rank, world, local_rank, dev, stream)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -306,6 +308,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "cpu_baseline": cpu,
             "train": train,
+            "large_render": large,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
@@ -355,6 +358,7 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier(device_ids=[local_rank])
+    ctx.set_profiling(True)
     ctx.reset_stage_times()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -363,6 +367,7 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream):
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     stages = {k: round(v[0] / max(args.train_steps, 1), 4) for k, v in ctx.stage_times().items() if v[1] > 0}
+    ctx.set_profiling(False)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -372,6 +377,77 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream):
             "steps": args.train_steps, "warmup": 2, "views_per_gpu": len(tr.mine), "n_gpus": world,
             "scaling": "strong", "loss": "L1 (lambda_ssim = 0)", "collective": "NCCL all-reduce (sum) of 16n+n values",
             "stage_ms_per_step": stages, "first_loss": losses[0], "last_loss": losses[-1]}
+
+
+def run_large(args, ctx, rank, world, local_rank, dev, stream):
+    """BASELINE config 5: 10M Gaussians at 4096x2048, rank r renders ERP rows
+    [r*H/G, (r+1)*H/G) (odgs_render_band; each band is bit-identical to the full render's
+    rows) and the bands are all-gathered over NCCL into the full image."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2410_20686_b200 import GaussianCloud, RenderOutput, RenderSettings, render_band, scenes
+    from paper_2410_20686_b200 import _capi as capi
+
+    W, H, n = 4096, 2048, 10_000_000
+    src = scenes.cloud_c5(n)
+    cloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(src, k))).to(dev)
+                            for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")])
+    del src
+    rows = H // world
+    r0, r1 = rank * rows, (rank + 1) * rows
+    settings = RenderSettings()
+    fr = RenderOutput(ctx)
+    gathered = torch.empty((world, 3, W, rows), dtype=torch.float32, device=dev) if world > 1 else None
+
+    def frame(k):
+        render_band(ctx, cloud, scenes.yaw_camera(2 * math.pi * k / 16, W, H), settings, r0, r1, out=fr)
+        ptr = fr.device_ptr(capi.FRAME_IMAGE)
+        band = _device_view(ptr, 3 * W * H, dev).view(3, W, H)[:, :, r0:r1].contiguous()
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, band)
+        return band
+
+    for k in range(2):
+        frame(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(device_ids=[local_rank])
+    steps = max(3, min(args.steps, 10))
+    ctx.set_profiling(True)
+    ctx.reset_stage_times()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(steps):
+        frame(k)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    stages = {k: round(v[0] / steps, 4) for k, v in ctx.stage_times().items() if v[1] > 0}
+    ctx.set_profiling(False)
+    info = fr.info()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    fr.destroy()
+    return {"metric": "ERP frames/sec (C5: 10M Gaussians, 4096x2048, row bands over the GPUs)",
+            "value": steps / (ms_max / 1000.0), "unit": "frames/s", "ms_per_frame": ms_max / steps,
+            "bands": world, "rows_per_band": rows, "n_gpus": world, "scaling": "strong",
+            "collective": "NCCL all_gather of the band images" if world > 1 else "none",
+            "band_tile_entries_rank0": info.n_entries, "stage_ms_per_frame_rank0": stages}
+
+
+def _device_view(ptr: int, numel: int, dev):
+    """A float32 torch view of device memory owned by the library (no copy)."""
+    import torch
+
+    class _Holder:
+        pass
+
+    h = _Holder()
+    h.__cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (ptr, False), "version": 2}
+    return torch.as_tensor(h, device=dev)
 
 
 def main():
