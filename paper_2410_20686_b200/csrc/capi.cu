@@ -896,6 +896,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   ra.alpha_clamp = f->settings.alpha_clamp;
   ra.cutoff_sigma = f->settings.cutoff_sigma;
   ra.records = f->records.as<float>();
+  ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
   launch_bwd_raster(ra, s);
   delete bwd_scope;
 

@@ -109,6 +109,7 @@ struct BwdRasterArgs {
   int width, height, tile_size, tiles_x, tiles_y, band_ty0, band_ty1;
   float alpha_clamp, cutoff_sigma;
   float* records;  // [K][9] per tile entry, at the entry's emit position
+  bool plain;      // un-culled reference kernel (A/B checks)
 };
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
 

@@ -184,11 +184,229 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   }
 }
 
+// Culled variant for tiles up to 16x16 (one pixel per thread): the forward's
+// conservative per-warp ellipse test (cull_extents) decides which entries a warp
+// can touch; only those are replayed and warp-reduced. Entries no warp touches
+// keep their zero record (the buffer is cleared before the launch). Skipping is
+// exact: a culled entry has computed d2 > cutoff^2 at every pixel of the warp, so
+// its contribution there is zero and it does not change t or the suffix.
+__global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
+    const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
+    const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
+    const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
+    const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
+    float cutoff2, float* __restrict__ records, int band_ty0, int band_ty1) {
+  __shared__ float4 s_geo[kBwdBatch];   // cx, cy, i00, i01
+  __shared__ float4 s_att[kBwdBatch];   // i11, opacity, r, g
+  __shared__ float s_b[kBwdBatch];
+  __shared__ uint32_t s_pos[kBwdBatch];
+  __shared__ uint8_t s_mask[kBwdBatch];
+  __shared__ uint8_t s_list[kBwdWarps][kBwdBatch];
+  __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];
+  __shared__ int s_maxw[kBwdWarps];
+  __shared__ float4 s_wbox[kBwdWarps];
+
+  const int tile = band_ty0 * tiles_x + blockIdx.x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int e0 = offsets[tile];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t plane = (int64_t)width * height;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  int lx, ly;
+  bool valid;
+  if (tile_size == 16) {
+    lx = (warp >> 1) * 4 + (lane >> 3);
+    ly = (warp & 1) * 8 + (lane & 7);
+    valid = true;
+  } else {
+    lx = tid / tile_size;
+    ly = tid - lx * tile_size;
+    valid = tid < tile_size * tile_size;
+  }
+  const int x = tx * tile_size + lx, y = ty * tile_size + ly;
+  valid = valid && x < width && y < height;
+  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  float t = 1.0f, d0 = 0.0f, d1 = 0.0f, d2v = 0.0f, suf0 = 0.0f, suf1 = 0.0f, suf2 = 0.0f;
+  int wk = 0;
+  if (valid) {
+    const int64_t p = (int64_t)x * height + y;
+    d0 = dl_dimage[p];
+    d1 = dl_dimage[plane + p];
+    d2v = dl_dimage[2 * plane + p];
+    // Only exact zeros are skipped (the reference's float isZero()).
+    if (d0 != 0.0f || d1 != 0.0f || d2v != 0.0f) {
+      wk = walked_in[p];
+      t = transmittance[p];
+    }
+  }
+  // Warp box over the pixels that replay anything; max walk over the CTA.
+  const bool active = wk > 0;
+  float bx0 = active ? px : INFINITY, bx1 = active ? px : -INFINITY;
+  float by0 = active ? py : INFINITY, by1 = active ? py : -INFINITY;
+  int my_max = wk;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, d));
+    bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, d));
+    by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, d));
+    by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, d));
+    my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, d));
+  }
+  if (lane == 0) {
+    s_maxw[warp] = my_max;
+    s_wbox[warp] = make_float4(bx0, bx1, by0, by1);
+  }
+  __syncthreads();
+  int max_walked = 0;
+  for (int w = 0; w < kBwdWarps; ++w) max_walked = max(max_walked, s_maxw[w]);
+
+  for (int hi = max_walked; hi > 0; hi -= kBwdBatch) {
+    const int lo = max(0, hi - kBwdBatch);
+    const int count = hi - lo;
+    if (tid < kBwdBatch) {
+      uint32_t mask = 0;
+      if (tid < count) {
+        const int e = e0 + lo + tid;
+        const uint32_t v = vals[e];
+        const uint32_t g = v >> 2;
+        const int k = (int)(v & 3u);
+        const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+        const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+        const float4 c = __ldg(sp_c + g);
+        const float cx = a.x + shift_of(k, width), cy = a.y;
+        s_geo[tid] = make_float4(cx, cy, a.z, a.w);
+        s_att[tid] = b;
+        s_b[tid] = c.x;
+        float ex, ey;
+        if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
+#pragma unroll
+          for (int w = 0; w < kBwdWarps; ++w) {
+            const float4 bx = s_wbox[w];
+            const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
+            mask |= out ? 0u : (1u << w);
+          }
+        } else {
+          mask = 0xFFu;
+        }
+        if (mask) {
+          // Emit position of (tile, g, k): first entry of g + earlier shifts' areas +
+          // row-major offset inside this shift's (band-clipped) tile rectangle.
+          uint32_t pos = __ldg(ent_off_idx + g);
+          for (int kk = 0; kk <= k; ++kk) {
+            int span[4];
+            if (!band_tiles(a.x, a.y, c.z, kk, width, height, tile_size, band_ty0, band_ty1, span)) continue;
+            const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
+            if (kk < k) pos += w * (uint32_t)(span[3] - span[2] + 1);
+            else pos += (uint32_t)(ty - span[2]) * w + (uint32_t)(tx - span[0]);
+          }
+          s_pos[tid] = pos;
+        }
+      }
+      s_mask[tid] = (uint8_t)mask;
+    }
+    __syncthreads();
+    int n_list = 0;
+#pragma unroll
+    for (int cidx = 0; cidx < kBwdBatch / 32; ++cidx) {
+      const bool mine = (s_mask[cidx * 32 + lane] >> warp) & 1u;
+      const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+      if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(cidx * 32 + lane);
+      n_list += __popc(bal);
+    }
+    __syncwarp();
+    for (int qi = n_list - 1; qi >= 0; --qi) {  // back to front
+      const int j = s_list[warp][qi];
+      const int rel = lo + j;
+      float acc[kRec];
+#pragma unroll
+      for (int c = 0; c < kRec; ++c) acc[c] = 0.0f;
+      bool any = false;
+      if (rel < wk) {
+        const float4 geo = s_geo[j];
+        const float4 att = s_att[j];
+        const float dx = px - geo.x;
+        const float dy = py - geo.y;
+        const float i00 = geo.z, i01 = geo.w, i11 = att.x;
+        const float dd = i00 * dx * dx + 2.0f * i01 * dx * dy + i11 * dy * dy;
+        if (dd <= cutoff2) {
+          const float op = att.y;
+          const float G = pm_expf_blend(-dd / 2.0f);
+          const float raw_alpha = op * G;
+          const float alpha = std_min(alpha_clamp, raw_alpha);
+          const float inv_om = 1.0f / (1.0f - alpha);
+          const float t_here = t * inv_om;
+          const float c0 = att.z, c1 = att.w, c2 = s_b[j];
+          const float at = alpha * t_here;
+          acc[6] = d0 * at;
+          acc[7] = d1 * at;
+          acc[8] = d2v * at;
+          const float v0 = c0 * t_here - suf0 * inv_om;
+          const float v1 = c1 * t_here - suf1 * inv_om;
+          const float v2 = c2 * t_here - suf2 * inv_om;
+          const float dl_dalpha = d0 * v0 + (d1 * v1 + d2v * v2);
+          suf0 += c0 * at;
+          suf1 += c1 * at;
+          suf2 += c2 * at;
+          t = t_here;
+          any = true;
+          if (!(raw_alpha > alpha_clamp)) {  // clamped: no alpha gradient (backward.hpp:289)
+            acc[5] = dl_dalpha * G;
+            const float dl_dd2 = dl_dalpha * op * (-G / 2.0f);
+            const float gx = i00 * dx + i01 * dy;
+            const float gy = i01 * dx + i11 * dy;
+            acc[0] = dl_dd2 * (-2.0f) * gx;
+            acc[1] = dl_dd2 * (-2.0f) * gy;
+            acc[2] = dl_dd2 * dx * dx;
+            acc[3] = dl_dd2 * dx * dy;
+            acc[4] = dl_dd2 * dy * dy;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) {
+          float v = acc[c];
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+          acc[c] = v;
+        }
+      }
+      if (lane < kRec) {
+        float v = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) v = (lane == c) ? acc[c] : v;
+        s_part[warp][j][lane] = v;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < count * kRec; idx += kBwdThreads) {
+      const int j = idx / kRec, c = idx - j * kRec;
+      const uint32_t m = s_mask[j];
+      if (!m) continue;
+      float sum = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kBwdWarps; ++w)
+        if ((m >> w) & 1u) sum += s_part[w][j][c];
+      records[(int64_t)s_pos[j] * kRec + c] = sum;
+    }
+    __syncthreads();
+  }
+}
+
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
   const int n_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
   if (n_tiles <= 0) return;
   const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
   const int area = a.tile_size * a.tile_size;
+  if (!a.plain && a.tile_size <= 16) {
+    k_bwd_raster_cull<<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
+                                                           a.transmittance, a.walked, a.dl_dimage, a.width,
+                                                           a.height, a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2,
+                                                           a.records, a.band_ty0, a.band_ty1);
+    ++g_launches;
+    return;
+  }
 #define ODGS_BWD(PPT)                                                                                             \
   k_bwd_raster<PPT><<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,       \
                                                          a.transmittance, a.walked, a.dl_dimage, a.width, a.height, \

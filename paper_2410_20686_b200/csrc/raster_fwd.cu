@@ -393,27 +393,6 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
 }
 
 // ------------------------------------------------------------------ blend with warp culling
-// Conservative half extents (ex, ey) of an entry's cutoff ellipse such that any pixel
-// whose *computed* offset dx = fl(px - cx) satisfies |dx| > ex (or |dy| > ey) has a
-// computed d2 > cutoff^2, so the reference loop would skip it (rasterizer.hpp:247).
-//   exact:    min_dy Q(dx, dy) = dx^2 / Sigma00 with Sigma00 = i11 / det(conic);
-//   rounding: |fl(d2) - Q| <= 4 eps (|t1|+|t2|+|t3|) <= 4 eps kappa Q with
-//             kappa = (max(i00, i11) + |i01|) * (i00 + i11) / det(conic);
-//   margin:   delta = 64 eps kappa covers that, and the rounding of det and Sigma00
-//             (each <= 3 eps kappa); extents are inflated by (1 + 4 delta) in Q.
-// Ill-conditioned entries (delta >= 0.25) are never culled.
-__device__ __forceinline__ bool cull_extents(float i00, float i01, float i11, float cutoff2, float* ex, float* ey) {
-  const float det = i00 * i11 - i01 * i01;
-  if (!(det > 0.0f) || !(i00 > 0.0f) || !(i11 > 0.0f)) return false;
-  const float kappa = (fmaxf(i00, i11) + fabsf(i01)) * (i00 + i11) / det;
-  const float delta = 64.0f * 1.1920929e-7f * kappa;
-  if (!(delta < 0.25f)) return false;
-  const float f = cutoff2 * (1.0f + 4.0f * delta);
-  *ex = sqrtf(i11 / det * f) * 1.00001f + 1e-4f;
-  *ey = sqrtf(i00 / det * f) * 1.00001f + 1e-4f;
-  return true;
-}
-
 __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,

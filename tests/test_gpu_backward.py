@@ -179,3 +179,18 @@ def test_device_gradient_buffers(gpu_ctx):
     torch.cuda.synchronize()
     for k in GROUPS:
         assert np.array_equal(getattr(dev, k).cpu().numpy(), getattr(host, k)), k
+
+
+def test_culled_backward_matches_plain_backward(gpu_ctx):
+    """The warp-culled backward raster equals the un-culled one (up to the reciprocal
+    used for 1/(1 - alpha)); both are checked against the oracle above."""
+    from paper_2410_20686_b200 import scenes
+    c = scenes.cloud_c3(100_000)
+    cam = CameraPose(1024, 512)
+    gs, _ = settings_pair()
+    dl = probe(9, 1024, 512)
+    a = backward(gpu_ctx, c, cam, render(gpu_ctx, c, cam, gs), dl, gs)
+    b = backward(gpu_ctx, c, cam, render(gpu_ctx, c, cam, gs, flags=capi.FRAME_PLAIN_BLEND), dl, gs)
+    for k in GROUPS:
+        assert group_rel(getattr(a, k), getattr(b, k)) < 1e-4, k
+    assert np.array_equal(a.observed, b.observed)
