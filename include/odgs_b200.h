@@ -123,7 +123,8 @@ typedef enum {
   ODGS_FRAME_SPLAT_OPACITY = 13, /* float [n_splats]                                       */
   ODGS_FRAME_SPLAT_COLOR = 14,   /* float [n_splats][3]                                    */
   ODGS_FRAME_SPLAT_CLAMPED = 15, /* int32 [n_splats] pole clamp engaged                    */
-  /* SplatGrads (backward.hpp:19-25) of the last odgs_backward on this frame: */
+  /* SplatGrads (backward.hpp:19-25) of the last odgs_backward on this frame
+     (needs ODGS_FRAME_KEEP_SPLAT_GRADS): */
   ODGS_FRAME_SPLATGRAD_MEAN = 16,    /* float [n_splats][2]                                */
   ODGS_FRAME_SPLATGRAD_COV2D = 17,   /* float [n_splats][4] full-matrix convention          */
   ODGS_FRAME_SPLATGRAD_OPACITY = 18, /* float [n_splats] w.r.t. activated opacity           */
@@ -134,6 +135,7 @@ typedef enum {
 /* odgs_frame_set_flags */
 #define ODGS_FRAME_KEEP_COV2D 0x1u   /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
 #define ODGS_FRAME_PLAIN_BLEND 0x2u  /* disable warp culling in the blend (A/B checks) */
+#define ODGS_FRAME_KEEP_SPLAT_GRADS 0x4u /* backward also stores SplatGrads (SPLATGRAD_* fields) */
 
 /* odgs_backward flags */
 #define ODGS_ACCUMULATE 0x1u /* add into the gradient buffers (GradBuffers::accumulate) */

@@ -727,7 +727,7 @@ odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* f, int field, void* h
   if (field == ODGS_FRAME_SPLAT_COV2D && !(f->flags & ODGS_FRAME_KEEP_COV2D))
     return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "SPLAT_COV2D needs ODGS_FRAME_KEEP_COV2D");
   if (field >= ODGS_FRAME_SPLATGRAD_MEAN && !f->have_splat_grads)
-    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "no backward on this frame");
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "no backward with ODGS_FRAME_KEEP_SPLAT_GRADS on this frame");
 
   // Reference-format views, materialised on the host from the device arrays.
   HostViews v;
@@ -874,7 +874,8 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
   StageScope* bwd_scope = new StageScope(ctx, ODGS_STAGE_BWD_RASTER);
   if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->records.p, 0, sizeof(float) * 9 * (size_t)K, s));
-  ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
+  const bool keep_sg = (f->flags & ODGS_FRAME_KEEP_SPLAT_GRADS) != 0;
+  if (keep_sg) ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
   if ((st = reset_errors(ctx)) != ODGS_OK) return st;
 
   BwdRasterArgs ra;
@@ -923,14 +924,14 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.g_pixel_grad_norm = gpn;
   sa.g_one_minus_cos = gomc;
   sa.g_observed = gobs;
-  sa.splat_grads = f->splat_grads.as<float>();
+  sa.splat_grads = keep_sg ? f->splat_grads.as<float>() : nullptr;
   sa.err = ctx->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
     launch_bwd_splat(sa, s);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
-  f->have_splat_grads = true;
+  f->have_splat_grads = keep_sg;
 
   if (host_out && n > 0) {
     float* b = ctx->grads_buf.as<float>();

@@ -184,6 +184,82 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   }
 }
 
+// Deterministic butterfly reduce-scatter of 9 per-lane values over a warp (12
+// shuffles instead of 9 x 5). After it, lane l holds the full warp sum of value
+// kValueOfLane[l]; the lanes in kWriterLanes hold values 0..8 respectively.
+// Level xor16 splits {0..4 | 5..8}, xor8 {0,1,2 | 3,4} and {5,6 | 7,8}, xor4 down to
+// {0,1 | 2}, {3 | 4}, {5 | 6}, {7 | 8}, xor2 {0 | 1}, xor1 sums singletons.
+__device__ __forceinline__ float reduce_scatter9(float v[9], int lane) {
+  const unsigned F = 0xffffffffu;
+  const bool hi16 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  // xor16: low keeps 0..4, high keeps 5..8.
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const float send = hi16 ? v[i] : (i < 4 ? v[5 + i] : 0.0f);
+    const float r = __shfl_xor_sync(F, send, 16);
+    if (!hi16) v[i] += r;
+    else if (i < 4) v[5 + i] += r;
+  }
+  // xor8: low: !b3 keeps {0,1,2}, b3 keeps {3,4}; high: !b3 keeps {5,6}, b3 keeps {7,8}.
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float send;
+    if (!hi16) send = b3 ? v[i] : (i < 2 ? v[3 + i] : 0.0f);
+    else send = (i < 2) ? (b3 ? v[5 + i] : v[7 + i]) : 0.0f;
+    const float r = __shfl_xor_sync(F, send, 8);
+    if (!hi16) {
+      if (!b3) v[i] += r;
+      else if (i < 2) v[3 + i] += r;
+    } else if (i < 2) {
+      if (!b3) v[5 + i] += r;
+      else v[7 + i] += r;
+    }
+  }
+  // xor4: {0,1,2} -> {0,1} | {2}; {3,4} -> {3} | {4}; {5,6} -> {5} | {6}; {7,8} -> {7} | {8}.
+  // Two-singleton groups: low&b3 {3,4}; high&!b3 {5,6}; high&b3 {7,8}.
+  const float va = hi16 ? (b3 ? v[7] : v[5]) : v[3];
+  const float vb = hi16 ? (b3 ? v[8] : v[6]) : v[4];
+  float mine = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    float send;
+    if (!hi16 && !b3) send = b2 ? v[i] : (i == 0 ? v[2] : 0.0f);  // {0,1,2}: !b2 keeps {0,1}, b2 keeps {2}
+    else send = (i == 0) ? (b2 ? va : vb) : 0.0f;
+    const float r = __shfl_xor_sync(F, send, 4);
+    if (!hi16 && !b3) {
+      if (!b2) v[i] += r;
+      else if (i == 0) v[2] += r;
+    } else if (i == 0) {
+      mine = (b2 ? vb : va) + r;
+    }
+  }
+  // xor2: group {0,1}: !b1 keeps 0, b1 keeps 1; singletons sum.
+  if (!hi16 && !b3 && !b2) {
+    const float send = b1 ? v[0] : v[1];
+    const float r = __shfl_xor_sync(F, send, 2);
+    mine = (b1 ? v[1] : v[0]) + r;
+  } else {
+    if (!hi16 && !b3) mine = v[2];  // the {2} lanes
+    mine += __shfl_xor_sync(F, mine, 2);
+  }
+  mine += __shfl_xor_sync(F, mine, 1);
+  return mine;
+}
+
+// Which value lane l holds after reduce_scatter9 (its writer lane is the lowest).
+__device__ __forceinline__ int value_of_lane(int lane) {
+  if (lane < 2) return 0;
+  if (lane < 4) return 1;
+  if (lane < 8) return 2;
+  if (lane < 12) return 3;
+  if (lane < 16) return 4;
+  return 5 + ((lane - 16) >> 2);
+}
+__device__ __forceinline__ bool is_writer_lane(int lane) {
+  return lane == 0 || lane == 2 || lane == 4 || lane == 8 || lane == 12 || lane == 16 || lane == 20 || lane == 24 ||
+         lane == 28;
+}
+
 // Culled variant for tiles up to 16x16 (one pixel per thread): the forward's
 // conservative per-warp ellipse test (cull_extents) decides which entries a warp
 // can touch; only those are replayed and warp-reduced. Entries no warp touches
@@ -363,21 +439,9 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
           }
         }
       }
-      if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-        for (int c = 0; c < kRec; ++c) {
-          float v = acc[c];
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-          acc[c] = v;
-        }
-      }
-      if (lane < kRec) {
-        float v = 0.0f;
-#pragma unroll
-        for (int c = 0; c < kRec; ++c) v = (lane == c) ? acc[c] : v;
-        s_part[warp][j][lane] = v;
-      }
+      float red = 0.0f;
+      if (__any_sync(0xffffffffu, any)) red = reduce_scatter9(acc, lane);
+      if (is_writer_lane(lane)) s_part[warp][j][value_of_lane(lane)] = red;
     }
     __syncthreads();
     for (int idx = tid; idx < count * kRec; idx += kBwdThreads) {
@@ -426,6 +490,23 @@ __device__ __forceinline__ bool all_finite(const float* v, int n) {
   return ok;
 }
 
+// jacobian_omni_factored with library float trig (closed form of the factored
+// product, projection.hpp:75-96): rows (kw sec / r)(cp, 0, -sp), (kh / r)(st sp, ct, st cp).
+__device__ __forceinline__ M23 jacobian_factored_fast(float phi, float theta, float r, float W, float H,
+                                                      float max_elevation, bool* clamped) {
+  const bool clamp = fabsf(theta) > max_elevation;
+  *clamped = clamp;
+  const float sec = 1.0f / cosf(clamp ? max_elevation : fabsf(theta));
+  float sp, cp, st, ct;
+  sincosf(phi, &sp, &cp);
+  sincosf(theta, &st, &ct);
+  const float a0 = W / (2.0f * kPiF) * sec / r, a1 = H / kPiF / r;
+  M23 j;
+  j.a[0][0] = a0 * cp; j.a[0][1] = 0.0f; j.a[0][2] = -a0 * sp;
+  j.a[1][0] = a1 * st * sp; j.a[1][1] = a1 * ct; j.a[1][2] = a1 * st * cp;
+  return j;
+}
+
 __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = a.n;
@@ -471,17 +552,21 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
     to_camera(a.cam, p, mu);
     const float x = mu[0], y = mu[1], z = mu[2];
     const float W = (float)a.cam.width, H = (float)a.cam.height;
-    const float phi = pm_atan2f(x, z);
-    const float rho_h = pm_hypotf(x, z);
-    const float theta = pm_atan2f(-y, rho_h);
-    omc = 1.0f - pm_cosf(theta);
+    // The backward is tolerance-checked (not bit-exact), so it uses the fast float
+    // library functions rather than the forward's portable binary64 ones.
+    const float phi = atan2f(x, z);
+    const float rho_h = hypotf(x, z);
+    const float theta = atan2f(-y, rho_h);
+    float st_, ct_;
+    sincosf(theta, &st_, &ct_);
+    omc = 1.0f - ct_;
     const float depth = sqrtf(sum3(x * x, y * y, z * z));
     bool clamped;
-    const M23 J = jacobian_factored(phi, theta, depth, W, H, a.settings.max_elevation, &clamped);
+    const M23 J = jacobian_factored_fast(phi, theta, depth, W, H, a.settings.max_elevation, &clamped);
     const float qn = sqrtf(sum4(qraw[0] * qraw[0], qraw[1] * qraw[1], qraw[2] * qraw[2], qraw[3] * qraw[3]));
     const float qq[4] = {qraw[0] / qn, qraw[1] / qn, qraw[2] / qn, qraw[3] / qn};
     const M3 Rq = quaternion_matrix(qq[0], qq[1], qq[2], qq[3]);
-    const float sc[3] = {pm_expf(ls[0]), pm_expf(ls[1]), pm_expf(ls[2])};
+    const float sc[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
     M3 m;
     for (int rr = 0; rr < 3; ++rr)
       for (int k = 0; k < 3; ++k) m.a[rr][k] = Rq.a[rr][k] * sc[k];
@@ -533,8 +618,10 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
                  kh0 * z * straight * g22 - kh0 * y * (x * x * r2 - 2.0f * z * z * rho2) / (r4 * rho2 * rho) * g23;
       } else {  // grad_position_clamped (backward.hpp:111-150)
         const float r = sqrtf(r2);
-        const float cp = pm_cosf(phi), sp = pm_sinf(phi), ct = pm_cosf(theta), st = pm_sinf(theta);
-        const float sec = 1.0f / pm_cosf(a.settings.max_elevation);
+        float cp, sp;
+        sincosf(phi, &sp, &cp);
+        const float ct = ct_, st = st_;
+        const float sec = 1.0f / cosf(a.settings.max_elevation);
         const float kw = W / (2.0f * kPiF) * sec / r;
         const float kh = H / kPiF / r;
         const float djr[2][3] = {{-kw * cp / r, 0.0f, kw * sp / r}, {-kh * st * sp / r, -kh * ct / r, -kh * st * cp / r}};

@@ -32,7 +32,7 @@ def probe(seed, W, H):
 
 def run_both(ctx, arrs, cam, gs, os_, dl, signs=None, dbl=True, portable=False):
     cloud = to_cloud32(arrs)
-    fr = render(ctx, cloud, cam, gs)
+    fr = render(ctx, cloud, cam, gs, flags=capi.FRAME_KEEP_SPLAT_GRADS)
     g = backward(ctx, cloud, cam, fr, dl, gs, signs=signs)
     r, t = cam32(cam)
     of = oracle_lib.render(arrs, r, t, cam.width, cam.height, os_, dbl=dbl, portable=portable)
