@@ -184,82 +184,6 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   }
 }
 
-// Deterministic butterfly reduce-scatter of 9 per-lane values over a warp (12
-// shuffles instead of 9 x 5). After it, lane l holds the full warp sum of value
-// kValueOfLane[l]; the lanes in kWriterLanes hold values 0..8 respectively.
-// Level xor16 splits {0..4 | 5..8}, xor8 {0,1,2 | 3,4} and {5,6 | 7,8}, xor4 down to
-// {0,1 | 2}, {3 | 4}, {5 | 6}, {7 | 8}, xor2 {0 | 1}, xor1 sums singletons.
-__device__ __forceinline__ float reduce_scatter9(float v[9], int lane) {
-  const unsigned F = 0xffffffffu;
-  const bool hi16 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-  // xor16: low keeps 0..4, high keeps 5..8.
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const float send = hi16 ? v[i] : (i < 4 ? v[5 + i] : 0.0f);
-    const float r = __shfl_xor_sync(F, send, 16);
-    if (!hi16) v[i] += r;
-    else if (i < 4) v[5 + i] += r;
-  }
-  // xor8: low: !b3 keeps {0,1,2}, b3 keeps {3,4}; high: !b3 keeps {5,6}, b3 keeps {7,8}.
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    float send;
-    if (!hi16) send = b3 ? v[i] : (i < 2 ? v[3 + i] : 0.0f);
-    else send = (i < 2) ? (b3 ? v[5 + i] : v[7 + i]) : 0.0f;
-    const float r = __shfl_xor_sync(F, send, 8);
-    if (!hi16) {
-      if (!b3) v[i] += r;
-      else if (i < 2) v[3 + i] += r;
-    } else if (i < 2) {
-      if (!b3) v[5 + i] += r;
-      else v[7 + i] += r;
-    }
-  }
-  // xor4: {0,1,2} -> {0,1} | {2}; {3,4} -> {3} | {4}; {5,6} -> {5} | {6}; {7,8} -> {7} | {8}.
-  // Two-singleton groups: low&b3 {3,4}; high&!b3 {5,6}; high&b3 {7,8}.
-  const float va = hi16 ? (b3 ? v[7] : v[5]) : v[3];
-  const float vb = hi16 ? (b3 ? v[8] : v[6]) : v[4];
-  float mine = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    float send;
-    if (!hi16 && !b3) send = b2 ? v[i] : (i == 0 ? v[2] : 0.0f);  // {0,1,2}: !b2 keeps {0,1}, b2 keeps {2}
-    else send = (i == 0) ? (b2 ? va : vb) : 0.0f;
-    const float r = __shfl_xor_sync(F, send, 4);
-    if (!hi16 && !b3) {
-      if (!b2) v[i] += r;
-      else if (i == 0) v[2] += r;
-    } else if (i == 0) {
-      mine = (b2 ? vb : va) + r;
-    }
-  }
-  // xor2: group {0,1}: !b1 keeps 0, b1 keeps 1; singletons sum.
-  if (!hi16 && !b3 && !b2) {
-    const float send = b1 ? v[0] : v[1];
-    const float r = __shfl_xor_sync(F, send, 2);
-    mine = (b1 ? v[1] : v[0]) + r;
-  } else {
-    if (!hi16 && !b3) mine = v[2];  // the {2} lanes
-    mine += __shfl_xor_sync(F, mine, 2);
-  }
-  mine += __shfl_xor_sync(F, mine, 1);
-  return mine;
-}
-
-// Which value lane l holds after reduce_scatter9 (its writer lane is the lowest).
-__device__ __forceinline__ int value_of_lane(int lane) {
-  if (lane < 2) return 0;
-  if (lane < 4) return 1;
-  if (lane < 8) return 2;
-  if (lane < 12) return 3;
-  if (lane < 16) return 4;
-  return 5 + ((lane - 16) >> 2);
-}
-__device__ __forceinline__ bool is_writer_lane(int lane) {
-  return lane == 0 || lane == 2 || lane == 4 || lane == 8 || lane == 12 || lane == 16 || lane == 20 || lane == 24 ||
-         lane == 28;
-}
-
 // Culled variant for tiles up to 16x16 (one pixel per thread): the forward's
 // conservative per-warp ellipse test (cull_extents) decides which entries a warp
 // can touch; only those are replayed and warp-reduced. Entries no warp touches
@@ -278,7 +202,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
   __shared__ uint32_t s_pos[kBwdBatch];
   __shared__ uint8_t s_mask[kBwdBatch];
   __shared__ uint8_t s_list[kBwdWarps][kBwdBatch];
-  __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];
+  __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];  // 9 sums per (warp, entry)
+  __shared__ uint8_t s_wrote[kBwdWarps][kBwdBatch];
   __shared__ int s_maxw[kBwdWarps];
   __shared__ float4 s_wbox[kBwdWarps];
 
@@ -381,6 +306,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
       }
       s_mask[tid] = (uint8_t)mask;
     }
+    reinterpret_cast<uint32_t*>(&s_wrote[0][0])[tid] = 0u;  // 8 x 128 bytes = 256 words
     __syncthreads();
     int n_list = 0;
 #pragma unroll
@@ -439,20 +365,34 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
           }
         }
       }
-      float red = 0.0f;
-      if (__any_sync(0xffffffffu, any)) red = reduce_scatter9(acc, lane);
-      if (is_writer_lane(lane)) s_part[warp][j][value_of_lane(lane)] = red;
+      if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) {
+          float v = acc[c];
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+          acc[c] = v;
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) s_part[warp][j][c] = acc[c];
+          s_wrote[warp][j] = 1;
+        }
+      }
     }
     __syncthreads();
     for (int idx = tid; idx < count * kRec; idx += kBwdThreads) {
       const int j = idx / kRec, c = idx - j * kRec;
-      const uint32_t m = s_mask[j];
-      if (!m) continue;
+      if (!s_mask[j]) continue;
       float sum = 0.0f;
+      bool any_w = false;
 #pragma unroll
       for (int w = 0; w < kBwdWarps; ++w)
-        if ((m >> w) & 1u) sum += s_part[w][j][c];
-      records[(int64_t)s_pos[j] * kRec + c] = sum;
+        if (s_wrote[w][j]) {
+          sum += s_part[w][j][c];
+          any_w = true;
+        }
+      if (any_w) records[(int64_t)s_pos[j] * kRec + c] = sum;
     }
     __syncthreads();
   }

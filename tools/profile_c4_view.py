@@ -16,8 +16,15 @@ cloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(src, k))).
 cam = scenes.c4_views()[1]
 s = RenderSettings()
 dl = torch.from_numpy(np.random.default_rng(0).uniform(-1e-7, 1e-7, (3, 2048, 1024)).astype(np.float32)).to(dev)
-for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+for _ in range(2):
+    fr = render(ctx, cloud, cam, s)
+    g = backward(ctx, cloud, cam, fr, dl, s)
+ctx.set_profiling(True)
+ctx.reset_stage_times()
+for _ in range(iters):
     fr = render(ctx, cloud, cam, s)
     g = backward(ctx, cloud, cam, fr, dl, s)
 torch.cuda.synchronize()
 print("n_entries", fr.info().n_entries, "work", fr.work())
+print({k: round(v[0] / max(v[1], 1), 4) for k, v in ctx.stage_times().items() if v[1]})
