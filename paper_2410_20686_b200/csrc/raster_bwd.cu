@@ -184,6 +184,55 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   }
 }
 
+// One pixel's contribution to one tile entry in the back-to-front recursion
+// (backward.hpp:271-305), starting from the pixel's state after the entries behind
+// it; updates (t, suffix) and writes the 9 accumulators. False if it contributed
+// nothing (entry beyond the pixel's walk, or d2 > cutoff^2).
+__device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, const float b, int rel, int wk,
+                                            float px, float py, float cutoff2, float alpha_clamp, float d0,
+                                            float d1, float d2v, float& t, float& suf0, float& suf1, float& suf2,
+                                            float acc[kRec]) {
+#pragma unroll
+  for (int c = 0; c < kRec; ++c) acc[c] = 0.0f;
+  if (rel >= wk) return false;
+  const float dx = px - geo.x;
+  const float dy = py - geo.y;
+  const float i00 = geo.z, i01 = geo.w, i11 = att.x;
+  const float dd = i00 * dx * dx + 2.0f * i01 * dx * dy + i11 * dy * dy;
+  if (!(dd <= cutoff2)) return false;
+  const float op = att.y;
+  const float G = pm_expf_blend(-dd / 2.0f);
+  const float raw_alpha = op * G;
+  const float alpha = std_min(alpha_clamp, raw_alpha);
+  const float inv_om = 1.0f / (1.0f - alpha);
+  const float t_here = t * inv_om;
+  const float c0 = att.z, c1 = att.w, c2 = b;
+  const float at = alpha * t_here;
+  acc[6] = d0 * at;
+  acc[7] = d1 * at;
+  acc[8] = d2v * at;
+  const float v0 = c0 * t_here - suf0 * inv_om;
+  const float v1 = c1 * t_here - suf1 * inv_om;
+  const float v2 = c2 * t_here - suf2 * inv_om;
+  const float dl_dalpha = d0 * v0 + (d1 * v1 + d2v * v2);
+  suf0 += c0 * at;
+  suf1 += c1 * at;
+  suf2 += c2 * at;
+  t = t_here;
+  if (!(raw_alpha > alpha_clamp)) {  // clamped: no alpha gradient (backward.hpp:289)
+    acc[5] = dl_dalpha * G;
+    const float dl_dd2 = dl_dalpha * op * (-G / 2.0f);
+    const float gx = i00 * dx + i01 * dy;
+    const float gy = i01 * dx + i11 * dy;
+    acc[0] = dl_dd2 * (-2.0f) * gx;
+    acc[1] = dl_dd2 * (-2.0f) * gy;
+    acc[2] = dl_dd2 * dx * dx;
+    acc[3] = dl_dd2 * dx * dy;
+    acc[4] = dl_dd2 * dy * dy;
+  }
+  return true;
+}
+
 // Culled variant for tiles up to 16x16 (one pixel per thread): the forward's
 // conservative per-warp ellipse test (cull_extents) decides which entries a warp
 // can touch; only those are replayed and warp-reduced. Entries no warp touches
@@ -317,65 +366,43 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
       n_list += __popc(bal);
     }
     __syncwarp();
-    for (int qi = n_list - 1; qi >= 0; --qi) {  // back to front
-      const int j = s_list[warp][qi];
-      const int rel = lo + j;
-      float acc[kRec];
+    // Back to front over this warp's entries, two at a time: both entries' 9
+    // per-pixel contributions are computed (in order), then one butterfly level
+    // splits them across the half-warps (lanes 0-15 keep the first, 16-31 the second)
+    // and four more levels finish both sums — 45 shuffles for 2 entries instead of 90.
+    const bool upper = lane & 16;
+    for (int qi = n_list - 1; qi >= 0; qi -= 2) {
+      const int ja = s_list[warp][qi];
+      const bool has_b = qi >= 1;
+      const int jb = has_b ? s_list[warp][qi - 1] : ja;
+      float A[kRec], B[kRec];
+      const bool any_a = bwd_contrib(s_geo[ja], s_att[ja], s_b[ja], lo + ja, wk, px, py, cutoff2, alpha_clamp, d0, d1,
+                                     d2v, t, suf0, suf1, suf2, A);
+      bool any_b = false;
+      if (has_b)
+        any_b = bwd_contrib(s_geo[jb], s_att[jb], s_b[jb], lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+                            t, suf0, suf1, suf2, B);
+      else {
 #pragma unroll
-      for (int c = 0; c < kRec; ++c) acc[c] = 0.0f;
-      bool any = false;
-      if (rel < wk) {
-        const float4 geo = s_geo[j];
-        const float4 att = s_att[j];
-        const float dx = px - geo.x;
-        const float dy = py - geo.y;
-        const float i00 = geo.z, i01 = geo.w, i11 = att.x;
-        const float dd = i00 * dx * dx + 2.0f * i01 * dx * dy + i11 * dy * dy;
-        if (dd <= cutoff2) {
-          const float op = att.y;
-          const float G = pm_expf_blend(-dd / 2.0f);
-          const float raw_alpha = op * G;
-          const float alpha = std_min(alpha_clamp, raw_alpha);
-          const float inv_om = 1.0f / (1.0f - alpha);
-          const float t_here = t * inv_om;
-          const float c0 = att.z, c1 = att.w, c2 = s_b[j];
-          const float at = alpha * t_here;
-          acc[6] = d0 * at;
-          acc[7] = d1 * at;
-          acc[8] = d2v * at;
-          const float v0 = c0 * t_here - suf0 * inv_om;
-          const float v1 = c1 * t_here - suf1 * inv_om;
-          const float v2 = c2 * t_here - suf2 * inv_om;
-          const float dl_dalpha = d0 * v0 + (d1 * v1 + d2v * v2);
-          suf0 += c0 * at;
-          suf1 += c1 * at;
-          suf2 += c2 * at;
-          t = t_here;
-          any = true;
-          if (!(raw_alpha > alpha_clamp)) {  // clamped: no alpha gradient (backward.hpp:289)
-            acc[5] = dl_dalpha * G;
-            const float dl_dd2 = dl_dalpha * op * (-G / 2.0f);
-            const float gx = i00 * dx + i01 * dy;
-            const float gy = i01 * dx + i11 * dy;
-            acc[0] = dl_dd2 * (-2.0f) * gx;
-            acc[1] = dl_dd2 * (-2.0f) * gy;
-            acc[2] = dl_dd2 * dx * dx;
-            acc[3] = dl_dd2 * dx * dy;
-            acc[4] = dl_dd2 * dy * dy;
-          }
-        }
+        for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
       }
-      if (__any_sync(0xffffffffu, any)) {
+      const unsigned ma = __ballot_sync(0xffffffffu, any_a), mb = __ballot_sync(0xffffffffu, any_b);
+      if (ma | mb) {
+        float K[kRec];
 #pragma unroll
         for (int c = 0; c < kRec; ++c) {
-          float v = acc[c];
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-          acc[c] = v;
+          const float r = __shfl_xor_sync(0xffffffffu, upper ? A[c] : B[c], 16);
+          K[c] = (upper ? B[c] : A[c]) + r;
         }
-        if (lane == 0) {
 #pragma unroll
-          for (int c = 0; c < kRec; ++c) s_part[warp][j][c] = acc[c];
+        for (int d = 8; d > 0; d >>= 1)
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) K[c] += __shfl_xor_sync(0xffffffffu, K[c], d);
+        const bool write = (lane == 0 && ma) || (lane == 16 && mb);
+        if (write) {
+          const int j = upper ? jb : ja;
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) s_part[warp][j][c] = K[c];
           s_wrote[warp][j] = 1;
         }
       }
