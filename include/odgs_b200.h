@@ -69,7 +69,11 @@ typedef struct {
   int32_t height;
 } odgs_camera;
 
-/* GaussianCloud<float> (types.hpp:53-143). All five arrays live in `memory`. */
+/* GaussianCloud<float> (types.hpp:53-143). All arrays live in `memory`.
+   sh_degree / sh_rest: extension beyond the reference (whose colour is RGB only,
+   SPEC.md:83): view-dependent colour c = rgb + sum_k Y_k(d) sh_rest[k] with real SH
+   of degree 1..3 at the world-space view direction d (camera centre to Gaussian);
+   sh_rest is [(deg+1)^2 - 1][3][n]. sh_degree = 0 (sh_rest NULL) is the reference. */
 typedef struct {
   int64_t n;
   const float* means;
@@ -78,6 +82,8 @@ typedef struct {
   const float* raw_opacities;
   const float* colors;
   int32_t memory;
+  int32_t sh_degree;
+  const float* sh_rest;
 } odgs_cloud;
 
 /* GradBuffers<float> (backward.hpp:342-374), same SoA layout as the cloud. */
@@ -91,6 +97,7 @@ typedef struct {
   float* one_minus_cos;
   int32_t* observed;
   int32_t memory;
+  float* sh_rest; /* gradients of sh_rest (SH extension), same layout; NULL if sh_degree = 0 */
 } odgs_grads;
 
 typedef struct odgs_ctx odgs_ctx;

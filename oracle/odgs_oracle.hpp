@@ -129,6 +129,12 @@ template <class S> inline bool finite(S x) { return std::isfinite(x); }
 template <class S> struct Cloud {
   int64_t n = 0;
   std::vector<S> means, rotations, log_scales, raw_opacities, colors;
+  // Extension beyond the reference (SH degree 0 only): view-dependent
+  // colour with real spherical harmonics of degree 1..3. sh_rest holds the
+  // (deg+1)^2 - 1 non-DC coefficients per channel, layout [basis k][channel c][n]:
+  // sh_rest[(3k + c) * n + i]. Degree 0 is exactly the reference's passthrough.
+  int sh_degree = 0;
+  std::vector<S> sh_rest;
   void resize(int64_t m) {  // types.hpp:63-70
     n = m;
     means.assign(3 * m, S(0));
@@ -159,6 +165,8 @@ template <class S> struct Cloud {
       for (int c = 0; c < 3; ++c) ok = ok && finite(ls(i, c));
       ok = ok && finite(raw_opacities[i]);
       for (int c = 0; c < 3; ++c) ok = ok && finite(col(i, c));
+      if (sh_degree > 0)
+        for (int k = 0; k < 3 * ((sh_degree + 1) * (sh_degree + 1) - 1); ++k) ok = ok && finite(sh_rest[k * n + i]);
       if (!ok) return i;
     }
     return -1;
@@ -372,6 +380,93 @@ inline M2<S> project_covariance(const M3<S>& sigma_world, const M3<S>& world_rot
   return cov;
 }
 
+// ------------------------------------------------------------------ SH colour (extension)
+// Real SH basis of degrees 1..3 (the usual 3DGS convention) at unit direction d.
+inline constexpr int sh_count(int degree) { return (degree + 1) * (degree + 1) - 1; }
+
+template <class S> inline void sh_basis(int degree, S x, S y, S z, S Y[15]) {
+  const S C1 = S(0.4886025119029199);
+  const S C2[5] = {S(1.0925484305920792), S(-1.0925484305920792), S(0.31539156525252005), S(-1.0925484305920792),
+                   S(0.5462742152960396)};
+  const S C3[7] = {S(-0.5900435899266435), S(2.890611442640554), S(-0.4570457994644658), S(0.3731763325901154),
+                   S(-0.4570457994644658), S(1.445305721320277), S(-0.5900435899266435)};
+  Y[0] = -C1 * y;
+  Y[1] = C1 * z;
+  Y[2] = -C1 * x;
+  if (degree < 2) return;
+  const S xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  Y[3] = C2[0] * xy;
+  Y[4] = C2[1] * yz;
+  Y[5] = C2[2] * (S(2) * zz - xx - yy);
+  Y[6] = C2[3] * xz;
+  Y[7] = C2[4] * (xx - yy);
+  if (degree < 3) return;
+  Y[8] = C3[0] * y * (S(3) * xx - yy);
+  Y[9] = C3[1] * xy * z;
+  Y[10] = C3[2] * y * (S(4) * zz - xx - yy);
+  Y[11] = C3[3] * z * (S(2) * zz - S(3) * xx - S(3) * yy);
+  Y[12] = C3[4] * x * (S(4) * zz - xx - yy);
+  Y[13] = C3[5] * z * (xx - yy);
+  Y[14] = C3[6] * x * (xx - S(3) * yy);
+}
+
+// d Y_k / d(x, y, z) for the basis above.
+template <class S> inline void sh_basis_grad(int degree, S x, S y, S z, S dY[15][3]) {
+  const S C1 = S(0.4886025119029199);
+  const S C2[5] = {S(1.0925484305920792), S(-1.0925484305920792), S(0.31539156525252005), S(-1.0925484305920792),
+                   S(0.5462742152960396)};
+  const S C3[7] = {S(-0.5900435899266435), S(2.890611442640554), S(-0.4570457994644658), S(0.3731763325901154),
+                   S(-0.4570457994644658), S(1.445305721320277), S(-0.5900435899266435)};
+  const S d1[3][3] = {{0, -C1, 0}, {0, 0, C1}, {-C1, 0, 0}};
+  for (int k = 0; k < 3; ++k)
+    for (int a = 0; a < 3; ++a) dY[k][a] = d1[k][a];
+  if (degree < 2) return;
+  const S xx = x * x, yy = y * y, zz = z * z;
+  const S g2[5][3] = {{C2[0] * y, C2[0] * x, 0},
+                      {0, C2[1] * z, C2[1] * y},
+                      {S(-2) * C2[2] * x, S(-2) * C2[2] * y, S(4) * C2[2] * z},
+                      {C2[3] * z, 0, C2[3] * x},
+                      {S(2) * C2[4] * x, S(-2) * C2[4] * y, 0}};
+  for (int k = 0; k < 5; ++k)
+    for (int a = 0; a < 3; ++a) dY[3 + k][a] = g2[k][a];
+  if (degree < 3) return;
+  const S g3[7][3] = {{S(6) * C3[0] * x * y, C3[0] * (S(3) * xx - S(3) * yy), 0},
+                      {C3[1] * y * z, C3[1] * x * z, C3[1] * x * y},
+                      {S(-2) * C3[2] * x * y, C3[2] * (S(4) * zz - xx - S(3) * yy), S(8) * C3[2] * y * z},
+                      {S(-6) * C3[3] * x * z, S(-6) * C3[3] * y * z, C3[3] * (S(6) * zz - S(3) * xx - S(3) * yy)},
+                      {C3[4] * (S(4) * zz - S(3) * xx - yy), S(-2) * C3[4] * x * y, S(8) * C3[4] * x * z},
+                      {S(2) * C3[5] * x * z, S(-2) * C3[5] * y * z, C3[5] * (xx - yy)},
+                      {C3[6] * (S(3) * xx - S(3) * yy), S(-6) * C3[6] * x * y, 0}};
+  for (int k = 0; k < 7; ++k)
+    for (int a = 0; a < 3; ++a) dY[8 + k][a] = g3[k][a];
+}
+
+// Unit view direction from the camera centre c = -R^T t to the Gaussian (world frame)
+// and the distance; zero direction if the Gaussian sits at the centre.
+template <class S> inline S sh_direction(const Camera<S>& cam, const V3<S>& p, S d[3]) {
+  S v[3];
+  for (int k = 0; k < 3; ++k) {
+    const S cc = -sum3(cam.rotation(0, k) * cam.translation[0], cam.rotation(1, k) * cam.translation[1],
+                       cam.rotation(2, k) * cam.translation[2]);
+    v[k] = p[k] - cc;
+  }
+  const S len = std::sqrt(sum3(v[0] * v[0], v[1] * v[1], v[2] * v[2]));
+  for (int k = 0; k < 3; ++k) d[k] = len > S(0) ? v[k] / len : S(0);
+  return len;
+}
+
+template <class S> inline V3<S> sh_color(const Cloud<S>& cloud, int64_t i, const Camera<S>& cam) {
+  V3<S> c{{cloud.col(i, 0), cloud.col(i, 1), cloud.col(i, 2)}};
+  if (cloud.sh_degree <= 0) return c;
+  S d[3], Y[15];
+  sh_direction(cam, cloud.mean_v(i), d);
+  sh_basis(cloud.sh_degree, d[0], d[1], d[2], Y);
+  const int nb = sh_count(cloud.sh_degree);
+  for (int ch = 0; ch < 3; ++ch)
+    for (int k = 0; k < nb; ++k) c[ch] = c[ch] + Y[k] * cloud.sh_rest[(3 * k + ch) * cloud.n + i];
+  return c;
+}
+
 template <class S> struct Splat2D {  // projection.hpp:163-174
   V2<S> pixel_mean;
   M2<S> cov2d, cov2d_inv;
@@ -407,7 +502,7 @@ inline std::optional<Splat2D<S>> project_gaussian(const Cloud<S>& cloud, int64_t
   splat.radius = settings.cutoff_sigma * std::sqrt(lambda_max);
   splat.depth = depth;
   splat.opacity = sigmoid<S, M>(cloud.raw_opacities[i]);
-  splat.color = {{cloud.col(i, 0), cloud.col(i, 1), cloud.col(i, 2)}};
+  splat.color = sh_color(cloud, i, camera);  // degree 0: the reference's passthrough
   splat.index = i;
   return splat;
 }
@@ -904,9 +999,11 @@ inline std::vector<SplatGrads<S>> grad_pixels_to_splats(const RenderOutput<S>& f
 template <class S> struct GradBuffers {  // backward.hpp:342-374
   int64_t n = 0;
   std::vector<S> means, rotations, log_scales, raw_opacities, colors, pixel_grad_norm, one_minus_cos;
+  std::vector<S> sh_rest;  // extension: gradients of the SH coefficients (same layout as the cloud's)
   std::vector<int32_t> observed;
-  void init(int64_t m) {
+  void init(int64_t m, int sh_coefs = 0) {
     n = m;
+    sh_rest.assign((std::size_t)sh_coefs * m, 0);
     means.assign(3 * m, 0); rotations.assign(4 * m, 0); log_scales.assign(3 * m, 0);
     raw_opacities.assign(m, 0); colors.assign(3 * m, 0);
     pixel_grad_norm.assign(m, 0); one_minus_cos.assign(m, 0); observed.assign(m, 0);
@@ -916,6 +1013,7 @@ template <class S> struct GradBuffers {  // backward.hpp:342-374
     add(means, o.means); add(rotations, o.rotations); add(log_scales, o.log_scales);
     add(raw_opacities, o.raw_opacities); add(colors, o.colors);
     add(pixel_grad_norm, o.pixel_grad_norm); add(one_minus_cos, o.one_minus_cos); add(observed, o.observed);
+    add(sh_rest, o.sh_rest);
   }
 };
 
@@ -927,7 +1025,7 @@ inline GradBuffers<S> backward(const Cloud<S>& cloud, const Camera<S>& camera,
   const auto splat_grads = grad_pixels_to_splats<S, M>(fwd, dl_dimage, settings);
   if (splat_grads_out) *splat_grads_out = splat_grads;
   GradBuffers<S> out;
-  out.init(cloud.n);
+  out.init(cloud.n, cloud.sh_degree > 0 ? 3 * sh_count(cloud.sh_degree) : 0);
   const S width = S(camera.width), height = S(camera.height);
   const int64_t n = cloud.n;
   parallel_for(0, static_cast<int>(fwd.splats.size()), settings.threads, [&](int si) {
@@ -949,7 +1047,25 @@ inline GradBuffers<S> backward(const Cloud<S>& cloud, const Camera<S>& camera,
     const M23<S> jd = jacobian_omni_direct(mu, width, height);
     for (int k = 0; k < 3; ++k) dl_dmu[k] += sum2(jd(0, k) * sg.pixel_mean[0], jd(1, k) * sg.pixel_mean[1]);
     const M3<S> rt = transpose(camera.rotation);
-    const V3<S> gm = mulv(rt, dl_dmu);
+    V3<S> gm = mulv(rt, dl_dmu);
+    if (cloud.sh_degree > 0) {  // SH extension: coefficients and the view-direction term
+      S d[3], Y[15], dY[15][3];
+      const S len = sh_direction(camera, cloud.mean_v(i), d);
+      sh_basis(cloud.sh_degree, d[0], d[1], d[2], Y);
+      sh_basis_grad(cloud.sh_degree, d[0], d[1], d[2], dY);
+      const int nb = sh_count(cloud.sh_degree);
+      S dd[3] = {0, 0, 0};
+      for (int k = 0; k < nb; ++k)
+        for (int ch = 0; ch < 3; ++ch) {
+          out.sh_rest[(std::size_t)(3 * k + ch) * n + i] = sg.color[ch] * Y[k];
+          const S w = sg.color[ch] * cloud.sh_rest[(std::size_t)(3 * k + ch) * n + i];
+          for (int a = 0; a < 3; ++a) dd[a] += w * dY[k][a];
+        }
+      if (len > S(0)) {
+        const S dot = sum3(d[0] * dd[0], d[1] * dd[1], d[2] * dd[2]);
+        for (int a = 0; a < 3; ++a) gm[a] += (dd[a] - d[a] * dot) / len;
+      }
+    }
     for (int k = 0; k < 3; ++k) out.means[k * n + i] = gm[k];
     out.pixel_grad_norm[i] = std::sqrt(sum2(sg.pixel_mean[0] * sg.pixel_mean[0], sg.pixel_mean[1] * sg.pixel_mean[1]));
     const M3<S> dl_dsigma = mul(mul(transpose(t), sg.cov2d), t);
@@ -967,6 +1083,8 @@ inline GradBuffers<S> backward(const Cloud<S>& cloud, const Camera<S>& camera,
     for (int k = 0; k < 3; ++k) ok = ok && finite(out.log_scales[k * n + i]);
     ok = ok && finite(out.raw_opacities[i]);
     for (int k = 0; k < 3; ++k) ok = ok && finite(out.colors[k * n + i]);
+    for (std::size_t k = 0; k < out.sh_rest.size() / (std::size_t)std::max<int64_t>(n, 1); ++k)
+      ok = ok && finite(out.sh_rest[k * n + i]);
     if (!ok) throw std::runtime_error("backward: non-finite gradient for Gaussian " + std::to_string(i));
   }
   return out;

@@ -53,8 +53,11 @@ template <class F> int guarded(char* err, int errlen, F&& f) {
 template <class S>
 void load(Cloud<S>& c, Camera<S>& cam, Settings<S>& s, int64_t n, const double* means, const double* rotations,
           const double* log_scales, const double* raw_opacities, const double* colors, const double* R,
-          const double* t, int width, int height, const double* st, int threads) {
+          const double* t, int width, int height, const double* st, int threads, int sh_degree,
+          const double* sh_rest) {
   c.n = n;
+  c.sh_degree = sh_degree;
+  if (sh_degree > 0) c.sh_rest.assign(sh_rest, sh_rest + 3 * sh_count(sh_degree) * n);
   c.means.assign(means, means + 3 * n);
   c.rotations.assign(rotations, rotations + 4 * n);
   c.log_scales.assign(log_scales, log_scales + 3 * n);
@@ -139,6 +142,7 @@ int64_t get_from(const RenderOutput<S>& r, const GradBuffers<S>& g, const std::v
   if (w == "g_pixel_grad_norm") return copy_out<double>(g.pixel_grad_norm, dst);
   if (w == "g_one_minus_cos") return copy_out<double>(g.one_minus_cos, dst);
   if (w == "g_observed") return copy_out<int32_t>(g.observed, dst);
+  if (w == "g_sh_rest") return copy_out<double>(g.sh_rest, dst);
   auto sg_field = [&](int width, auto getter) -> int64_t {
     if (dst) {
       double* d = static_cast<double*>(dst);
@@ -169,8 +173,8 @@ extern "C" {
 // 3 domain_error, 4 other, with the message in err.
 int oracle_render(int dbl, int portable, int brute, int64_t n, const double* means, const double* rotations,
                   const double* log_scales, const double* raw_opacities, const double* colors, const double* R,
-                  const double* t, int width, int height, const double* st, int threads, void** out, char* err,
-                  int errlen) {
+                  const double* t, int width, int height, const double* st, int threads, int sh_degree,
+                  const double* sh_rest, void** out, char* err, int errlen) {
   auto h = std::make_unique<Handle>();
   h->dbl = dbl != 0;
   h->portable = portable != 0;
@@ -178,12 +182,14 @@ int oracle_render(int dbl, int portable, int brute, int64_t n, const double* mea
   const int rc = guarded(err, errlen, [&] {
     const double t0 = now();
     if (h->dbl) {
-      load(h->cd, h->camd, h->sd, n, means, rotations, log_scales, raw_opacities, colors, R, t, width, height, st, threads);
+      load(h->cd, h->camd, h->sd, n, means, rotations, log_scales, raw_opacities, colors, R, t, width, height, st, threads,
+           sh_degree, sh_rest);
       h->rd = render<double, StdMath>(h->cd, h->camd, h->sd);
       h->seconds_render = now() - t0;
       if (brute) h->brute = brute_force_render<double, StdMath>(h->cd, h->camd, h->sd);
     } else {
-      load(h->cf, h->camf, h->sf, n, means, rotations, log_scales, raw_opacities, colors, R, t, width, height, st, threads);
+      load(h->cf, h->camf, h->sf, n, means, rotations, log_scales, raw_opacities, colors, R, t, width, height, st, threads,
+           sh_degree, sh_rest);
       if (h->portable) {
         h->rf = render<float, PortableMath>(h->cf, h->camf, h->sf);
         h->seconds_render = now() - t0;

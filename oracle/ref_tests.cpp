@@ -1056,6 +1056,58 @@ TEST_CASE("backward: end to end") {  // :434-557
   }
 }
 
+// ================================================================== SH extension (not in the reference)
+TEST_CASE("extension: SH degree 0 is the reference's RGB passthrough") {
+  std::mt19937 rng(55);
+  auto cloud = random_cloud<double>(rng, 50);
+  auto cam = identity_camera<double>(128, 64);
+  const auto a = render(cloud, cam, Settings<double>{});
+  cloud.sh_degree = 0;
+  cloud.sh_rest.clear();
+  const auto b = render(cloud, cam, Settings<double>{});
+  CHECK(image_max_abs_diff(a.image, b.image) == 0.0);
+}
+
+TEST_CASE("extension: SH gradients (degrees 1-3) match finite differences") {
+  for (int degree = 1; degree <= 3; ++degree) {
+    std::mt19937 rng(600 + degree);
+    const auto cam = identity_camera<double>(64, 32);
+    auto settings = fd_settings();
+    Cloud<double> cloud = fd_cloud(rng, 6);
+    cloud.sh_degree = degree;
+    std::normal_distribution<double> g(0.0, 0.05);
+    cloud.sh_rest.resize((std::size_t)3 * sh_count(degree) * cloud.n);
+    for (auto& v : cloud.sh_rest) v = g(rng);
+    Camera<double> pitched = cam;
+    pitched.rotation = angle_axis(0.3, {{1, 0.5, 0.2}});
+    pitched.translation = {{0.1, -0.05, 0.2}};
+    auto fwd = render(cloud, pitched, settings);
+    const auto probe = random_probe(rng, 32, 64);
+    const auto grads = backward(cloud, pitched, fwd, probe, settings);
+    auto group_rel = [&](std::vector<double> Cloud<double>::*field, const std::vector<double>& an_vec) {
+      double max_abs_fd = 0, max_abs_an = 0, max_diff = 0;
+      for (std::size_t k = 0; k < an_vec.size(); ++k) {
+        Cloud<double> hi = cloud, lo = cloud;
+        const double h = 1e-4;
+        (hi.*field)[k] += h;
+        (lo.*field)[k] -= h;
+        const double fd = (probe_loss(hi, pitched, settings, probe) - probe_loss(lo, pitched, settings, probe)) / (2 * h);
+        max_abs_fd = std::max(max_abs_fd, std::abs(fd));
+        max_abs_an = std::max(max_abs_an, std::abs(an_vec[k]));
+        max_diff = std::max(max_diff, std::abs(fd - an_vec[k]));
+      }
+      return max_diff / std::max({max_abs_fd, max_abs_an, 1e-12});
+    };
+    const double e_sh = group_rel(&Cloud<double>::sh_rest, grads.sh_rest);
+    const double e_mu = group_rel(&Cloud<double>::means, grads.means);
+    const double e_col = group_rel(&Cloud<double>::colors, grads.colors);
+    std::printf("  SH degree %d: group-relative FD error sh %.2e means %.2e colors %.2e\n", degree, e_sh, e_mu, e_col);
+    CHECK(e_sh < 1e-3);
+    CHECK(e_mu < 1e-3);
+    CHECK(e_col < 1e-3);
+  }
+}
+
 // ================================================================== acceptance.cpp 1-5
 namespace {
 V3d acc_sample_position(std::mt19937& rng, double margin_rad = 0.0) {  // acceptance.cpp:48-57

@@ -49,14 +49,14 @@ class Camera(C.Structure):
 class Cloud(C.Structure):
     _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("rotations", C.c_void_p),
                 ("log_scales", C.c_void_p), ("raw_opacities", C.c_void_p), ("colors", C.c_void_p),
-                ("memory", C.c_int32)]
+                ("memory", C.c_int32), ("sh_degree", C.c_int32), ("sh_rest", C.c_void_p)]
 
 
 class Grads(C.Structure):
     _fields_ = [("means", C.c_void_p), ("rotations", C.c_void_p), ("log_scales", C.c_void_p),
                 ("raw_opacities", C.c_void_p), ("colors", C.c_void_p),
                 ("pixel_grad_norm", C.c_void_p), ("one_minus_cos", C.c_void_p),
-                ("observed", C.c_void_p), ("memory", C.c_int32)]
+                ("observed", C.c_void_p), ("memory", C.c_int32), ("sh_rest", C.c_void_p)]
 
 
 class Params(C.Structure):

@@ -236,25 +236,32 @@ DevSettings to_dev(const odgs_settings& s) {
 // Resolves the cloud to device pointers, copying host arrays into the context.
 struct CloudPtrs {
   const float *means, *rotations, *log_scales, *raw_opacities, *colors;
+  int sh_degree;
+  const float* sh_rest;
 };
 
 odgs_status resolve_cloud(odgs_ctx* ctx, const odgs_cloud* c, CloudPtrs* out) {
   if (!c) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cloud: null");
   if (c->n < 0 || c->n >= ((int64_t)1 << 30))
     return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cloud: size must be in [0, 2^30)");
+  if (c->sh_degree < 0 || c->sh_degree > 3 || (c->sh_degree > 0 && !c->sh_rest))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "cloud: sh_degree must be 0..3 with sh_rest given");
+  const int nb = c->sh_degree > 0 ? sh_count(c->sh_degree) : 0;
   if (c->memory == ODGS_MEM_DEVICE || c->n == 0) {
-    *out = {c->means, c->rotations, c->log_scales, c->raw_opacities, c->colors};
+    *out = {c->means, c->rotations, c->log_scales, c->raw_opacities, c->colors, c->sh_degree, c->sh_rest};
     return ODGS_OK;
   }
   const int64_t n = c->n;
-  ODGS_CUDA(ctx, ensure(ctx->cloud_buf, sizeof(float) * 14 * n, ctx->stream));
+  ODGS_CUDA(ctx, ensure(ctx->cloud_buf, sizeof(float) * (14 + 3 * nb) * n, ctx->stream));
   float* b = ctx->cloud_buf.as<float>();
-  float* dst[5] = {b, b + 3 * n, b + 7 * n, b + 10 * n, b + 11 * n};
-  const float* src[5] = {c->means, c->rotations, c->log_scales, c->raw_opacities, c->colors};
-  const int64_t width[5] = {3, 4, 3, 1, 3};
-  for (int k = 0; k < 5; ++k)
-    ODGS_CUDA(ctx, cudaMemcpyAsync(dst[k], src[k], sizeof(float) * width[k] * n, cudaMemcpyHostToDevice, ctx->stream));
-  *out = {dst[0], dst[1], dst[2], dst[3], dst[4]};
+  float* dst[6] = {b, b + 3 * n, b + 7 * n, b + 10 * n, b + 11 * n, b + 14 * n};
+  const float* src[6] = {c->means, c->rotations, c->log_scales, c->raw_opacities, c->colors, c->sh_rest};
+  const int64_t width[6] = {3, 4, 3, 1, 3, 3 * nb};
+  for (int k = 0; k < 6; ++k)
+    if (width[k] > 0)
+      ODGS_CUDA(ctx, cudaMemcpyAsync(dst[k], src[k], sizeof(float) * width[k] * n, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+  *out = {dst[0], dst[1], dst[2], dst[3], dst[4], c->sh_degree, nb > 0 ? dst[5] : nullptr};
   return ODGS_OK;
 }
 
@@ -323,6 +330,8 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   pa.log_scales = cp.log_scales;
   pa.raw_opacities = cp.raw_opacities;
   pa.colors = cp.colors;
+  pa.sh_degree = cp.sh_degree;
+  pa.sh_rest = cp.sh_rest;
   pa.cam = f->cam;
   pa.settings = f->settings;
   pa.sp_ab = f->sp_ab.as<float4>();
@@ -855,9 +864,18 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   float *gm = grads->means, *gq = grads->rotations, *gls = grads->log_scales, *gop = grads->raw_opacities,
         *gcol = grads->colors, *gpn = grads->pixel_grad_norm, *gomc = grads->one_minus_cos;
   int32_t* gobs = grads->observed;
+  const int nb = cp.sh_degree > 0 ? sh_count(cp.sh_degree) : 0;
+  if (nb > 0 && !grads->sh_rest)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: sh_rest gradient buffer required for sh_degree > 0");
+  float* gsh = grads->sh_rest;
   if (host_out && n > 0) {
-    ODGS_CUDA(ctx, ensure(ctx->grads_buf, sizeof(float) * 17 * n, s));
+    ODGS_CUDA(ctx, ensure(ctx->grads_buf, sizeof(float) * (17 + 3 * nb) * n, s));
     float* b = ctx->grads_buf.as<float>();
+    if (nb > 0) {
+      if (flags & ODGS_ACCUMULATE)
+        ODGS_CUDA(ctx, cudaMemcpyAsync(b + 17 * n, grads->sh_rest, 4 * 3 * nb * n, cudaMemcpyHostToDevice, s));
+      gsh = b + 17 * n;
+    }
     float* dst[8] = {b, b + 3 * n, b + 7 * n, b + 10 * n, b + 11 * n, b + 14 * n, b + 15 * n, b + 16 * n};
     const void* src[8] = {gm, gq, gls, gop, gcol, gpn, gomc, gobs};
     const int64_t width[8] = {3, 4, 3, 1, 3, 1, 1, 1};
@@ -907,6 +925,9 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.rotations = cp.rotations;
   sa.log_scales = cp.log_scales;
   sa.raw_opacities = cp.raw_opacities;
+  sa.sh_degree = cp.sh_degree;
+  sa.sh_rest = cp.sh_rest;
+  sa.g_sh_rest = gsh;
   sa.cam = f->cam;
   sa.settings = f->settings;
   sa.sp_ab = f->sp_ab.as<float4>();
@@ -941,6 +962,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     const int64_t width[8] = {3, 4, 3, 1, 3, 1, 1, 1};
     for (int k = 0; k < 8; ++k)
       if (dsth[k]) ODGS_CUDA(ctx, cudaMemcpyAsync(dsth[k], srcd[k], 4 * width[k] * n, cudaMemcpyDeviceToHost, s));
+    if (nb > 0) ODGS_CUDA(ctx, cudaMemcpyAsync(grads->sh_rest, gsh, 4 * 3 * nb * n, cudaMemcpyDeviceToHost, s));
   }
   if ((st = read_errors(ctx)) != ODGS_OK) return st;
   if (ctx->timers.enabled) resolve_timers(ctx);

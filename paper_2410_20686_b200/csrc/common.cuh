@@ -210,6 +210,73 @@ __device__ __forceinline__ bool cull_extents(float i00, float i01, float i11, fl
   return true;
 }
 
+// ------------------------------------------------------------------ SH colour (extension)
+// Same basis, constants (double literals rounded to float, as the oracle's S(...))
+// and operation order as oracle::sh_basis / sh_color.
+__host__ __device__ __forceinline__ int sh_count(int degree) { return (degree + 1) * (degree + 1) - 1; }
+
+__device__ __forceinline__ void sh_basis(int degree, float x, float y, float z, float Y[15]) {
+  const float C1 = (float)0.4886025119029199;
+  Y[0] = -C1 * y;
+  Y[1] = C1 * z;
+  Y[2] = -C1 * x;
+  if (degree < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  Y[3] = (float)1.0925484305920792 * xy;
+  Y[4] = (float)-1.0925484305920792 * yz;
+  Y[5] = (float)0.31539156525252005 * (2.0f * zz - xx - yy);
+  Y[6] = (float)-1.0925484305920792 * xz;
+  Y[7] = (float)0.5462742152960396 * (xx - yy);
+  if (degree < 3) return;
+  Y[8] = (float)-0.5900435899266435 * y * (3.0f * xx - yy);
+  Y[9] = (float)2.890611442640554 * xy * z;
+  Y[10] = (float)-0.4570457994644658 * y * (4.0f * zz - xx - yy);
+  Y[11] = (float)0.3731763325901154 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+  Y[12] = (float)-0.4570457994644658 * x * (4.0f * zz - xx - yy);
+  Y[13] = (float)1.445305721320277 * z * (xx - yy);
+  Y[14] = (float)-0.5900435899266435 * x * (xx - 3.0f * yy);
+}
+
+__device__ __forceinline__ void sh_basis_grad(int degree, float x, float y, float z, float dY[15][3]) {
+  const float C1 = (float)0.4886025119029199;
+  dY[0][0] = 0.0f; dY[0][1] = -C1; dY[0][2] = 0.0f;
+  dY[1][0] = 0.0f; dY[1][1] = 0.0f; dY[1][2] = C1;
+  dY[2][0] = -C1; dY[2][1] = 0.0f; dY[2][2] = 0.0f;
+  if (degree < 2) return;
+  const float C2[5] = {(float)1.0925484305920792, (float)-1.0925484305920792, (float)0.31539156525252005,
+                       (float)-1.0925484305920792, (float)0.5462742152960396};
+  const float xx = x * x, yy = y * y, zz = z * z;
+  dY[3][0] = C2[0] * y; dY[3][1] = C2[0] * x; dY[3][2] = 0.0f;
+  dY[4][0] = 0.0f; dY[4][1] = C2[1] * z; dY[4][2] = C2[1] * y;
+  dY[5][0] = -2.0f * C2[2] * x; dY[5][1] = -2.0f * C2[2] * y; dY[5][2] = 4.0f * C2[2] * z;
+  dY[6][0] = C2[3] * z; dY[6][1] = 0.0f; dY[6][2] = C2[3] * x;
+  dY[7][0] = 2.0f * C2[4] * x; dY[7][1] = -2.0f * C2[4] * y; dY[7][2] = 0.0f;
+  if (degree < 3) return;
+  const float C3[7] = {(float)-0.5900435899266435, (float)2.890611442640554, (float)-0.4570457994644658,
+                       (float)0.3731763325901154, (float)-0.4570457994644658, (float)1.445305721320277,
+                       (float)-0.5900435899266435};
+  dY[8][0] = 6.0f * C3[0] * x * y; dY[8][1] = C3[0] * (3.0f * xx - 3.0f * yy); dY[8][2] = 0.0f;
+  dY[9][0] = C3[1] * y * z; dY[9][1] = C3[1] * x * z; dY[9][2] = C3[1] * x * y;
+  dY[10][0] = -2.0f * C3[2] * x * y; dY[10][1] = C3[2] * (4.0f * zz - xx - 3.0f * yy); dY[10][2] = 8.0f * C3[2] * y * z;
+  dY[11][0] = -6.0f * C3[3] * x * z; dY[11][1] = -6.0f * C3[3] * y * z;
+  dY[11][2] = C3[3] * (6.0f * zz - 3.0f * xx - 3.0f * yy);
+  dY[12][0] = C3[4] * (4.0f * zz - 3.0f * xx - yy); dY[12][1] = -2.0f * C3[4] * x * y; dY[12][2] = 8.0f * C3[4] * x * z;
+  dY[13][0] = 2.0f * C3[5] * x * z; dY[13][1] = -2.0f * C3[5] * y * z; dY[13][2] = C3[5] * (xx - yy);
+  dY[14][0] = C3[6] * (3.0f * xx - 3.0f * yy); dY[14][1] = -6.0f * C3[6] * x * y; dY[14][2] = 0.0f;
+}
+
+// World-space unit view direction from the camera centre -R^T t to p (oracle::sh_direction).
+__device__ __forceinline__ float sh_direction(const DevCamera& cam, const float p[3], float d[3]) {
+  float v[3];
+  for (int k = 0; k < 3; ++k) {
+    const float cc = -sum3(cam.R[0][k] * cam.t[0], cam.R[1][k] * cam.t[1], cam.R[2][k] * cam.t[2]);
+    v[k] = p[k] - cc;
+  }
+  const float len = sqrtf(sum3(v[0] * v[0], v[1] * v[1], v[2] * v[2]));
+  for (int k = 0; k < 3; ++k) d[k] = len > 0.0f ? v[k] / len : 0.0f;
+  return len;
+}
+
 __device__ __forceinline__ void atomic_min_error(unsigned long long* word, long long index, int code) {
   atomicMin(word, ((unsigned long long)index << 4) | (unsigned long long)code);
 }

@@ -16,6 +16,8 @@ extern thread_local int64_t g_launches;
 struct PreprocessArgs {
   int64_t n;
   const float *means, *rotations, *log_scales, *raw_opacities, *colors;
+  int sh_degree;
+  const float* sh_rest;  // [(deg+1)^2-1][3][n] or null
   DevCamera cam;
   DevSettings settings;
   float4* sp_ab;   // [2n] {mx,my,i00,i01},{i11,opacity,r,g}
@@ -116,6 +118,9 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
 struct BwdSplatArgs {
   int64_t n;
   const float *means, *rotations, *log_scales, *raw_opacities;
+  int sh_degree;
+  const float* sh_rest;
+  float* g_sh_rest;
   DevCamera cam;
   DevSettings settings;
   const float4 *sp_ab, *sp_c;

@@ -613,6 +613,27 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
     }
     // means = R^T dmu
     for (int c = 0; c < 3; ++c) gm[c] = Rc.a[0][c] * dmu[0] + (Rc.a[1][c] * dmu[1] + Rc.a[2][c] * dmu[2]);
+    if (a.sh_degree > 0) {  // SH extension: coefficient gradients and the view-direction term
+      const int nb = sh_count(a.sh_degree);
+      float d[3], Y[15], dY[15][3];
+      const float len = sh_direction(a.cam, p, d);
+      sh_basis(a.sh_degree, d[0], d[1], d[2], Y);
+      sh_basis_grad(a.sh_degree, d[0], d[1], d[2], dY);
+      float dd[3] = {0.0f, 0.0f, 0.0f};
+      for (int k = 0; k < nb; ++k)
+        for (int ch = 0; ch < 3; ++ch) {
+          const int64_t idx = (int64_t)(3 * k + ch) * n + i;
+          const float g = r[6 + ch] * Y[k];
+          if (a.accumulate) a.g_sh_rest[idx] += g;
+          else a.g_sh_rest[idx] = g;
+          const float w = r[6 + ch] * a.sh_rest[idx];
+          for (int q = 0; q < 3; ++q) dd[q] += w * dY[k][q];
+        }
+      if (len > 0.0f) {
+        const float dot = d[0] * dd[0] + d[1] * dd[1] + d[2] * dd[2];
+        for (int q = 0; q < 3; ++q) gm[q] += (dd[q] - d[q] * dot) / len;
+      }
+    }
     pgn = sqrtf(sg_mean[0] * sg_mean[0] + sg_mean[1] * sg_mean[1]);
 
     // dL/dSigma3D = T^T dcov T; grad_cov3d_params (backward.hpp:156-201)
@@ -661,6 +682,8 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
     for (int k = 0; k < 3; ++k) all[11 + k] = gcol[k];
     if (!all_finite(all, 14)) atomic_min_error(&a.err->bwd_nonfinite, i, 2);
   }
+  if (a.sh_degree > 0 && !(flags & kFlagVisible) && !a.accumulate)
+    for (int k = 0; k < 3 * sh_count(a.sh_degree); ++k) a.g_sh_rest[(int64_t)k * n + i] = 0.0f;
   if (a.accumulate) {
     for (int k = 0; k < 3; ++k) a.g_means[k * n + i] += gm[k];
     for (int k = 0; k < 4; ++k) a.g_rotations[k * n + i] += gq[k];

@@ -23,16 +23,18 @@ namespace odgs_b200 {
 __device__ __forceinline__ uint32_t preprocess_one(
     int64_t i, int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
     const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
-    const float* __restrict__ colors, const DevCamera& cam, const DevSettings& s, float4* __restrict__ sp_ab,
-    float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
-    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, bool* visible) {
+    const float* __restrict__ colors, int sh_degree, const float* __restrict__ sh_rest, const DevCamera& cam,
+    const DevSettings& s, float4* __restrict__ sp_ab, float4* __restrict__ sp_c, float4* __restrict__ cov_out,
+    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err,
+    bool* visible) {
   *visible = false;
   const float p[3] = {__ldg(means + i), __ldg(means + n + i), __ldg(means + 2 * n + i)};
   const float q[4] = {__ldg(rotations + i), __ldg(rotations + n + i), __ldg(rotations + 2 * n + i),
                       __ldg(rotations + 3 * n + i)};
   const float ls[3] = {__ldg(log_scales + i), __ldg(log_scales + n + i), __ldg(log_scales + 2 * n + i)};
   const float raw = __ldg(raw_opacities + i);
-  const float col[3] = {__ldg(colors + i), __ldg(colors + n + i), __ldg(colors + 2 * n + i)};
+  float col[3] = {__ldg(colors + i), __ldg(colors + n + i), __ldg(colors + 2 * n + i)};
+  const int nb = sh_degree > 0 ? sh_count(sh_degree) : 0;
 
   keys[i] = kCulledKey;
   vals[i] = (uint32_t)i;
@@ -42,6 +44,7 @@ __device__ __forceinline__ uint32_t preprocess_one(
   bool finite = isfinite(raw);
   for (int c = 0; c < 3; ++c) finite = finite && isfinite(p[c]) && isfinite(ls[c]) && isfinite(col[c]);
   for (int c = 0; c < 4; ++c) finite = finite && isfinite(q[c]);
+  for (int k = 0; k < 3 * nb; ++k) finite = finite && isfinite(__ldg(sh_rest + (int64_t)k * n + i));
   if (!finite) {
     atomic_min_error(&err->nonfinite, i, 2);
     return 0;
@@ -98,6 +101,13 @@ __device__ __forceinline__ uint32_t preprocess_one(
   const float lambda_max = mid + sqrtf(std_max(0.0f, mid * mid - det));
   const float radius = s.cutoff_sigma * sqrtf(lambda_max);
   const float opacity = 1.0f / (1.0f + pm_expf(-raw));
+  if (nb > 0) {  // SH extension (oracle::sh_color): c = rgb + sum_k Y_k(d) coef_k, in k order
+    float d[3], Y[15];
+    sh_direction(cam, p, d);
+    sh_basis(sh_degree, d[0], d[1], d[2], Y);
+    for (int ch = 0; ch < 3; ++ch)
+      for (int k = 0; k < nb; ++k) col[ch] = col[ch] + Y[k] * __ldg(sh_rest + (int64_t)(3 * k + ch) * n + i);
+  }
 
   // Seam instances (rasterizer.hpp:146-156) and their tile counts (:187-193).
   uint32_t flags = kFlagVisible | (clamped ? kFlagClamped : 0u);
@@ -127,13 +137,14 @@ __global__ void __launch_bounds__(256) k_preprocess(
     const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
     const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
     float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
-    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err) {
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, int sh_degree,
+    const float* __restrict__ sh_rest) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool visible = false;
   uint32_t n_inst = 0;
   if (i < n)
-    n_inst = preprocess_one(i, n, means, rotations, log_scales, raw_opacities, colors, cam, s, sp_ab, sp_c, cov_out,
-                            keys, vals, cnt, err, &visible);
+    n_inst = preprocess_one(i, n, means, rotations, log_scales, raw_opacities, colors, sh_degree, sh_rest, cam, s,
+                            sp_ab, sp_c, cov_out, keys, vals, cnt, err, &visible);
   const uint32_t v_sum = __reduce_add_sync(0xffffffffu, visible ? 1u : 0u);
   const uint32_t i_sum = __reduce_add_sync(0xffffffffu, n_inst);
   if ((threadIdx.x & 31) == 0 && (v_sum | i_sum)) {
@@ -148,7 +159,7 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   const int64_t grid = (a.n + block - 1) / block;
   k_preprocess<<<(unsigned)grid, block, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
                                                      a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
-                                                     a.vals, a.cnt, a.err);
+                                                     a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest);
   ++g_launches;
 }
 

@@ -101,6 +101,8 @@ class GaussianCloud:  # types.hpp:53-143
     log_scales: object     # (3, n)
     raw_opacities: object  # (n,)
     colors: object         # (3, n)
+    sh_degree: int = 0     # extension: view-dependent colour (SH degree 1..3)
+    sh_rest: object = None  # ((deg+1)^2 - 1, 3, n) non-DC coefficients
 
     @property
     def n(self) -> int:
@@ -111,12 +113,15 @@ class GaussianCloud:  # types.hpp:53-143
         return _is_torch(self.means) and self.means.is_cuda
 
     @staticmethod
-    def from_numpy(means, rotations, log_scales, raw_opacities, colors) -> "GaussianCloud":
+    def from_numpy(means, rotations, log_scales, raw_opacities, colors, sh_degree=0, sh_rest=None) -> "GaussianCloud":
         f = lambda a: np.ascontiguousarray(a, dtype=np.float32)
-        return GaussianCloud(f(means), f(rotations), f(log_scales), f(raw_opacities), f(colors))
+        return GaussianCloud(f(means), f(rotations), f(log_scales), f(raw_opacities), f(colors), sh_degree,
+                             None if sh_rest is None else f(sh_rest))
 
     def to_c(self) -> capi.Cloud:
         arrs = (self.means, self.rotations, self.log_scales, self.raw_opacities, self.colors)
+        if self.sh_degree > 0:
+            arrs = arrs + (self.sh_rest,)
         if self.on_device:
             for a in arrs:
                 if not (a.is_contiguous() and str(a.dtype) == "torch.float32"):
@@ -132,7 +137,8 @@ class GaussianCloud:  # types.hpp:53-143
                     raise InvalidArgument("cloud arrays must be C-contiguous float32")
             ptrs = [a.ctypes.data for a in arrs]
             mem = capi.MEM_HOST
-        return capi.Cloud(self.n, *ptrs, mem)
+        sh_ptr = ptrs[5] if self.sh_degree > 0 else None
+        return capi.Cloud(self.n, *ptrs[:5], mem, self.sh_degree, sh_ptr)
 
 
 class Context:
@@ -292,18 +298,23 @@ class GradBuffers:  # backward.hpp:342-374
     pixel_grad_norm: np.ndarray
     one_minus_cos: np.ndarray
     observed: np.ndarray
+    sh_rest: object = None  # SH extension: gradients of the non-DC coefficients
 
     @staticmethod
-    def zeros(n: int) -> "GradBuffers":
+    def zeros(n: int, sh_degree: int = 0) -> "GradBuffers":
         z = lambda *s: np.zeros(s, np.float32)
-        return GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n), np.zeros(n, np.int32))
+        nb = (sh_degree + 1) ** 2 - 1
+        return GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n), np.zeros(n, np.int32),
+                           z(nb, 3, n) if sh_degree > 0 else None)
 
     def to_c(self) -> capi.Grads:
         arrs = (self.means, self.rotations, self.log_scales, self.raw_opacities, self.colors,
                 self.pixel_grad_norm, self.one_minus_cos, self.observed)
         if _is_torch(self.means) and self.means.is_cuda:
-            return capi.Grads(*[a.data_ptr() for a in arrs], capi.MEM_DEVICE)
-        return capi.Grads(*[a.ctypes.data for a in arrs], capi.MEM_HOST)
+            sh = self.sh_rest.data_ptr() if self.sh_rest is not None else None
+            return capi.Grads(*[a.data_ptr() for a in arrs], capi.MEM_DEVICE, sh)
+        sh = self.sh_rest.ctypes.data if self.sh_rest is not None else None
+        return capi.Grads(*[a.ctypes.data for a in arrs], capi.MEM_HOST, sh)
 
 
 def prepare_render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings,
@@ -335,7 +346,7 @@ def render_band(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings
 def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: RenderOutput, dl_dimage,
              settings: RenderSettings, signs=None, grads: Optional[GradBuffers] = None,
              accumulate: bool = False) -> GradBuffers:
-    grads = grads or GradBuffers.zeros(cloud.n)
+    grads = grads or GradBuffers.zeros(cloud.n, cloud.sh_degree)
     cc, cam, st, gc = cloud.to_c(), camera.to_c(), settings.to_c(), grads.to_c()
     if _is_torch(dl_dimage):
         dptr, dmem = dl_dimage.data_ptr(), (capi.MEM_DEVICE if dl_dimage.is_cuda else capi.MEM_HOST)

@@ -34,7 +34,7 @@ def lib() -> C.CDLL:
         dp = C.POINTER(C.c_double)
         L.oracle_render.restype = C.c_int
         L.oracle_render.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, dp, dp, dp, dp, dp, dp, dp, C.c_int,
-                                    C.c_int, dp, C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]
+                                    C.c_int, dp, C.c_int, C.c_int, dp, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]
         L.oracle_backward.restype = C.c_int
         L.oracle_backward.argtypes = [C.c_void_p, dp, C.c_int, C.c_char_p, C.c_int]
         L.oracle_get.restype = C.c_int64
@@ -118,15 +118,18 @@ class OracleFrame:
 
 
 def render(cloud, R, t, width, height, settings: OracleSettings = OracleSettings(), dbl=False, portable=False,
-           brute=False, threads=0) -> OracleFrame:
-    means, rot, ls, op, col = [np.ascontiguousarray(a, dtype=np.float64) for a in cloud]
+           brute=False, threads=0, sh_degree: int = 0, sh_rest=None) -> OracleFrame:
+    """cloud = (means, rotations, log_scales, raw_opacities, colors); sh_rest (3*nb, n)
+    for the SH extension (sh_degree 1..3)."""
+    means, rot, ls, op, col = [np.ascontiguousarray(a, dtype=np.float64) for a in cloud[:5]]
+    sh = np.ascontiguousarray(sh_rest if sh_rest is not None else np.zeros(1), dtype=np.float64)
     R = np.ascontiguousarray(R, dtype=np.float64).reshape(9)
     t = np.ascontiguousarray(t, dtype=np.float64).reshape(3)
     h = C.c_void_p()
     err = C.create_string_buffer(512)
     rc = lib().oracle_render(int(dbl), int(portable), int(brute), op.shape[0], _dp(means), _dp(rot), _dp(ls),
                              _dp(op), _dp(col), _dp(R), _dp(t), width, height, _dp(settings.array()), threads,
-                             C.byref(h), err, 512)
+                             sh_degree, _dp(sh), C.byref(h), err, 512)
     if rc != 0:
         raise OracleError(rc, err.value.decode())
     return OracleFrame(h)

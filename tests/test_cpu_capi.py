@@ -44,5 +44,5 @@ def test_abi_version_and_defaults():
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(capi.Settings) == 36
     assert ctypes.sizeof(capi.Camera) == 56
-    assert ctypes.sizeof(capi.Cloud) == 56
+    assert ctypes.sizeof(capi.Cloud) == 64
     assert ctypes.sizeof(capi.FrameInfo) == 56
