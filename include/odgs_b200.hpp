@@ -106,6 +106,8 @@ template <class Cloud> odgs_cloud to_c_cloud(const Cloud& c) {
   o.raw_opacities = c.raw_opacities.data();
   o.colors = c.colors.data();
   o.memory = ODGS_MEM_HOST;
+  o.sh_degree = 0;  // the reference's clouds are RGB (SH degree 0)
+  o.sh_rest = nullptr;
   return o;
 }
 
@@ -216,6 +218,7 @@ void backward_into(Context& gpu, const Cloud& cloud, const Camera& camera, const
   g.one_minus_cos = out.one_minus_cos.data();
   g.observed = out.observed.data();
   g.memory = ODGS_MEM_HOST;
+  g.sh_rest = nullptr;
   gpu.check(odgs_backward(gpu.get(), &c, &cam, gpu.frame(), dl.data(), ODGS_MEM_HOST, &s, &g, signs,
                           accumulate ? ODGS_ACCUMULATE : 0u));
 }
