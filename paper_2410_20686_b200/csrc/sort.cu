@@ -8,9 +8,12 @@
 //     tile id, ceil(log2 T) bits) — stability keeps that order inside every tile, so
 //     the per-tile lists equal the reference's (rasterizer.hpp:158-205).
 //
-// Each pass = upsweep (per-tile digit histogram) + exclusive scan of the digit-major
-// histogram + downsweep (warp-level ballot ranking, block-local scatter through shared
-// memory, then coalesced-run writes). Tiles are 4096 items (256 threads x 16).
+// Onesweep LSD radix sort: one kernel histograms all passes' digits, then one kernel
+// per pass ranks a 4096-item tile with warp-level ballot matching (stable), finds its
+// global offsets by decoupled look-back, and scatters through shared memory so the
+// writes are runs per digit. 16 B of traffic per item per pass (+4 B once).
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace odgs_b200 {
@@ -100,47 +103,75 @@ __global__ void __launch_bounds__(kThreads) k_scan_downsweep(const uint32_t* __r
   }
 }
 
-// ------------------------------------------------------------------ radix sort
-__global__ void __launch_bounds__(kThreads) k_radix_upsweep(const uint32_t* __restrict__ keys, int64_t n,
-                                                            int shift, int bits, uint32_t* __restrict__ hist,
-                                                            int64_t n_blocks) {
-  __shared__ uint32_t s_cnt[kWarps][256];
-  const int warp = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < kWarps * 256; k += kThreads) (&s_cnt[0][0])[k] = 0;
+// ------------------------------------------------------------------ onesweep (one kernel per pass)
+// Merrill & Adinets' single-pass LSD scheme: one kernel histograms every pass's
+// digits up front; each pass is then a single kernel in which a CTA claims the next
+// tile id (atomic counter, so every predecessor is already resident), ranks its 4096
+// items exactly like k_radix_downsweep, publishes its per-digit counts, and derives
+// its per-digit global offsets by decoupled look-back over the predecessors' status
+// words (flag in the top 2 bits: 1 = tile aggregate, 2 = inclusive prefix).
+constexpr uint32_t kStatAgg = 1u << 30;
+constexpr uint32_t kStatPrefix = 2u << 30;
+constexpr uint32_t kStatMask = (1u << 30) - 1u;
+constexpr int kMaxPasses = 4;
+
+struct PassPlan {
+  int n_passes;
+  int shift[kMaxPasses];
+  int bits[kMaxPasses];
+};
+
+__global__ void __launch_bounds__(kThreads) k_onesweep_hist(const uint32_t* __restrict__ keys, int64_t n,
+                                                            PassPlan plan, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_cnt[kMaxPasses][256];
+  for (int k = threadIdx.x; k < kMaxPasses * 256; k += kThreads) (&s_cnt[0][0])[k] = 0;
   __syncthreads();
-  const uint32_t mask = (1u << bits) - 1u;
-  const int64_t base = (int64_t)blockIdx.x * kTile;
-#pragma unroll 4
-  for (int k = threadIdx.x; k < kTile; k += kThreads) {
-    const int64_t idx = base + k;
-    if (idx < n) atomicAdd(&s_cnt[warp][(keys[idx] >> shift) & mask], 1u);
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const uint32_t key = keys[i];
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p)
+      if (p < plan.n_passes) atomicAdd(&s_cnt[p][(key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u)], 1u);
   }
   __syncthreads();
-  const int radix = 1 << bits;
-  for (int d = threadIdx.x; d < radix; d += kThreads) {
-    uint32_t t = 0;
-    for (int w = 0; w < kWarps; ++w) t += s_cnt[w][d];
-    hist[(int64_t)d * n_blocks + blockIdx.x] = t;
+  for (int k = threadIdx.x; k < kMaxPasses * 256; k += kThreads) {
+    const uint32_t c = (&s_cnt[0][0])[k];
+    if (c) atomicAdd(hist + k, c);
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_radix_downsweep(
+// Exclusive scan of each pass's 256 digit counts (one CTA of 256 threads per pass).
+__global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
+  __shared__ uint32_t s_w[8];
+  const int p = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
+  const uint32_t v = hist[p * 256 + d];
+  const uint32_t incl = warp_inclusive_scan(v, lane);
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int w = 0; w < warp; ++w) off += s_w[w];
+  hist[p * 256 + d] = off + incl - v;
+}
+
+__global__ void __launch_bounds__(kThreads) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ hist_scanned,
-    int64_t n_blocks) {
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ digit_start,
+    uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
   __shared__ uint32_t s_keys[kTile];
   __shared__ uint32_t s_vals[kTile];
   __shared__ uint32_t s_wcnt[kWarps][256];
   __shared__ uint32_t s_start[256];
   __shared__ uint32_t s_gbase[256];
   __shared__ uint32_t s_wsum[kWarps];
+  __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int radix = 1 << bits;
   const uint32_t mask = (uint32_t)radix - 1u;
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
   for (int k = threadIdx.x; k < kWarps * 256; k += kThreads) (&s_wcnt[0][0])[k] = 0;
   __syncthreads();
-
-  const int64_t tile_base = (int64_t)blockIdx.x * kTile;
+  const int tile = s_tile;
+  const int64_t tile_base = (int64_t)tile * kTile;
   const int64_t base = tile_base + (int64_t)warp * kWarpItems;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t key[kIPT], val[kIPT], rank[kIPT];
@@ -150,7 +181,6 @@ __global__ void __launch_bounds__(kThreads) k_radix_downsweep(
     const bool valid = idx < n;
     key[j] = valid ? keys_in[idx] : 0u;
     val[j] = valid ? vals_in[idx] : 0u;
-    // Padding sorts behind every real item of the tile: last digit, largest index.
     const uint32_t d = valid ? (key[j] >> shift) & mask : mask;
     uint32_t peers = 0xffffffffu;
     for (int b = 0; b < bits; ++b) {
@@ -165,7 +195,9 @@ __global__ void __launch_bounds__(kThreads) k_radix_downsweep(
     rank[j] = pre + __popc(peers & lt_mask);
   }
   __syncthreads();
-  // Per digit: exclusive over warps (in place), then exclusive over digits.
+  // Per-digit tile totals (padding excluded: it sits in the last digit, after every
+  // real item, so subtract it from that digit's count).
+  const int64_t valid_count = n - tile_base < kTile ? n - tile_base : kTile;
   uint32_t digit_total = 0;
   if (threadIdx.x < radix) {
     const int d = threadIdx.x;
@@ -175,16 +207,34 @@ __global__ void __launch_bounds__(kThreads) k_radix_downsweep(
       digit_total += c;
     }
   }
-  // Block exclusive scan of digit_total over threadIdx (digits), 256 threads.
   const uint32_t incl = warp_inclusive_scan(digit_total, lane);
   if (lane == 31) s_wsum[warp] = incl;
   __syncthreads();
   uint32_t woff = 0;
   for (int w = 0; w < warp; ++w) woff += s_wsum[w];
   if (threadIdx.x < radix) {
+    const int d = threadIdx.x;
     const uint32_t start = woff + incl - digit_total;
-    s_start[threadIdx.x] = start;
-    s_gbase[threadIdx.x] = hist_scanned[(int64_t)threadIdx.x * n_blocks + blockIdx.x] - start;
+    s_start[d] = start;
+    const uint32_t real = (d == radix - 1) ? digit_total - (uint32_t)(kTile - valid_count) : digit_total;
+    // Publish, then look back over the predecessors for this digit's exclusive prefix.
+    volatile uint32_t* st = status;
+    if (tile == 0) {
+      st[d] = kStatPrefix | real;
+      s_gbase[d] = digit_start[d] - start;
+    } else {
+      st[(int64_t)tile * 256 + d] = kStatAgg | real;
+      uint32_t excl = 0;
+      for (int look = tile - 1; look >= 0;) {
+        const uint32_t w = st[(int64_t)look * 256 + d];
+        if ((w & ~kStatMask) == 0) continue;  // predecessor not published yet: spin
+        excl += w & kStatMask;
+        if (w & kStatPrefix) break;
+        --look;
+      }
+      st[(int64_t)tile * 256 + d] = kStatPrefix | (excl + real);
+      s_gbase[d] = digit_start[d] + excl - start;
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -196,7 +246,6 @@ __global__ void __launch_bounds__(kThreads) k_radix_downsweep(
     s_vals[pos] = val[j];
   }
   __syncthreads();
-  const int64_t valid_count = n - tile_base < kTile ? n - tile_base : kTile;
   for (int k = threadIdx.x; k < valid_count; k += kThreads) {
     const uint32_t kk = s_keys[k];
     const uint32_t d = (kk >> shift) & mask;
@@ -239,32 +288,42 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
 
 size_t radix_sort_temp_bytes(int64_t n) {
   const int64_t nb = blocks_for(n > 0 ? n : 1);
-  const int64_t hist = 256 * nb;
-  return (size_t)(2 * hist) * sizeof(uint32_t) + 256 + scan_temp_bytes(hist);
+  // hist [kMaxPasses][256] + status [nb][256] + tile counters [kMaxPasses] (+ alignment)
+  return (size_t)(kMaxPasses * 256 + nb * 256 + kMaxPasses + 64) * sizeof(uint32_t);
 }
 
 void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
                       int* which, cudaStream_t stream) {
-  int cur = 0;
   *which = 0;
   if (n <= 1 || end_bit <= begin_bit) return;
+  PassPlan plan{};
+  int passes = (end_bit - begin_bit + 7) / 8;
+  if (passes > kMaxPasses) passes = kMaxPasses;
+  plan.n_passes = passes;
+  for (int bit = begin_bit, p = 0, left = passes; p < passes; ++p, --left) {
+    const int bits = (end_bit - bit + left - 1) / left;
+    plan.shift[p] = bit;
+    plan.bits[p] = bits;
+    bit += bits;
+  }
   const int64_t nb = blocks_for(n);
   uint32_t* hist = static_cast<uint32_t*>(temp);
-  uint32_t* hist_scanned = hist + 256 * nb;
-  void* scan_tmp = reinterpret_cast<char*>(temp) + (((size_t)(2 * 256 * nb) * sizeof(uint32_t) + 255) / 256) * 256;
-  int bit = begin_bit;
-  int passes = (end_bit - begin_bit + 7) / 8;
-  while (bit < end_bit) {
-    const int bits = (end_bit - bit + passes - 1) / passes;
-    --passes;
-    k_radix_upsweep<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], n, bit, bits, hist, nb);
-    ++g_launches;
-    exclusive_scan_u32(hist, hist_scanned, (int64_t)(1 << bits) * nb, scan_tmp, nullptr, stream);
-    k_radix_downsweep<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
-                                                             bit, bits, hist_scanned, nb);
+  uint32_t* counters = hist + kMaxPasses * 256;
+  uint32_t* status = counters + 64;
+  cudaMemsetAsync(hist, 0, (kMaxPasses * 256 + 64) * sizeof(uint32_t), stream);
+  int sms = 148;
+  k_onesweep_hist<<<(unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream>>>(keys[0], n, plan, hist);
+  ++g_launches;
+  k_onesweep_hist_scan<<<passes, 256, 0, stream>>>(hist);
+  ++g_launches;
+  int cur = 0;
+  for (int p = 0; p < passes; ++p) {
+    cudaMemsetAsync(status, 0, (size_t)nb * 256 * sizeof(uint32_t), stream);
+    k_onesweep_pass<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
+                                                           plan.shift[p], plan.bits[p], hist + p * 256, status,
+                                                           counters + p);
     ++g_launches;
     cur ^= 1;
-    bit += bits;
   }
   *which = cur;
 }
