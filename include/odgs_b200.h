@@ -143,7 +143,6 @@ typedef enum {
 #define ODGS_FRAME_KEEP_COV2D 0x1u   /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
 #define ODGS_FRAME_PLAIN_BLEND 0x2u  /* disable warp culling in the blend (A/B checks) */
 #define ODGS_FRAME_KEEP_SPLAT_GRADS 0x4u /* backward also stores SplatGrads (SPLATGRAD_* fields) */
-#define ODGS_FRAME_BLEND_1PX 0x8u        /* one pixel per thread in the culled blend (A/B checks) */
 
 /* odgs_backward flags */
 #define ODGS_ACCUMULATE 0x1u /* add into the gradient buffers (GradBuffers::accumulate) */

@@ -19,7 +19,6 @@ ACCUMULATE = 0x1
 FRAME_KEEP_COV2D = 0x1
 FRAME_PLAIN_BLEND = 0x2
 FRAME_KEEP_SPLAT_GRADS = 0x4
-FRAME_BLEND_1PX = 0x8
 
 (FRAME_IMAGE, FRAME_TRANSMITTANCE, FRAME_WALKED, FRAME_TILE_OFFSETS, FRAME_TILE_ENTRIES,
  FRAME_INSTANCE_SPLAT, FRAME_INSTANCE_SHIFT, FRAME_SPLAT_INDEX, FRAME_SPLAT_MEAN, FRAME_SPLAT_COV2D,

@@ -451,7 +451,6 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ba.walked = f->walked.as<int32_t>();
   ba.work = f->work.as<unsigned long long>();
   ba.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
-  ba.one_pixel_per_thread = (f->flags & ODGS_FRAME_BLEND_1PX) != 0;
   {
     StageScope sc(ctx, ODGS_STAGE_BLEND);
     launch_blend(ba, s);

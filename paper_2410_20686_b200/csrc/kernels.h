@@ -59,7 +59,6 @@ struct BlendArgs {
   int32_t* walked;
   unsigned long long* work;  // [2] += entries examined, entries composited (or null)
   bool plain;                // force the un-culled reference kernel (A/B checks)
-  bool one_pixel_per_thread; // force k_blend_cull over k_blend_cull2 (A/B checks)
 };
 void launch_blend(const BlendArgs& a, cudaStream_t stream);
 void launch_blend_plain(const BlendArgs& a, cudaStream_t stream);

@@ -542,169 +542,9 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
   }
 }
 
-// 16x16 tiles, two pixels per lane: 4 warps per tile, each owning an 8x8 block
-// (lane l: x = l/8 and x + 4, y = l%8), so every staged entry's shared-memory loads,
-// cull test and loop control are shared by two pixels. Same batch/mask/compaction
-// scheme and the same exactness argument as k_blend_cull.
-constexpr int kBlend2Threads = 128;
-constexpr int kBlend2Batch = 256;
-
-__device__ __forceinline__ void composite_one(const float4 geo, const float4 att, const float b, float px, float py,
-                                              float cutoff2, float alpha_clamp, float floor_t, int e_rel,
-                                              float& t, float& cr, float& cg, float& cb, int& walked, bool& done,
-                                              uint32_t& contrib) {
-  const float dx = px - geo.x;
-  const float dy = py - geo.y;
-  const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
-  if (d2 > cutoff2) return;
-  const float alpha = std_min(alpha_clamp, att.y * pm_expf_blend(-d2 / 2.0f));
-  const float t_next = t * (1.0f - alpha);
-  if (t_next < floor_t) {
-    walked = e_rel;
-    done = true;
-    return;
-  }
-  const float wgt = alpha * t;
-  ++contrib;
-  cr = cr + att.z * wgt;
-  cg = cg + att.w * wgt;
-  cb = cb + b * wgt;
-  t = t_next;
-}
-
-__global__ void __launch_bounds__(kBlend2Threads) k_blend_cull2(
-    const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
-    const float4* __restrict__ sp_c, int width, int height, int tiles_x, float alpha_clamp,
-    float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
-    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base) {
-  constexpr int kWarps = kBlend2Threads / 32;
-  __shared__ float4 s_geo[kBlend2Batch];
-  __shared__ float4 s_att[kBlend2Batch];
-  __shared__ float s_b[kBlend2Batch];
-  __shared__ uint8_t s_mask[kBlend2Batch];
-  __shared__ uint8_t s_list[kWarps][kBlend2Batch];
-  __shared__ float4 s_wbox[kWarps];
-
-  const int tile = tile_base + blockIdx.x;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int e0 = offsets[tile], e1 = offsets[tile + 1];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int bx = (warp >> 1) * 8, by = (warp & 1) * 8;
-  const int x0 = tx * 16 + bx + (lane >> 3), y = ty * 16 + by + (lane & 7);
-  const int x1 = x0 + 4;
-  const bool v0 = x0 < width && y < height, v1 = x1 < width && y < height;
-  const float px0 = (float)x0 + 0.5f, px1 = (float)x1 + 0.5f, py = (float)y + 0.5f;
-  {
-    float xmin = v0 ? px0 : (v1 ? px1 : INFINITY), xmax = v1 ? px1 : (v0 ? px0 : -INFINITY);
-    float ymin = (v0 || v1) ? py : INFINITY, ymax = (v0 || v1) ? py : -INFINITY;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      xmin = fminf(xmin, __shfl_xor_sync(0xffffffffu, xmin, d));
-      xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, d));
-      ymin = fminf(ymin, __shfl_xor_sync(0xffffffffu, ymin, d));
-      ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, d));
-    }
-    if (lane == 0) s_wbox[warp] = make_float4(xmin, xmax, ymin, ymax);
-  }
-  float t0 = 1.0f, r0 = 0.0f, g0 = 0.0f, b0 = 0.0f, t1 = 1.0f, r1 = 0.0f, g1 = 0.0f, b1 = 0.0f;
-  int w0 = e1 - e0, w1 = e1 - e0;
-  bool d0 = !v0, d1 = !v1;
-  uint32_t contrib = 0;
-  const float W = (float)width;
-  const uint32_t lt_mask = (1u << lane) - 1u;
-
-  for (int base = e0; base < e1; base += kBlend2Batch) {
-    if (__syncthreads_count(!(d0 && d1)) == 0) break;
-#pragma unroll
-    for (int h = 0; h < kBlend2Batch / kBlend2Threads; ++h) {
-      const int slot = tid + h * kBlend2Threads;
-      const int e = base + slot;
-      uint32_t mask = 0;
-      if (e < e1) {
-        const uint32_t v = vals[e];
-        const uint32_t g = v >> 2;
-        const int k = (int)(v & 3u);
-        const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
-        const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
-        const float c2 = __ldg(&sp_c[g].x);
-        const float cx = a.x + (k == 0 ? -W : (k == 1 ? 0.0f : W));
-        const float cy = a.y;
-        s_geo[slot] = make_float4(cx, cy, a.z, 2.0f * a.w);
-        s_att[slot] = b;
-        s_b[slot] = c2;
-        float ex, ey;
-        if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
-#pragma unroll
-          for (int w = 0; w < kWarps; ++w) {
-            const float4 bb = s_wbox[w];
-            const bool out = (bb.x - cx > ex) || (bb.y - cx < -ex) || (bb.z - cy > ey) || (bb.w - cy < -ey);
-            mask |= out ? 0u : (1u << w);
-          }
-        } else {
-          mask = 0xFu;
-        }
-      }
-      s_mask[slot] = (uint8_t)mask;
-    }
-    __syncthreads();
-    int n_list = 0;
-#pragma unroll
-    for (int c = 0; c < kBlend2Batch / 32; ++c) {
-      const bool mine = (s_mask[c * 32 + lane] >> warp) & 1u;
-      const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-      if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(c * 32 + lane);
-      n_list += __popc(bal);
-    }
-    __syncwarp();
-    for (int q = 0; q < n_list && !(d0 && d1); ++q) {
-      const int j = s_list[warp][q];
-      const float4 geo = s_geo[j];
-      const float4 att = s_att[j];
-      const float bj = s_b[j];
-      const int e_rel = base + j - e0;
-      if (!d0) composite_one(geo, att, bj, px0, py, cutoff2, alpha_clamp, transmittance_floor, e_rel, t0, r0, g0, b0,
-                             w0, d0, contrib);
-      if (!d1) composite_one(geo, att, bj, px1, py, cutoff2, alpha_clamp, transmittance_floor, e_rel, t1, r1, g1, b1,
-                             w1, d1, contrib);
-    }
-  }
-
-  const uint32_t exam = (v0 ? (uint32_t)min(w0 + 1, e1 - e0) : 0u) + (v1 ? (uint32_t)min(w1 + 1, e1 - e0) : 0u);
-  const uint32_t w_exam = __reduce_add_sync(0xffffffffu, exam);
-  const uint32_t w_contrib = __reduce_add_sync(0xffffffffu, contrib);
-  if (lane == 0 && work) {
-    atomicAdd(work, (unsigned long long)w_exam);
-    atomicAdd(work + 1, (unsigned long long)w_contrib);
-  }
-  const int64_t plane = (int64_t)width * height;
-  if (v0) {
-    const int64_t p = (int64_t)x0 * height + y;
-    image[p] = r0;
-    image[plane + p] = g0;
-    image[2 * plane + p] = b0;
-    trans_out[p] = t0;
-    walked_out[p] = w0;
-  }
-  if (v1) {
-    const int64_t p = (int64_t)x1 * height + y;
-    image[p] = r1;
-    image[plane + p] = g1;
-    image[2 * plane + p] = b1;
-    trans_out[p] = t1;
-    walked_out[p] = w1;
-  }
-}
-
 void launch_blend(const BlendArgs& a, cudaStream_t stream) {
   const int n_band_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
   if (n_band_tiles <= 0) return;
-  if (!a.plain && a.tile_size == 16 && !a.one_pixel_per_thread) {
-    k_blend_cull2<<<n_band_tiles, kBlend2Threads, 0, stream>>>(
-        a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tiles_x, a.alpha_clamp, a.transmittance_floor,
-        a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work, a.band_ty0 * a.tiles_x);
-    ++g_launches;
-    return;
-  }
   if (!a.plain && a.tile_size <= 16) {
     k_blend_cull<<<n_band_tiles, kBlendThreads, 0, stream>>>(
         a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.alpha_clamp,

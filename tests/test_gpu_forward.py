@@ -221,9 +221,8 @@ def test_warp_culled_blend_equals_plain_blend(gpu_ctx, tile):
     cam = CameraPose(2048, 1024, rot_yaw(0.3))
     s = RenderSettings(tile_size=tile)
     a = render(gpu_ctx, c, cam, s)
-    for flag in (capi.FRAME_PLAIN_BLEND, capi.FRAME_BLEND_1PX):
-        b = render(gpu_ctx, c, cam, s, flags=flag)
-        assert np.array_equal(a.image, b.image)
-        assert np.array_equal(a.walked, b.walked)
-        assert np.array_equal(a.transmittance, b.transmittance)
-        assert a.work() == b.work()
+    b = render(gpu_ctx, c, cam, s, flags=capi.FRAME_PLAIN_BLEND)
+    assert np.array_equal(a.image, b.image)
+    assert np.array_equal(a.walked, b.walked)
+    assert np.array_equal(a.transmittance, b.transmittance)
+    assert a.work() == b.work()
