@@ -224,13 +224,25 @@ __global__ void __launch_bounds__(kThreads) k_onesweep_pass(
       s_gbase[d] = digit_start[d] - start;
     } else {
       st[(int64_t)tile * 256 + d] = kStatAgg | real;
+      // Look back 8 predecessors per round trip (independent loads in flight), consume
+      // them in order; an unpublished slot is re-polled from that position.
       uint32_t excl = 0;
-      for (int look = tile - 1; look >= 0;) {
-        const uint32_t w = st[(int64_t)look * 256 + d];
-        if ((w & ~kStatMask) == 0) continue;  // predecessor not published yet: spin
-        excl += w & kStatMask;
-        if (w & kStatPrefix) break;
-        --look;
+      int look = tile - 1;
+      bool found = false;
+      while (!found && look >= 0) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = (look - k >= 0) ? st[(int64_t)(look - k) * 256 + d] : kStatPrefix;
+        int consumed = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (found || consumed != k) continue;
+          if ((w[k] & ~kStatMask) == 0) continue;  // not published yet: re-poll from here
+          excl += w[k] & kStatMask;
+          ++consumed;
+          if (w[k] & kStatPrefix) found = true;
+        }
+        look -= consumed;
       }
       st[(int64_t)tile * 256 + d] = kStatPrefix | (excl + real);
       s_gbase[d] = digit_start[d] + excl - start;
