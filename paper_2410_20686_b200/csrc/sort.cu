@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep_pass(
       while (!found && look >= 0) {
         uint32_t w[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = (look - k >= 0) ? st[(int64_t)(look - k) * 256 + d] : kStatPrefix;
+        for (int k = 0; k < 8; ++k) w[k] = (look - k >= 0) ? (uint32_t)st[(int64_t)(look - k) * 256 + d] : (uint32_t)kStatPrefix;
         int consumed = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
