@@ -153,7 +153,7 @@ __global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
   hist[p * 256 + d] = off + incl - v;
 }
 
-__global__ void __launch_bounds__(kThreads) k_onesweep_pass(
+__global__ void __launch_bounds__(kThreads, 3) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
@@ -175,12 +175,17 @@ __global__ void __launch_bounds__(kThreads) k_onesweep_pass(
   const int64_t base = tile_base + (int64_t)warp * kWarpItems;
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t key[kIPT], val[kIPT], rank[kIPT];
+  // All loads first, so the tile's 32 loads per thread are in flight together.
+#pragma unroll
+  for (int j = 0; j < kIPT; ++j) {
+    const int64_t idx = base + j * 32 + lane;
+    key[j] = idx < n ? __ldcs(keys_in + idx) : 0u;
+    val[j] = idx < n ? __ldcs(vals_in + idx) : 0u;
+  }
 #pragma unroll
   for (int j = 0; j < kIPT; ++j) {
     const int64_t idx = base + j * 32 + lane;
     const bool valid = idx < n;
-    key[j] = valid ? keys_in[idx] : 0u;
-    val[j] = valid ? vals_in[idx] : 0u;
     const uint32_t d = valid ? (key[j] >> shift) & mask : mask;
     uint32_t peers = 0xffffffffu;
     for (int b = 0; b < bits; ++b) {
@@ -224,25 +229,13 @@ __global__ void __launch_bounds__(kThreads) k_onesweep_pass(
       s_gbase[d] = digit_start[d] - start;
     } else {
       st[(int64_t)tile * 256 + d] = kStatAgg | real;
-      // Look back 8 predecessors per round trip (independent loads in flight), consume
-      // them in order; an unpublished slot is re-polled from that position.
       uint32_t excl = 0;
-      int look = tile - 1;
-      bool found = false;
-      while (!found && look >= 0) {
-        uint32_t w[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = (look - k >= 0) ? (uint32_t)st[(int64_t)(look - k) * 256 + d] : (uint32_t)kStatPrefix;
-        int consumed = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (found || consumed != k) continue;
-          if ((w[k] & ~kStatMask) == 0) continue;  // not published yet: re-poll from here
-          excl += w[k] & kStatMask;
-          ++consumed;
-          if (w[k] & kStatPrefix) found = true;
-        }
-        look -= consumed;
+      for (int look = tile - 1; look >= 0;) {
+        const uint32_t w = st[(int64_t)look * 256 + d];
+        if ((w & ~kStatMask) == 0) continue;  // predecessor not published yet: spin
+        excl += w & kStatMask;
+        if (w & kStatPrefix) break;
+        --look;
       }
       st[(int64_t)tile * 256 + d] = kStatPrefix | (excl + real);
       s_gbase[d] = digit_start[d] + excl - start;
