@@ -498,52 +498,28 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
       n_list += __popc(bal);
     }
     __syncwarp();
-    // Two entries per iteration: their d2 and exponentials are independent of the
-    // compositing state, so both are evaluated up front (two dependency chains in
-    // flight); compositing then applies them in list order, exactly as one at a time.
     if (!done) {
-      for (int q = 0; q < n_list; q += 2) {
-        const int ja = s_list[warp][q];
-        const bool has_b = q + 1 < n_list;
-        const int jb = has_b ? s_list[warp][q + 1] : ja;
-        const float4 ga = s_geo[ja], gb = s_geo[jb];
-        const float4 aa = s_att[ja], ab = s_att[jb];
-        const float dxa = px - ga.x, dya = py - ga.y;
-        const float dxb = px - gb.x, dyb = py - gb.y;
-        const float d2a = ga.z * dxa * dxa + ga.w * dxa * dya + aa.x * dya * dya;
-        const float d2b = gb.z * dxb * dxb + gb.w * dxb * dyb + ab.x * dyb * dyb;
-        const float Ea = pm_expf_blend(-d2a / 2.0f);
-        const float Eb = pm_expf_blend(-d2b / 2.0f);
-        if (!(d2a > cutoff2)) {
-          const float alpha = std_min(alpha_clamp, aa.y * Ea);
-          const float t_next = t * (1.0f - alpha);
-          if (t_next < transmittance_floor) {
-            walked = base + ja - e0;
-            done = true;
-            break;
-          }
-          const float wgt = alpha * t;
-          ++contrib;
-          cr = cr + aa.z * wgt;
-          cg = cg + aa.w * wgt;
-          cb = cb + s_b[ja] * wgt;
-          t = t_next;
+      for (int q = 0; q < n_list; ++q) {
+        const int j = s_list[warp][q];
+        const float4 geo = s_geo[j];
+        const float dx = px - geo.x;
+        const float dy = py - geo.y;
+        const float4 att = s_att[j];
+        const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
+        if (d2 > cutoff2) continue;
+        const float alpha = std_min(alpha_clamp, att.y * pm_expf_blend(-d2 / 2.0f));
+        const float t_next = t * (1.0f - alpha);
+        if (t_next < transmittance_floor) {
+          walked = base + j - e0;
+          done = true;
+          break;
         }
-        if (has_b && !(d2b > cutoff2)) {
-          const float alpha = std_min(alpha_clamp, ab.y * Eb);
-          const float t_next = t * (1.0f - alpha);
-          if (t_next < transmittance_floor) {
-            walked = base + jb - e0;
-            done = true;
-            break;
-          }
-          const float wgt = alpha * t;
-          ++contrib;
-          cr = cr + ab.z * wgt;
-          cg = cg + ab.w * wgt;
-          cb = cb + s_b[jb] * wgt;
-          t = t_next;
-        }
+        const float wgt = alpha * t;
+        ++contrib;
+        cr = cr + att.z * wgt;
+        cg = cg + att.w * wgt;
+        cb = cb + s_b[j] * wgt;
+        t = t_next;
       }
     }
   }
