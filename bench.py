@@ -81,6 +81,8 @@ class ClockSampler:
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nvml = None
+            self.thread = threading.Thread(target=self._poll_smi, daemon=True)
+            self.thread.start()
             return self
         self.thread = threading.Thread(target=self._poll, daemon=True)
         self.thread.start()
@@ -97,17 +99,30 @@ class ClockSampler:
                 pass
             self.stop.wait(0.02)
 
+    def _poll_smi(self):
+        q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-i",
+                                      str(self.gpu)], capture_output=True, text=True, timeout=5).stdout.strip()
+                sm, smax, bits = [x.strip() for x in out.split(",")]
+                self.max_mhz = float(smax)
+                self.rows.append((float(sm), int(bits, 16)))
+            except Exception:
+                return
+            self.stop.wait(0.05)
+
     def __exit__(self, *a):
         self.stop.set()
-        if self.nvml is not None:
-            self.thread.join(timeout=2)
+        if hasattr(self, "thread"):
+            self.thread.join(timeout=6)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [r[0] for r in self.rows]
         reasons = sorted({name for _, bits in self.rows for name, m in self.REASONS.items() if bits & m})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": reasons,
                 "samples": len(self.rows)}
 
 
