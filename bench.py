@@ -35,6 +35,7 @@ METRIC = "ERP frames/sec (1M Gaussians, 2048×1024)"
 UNIT = "frames/s"
 W_IMG, H_IMG = 2048, 1024
 N_GAUSS = 1_000_000
+E2E_LANES = 3  # frames in flight on the e2e path (contexts / streams / host threads)
 WORKLOAD = ("C3: 1M synthetic Gaussians (50% uniform, 25% poles |elev| 75-89.5 deg, 25% azimuth seam), "
             "SH0, 2048x1024 ERP, camera yawed per step")
 
@@ -293,7 +294,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     h2d = sum(int(np.asarray(a).nbytes) for a in arrs)
     d2h = 3 * W_IMG * H_IMG * 4
     lanes = []
-    for _ in range(2):
+    for _ in range(E2E_LANES):
         c2 = Context(local_rank)  # private stream
         lanes.append((c2, RenderOutput(c2), torch.empty(3 * W_IMG * H_IMG, dtype=torch.float32).pin_memory()))
 
@@ -358,8 +359,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "stage_rooflines": stage_roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "odgs_render (host cloud, pinned) + odgs_frame_download (pinned), 2 contexts / "
-                            "2 streams / 2 host threads pipelining frames"},
+                    "path": f"odgs_render (host cloud, pinned) + odgs_frame_download (pinned), {E2E_LANES} "
+                            f"contexts / streams / host threads pipelining frames"},
             "cpu_baseline": cpu,
             "train": train,
             "large_render": large,
