@@ -270,6 +270,28 @@ PM_HD float pm_cosf(float x) {
   return pm_d2f(v);
 }
 
+/* sin and cos of the same argument with one range reduction; bit-identical to
+   pm_sinf(x) and pm_cosf(x). */
+PM_HD void pm_sincosf(float x, float* s, float* c) {
+  if (x != x || x - x != 0.0f) {
+    *s = x - x;
+    *c = x - x;
+    return;
+  }
+  int q;
+  const double r = pm_reduce_pio2((double)x, &q);
+  const double sp = pm_sin_poly(r), cp = pm_cos_poly(r);
+  double vs, vc;
+  switch (q) {
+    case 0: vs = sp; vc = cp; break;
+    case 1: vs = cp; vc = -sp; break;
+    case 2: vs = -sp; vc = -cp; break;
+    default: vs = -cp; vc = sp; break;
+  }
+  *s = pm_d2f(vs);
+  *c = pm_d2f(vc);
+}
+
 /* ---------------------------------------------------------------- atan2 / hypot */
 
 /* atan(t) for 0 <= t <= 1 in binary64. */

@@ -1375,6 +1375,18 @@ TEST_CASE("portable math: within 1 ulp of libm on the arguments the path sees") 
   CHECK(pm_expf_blend(-100.0f) == 0.0f);
   CHECK(pm_cosf(0.0f) == 1.0f);
   CHECK(pm_sinf(0.0f) == 0.0f);
+  // Properties the kernels rely on: cos is exactly even, and sincos == (sin, cos).
+  std::uniform_real_distribution<float> wide(-7.0f, 7.0f);
+  int even_bad = 0, sincos_bad = 0;
+  for (int k = 0; k < 4000000; ++k) {
+    const float x = wide(rng);
+    if (pm_cosf(x) != pm_cosf(-x)) ++even_bad;
+    float sn, cs;
+    pm_sincosf(x, &sn, &cs);
+    if (sn != pm_sinf(x) || cs != pm_cosf(x)) ++sincos_bad;
+  }
+  CHECK(even_bad == 0);
+  CHECK(sincos_bad == 0);
 }
 
 TEST_CASE("portable oracle: float images agree with the libm oracle, walks nearly always") {

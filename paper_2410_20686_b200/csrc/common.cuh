@@ -123,7 +123,12 @@ __device__ __forceinline__ M23 jacobian_factored(float phi, float theta, float r
                                                  float max_elevation, bool* clamped) {
   const bool clamp = fabsf(theta) > max_elevation;
   *clamped = clamp;
-  const float sec = 1.0f / pm_cosf(clamp ? max_elevation : fabsf(theta));
+  float cp, sp, ct, st;
+  pm_sincosf(phi, &sp, &cp);
+  pm_sincosf(theta, &st, &ct);
+  // pm_cosf is exactly even (sign-symmetric reduction and polynomials), so
+  // cos(|theta|) == cos(theta) bit for bit (checked in oracle/ref_tests.cpp).
+  const float sec = 1.0f / (clamp ? pm_cosf(max_elevation) : ct);
   M23 j_o;
   j_o.a[0][0] = 1.0f / r; j_o.a[0][1] = 0.0f; j_o.a[0][2] = 0.0f;
   j_o.a[1][0] = 0.0f; j_o.a[1][1] = 1.0f / r; j_o.a[1][2] = 0.0f;
@@ -131,8 +136,6 @@ __device__ __forceinline__ M23 jacobian_factored(float phi, float theta, float r
   q_o.a[0][0] = sec; q_o.a[0][1] = 0.0f; q_o.a[1][0] = 0.0f; q_o.a[1][1] = 1.0f;
   M2 s_o;
   s_o.a[0][0] = W / (2.0f * kPiF); s_o.a[0][1] = 0.0f; s_o.a[1][0] = 0.0f; s_o.a[1][1] = H / kPiF;
-  const float cp = pm_cosf(phi), sp = pm_sinf(phi);
-  const float ct = pm_cosf(theta), st = pm_sinf(theta);
   M3 t_phi, t_theta;
   t_phi.a[0][0] = cp;   t_phi.a[0][1] = 0.0f; t_phi.a[0][2] = -sp;
   t_phi.a[1][0] = 0.0f; t_phi.a[1][1] = 1.0f; t_phi.a[1][2] = 0.0f;
