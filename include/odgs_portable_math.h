@@ -15,7 +15,7 @@
  *   pm_expf, pm_sinf, pm_cosf, pm_atan2f, pm_hypotf evaluate in binary64 and round
  *   once to binary32: nearly always the correctly rounded float result (they agree
  *   with glibc's float functions except in rare last-place cases).
- *   pm_expf_blend evaluates in binary32 (7th-degree Horner), <= ~1 ulp, and is the
+ *   pm_expf_blend evaluates in binary32 (degree-6 Horner), <= ~1 ulp, and is the
  *   per-pixel exponential of the blend and backward loops, where throughput matters.
  *
  * Build rules (both sides): no floating-point contraction — the host oracle is
@@ -176,27 +176,42 @@ PM_HD float pm_expf(float x) {
 }
 
 /*
- * expf(x) in binary32 for the per-pixel loops (argument -d2/2 <= 0). Results
- * below 2^-126 (x < -87) are flushed to +0 — the alpha they would produce is
- * < 1e-38 and can change neither the transmittance nor the colour.
+ * expf(x) in binary32 for the per-pixel loops (argument -d2/2 <= 0): n = rint(x/ln2)
+ * via the 1.5*2^23 shifter, Cody-Waite reduction, a degree-6 near-minimax polynomial
+ * on |r| <= ln2/2 (relative error 1.9e-9), and the scaling 2^n applied by adding n to
+ * the exponent field (exact: for -86 <= x <= 88 the result is a normal float).
+ * Results below e^-86 (x < -86) are flushed to +0 — the alpha they would produce is
+ * < 1e-37 and can change neither the transmittance nor the colour.
  */
 PM_HD float pm_expf_blend(float x) {
-  if (!(x >= -87.0f)) return (x != x) ? x : 0.0f;
+  if (!(x >= -86.0f)) return (x != x) ? x : 0.0f;
   if (x > 88.0f) return pm_expf(x);
   const float shifter = 12582912.0f; /* 1.5 * 2^23 */
   const float t = pm_ffma(x, 0x1.715476p+0f, shifter);
   const float n = pm_fsub(t, shifter);
   float r = pm_ffma(n, -0x1.62e400p-1f, x); /* n * ln2_hi is exact for |n| < 2^8 */
   r = pm_ffma(n, -0x1.7f7d1cp-20f, r);
-  float p = 0x1.a01a02p-13f;
-  p = pm_ffma(p, r, 0x1.6c16c2p-10f);
-  p = pm_ffma(p, r, 0x1.111112p-7f);
-  p = pm_ffma(p, r, 0x1.555556p-5f);
-  p = pm_ffma(p, r, 0x1.555556p-3f);
-  p = pm_ffma(p, r, 0x1.0p-1f);
+  float p = 0x1.6ac294p-10f;
+  p = pm_ffma(p, r, 0x1.126e46p-7f);
+  p = pm_ffma(p, r, 0x1.55589p-5f);
+  p = pm_ffma(p, r, 0x1.555408p-3f);
+  p = pm_ffma(p, r, 0x1.fffffap-2f);
   p = pm_ffma(p, r, 0x1.0p+0f);
   p = pm_ffma(p, r, 0x1.0p+0f);
-  return pm_fmul(p, pm_pow2i_f((int)n));
+#if defined(__CUDA_ARCH__)
+  const int32_t ni = __float_as_int(t) - __float_as_int(shifter);
+  return __int_as_float(__float_as_int(p) + (int32_t)((uint32_t)ni << 23));
+#else
+  int32_t tb, sb, pb;
+  memcpy(&tb, &t, 4);
+  memcpy(&sb, &shifter, 4);
+  memcpy(&pb, &p, 4);
+  const int32_t ni = tb - sb;
+  const int32_t rb = pb + (int32_t)((uint32_t)ni << 23);
+  float res;
+  memcpy(&res, &rb, 4);
+  return res;
+#endif
 }
 
 /* ---------------------------------------------------------------- sin / cos */

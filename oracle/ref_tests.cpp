@@ -1338,7 +1338,7 @@ int64_t ulp_diff(float a, float b) {
 
 TEST_CASE("portable math: within 1 ulp of libm on the arguments the path sees") {
   std::mt19937 rng(2024);
-  std::uniform_real_distribution<float> ang(-3.2f, 3.2f), ex(-40.f, 10.f), bl(-50.f, 0.f), co(-30.f, 30.f);
+  std::uniform_real_distribution<float> ang(-3.2f, 3.2f), ex(-40.f, 10.f), bl(-86.f, 88.f), co(-30.f, 30.f);
   int64_t w_exp = 0, w_blend = 0, w_sin = 0, w_cos = 0, w_atan2 = 0, w_hypot = 0;
   int64_t diff_exp = 0, diff_atan2 = 0;
   const int n = 2000000;
@@ -1373,6 +1373,8 @@ TEST_CASE("portable math: within 1 ulp of libm on the arguments the path sees") 
   CHECK(pm_expf(0.0f) == 1.0f);
   CHECK(pm_expf_blend(0.0f) == 1.0f);
   CHECK(pm_expf_blend(-100.0f) == 0.0f);
+  CHECK(pm_expf_blend(-86.5f) == 0.0f);
+  CHECK(pm_expf_blend(88.0f) == std::exp(88.0f) || ulp_diff(pm_expf_blend(88.0f), std::exp(88.0f)) <= 1);
   CHECK(pm_cosf(0.0f) == 1.0f);
   CHECK(pm_sinf(0.0f) == 0.0f);
   // Properties the kernels rely on: cos is exactly even, and sincos == (sin, cos).
