@@ -429,7 +429,7 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream):
     return {"metric": "train iters/sec (C4: 3M Gaussians, batch of 8 ERP views at 2048x1024)",
             "value": args.train_steps / (ms_max / 1000.0), "unit": "iters/s", "ms_per_step": ms_max / args.train_steps,
             "steps": args.train_steps, "warmup": 2, "views_per_gpu": len(tr.mine), "n_gpus": world,
-            "scaling": "strong", "loss": "L1 (lambda_ssim = 0)", "collective": "NCCL all-reduce (sum) of 16n+n values",
+            "scaling": "strong", "loss": "photometric_loss, lambda_ssim = 0.2 (L1 + SSIM on the GPU)", "collective": "NCCL all-reduce (sum) of 16n+n values",
             "stage_ms_per_step": stages, "first_loss": losses[0], "last_loss": losses[-1]}
 
 

@@ -258,9 +258,10 @@ typedef struct {
   int64_t step;
 } odgs_adam_params;
 
-/* photometric_loss (metrics.hpp:152-184) for lambda_ssim = 0 (L1): writes the image
-   gradient to dl_dimage and the loss to *loss (synchronizes). lambda_ssim > 0 is
-   rejected with ODGS_ERR_INVALID_ARGUMENT (SSIM is not on the GPU yet). */
+/* photometric_loss (metrics.hpp:152-184): (1 - lambda) L1 + lambda (1 - SSIM) with the
+   11x11 Gaussian window (sigma 1.5) of ssim_with_gradient (metrics.hpp:83-136); writes
+   the image gradient to dl_dimage and the loss to *loss (synchronizes). Images are
+   [3][W][H] device buffers; lambda in [0, 1); SSIM needs W, H >= 11. */
 odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
                                   int32_t height, float lambda_ssim, float* dl_dimage, double* loss);
 

@@ -985,12 +985,19 @@ odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const fl
   cudaSetDevice(ctx->device);
   if (!(lambda_ssim >= 0.0f) || !(lambda_ssim < 1.0f))
     return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "photometric_loss: lambda must be in [0, 1)");
-  if (lambda_ssim > 0.0f)
-    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "photometric_loss: SSIM term not available on the GPU");
   if (width <= 0 || height <= 0) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "photometric_loss: bad size");
   const int64_t count = 3 * (int64_t)width * height;
-  ODGS_CUDA(ctx, ensure(ctx->loss_buf, l1_loss_temp_bytes(count), ctx->stream));
-  launch_l1_loss(rendered, target, count, lambda_ssim, dl_dimage, ctx->loss_buf.as<double>(), ctx->stream);
+  if (lambda_ssim > 0.0f) {
+    if (width < 11 || height < 11)
+      return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "ssim: images smaller than the 11x11 window");
+    ODGS_CUDA(ctx, ensure(ctx->loss_buf, ssim_temp_bytes(height, width) + 64, ctx->stream));
+    char* base = ctx->loss_buf.as<char>();
+    launch_ssim_loss(rendered, target, height, width, lambda_ssim, dl_dimage, base + 64,
+                     reinterpret_cast<double*>(base), ctx->stream);
+  } else {
+    ODGS_CUDA(ctx, ensure(ctx->loss_buf, l1_loss_temp_bytes(count), ctx->stream));
+    launch_l1_loss(rendered, target, count, lambda_ssim, dl_dimage, ctx->loss_buf.as<double>(), ctx->stream);
+  }
   ODGS_CUDA(ctx, cudaGetLastError());
   if (loss) {
     ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->loss_buf.p, sizeof(double), cudaMemcpyDeviceToHost,

@@ -82,6 +82,11 @@ size_t l1_loss_temp_bytes(int64_t count);
 void launch_l1_loss(const float* rendered, const float* target, int64_t count, float lambda, float* grad,
                     double* temp, cudaStream_t stream);
 
+size_t ssim_temp_bytes(int H, int W);
+// photometric_loss with lambda > 0 (metrics.hpp:152-184): image gradient and *loss_out.
+void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda, float* grad, void* temp,
+                      double* loss_out, cudaStream_t stream);
+
 struct AdamArgs {
   int64_t n;
   float *means, *rotations, *log_scales, *raw_opacities, *colors;

@@ -6,6 +6,8 @@
 //   k_adam         train_step's update (optimizer.hpp:74-84, 114-139): densify-window
 //                  accumulation, Adam on the five parameter groups, quaternion
 //                  renormalisation — one pass over the cloud, elementwise.
+#include <cmath>
+
 #include "kernels.h"
 
 namespace odgs_b200 {
@@ -97,6 +99,205 @@ void launch_l1_loss(const float* rendered, const float* target, int64_t count, f
   ++g_launches;
   k_sum_partials<<<1, 256, 0, stream>>>(temp + 1, blocks, (1.0 - (double)lambda) / (double)count, temp);
   ++g_launches;
+}
+
+// ------------------------------------------------------------------ SSIM (metrics.hpp:27-136)
+// Images are 3 planes of H x W, each column-major (y + x*H): "rows" are y, "columns" x.
+// window_valid = horizontal then vertical 11-tap correlation (valid mode); the
+// adjoint window_scatter = the same on the zero-padded map. Channels run on grid.z.
+struct SsimWindow {
+  float w[11];
+};
+
+// 5 horizontally filtered maps of (a, b, a^2, b^2, ab): [5][3][W-10][H].
+__global__ void k_ssim_h(const float* __restrict__ a, const float* __restrict__ b, int H, int W, SsimWindow win,
+                         float* __restrict__ out) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x, xo = blockIdx.y, c = blockIdx.z;
+  if (y >= H) return;
+  const int Wo = W - 10;
+  const int64_t plane = (int64_t)W * H;
+  const float* pa = a + c * plane;
+  const float* pb = b + c * plane;
+  float s[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 11; ++i) {
+    const float va = pa[(int64_t)(xo + i) * H + y], vb = pb[(int64_t)(xo + i) * H + y];
+    const float w = win.w[i];
+    s[0] += w * va;
+    s[1] += w * vb;
+    s[2] += w * (va * va);
+    s[3] += w * (vb * vb);
+    s[4] += w * (va * vb);
+  }
+  const int64_t mplane = (int64_t)Wo * H, stride = 3 * mplane;
+  for (int m = 0; m < 5; ++m) out[m * stride + c * mplane + (int64_t)xo * H + y] = s[m];
+}
+
+// Vertical pass + the per-window SSIM terms (metrics.hpp:106-122): writes the four
+// window-grid gradient maps [4][3][W-10][H-10] and per-block partial sums of s.
+__global__ void k_ssim_v(const float* __restrict__ hmaps, int H, int W, SsimWindow win, double inv_windows,
+                         float* __restrict__ gmaps, double* __restrict__ partial) {
+  __shared__ double s_w[8];
+  const int yo = blockIdx.x * blockDim.x + threadIdx.x, xo = blockIdx.y, c = blockIdx.z;
+  const int Ho = H - 10, Wo = W - 10;
+  double sval = 0.0;
+  if (yo < Ho) {
+    const int64_t mplane = (int64_t)Wo * H, stride = 3 * mplane;
+    float v[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      const float* src = hmaps + m * stride + c * mplane + (int64_t)xo * H + yo;
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 11; ++i) acc += win.w[i] * src[i];
+      v[m] = acc;
+    }
+    const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
+    const float mu_a = v[0], mu_b = v[1];
+    const float var_a = v[2] - mu_a * mu_a, var_b = v[3] - mu_b * mu_b, cov = v[4] - mu_a * mu_b;
+    const float n1 = 2.0f * mu_a * mu_b + c1, n2 = 2.0f * cov + c2;
+    const float d1 = mu_a * mu_a + mu_b * mu_b + c1, d2 = var_a + var_b + c2;
+    const float sc = (n1 * n2) / (d1 * d2);
+    sval = sc;
+    const float iw = (float)inv_windows;
+    const float d_mu_a = (2.0f * mu_b * n2 - 2.0f * mu_a * sc * d2) / (d1 * d2) * iw;
+    const float d_var_a = (-sc / d2) * iw;
+    const float d_cov = (2.0f * (n1 / d1) / d2) * iw;
+    const int64_t gplane = (int64_t)Wo * Ho, gstride = 3 * gplane;
+    const int64_t idx = c * gplane + (int64_t)xo * Ho + yo;
+    gmaps[0 * gstride + idx] = d_mu_a;
+    gmaps[1 * gstride + idx] = d_var_a;
+    gmaps[2 * gstride + idx] = d_cov;
+    gmaps[3 * gstride + idx] = 2.0f * d_var_a * mu_a + d_cov * mu_b;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) sval += __shfl_xor_sync(0xffffffffu, sval, d);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = sval;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+    partial[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// window_scatter, horizontal half: [4][3][W][H+10] from the zero-padded grid maps.
+__global__ void k_ssim_scatter_h(const float* __restrict__ gmaps, int H, int W, SsimWindow win,
+                                 float* __restrict__ out) {
+  const int yp = blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y, c = blockIdx.z;
+  const int Hp = H + 10, Ho = H - 10, Wo = W - 10;
+  if (yp >= Hp) return;
+  const int yo = yp - 10;  // padded row -> grid row
+  const int64_t gplane = (int64_t)Wo * Ho, gstride = 3 * gplane;
+  const int64_t oplane = (int64_t)W * Hp, ostride = 3 * oplane;
+  for (int m = 0; m < 4; ++m) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 11; ++i) {
+      const int xo = x + i - 10;  // padded column (x + i) -> grid column
+      const float v = (yo >= 0 && yo < Ho && xo >= 0 && xo < Wo) ? gmaps[m * gstride + c * gplane + (int64_t)xo * Ho + yo]
+                                                                  : 0.0f;
+      acc += win.w[i] * v;
+    }
+    out[m * ostride + c * oplane + (int64_t)x * Hp + yp] = acc;
+  }
+}
+
+// window_scatter, vertical half, and the SSIM image gradient combined with the L1 part:
+// dl = (1 - lambda) sign(a - b) / pixels - lambda (S_mu + (2 a S_var + b S_cov) - S_mix).
+__global__ void k_ssim_combine(const float* __restrict__ hs, const float* __restrict__ a,
+                               const float* __restrict__ b, int H, int W, SsimWindow win, float lambda,
+                               float pixels, float* __restrict__ grad, double* __restrict__ l1_partial) {
+  __shared__ double s_w[8];
+  const int y = blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y, c = blockIdx.z;
+  const int Hp = H + 10;
+  double l1 = 0.0;
+  if (y < H) {
+    const int64_t oplane = (int64_t)W * Hp, ostride = 3 * oplane;
+    float S[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const float* src = hs + m * ostride + c * oplane + (int64_t)x * Hp + y;
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 11; ++i) acc += win.w[i] * src[i];
+      S[m] = acc;
+    }
+    const int64_t p = (int64_t)c * W * H + (int64_t)x * H + y;
+    const float va = a[p], vb = b[p];
+    const float d = va - vb;
+    l1 = (double)fabsf(d);
+    const float sign = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
+    const float g_ssim = S[0] + (2.0f * va * S[1] + vb * S[2]) - S[3];
+    grad[p] = (1.0f - lambda) * sign / pixels - lambda * g_ssim;
+  }
+#pragma unroll
+  for (int dd = 16; dd > 0; dd >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, dd);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = l1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+    l1_partial[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// loss = (1 - lambda) sum|d| / pixels + lambda (1 - sum s / windows), fixed-order sums.
+__global__ void k_ssim_loss(const double* __restrict__ l1_partial, int64_t n_l1, const double* __restrict__ s_partial,
+                            int64_t n_s, double lambda, double pixels, double windows, double* out) {
+  __shared__ double s_a[256], s_b[256];
+  double ta = 0.0, tb = 0.0;
+  for (int64_t i = threadIdx.x; i < n_l1; i += 256) ta += l1_partial[i];
+  for (int64_t i = threadIdx.x; i < n_s; i += 256) tb += s_partial[i];
+  s_a[threadIdx.x] = ta;
+  s_b[threadIdx.x] = tb;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s_a[threadIdx.x] += s_a[threadIdx.x + w];
+      s_b[threadIdx.x] += s_b[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = (1.0 - lambda) * s_a[0] / pixels + lambda * (1.0 - s_b[0] / windows);
+}
+
+size_t ssim_temp_bytes(int H, int W) {
+  const int64_t Ho = H - 10, Wo = W - 10, Hp = H + 10;
+  const int64_t blocks_v = ((Ho + 255) / 256) * Wo * 3, blocks_c = ((H + 255) / 256) * W * 3;
+  return sizeof(float) * (size_t)(5 * 3 * Wo * H + 4 * 3 * Wo * Ho + 4 * 3 * W * Hp) +
+         sizeof(double) * (size_t)(blocks_v + blocks_c + 8);
+}
+
+void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda, float* grad, void* temp,
+                      double* loss_out, cudaStream_t stream) {
+  SsimWindow win;
+  float sum = 0.0f;
+  for (int i = 0; i < 11; ++i) {  // metrics.hpp:31-39 (libm exp on the host, in float)
+    const float d = (float)i - 5.0f;
+    win.w[i] = std::exp(-d * d / (2.0f * 1.5f * 1.5f));
+    sum += win.w[i];
+  }
+  for (int i = 0; i < 11; ++i) win.w[i] /= sum;
+  const int64_t Ho = H - 10, Wo = W - 10, Hp = H + 10;
+  float* hmaps = static_cast<float*>(temp);
+  float* gmaps = hmaps + 5 * 3 * Wo * H;
+  float* hs = gmaps + 4 * 3 * Wo * Ho;
+  double* s_part = reinterpret_cast<double*>(hs + 4 * 3 * W * Hp);
+  const int64_t bx_v = (Ho + 255) / 256;
+  double* l1_part = s_part + bx_v * Wo * 3;
+  const int64_t bx_c = (H + 255) / 256;
+  const double windows = 3.0 * (double)Ho * (double)Wo;
+  k_ssim_h<<<dim3((unsigned)((H + 255) / 256), (unsigned)Wo, 3), 256, 0, stream>>>(a, b, H, W, win, hmaps);
+  k_ssim_v<<<dim3((unsigned)bx_v, (unsigned)Wo, 3), 256, 0, stream>>>(hmaps, H, W, win, 1.0 / windows, gmaps,
+                                                                       s_part);
+  k_ssim_scatter_h<<<dim3((unsigned)((Hp + 255) / 256), (unsigned)W, 3), 256, 0, stream>>>(gmaps, H, W, win, hs);
+  const float pixels = 3.0f * (float)H * (float)W;
+  k_ssim_combine<<<dim3((unsigned)bx_c, (unsigned)W, 3), 256, 0, stream>>>(hs, a, b, H, W, win, lambda, pixels,
+                                                                           grad, l1_part);
+  k_ssim_loss<<<1, 256, 0, stream>>>(l1_part, bx_c * W * 3, s_part, bx_v * Wo * 3, (double)lambda,
+                                     3.0 * (double)H * (double)W, windows, loss_out);
+  g_launches += 5;
 }
 
 __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float lr, float c1, float c2) {

@@ -37,7 +37,7 @@ class TrainConfig:  # optimizer.hpp:23-48 (defaults)
     lr_scale: float = 5e-3
     lr_opacity: float = 0.05
     lr_color: float = 2.5e-3
-    lambda_ssim: float = 0.0  # the GPU loss is L1 for now (C4 runs at lambda = 0)
+    lambda_ssim: float = 0.2
 
 
 def means_lr_at(iteration: int, cfg: TrainConfig) -> float:

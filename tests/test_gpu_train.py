@@ -135,3 +135,26 @@ def test_view_sharded_step_sums_views_on_one_gpu(gpu_ctx):
     assert all(math.isfinite(l) for l in losses)
     assert losses[-1] < losses[0]
     assert not torch.equal(before, cloud.means)
+
+
+@pytest.mark.parametrize("lam", [0.2, 0.5])
+def test_photometric_loss_with_ssim_matches_oracle(gpu_ctx, lam):
+    """metrics.hpp:83-184 (SSIM window 11, sigma 1.5, K1 .01, K2 .03) vs the fp64 oracle."""
+    W, H = 256, 128
+    rng = np.random.default_rng(11)
+    a = rng.random(3 * W * H, dtype=np.float32)
+    b = np.clip(a + rng.normal(0, 0.1, a.shape).astype(np.float32), 0, 1).astype(np.float32)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    grad = torch.empty_like(da)
+    loss = C.c_double()
+    gpu_ctx.check(gpu_ctx.lib.odgs_photometric_loss(gpu_ctx.handle, C.c_void_p(da.data_ptr()),
+                                                    C.c_void_p(db.data_ptr()), W, H, lam,
+                                                    C.c_void_p(grad.data_ptr()), C.byref(loss)))
+    g64 = np.empty(3 * W * H)
+    oloss = oracle_lib.lib().oracle_photometric_loss(
+        a.astype(np.float64).ctypes.data_as(C.POINTER(C.c_double)),
+        b.astype(np.float64).ctypes.data_as(C.POINTER(C.c_double)), H, W, lam,
+        g64.ctypes.data_as(C.POINTER(C.c_double)))
+    assert abs(loss.value - oloss) <= 1e-5 * abs(oloss)
+    g = grad.cpu().numpy().astype(np.float64)
+    assert np.abs(g - g64).max() <= 1e-4 * np.abs(g64).max()
