@@ -76,7 +76,7 @@ def allreduce_grads(flat, observed, group=None):
 
 
 class ViewShardedTrainer:
-    """C4 training step: render + L1 loss + backward for this rank's views, gradient
+    """C4 training step: render + photometric loss (L1 + SSIM) + backward for this rank's views, gradient
     all-reduce, Adam. Everything stays on the device."""
 
     def __init__(self, ctx: Context, cloud: GaussianCloud, views: Sequence[CameraPose], targets, settings,

@@ -112,7 +112,7 @@ def test_view_sharded_step_sums_views_on_one_gpu(gpu_ctx):
     tgt = [torch.from_numpy(render(gpu_ctx, to_cloud32(oracle_lib.random_cloud(302, 4000)), v,
                                    RenderSettings()).image.ravel()).cuda() for v in views]
     cloud = dev()
-    tr = ViewShardedTrainer(gpu_ctx, cloud, views, tgt, RenderSettings(), TrainConfig(), extent=10.0)
+    tr = ViewShardedTrainer(gpu_ctx, cloud, views, tgt, RenderSettings(), TrainConfig(lambda_ssim=0.0), extent=10.0)
     # Expected gradient: sum of per-view backward passes of the L1 loss.
     expected = None
     for v, t in zip(views, tgt):
