@@ -43,9 +43,9 @@ def test_l1_loss_and_gradient(gpu_ctx):
         b.astype(np.float64).ctypes.data_as(C.POINTER(C.c_double)), H, W, 0.0,
         g64.ctypes.data_as(C.POINTER(C.c_double)))
     assert abs(loss.value - oloss) <= 1e-9 * oloss
-    with pytest.raises(Exception):
+    with pytest.raises(ValueError):  # lambda must lie in [0, 1) (metrics.hpp:160-161)
         gpu_ctx.check(gpu_ctx.lib.odgs_photometric_loss(gpu_ctx.handle, C.c_void_p(da.data_ptr()),
-                                                        C.c_void_p(db.data_ptr()), W, H, 0.2,
+                                                        C.c_void_p(db.data_ptr()), W, H, 1.0,
                                                         C.c_void_p(grad.data_ptr()), C.byref(loss)))
 
 
