@@ -271,6 +271,65 @@ odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const fl
 odgs_status odgs_adam_step(odgs_ctx* ctx, const odgs_params* params, const odgs_grads* grads,
                            const odgs_train_state* state, const odgs_adam_params* adam);
 
+/* ------------------------------------------------------------------ density control
+   (densify.hpp) */
+
+/* DensifyConfig (densify.hpp:16-33): the fields densify_and_prune reads. */
+typedef struct {
+  double grad_threshold_min;  /* 2e-5, trigger at the equator */
+  double grad_threshold_max;  /* 1e-4, trigger at the poles */
+  double percent_dense;       /* 1e-3 of the scene extent: clone / split boundary */
+  double opacity_prune_floor; /* 0.005 */
+  double split_scale_divisor; /* 1.6 */
+} odgs_densify_config;
+
+void odgs_default_densify_config(odgs_densify_config* out);
+
+/* DensifyStats (densify.hpp:51-55) plus the row count after the round. */
+typedef struct {
+  int64_t cloned, split, pruned, n_out;
+} odgs_densify_stats;
+
+/* std::mt19937 owned by the library: the generator densify_and_prune draws split
+   offsets from (densify.hpp:85, :61-69). Host object. */
+typedef struct odgs_rng odgs_rng;
+odgs_rng* odgs_rng_create(uint32_t seed);
+void odgs_rng_destroy(odgs_rng* rng);
+/* The generator's next raw 32-bit output (advances it). */
+uint32_t odgs_rng_next(odgs_rng* rng);
+/* count samples of detail::unit_ball_normal<float> (densify.hpp:61-69), the exact
+   draw sequence of the reference: out[3k..3k+2] = (x, y, z) of the k-th sample. */
+void odgs_rng_unit_ball(odgs_rng* rng, int64_t count, float* out);
+
+/* densify_and_prune (densify.hpp:81-153), first half: validates cfg and the extent,
+   classifies every Gaussian on the device (clone / split / prune) and computes the
+   output positions; stats receives the counts and n_out (synchronizes). The plan
+   stays in the context until the next odgs_densify_plan. Errors as the reference:
+   ODGS_ERR_INVALID_ARGUMENT for a bad config / extent, or for a split parent with a
+   near-zero quaternion (index = that Gaussian). */
+odgs_status odgs_densify_plan(odgs_ctx* ctx, const odgs_params* cloud, const odgs_train_state* state,
+                              const odgs_densify_config* cfg, float scene_extent, odgs_densify_stats* stats);
+
+/* Second half: writes the densified cloud and train state (n_out rows, device
+   buffers that must not overlap the inputs): surviving rows in order, then the
+   surviving clones / split children in parent order; moments follow their rows (new
+   rows zero), the densify window is cleared. unit_ball: host array of 2 * split
+   samples (odgs_rng_unit_ball, or the caller's own generator), child order. The
+   inputs must be the ones passed to odgs_densify_plan. */
+odgs_status odgs_densify_apply(odgs_ctx* ctx, const odgs_params* cloud, const odgs_train_state* state,
+                               const float* unit_ball, const odgs_params* out_cloud,
+                               const odgs_train_state* out_state);
+
+/* reset_opacity (densify.hpp:158-166): raw <- logit(min(sigmoid(raw), ceiling)) and
+   zeroes the opacity moments. If some row's logit argument leaves (0, 1) the rows
+   before it are rewritten, the moments are left alone, and ODGS_ERR_INVALID_ARGUMENT
+   names that row — the reference's throw point. */
+odgs_status odgs_reset_opacity(odgs_ctx* ctx, const odgs_params* cloud, const odgs_train_state* state,
+                               float ceiling);
+
+/* dynamic_threshold (densify.hpp:39-49), binary64 host helper. */
+odgs_status odgs_dynamic_threshold(double elevation, const odgs_densify_config* cfg, double* out);
+
 /* cull (rasterizer.hpp:15-28): host output of the kept rows, ascending. */
 odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, float near_radius,
                       float far_radius, int64_t* out_indices, int64_t* out_count);

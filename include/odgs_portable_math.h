@@ -385,4 +385,54 @@ PM_HD float pm_hypotf(float x, float y) {
   return pm_d2f(pm_dsqrt(pm_dadd(pm_dmul(ax, ax), pm_dmul(ay, ay))));
 }
 
+/* ---------------------------------------------------------------- log */
+
+/*
+ * ln(x) for binary32 x, evaluated in binary64 and rounded once (logit, types.hpp:38,
+ * and the split shrink log(1.6), densify.hpp:123). x = m 2^e with m in
+ * [sqrt(1/2), sqrt(2)); ln m = 2 atanh(s), s = (m - 1)/(m + 1), |s| <= 0.1716, summed
+ * to s^23 (truncation < 1e-19 relative); e ln2 in a hi/lo split.
+ */
+PM_HD float pm_logf(float x) {
+  if (x != x || x < 0.0f) return NAN;
+  if (x == 0.0f) return -INFINITY;
+  if (x == INFINITY) return x;
+  const double d = (double)x; /* exact; subnormal floats are normal doubles */
+  uint64_t bits;
+#if defined(__CUDA_ARCH__)
+  bits = (uint64_t)__double_as_longlong(d);
+#else
+  memcpy(&bits, &d, sizeof bits);
+#endif
+  int e = (int)((bits >> 52) & 0x7ff) - 1023;
+  uint64_t mb = (bits & 0x000fffffffffffffull) | 0x3ff0000000000000ull; /* m in [1, 2) */
+  if (mb > 0x3ff6a09e667f3bcdull) { /* m > sqrt(2): halve it (exact) */
+    mb -= 0x0010000000000000ull;
+    e += 1;
+  }
+  double m;
+#if defined(__CUDA_ARCH__)
+  m = __longlong_as_double((long long)mb);
+#else
+  memcpy(&m, &mb, sizeof m);
+#endif
+  const double s = pm_ddiv(pm_dsub(m, 1.0), pm_dadd(m, 1.0));
+  const double z = pm_dmul(s, s);
+  double p = 1.0 / 23.0;
+  p = pm_dfma(p, z, 1.0 / 21.0);
+  p = pm_dfma(p, z, 1.0 / 19.0);
+  p = pm_dfma(p, z, 1.0 / 17.0);
+  p = pm_dfma(p, z, 1.0 / 15.0);
+  p = pm_dfma(p, z, 1.0 / 13.0);
+  p = pm_dfma(p, z, 1.0 / 11.0);
+  p = pm_dfma(p, z, 1.0 / 9.0);
+  p = pm_dfma(p, z, 1.0 / 7.0);
+  p = pm_dfma(p, z, 1.0 / 5.0);
+  p = pm_dfma(p, z, 1.0 / 3.0);
+  const double lm = pm_dmul(pm_dmul(2.0, s), pm_dfma(p, z, 1.0)); /* 2s (1 + z p) */
+  const double ln2_hi = 0x1.62e42fefa39efp-1, ln2_lo = 0x1.abc9e3b39803fp-56;
+  const double ed = (double)e;
+  return pm_d2f(pm_dfma(ed, ln2_hi, pm_dfma(ed, ln2_lo, lm)));
+}
+
 #endif /* ODGS_PORTABLE_MATH_H */

@@ -55,6 +55,7 @@ struct StdMath {
   template <class S> static S exp(S x) { return std::exp(x); }
   // The per-pixel exponential of rasterizer.hpp:249 / backward.hpp:264-266.
   template <class S> static S exp_blend(S x) { return std::exp(x); }
+  template <class S> static S log(S x) { return std::log(x); }
 };
 
 struct PortableMath {
@@ -64,6 +65,7 @@ struct PortableMath {
   static float cos(float x) { return pm_cosf(x); }
   static float exp(float x) { return pm_expf(x); }
   static float exp_blend(float x) { return pm_expf_blend(x); }
+  static float log(float x) { return pm_logf(x); }
 };
 
 template <class S> inline constexpr S pi_v = S(3.141592653589793238462643383279502884L);
@@ -175,9 +177,9 @@ template <class S> struct Cloud {
 
 // types.hpp:28-39
 template <class S, class M = StdMath> inline S sigmoid(S x) { return S(1) / (S(1) + M::exp(-x)); }
-template <class S> inline S logit(S x) {
+template <class S, class M = StdMath> inline S logit(S x) {
   if (!(x > S(0) && x < S(1))) throw std::invalid_argument("logit: argument must lie in (0, 1)");
-  return std::log(x / (S(1) - x));
+  return M::log(x / (S(1) - x));
 }
 
 // types.hpp:148-180 CameraPose (y-down, z-forward; W == 2H).
@@ -1207,6 +1209,187 @@ inline S photometric_loss(const std::vector<S>& rendered, const std::vector<S>& 
     for (std::size_t p = 0; p < gradient->size(); ++p) (*gradient)[p] -= lambda_ssim * sg[p];
   }
   return loss;
+}
+
+// ------------------------------------------------------------------ densify.hpp
+// TrainState (types.hpp:257-325): Adam moments per group and the densify window, SoA
+// with the same layouts as Cloud (member(i, c) at c*n + i).
+template <class S> struct TrainState {
+  int64_t n = 0;
+  std::vector<S> means_m, means_v, rot_m, rot_v, scale_m, scale_v, opac_m, opac_v, color_m, color_v;
+  std::vector<S> grad_accum, elev_accum;
+  std::vector<int32_t> grad_count;
+  void init(int64_t m) {  // types.hpp:270-281
+    n = m;
+    for (auto* v : {&means_m, &means_v, &scale_m, &scale_v, &color_m, &color_v}) v->assign(3 * m, S(0));
+    rot_m.assign(4 * m, S(0));
+    rot_v.assign(4 * m, S(0));
+    opac_m.assign(m, S(0));
+    opac_v.assign(m, S(0));
+    reset_densify_stats(m);
+  }
+  void reset_densify_stats(int64_t m) {  // types.hpp:283-287
+    grad_accum.assign(m, S(0));
+    elev_accum.assign(m, S(0));
+    grad_count.assign(m, 0);
+  }
+};
+
+struct DensifyConfig {  // densify.hpp:16-33
+  double grad_threshold_min = 2e-5;
+  double grad_threshold_max = 1e-4;
+  double percent_dense = 1e-3;
+  double opacity_prune_floor = 0.005;
+  double split_scale_divisor = 1.6;
+  void validate() const {
+    if (!(grad_threshold_min > 0) || !(grad_threshold_max >= grad_threshold_min))
+      throw std::invalid_argument("DensifyConfig: need 0 < grad_threshold_min <= grad_threshold_max");
+    if (!(percent_dense > 0) || !(percent_dense < 1))
+      throw std::invalid_argument("DensifyConfig: percent_dense outside (0, 1)");
+  }
+};
+
+struct DensifyStats { int64_t cloned = 0, split = 0, pruned = 0; };
+
+// densify.hpp:61-69. `Vec3<Scalar> e(Scalar(gauss(rng)), Scalar(gauss(rng)),
+// Scalar(gauss(rng)))` is a parenthesised call; GCC evaluates its arguments right to
+// left, so the first draw lands in z (checked with the image's g++). The
+// normal_distribution object lives across the rejection loop and dies with the call,
+// so a cached second polar value is carried between tries but never between calls.
+template <class S> V3<S> unit_ball_normal(std::mt19937& rng) {
+  std::normal_distribution<double> gauss;
+  for (;;) {
+    V3<S> e;
+    e[2] = S(gauss(rng));
+    e[1] = S(gauss(rng));
+    e[0] = S(gauss(rng));
+    if (norm3(e) <= S(1)) return e;
+  }
+}
+
+namespace detail {
+// One row of the cloud as the reference's append_row copies it (types.hpp:92-106),
+// plus the SH rest coefficients of this build's extension.
+template <class S> struct Row {
+  S mean[3], rot[4], ls[3], opac, col[3];
+  std::vector<S> sh;
+};
+template <class S> Row<S> get_row(const Cloud<S>& c, int64_t i) {
+  Row<S> r;
+  for (int k = 0; k < 3; ++k) { r.mean[k] = c.mean(i, k); r.ls[k] = c.ls(i, k); r.col[k] = c.col(i, k); }
+  for (int k = 0; k < 4; ++k) r.rot[k] = c.rot(i, k);
+  r.opac = c.raw_opacities[i];
+  if (c.sh_degree > 0)
+    for (int k = 0; k < 3 * sh_count(c.sh_degree); ++k) r.sh.push_back(c.sh_rest[k * c.n + i]);
+  return r;
+}
+template <class S> Cloud<S> from_rows(const std::vector<Row<S>>& rows, int sh_degree) {
+  Cloud<S> c;
+  c.resize((int64_t)rows.size());
+  c.sh_degree = sh_degree;
+  const int64_t n = c.n;
+  if (sh_degree > 0) c.sh_rest.assign(3 * sh_count(sh_degree) * n, S(0));
+  for (int64_t i = 0; i < n; ++i) {
+    const Row<S>& r = rows[(std::size_t)i];
+    for (int k = 0; k < 3; ++k) { c.mean(i, k) = r.mean[k]; c.ls(i, k) = r.ls[k]; c.col(i, k) = r.col[k]; }
+    for (int k = 0; k < 4; ++k) c.rot(i, k) = r.rot[k];
+    c.raw_opacities[i] = r.opac;
+    for (std::size_t k = 0; k < r.sh.size(); ++k) c.sh_rest[k * n + i] = r.sh[k];
+  }
+  return c;
+}
+}  // namespace detail
+
+// densify.hpp:81-153. Clones and split children are appended in parent order (one
+// row per clone, two per split), then split parents and Gaussians under the opacity
+// floor are dropped; moments follow the rows (new rows zero), the window is cleared.
+template <class S, class M = StdMath>
+DensifyStats densify_and_prune(Cloud<S>& cloud, TrainState<S>& state, const DensifyConfig& cfg, S scene_extent,
+                               std::mt19937& rng) {
+  cfg.validate();
+  if (!(scene_extent > S(0))) throw std::invalid_argument("densify_and_prune: scene extent must be positive");
+  const int64_t n = cloud.n;
+  DensifyStats stats;
+  const S tmin = S(cfg.grad_threshold_min), tmax = S(cfg.grad_threshold_max);
+  const S size_split = S(cfg.percent_dense) * scene_extent;
+  std::vector<bool> remove((std::size_t)n, false);
+  std::vector<detail::Row<S>> added;
+  for (int64_t i = 0; i < n; ++i) {
+    if (state.grad_count[i] <= 0) continue;
+    const S count = S(state.grad_count[i]);
+    const S mean_grad = state.grad_accum[i] / count;
+    const S mean_omc = state.elev_accum[i] / count;
+    const S threshold = tmin + mean_omc * (tmax - tmin);
+    if (mean_grad < threshold) continue;
+    const V3<S> s{{M::exp(cloud.ls(i, 0)), M::exp(cloud.ls(i, 1)), M::exp(cloud.ls(i, 2))}};
+    const S max_scale = std::max(s[0], std::max(s[1], s[2]));
+    if (max_scale < size_split) {
+      added.push_back(detail::get_row(cloud, i));
+      ++stats.cloned;
+    } else {
+      const M3<S> rot = rotation_from_quaternion(cloud.rot_v(i));
+      for (int child = 0; child < 2; ++child) {
+        detail::Row<S> row = detail::get_row(cloud, i);
+        const V3<S> e = unit_ball_normal<S>(rng);
+        const V3<S> offset = mulv(rot, V3<S>{{s[0] * e[0], s[1] * e[1], s[2] * e[2]}});
+        const S shrink = M::log(S(cfg.split_scale_divisor));
+        for (int k = 0; k < 3; ++k) {
+          row.mean[k] += offset[k];
+          row.ls[k] -= shrink;
+        }
+        added.push_back(std::move(row));
+      }
+      remove[(std::size_t)i] = true;
+      ++stats.split;
+    }
+  }
+  std::vector<detail::Row<S>> rows;
+  std::vector<int64_t> src;  // state row of each output row, -1 = fresh zeros
+  const int64_t total = n + (int64_t)added.size();
+  for (int64_t i = 0; i < total; ++i) {
+    if (i < n && remove[(std::size_t)i]) continue;
+    const S raw = i < n ? cloud.raw_opacities[i] : added[(std::size_t)(i - n)].opac;
+    if (sigmoid<S, M>(raw) < S(cfg.opacity_prune_floor)) {
+      ++stats.pruned;
+      continue;
+    }
+    rows.push_back(i < n ? detail::get_row(cloud, i) : added[(std::size_t)(i - n)]);
+    src.push_back(i < n ? i : -1);
+  }
+  const int sh_degree = cloud.sh_degree;
+  cloud = detail::from_rows(rows, sh_degree);
+  TrainState<S> out;
+  out.init(cloud.n);
+  const int64_t m = cloud.n;
+  auto move_rows = [&](const std::vector<S>& from, std::vector<S>& to, int width) {
+    for (int64_t k = 0; k < m; ++k)
+      if (src[(std::size_t)k] >= 0)
+        for (int c = 0; c < width; ++c) to[c * m + k] = from[c * n + src[(std::size_t)k]];
+  };
+  move_rows(state.means_m, out.means_m, 3); move_rows(state.means_v, out.means_v, 3);
+  move_rows(state.rot_m, out.rot_m, 4);     move_rows(state.rot_v, out.rot_v, 4);
+  move_rows(state.scale_m, out.scale_m, 3); move_rows(state.scale_v, out.scale_v, 3);
+  move_rows(state.opac_m, out.opac_m, 1);   move_rows(state.opac_v, out.opac_v, 1);
+  move_rows(state.color_m, out.color_m, 3); move_rows(state.color_v, out.color_v, 3);
+  state = std::move(out);  // window cleared (init), densify.hpp:151
+  return stats;
+}
+
+// densify.hpp:158-166.
+template <class S, class M = StdMath>
+void reset_opacity(Cloud<S>& cloud, TrainState<S>& state, S ceiling = S(0.01)) {
+  for (int64_t i = 0; i < cloud.n; ++i)
+    cloud.raw_opacities[i] = logit<S, M>(std::min(sigmoid<S, M>(cloud.raw_opacities[i]), ceiling));
+  std::fill(state.opac_m.begin(), state.opac_m.end(), S(0));
+  std::fill(state.opac_v.begin(), state.opac_v.end(), S(0));
+}
+
+// densify.hpp:39-49.
+template <class S> inline S dynamic_threshold(S elevation, const DensifyConfig& cfg) {
+  if (!(std::abs(elevation) <= pi_v<S> / 2 + S(1e-12)))
+    throw std::domain_error("dynamic_threshold: elevation outside [-pi/2, pi/2]");
+  const S tmin = S(cfg.grad_threshold_min), tmax = S(cfg.grad_threshold_max);
+  return std::fma(S(1) - std::cos(elevation), tmax - tmin, tmin);
 }
 
 // ------------------------------------------------------------------ scenes (tests/scenes.hpp:11-73)

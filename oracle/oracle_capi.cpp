@@ -281,6 +281,110 @@ double oracle_photometric_loss(const double* rendered, const double* target, int
   return loss;
 }
 
+// densify_and_prune<float, M> (proj/include/odgs/densify.hpp:81-153) on a float cloud
+// and TrainState. moments: the ten Adam arrays concatenated in TrainState order
+// (means_m 3n, means_v 3n, rot_m 4n, rot_v 4n, scale_m 3n, scale_v 3n, opac_m n,
+// opac_v n, color_m 3n, color_v 3n = 28 n). cfg: {grad_threshold_min,
+// grad_threshold_max, percent_dense, opacity_prune_floor, split_scale_divisor}.
+// Outputs are written into caller buffers sized for n_cap rows (n_cap >= 3 n is always
+// enough): params 14 n_out (means 3, rotations 4, log_scales 3, raw 1, colors 3, each
+// block n_out long), moments 28 n_out; stats = {cloned, split, pruned, n_out};
+// *next_draw = the generator's next 32-bit output afterwards (stream position check).
+int oracle_densify(int portable, int64_t n, const double* params, const double* moments, const double* grad_accum,
+                   const double* elev_accum, const int32_t* grad_count, const double* cfg, double extent,
+                   uint32_t seed, int64_t n_cap, double* params_out, double* moments_out, int64_t* stats,
+                   uint32_t* next_draw, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Cloud<float> c;
+    c.resize(n);
+    auto take = [&](std::vector<float>& v, const double* src, int64_t count) {
+      for (int64_t k = 0; k < count; ++k) v[(std::size_t)k] = (float)src[k];
+    };
+    take(c.means, params, 3 * n);
+    take(c.rotations, params + 3 * n, 4 * n);
+    take(c.log_scales, params + 7 * n, 3 * n);
+    take(c.raw_opacities, params + 10 * n, n);
+    take(c.colors, params + 11 * n, 3 * n);
+    TrainState<float> st;
+    st.init(n);
+    std::vector<float>* mv[10] = {&st.means_m, &st.means_v, &st.rot_m, &st.rot_v, &st.scale_m,
+                                  &st.scale_v, &st.opac_m, &st.opac_v, &st.color_m, &st.color_v};
+    const int widths[10] = {3, 3, 4, 4, 3, 3, 1, 1, 3, 3};
+    int64_t off = 0;
+    for (int k = 0; k < 10; ++k) {
+      take(*mv[k], moments + off, widths[k] * n);
+      off += widths[k] * n;
+    }
+    take(st.grad_accum, grad_accum, n);
+    take(st.elev_accum, elev_accum, n);
+    for (int64_t i = 0; i < n; ++i) st.grad_count[(std::size_t)i] = grad_count[i];
+    DensifyConfig dc;
+    dc.grad_threshold_min = cfg[0];
+    dc.grad_threshold_max = cfg[1];
+    dc.percent_dense = cfg[2];
+    dc.opacity_prune_floor = cfg[3];
+    dc.split_scale_divisor = cfg[4];
+    std::mt19937 rng(seed);
+    const DensifyStats ds = portable ? densify_and_prune<float, PortableMath>(c, st, dc, (float)extent, rng)
+                                     : densify_and_prune<float, StdMath>(c, st, dc, (float)extent, rng);
+    const int64_t m = c.n;
+    if (m > n_cap) throw std::runtime_error("oracle_densify: output capacity too small");
+    stats[0] = ds.cloned; stats[1] = ds.split; stats[2] = ds.pruned; stats[3] = m;
+    auto put = [&](const std::vector<float>& v, double* dst) {
+      for (std::size_t k = 0; k < v.size(); ++k) dst[k] = v[k];
+    };
+    put(c.means, params_out);
+    put(c.rotations, params_out + 3 * m);
+    put(c.log_scales, params_out + 7 * m);
+    put(c.raw_opacities, params_out + 10 * m);
+    put(c.colors, params_out + 11 * m);
+    off = 0;
+    for (int k = 0; k < 10; ++k) {
+      put(*mv[k], moments_out + off);
+      off += widths[k] * m;
+    }
+    *next_draw = (uint32_t)rng();
+  });
+}
+
+// reset_opacity<float, M> (densify.hpp:158-166) on the raw opacities, in place.
+int oracle_reset_opacity(int portable, int64_t n, double* raw_opacities, double ceiling, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    Cloud<float> c;
+    c.resize(n);
+    for (int64_t i = 0; i < n; ++i) c.raw_opacities[(std::size_t)i] = (float)raw_opacities[i];
+    TrainState<float> st;
+    st.init(n);
+    if (portable) reset_opacity<float, PortableMath>(c, st, (float)ceiling);
+    else reset_opacity<float, StdMath>(c, st, (float)ceiling);
+    for (int64_t i = 0; i < n; ++i) raw_opacities[i] = c.raw_opacities[(std::size_t)i];
+  });
+}
+
+// count samples of detail::unit_ball_normal<float> (densify.hpp:61-69) from
+// std::mt19937(seed), (x, y, z) per sample; returns the generator's next output.
+uint32_t oracle_unit_ball(uint32_t seed, int64_t count, float* out) {
+  std::mt19937 rng(seed);
+  for (int64_t k = 0; k < count; ++k) {
+    const V3<float> e = unit_ball_normal<float>(rng);
+    for (int c = 0; c < 3; ++c) out[3 * k + c] = e[c];
+  }
+  return (uint32_t)rng();
+}
+
+// dynamic_threshold<double> (densify.hpp:39-49); returns 3 on domain_error.
+int oracle_dynamic_threshold(double elevation, double tmin, double tmax, double* out) {
+  DensifyConfig c;
+  c.grad_threshold_min = tmin;
+  c.grad_threshold_max = tmax;
+  try {
+    *out = dynamic_threshold(elevation, c);
+  } catch (const std::domain_error&) {
+    return 3;
+  }
+  return 0;
+}
+
 int oracle_hardware_concurrency() { return effective_threads(0); }
 
 }  // extern "C"

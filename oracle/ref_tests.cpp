@@ -1322,6 +1322,220 @@ TEST_CASE("acceptance 5: a yaw by whole pixels circularly shifts the panorama") 
   CHECK(worst <= 1e-4);
 }
 
+// ================================================================== test_densify.cpp
+namespace {
+Cloud<double> marker_cloud(int n) {  // test_densify.cpp:14-24
+  Cloud<double> cloud;
+  cloud.resize(n);
+  for (int i = 0; i < n; ++i) {
+    cloud.mean(i, 0) = i; cloud.mean(i, 1) = 0.5 * i; cloud.mean(i, 2) = 2.0 + i;
+    for (int c = 0; c < 3; ++c) cloud.ls(i, c) = std::log(0.05);
+    cloud.raw_opacities[i] = logit(0.5);
+    for (int c = 0; c < 3; ++c) cloud.col(i, c) = 0.1 * (i + 1);
+  }
+  return cloud;
+}
+void set_window(TrainState<double>& state, int i, double mean_grad, double elevation, int count = 2) {
+  state.grad_count[i] = count;  // test_densify.cpp:28-34
+  state.grad_accum[i] = mean_grad * count;
+  state.elev_accum[i] = (1.0 - std::cos(elevation)) * count;
+}
+}  // namespace
+
+TEST_CASE("densify: dynamic_threshold") {  // test_densify.cpp:37-74
+  const DensifyConfig cfg;
+  const double kPi = pi_v<double>;
+  CHECK(dynamic_threshold(0.0, cfg) == 2e-5);
+  CHECK(dynamic_threshold(kPi / 2, cfg) == 1e-4);
+  CHECK(dynamic_threshold(-kPi / 2, cfg) == 1e-4);
+  CHECK(dynamic_threshold(kPi / 3, cfg) == Approx(6e-5).epsilon(1e-12));
+  double prev = dynamic_threshold(0.0, cfg);
+  bool even = true, mono = true;
+  for (int k = 1; k < 1000; ++k) {
+    const double theta = (kPi / 2) * k / 999.0;
+    const double tau = dynamic_threshold(theta, cfg);
+    even = even && tau == dynamic_threshold(-theta, cfg);
+    mono = mono && tau >= prev;
+    prev = tau;
+  }
+  CHECK(even);
+  CHECK(mono);
+  CHECK(prev == Approx(1e-4).epsilon(1e-12));
+  CHECK_THROWS_AS(dynamic_threshold(1.8, cfg), std::domain_error);
+  DensifyConfig bad = cfg;
+  bad.grad_threshold_min = 2e-4;
+  CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+  bad = cfg;
+  bad.percent_dense = 0.0;
+  CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+}
+
+TEST_CASE("densify: densify_and_prune") {  // test_densify.cpp:76-195
+  const DensifyConfig cfg;
+  const double extent = 100.0;
+  const double kPi = pi_v<double>;
+  std::mt19937 rng(41);
+  {  // zero gradients leave the cloud untouched
+    auto cloud = marker_cloud(4);
+    TrainState<double> state;
+    state.init(4);
+    for (int i = 0; i < 4; ++i) set_window(state, i, 0.0, 0.3);
+    const auto before = cloud;
+    const auto stats = densify_and_prune(cloud, state, cfg, extent, rng);
+    CHECK(stats.cloned == 0);
+    CHECK(stats.split == 0);
+    CHECK(stats.pruned == 0);
+    CHECK(cloud.n == 4);
+    CHECK(cloud.means == before.means);
+    bool zero = true;
+    for (int32_t c : state.grad_count) zero = zero && c == 0;
+    CHECK(zero);
+  }
+  {  // equatorial Gaussian over threshold and small: cloned
+    auto cloud = marker_cloud(3);
+    TrainState<double> state;
+    state.init(3);
+    set_window(state, 0, 5e-5, 0.0);
+    const auto stats = densify_and_prune(cloud, state, cfg, extent, rng);
+    CHECK(stats.cloned == 1);
+    CHECK(cloud.n == 4);
+    for (int c = 0; c < 3; ++c) CHECK(cloud.mean(3, c) == cloud.mean(0, c));
+    CHECK(cloud.raw_opacities[3] == cloud.raw_opacities[0]);
+    for (int c = 0; c < 3; ++c) CHECK(cloud.col(3, c) == cloud.col(0, c));
+  }
+  {  // same gradient observed only near the pole: threshold blocks it
+    auto cloud = marker_cloud(3);
+    TrainState<double> state;
+    state.init(3);
+    set_window(state, 0, 5e-5, kPi / 2);
+    const auto stats = densify_and_prune(cloud, state, cfg, extent, rng);
+    CHECK(stats.cloned == 0);
+    CHECK(stats.split == 0);
+    CHECK(cloud.n == 3);
+  }
+  {  // large Gaussian over threshold: split into two shrunken children
+    auto cloud = marker_cloud(2);
+    for (int c = 0; c < 3; ++c) cloud.ls(0, c) = std::log(0.5);
+    const double q0[4] = {0.8, 0.1, -0.3, 0.2};
+    for (int c = 0; c < 4; ++c) cloud.rot(0, c) = q0[c];
+    TrainState<double> state;
+    state.init(2);
+    set_window(state, 0, 5e-5, 0.0);
+    const V3<double> parent_mean = cloud.mean_v(0);
+    const V4<double> parent_quat = cloud.rot_v(0);
+    const V3<double> parent_scale{{std::exp(cloud.ls(0, 0)), std::exp(cloud.ls(0, 1)), std::exp(cloud.ls(0, 2))}};
+    const double parent_opacity = sigmoid(cloud.raw_opacities[0]);
+    const auto stats = densify_and_prune(cloud, state, cfg, extent, rng);
+    CHECK(stats.split == 1);
+    CHECK(cloud.n == 3);
+    const M3<double> rot = rotation_from_quaternion(parent_quat);
+    for (int child : {1, 2}) {
+      CHECK(sigmoid(cloud.raw_opacities[child]) == Approx(parent_opacity).epsilon(1e-12));
+      double ds = 0, dq = 0;
+      for (int c = 0; c < 3; ++c) ds = std::max(ds, std::abs(std::exp(cloud.ls(child, c)) * 1.6 - parent_scale[c]));
+      for (int c = 0; c < 4; ++c) dq = std::max(dq, std::abs(cloud.rot(child, c) - parent_quat[c]));
+      CHECK(ds < 1e-12);
+      CHECK(dq == 0.0);
+      V3<double> d;
+      for (int c = 0; c < 3; ++c) d[c] = cloud.mean(child, c) - parent_mean[c];
+      const V3<double> l = mulv(transpose(rot), d);
+      const V3<double> local{{l[0] / parent_scale[0], l[1] / parent_scale[1], l[2] / parent_scale[2]}};
+      CHECK(norm3(local) <= 1.0 + 1e-12);
+    }
+  }
+  {  // transparent Gaussians are pruned and moments follow the survivors
+    auto cloud = marker_cloud(4);
+    cloud.raw_opacities[1] = logit(0.004);
+    TrainState<double> state;
+    state.init(4);
+    for (int c = 0; c < 3; ++c) state.means_m[c * 4 + 3] = 7.0;
+    const auto stats = densify_and_prune(cloud, state, cfg, extent, rng);
+    CHECK(stats.pruned == 1);
+    CHECK(cloud.n == 3);
+    CHECK(cloud.col(1, 0) == Approx(0.3));
+    CHECK(state.means_m[0 * 3 + 2] == 7.0);
+    CHECK(state.n == 3);
+  }
+  {  // lowering both thresholds densifies a superset
+    DensifyConfig loose = cfg;
+    loose.grad_threshold_min = 1e-5;
+    loose.grad_threshold_max = 5e-5;
+    const int n = 12;
+    std::mt19937 rng_elev(43);
+    std::uniform_real_distribution<double> u(0.0, kPi / 2);
+    std::vector<double> elevations;
+    for (int i = 0; i < n; ++i) elevations.push_back(u(rng_elev));
+    auto run = [&](const DensifyConfig& c) {
+      auto cloud = marker_cloud(n);
+      TrainState<double> state;
+      state.init(n);
+      for (int i = 0; i < n; ++i) set_window(state, i, 4e-5, elevations[(std::size_t)i]);
+      std::mt19937 local_rng(47);
+      densify_and_prune(cloud, state, c, extent, local_rng);
+      return cloud.n;
+    };
+    const int64_t strict_n = run(cfg), loose_n = run(loose);
+    CHECK(loose_n >= strict_n);
+    CHECK(loose_n > n);
+  }
+}
+
+TEST_CASE("densify: reset_opacity") {  // test_densify.cpp:197-213
+  auto cloud = marker_cloud(3);
+  cloud.raw_opacities[0] = logit(0.8);
+  cloud.raw_opacities[1] = logit(0.006);
+  TrainState<double> state;
+  state.init(3);
+  std::fill(state.opac_m.begin(), state.opac_m.end(), 0.5);
+  std::fill(state.opac_v.begin(), state.opac_v.end(), 0.25);
+  reset_opacity(cloud, state);
+  CHECK(sigmoid(cloud.raw_opacities[0]) == Approx(0.01).epsilon(1e-12));
+  CHECK(sigmoid(cloud.raw_opacities[1]) == Approx(0.006).epsilon(1e-12));
+  CHECK(sigmoid(cloud.raw_opacities[2]) == Approx(0.01).epsilon(1e-12));
+  bool zero = true;
+  for (double v : state.opac_m) zero = zero && v == 0;
+  for (double v : state.opac_v) zero = zero && v == 0;
+  CHECK(zero);
+}
+
+TEST_CASE("densify: float portable restatement makes the same decisions as float libm") {
+  // The GPU parity target is densify_and_prune<float, PortableMath>; on a random
+  // cloud with a random window it must agree with <float, StdMath> on every count and
+  // (within the last-ulp exp/log differences) on every value.
+  std::mt19937 rng(5);
+  auto base = random_cloud<float>(rng, 3000);
+  TrainState<float> st;
+  st.init(base.n);
+  std::uniform_real_distribution<float> u(0.f, 1.f);
+  for (int64_t i = 0; i < base.n; ++i) {
+    st.grad_count[i] = (int32_t)(u(rng) * 4);
+    st.grad_accum[i] = u(rng) * 2e-4f * (float)st.grad_count[i];
+    st.elev_accum[i] = u(rng) * (float)st.grad_count[i];
+    if (u(rng) < 0.1f) base.raw_opacities[i] = -6.0f;
+  }
+  auto ca = base, cb = base;
+  auto sa = st, sb = st;
+  std::mt19937 ra(9), rb(9);
+  const DensifyConfig cfg;
+  const auto a = densify_and_prune<float, StdMath>(ca, sa, cfg, 60.0f, ra);
+  const auto b = densify_and_prune<float, PortableMath>(cb, sb, cfg, 60.0f, rb);
+  std::printf("  cloned %lld split %lld pruned %lld -> %lld\n", (long long)a.cloned, (long long)a.split,
+              (long long)a.pruned, (long long)ca.n);
+  CHECK(a.cloned == b.cloned);
+  CHECK(a.split == b.split);
+  CHECK(a.pruned == b.pruned);
+  CHECK(a.cloned > 0);
+  CHECK(a.split > 0);
+  CHECK(a.pruned > 0);
+  REQUIRE(ca.n == cb.n);
+  double w = 0;
+  for (std::size_t k = 0; k < ca.means.size(); ++k) w = std::max(w, (double)std::abs(ca.means[k] - cb.means[k]));
+  for (std::size_t k = 0; k < ca.log_scales.size(); ++k)
+    w = std::max(w, (double)std::abs(ca.log_scales[k] - cb.log_scales[k]));
+  CHECK(w < 1e-5);
+  CHECK(ra() == rb());  // same number of draws
+}
+
 // ================================================================== PortableMath (this build)
 namespace {
 int64_t ulp_diff(float a, float b) {
@@ -1365,6 +1579,24 @@ TEST_CASE("portable math: within 1 ulp of libm on the arguments the path sees") 
   CHECK(w_cos <= 1);
   CHECK(w_atan2 <= 1);
   CHECK(w_hypot <= 1);
+  {  // pm_logf (logit and the split shrink) over the whole positive float range
+    std::uniform_real_distribution<float> mant(1.0f, 2.0f);
+    std::uniform_int_distribution<int> ex2(-149, 127);
+    int64_t w_log = 0, diff_log = 0;
+    for (int k = 0; k < n; ++k) {
+      const float x = std::ldexp(mant(rng), ex2(rng));
+      if (!(x > 0.0f) || !std::isfinite(x)) continue;
+      const int64_t d = ulp_diff(pm_logf(x), std::log(x));
+      w_log = std::max(w_log, d);
+      diff_log += d != 0;
+    }
+    std::printf("  pm_logf: max ulp %lld (differs %lld of %d)\n", (long long)w_log, (long long)diff_log, n);
+    CHECK(w_log <= 1);
+    CHECK(pm_logf(1.0f) == 0.0f);
+    CHECK(pm_logf(0.0f) == -INFINITY);
+    CHECK(pm_logf(-1.0f) != pm_logf(-1.0f));
+    CHECK(pm_logf(1.6f) == std::log(1.6f));
+  }
   // Special values.
   CHECK(pm_atan2f(0.0f, -1.0f) == std::atan2(0.0f, -1.0f));
   CHECK(pm_atan2f(-0.0f, -1.0f) == std::atan2(-0.0f, -1.0f));

@@ -75,6 +75,16 @@ class AdamParams(C.Structure):
                 ("lr_opacity", C.c_float), ("lr_color", C.c_float), ("step", C.c_int64)]
 
 
+class DensifyConfig(C.Structure):
+    _fields_ = [("grad_threshold_min", C.c_double), ("grad_threshold_max", C.c_double),
+                ("percent_dense", C.c_double), ("opacity_prune_floor", C.c_double),
+                ("split_scale_divisor", C.c_double)]
+
+
+class DensifyStats(C.Structure):
+    _fields_ = [("cloned", C.c_int64), ("split", C.c_int64), ("pruned", C.c_int64), ("n_out", C.c_int64)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("n_gaussians", C.c_int64), ("n_splats", C.c_int64),
@@ -115,6 +125,17 @@ SIGNATURES = {
     "odgs_photometric_loss": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float, _P, C.POINTER(C.c_double)]),
     "odgs_adam_step": (C.c_int, [_P, C.POINTER(Params), C.POINTER(Grads), C.POINTER(TrainState),
                                  C.POINTER(AdamParams)]),
+    "odgs_default_densify_config": (None, [C.POINTER(DensifyConfig)]),
+    "odgs_rng_create": (_P, [C.c_uint32]),
+    "odgs_rng_destroy": (None, [_P]),
+    "odgs_rng_next": (C.c_uint32, [_P]),
+    "odgs_rng_unit_ball": (None, [_P, C.c_int64, C.POINTER(C.c_float)]),
+    "odgs_densify_plan": (C.c_int, [_P, C.POINTER(Params), C.POINTER(TrainState), C.POINTER(DensifyConfig),
+                                    C.c_float, C.POINTER(DensifyStats)]),
+    "odgs_densify_apply": (C.c_int, [_P, C.POINTER(Params), C.POINTER(TrainState), C.POINTER(C.c_float),
+                                     C.POINTER(Params), C.POINTER(TrainState)]),
+    "odgs_reset_opacity": (C.c_int, [_P, C.POINTER(Params), C.POINTER(TrainState), C.c_float]),
+    "odgs_dynamic_threshold": (C.c_int, [C.c_double, C.POINTER(DensifyConfig), C.POINTER(C.c_double)]),
     "odgs_cull": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.c_float, C.c_float,
                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }

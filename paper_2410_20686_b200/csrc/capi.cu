@@ -6,6 +6,7 @@
 #include <cstring>
 #include <limits>
 #include <new>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -48,6 +49,15 @@ struct odgs_ctx {
   DevBuf cloud_buf, dl_buf, grads_buf, signs_buf, cull_buf, loss_buf;
   float* d_unit_signs = nullptr;
   int64_t launches = 0;
+  // densify_and_prune plan (odgs_densify_plan -> odgs_densify_apply)
+  DevBuf densify_buf, unit_ball_buf, misc_buf;
+  struct {
+    bool valid = false;
+    int64_t n = 0, split = 0, n_out = 0;
+    const float* key = nullptr;  // cloud->means of the planned cloud
+    uint32_t total_a = 0;
+    float log_shrink = 0.0f;
+  } plan;
 };
 
 struct odgs_frame {
@@ -573,6 +583,9 @@ void odgs_ctx_destroy(odgs_ctx* ctx) {
     release(ctx->signs_buf, ctx->stream);
     release(ctx->cull_buf, ctx->stream);
     release(ctx->loss_buf, ctx->stream);
+    release(ctx->densify_buf, ctx->stream);
+    release(ctx->unit_ball_buf, ctx->stream);
+    release(ctx->misc_buf, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
   }
   if (ctx->d_err) cudaFree(ctx->d_err);
@@ -1129,5 +1142,214 @@ odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera*
   *out_count = c;
   return ok(ctx);
 }
+
+// ------------------------------------------------------------------ density control
+void odgs_default_densify_config(odgs_densify_config* out) {  // densify.hpp:16-24
+  if (!out) return;
+  out->grad_threshold_min = 2e-5;
+  out->grad_threshold_max = 1e-4;
+  out->percent_dense = 1e-3;
+  out->opacity_prune_floor = 0.005;
+  out->split_scale_divisor = 1.6;
+}
+
+struct odgs_rng {
+  std::mt19937 gen;
+};
+
+odgs_rng* odgs_rng_create(uint32_t seed) { return new (std::nothrow) odgs_rng{std::mt19937(seed)}; }
+void odgs_rng_destroy(odgs_rng* rng) { delete rng; }
+uint32_t odgs_rng_next(odgs_rng* rng) { return rng ? (uint32_t)rng->gen() : 0u; }
+
+void odgs_rng_unit_ball(odgs_rng* rng, int64_t count, float* out) {
+  if (!rng || !out) return;
+  for (int64_t k = 0; k < count; ++k) {
+    // densify.hpp:61-69: one normal_distribution per sample (its cached polar value
+    // lives across rejected tries only); Vec3(g(), g(), g()) evaluates right to left
+    // under GCC, so the first draw is z. Norm in float, Eigen's order x² + (y² + z²).
+    std::normal_distribution<double> gauss;
+    for (;;) {
+      const float z = (float)gauss(rng->gen);
+      const float y = (float)gauss(rng->gen);
+      const float x = (float)gauss(rng->gen);
+      const float yy = y * y, zz = z * z, xx = x * x;
+      if (std::sqrt(xx + (yy + zz)) <= 1.0f) {
+        out[3 * k] = x;
+        out[3 * k + 1] = y;
+        out[3 * k + 2] = z;
+        break;
+      }
+    }
+  }
+}
+
+namespace {
+odgs_status check_densify_config(odgs_ctx* ctx, const odgs_densify_config* c) {  // densify.hpp:26-32
+  if (!c) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify: null config");
+  if (!(c->grad_threshold_min > 0) || !(c->grad_threshold_max >= c->grad_threshold_min))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1,
+                     "DensifyConfig: need 0 < grad_threshold_min <= grad_threshold_max");
+  if (!(c->percent_dense > 0) || !(c->percent_dense < 1))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "DensifyConfig: percent_dense outside (0, 1)");
+  return ODGS_OK;
+}
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+}  // namespace
+
+odgs_status odgs_densify_plan(odgs_ctx* ctx, const odgs_params* cloud, const odgs_train_state* state,
+                              const odgs_densify_config* cfg, float scene_extent, odgs_densify_stats* stats) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  ctx->plan.valid = false;
+  odgs_status st;
+  if ((st = check_densify_config(ctx, cfg)) != ODGS_OK) return st;
+  if (!(scene_extent > 0.0f))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_and_prune: scene extent must be positive");
+  if (!cloud || !state || !stats || cloud->n < 0 || cloud->n >= (int64_t)1 << 31)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_and_prune: bad arguments");
+  const int64_t n = cloud->n;
+  if (n > 0 && (!cloud->means || !cloud->rotations || !cloud->log_scales || !cloud->raw_opacities ||
+                !cloud->colors || !state->grad_accum || !state->elev_accum || !state->grad_count))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_and_prune: null buffer");
+  const size_t arr = align256((size_t)n * 4);
+  ODGS_CUDA(ctx, ensure(ctx->densify_buf, 256 + 6 * arr + scan_temp_bytes(n), ctx->stream));
+  char* base = ctx->densify_buf.as<char>();
+  auto* counters = reinterpret_cast<unsigned long long*>(base);  // [0..2] counts, [3..5] totals, [6] bad
+  uint32_t* u[6];
+  for (int k = 0; k < 6; ++k) u[k] = reinterpret_cast<uint32_t*>(base + 256 + k * arr);
+  void* scan_tmp = base + 256 + 6 * arr;
+  ODGS_CUDA(ctx, cudaMemsetAsync(counters, 0, 6 * sizeof(unsigned long long), ctx->stream));
+  ODGS_CUDA(ctx, cudaMemsetAsync(counters + 6, 0xff, sizeof(unsigned long long), ctx->stream));
+  DensifyArgs a;
+  a.n = n;
+  a.rotations = cloud->rotations; a.log_scales = cloud->log_scales; a.raw_opacities = cloud->raw_opacities;
+  a.grad_accum = state->grad_accum; a.elev_accum = state->elev_accum; a.grad_count = state->grad_count;
+  a.tmin = (float)cfg->grad_threshold_min;  // Scalar(cfg.*) (densify.hpp:92-94)
+  a.tmax = (float)cfg->grad_threshold_max;
+  a.size_split = (float)cfg->percent_dense * scene_extent;
+  a.prune_floor = (float)cfg->opacity_prune_floor;
+  a.keep_self = u[0]; a.added_kept = u[1]; a.split_flag = u[2];
+  a.counters = counters;
+  a.bad_quaternion = counters + 6;
+  launch_densify_classify(a, ctx->stream);
+  for (int k = 0; k < 3; ++k) exclusive_scan_u32(u[k], u[3 + k], n, scan_tmp, counters + 3 + k, ctx->stream);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->h_scratch, counters, 7 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  unsigned long long h[7];
+  std::memcpy(h, ctx->h_scratch, sizeof h);
+  if (h[6] != kNoError)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, (int64_t)h[6], "normalize_quaternion: near-zero quaternion");
+  stats->cloned = (int64_t)h[0];
+  stats->split = (int64_t)h[1];
+  stats->pruned = (int64_t)h[2];
+  stats->n_out = (int64_t)(h[3] + h[4]);
+  ctx->plan.valid = true;
+  ctx->plan.n = n;
+  ctx->plan.split = (int64_t)h[5];
+  ctx->plan.n_out = stats->n_out;
+  ctx->plan.key = cloud->means;
+  ctx->plan.total_a = (uint32_t)h[3];
+  ctx->plan.log_shrink = pm_logf((float)cfg->split_scale_divisor);  // std::log(Scalar(divisor))
+  return ok(ctx);
+}
+
+odgs_status odgs_densify_apply(odgs_ctx* ctx, const odgs_params* cloud, const odgs_train_state* state,
+                               const float* unit_ball, const odgs_params* out_cloud,
+                               const odgs_train_state* out_state) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!cloud || !state || !out_cloud || !out_state || !ctx->plan.valid || ctx->plan.n != cloud->n ||
+      ctx->plan.key != cloud->means)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_apply: no matching odgs_densify_plan");
+  const int64_t n = cloud->n, m = ctx->plan.n_out;
+  if (out_cloud->n != m)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_apply: out_cloud->n must equal stats.n_out");
+  if (ctx->plan.split > 0 && !unit_ball)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_apply: unit_ball samples required");
+  const float* const mom_in[10] = {state->means_m, state->means_v, state->rot_m, state->rot_v, state->scale_m,
+                                   state->scale_v, state->opac_m, state->opac_v, state->color_m, state->color_v};
+  float* const mom_out[10] = {out_state->means_m, out_state->means_v, out_state->rot_m, out_state->rot_v,
+                              out_state->scale_m, out_state->scale_v, out_state->opac_m, out_state->opac_v,
+                              out_state->color_m, out_state->color_v};
+  if (m > 0) {
+    bool okp = out_cloud->means && out_cloud->rotations && out_cloud->log_scales && out_cloud->raw_opacities &&
+               out_cloud->colors;
+    for (int k = 0; k < 10; ++k) okp = okp && mom_in[k] && mom_out[k];
+    if (!okp) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "densify_apply: null buffer");
+    if (out_state->grad_accum) ODGS_CUDA(ctx, cudaMemsetAsync(out_state->grad_accum, 0, m * 4, ctx->stream));
+    if (out_state->elev_accum) ODGS_CUDA(ctx, cudaMemsetAsync(out_state->elev_accum, 0, m * 4, ctx->stream));
+    if (out_state->grad_count) ODGS_CUDA(ctx, cudaMemsetAsync(out_state->grad_count, 0, m * 4, ctx->stream));
+  }
+  const float* d_ball = nullptr;
+  if (ctx->plan.split > 0) {
+    const size_t bytes = (size_t)ctx->plan.split * 6 * sizeof(float);
+    ODGS_CUDA(ctx, ensure(ctx->unit_ball_buf, bytes, ctx->stream));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->unit_ball_buf.p, unit_ball, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    d_ball = ctx->unit_ball_buf.as<float>();
+  }
+  const size_t arr = align256((size_t)n * 4);
+  char* base = ctx->densify_buf.as<char>();
+  uint32_t* u[6];
+  for (int k = 0; k < 6; ++k) u[k] = reinterpret_cast<uint32_t*>(base + 256 + k * arr);
+  DensifyApplyArgs a;
+  a.n = n;
+  a.m = m;
+  a.means = cloud->means; a.rotations = cloud->rotations; a.log_scales = cloud->log_scales;
+  a.raw_opacities = cloud->raw_opacities; a.colors = cloud->colors;
+  for (int k = 0; k < 10; ++k) { a.moments[k] = mom_in[k]; a.out_moments[k] = mom_out[k]; }
+  a.out_means = out_cloud->means; a.out_rotations = out_cloud->rotations; a.out_log_scales = out_cloud->log_scales;
+  a.out_raw_opacities = out_cloud->raw_opacities; a.out_colors = out_cloud->colors;
+  a.keep_self = u[0]; a.added_kept = u[1]; a.split_flag = u[2];
+  a.off_a = u[3]; a.off_b = u[4]; a.off_c = u[5];
+  a.total_a = ctx->plan.total_a;
+  a.unit_ball = d_ball;
+  a.log_shrink = ctx->plan.log_shrink;
+  launch_densify_apply(a, ctx->stream);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  ctx->plan.valid = false;
+  return ok(ctx);
+}
+
+odgs_status odgs_reset_opacity(odgs_ctx* ctx, const odgs_params* cloud, const odgs_train_state* state,
+                               float ceiling) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!cloud || cloud->n < 0 || (cloud->n > 0 && !cloud->raw_opacities))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "reset_opacity: bad arguments");
+  const int64_t n = cloud->n;
+  if (n > 0) {
+    ODGS_CUDA(ctx, ensure(ctx->misc_buf, 256, ctx->stream));
+    auto* bad = ctx->misc_buf.as<unsigned long long>();
+    ODGS_CUDA(ctx, cudaMemsetAsync(bad, 0xff, sizeof *bad, ctx->stream));
+    launch_reset_opacity(cloud->raw_opacities, n, ceiling, bad, ctx->stream);
+    ODGS_CUDA(ctx, cudaGetLastError());
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->h_scratch, bad, sizeof *bad, cudaMemcpyDeviceToHost, ctx->stream));
+    ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    unsigned long long hb;
+    std::memcpy(&hb, ctx->h_scratch, sizeof hb);
+    if (hb != kNoError)
+      return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, (int64_t)hb, "logit: argument must lie in (0, 1)");
+  }
+  if (state && n > 0) {  // densify.hpp:164-165
+    if (state->opac_m) ODGS_CUDA(ctx, cudaMemsetAsync(state->opac_m, 0, n * 4, ctx->stream));
+    if (state->opac_v) ODGS_CUDA(ctx, cudaMemsetAsync(state->opac_v, 0, n * 4, ctx->stream));
+  }
+  return ok(ctx);
+}
+
+odgs_status odgs_dynamic_threshold(double elevation, const odgs_densify_config* cfg, double* out) {
+  if (!cfg || !out) return ODGS_ERR_INVALID_ARGUMENT;
+  const double pi = 3.141592653589793238462643383279502884;
+  if (!(std::abs(elevation) <= pi / 2 + 1e-12)) return ODGS_ERR_DOMAIN;
+  const double tmin = cfg->grad_threshold_min, tmax = cfg->grad_threshold_max;
+  *out = std::fma(1.0 - std::cos(elevation), tmax - tmin, tmin);
+  return ODGS_OK;
+}
+
 
 }  // extern "C"

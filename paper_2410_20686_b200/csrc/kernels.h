@@ -100,6 +100,39 @@ struct AdamArgs {
 };
 void launch_adam(const AdamArgs& a, cudaStream_t stream);
 
+// ------------------------------------------------------------------ densify (densify.hpp)
+// Adam moment groups in TrainState order (types.hpp:257-268): means_m/v, rot_m/v,
+// scale_m/v, opac_m/v, color_m/v.
+__host__ __device__ constexpr int moment_width(int k) { return (k == 2 || k == 3) ? 4 : (k == 6 || k == 7) ? 1 : 3; }
+
+struct DensifyArgs {
+  int64_t n;
+  const float *rotations, *log_scales, *raw_opacities;
+  const float *grad_accum, *elev_accum;
+  const int32_t* grad_count;
+  float tmin, tmax, size_split, prune_floor;
+  uint32_t *keep_self, *added_kept, *split_flag;  // [n] each
+  unsigned long long* counters;                   // [3] cloned, split, pruned
+  unsigned long long* bad_quaternion;             // first split parent with |q| <= 1e-12
+};
+void launch_densify_classify(const DensifyArgs& a, cudaStream_t stream);
+
+struct DensifyApplyArgs {
+  int64_t n, m;  // rows in, rows out
+  const float *means, *rotations, *log_scales, *raw_opacities, *colors;
+  const float* moments[10];
+  float *out_means, *out_rotations, *out_log_scales, *out_raw_opacities, *out_colors;
+  float* out_moments[10];
+  const uint32_t *keep_self, *added_kept, *split_flag, *off_a, *off_b, *off_c;
+  uint32_t total_a;
+  const float* unit_ball;  // [split][child][3]
+  float log_shrink;        // log(split_scale_divisor) in float
+};
+void launch_densify_apply(const DensifyApplyArgs& a, cudaStream_t stream);
+
+// reset_opacity (densify.hpp:158-166); *bad must hold kNoError on entry.
+void launch_reset_opacity(float* raw, int64_t n, float ceiling, unsigned long long* bad, cudaStream_t stream);
+
 // FP32 FMA throughput microbenchmark (for the roofline denominator).
 void launch_fp32_peak(int blocks, int threads, int iters, float* sink, cudaStream_t stream);
 double fp32_peak_flops_per_thread(int iters);

@@ -20,6 +20,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _capi as capi
+from .densify import DensifyConfig, DensifyStats, Rng, TrainState, densify_and_prune, reset_opacity
 from .rasterizer import (CameraPose, Context, GaussianCloud, GradBuffers, RenderOutput, RenderSettings, backward,
                          render)
 
@@ -38,6 +39,11 @@ class TrainConfig:  # optimizer.hpp:23-48 (defaults)
     lr_opacity: float = 0.05
     lr_color: float = 2.5e-3
     lambda_ssim: float = 0.2
+    # Density control schedule (optimizer.hpp:144-153); None = off. Every rank runs
+    # it on identical inputs with an identically seeded generator, so replicas stay
+    # identical without any exchange.
+    densify: Optional[DensifyConfig] = None
+    seed: int = 0
 
 
 def means_lr_at(iteration: int, cfg: TrainConfig) -> float:
@@ -87,28 +93,24 @@ class ViewShardedTrainer:
         self.settings, self.cfg, self.extent = settings, cfg, float(extent)
         self.rank, self.world, self.group = rank, world, group
         self.mine = assign_views(len(self.views), rank, world)
-        n = cloud.n
-        dev = cloud.means.device
+        self.state = TrainState(cloud.n, cloud.means.device)
+        self.rng = Rng(cfg.seed)
+        self.last_densify: Optional[DensifyStats] = None
+        H, W = views[0].height, views[0].width
+        self.dl = self.torch.empty(3 * W * H, dtype=self.torch.float32, device=cloud.means.device)
+        self.frame = RenderOutput(ctx)
+        self.iteration = 0
+        self._alloc_grads()
+
+    def _alloc_grads(self) -> None:
+        torch = self.torch
+        n, dev = self.cloud.n, self.cloud.means.device
         self.n = n
         self.flat = torch.zeros(FLAT_WIDTH * n, dtype=torch.float32, device=dev)
         self.observed = torch.zeros(n, dtype=torch.int32, device=dev)
         fv = flat_views(self.flat, n)
         self.grads = GradBuffers(fv["means"], fv["rotations"], fv["log_scales"], fv["raw_opacities"],
                                  fv["colors"], fv["pixel_grad_norm"], fv["one_minus_cos"], self.observed)
-        z = lambda a: torch.zeros_like(a)
-        c = cloud
-        self.state = {k: z(v) for k, v in (("means_m", c.means), ("means_v", c.means), ("rot_m", c.rotations),
-                                            ("rot_v", c.rotations), ("scale_m", c.log_scales),
-                                            ("scale_v", c.log_scales), ("opac_m", c.raw_opacities),
-                                            ("opac_v", c.raw_opacities), ("color_m", c.colors),
-                                            ("color_v", c.colors))}
-        self.state["grad_accum"] = torch.zeros(n, dtype=torch.float32, device=dev)
-        self.state["elev_accum"] = torch.zeros(n, dtype=torch.float32, device=dev)
-        self.state["grad_count"] = torch.zeros(n, dtype=torch.int32, device=dev)
-        H, W = views[0].height, views[0].width
-        self.dl = torch.empty(3 * W * H, dtype=torch.float32, device=dev)
-        self.frame = RenderOutput(ctx)
-        self.iteration = 0
 
     def step(self) -> float:
         torch = self.torch
@@ -131,14 +133,21 @@ class ViewShardedTrainer:
         p = capi.Params(self.n, self.cloud.means.data_ptr(), self.cloud.rotations.data_ptr(),
                         self.cloud.log_scales.data_ptr(), self.cloud.raw_opacities.data_ptr(),
                         self.cloud.colors.data_ptr())
-        st = capi.TrainState(*[self.state[k].data_ptr() for k in (
-            "means_m", "means_v", "rot_m", "rot_v", "scale_m", "scale_v", "opac_m", "opac_v", "color_m", "color_v",
-            "grad_accum", "elev_accum", "grad_count")])
+        st = self.state.to_c()
         ap = capi.AdamParams(means_lr_at(self.iteration, self.cfg) * self.extent, self.cfg.lr_rotation,
                              self.cfg.lr_scale, self.cfg.lr_opacity, self.cfg.lr_color, step)
         g = self.grads.to_c()
         ctx.check(lib.odgs_adam_step(ctx.handle, byref(p), byref(g), byref(st), byref(ap)))
         self.iteration = step
+        self.state.iteration = step
+        self.last_densify = None
+        d = self.cfg.densify
+        if d is not None and step <= d.densify_until:  # optimizer.hpp:144-153
+            if d.densify_interval > 0 and step % d.densify_interval == 0:
+                self.last_densify = densify_and_prune(ctx, self.cloud, self.state, d, self.extent, self.rng)
+                self._alloc_grads()
+            if d.opacity_reset_interval > 0 and step % d.opacity_reset_interval == 0:
+                reset_opacity(ctx, self.cloud, self.state)
         return loss_sum
 
 

@@ -44,6 +44,16 @@ def lib() -> C.CDLL:
         L.oracle_photometric_loss.restype = C.c_double
         L.oracle_photometric_loss.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, dp]
         L.oracle_hardware_concurrency.restype = C.c_int
+        L.oracle_densify.restype = C.c_int
+        L.oracle_densify.argtypes = [C.c_int, C.c_int64, dp, dp, dp, dp, C.POINTER(C.c_int32), dp, C.c_double,
+                                     C.c_uint32, C.c_int64, dp, dp, C.POINTER(C.c_int64), C.POINTER(C.c_uint32),
+                                     C.c_char_p, C.c_int]
+        L.oracle_reset_opacity.restype = C.c_int
+        L.oracle_reset_opacity.argtypes = [C.c_int, C.c_int64, dp, C.c_double, C.c_char_p, C.c_int]
+        L.oracle_unit_ball.restype = C.c_uint32
+        L.oracle_unit_ball.argtypes = [C.c_uint32, C.c_int64, C.POINTER(C.c_float)]
+        L.oracle_dynamic_threshold.restype = C.c_int
+        L.oracle_dynamic_threshold.argtypes = [C.c_double, C.c_double, C.c_double, dp]
         _lib = L
     return _lib
 
@@ -133,3 +143,78 @@ def render(cloud, R, t, width, height, settings: OracleSettings = OracleSettings
     if rc != 0:
         raise OracleError(rc, err.value.decode())
     return OracleFrame(h)
+
+
+# ------------------------------------------------------------------ densify (densify.hpp:81-166)
+MOMENT_WIDTHS = (("means_m", 3), ("means_v", 3), ("rot_m", 4), ("rot_v", 4), ("scale_m", 3), ("scale_v", 3),
+                 ("opac_m", 1), ("opac_v", 1), ("color_m", 3), ("color_v", 3))
+PARAM_WIDTHS = (("means", 3), ("rotations", 4), ("log_scales", 3), ("raw_opacities", 1), ("colors", 3))
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def _split(flat, widths, m):
+    out, off = {}, 0
+    for name, w in widths:
+        seg = flat[off * m:(off + w) * m]
+        out[name] = seg.reshape(w, m) if w > 1 else seg
+        off += w
+    return out
+
+
+def densify(params: dict, moments: dict, grad_accum, elev_accum, grad_count, cfg, extent: float, seed: int,
+            portable: bool = True):
+    """densify_and_prune<float, Portable|Std>(cloud, state, cfg, extent, std::mt19937(seed)).
+
+    params / moments: dicts of [w][n] arrays (see PARAM_WIDTHS / MOMENT_WIDTHS). cfg: (grad_threshold_min,
+    grad_threshold_max, percent_dense, opacity_prune_floor, split_scale_divisor). Returns
+    (params_out, moments_out, (cloned, split, pruned), next_draw)."""
+    n = int(np.asarray(grad_count).shape[0])
+    pf = np.concatenate([np.asarray(params[k], np.float64).reshape(-1) for k, _ in PARAM_WIDTHS])
+    mf = np.concatenate([np.asarray(moments[k], np.float64).reshape(-1) for k, _ in MOMENT_WIDTHS])
+    ga = np.ascontiguousarray(grad_accum, np.float64)
+    ea = np.ascontiguousarray(elev_accum, np.float64)
+    gc = np.ascontiguousarray(grad_count, np.int32)
+    cf = np.asarray(cfg, np.float64)
+    cap = 3 * n + 1
+    po, mo = np.zeros(14 * cap), np.zeros(28 * cap)
+    stats = np.zeros(4, np.int64)
+    nd = C.c_uint32()
+    err = C.create_string_buffer(256)
+    rc = lib().oracle_densify(int(portable), n, _dp(pf), _dp(mf), _dp(ga), _dp(ea),
+                              gc.ctypes.data_as(C.POINTER(C.c_int32)), _dp(cf), float(extent), seed, cap, _dp(po),
+                              _dp(mo), stats.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(nd), err, 256)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    m = int(stats[3])
+    return (_split(po[:14 * m], PARAM_WIDTHS, m), _split(mo[:28 * m], MOMENT_WIDTHS, m),
+            tuple(int(x) for x in stats[:3]), nd.value)
+
+
+def reset_opacity(raw_opacities, ceiling: float = 0.01, portable: bool = True):
+    """reset_opacity<float> on a copy of raw_opacities (float64 array of float values)."""
+    raw = np.array(raw_opacities, np.float64)
+    err = C.create_string_buffer(256)
+    rc = lib().oracle_reset_opacity(int(portable), raw.shape[0], _dp(raw), float(ceiling), err, 256)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    return raw
+
+
+def unit_ball(seed: int, count: int):
+    """(samples (count, 3) float32, next raw draw) of unit_ball_normal<float> from mt19937(seed)."""
+    out = np.empty((count, 3), np.float32)
+    nxt = lib().oracle_unit_ball(seed, count, out.ctypes.data_as(C.POINTER(C.c_float)))
+    return out, int(nxt)
+
+
+def dynamic_threshold(elevation: float, tmin: float = 2e-5, tmax: float = 1e-4):
+    out = C.c_double()
+    rc = lib().oracle_dynamic_threshold(elevation, tmin, tmax, C.byref(out))
+    if rc:
+        raise OracleError(rc, "dynamic_threshold: elevation outside [-pi/2, pi/2]")
+    return out.value
