@@ -188,6 +188,19 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
 // (backward.hpp:271-305), starting from the pixel's state after the entries behind
 // it; updates (t, suffix) and writes the 9 accumulators. False if it contributed
 // nothing (entry beyond the pixel's walk, or d2 > cutoff^2).
+//
+// The backward is tolerance-checked (group-relative 1e-3 vs fp64), so its arithmetic
+// is free to use FMAs, MUFU ex2 and an approximate reciprocal. The two decisions that
+// must replay the forward exactly are kept exact: d2 is computed with the forward's
+// un-fused products (same bits, so the cutoff skip matches), and when the fast
+// exponential lands within 1e-4 of the alpha clamp the exact pm_expf_blend decides
+// whether the contribution was clamped (backward.hpp:289).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, const float b, int rel, int wk,
                                             float px, float py, float cutoff2, float alpha_clamp, float d0,
                                             float d1, float d2v, float& t, float& suf0, float& suf1, float& suf2,
@@ -197,40 +210,58 @@ __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, 
   if (rel >= wk) return false;
   const float dx = px - geo.x;
   const float dy = py - geo.y;
-  const float i00 = geo.z, i01 = geo.w, i11 = att.x;
-  const float dd = i00 * dx * dx + 2.0f * i01 * dx * dy + i11 * dy * dy;
+  // geo = (cx, cy, i00, 2*i01): the forward's d2 bit for bit.
+  const float dd = __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(geo.z, dx), dx), __fmul_rn(__fmul_rn(geo.w, dx), dy)),
+                             __fmul_rn(__fmul_rn(att.x, dy), dy));
   if (!(dd <= cutoff2)) return false;
   const float op = att.y;
-  const float G = pm_expf_blend(-dd / 2.0f);
-  const float raw_alpha = op * G;
-  const float alpha = std_min(alpha_clamp, raw_alpha);
-  const float inv_om = 1.0f / (1.0f - alpha);
+  float G = __expf(-0.5f * dd);
+  float raw_alpha = op * G;
+  if (fabsf(raw_alpha - alpha_clamp) < 1e-4f) {
+    G = pm_expf_blend(-dd / 2.0f);
+    raw_alpha = op * G;
+  }
+  const float alpha = fminf(alpha_clamp, raw_alpha);
+  const float inv_om = rcp_approx(1.0f - alpha);
   const float t_here = t * inv_om;
   const float c0 = att.z, c1 = att.w, c2 = b;
   const float at = alpha * t_here;
   acc[6] = d0 * at;
   acc[7] = d1 * at;
   acc[8] = d2v * at;
-  const float v0 = c0 * t_here - suf0 * inv_om;
-  const float v1 = c1 * t_here - suf1 * inv_om;
-  const float v2 = c2 * t_here - suf2 * inv_om;
-  const float dl_dalpha = d0 * v0 + (d1 * v1 + d2v * v2);
-  suf0 += c0 * at;
-  suf1 += c1 * at;
-  suf2 += c2 * at;
+  const float v0 = fmaf(-suf0, inv_om, c0 * t_here);
+  const float v1 = fmaf(-suf1, inv_om, c1 * t_here);
+  const float v2 = fmaf(-suf2, inv_om, c2 * t_here);
+  const float dl_dalpha = fmaf(d0, v0, fmaf(d1, v1, d2v * v2));
+  suf0 = fmaf(c0, at, suf0);
+  suf1 = fmaf(c1, at, suf1);
+  suf2 = fmaf(c2, at, suf2);
   t = t_here;
   if (!(raw_alpha > alpha_clamp)) {  // clamped: no alpha gradient (backward.hpp:289)
     acc[5] = dl_dalpha * G;
-    const float dl_dd2 = dl_dalpha * op * (-G / 2.0f);
-    const float gx = i00 * dx + i01 * dy;
-    const float gy = i01 * dx + i11 * dy;
-    acc[0] = dl_dd2 * (-2.0f) * gx;
-    acc[1] = dl_dd2 * (-2.0f) * gy;
-    acc[2] = dl_dd2 * dx * dx;
-    acc[3] = dl_dd2 * dx * dy;
-    acc[4] = dl_dd2 * dy * dy;
+    const float dl_dd2 = dl_dalpha * raw_alpha * -0.5f;  // dl_dalpha * op * (-G / 2)
+    const float i01 = 0.5f * geo.w;
+    const float gx = fmaf(geo.z, dx, i01 * dy);
+    const float gy = fmaf(i01, dx, att.x * dy);
+    const float m2 = -2.0f * dl_dd2;
+    acc[0] = m2 * gx;
+    acc[1] = m2 * gy;
+    const float ex = dl_dd2 * dx, ey = dl_dd2 * dy;
+    acc[2] = ex * dx;
+    acc[3] = ex * dy;
+    acc[4] = ey * dy;
   }
   return true;
+}
+
+// First butterfly level of a pair reduce-scatter: lanes 0-15 keep the sum of A over
+// lanes {l, l^16}, lanes 16-31 the sum of B.
+__device__ __forceinline__ void pair_level16(const float A[kRec], const float B[kRec], bool upper, float K[kRec]) {
+#pragma unroll
+  for (int c = 0; c < kRec; ++c) {
+    const float r = __shfl_xor_sync(0xffffffffu, upper ? A[c] : B[c], 16);
+    K[c] = (upper ? B[c] : A[c]) + r;
+  }
 }
 
 // Culled variant for tiles up to 16x16 (one pixel per thread): the forward's
@@ -239,20 +270,20 @@ __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, 
 // keep their zero record (the buffer is cleared before the launch). Skipping is
 // exact: a culled entry has computed d2 > cutoff^2 at every pixel of the warp, so
 // its contribution there is zero and it does not change t or the suffix.
-__global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
+__global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float cutoff2, float* __restrict__ records, int band_ty0, int band_ty1) {
-  __shared__ float4 s_geo[kBwdBatch];   // cx, cy, i00, i01
+  __shared__ float4 s_geo[kBwdBatch];   // cx, cy, i00, 2*i01
   __shared__ float4 s_att[kBwdBatch];   // i11, opacity, r, g
   __shared__ float s_b[kBwdBatch];
-  __shared__ uint32_t s_pos[kBwdBatch];
-  __shared__ uint8_t s_mask[kBwdBatch];
+  __shared__ uint32_t s_pos[2][kBwdBatch];  // double-buffered: read one batch later
+  __shared__ uint8_t s_mask[2][kBwdBatch];
   __shared__ uint8_t s_list[kBwdWarps][kBwdBatch];
-  __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];  // 9 sums per (warp, entry)
-  __shared__ uint8_t s_wrote[kBwdWarps][kBwdBatch];
+  __shared__ float s_part[kBwdWarps][kRec][kBwdBatch];  // 9 sums per (warp, entry), component-major
+  __shared__ int s_wrote[kBwdWarps][kBwdBatch];  // batch tag (its `hi`) of the last write
   __shared__ int s_maxw[kBwdWarps];
   __shared__ float4 s_wbox[kBwdWarps];
 
@@ -311,117 +342,172 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster_cull(
   int max_walked = 0;
   for (int w = 0; w < kBwdWarps; ++w) max_walked = max(max_walked, s_maxw[w]);
 
-  for (int hi = max_walked; hi > 0; hi -= kBwdBatch) {
-    const int lo = max(0, hi - kBwdBatch);
-    const int count = hi - lo;
+  for (int i = tid; i < kBwdWarps * kBwdBatch; i += kBwdThreads) (&s_wrote[0][0])[i] = 0;
+
+  // Batches of kBwdBatch entries, back to front. Per batch two barriers:
+  //   phase A  threads 0-127 stage batch b (entry data, warp masks, emit positions);
+  //            threads 128-255 sum batch b-1's per-warp partials in warp order and
+  //            write its records
+  //   -- barrier --
+  //   phase B  every warp compacts its entries of batch b and walks them
+  //   -- barrier --
+  // A final phase A writes the last batch.
+  int prev_hi = 0, prev_count = 0, buf = 0;
+  for (int hi = max_walked;; hi -= kBwdBatch) {
+    const bool have = hi > 0;
+    const int lo = have ? max(0, hi - kBwdBatch) : 0;
+    const int count = have ? hi - lo : 0;
     if (tid < kBwdBatch) {
-      uint32_t mask = 0;
-      if (tid < count) {
-        const int e = e0 + lo + tid;
-        const uint32_t v = vals[e];
-        const uint32_t g = v >> 2;
-        const int k = (int)(v & 3u);
-        const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
-        const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
-        const float4 c = __ldg(sp_c + g);
-        const float cx = a.x + shift_of(k, width), cy = a.y;
-        s_geo[tid] = make_float4(cx, cy, a.z, a.w);
-        s_att[tid] = b;
-        s_b[tid] = c.x;
-        float ex, ey;
-        if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
+      if (have) {
+        uint32_t mask = 0;
+        if (tid < count) {
+          const int e = e0 + lo + tid;
+          const uint32_t v = vals[e];
+          const uint32_t g = v >> 2;
+          const int k = (int)(v & 3u);
+          const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+          const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+          const float4 c = __ldg(sp_c + g);
+          const float cx = a.x + shift_of(k, width), cy = a.y;
+          s_geo[tid] = make_float4(cx, cy, a.z, 2.0f * a.w);
+          s_att[tid] = b;
+          s_b[tid] = c.x;
+          float ex, ey;
+          if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
 #pragma unroll
-          for (int w = 0; w < kBwdWarps; ++w) {
-            const float4 bx = s_wbox[w];
-            const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
-            mask |= out ? 0u : (1u << w);
+            for (int w = 0; w < kBwdWarps; ++w) {
+              const float4 bx = s_wbox[w];
+              const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
+              mask |= out ? 0u : (1u << w);
+            }
+          } else {
+            mask = 0xFFu;
           }
-        } else {
-          mask = 0xFFu;
+          if (mask) {
+            // Emit position of (tile, g, k): first entry of g + earlier shifts' areas +
+            // row-major offset inside this shift's (band-clipped) tile rectangle.
+            uint32_t pos = __ldg(ent_off_idx + g);
+            for (int kk = 0; kk <= k; ++kk) {
+              int span[4];
+              if (!band_tiles(a.x, a.y, c.z, kk, width, height, tile_size, band_ty0, band_ty1, span)) continue;
+              const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
+              if (kk < k) pos += w * (uint32_t)(span[3] - span[2] + 1);
+              else pos += (uint32_t)(ty - span[2]) * w + (uint32_t)(tx - span[0]);
+            }
+            s_pos[buf][tid] = pos;
+          }
         }
-        if (mask) {
-          // Emit position of (tile, g, k): first entry of g + earlier shifts' areas +
-          // row-major offset inside this shift's (band-clipped) tile rectangle.
-          uint32_t pos = __ldg(ent_off_idx + g);
-          for (int kk = 0; kk <= k; ++kk) {
-            int span[4];
-            if (!band_tiles(a.x, a.y, c.z, kk, width, height, tile_size, band_ty0, band_ty1, span)) continue;
-            const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
-            if (kk < k) pos += w * (uint32_t)(span[3] - span[2] + 1);
-            else pos += (uint32_t)(ty - span[2]) * w + (uint32_t)(tx - span[0]);
+        s_mask[buf][tid] = (uint8_t)mask;
+      }
+    } else if (prev_count > 0) {
+      const int j = tid - kBwdBatch;
+      if (j < prev_count && s_mask[buf ^ 1][j]) {
+        float sum[kRec];
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) sum[c] = 0.0f;
+        bool any_w = false;
+#pragma unroll
+        for (int w = 0; w < kBwdWarps; ++w)
+          if (s_wrote[w][j] == prev_hi) {
+            any_w = true;
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) sum[c] += s_part[w][c][j];
           }
-          s_pos[tid] = pos;
+        if (any_w) {
+          float* r = records + (int64_t)s_pos[buf ^ 1][j] * kRec;
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) r[c] = sum[c];
         }
       }
-      s_mask[tid] = (uint8_t)mask;
     }
-    reinterpret_cast<uint32_t*>(&s_wrote[0][0])[tid] = 0u;  // 8 x 128 bytes = 256 words
+    if (!have) break;
     __syncthreads();
     int n_list = 0;
 #pragma unroll
     for (int cidx = 0; cidx < kBwdBatch / 32; ++cidx) {
-      const bool mine = (s_mask[cidx * 32 + lane] >> warp) & 1u;
+      const bool mine = (s_mask[buf][cidx * 32 + lane] >> warp) & 1u;
       const uint32_t bal = __ballot_sync(0xffffffffu, mine);
       if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(cidx * 32 + lane);
       n_list += __popc(bal);
     }
     __syncwarp();
-    // Back to front over this warp's entries, two at a time: both entries' 9
-    // per-pixel contributions are computed (in order), then one butterfly level
-    // splits them across the half-warps (lanes 0-15 keep the first, 16-31 the second)
-    // and four more levels finish both sums — 45 shuffles for 2 entries instead of 90.
-    const bool upper = lane & 16;
-    for (int qi = n_list - 1; qi >= 0; qi -= 2) {
+    // Back to front over this warp's entries, four at a time: the 4 x 9 per-pixel
+    // contributions are reduce-scattered over the warp (level 16 splits A|B and C|D,
+    // level 8 splits AB|CD, levels 4-2-1 finish) — 54 shuffles per 4 entries. The
+    // totals land on lanes 0 (A), 8 (C), 16 (B) and 24 (D).
+    const bool upper = lane & 16, mid = lane & 8;
+    for (int qi = n_list - 1; qi >= 0; qi -= 4) {
       const int ja = s_list[warp][qi];
-      const bool has_b = qi >= 1;
-      const int jb = has_b ? s_list[warp][qi - 1] : ja;
-      float A[kRec], B[kRec];
-      const bool any_a = bwd_contrib(s_geo[ja], s_att[ja], s_b[ja], lo + ja, wk, px, py, cutoff2, alpha_clamp, d0, d1,
-                                     d2v, t, suf0, suf1, suf2, A);
-      bool any_b = false;
-      if (has_b)
-        any_b = bwd_contrib(s_geo[jb], s_att[jb], s_b[jb], lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
-                            t, suf0, suf1, suf2, B);
-      else {
+      const int jb = qi >= 1 ? s_list[warp][qi - 1] : -1;
+      const int jc = qi >= 2 ? s_list[warp][qi - 2] : -1;
+      const int jd = qi >= 3 ? s_list[warp][qi - 3] : -1;
+      float K1[kRec], K2[kRec];
+      unsigned ma, mb, mc, md;
+      {
+        float A[kRec], B[kRec];
+        const bool any_a = bwd_contrib(s_geo[ja], s_att[ja], s_b[ja], lo + ja, wk, px, py, cutoff2, alpha_clamp, d0,
+                                       d1, d2v, t, suf0, suf1, suf2, A);
+        bool any_b = false;
+        if (jb >= 0)
+          any_b = bwd_contrib(s_geo[jb], s_att[jb], s_b[jb], lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+                              t, suf0, suf1, suf2, B);
+        else
 #pragma unroll
-        for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
+          for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
+        ma = __ballot_sync(0xffffffffu, any_a);
+        mb = __ballot_sync(0xffffffffu, any_b);
+        if (ma | mb) pair_level16(A, B, upper, K1);
+        else
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) K1[c] = 0.0f;
       }
-      const unsigned ma = __ballot_sync(0xffffffffu, any_a), mb = __ballot_sync(0xffffffffu, any_b);
-      if (ma | mb) {
-        float K[kRec];
+      {
+        float C[kRec], D[kRec];
+        bool any_c = false, any_d = false;
+        if (jc >= 0)
+          any_c = bwd_contrib(s_geo[jc], s_att[jc], s_b[jc], lo + jc, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+                              t, suf0, suf1, suf2, C);
+        else
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) C[c] = 0.0f;
+        if (jd >= 0)
+          any_d = bwd_contrib(s_geo[jd], s_att[jd], s_b[jd], lo + jd, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+                              t, suf0, suf1, suf2, D);
+        else
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) D[c] = 0.0f;
+        mc = __ballot_sync(0xffffffffu, any_c);
+        md = __ballot_sync(0xffffffffu, any_d);
+        if (mc | md) pair_level16(C, D, upper, K2);
+        else
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) K2[c] = 0.0f;
+      }
+      if (ma | mb | mc | md) {
+        float L[kRec];
 #pragma unroll
         for (int c = 0; c < kRec; ++c) {
-          const float r = __shfl_xor_sync(0xffffffffu, upper ? A[c] : B[c], 16);
-          K[c] = (upper ? B[c] : A[c]) + r;
+          const float r = __shfl_xor_sync(0xffffffffu, mid ? K1[c] : K2[c], 8);
+          L[c] = (mid ? K2[c] : K1[c]) + r;
         }
 #pragma unroll
-        for (int d = 8; d > 0; d >>= 1)
+        for (int d = 4; d > 0; d >>= 1)
 #pragma unroll
-          for (int c = 0; c < kRec; ++c) K[c] += __shfl_xor_sync(0xffffffffu, K[c], d);
-        const bool write = (lane == 0 && ma) || (lane == 16 && mb);
-        if (write) {
-          const int j = upper ? jb : ja;
+          for (int c = 0; c < kRec; ++c) L[c] += __shfl_xor_sync(0xffffffffu, L[c], d);
+        const int grp = lane >> 3;  // 0: A, 1: C, 2: B, 3: D
+        const unsigned mine = grp == 0 ? ma : (grp == 1 ? mc : (grp == 2 ? mb : md));
+        if ((lane & 7) == 0 && mine) {
+          const int j = grp == 0 ? ja : (grp == 1 ? jc : (grp == 2 ? jb : jd));
 #pragma unroll
-          for (int c = 0; c < kRec; ++c) s_part[warp][j][c] = K[c];
-          s_wrote[warp][j] = 1;
+          for (int c = 0; c < kRec; ++c) s_part[warp][c][j] = L[c];
+          s_wrote[warp][j] = hi;
         }
       }
     }
     __syncthreads();
-    for (int idx = tid; idx < count * kRec; idx += kBwdThreads) {
-      const int j = idx / kRec, c = idx - j * kRec;
-      if (!s_mask[j]) continue;
-      float sum = 0.0f;
-      bool any_w = false;
-#pragma unroll
-      for (int w = 0; w < kBwdWarps; ++w)
-        if (s_wrote[w][j]) {
-          sum += s_part[w][j][c];
-          any_w = true;
-        }
-      if (any_w) records[(int64_t)s_pos[j] * kRec + c] = sum;
-    }
-    __syncthreads();
+    prev_hi = hi;
+    prev_count = count;
+    buf ^= 1;
   }
 }
 
