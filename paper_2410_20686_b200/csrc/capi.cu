@@ -70,7 +70,7 @@ struct odgs_frame {
   int32_t row_begin = 0, row_end = 0;
   bool prepared = false, rendered = false, have_splat_grads = false;
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
-  DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, splat_grads, work;
+  DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, touched, folded, splat_grads, work;
   int depth_which = 0, tile_which = 0;
   DevCamera cam{};
   DevSettings settings{};
@@ -638,7 +638,7 @@ void odgs_frame_destroy(odgs_frame* f) {
   DevBuf* bufs[] = {&f->sp_ab, &f->sp_c, &f->cov, &f->keys[0], &f->keys[1], &f->vals[0], &f->vals[1], &f->cnt,
                     &f->cnt_sorted, &f->off_sorted, &f->ent_off_idx, &f->sort_tmp, &f->scan_tmp, &f->ekeys[0],
                     &f->ekeys[1], &f->evals[0], &f->evals[1], &f->offsets, &f->image, &f->trans, &f->walked,
-                    &f->records, &f->splat_grads, &f->work};
+                    &f->records, &f->touched, &f->folded, &f->splat_grads, &f->work};
   for (DevBuf* b : bufs) release(*b, s);
   cudaStreamSynchronize(s);
   delete f;
@@ -903,8 +903,10 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     gobs = gobs ? reinterpret_cast<int32_t*>(dst[7]) : nullptr;
   }
   ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
+  ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
+  ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
   StageScope* bwd_scope = new StageScope(ctx, ODGS_STAGE_BWD_RASTER);
-  if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->records.p, 0, sizeof(float) * 9 * (size_t)K, s));
+  if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, (size_t)K, s));
   const bool keep_sg = (f->flags & ODGS_FRAME_KEEP_SPLAT_GRADS) != 0;
   if (keep_sg) ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
   if ((st = reset_errors(ctx)) != ODGS_OK) return st;
@@ -928,6 +930,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   ra.alpha_clamp = f->settings.alpha_clamp;
   ra.cutoff_sigma = f->settings.cutoff_sigma;
   ra.records = f->records.as<float>();
+  ra.touched = f->touched.as<uint8_t>();
   ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
   launch_bwd_raster(ra, s);
   delete bwd_scope;
@@ -946,8 +949,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.sp_ab = f->sp_ab.as<float4>();
   sa.sp_c = f->sp_c.as<float4>();
   sa.cnt = f->cnt.as<uint32_t>();
-  sa.ent_off_idx = f->ent_off_idx.as<uint32_t>();
-  sa.records = f->records.as<float>();
+  sa.folded = f->folded.as<float>();
   sa.signs = signs;
   sa.accumulate = (flags & ODGS_ACCUMULATE) ? 1 : 0;
   sa.g_means = gm;
@@ -962,6 +964,9 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.err = ctx->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
+    launch_fold_records(n, f->vals[f->depth_which].as<uint32_t>(), f->cnt_sorted.as<uint32_t>(),
+                        f->off_sorted.as<uint32_t>(), f->touched.as<uint8_t>(), f->records.as<float>(),
+                        f->folded.as<float>(), s);
     launch_bwd_splat(sa, s);
   }
   ODGS_CUDA(ctx, cudaGetLastError());

@@ -148,10 +148,18 @@ struct BwdRasterArgs {
   const float* dl_dimage;
   int width, height, tile_size, tiles_x, tiles_y, band_ty0, band_ty1;
   float alpha_clamp, cutoff_sigma;
-  float* records;  // [K][9] per tile entry, at the entry's emit position
-  bool plain;      // un-culled reference kernel (A/B checks)
+  float* records;    // [K][9] per tile entry, at the entry's emit position
+  uint8_t* touched;  // [K] 1 where a record was written (cleared before the launch)
+  bool plain;        // un-culled reference kernel (A/B checks)
 };
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
+
+// Ordered per-Gaussian fold of the entry records (backward.hpp:310-327), one thread per
+// depth rank so a warp reads one contiguous record range: folded[g][9] for every
+// Gaussian with entries.
+void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
+                         const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
+                         cudaStream_t stream);
 
 struct BwdSplatArgs {
   int64_t n;
@@ -162,8 +170,8 @@ struct BwdSplatArgs {
   DevCamera cam;
   DevSettings settings;
   const float4 *sp_ab, *sp_c;
-  const uint32_t *cnt, *ent_off_idx;
-  const float* records;
+  const uint32_t* cnt;
+  const float* folded;  // [n][9] folded records (launch_fold_records), read where cnt > 0
   const float* signs;  // [12] GradTSigns
   int accumulate;
   float *g_means, *g_rotations, *g_log_scales, *g_raw_opacities, *g_colors, *g_pixel_grad_norm, *g_one_minus_cos;

@@ -7,7 +7,9 @@
 //                 summed over the tile's pixels in a fixed order (pixel -> warp xor tree
 //                 -> warps in index order) and written to the entry's EMIT position, so
 //                 every Gaussian's records are contiguous. Deterministic, no atomics.
-//   k_bwd_splat   one thread per Gaussian: ordered fold of its records (:310-327),
+//   k_fold_records one thread per depth rank: ordered fold of a Gaussian's records
+//                 (:310-327) into folded[g][9].
+//   k_bwd_splat   one thread per Gaussian: its folded records,
 //                 Sigma_2D transport (:329-337), then the per-splat chain rule
 //                 (:393-438) incl. the densify statistics, plus the error checks
 //                 (pole axis :79-80, non-finite gradient :440-446).
@@ -27,7 +29,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
-    float cutoff2, float* __restrict__ records, int band_ty0, int band_ty1) {
+    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1) {
   __shared__ float s_cx[kBwdBatch], s_cy[kBwdBatch], s_i00[kBwdBatch], s_i01[kBwdBatch], s_i11[kBwdBatch],
       s_op[kBwdBatch], s_col[3][kBwdBatch];
   __shared__ uint32_t s_pos[kBwdBatch];
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
 #pragma unroll
       for (int w = 0; w < kBwdWarps; ++w) s += s_part[w][j][c];
       records[(int64_t)s_pos[j] * kRec + c] = s;
+      if (c == 0) touched[s_pos[j]] = 1;
     }
     __syncthreads();
   }
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
-    float cutoff2, float* __restrict__ records, int band_ty0, int band_ty1) {
+    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1) {
   __shared__ float4 s_geo[kBwdBatch];   // cx, cy, i00, 2*i01
   __shared__ float4 s_att[kBwdBatch];   // i11, opacity, r, g
   __shared__ float s_b[kBwdBatch];
@@ -373,15 +376,19 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
           s_att[tid] = b;
           s_b[tid] = c.x;
           float ex, ey;
+          // Warps whose longest walk ends before this entry never replay it.
+          const int rel = lo + tid;
           if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
 #pragma unroll
             for (int w = 0; w < kBwdWarps; ++w) {
               const float4 bx = s_wbox[w];
-              const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
+              const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey) ||
+                               rel >= s_maxw[w];
               mask |= out ? 0u : (1u << w);
             }
           } else {
-            mask = 0xFFu;
+#pragma unroll
+            for (int w = 0; w < kBwdWarps; ++w) mask |= rel < s_maxw[w] ? (1u << w) : 0u;
           }
           if (mask) {
             // Emit position of (tile, g, k): first entry of g + earlier shifts' areas +
@@ -414,9 +421,11 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
             for (int c = 0; c < kRec; ++c) sum[c] += s_part[w][c][j];
           }
         if (any_w) {
-          float* r = records + (int64_t)s_pos[buf ^ 1][j] * kRec;
+          const uint32_t pos = s_pos[buf ^ 1][j];
+          float* r = records + (int64_t)pos * kRec;
 #pragma unroll
           for (int c = 0; c < kRec; ++c) r[c] = sum[c];
+          touched[pos] = 1;
         }
       }
     }
@@ -520,14 +529,14 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
     k_bwd_raster_cull<<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
                                                            a.transmittance, a.walked, a.dl_dimage, a.width,
                                                            a.height, a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2,
-                                                           a.records, a.band_ty0, a.band_ty1);
+                                                           a.records, a.touched, a.band_ty0, a.band_ty1);
     ++g_launches;
     return;
   }
 #define ODGS_BWD(PPT)                                                                                             \
   k_bwd_raster<PPT><<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,       \
                                                          a.transmittance, a.walked, a.dl_dimage, a.width, a.height, \
-                                                         a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2, a.records, \
+                                                         a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2, a.records, a.touched, \
                                                          a.band_ty0, a.band_ty1)
   if (area <= kBwdThreads) ODGS_BWD(1);
   else if (area <= 4 * kBwdThreads) ODGS_BWD(4);
@@ -571,13 +580,11 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
   int observed = 0;
   if (flags & kFlagVisible) {
     observed = 1;
-    // Ordered fold of this Gaussian's entry records (contiguous, emit order).
+    // This Gaussian's folded entry records (k_fold_records).
     float r[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const uint32_t off = a.ent_off_idx[i], cnt = a.cnt[i];
-    for (uint32_t e = 0; e < cnt; ++e) {
-      const float* rec = a.records + (int64_t)(off + e) * kRec;
+    if (a.cnt[i] > 0) {
 #pragma unroll
-      for (int c = 0; c < kRec; ++c) r[c] += rec[c];
+      for (int c = 0; c < kRec; ++c) r[c] = a.folded[i * kRec + c];
     }
     const float4 ab0 = a.sp_ab[2 * i], ab1 = a.sp_ab[2 * i + 1];
     const float inv[2][2] = {{ab0.z, ab0.w}, {ab0.w, ab1.x}};
@@ -789,6 +796,42 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
     if (a.g_one_minus_cos) a.g_one_minus_cos[i] = omc;
     if (a.g_observed) a.g_observed[i] = observed;
   }
+}
+
+// ------------------------------------------------------------------ ordered fold
+// Thread r folds the records of the depth-rank-r Gaussian in emit order (the
+// reference's tile-entry order per splat, backward.hpp:310-327); records no warp
+// wrote (touched == 0) are zero and skipped. Consecutive ranks own consecutive
+// record ranges, so a warp streams one contiguous region.
+__global__ void __launch_bounds__(256) k_fold_records(int64_t n, const uint32_t* __restrict__ sorted_idx,
+                                                      const uint32_t* __restrict__ cnt_sorted,
+                                                      const uint32_t* __restrict__ off_sorted,
+                                                      const uint8_t* __restrict__ touched,
+                                                      const float* __restrict__ records, float* __restrict__ folded) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t cnt = cnt_sorted[r];
+  if (cnt == 0) return;
+  const uint32_t off = off_sorted[r];
+  float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (uint32_t e = 0; e < cnt; ++e) {
+    if (!touched[off + e]) continue;
+    const float* rec = records + (int64_t)(off + e) * kRec;
+#pragma unroll
+    for (int c = 0; c < kRec; ++c) acc[c] += rec[c];
+  }
+  float* o = folded + (int64_t)sorted_idx[r] * kRec;
+#pragma unroll
+  for (int c = 0; c < kRec; ++c) o[c] = acc[c];
+}
+
+void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
+                         const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
+                         cudaStream_t stream) {
+  if (n == 0) return;
+  k_fold_records<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, sorted_idx, cnt_sorted, off_sorted, touched,
+                                                                  records, folded);
+  ++g_launches;
 }
 
 void launch_bwd_splat(const BwdSplatArgs& a, cudaStream_t stream) {
