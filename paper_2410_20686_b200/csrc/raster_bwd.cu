@@ -569,7 +569,7 @@ __device__ __forceinline__ M23 jacobian_factored_fast(float phi, float theta, fl
   return j;
 }
 
-__global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
+__global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = a.n;
   if (i >= n) return;
@@ -799,27 +799,63 @@ __global__ void __launch_bounds__(256) k_bwd_splat(BwdSplatArgs a) {
 }
 
 // ------------------------------------------------------------------ ordered fold
-// Thread r folds the records of the depth-rank-r Gaussian in emit order (the
+// Lane l of a warp folds the records of depth rank r0 + l in emit order (the
 // reference's tile-entry order per splat, backward.hpp:310-327); records no warp
-// wrote (touched == 0) are zero and skipped. Consecutive ranks own consecutive
-// record ranges, so a warp streams one contiguous region.
-__global__ void __launch_bounds__(256) k_fold_records(int64_t n, const uint32_t* __restrict__ sorted_idx,
-                                                      const uint32_t* __restrict__ cnt_sorted,
-                                                      const uint32_t* __restrict__ off_sorted,
-                                                      const uint8_t* __restrict__ touched,
-                                                      const float* __restrict__ records, float* __restrict__ folded) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  const uint32_t cnt = cnt_sorted[r];
-  if (cnt == 0) return;
-  const uint32_t off = off_sorted[r];
+// wrote (touched == 0) are zero and skipped. The 32 ranks own one contiguous record
+// range, which the warp streams through shared memory in coalesced chunks of
+// kFoldChunk records; each lane then adds the part of its own range inside the chunk,
+// in order.
+constexpr int kFoldWarps = 8;
+constexpr int kFoldChunk = 128;
+
+__global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
+    int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
+    const uint32_t* __restrict__ off_sorted, const uint8_t* __restrict__ touched, const float* __restrict__ records,
+    float* __restrict__ folded) {
+  __shared__ float s_rec[kFoldWarps][kFoldChunk * kRec];
+  __shared__ uint8_t s_touch[kFoldWarps][kFoldChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = ((int64_t)blockIdx.x * kFoldWarps + warp) * 32;
+  if (r0 >= n) return;
+  const int64_t r = r0 + lane;
+  const uint32_t cnt = r < n ? cnt_sorted[r] : 0u;
+  const uint32_t off = r < n ? off_sorted[r] : 0u;
+  // The warp's range: from its first rank's offset to the end of its last rank's.
+  const uint32_t beg = __shfl_sync(0xffffffffu, off, 0);
+  const int last = n - r0 >= 32 ? 31 : (int)(n - 1 - r0);
+  const uint32_t end = __shfl_sync(0xffffffffu, off + cnt, last);
   float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (uint32_t e = 0; e < cnt; ++e) {
-    if (!touched[off + e]) continue;
-    const float* rec = records + (int64_t)(off + e) * kRec;
+  for (uint32_t c0 = beg; c0 < end; c0 += kFoldChunk) {
+    const uint32_t m = min((uint32_t)kFoldChunk, end - c0);
+    __syncwarp();
+    for (uint32_t k = lane; k < m; k += 32) s_touch[warp][k] = touched[c0 + k];
+    __syncwarp();
+    // Only written records are read (untouched ones hold stale data).
+    const float* src = records + (int64_t)c0 * kRec;
+    const uint32_t mf = m * kRec;
+    for (uint32_t k0 = 0; k0 < mf; k0 += 32 * 12) {  // 12 loads in flight per lane
+      float v[12];
 #pragma unroll
-    for (int c = 0; c < kRec; ++c) acc[c] += rec[c];
+      for (int u = 0; u < 12; ++u) {
+        const uint32_t k = k0 + lane + 32 * u;
+        v[u] = (k < mf && s_touch[warp][k / kRec]) ? __ldcs(src + k) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const uint32_t k = k0 + lane + 32 * u;
+        if (k < mf) s_rec[warp][k] = v[u];
+      }
+    }
+    __syncwarp();
+    const uint32_t lo = max(off, c0), hi = min(off + cnt, c0 + m);
+    for (uint32_t e = lo; e < hi; ++e) {
+      if (!s_touch[warp][e - c0]) continue;
+      const float* rec = &s_rec[warp][(e - c0) * kRec];
+#pragma unroll
+      for (int c = 0; c < kRec; ++c) acc[c] += rec[c];
+    }
   }
+  if (cnt == 0) return;
   float* o = folded + (int64_t)sorted_idx[r] * kRec;
 #pragma unroll
   for (int c = 0; c < kRec; ++c) o[c] = acc[c];
@@ -829,8 +865,9 @@ void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* 
                          const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
                          cudaStream_t stream) {
   if (n == 0) return;
-  k_fold_records<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, sorted_idx, cnt_sorted, off_sorted, touched,
-                                                                  records, folded);
+  const int64_t warps = (n + 31) / 32;
+  k_fold_records<<<(unsigned)((warps + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, stream>>>(
+      n, sorted_idx, cnt_sorted, off_sorted, touched, records, folded);
   ++g_launches;
 }
 
