@@ -330,6 +330,53 @@ odgs_status odgs_reset_opacity(odgs_ctx* ctx, const odgs_params* cloud, const od
 /* dynamic_threshold (densify.hpp:39-49), binary64 host helper. */
 odgs_status odgs_dynamic_threshold(double elevation, const odgs_densify_config* cfg, double* out);
 
+/* ------------------------------------------------------------------ scene I/O
+   (reference io.hpp / src/io.cpp). Host code: polygon (.ply)
+   point clouds and checkpoints in the reference's exact formats. Every array is the
+   reference's Eigen column-major storage in binary64 (GaussianCloud<double>,
+   PointCloud): positions/means/colors [3][n], rotations (w,x,y,z) [4][n], log_scales
+   [3][n], raw_opacities [n]. Failures return ODGS_ERR_RUNTIME (std::runtime_error in
+   the reference) with the reference's message ("<path>: <what> (byte N)"), read with
+   odgs_io_last_error() (per host thread). */
+
+/* GaussianCloud<double> (types.hpp:53-143), host or device arrays. */
+typedef struct {
+  int64_t n;
+  double* means;
+  double* rotations;
+  double* log_scales;
+  double* raw_opacities;
+  double* colors;
+} odgs_cloud64;
+
+/* Message of the last failed odgs_ply / checkpoint call on this thread. */
+size_t odgs_io_last_error(char* message, size_t message_len);
+/* Vertex count declared by a polygon file's header (parse_ply_header, io.cpp:41-118). */
+odgs_status odgs_ply_vertex_count(const char* path, int64_t* n);
+/* load_pointcloud (io.cpp:203-223): needs x, y, z, red, green, blue; uchar colours
+   are scaled by 1/255. n must be the file's vertex count (odgs_ply_vertex_count). */
+odgs_status odgs_load_pointcloud(const char* path, int64_t n, double* positions, double* colors);
+/* save_pointcloud (io.cpp:225-257): float positions, uchar colours (round(clamp*255)). */
+odgs_status odgs_save_pointcloud(const char* path, int64_t n, const double* positions, const double* colors,
+                                 int32_t binary);
+/* save_checkpoint (io.cpp:299-332): float32 x,y,z, f_dc_0..2 (= (c - 0.5) / C0, flushed
+   below 2^-27), opacity, scale_0..2, rot_0..3, with the version comment. */
+odgs_status odgs_save_checkpoint(const char* path, const odgs_cloud64* cloud);
+/* load_checkpoint (io.cpp:334-362): rejects newer versions and missing properties.
+   cloud->n must be the file's vertex count; all five arrays are written. */
+odgs_status odgs_load_checkpoint(const char* path, const odgs_cloud64* cloud);
+
+/* init_from_points (io.cpp:259-297) on the GPU: means = positions, colours copied,
+   identity rotations, raw opacity logit(0.1), isotropic log-scale = log of the mean
+   distance to the (up to) three nearest neighbours, floored at 1e-7 (0.1 for a point
+   with no finite neighbour distance). Exact 3-NN through a uniform grid: the mean
+   distances equal the reference's brute force bit for bit (nn_scale, optional [n],
+   receives them before the log). positions/colors and every output array live in
+   `memory`. Errors: ODGS_ERR_INVALID_ARGUMENT for n < 1 ("init_from_points: no
+   points"). */
+odgs_status odgs_init_from_points(odgs_ctx* ctx, int64_t n, const double* positions, const double* colors,
+                                  int32_t memory, const odgs_cloud64* out, double* nn_scale);
+
 /* cull (rasterizer.hpp:15-28): host output of the kept rows, ascending. */
 odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera, float near_radius,
                       float far_radius, int64_t* out_indices, int64_t* out_count);

@@ -27,6 +27,7 @@
 #pragma once
 
 #include <algorithm>
+#include <limits>
 #include <array>
 #include <cmath>
 #include <cstdint>
@@ -1447,6 +1448,37 @@ template <class S> Camera<S> yawed_camera(const Camera<S>& base, S angle) {  // 
   out.rotation = mul(yaw, base.rotation);
   out.translation = mulv(yaw, base.translation);
   return out;
+}
+
+// init_from_points' neighbour scale (io.cpp:268-296): brute-force O(n^2) scan keeping
+// the three smallest squared distances (strict <, replace the largest, re-sort),
+// then the ascending sum of their square roots, mean, 1e-7 floor or 0.1 fallback.
+// d2 = (p_j - p_i).squaredNorm() with Eigen's unroller order x^2 + (y^2 + z^2)
+// (Appendix B of SURVEY.md). pos is [3][n] column-major; writes scale[i] and the
+// log-scale ls[i] = std::log(scale[i]).
+inline void init_scales_brute(int64_t n, const double* pos, double* scale, double* ls) {
+  for (int64_t i = 0; i < n; ++i) {
+    double best[3] = {std::numeric_limits<double>::infinity(), std::numeric_limits<double>::infinity(),
+                      std::numeric_limits<double>::infinity()};
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double dx = pos[j] - pos[i], dy = pos[n + j] - pos[n + i], dz = pos[2 * n + j] - pos[2 * n + i];
+      const double d2 = dx * dx + (dy * dy + dz * dz);
+      if (d2 < best[2]) {
+        best[2] = d2;
+        std::sort(best, best + 3);
+      }
+    }
+    double sum = 0;
+    int count = 0;
+    for (const double d2 : best)
+      if (std::isfinite(d2)) {
+        sum += std::sqrt(d2);
+        ++count;
+      }
+    scale[i] = count > 0 ? std::max(sum / count, 1e-7) : 0.1;
+    ls[i] = std::log(scale[i]);
+  }
 }
 
 }  // namespace oracle

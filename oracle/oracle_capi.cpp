@@ -387,4 +387,9 @@ int oracle_dynamic_threshold(double elevation, double tmin, double tmax, double*
 
 int oracle_hardware_concurrency() { return effective_threads(0); }
 
+// init_from_points scales (io.cpp:268-296), brute force.
+void oracle_init_scales(int64_t n, const double* pos, double* scale, double* ls) {
+  init_scales_brute(n, pos, scale, ls);
+}
+
 }  // extern "C"

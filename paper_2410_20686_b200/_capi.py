@@ -85,6 +85,11 @@ class DensifyStats(C.Structure):
     _fields_ = [("cloned", C.c_int64), ("split", C.c_int64), ("pruned", C.c_int64), ("n_out", C.c_int64)]
 
 
+class Cloud64(C.Structure):
+    _fields_ = [("n", C.c_int64), ("means", C.c_void_p), ("rotations", C.c_void_p), ("log_scales", C.c_void_p),
+                ("raw_opacities", C.c_void_p), ("colors", C.c_void_p)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("n_gaussians", C.c_int64), ("n_splats", C.c_int64),
@@ -136,6 +141,13 @@ SIGNATURES = {
                                      C.POINTER(Params), C.POINTER(TrainState)]),
     "odgs_reset_opacity": (C.c_int, [_P, C.POINTER(Params), C.POINTER(TrainState), C.c_float]),
     "odgs_dynamic_threshold": (C.c_int, [C.c_double, C.POINTER(DensifyConfig), C.POINTER(C.c_double)]),
+    "odgs_io_last_error": (C.c_size_t, [C.c_char_p, C.c_size_t]),
+    "odgs_ply_vertex_count": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64)]),
+    "odgs_load_pointcloud": (C.c_int, [C.c_char_p, C.c_int64, _P, _P]),
+    "odgs_save_pointcloud": (C.c_int, [C.c_char_p, C.c_int64, _P, _P, C.c_int32]),
+    "odgs_save_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(Cloud64)]),
+    "odgs_load_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(Cloud64)]),
+    "odgs_init_from_points": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, C.POINTER(Cloud64), _P]),
     "odgs_cull": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.c_float, C.c_float,
                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }

@@ -1148,6 +1148,152 @@ odgs_status odgs_cull(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera*
   return ok(ctx);
 }
 
+// ------------------------------------------------------------------ init_from_points
+namespace {
+
+// Grid plan: the largest cell size h whose grid has at most `target` cells
+// (dims_a = max(1, ceil(extent_a / h))), so cells hold ~2 points on average.
+KnnGrid plan_grid(const double lo[3], const double hi[3], int64_t n_finite) {
+  KnnGrid g{};
+  for (int a = 0; a < 3; ++a) g.lo[a] = lo[a];
+  double ext[3], emax = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    ext[a] = hi[a] - lo[a];
+    emax = std::max(emax, ext[a]);
+  }
+  const double target = (double)std::min<int64_t>(std::max<int64_t>(n_finite / 2, 1), (int64_t)1 << 26);
+  auto cells = [&](double h) {
+    double c = 1.0;
+    for (int a = 0; a < 3; ++a) c *= std::max(1.0, std::ceil(ext[a] / h));
+    return c;
+  };
+  if (!(emax > 0.0) || !std::isfinite(emax) || target <= 1.0) {
+    g.h = 1.0;
+    g.dims[0] = g.dims[1] = g.dims[2] = 1;
+  } else {
+    double lo_h = emax / std::cbrt(target) / 4.0, hi_h = emax;  // cells(hi_h) == 1 <= target
+    while (cells(lo_h) <= target) lo_h /= 2.0;
+    for (int it = 0; it < 64; ++it) {
+      const double mid = std::sqrt(lo_h * hi_h);
+      if (cells(mid) <= target) hi_h = mid;
+      else lo_h = mid;
+    }
+    g.h = hi_h;
+    for (int a = 0; a < 3; ++a) g.dims[a] = (int)std::max(1.0, std::ceil(ext[a] / g.h));
+  }
+  g.n_cells = (uint32_t)((uint64_t)g.dims[0] * g.dims[1] * g.dims[2]);
+  return g;
+}
+
+}  // namespace
+
+odgs_status odgs_init_from_points(odgs_ctx* ctx, int64_t n, const double* positions, const double* colors,
+                                  int32_t memory, const odgs_cloud64* out, double* nn_scale) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (n < 1) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "init_from_points: no points");
+  if (!positions || !colors || !out || !out->means || !out->rotations || !out->log_scales || !out->raw_opacities ||
+      !out->colors)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "init_from_points: null argument");
+  if (out->n != n) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "init_from_points: out->n != n");
+  if (n >= ((int64_t)1 << 32) - 1)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "init_from_points: more than 2^32 - 2 points");
+  const bool host = memory == ODGS_MEM_HOST;
+  cudaStream_t s = ctx->stream;
+  const size_t n3 = 3 * (size_t)n;
+
+  // Scratch: positions (host input), keys/indices ping-pong, sorted xyz, log-scales.
+  DevBuf pos_b, k0, k1, v0, v1, xyz_b, cells_b, part_b, ls_b, sc_b, tmp_b;
+  struct Release {
+    std::vector<DevBuf*> bufs;
+    cudaStream_t s;
+    ~Release() {
+      for (DevBuf* b : bufs) release(*b, s);
+    }
+  } rel{{&pos_b, &k0, &k1, &v0, &v1, &xyz_b, &cells_b, &part_b, &ls_b, &sc_b, &tmp_b}, s};
+  const double* dpos = positions;
+  if (host) {
+    ODGS_CUDA(ctx, ensure(pos_b, sizeof(double) * n3, s));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(pos_b.p, positions, sizeof(double) * n3, cudaMemcpyHostToDevice, s));
+    dpos = pos_b.as<double>();
+  }
+  // 1. bounding box of the finite points
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 1184);
+  ODGS_CUDA(ctx, ensure(part_b, sizeof(double) * 6 * blocks + 64, s));
+  unsigned long long* d_count = reinterpret_cast<unsigned long long*>(part_b.as<char>() + sizeof(double) * 6 * blocks);
+  ODGS_CUDA(ctx, cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+  launch_bbox_partial(n, dpos, part_b.as<double>(), blocks, d_count, s);
+  std::vector<double> part(6 * (size_t)blocks + 8);
+  ODGS_CUDA(ctx, cudaMemcpyAsync(part.data(), part_b.p, sizeof(double) * 6 * blocks + 8, cudaMemcpyDeviceToHost, s));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(s));
+  unsigned long long m_u = 0;
+  std::memcpy(&m_u, part.data() + 6 * blocks, 8);
+  const int64_t m = (int64_t)m_u;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  if (m > 0) {
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = part[a];
+      hi[a] = part[3 + a];
+      for (int b = 1; b < blocks; ++b) {
+        lo[a] = std::min(lo[a], part[6 * b + a]);
+        hi[a] = std::max(hi[a], part[6 * b + 3 + a]);
+      }
+    }
+  }
+  const KnnGrid g = plan_grid(lo, hi, m);
+
+  // 2. cell keys, stable sort by cell, positions in cell order, cell CSR
+  for (DevBuf* b : {&k0, &k1, &v0, &v1}) ODGS_CUDA(ctx, ensure(*b, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(tmp_b, std::max(radix_sort_temp_bytes(n), (size_t)16), s));
+  ODGS_CUDA(ctx, ensure(xyz_b, sizeof(double) * n3, s));
+  ODGS_CUDA(ctx, ensure(cells_b, sizeof(uint32_t) * ((size_t)g.n_cells + 1), s));
+  launch_cell_keys(n, dpos, g, k0.as<uint32_t>(), v0.as<uint32_t>(), s);
+  uint32_t* kk[2] = {k0.as<uint32_t>(), k1.as<uint32_t>()};
+  uint32_t* vv[2] = {v0.as<uint32_t>(), v1.as<uint32_t>()};
+  int which = 0;
+  radix_sort_pairs(kk, vv, n, 0, bits_for(g.n_cells + 1u), tmp_b.p, &which, s);
+  launch_gather_xyz(n, vv[which], dpos, xyz_b.as<double>(), s);
+  launch_cell_ranges(m, kk[which], g.n_cells, cells_b.as<uint32_t>(), s);
+
+  // 3. exact 3-NN and the log-scales
+  double* d_ls = out->log_scales;
+  double* d_sc = nn_scale;
+  if (host) {
+    ODGS_CUDA(ctx, ensure(ls_b, sizeof(double) * n3, s));
+    d_ls = ls_b.as<double>();
+    if (nn_scale) {
+      ODGS_CUDA(ctx, ensure(sc_b, sizeof(double) * n, s));
+      d_sc = sc_b.as<double>();
+    }
+  }
+  launch_knn_query(n, m, xyz_b.as<double>(), vv[which], cells_b.as<uint32_t>(), g, d_sc, d_ls, s);
+
+  // 4. the other fields (io.cpp:263-267): means and colours copied, identity
+  //    rotations, raw opacity logit(0.1) (types.hpp:35-39, binary64 on the host).
+  const double raw = std::log(0.1 / (1.0 - 0.1));
+  if (host) {
+    std::memcpy(out->means, positions, sizeof(double) * n3);
+    std::memcpy(out->colors, colors, sizeof(double) * n3);
+    for (int64_t i = 0; i < n; ++i) {
+      out->rotations[i] = 1.0;
+      out->raw_opacities[i] = raw;
+    }
+    std::fill(out->rotations + n, out->rotations + 4 * n, 0.0);
+    ODGS_CUDA(ctx, cudaMemcpyAsync(out->log_scales, d_ls, sizeof(double) * n3, cudaMemcpyDeviceToHost, s));
+    if (nn_scale) ODGS_CUDA(ctx, cudaMemcpyAsync(nn_scale, d_sc, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  } else {
+    ODGS_CUDA(ctx, cudaMemcpyAsync(out->means, positions, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(out->colors, colors, sizeof(double) * n3, cudaMemcpyDeviceToDevice, s));
+    launch_fill_f64(out->rotations, n, 1.0, s);
+    ODGS_CUDA(ctx, cudaMemsetAsync(out->rotations + n, 0, sizeof(double) * n3, s));
+    launch_fill_f64(out->raw_opacities, n, raw, s);
+  }
+  ODGS_CUDA(ctx, cudaStreamSynchronize(s));
+  ODGS_CUDA(ctx, cudaGetLastError());
+  return ok(ctx);
+}
+
 // ------------------------------------------------------------------ density control
 void odgs_default_densify_config(odgs_densify_config* out) {  // densify.hpp:16-24
   if (!out) return;

@@ -181,4 +181,27 @@ struct BwdSplatArgs {
 };
 void launch_bwd_splat(const BwdSplatArgs& a, cudaStream_t stream);
 
+// ------------------------------------------------------------------ init_from_points (io.cpp:259-297)
+// Uniform grid over the finite points' bounding box: cell (x, y, z) of point p is
+// floor((p - lo) / h) clamped to [0, dims); id = (z * dims[1] + y) * dims[0] + x.
+struct KnnGrid {
+  double lo[3];
+  double h;
+  int dims[3];
+  uint32_t n_cells;
+};
+void launch_fill_f64(double* p, int64_t n, double v, cudaStream_t stream);
+// partial[b][6] = (min xyz, max xyz) of block b's finite points; *n_finite += count.
+void launch_bbox_partial(int64_t n, const double* pos, double* partial, int blocks, unsigned long long* n_finite,
+                         cudaStream_t stream);
+void launch_cell_keys(int64_t n, const double* pos, const KnnGrid& g, uint32_t* keys, uint32_t* idx,
+                      cudaStream_t stream);
+void launch_gather_xyz(int64_t n, const uint32_t* idx, const double* pos, double* sorted, cudaStream_t stream);
+void launch_cell_ranges(int64_t m, const uint32_t* keys, uint32_t n_cells, uint32_t* cell_start,
+                        cudaStream_t stream);
+// n points, the first m (in cell order) finite; writes scale_out[i] (optional) and
+// log_scales[3][n] (isotropic) per original index.
+void launch_knn_query(int64_t n, int64_t m, const double* xyz, const uint32_t* idx, const uint32_t* cell_start,
+                      const KnnGrid& g, double* scale_out, double* log_scales, cudaStream_t stream);
+
 }  // namespace odgs_b200

@@ -54,8 +54,21 @@ def lib() -> C.CDLL:
         L.oracle_unit_ball.argtypes = [C.c_uint32, C.c_int64, C.POINTER(C.c_float)]
         L.oracle_dynamic_threshold.restype = C.c_int
         L.oracle_dynamic_threshold.argtypes = [C.c_double, C.c_double, C.c_double, dp]
+        L.oracle_init_scales.restype = None
+        L.oracle_init_scales.argtypes = [C.c_int64, dp, dp, dp]
         _lib = L
     return _lib
+
+
+def init_scales(positions):
+    """Brute-force init_from_points scales (io.cpp:268-296): (scale, log_scale) per point."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    n = pos.shape[1]
+    sc = np.zeros(n)
+    ls = np.zeros(n)
+    dp = C.POINTER(C.c_double)
+    lib().oracle_init_scales(n, pos.ctypes.data_as(dp), sc.ctypes.data_as(dp), ls.ctypes.data_as(dp))
+    return sc, ls
 
 
 def _dp(a: np.ndarray):
