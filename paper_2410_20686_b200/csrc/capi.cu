@@ -70,7 +70,7 @@ struct odgs_frame {
   int32_t row_begin = 0, row_end = 0;
   bool prepared = false, rendered = false, have_splat_grads = false;
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
-  DevBuf ekeys[2], evals[2], offsets, image, trans, walked, records, touched, folded, splat_grads, work;
+  DevBuf ekeys[2], evals[2], offsets, tile_order, image, trans, walked, records, touched, folded, splat_grads, work;
   int depth_which = 0, tile_which = 0;
   DevCamera cam{};
   DevSettings settings{};
@@ -427,6 +427,10 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   {
     StageScope sc(ctx, ODGS_STAGE_RANGES);
     launch_tile_ranges(K, ek[f->tile_which], n_tiles, f->offsets.as<int32_t>(), s);
+    const int band_tiles = f->tiles_x * (f->settings.band_ty1 - f->settings.band_ty0);
+    ODGS_CUDA(ctx, ensure(f->tile_order, sizeof(uint32_t) * std::max(band_tiles, 1), s));
+    launch_tile_order(f->offsets.as<int32_t>(), f->settings.band_ty0 * f->tiles_x, band_tiles,
+                      f->tile_order.as<uint32_t>(), s);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
   f->prepared = true;
@@ -460,6 +464,7 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ba.transmittance = f->trans.as<float>();
   ba.walked = f->walked.as<int32_t>();
   ba.work = f->work.as<unsigned long long>();
+  ba.order = f->tile_order.as<uint32_t>();
   ba.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
   {
     StageScope sc(ctx, ODGS_STAGE_BLEND);
@@ -637,7 +642,7 @@ void odgs_frame_destroy(odgs_frame* f) {
   cudaStream_t s = f->ctx->stream;
   DevBuf* bufs[] = {&f->sp_ab, &f->sp_c, &f->cov, &f->keys[0], &f->keys[1], &f->vals[0], &f->vals[1], &f->cnt,
                     &f->cnt_sorted, &f->off_sorted, &f->ent_off_idx, &f->sort_tmp, &f->scan_tmp, &f->ekeys[0],
-                    &f->ekeys[1], &f->evals[0], &f->evals[1], &f->offsets, &f->image, &f->trans, &f->walked,
+                    &f->ekeys[1], &f->evals[0], &f->evals[1], &f->offsets, &f->tile_order, &f->image, &f->trans, &f->walked,
                     &f->records, &f->touched, &f->folded, &f->splat_grads, &f->work};
   for (DevBuf* b : bufs) release(*b, s);
   cudaStreamSynchronize(s);
@@ -931,6 +936,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   ra.cutoff_sigma = f->settings.cutoff_sigma;
   ra.records = f->records.as<float>();
   ra.touched = f->touched.as<uint8_t>();
+  ra.order = f->tile_order.as<uint32_t>();
   ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
   launch_bwd_raster(ra, s);
   delete bwd_scope;

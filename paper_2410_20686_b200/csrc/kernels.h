@@ -58,8 +58,11 @@ struct BlendArgs {
   float* transmittance;
   int32_t* walked;
   unsigned long long* work;  // [2] += entries examined, entries composited (or null)
+  const uint32_t* order;     // launch order of the band's tiles (launch_tile_order) or null
   bool plain;                // force the un-culled reference kernel (A/B checks)
 };
+// order[k] = band-relative tile index of the k-th CTA: tiles by descending list length.
+void launch_tile_order(const int32_t* offsets, int tile_base, int n, uint32_t* order, cudaStream_t stream);
 void launch_blend(const BlendArgs& a, cudaStream_t stream);
 void launch_blend_plain(const BlendArgs& a, cudaStream_t stream);
 
@@ -150,6 +153,7 @@ struct BwdRasterArgs {
   float alpha_clamp, cutoff_sigma;
   float* records;    // [K][9] per tile entry, at the entry's emit position
   uint8_t* touched;  // [K] 1 where a record was written (cleared before the launch)
+  const uint32_t* order;  // launch order of the band's tiles or null
   bool plain;        // un-culled reference kernel (A/B checks)
 };
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);

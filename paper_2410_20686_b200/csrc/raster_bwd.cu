@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
-    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1) {
+    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1,
+    const uint32_t* __restrict__ order) {
   __shared__ float4 s_geo[kBwdBatch];   // cx, cy, i00, 2*i01
   __shared__ float4 s_att[kBwdBatch];   // i11, opacity, r, g
   __shared__ float s_b[kBwdBatch];
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
   __shared__ int s_maxw[kBwdWarps];
   __shared__ float4 s_wbox[kBwdWarps];
 
-  const int tile = band_ty0 * tiles_x + blockIdx.x;
+  const int tile = band_ty0 * tiles_x + (int)(order ? order[blockIdx.x] : blockIdx.x);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -529,7 +530,7 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
     k_bwd_raster_cull<<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
                                                            a.transmittance, a.walked, a.dl_dimage, a.width,
                                                            a.height, a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2,
-                                                           a.records, a.touched, a.band_ty0, a.band_ty1);
+                                                           a.records, a.touched, a.band_ty0, a.band_ty1, a.order);
     ++g_launches;
     return;
   }

@@ -280,6 +280,49 @@ void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_til
   ++g_launches;
 }
 
+// ------------------------------------------------------------------ tile order
+// Launch order of the per-tile kernels (blend, backward raster): tiles by descending
+// list length (quarter-octave buckets), so the few very long lists of the pole and
+// seam tiles start first instead of trailing the grid. Per-tile results do not depend
+// on the order (each CTA owns its tile), so the bucket-internal order — set by
+// shared-memory atomics — is free.
+constexpr int kOrderThreads = 1024;
+constexpr int kOrderBuckets = 128;
+
+__device__ __forceinline__ int order_bucket(int32_t len) {
+  const uint32_t v = (uint32_t)len + 1u;
+  const int b = 31 - __clz(v);                                  // floor(log2 v)
+  const int frac = b >= 2 ? (int)((v >> (b - 2)) & 3u) : (int)((v << (2 - b)) & 3u);
+  return kOrderBuckets - 1 - min(kOrderBuckets - 1, 4 * b + frac);  // longest first
+}
+
+__global__ void __launch_bounds__(kOrderThreads) k_tile_order(const int32_t* __restrict__ offsets, int tile_base,
+                                                              int n, uint32_t* __restrict__ order) {
+  __shared__ uint32_t s_cnt[kOrderBuckets];
+  for (int b = threadIdx.x; b < kOrderBuckets; b += kOrderThreads) s_cnt[b] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += kOrderThreads)
+    atomicAdd(&s_cnt[order_bucket(offsets[tile_base + t + 1] - offsets[tile_base + t])], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int b = 0; b < kOrderBuckets; ++b) {
+      const uint32_t c = s_cnt[b];
+      s_cnt[b] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += kOrderThreads)
+    order[atomicAdd(&s_cnt[order_bucket(offsets[tile_base + t + 1] - offsets[tile_base + t])], 1u)] = (uint32_t)t;
+}
+
+void launch_tile_order(const int32_t* offsets, int tile_base, int n, uint32_t* order, cudaStream_t stream) {
+  if (n <= 0) return;
+  k_tile_order<<<1, kOrderThreads, 0, stream>>>(offsets, tile_base, n, order);
+  ++g_launches;
+}
+
 // ------------------------------------------------------------------ blend
 constexpr int kBlendThreads = 256;
 
@@ -408,7 +451,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
-    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base) {
+    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base,
+    const uint32_t* __restrict__ order) {
   constexpr int kWarps = kBlendThreads / 32;
   __shared__ float4 s_geo[kBlendThreads];  // cx, cy, i00, 2*i01
   __shared__ float4 s_att[kBlendThreads];  // i11, opacity, r, g
@@ -417,7 +461,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
   __shared__ uint8_t s_list[kWarps][kBlendThreads];
   __shared__ float4 s_wbox[kWarps];  // pixel-centre bbox of each warp: xmin, xmax, ymin, ymax
 
-  const int tile = tile_base + blockIdx.x;
+  const int tile = tile_base + (int)(order ? order[blockIdx.x] : blockIdx.x);
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile], e1 = offsets[tile + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -549,7 +593,7 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
     k_blend_cull<<<n_band_tiles, kBlendThreads, 0, stream>>>(
         a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.alpha_clamp,
         a.transmittance_floor, a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work,
-        a.band_ty0 * a.tiles_x);
+        a.band_ty0 * a.tiles_x, a.order);
     ++g_launches;
     return;
   }
