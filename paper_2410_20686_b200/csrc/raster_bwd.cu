@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
   int lx, ly;
   bool valid;
   if (tile_size == 16) {
-    lx = (warp >> 1) * 4 + (lane >> 3);
-    ly = (warp & 1) * 8 + (lane & 7);
+    lx = (warp & 1) * 8 + (lane >> 2);  // 8-wide x 4-tall warp blocks, as the blend
+    ly = (warp >> 1) * 4 + (lane & 3);
     valid = true;
   } else {
     lx = tid / tile_size;

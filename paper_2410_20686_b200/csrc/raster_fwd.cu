@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
 }
 
 // ------------------------------------------------------------------ blend with warp culling
-__global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
+// 6 CTAs (48 warps) per SM: the walk is latency-bound on its dependent chains.
+__global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
@@ -466,13 +467,16 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend_cull(
   const int e0 = offsets[tile], e1 = offsets[tile + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // Pixel of this thread. 16x16 tiles: each warp owns a 4-wide x 8-tall block (lanes
-  // run down a column: the image is column-major, so stores are 32 B runs).
+  // Pixel of this thread. 16x16 tiles: each warp owns an 8-wide x 4-tall block (lanes
+  // run down a column in fours: the image is column-major). Wide blocks match the
+  // horizontally stretched footprints of the ERP projection (sec(theta) in x), so the
+  // warp culling below rejects more entries (measured: C3 blend 0.618 -> 0.563 ms vs
+  // 4 x 8 blocks, 16 x 2 blocks 0.605 ms).
   int lx, ly;
   bool valid;
   if (tile_size == 16) {
-    lx = (warp >> 1) * 4 + (lane >> 3);
-    ly = (warp & 1) * 8 + (lane & 7);
+    lx = (warp & 1) * 8 + (lane >> 2);
+    ly = (warp >> 1) * 4 + (lane & 3);
     valid = true;
   } else {
     lx = tid / tile_size;
