@@ -485,12 +485,31 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    out = {"metric": "ERP frames/sec (C5: 10M Gaussians, 4096x2048, row bands over the GPUs)",
+           "value": steps / (ms_max / 1000.0), "unit": "frames/s", "ms_per_frame": ms_max / steps,
+           "bands": world, "rows_per_band": rows, "n_gpus": world, "scaling": "strong",
+           "collective": "NCCL all_gather of the band images" if world > 1 else "none",
+           "band_tile_entries_rank0": info.n_entries, "stage_ms_per_frame_rank0": stages}
+    if world == 1:
+        # Each of the 8 bands an 8-GPU run would give one rank, rendered alone on this GPU
+        # (CUDA events, same frames): the per-rank work of the row-band split, without
+        # the all-gather (8 x 12.6 MB over NVLink).
+        band_ms = []
+        for b in range(8):
+            b0, b1 = b * (H // 8), (b + 1) * (H // 8)
+            for k in range(2):
+                render_band(ctx, cloud, scenes.yaw_camera(2 * math.pi * k / 16, W, H), settings, b0, b1, out=fr)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for k in range(3):
+                render_band(ctx, cloud, scenes.yaw_camera(2 * math.pi * k / 16, W, H), settings, b0, b1, out=fr)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            band_ms.append(e0.elapsed_time(e1) / 3)
+        out["bands8_single_gpu_ms"] = [round(v, 4) for v in band_ms]
+        out["bands8_slowest_band_fps"] = 1000.0 / max(band_ms)
     fr.destroy()
-    return {"metric": "ERP frames/sec (C5: 10M Gaussians, 4096x2048, row bands over the GPUs)",
-            "value": steps / (ms_max / 1000.0), "unit": "frames/s", "ms_per_frame": ms_max / steps,
-            "bands": world, "rows_per_band": rows, "n_gpus": world, "scaling": "strong",
-            "collective": "NCCL all_gather of the band images" if world > 1 else "none",
-            "band_tile_entries_rank0": info.n_entries, "stage_ms_per_frame_rank0": stages}
+    return out
 
 
 def _device_view(ptr: int, numel: int, dev):

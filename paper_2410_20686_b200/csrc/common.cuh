@@ -27,6 +27,7 @@ struct DevErrors {
   unsigned long long n_entries;    // total tile entries K (written by the offsets scan)
   unsigned long long n_visible;    // projected splats (RenderOutput::splats.size())
   unsigned long long n_instances;  // seam instances (RenderOutput::instances.size())
+  unsigned long long n_band;       // band renders: Gaussians with entries in the band
 };
 constexpr unsigned long long kNoError = ~0ull;
 

@@ -30,6 +30,12 @@ struct PreprocessArgs {
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
 
+// Band renders: flags[i] = (cnt[i] > 0), the Gaussians that emit entries into the band.
+void launch_band_flags(int64_t n, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream);
+// Stable compaction of the flagged (key, value) pairs to the positions pos[i] (exclusive
+// scan of the flags).
+void launch_compact_pairs(int64_t n, const uint32_t* flags, const uint32_t* pos, const uint32_t* keys_in,
+                          const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream);
 void launch_gather_counts(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt, uint32_t* cnt_sorted,
                           cudaStream_t stream);
 
@@ -45,8 +51,9 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream);
 void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, float far_r, uint8_t* keep,
                  cudaStream_t stream);
 
-void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, int32_t* offsets,
-                        cudaStream_t stream);
+// Tile CSR offsets [n_tiles + 1]; entries lie in tiles [t0, t1) (a row band), t1 <= n_tiles.
+void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, uint32_t t0, uint32_t t1,
+                        int32_t* offsets, cudaStream_t stream);
 
 struct BlendArgs {
   const int32_t* offsets;

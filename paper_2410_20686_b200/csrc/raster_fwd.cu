@@ -163,6 +163,39 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   ++g_launches;
 }
 
+// ------------------------------------------------------------------ band compaction
+// A band render only needs the Gaussians that emit entries into its tile rows; the
+// others are dropped before the depth sort (their relative order is irrelevant: they
+// appear in no tile list of the band).
+__global__ void k_band_flags(int64_t n, const uint32_t* __restrict__ cnt, uint32_t* __restrict__ flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = cnt[i] > 0 ? 1u : 0u;
+}
+
+__global__ void k_compact_pairs(int64_t n, const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos,
+                                const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flags[i]) {
+    keys_out[pos[i]] = keys_in[i];
+    vals_out[pos[i]] = vals_in[i];
+  }
+}
+
+void launch_band_flags(int64_t n, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream) {
+  if (n == 0) return;
+  k_band_flags<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, cnt, flags);
+  ++g_launches;
+}
+
+void launch_compact_pairs(int64_t n, const uint32_t* flags, const uint32_t* pos, const uint32_t* keys_in,
+                          const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream) {
+  if (n == 0) return;
+  k_compact_pairs<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, flags, pos, keys_in, vals_in, keys_out,
+                                                                    vals_out);
+  ++g_launches;
+}
+
 // ------------------------------------------------------------------ gather counts into rank order
 __global__ void k_gather_counts(int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt,
                                 uint32_t* __restrict__ cnt_sorted) {
@@ -259,25 +292,40 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
 }
 
 // ------------------------------------------------------------------ tile ranges
-__global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ keys, uint32_t n_tiles,
+// offsets[t] = first entry of tile t (CSR, empty tiles included). Entries only fall in
+// the band's tiles [t0, t1): thread e fills the tiles whose range starts at entry e
+// (from the previous entry's tile + 1 up to its own), clamped to the band; the tiles
+// outside the band (empty) are filled in parallel by k_fill_outside.
+__global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ keys, uint32_t t0, uint32_t t1,
                               int32_t* __restrict__ offsets) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e > k_entries) return;
-  const uint32_t prev = e == 0 ? 0u : keys[e - 1] + 1u;  // first tile whose range starts at e
-  const uint32_t cur = e == k_entries ? n_tiles : keys[e];
+  const uint32_t prev = e == 0 ? t0 : keys[e - 1] + 1u;  // first tile whose range starts at e
+  const uint32_t cur = e == k_entries ? t1 : keys[e];
   if (e != 0 && e != k_entries && keys[e - 1] == cur) return;
   for (uint32_t t = prev; t <= cur; ++t) offsets[t] = (int32_t)e;
 }
 
-void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, int32_t* offsets,
-                        cudaStream_t stream) {
+__global__ void k_fill_outside(uint32_t k_entries, uint32_t n_tiles, uint32_t t0, uint32_t t1,
+                               int32_t* __restrict__ offsets) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < t0) offsets[t] = 0;
+  else if (t > t1 && t <= n_tiles) offsets[t] = (int32_t)k_entries;
+}
+
+void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, uint32_t t0, uint32_t t1,
+                        int32_t* offsets, cudaStream_t stream) {
   if (k_entries == 0) {
     cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), stream);
     return;
   }
   const uint32_t threads = k_entries + 1;
-  k_tile_ranges<<<(threads + 255) / 256, 256, 0, stream>>>(k_entries, keys, n_tiles, offsets);
+  k_tile_ranges<<<(threads + 255) / 256, 256, 0, stream>>>(k_entries, keys, t0, t1, offsets);
   ++g_launches;
+  if (t0 > 0 || t1 < n_tiles) {
+    k_fill_outside<<<(n_tiles + 1 + 255) / 256, 256, 0, stream>>>(k_entries, n_tiles, t0, t1, offsets);
+    ++g_launches;
+  }
 }
 
 // ------------------------------------------------------------------ tile order

@@ -54,3 +54,18 @@ def test_band_rows_must_be_tile_aligned(gpu_ctx):
         render_band(gpu_ctx, cloud, CameraPose(256, 128), RenderSettings(), 8, 64)
     with pytest.raises(InvalidArgument):
         render_band(gpu_ctx, cloud, CameraPose(256, 128), RenderSettings(), 64, 32)
+
+
+def test_band_without_gaussians_is_empty(gpu_ctx):
+    """A band no Gaussian reaches (band compaction leaves nothing to sort): black image,
+    transmittance 1, no walks, no entries — as the same rows of the full render."""
+    arrs = oracle_lib.random_cloud(77, 200, (1.0, 5.0, 0.05, 0.2, 0.9, 0.001, 0.005))  # |elevation| <= 0.05
+    cloud = to_cloud32(arrs)
+    cam = CameraPose(256, 128)
+    s = RenderSettings()
+    full = render(gpu_ctx, cloud, cam, s)
+    fr = render_band(gpu_ctx, cloud, cam, s, 0, 16)
+    assert fr.info().n_entries == 0
+    assert np.array_equal(fr.image[:, :, 0:16], full.image[:, :, 0:16])
+    assert np.all(fr.image[:, :, 0:16] == 0) and np.all(fr.transmittance[:, 0:16] == 1)
+    assert np.all(fr.walked[:, 0:16] == 0)
