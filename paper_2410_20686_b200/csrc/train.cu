@@ -109,61 +109,75 @@ struct SsimWindow {
   float w[11];
 };
 
-// 5 horizontally filtered maps of (a, b, a^2, b^2, ab): [5][3][W-10][H].
-__global__ void k_ssim_h(const float* __restrict__ a, const float* __restrict__ b, int H, int W, SsimWindow win,
-                         float* __restrict__ out) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x, xo = blockIdx.y, c = blockIdx.z;
-  if (y >= H) return;
-  const int Wo = W - 10;
+// Two tiled kernels, each doing both separable passes in shared memory (no full-size
+// intermediate maps): a tile covers kSsimTY rows (y, contiguous) x kSsimTX columns (x)
+// of its output grid plus the 10-pixel halo of the 11-tap window.
+constexpr int kSsimTY = 56, kSsimTX = 16;
+constexpr int kSsimIY = kSsimTY + 10, kSsimIX = kSsimTX + 10;
+constexpr int kSsimThreads = 256;
+
+// Forward: per window (metrics.hpp:106-122) the five windowed moments of (a, b) —
+// horizontal 11-tap correlation then vertical — the SSIM value (block partial sums)
+// and the four window-grid gradient maps [4][3][W-10][H-10].
+__global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const float* __restrict__ a, const float* __restrict__ b,
+                                                           int H, int W, SsimWindow win, double inv_windows,
+                                                           float* __restrict__ gmaps, double* __restrict__ partial) {
+  __shared__ float s_a[kSsimIX][kSsimIY], s_b[kSsimIX][kSsimIY];
+  __shared__ float s_h[5][kSsimTX][kSsimIY];
+  __shared__ double s_w[kSsimThreads / 32];
+  const int Ho = H - 10, Wo = W - 10;
+  const int y0 = blockIdx.x * kSsimTY, x0 = blockIdx.y * kSsimTX, c = blockIdx.z;
   const int64_t plane = (int64_t)W * H;
   const float* pa = a + c * plane;
   const float* pb = b + c * plane;
-  float s[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-  for (int i = 0; i < 11; ++i) {
-    const float va = pa[(int64_t)(xo + i) * H + y], vb = pb[(int64_t)(xo + i) * H + y];
-    const float w = win.w[i];
-    s[0] += w * va;
-    s[1] += w * vb;
-    s[2] += w * (va * va);
-    s[3] += w * (vb * vb);
-    s[4] += w * (va * vb);
+  for (int k = threadIdx.x; k < kSsimIX * kSsimIY; k += kSsimThreads) {
+    const int ix = k / kSsimIY, iy = k - ix * kSsimIY;
+    const int x = x0 + ix, y = y0 + iy;
+    const bool in = x < W && y < H;
+    s_a[ix][iy] = in ? pa[(int64_t)x * H + y] : 0.0f;
+    s_b[ix][iy] = in ? pb[(int64_t)x * H + y] : 0.0f;
   }
-  const int64_t mplane = (int64_t)Wo * H, stride = 3 * mplane;
-  for (int m = 0; m < 5; ++m) out[m * stride + c * mplane + (int64_t)xo * H + y] = s[m];
-}
-
-// Vertical pass + the per-window SSIM terms (metrics.hpp:106-122): writes the four
-// window-grid gradient maps [4][3][W-10][H-10] and per-block partial sums of s.
-__global__ void k_ssim_v(const float* __restrict__ hmaps, int H, int W, SsimWindow win, double inv_windows,
-                         float* __restrict__ gmaps, double* __restrict__ partial) {
-  __shared__ double s_w[8];
-  const int yo = blockIdx.x * blockDim.x + threadIdx.x, xo = blockIdx.y, c = blockIdx.z;
-  const int Ho = H - 10, Wo = W - 10;
+  __syncthreads();
+  for (int k = threadIdx.x; k < kSsimTX * kSsimIY; k += kSsimThreads) {
+    const int tx = k / kSsimIY, iy = k - tx * kSsimIY;
+    float m[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 11; ++i) {
+      const float va = s_a[tx + i][iy], vb = s_b[tx + i][iy], w = win.w[i];
+      m[0] += w * va;
+      m[1] += w * vb;
+      m[2] += w * (va * va);
+      m[3] += w * (vb * vb);
+      m[4] += w * (va * vb);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) s_h[q][tx][iy] = m[q];
+  }
+  __syncthreads();
   double sval = 0.0;
-  if (yo < Ho) {
-    const int64_t mplane = (int64_t)Wo * H, stride = 3 * mplane;
+  const int64_t gplane = (int64_t)Wo * Ho, gstride = 3 * gplane;
+  const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f, iw = (float)inv_windows;
+  for (int k = threadIdx.x; k < kSsimTX * kSsimTY; k += kSsimThreads) {
+    const int tx = k / kSsimTY, ty = k - tx * kSsimTY;
+    const int xo = x0 + tx, yo = y0 + ty;
+    if (xo >= Wo || yo >= Ho) continue;
     float v[5];
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
-      const float* src = hmaps + m * stride + c * mplane + (int64_t)xo * H + yo;
+    for (int q = 0; q < 5; ++q) {
       float acc = 0.0f;
 #pragma unroll
-      for (int i = 0; i < 11; ++i) acc += win.w[i] * src[i];
-      v[m] = acc;
+      for (int i = 0; i < 11; ++i) acc += win.w[i] * s_h[q][tx][ty + i];
+      v[q] = acc;
     }
-    const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f;
     const float mu_a = v[0], mu_b = v[1];
     const float var_a = v[2] - mu_a * mu_a, var_b = v[3] - mu_b * mu_b, cov = v[4] - mu_a * mu_b;
     const float n1 = 2.0f * mu_a * mu_b + c1, n2 = 2.0f * cov + c2;
     const float d1 = mu_a * mu_a + mu_b * mu_b + c1, d2 = var_a + var_b + c2;
     const float sc = (n1 * n2) / (d1 * d2);
-    sval = sc;
-    const float iw = (float)inv_windows;
+    sval += sc;
     const float d_mu_a = (2.0f * mu_b * n2 - 2.0f * mu_a * sc * d2) / (d1 * d2) * iw;
     const float d_var_a = (-sc / d2) * iw;
     const float d_cov = (2.0f * (n1 / d1) / d2) * iw;
-    const int64_t gplane = (int64_t)Wo * Ho, gstride = 3 * gplane;
     const int64_t idx = c * gplane + (int64_t)xo * Ho + yo;
     gmaps[0 * gstride + idx] = d_mu_a;
     gmaps[1 * gstride + idx] = d_var_a;
@@ -176,57 +190,64 @@ __global__ void k_ssim_v(const float* __restrict__ hmaps, int H, int W, SsimWind
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+    for (int w = 0; w < kSsimThreads / 32; ++w) t += s_w[w];
     partial[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
   }
 }
 
-// window_scatter, horizontal half: [4][3][W][H+10] from the zero-padded grid maps.
-__global__ void k_ssim_scatter_h(const float* __restrict__ gmaps, int H, int W, SsimWindow win,
-                                 float* __restrict__ out) {
-  const int yp = blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y, c = blockIdx.z;
-  const int Hp = H + 10, Ho = H - 10, Wo = W - 10;
-  if (yp >= Hp) return;
-  const int yo = yp - 10;  // padded row -> grid row
+// Adjoint: window_scatter of the four grid maps (the same separable correlation on the
+// zero-padded grid, horizontal then vertical) and the image gradient combined with the
+// L1 part: dl = (1 - lambda) sign(a - b) / pixels - lambda (S_mu + (2 a S_var + b S_cov)
+// - S_mix), plus block partial sums of |a - b|.
+__global__ void __launch_bounds__(kSsimThreads) k_ssim_bwd(const float* __restrict__ gmaps,
+                                                           const float* __restrict__ a, const float* __restrict__ b,
+                                                           int H, int W, SsimWindow win, float lambda, float pixels,
+                                                           float* __restrict__ grad, double* __restrict__ l1_partial) {
+  __shared__ float s_g[4][kSsimIX][kSsimIY];
+  __shared__ float s_h[4][kSsimTX][kSsimIY];
+  __shared__ double s_w[kSsimThreads / 32];
+  const int Ho = H - 10, Wo = W - 10;
+  const int y0 = blockIdx.x * kSsimTY, x0 = blockIdx.y * kSsimTX, c = blockIdx.z;
   const int64_t gplane = (int64_t)Wo * Ho, gstride = 3 * gplane;
-  const int64_t oplane = (int64_t)W * Hp, ostride = 3 * oplane;
-  for (int m = 0; m < 4; ++m) {
-    float acc = 0.0f;
+  // Grid rows [y0 - 10, y0 + TY), columns [x0 - 10, x0 + TX), zero outside the grid.
+  for (int k = threadIdx.x; k < kSsimIX * kSsimIY; k += kSsimThreads) {
+    const int ix = k / kSsimIY, iy = k - ix * kSsimIY;
+    const int xo = x0 - 10 + ix, yo = y0 - 10 + iy;
+    const bool in = xo >= 0 && xo < Wo && yo >= 0 && yo < Ho;
+    const int64_t idx = c * gplane + (int64_t)xo * Ho + yo;
 #pragma unroll
-    for (int i = 0; i < 11; ++i) {
-      const int xo = x + i - 10;  // padded column (x + i) -> grid column
-      const float v = (yo >= 0 && yo < Ho && xo >= 0 && xo < Wo) ? gmaps[m * gstride + c * gplane + (int64_t)xo * Ho + yo]
-                                                                  : 0.0f;
-      acc += win.w[i] * v;
-    }
-    out[m * ostride + c * oplane + (int64_t)x * Hp + yp] = acc;
+    for (int q = 0; q < 4; ++q) s_g[q][ix][iy] = in ? gmaps[q * gstride + idx] : 0.0f;
   }
-}
-
-// window_scatter, vertical half, and the SSIM image gradient combined with the L1 part:
-// dl = (1 - lambda) sign(a - b) / pixels - lambda (S_mu + (2 a S_var + b S_cov) - S_mix).
-__global__ void k_ssim_combine(const float* __restrict__ hs, const float* __restrict__ a,
-                               const float* __restrict__ b, int H, int W, SsimWindow win, float lambda,
-                               float pixels, float* __restrict__ grad, double* __restrict__ l1_partial) {
-  __shared__ double s_w[8];
-  const int y = blockIdx.x * blockDim.x + threadIdx.x, x = blockIdx.y, c = blockIdx.z;
-  const int Hp = H + 10;
-  double l1 = 0.0;
-  if (y < H) {
-    const int64_t oplane = (int64_t)W * Hp, ostride = 3 * oplane;
-    float S[4];
+  __syncthreads();
+  for (int k = threadIdx.x; k < kSsimTX * kSsimIY; k += kSsimThreads) {
+    const int tx = k / kSsimIY, iy = k - tx * kSsimIY;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const float* src = hs + m * ostride + c * oplane + (int64_t)x * Hp + y;
+    for (int q = 0; q < 4; ++q) {
       float acc = 0.0f;
 #pragma unroll
-      for (int i = 0; i < 11; ++i) acc += win.w[i] * src[i];
-      S[m] = acc;
+      for (int i = 0; i < 11; ++i) acc += win.w[i] * s_g[q][tx + i][iy];
+      s_h[q][tx][iy] = acc;
     }
-    const int64_t p = (int64_t)c * W * H + (int64_t)x * H + y;
+  }
+  __syncthreads();
+  double l1 = 0.0;
+  const int64_t plane = (int64_t)W * H;
+  for (int k = threadIdx.x; k < kSsimTX * kSsimTY; k += kSsimThreads) {
+    const int tx = k / kSsimTY, ty = k - tx * kSsimTY;
+    const int x = x0 + tx, y = y0 + ty;
+    if (x >= W || y >= H) continue;
+    float S[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 11; ++i) acc += win.w[i] * s_h[q][tx][ty + i];
+      S[q] = acc;
+    }
+    const int64_t p = c * plane + (int64_t)x * H + y;
     const float va = a[p], vb = b[p];
     const float d = va - vb;
-    l1 = (double)fabsf(d);
+    l1 += (double)fabsf(d);
     const float sign = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
     const float g_ssim = S[0] + (2.0f * va * S[1] + vb * S[2]) - S[3];
     grad[p] = (1.0f - lambda) * sign / pixels - lambda * g_ssim;
@@ -237,7 +258,7 @@ __global__ void k_ssim_combine(const float* __restrict__ hs, const float* __rest
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+    for (int w = 0; w < kSsimThreads / 32; ++w) t += s_w[w];
     l1_partial[((int64_t)c * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
   }
 }
@@ -263,10 +284,10 @@ __global__ void k_ssim_loss(const double* __restrict__ l1_partial, int64_t n_l1,
 }
 
 size_t ssim_temp_bytes(int H, int W) {
-  const int64_t Ho = H - 10, Wo = W - 10, Hp = H + 10;
-  const int64_t blocks_v = ((Ho + 255) / 256) * Wo * 3, blocks_c = ((H + 255) / 256) * W * 3;
-  return sizeof(float) * (size_t)(5 * 3 * Wo * H + 4 * 3 * Wo * Ho + 4 * 3 * W * Hp) +
-         sizeof(double) * (size_t)(blocks_v + blocks_c + 8);
+  const int64_t Ho = H - 10, Wo = W - 10;
+  const int64_t bf = ((Ho + kSsimTY - 1) / kSsimTY) * ((Wo + kSsimTX - 1) / kSsimTX) * 3;
+  const int64_t bb = ((H + kSsimTY - 1) / kSsimTY) * ((W + kSsimTX - 1) / kSsimTX) * 3;
+  return sizeof(float) * (size_t)(4 * 3 * Wo * Ho) + sizeof(double) * (size_t)(bf + bb + 8);
 }
 
 void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda, float* grad, void* temp,
@@ -279,25 +300,19 @@ void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda
     sum += win.w[i];
   }
   for (int i = 0; i < 11; ++i) win.w[i] /= sum;
-  const int64_t Ho = H - 10, Wo = W - 10, Hp = H + 10;
-  float* hmaps = static_cast<float*>(temp);
-  float* gmaps = hmaps + 5 * 3 * Wo * H;
-  float* hs = gmaps + 4 * 3 * Wo * Ho;
-  double* s_part = reinterpret_cast<double*>(hs + 4 * 3 * W * Hp);
-  const int64_t bx_v = (Ho + 255) / 256;
-  double* l1_part = s_part + bx_v * Wo * 3;
-  const int64_t bx_c = (H + 255) / 256;
+  const int64_t Ho = H - 10, Wo = W - 10;
+  float* gmaps = static_cast<float*>(temp);
+  double* s_part = reinterpret_cast<double*>(gmaps + 4 * 3 * Wo * Ho);
+  const dim3 gf((unsigned)((Ho + kSsimTY - 1) / kSsimTY), (unsigned)((Wo + kSsimTX - 1) / kSsimTX), 3);
+  const dim3 gb((unsigned)((H + kSsimTY - 1) / kSsimTY), (unsigned)((W + kSsimTX - 1) / kSsimTX), 3);
+  double* l1_part = s_part + (int64_t)gf.x * gf.y * gf.z;
   const double windows = 3.0 * (double)Ho * (double)Wo;
-  k_ssim_h<<<dim3((unsigned)((H + 255) / 256), (unsigned)Wo, 3), 256, 0, stream>>>(a, b, H, W, win, hmaps);
-  k_ssim_v<<<dim3((unsigned)bx_v, (unsigned)Wo, 3), 256, 0, stream>>>(hmaps, H, W, win, 1.0 / windows, gmaps,
-                                                                       s_part);
-  k_ssim_scatter_h<<<dim3((unsigned)((Hp + 255) / 256), (unsigned)W, 3), 256, 0, stream>>>(gmaps, H, W, win, hs);
+  k_ssim_fwd<<<gf, kSsimThreads, 0, stream>>>(a, b, H, W, win, 1.0 / windows, gmaps, s_part);
   const float pixels = 3.0f * (float)H * (float)W;
-  k_ssim_combine<<<dim3((unsigned)bx_c, (unsigned)W, 3), 256, 0, stream>>>(hs, a, b, H, W, win, lambda, pixels,
-                                                                           grad, l1_part);
-  k_ssim_loss<<<1, 256, 0, stream>>>(l1_part, bx_c * W * 3, s_part, bx_v * Wo * 3, (double)lambda,
-                                     3.0 * (double)H * (double)W, windows, loss_out);
-  g_launches += 5;
+  k_ssim_bwd<<<gb, kSsimThreads, 0, stream>>>(gmaps, a, b, H, W, win, lambda, pixels, grad, l1_part);
+  k_ssim_loss<<<1, 256, 0, stream>>>(l1_part, (int64_t)gb.x * gb.y * gb.z, s_part, (int64_t)gf.x * gf.y * gf.z,
+                                     (double)lambda, 3.0 * (double)H * (double)W, windows, loss_out);
+  g_launches += 3;
 }
 
 __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, float lr, float c1, float c2) {
