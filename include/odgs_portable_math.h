@@ -182,10 +182,11 @@ PM_HD float pm_expf(float x) {
  * the exponent field (exact: for -86 <= x <= 88 the result is a normal float).
  * Results below e^-86 (x < -86) are flushed to +0 — the alpha they would produce is
  * < 1e-37 and can change neither the transmittance nor the colour.
+ *
+ * pm_expf_blend_core is the evaluation alone, valid for -86 <= x <= 88; pm_expf_blend
+ * adds the special cases.
  */
-PM_HD float pm_expf_blend(float x) {
-  if (!(x >= -86.0f)) return (x != x) ? x : 0.0f;
-  if (x > 88.0f) return pm_expf(x);
+PM_HD float pm_expf_blend_core(float x) {
   const float shifter = 12582912.0f; /* 1.5 * 2^23 */
   const float t = pm_ffma(x, 0x1.715476p+0f, shifter);
   const float n = pm_fsub(t, shifter);
@@ -212,6 +213,12 @@ PM_HD float pm_expf_blend(float x) {
   memcpy(&res, &rb, 4);
   return res;
 #endif
+}
+
+PM_HD float pm_expf_blend(float x) {
+  if (!(x >= -86.0f)) return (x != x) ? x : 0.0f;
+  if (x > 88.0f) return pm_expf(x);
+  return pm_expf_blend_core(x);
 }
 
 /* ---------------------------------------------------------------- sin / cos */

@@ -496,6 +496,11 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
 
 // ------------------------------------------------------------------ blend with warp culling
 // 6 CTAs (48 warps) per SM: the walk is latency-bound on its dependent chains.
+// kSmallCutoff: cutoff^2 <= 172, so every composited entry has -d2/2 >= -86 and the
+// exponential's underflow branch is dead (pm_expf_blend == pm_expf_blend_core there,
+// bit for bit); the overflow branch stays (x > 88 needs d2 < -176, which float rounding
+// of a huge |d| can produce).
+template <bool kSmallCutoff>
 __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
@@ -503,9 +508,14 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base,
     const uint32_t* __restrict__ order) {
   constexpr int kWarps = kBlendThreads / 32;
-  __shared__ float4 s_geo[kBlendThreads];  // cx, cy, i00, 2*i01
-  __shared__ float4 s_att[kBlendThreads];  // i11, opacity, r, g
-  __shared__ float s_b[kBlendThreads];
+  // One 48-byte record per staged entry: the walk addresses all three parts from one
+  // base with immediate offsets (separate arrays cost an address computation each).
+  struct alignas(16) Staged {
+    float4 geo;  // cx, cy, i00, 2*i01
+    float4 att;  // i11, opacity, r, g
+    float4 b;    // b, -, -, -
+  };
+  __shared__ Staged s_ent[kBlendThreads];
   __shared__ uint8_t s_mask[kBlendThreads];
   __shared__ uint8_t s_list[kWarps][kBlendThreads];
   __shared__ float4 s_wbox[kWarps];  // pixel-centre bbox of each warp: xmin, xmax, ymin, ymax
@@ -567,9 +577,9 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
       const float c2 = __ldg(&sp_c[g].x);
       const float cx = a.x + (k == 0 ? -W : (k == 1 ? 0.0f : W));
       const float cy = a.y;
-      s_geo[tid] = make_float4(cx, cy, a.z, 2.0f * a.w);
-      s_att[tid] = make_float4(b.x, b.y, b.z, b.w);
-      s_b[tid] = c2;
+      s_ent[tid].geo = make_float4(cx, cy, a.z, 2.0f * a.w);
+      s_ent[tid].att = make_float4(b.x, b.y, b.z, b.w);
+      s_ent[tid].b.x = c2;
       float ex, ey;
       if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
 #pragma unroll
@@ -597,13 +607,16 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     if (!done) {
       for (int q = 0; q < n_list; ++q) {
         const int j = s_list[warp][q];
-        const float4 geo = s_geo[j];
+        const float4 geo = s_ent[j].geo;
         const float dx = px - geo.x;
         const float dy = py - geo.y;
-        const float4 att = s_att[j];
+        const float4 att = s_ent[j].att;
         const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
         if (d2 > cutoff2) continue;
-        const float alpha = std_min(alpha_clamp, att.y * pm_expf_blend(-d2 / 2.0f));
+        const float x = -d2 / 2.0f;
+        const float G = kSmallCutoff ? (x > 88.0f ? pm_expf(x) : pm_expf_blend_core(x)) : pm_expf_blend(x);
+        // fminf == std::min here: the product is never NaN or -0 for a projected splat.
+        const float alpha = fminf(alpha_clamp, att.y * G);
         const float t_next = t * (1.0f - alpha);
         if (t_next < transmittance_floor) {
           walked = base + j - e0;
@@ -614,7 +627,7 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
         ++contrib;
         cr = cr + att.z * wgt;
         cg = cg + att.w * wgt;
-        cb = cb + s_b[j] * wgt;
+        cb = cb + s_ent[j].b.x * wgt;
         t = t_next;
       }
     }
@@ -642,10 +655,12 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
   const int n_band_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
   if (n_band_tiles <= 0) return;
   if (!a.plain && a.tile_size <= 16) {
-    k_blend_cull<<<n_band_tiles, kBlendThreads, 0, stream>>>(
-        a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.alpha_clamp,
-        a.transmittance_floor, a.cutoff_sigma * a.cutoff_sigma, a.image, a.transmittance, a.walked, a.work,
-        a.band_ty0 * a.tiles_x, a.order);
+    const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
+    auto kern = cutoff2 <= 172.0f ? k_blend_cull<true> : k_blend_cull<false>;
+    kern<<<n_band_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,
+                                                      a.tile_size, a.tiles_x, a.alpha_clamp, a.transmittance_floor,
+                                                      cutoff2, a.image, a.transmittance, a.walked, a.work,
+                                                      a.band_ty0 * a.tiles_x, a.order);
     ++g_launches;
     return;
   }
