@@ -581,15 +581,30 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
       s_ent[tid].att = make_float4(b.x, b.y, b.z, b.w);
       s_ent[tid].b.x = c2;
       float ex, ey;
-      if (cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
+      if (!cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey)) {
+        mask = 0xFFu;
+      } else if (tile_size == 16) {
+        // The warp boxes form a 2 (x) x 4 (y) grid of blocks: test the entry against the
+        // two column and four row intervals (6 tests instead of 8 box tests). Warp w is
+        // column w & 1, row w >> 1; its box's x part equals its column's (warp w & 1),
+        // its y part its row's (warp w & ~1): same comparisons, same mask.
+        const float4 c0 = s_wbox[0], c1 = s_wbox[1];
+        const bool in0 = !((c0.x - cx > ex) || (c0.y - cx < -ex));
+        const bool in1 = !((c1.x - cx > ex) || (c1.y - cx < -ex));
+        uint32_t rows = 0;
+#pragma unroll
+        for (int wy = 0; wy < 4; ++wy) {
+          const float4 r = s_wbox[2 * wy];
+          rows |= ((r.z - cy > ey) || (r.w - cy < -ey)) ? 0u : (1u << (2 * wy));
+        }
+        mask = (in0 ? rows : 0u) | (in1 ? rows << 1 : 0u);
+      } else {
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
           const float4 bx = s_wbox[w];
           const bool out = (bx.x - cx > ex) || (bx.y - cx < -ex) || (bx.z - cy > ey) || (bx.w - cy < -ey);
           mask |= out ? 0u : (1u << w);
         }
-      } else {
-        mask = 0xFFu;
       }
     }
     s_mask[tid] = (uint8_t)mask;
