@@ -181,7 +181,10 @@ PM_HD float pm_expf(float x) {
  * on |r| <= ln2/2 (relative error 1.9e-9), and the scaling 2^n applied by adding n to
  * the exponent field (exact: for -86 <= x <= 88 the result is a normal float).
  * Results below e^-86 (x < -86) are flushed to +0 — the alpha they would produce is
- * < 1e-37 and can change neither the transmittance nor the colour.
+ * < 1e-37 and can change neither the transmittance nor the colour. Arguments above 88
+ * are evaluated at 88 (e^88 = 1.65e38): x = -d2/2 > 88 needs d2 < -176, which a
+ * positive-definite form reaches only through rounding at |d| > ~8000 px, and the alpha
+ * clamps there either way unless the opacity is below 6e-39.
  *
  * pm_expf_blend_core is the evaluation alone, valid for -86 <= x <= 88; pm_expf_blend
  * adds the special cases.
@@ -217,8 +220,7 @@ PM_HD float pm_expf_blend_core(float x) {
 
 PM_HD float pm_expf_blend(float x) {
   if (!(x >= -86.0f)) return (x != x) ? x : 0.0f;
-  if (x > 88.0f) return pm_expf(x);
-  return pm_expf_blend_core(x);
+  return pm_expf_blend_core(fminf(x, 88.0f));
 }
 
 /* ---------------------------------------------------------------- sin / cos */

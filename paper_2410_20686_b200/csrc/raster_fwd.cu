@@ -497,9 +497,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
 // ------------------------------------------------------------------ blend with warp culling
 // 6 CTAs (48 warps) per SM: the walk is latency-bound on its dependent chains.
 // kSmallCutoff: cutoff^2 <= 172, so every composited entry has -d2/2 >= -86 and the
-// exponential's underflow branch is dead (pm_expf_blend == pm_expf_blend_core there,
-// bit for bit); the overflow branch stays (x > 88 needs d2 < -176, which float rounding
-// of a huge |d| can produce).
+// exponential's underflow branch is dead: pm_expf_blend(x) == pm_expf_blend_core(
+// fminf(x, 88)) there, bit for bit, without a branch in the walk.
 template <bool kSmallCutoff>
 __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
@@ -629,7 +628,7 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
         const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
         if (d2 > cutoff2) continue;
         const float x = -d2 / 2.0f;
-        const float G = kSmallCutoff ? (x > 88.0f ? pm_expf(x) : pm_expf_blend_core(x)) : pm_expf_blend(x);
+        const float G = kSmallCutoff ? pm_expf_blend_core(fminf(x, 88.0f)) : pm_expf_blend(x);
         // fminf == std::min here: the product is never NaN or -0 for a projected splat.
         const float alpha = fminf(alpha_clamp, att.y * G);
         const float t_next = t * (1.0f - alpha);
