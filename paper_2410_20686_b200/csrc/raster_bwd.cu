@@ -218,7 +218,10 @@ __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, 
                              __fmul_rn(__fmul_rn(att.x, dy), dy));
   if (!(dd <= cutoff2)) return false;
   const float op = att.y;
-  float G = __expf(-0.5f * dd);
+  // e^(-dd/2) = 2^(dd * -log2(e)/2) on MUFU.EX2 (flush-to-zero: results below 2^-126
+  // contribute nothing)
+  float G;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(G) : "f"(dd * -0.72134752044448170368f));
   float raw_alpha = op * G;
   if (fabsf(raw_alpha - alpha_clamp) < 1e-4f) {
     G = pm_expf_blend(-dd / 2.0f);
