@@ -283,14 +283,18 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1,
     const uint32_t* __restrict__ order) {
-  __shared__ float4 s_geo[kBwdBatch];   // cx, cy, i00, 2*i01
-  __shared__ float4 s_att[kBwdBatch];   // i11, opacity, r, g
-  __shared__ float s_b[kBwdBatch];
+  // One 48-byte record per staged entry (all parts addressed from one base).
+  struct alignas(16) Staged {
+    float4 geo;  // cx, cy, i00, 2*i01
+    float4 att;  // i11, opacity, r, g
+    float4 b;    // b, -, -, -
+  };
+  __shared__ Staged s_ent[kBwdBatch];
   __shared__ uint32_t s_pos[2][kBwdBatch];  // double-buffered: read one batch later
   __shared__ uint8_t s_mask[2][kBwdBatch];
   __shared__ uint8_t s_list[kBwdWarps][kBwdBatch];
   __shared__ float s_part[kBwdWarps][kRec][kBwdBatch];  // 9 sums per (warp, entry), component-major
-  __shared__ int s_wrote[kBwdWarps][kBwdBatch];  // batch tag (its `hi`) of the last write
+  __shared__ uint8_t s_wrote[kBwdWarps][kBwdBatch];  // warp wrote the entry's partial (cleared by its reader)
   __shared__ int s_maxw[kBwdWarps];
   __shared__ float4 s_wbox[kBwdWarps];
 
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
   //   phase B  every warp compacts its entries of batch b and walks them
   //   -- barrier --
   // A final phase A writes the last batch.
-  int prev_hi = 0, prev_count = 0, buf = 0;
+  int prev_count = 0, buf = 0;
   for (int hi = max_walked;; hi -= kBwdBatch) {
     const bool have = hi > 0;
     const int lo = have ? max(0, hi - kBwdBatch) : 0;
@@ -376,9 +380,9 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
           const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
           const float4 c = __ldg(sp_c + g);
           const float cx = a.x + shift_of(k, width), cy = a.y;
-          s_geo[tid] = make_float4(cx, cy, a.z, 2.0f * a.w);
-          s_att[tid] = b;
-          s_b[tid] = c.x;
+          s_ent[tid].geo = make_float4(cx, cy, a.z, 2.0f * a.w);
+          s_ent[tid].att = b;
+          s_ent[tid].b.x = c.x;
           float ex, ey;
           // Warps whose longest walk ends before this entry never replay it.
           const int rel = lo + tid;
@@ -419,7 +423,8 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         bool any_w = false;
 #pragma unroll
         for (int w = 0; w < kBwdWarps; ++w)
-          if (s_wrote[w][j] == prev_hi) {
+          if (s_wrote[w][j]) {
+            s_wrote[w][j] = 0;
             any_w = true;
 #pragma unroll
             for (int c = 0; c < kRec; ++c) sum[c] += s_part[w][c][j];
@@ -458,11 +463,11 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
       unsigned ma, mb, mc, md;
       {
         float A[kRec], B[kRec];
-        const bool any_a = bwd_contrib(s_geo[ja], s_att[ja], s_b[ja], lo + ja, wk, px, py, cutoff2, alpha_clamp, d0,
+        const bool any_a = bwd_contrib(s_ent[ja].geo, s_ent[ja].att, s_ent[ja].b.x, lo + ja, wk, px, py, cutoff2, alpha_clamp, d0,
                                        d1, d2v, t, suf0, suf1, suf2, A);
         bool any_b = false;
         if (jb >= 0)
-          any_b = bwd_contrib(s_geo[jb], s_att[jb], s_b[jb], lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+          any_b = bwd_contrib(s_ent[jb].geo, s_ent[jb].att, s_ent[jb].b.x, lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
                               t, suf0, suf1, suf2, B);
         else
 #pragma unroll
@@ -478,13 +483,13 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         float C[kRec], D[kRec];
         bool any_c = false, any_d = false;
         if (jc >= 0)
-          any_c = bwd_contrib(s_geo[jc], s_att[jc], s_b[jc], lo + jc, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+          any_c = bwd_contrib(s_ent[jc].geo, s_ent[jc].att, s_ent[jc].b.x, lo + jc, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
                               t, suf0, suf1, suf2, C);
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) C[c] = 0.0f;
         if (jd >= 0)
-          any_d = bwd_contrib(s_geo[jd], s_att[jd], s_b[jd], lo + jd, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
+          any_d = bwd_contrib(s_ent[jd].geo, s_ent[jd].att, s_ent[jd].b.x, lo + jd, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
                               t, suf0, suf1, suf2, D);
         else
 #pragma unroll
@@ -513,12 +518,11 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
           const int j = grp == 0 ? ja : (grp == 1 ? jc : (grp == 2 ? jb : jd));
 #pragma unroll
           for (int c = 0; c < kRec; ++c) s_part[warp][c][j] = L[c];
-          s_wrote[warp][j] = hi;
+          s_wrote[warp][j] = 1;
         }
       }
     }
     __syncthreads();
-    prev_hi = hi;
     prev_count = count;
     buf ^= 1;
   }
