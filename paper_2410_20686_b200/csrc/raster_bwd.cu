@@ -246,18 +246,25 @@ __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, 
   if (!(raw_alpha > alpha_clamp)) {  // clamped: no alpha gradient (backward.hpp:289)
     acc[5] = dl_dalpha * G;
     const float dl_dd2 = dl_dalpha * raw_alpha * -0.5f;  // dl_dalpha * op * (-G / 2)
-    const float i01 = 0.5f * geo.w;
-    const float gx = fmaf(geo.z, dx, i01 * dy);
-    const float gy = fmaf(i01, dx, att.x * dy);
-    const float m2 = -2.0f * dl_dd2;
-    acc[0] = m2 * gx;
-    acc[1] = m2 * gy;
+    // dL/dmean = -2 dl_dd2 Sigma^-1 d is linear in (dl_dd2 dx, dl_dd2 dy) with per-entry
+    // coefficients: acc[0..1] carry those two sums, and the warp's writer applies
+    // Sigma^-1 once per entry (mean_grad_from_moments) instead of per pixel.
     const float ex = dl_dd2 * dx, ey = dl_dd2 * dy;
+    acc[0] = ex;
+    acc[1] = ey;
     acc[2] = ex * dx;
     acc[3] = ex * dy;
     acc[4] = ey * dy;
   }
   return true;
+}
+
+// acc[0..1] (sums of dl_dd2 dx, dl_dd2 dy) -> the mean gradient -2 Sigma^-1 (sums)
+// (backward.hpp:298-300); geo = (cx, cy, i00, 2*i01), i11 = att.x.
+__device__ __forceinline__ void mean_grad_from_moments(const float4 geo, float i11, float& a0, float& a1) {
+  const float i01 = 0.5f * geo.w, sx = a0, sy = a1;
+  a0 = -2.0f * fmaf(geo.z, sx, i01 * sy);
+  a1 = -2.0f * fmaf(i01, sx, i11 * sy);
 }
 
 // First butterfly level of a pair reduce-scatter: lanes 0-15 keep the sum of A over
@@ -516,6 +523,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         const unsigned mine = grp == 0 ? ma : (grp == 1 ? mc : (grp == 2 ? mb : md));
         if ((lane & 7) == 0 && mine) {
           const int j = grp == 0 ? ja : (grp == 1 ? jc : (grp == 2 ? jb : jd));
+          mean_grad_from_moments(s_ent[j].geo, s_ent[j].att.x, L[0], L[1]);
 #pragma unroll
           for (int c = 0; c < kRec; ++c) s_part[warp][c][j] = L[c];
           s_wrote[warp][j] = 1;
