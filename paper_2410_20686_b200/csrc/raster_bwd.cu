@@ -206,8 +206,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 
 __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, const float b, int rel, int wk,
                                             float px, float py, float cutoff2, float alpha_clamp, float d0,
-                                            float d1, float d2v, float& t, float& suf0, float& suf1, float& suf2,
-                                            float acc[kRec]) {
+                                            float d1, float d2v, float& t, float& sd, float acc[kRec]) {
 #pragma unroll
   for (int c = 0; c < kRec; ++c) acc[c] = 0.0f;
   if (rel >= wk) return false;
@@ -235,13 +234,12 @@ __device__ __forceinline__ bool bwd_contrib(const float4 geo, const float4 att, 
   acc[6] = d0 * at;
   acc[7] = d1 * at;
   acc[8] = d2v * at;
-  const float v0 = fmaf(-suf0, inv_om, c0 * t_here);
-  const float v1 = fmaf(-suf1, inv_om, c1 * t_here);
-  const float v2 = fmaf(-suf2, inv_om, c2 * t_here);
-  const float dl_dalpha = fmaf(d0, v0, fmaf(d1, v1, d2v * v2));
-  suf0 = fmaf(c0, at, suf0);
-  suf1 = fmaf(c1, at, suf1);
-  suf2 = fmaf(c2, at, suf2);
+  // dL/dalpha = sum_c d_c (c_c t_here - suffix_c / (1 - alpha)) (backward.hpp:284-287)
+  // needs the suffix only through sd = sum_c d_c suffix_c, which the recursion carries
+  // as one scalar: sd += (d . c) alpha t_here.
+  const float dc = fmaf(d0, c0, fmaf(d1, c1, d2v * c2));
+  const float dl_dalpha = fmaf(-sd, inv_om, dc * t_here);
+  sd = fmaf(dc, at, sd);
   t = t_here;
   if (!(raw_alpha > alpha_clamp)) {  // clamped: no alpha gradient (backward.hpp:289)
     acc[5] = dl_dalpha * G;
@@ -326,7 +324,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
   const int x = tx * tile_size + lx, y = ty * tile_size + ly;
   valid = valid && x < width && y < height;
   const float px = (float)x + 0.5f, py = (float)y + 0.5f;
-  float t = 1.0f, d0 = 0.0f, d1 = 0.0f, d2v = 0.0f, suf0 = 0.0f, suf1 = 0.0f, suf2 = 0.0f;
+  float t = 1.0f, d0 = 0.0f, d1 = 0.0f, d2v = 0.0f, sd = 0.0f;  // sd = dL/dpixel . suffix
   int wk = 0;
   if (valid) {
     const int64_t p = (int64_t)x * height + y;
@@ -471,11 +469,11 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
       {
         float A[kRec], B[kRec];
         const bool any_a = bwd_contrib(s_ent[ja].geo, s_ent[ja].att, s_ent[ja].b.x, lo + ja, wk, px, py, cutoff2, alpha_clamp, d0,
-                                       d1, d2v, t, suf0, suf1, suf2, A);
+                                       d1, d2v, t, sd, A);
         bool any_b = false;
         if (jb >= 0)
           any_b = bwd_contrib(s_ent[jb].geo, s_ent[jb].att, s_ent[jb].b.x, lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
-                              t, suf0, suf1, suf2, B);
+                              t, sd, B);
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
@@ -491,13 +489,13 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         bool any_c = false, any_d = false;
         if (jc >= 0)
           any_c = bwd_contrib(s_ent[jc].geo, s_ent[jc].att, s_ent[jc].b.x, lo + jc, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
-                              t, suf0, suf1, suf2, C);
+                              t, sd, C);
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) C[c] = 0.0f;
         if (jd >= 0)
           any_d = bwd_contrib(s_ent[jd].geo, s_ent[jd].att, s_ent[jd].b.x, lo + jd, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v,
-                              t, suf0, suf1, suf2, D);
+                              t, sd, D);
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) D[c] = 0.0f;
