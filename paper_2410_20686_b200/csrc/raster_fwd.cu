@@ -296,14 +296,32 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
 // the band's tiles [t0, t1): thread e fills the tiles whose range starts at entry e
 // (from the previous entry's tile + 1 up to its own), clamped to the band; the tiles
 // outside the band (empty) are filled in parallel by k_fill_outside.
+// Thread i covers entries 4i .. 4i+3 (one 16-byte key load; the sentinel position K
+// belongs to the thread whose range contains it).
 __global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ keys, uint32_t t0, uint32_t t1,
                               int32_t* __restrict__ offsets) {
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e > k_entries) return;
-  const uint32_t prev = e == 0 ? t0 : keys[e - 1] + 1u;  // first tile whose range starts at e
-  const uint32_t cur = e == k_entries ? t1 : keys[e];
-  if (e != 0 && e != k_entries && keys[e - 1] == cur) return;
-  for (uint32_t t = prev; t <= cur; ++t) offsets[t] = (int32_t)e;
+  const uint32_t e_first = 4u * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (e_first > k_entries) return;
+  uint32_t kv[4];
+  if (e_first + 4u <= k_entries) {
+    const uint4 q = *reinterpret_cast<const uint4*>(keys + e_first);
+    kv[0] = q.x; kv[1] = q.y; kv[2] = q.z; kv[3] = q.w;
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) kv[u] = e_first + u < k_entries ? keys[e_first + u] : t1;  // K: sentinel
+  }
+  uint32_t prev_key = e_first == 0 ? 0xFFFFFFFFu : keys[e_first - 1];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t e = e_first + u;
+    if (e > k_entries) break;
+    const uint32_t cur = kv[u];
+    if (e == 0 || e == k_entries || prev_key != cur) {
+      const uint32_t first = e == 0 ? t0 : prev_key + 1u;  // first tile whose range starts at e
+      for (uint32_t t = first; t <= cur; ++t) offsets[t] = (int32_t)e;
+    }
+    prev_key = cur;
+  }
 }
 
 __global__ void k_fill_outside(uint32_t k_entries, uint32_t n_tiles, uint32_t t0, uint32_t t1,
@@ -319,7 +337,7 @@ void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_til
     cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), stream);
     return;
   }
-  const uint32_t threads = k_entries + 1;
+  const uint32_t threads = k_entries / 4 + 1;
   k_tile_ranges<<<(threads + 255) / 256, 256, 0, stream>>>(k_entries, keys, t0, t1, offsets);
   ++g_launches;
   if (t0 > 0 || t1 < n_tiles) {
