@@ -385,7 +385,9 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   }
   {
     int which = 0;
-    radix_sort_pairs(dk, dv, m, 0, 32, f->sort_tmp.p, &which, s);
+    // The last pass also gathers each rank's tile count (cnt_sorted).
+    radix_sort_pairs(dk, dv, m, 0, 32, f->sort_tmp.p, &which, s, f->cnt.as<uint32_t>(),
+                     f->cnt_sorted.as<uint32_t>());
     f->depth_which = swapped ? 1 - which : which;  // index into f->vals / f->keys
   }
   delete depth_scope;
@@ -393,7 +395,6 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   const uint32_t* sorted_idx = f->vals[f->depth_which].as<uint32_t>();
   {
     StageScope sc(ctx, ODGS_STAGE_SCAN);
-    launch_gather_counts(m, sorted_idx, f->cnt.as<uint32_t>(), f->cnt_sorted.as<uint32_t>(), s);
     exclusive_scan_u32(f->cnt_sorted.as<uint32_t>(), f->off_sorted.as<uint32_t>(), m, f->scan_tmp.p,
                        &ctx->d_err->n_entries, s);
   }

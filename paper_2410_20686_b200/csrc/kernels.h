@@ -36,9 +36,6 @@ void launch_band_flags(int64_t n, const uint32_t* cnt, uint32_t* flags, cudaStre
 // scan of the flags).
 void launch_compact_pairs(int64_t n, const uint32_t* flags, const uint32_t* pos, const uint32_t* keys_in,
                           const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream);
-void launch_gather_counts(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt, uint32_t* cnt_sorted,
-                          cudaStream_t stream);
-
 struct EmitArgs {
   int64_t n;
   const uint32_t *sorted_idx, *cnt_sorted, *off_sorted;
@@ -83,8 +80,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
 size_t radix_sort_temp_bytes(int64_t n);
 // Stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit).
 // keys/vals: [2] ping-pong buffers of n each; on return *which (0/1) holds the result.
+// Optional payload gather: gather_dst[r] = gather_src[sorted value r], written by the
+// last pass (saves a separate gather over the sorted values).
 void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
-                      int* which, cudaStream_t stream);
+                      int* which, cudaStream_t stream, const uint32_t* gather_src = nullptr,
+                      uint32_t* gather_dst = nullptr);
 
 // ------------------------------------------------------------------ training step
 size_t l1_loss_temp_bytes(int64_t count);

@@ -196,20 +196,6 @@ void launch_compact_pairs(int64_t n, const uint32_t* flags, const uint32_t* pos,
   ++g_launches;
 }
 
-// ------------------------------------------------------------------ gather counts into rank order
-__global__ void k_gather_counts(int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt,
-                                uint32_t* __restrict__ cnt_sorted) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) cnt_sorted[r] = cnt[sorted_idx[r]];
-}
-
-void launch_gather_counts(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt, uint32_t* cnt_sorted,
-                          cudaStream_t stream) {
-  if (n == 0) return;
-  k_gather_counts<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, sorted_idx, cnt, cnt_sorted);
-  ++g_launches;
-}
-
 // ------------------------------------------------------------------ emit tile entries
 constexpr int kEmitWarps = 8;
 

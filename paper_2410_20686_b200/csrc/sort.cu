@@ -156,7 +156,8 @@ __global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
 __global__ void __launch_bounds__(kThreads, 3) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ digit_start,
-    uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter) {
+    uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
+    uint32_t* __restrict__ gather_dst) {
   __shared__ uint32_t s_keys[kTile];
   __shared__ uint32_t s_vals[kTile];
   __shared__ uint32_t s_wcnt[kWarps][256];
@@ -255,12 +256,20 @@ __global__ void __launch_bounds__(kThreads, 3) k_onesweep_pass(
     const uint32_t kk = s_keys[k];
     const uint32_t d = (kk >> shift) & mask;
     const uint32_t pos = s_gbase[d] + (uint32_t)k;
+    const uint32_t v = s_vals[k];
     keys_out[pos] = kk;
-    vals_out[pos] = s_vals[k];
+    vals_out[pos] = v;
+    if (gather_dst) gather_dst[pos] = gather_src[v];  // last pass: payload in sorted order
   }
 }
 
 int64_t blocks_for(int64_t n) { return (n + kTile - 1) / kTile; }
+
+__global__ void k_gather(int64_t n, const uint32_t* __restrict__ idx, const uint32_t* __restrict__ src,
+                         uint32_t* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
 
 }  // namespace
 
@@ -298,9 +307,15 @@ size_t radix_sort_temp_bytes(int64_t n) {
 }
 
 void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
-                      int* which, cudaStream_t stream) {
+                      int* which, cudaStream_t stream, const uint32_t* gather_src, uint32_t* gather_dst) {
   *which = 0;
-  if (n <= 1 || end_bit <= begin_bit) return;
+  if (n <= 1 || end_bit <= begin_bit) {
+    if (gather_dst && n > 0) {
+      k_gather<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, vals[0], gather_src, gather_dst);
+      ++g_launches;
+    }
+    return;
+  }
   PassPlan plan{};
   int passes = (end_bit - begin_bit + 7) / 8;
   if (passes > kMaxPasses) passes = kMaxPasses;
@@ -326,7 +341,8 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
     cudaMemsetAsync(status, 0, (size_t)nb * 256 * sizeof(uint32_t), stream);
     k_onesweep_pass<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
                                                            plan.shift[p], plan.bits[p], hist + p * 256, status,
-                                                           counters + p);
+                                                           counters + p, p == passes - 1 ? gather_src : nullptr,
+                                                           p == passes - 1 ? gather_dst : nullptr);
     ++g_launches;
     cur ^= 1;
   }
