@@ -453,15 +453,27 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     r0, r1 = rank * rows, (rank + 1) * rows
     settings = RenderSettings()
     fr = RenderOutput(ctx)
-    gathered = torch.empty((world, 3, W, rows), dtype=torch.float32, device=dev) if world > 1 else None
+    # The all-gather of the bands is fused into the blend: each rank's blend writes its
+    # rows straight into every rank's full-image buffer over NVLink (CUDA IPC peer
+    # pointers, paper_2410_20686_b200/peers.py); one barrier then completes the frame.
+    # Should the peer set-up fail, NCCL's all_gather is the fallback.
+    gather, gathered, collective = None, None, "none"
+    if world > 1:
+        try:
+            from paper_2410_20686_b200.peers import BandGather
+            gather = BandGather(ctx, fr, W, H, dev)
+            collective = "fused: blend writes its band into every rank's image over NVLink (CUDA IPC), 1 barrier"
+        except Exception as e:  # noqa: BLE001 — reported in the JSON line
+            gathered = torch.empty((world, 3, W, rows), dtype=torch.float32, device=dev)
+            collective = f"NCCL all_gather of the band images (peer set-up failed: {type(e).__name__})"
 
     def frame(k):
         render_band(ctx, cloud, scenes.yaw_camera(2 * math.pi * k / 16, W, H), settings, r0, r1, out=fr)
-        ptr = fr.device_ptr(capi.FRAME_IMAGE)
-        band = _device_view(ptr, 3 * W * H, dev).view(3, W, H)[:, :, r0:r1].contiguous()
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, band)
-        return band
+        if gather is not None:
+            gather.sync(local_rank)
+        elif gathered is not None:
+            band = _device_view(fr.device_ptr(capi.FRAME_IMAGE), 3 * W * H, dev).view(3, W, H)[:, :, r0:r1]
+            dist.all_gather_into_tensor(gathered, band.contiguous())
 
     for k in range(2):
         frame(k)
@@ -488,7 +500,7 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     out = {"metric": "ERP frames/sec (C5: 10M Gaussians, 4096x2048, row bands over the GPUs)",
            "value": steps / (ms_max / 1000.0), "unit": "frames/s", "ms_per_frame": ms_max / steps,
            "bands": world, "rows_per_band": rows, "n_gpus": world, "scaling": "strong",
-           "collective": "NCCL all_gather of the band images" if world > 1 else "none",
+           "collective": collective,
            "band_tile_entries_rank0": info.n_entries, "stage_ms_per_frame_rank0": stages}
     if world == 1:
         # Each of the 8 bands an 8-GPU run would give one rank, rendered alone on this GPU
@@ -508,6 +520,8 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
             band_ms.append(e0.elapsed_time(e1) / 3)
         out["bands8_single_gpu_ms"] = [round(v, 4) for v in band_ms]
         out["bands8_slowest_band_fps"] = 1000.0 / max(band_ms)
+    if gather is not None:
+        gather.close()
     fr.destroy()
     return out
 

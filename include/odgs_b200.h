@@ -199,6 +199,20 @@ odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, voi
    and entries composited. Synchronizes. */
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_examined,
                             int64_t* entries_composited);
+/* Row bands over several GPUs: the blend also writes every pixel it
+   renders into each of these n <= 8 image buffers ([3][W][H] float, the frame's
+   layout) — typically the other ranks' full-image buffers opened with odgs_ipc_open —
+   so a band render all-gathers its rows over NVLink as it produces them. Pointers stay
+   in effect for later renders into this frame; n = 0 clears them. Not with
+   ODGS_FRAME_PLAIN_BLEND. The caller synchronises the ranks before reading. */
+odgs_status odgs_frame_set_image_peers(odgs_frame* frame, int32_t n, void* const* peer_images);
+
+/* CUDA IPC (one process per GPU on a node): export a device allocation, open a peer's. */
+#define ODGS_IPC_HANDLE_BYTES 64
+odgs_status odgs_ipc_get_handle(const void* device_ptr, void* handle);
+odgs_status odgs_ipc_open(const void* handle, void** device_ptr);
+odgs_status odgs_ipc_close(void* device_ptr);
+
 /* Device pointer of a resident field (IMAGE, TRANSMITTANCE, WALKED, TILE_OFFSETS). */
 odgs_status odgs_frame_device_ptr(odgs_frame* frame, int field, void** device_ptr);
 

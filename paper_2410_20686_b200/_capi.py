@@ -26,6 +26,8 @@ FRAME_KEEP_SPLAT_GRADS = 0x4
  FRAME_SPLAT_CLAMPED, FRAME_SPLATGRAD_MEAN, FRAME_SPLATGRAD_COV2D, FRAME_SPLATGRAD_OPACITY,
  FRAME_SPLATGRAD_COLOR) = range(20)
 
+IPC_HANDLE_BYTES = 64
+
 STATUS_OK = 0
 STATUS_INVALID_ARGUMENT = 1
 STATUS_RUNTIME = 2
@@ -148,6 +150,10 @@ SIGNATURES = {
     "odgs_save_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(Cloud64)]),
     "odgs_load_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(Cloud64)]),
     "odgs_init_from_points": (C.c_int, [_P, C.c_int64, _P, _P, C.c_int32, C.POINTER(Cloud64), _P]),
+    "odgs_frame_set_image_peers": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "odgs_ipc_get_handle": (C.c_int, [_P, _P]),
+    "odgs_ipc_open": (C.c_int, [_P, C.POINTER(_P)]),
+    "odgs_ipc_close": (C.c_int, [_P]),
     "odgs_cull": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.c_float, C.c_float,
                             C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }

@@ -73,6 +73,7 @@ struct odgs_frame {
   DevBuf ekeys[2], evals[2], offsets, tile_order, image, trans, walked, records, touched, folded, splat_grads, work;
   int depth_which = 0, tile_which = 0;
   int64_t n_sorted = 0;  // depth-sorted ranks: n, or the band's Gaussians (band compaction)
+  PeerImages peers{};    // odgs_frame_set_image_peers
   DevCamera cam{};
   DevSettings settings{};
 };
@@ -493,6 +494,7 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ba.walked = f->walked.as<int32_t>();
   ba.work = f->work.as<unsigned long long>();
   ba.order = f->tile_order.as<uint32_t>();
+  ba.peers = f->peers;
   ba.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
   {
     StageScope sc(ctx, ODGS_STAGE_BLEND);
@@ -676,6 +678,40 @@ void odgs_frame_destroy(odgs_frame* f) {
   for (DevBuf* b : bufs) release(*b, s);
   cudaStreamSynchronize(s);
   delete f;
+}
+
+odgs_status odgs_frame_set_image_peers(odgs_frame* f, int32_t n, void* const* peer_images) {
+  if (!f || n < 0 || n > kMaxPeers || (n > 0 && !peer_images)) return ODGS_ERR_INVALID_ARGUMENT;
+  if (n > 0 && (f->flags & ODGS_FRAME_PLAIN_BLEND)) return ODGS_ERR_INVALID_ARGUMENT;
+  f->peers = PeerImages{};
+  for (int k = 0; k < n; ++k) {
+    if (!peer_images[k]) return ODGS_ERR_INVALID_ARGUMENT;
+    f->peers.ptr[k] = static_cast<float*>(peer_images[k]);
+  }
+  f->peers.n = n;
+  return ODGS_OK;
+}
+
+odgs_status odgs_ipc_get_handle(const void* device_ptr, void* handle) {
+  if (!device_ptr || !handle) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)) != cudaSuccess) return ODGS_ERR_CUDA;
+  static_assert(sizeof(h) == ODGS_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  std::memcpy(handle, &h, sizeof h);
+  return ODGS_OK;
+}
+
+odgs_status odgs_ipc_open(const void* handle, void** device_ptr) {
+  if (!handle || !device_ptr) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  if (cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return ODGS_ERR_CUDA;
+  return ODGS_OK;
+}
+
+odgs_status odgs_ipc_close(void* device_ptr) {
+  if (!device_ptr) return ODGS_ERR_INVALID_ARGUMENT;
+  return cudaIpcCloseMemHandle(device_ptr) == cudaSuccess ? ODGS_OK : ODGS_ERR_CUDA;
 }
 
 odgs_status odgs_frame_set_flags(odgs_frame* f, uint32_t flags) {

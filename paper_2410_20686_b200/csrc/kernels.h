@@ -52,6 +52,15 @@ void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, flo
 void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, uint32_t t0, uint32_t t1,
                         int32_t* offsets, cudaStream_t stream);
 
+// Peer image buffers ([3][W][H], the frame's layout) that the blend epilogue also writes
+// its pixels to: an all-gather of row bands fused into the kernel that produces them
+// (stores over NVLink to other GPUs' memory, opened with CUDA IPC).
+constexpr int kMaxPeers = 8;
+struct PeerImages {
+  float* ptr[kMaxPeers];
+  int n;
+};
+
 struct BlendArgs {
   const int32_t* offsets;
   const uint32_t* vals;
@@ -63,6 +72,7 @@ struct BlendArgs {
   int32_t* walked;
   unsigned long long* work;  // [2] += entries examined, entries composited (or null)
   const uint32_t* order;     // launch order of the band's tiles (launch_tile_order) or null
+  PeerImages peers;          // also write the image to these buffers (n = 0: none)
   bool plain;                // force the un-culled reference kernel (A/B checks)
 };
 // order[k] = band-relative tile index of the k-th CTA: tiles by descending list length.

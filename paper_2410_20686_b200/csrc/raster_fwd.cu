@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
     int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base,
-    const uint32_t* __restrict__ order) {
+    const uint32_t* __restrict__ order, PeerImages peers) {
   constexpr int kWarps = kBlendThreads / 32;
   // One 48-byte record per staged entry: the walk addresses all three parts from one
   // base with immediate offsets (separate arrays cost an address computation each).
@@ -666,6 +666,12 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     image[2 * plane + p] = cb;
     trans_out[p] = t;
     walked_out[p] = walked;
+    for (int k = 0; k < peers.n; ++k) {  // fused all-gather: the same pixel into every peer's image
+      float* q = peers.ptr[k];
+      q[p] = cr;
+      q[plane + p] = cg;
+      q[2 * plane + p] = cb;
+    }
   }
 }
 
@@ -678,7 +684,7 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
     kern<<<n_band_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,
                                                       a.tile_size, a.tiles_x, a.alpha_clamp, a.transmittance_floor,
                                                       cutoff2, a.image, a.transmittance, a.walked, a.work,
-                                                      a.band_ty0 * a.tiles_x, a.order);
+                                                      a.band_ty0 * a.tiles_x, a.order, a.peers);
     ++g_launches;
     return;
   }

@@ -245,6 +245,14 @@ class RenderOutput:
         self.ctx.check(self.ctx.lib.odgs_frame_work(self.ctx.handle, self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def set_image_peers(self, ptrs) -> None:
+        """odgs_frame_set_image_peers: the blend also writes each rendered pixel into
+        these [3][W][H] float device buffers (fused band all-gather)."""
+        arr = (C.c_void_p * max(len(ptrs), 1))(*[C.c_void_p(int(p)) for p in ptrs])
+        st = self.ctx.lib.odgs_frame_set_image_peers(self.handle, len(ptrs), arr)
+        if st != capi.STATUS_OK:
+            raise InvalidArgument(f"odgs_frame_set_image_peers failed ({st})")
+
     def device_ptr(self, fld: int) -> int:
         p = C.c_void_p()
         self.ctx.check(self.ctx.lib.odgs_frame_device_ptr(self.handle, fld, C.byref(p)))

@@ -69,3 +69,113 @@ def test_band_without_gaussians_is_empty(gpu_ctx):
     assert np.array_equal(fr.image[:, :, 0:16], full.image[:, :, 0:16])
     assert np.all(fr.image[:, :, 0:16] == 0) and np.all(fr.transmittance[:, 0:16] == 1)
     assert np.all(fr.walked[:, 0:16] == 0)
+
+
+def test_band_renders_write_peer_images(gpu_ctx):
+    """odgs_frame_set_image_peers: every band render also writes its rows into the peer
+    buffers, so after all bands each peer holds the full frame, bit for bit."""
+    import torch
+    from paper_2410_20686_b200 import RenderOutput
+    c = scenes.cloud_c3(100_000)
+    cam = CameraPose(1024, 512)
+    s = RenderSettings()
+    full = render(gpu_ctx, c, cam, s).image
+    peers = [torch.full((3 * 1024 * 512,), float("nan"), device="cuda") for _ in range(2)]
+    fr = RenderOutput(gpu_ctx)
+    fr.set_image_peers([p.data_ptr() for p in peers])
+    for r0 in range(0, 512, 128):
+        render_band(gpu_ctx, c, cam, s, r0, r0 + 128, out=fr)
+    torch.cuda.synchronize()
+    for p in peers:
+        assert np.array_equal(p.cpu().numpy().reshape(3, 1024, 512), full)
+    fr.set_image_peers([])
+    with pytest.raises(InvalidArgument):
+        fr.set_image_peers([0] * 9)
+
+
+def _ipc_child(handle, q):
+    try:
+        import torch
+        from paper_2410_20686_b200 import Context, RenderOutput, RenderSettings, render_band, scenes
+        from paper_2410_20686_b200.peers import ipc_open
+        ctx = Context(0)
+        ptr = ipc_open(ctx.lib, handle)
+        fr = RenderOutput(ctx)
+        fr.set_image_peers([ptr])
+        render_band(ctx, scenes.cloud_c3(20_000), CameraPose(512, 256), RenderSettings(), 64, 192, out=fr)
+        ctx.synchronize()
+        fr.set_image_peers([])
+        ctx.lib.odgs_ipc_close(__import__("ctypes").c_void_p(ptr))
+        q.put("ok")
+    except Exception as e:  # reported to the parent
+        q.put(repr(e))
+
+
+def test_band_written_into_another_process_buffer(gpu_ctx):
+    """CUDA IPC path of the fused band all-gather, two processes on one GPU: the child
+    renders rows [64, 192) straight into the parent's buffer."""
+    import multiprocessing as mp
+    import torch
+    from paper_2410_20686_b200.peers import ipc_handle
+    buf = torch.full((3 * 512 * 256,), -1.0, device="cuda")
+    torch.cuda.synchronize()
+    h = ipc_handle(gpu_ctx.lib, buf.data_ptr())
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    p = ctx_mp.Process(target=_ipc_child, args=(h, q))
+    p.start()
+    msg = q.get(timeout=300)
+    p.join(timeout=60)
+    assert msg == "ok", msg
+    ref = render(gpu_ctx, scenes.cloud_c3(20_000), CameraPose(512, 256), RenderSettings()).image
+    got = buf.cpu().numpy().reshape(3, 512, 256)
+    assert np.array_equal(got[:, :, 64:192], ref[:, :, 64:192])
+    assert np.all(got[:, :, :64] == -1.0) and np.all(got[:, :, 192:] == -1.0)
+
+
+def _gather_rank(rank, world, port, q):
+    try:
+        import os
+        import torch
+        import torch.distributed as dist
+        from paper_2410_20686_b200 import Context, RenderOutput, RenderSettings, render_band, scenes
+        from paper_2410_20686_b200.peers import BandGather
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ctx = Context(0)
+        fr = RenderOutput(ctx)
+        W, H = 512, 256
+        g = BandGather(ctx, fr, W, H, torch.device("cuda", 0))
+        rows = H // world
+        render_band(ctx, scenes.cloud_c3(20_000), CameraPose(W, H), RenderSettings(), rank * rows, (rank + 1) * rows,
+                    out=fr)
+        g.sync(0)
+        q.put((rank, g.full.cpu().numpy()))
+        dist.barrier()
+        g.close()
+        dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+def test_band_gather_two_ranks_on_one_gpu(gpu_ctx):
+    """BandGather end to end with two ranks (gloo for the handle exchange, both on GPU 0):
+    each renders half of the rows into both ranks' full images; both end up with the
+    whole frame."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    procs = [ctx_mp.Process(target=_gather_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    ref = render(gpu_ctx, scenes.cloud_c3(20_000), CameraPose(512, 256), RenderSettings()).image
+    for r in range(2):
+        assert not isinstance(res[r], str), res[r]
+        assert np.array_equal(res[r].reshape(3, 512, 256), ref), r
