@@ -355,6 +355,18 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   pa.err = ctx->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_PREPROCESS);
+    if (f->settings.band_ty0 > 0 || f->settings.band_ty1 < f->tiles_y) {
+      // Band pre-cull, then the exact projection on the compacted survivors only
+      // (flags / positions / list reuse buffers that are free until the depth sort).
+      uint32_t* keep = f->cnt_sorted.as<uint32_t>();
+      uint32_t* pos = f->off_sorted.as<uint32_t>();
+      uint32_t* list = f->ent_off_idx.as<uint32_t>();
+      launch_band_precull(pa, keep, s);
+      exclusive_scan_u32(keep, pos, n, f->scan_tmp.p, &ctx->d_err->n_precull, s);
+      launch_list_flagged(n, keep, pos, list, s);
+      pa.list = list;
+      pa.list_len = &ctx->d_err->n_precull;
+    }
     launch_preprocess(pa, s);
   }
 
@@ -603,6 +615,7 @@ odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out) {
   ctx->h_err_init->n_visible = 0;
   ctx->h_err_init->n_instances = 0;
   ctx->h_err_init->n_band = 0;
+  ctx->h_err_init->n_precull = 0;
   *out = ctx;
   return ODGS_OK;
 }

@@ -28,6 +28,7 @@ struct DevErrors {
   unsigned long long n_visible;    // projected splats (RenderOutput::splats.size())
   unsigned long long n_instances;  // seam instances (RenderOutput::instances.size())
   unsigned long long n_band;       // band renders: Gaussians with entries in the band
+  unsigned long long n_precull;    // band renders: pre-cull survivors
 };
 constexpr unsigned long long kNoError = ~0ull;
 

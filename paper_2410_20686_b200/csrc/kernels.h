@@ -27,8 +27,14 @@ struct PreprocessArgs {
   uint32_t* vals;  // [n] iota
   uint32_t* cnt;   // [n] tile entries of the Gaussian
   DevErrors* err;
+  const uint32_t* list = nullptr;                 // band pre-cull survivors (null: all n)
+  const unsigned long long* list_len = nullptr;  // device count of `list`
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
+// Row-band renders: conservative pre-cull (keep[i] = 0 -> culled outputs written).
+void launch_band_precull(const PreprocessArgs& a, uint32_t* keep, cudaStream_t stream);
+// list[pos[i]] = i for flagged i (pos = exclusive scan of flags).
+void launch_list_flagged(int64_t n, const uint32_t* flags, const uint32_t* pos, uint32_t* list, cudaStream_t stream);
 
 // Band renders: flags[i] = (cnt[i] > 0), the Gaussians that emit entries into the band.
 void launch_band_flags(int64_t n, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream);

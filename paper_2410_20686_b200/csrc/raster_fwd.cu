@@ -138,13 +138,18 @@ __global__ void __launch_bounds__(256) k_preprocess(
     const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
     float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
     uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, int sh_degree,
-    const float* __restrict__ sh_rest) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const float* __restrict__ sh_rest, const uint32_t* __restrict__ list,
+    const unsigned long long* __restrict__ list_len) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool visible = false;
   uint32_t n_inst = 0;
-  if (i < n)
+  // list: the band pre-cull's survivors (the others already hold their culled outputs).
+  const int64_t m = list ? (int64_t)*list_len : n;
+  if (t < m) {
+    const int64_t i = list ? (int64_t)list[t] : t;
     n_inst = preprocess_one(i, n, means, rotations, log_scales, raw_opacities, colors, sh_degree, sh_rest, cam, s,
                             sp_ab, sp_c, cov_out, keys, vals, cnt, err, &visible);
+  }
   const uint32_t v_sum = __reduce_add_sync(0xffffffffu, visible ? 1u : 0u);
   const uint32_t i_sum = __reduce_add_sync(0xffffffffu, n_inst);
   if ((threadIdx.x & 31) == 0 && (v_sum | i_sum)) {
@@ -159,7 +164,79 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   const int64_t grid = (a.n + block - 1) / block;
   k_preprocess<<<(unsigned)grid, block, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
                                                      a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
-                                                     a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest);
+                                                     a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest, a.list, a.list_len);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ band pre-cull
+// Row-band renders: a conservative float test finds the Gaussians whose instance boxes
+// certainly miss the band's pixel rows; they get the culled outputs here and skip the
+// exact projection (binary64 transcendentals), which then runs only on the compacted
+// survivors. The box half-height is at most cutoff * sqrt(lambda_max(Sigma_2D)) <=
+// cutoff * sqrt(s_max^2 ||J||_F^2 + lowpass) (Sigma_2D = J R Sigma R^T J^T + lowpass I,
+// lambda_max(Sigma) = s_max^2), with ||J||_F^2 = (W/2pi sec/r)^2 + (H/pi/r)^2
+// (projection.hpp:75-96); the centre row comes from float atan2f/hypotf, whose errors
+// are far inside the 2-pixel margin. Non-finite rows, near-zero quaternions and the
+// zero-direction case survive, so the exact path reports them as before.
+__global__ void __launch_bounds__(256) k_band_precull(int64_t n, const float* __restrict__ means,
+                                                      const float* __restrict__ rotations,
+                                                      const float* __restrict__ log_scales, DevCamera cam,
+                                                      DevSettings s, float4* __restrict__ sp_c,
+                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                      uint32_t* __restrict__ cnt, uint32_t* __restrict__ keep) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float p[3] = {__ldg(means + i), __ldg(means + n + i), __ldg(means + 2 * n + i)};
+  const float q[4] = {__ldg(rotations + i), __ldg(rotations + n + i), __ldg(rotations + 2 * n + i),
+                      __ldg(rotations + 3 * n + i)};
+  const float ls[3] = {__ldg(log_scales + i), __ldg(log_scales + n + i), __ldg(log_scales + 2 * n + i)};
+  bool survive = true;
+  float mu[3];
+  to_camera(cam, p, mu);
+  const float sq = sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]);
+  const float depth = sqrtf(sq);
+  const float qq = sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]);
+  if (sq > 0.0f && qq > 1e-20f && isfinite(depth)) {
+    if (!(depth >= s.near_radius && depth <= s.far_radius)) {
+      survive = false;  // shell-culled: the exact path would produce the same culled outputs
+    } else {
+      const float Wf = (float)cam.width, Hf = (float)cam.height;
+      const float th = atan2f(-mu[1], hypotf(mu[0], mu[2]));
+      const float v = -Hf / kPiF * th + Hf / 2.0f;
+      const float sec = 1.0f / cosf(fminf(fabsf(th), s.max_elevation));
+      const float a0 = Wf / (2.0f * kPiF) * sec / depth, a1 = Hf / kPiF / depth;
+      const float smax = expf(fmaxf(ls[0], fmaxf(ls[1], ls[2])));
+      const float rb =
+          s.cutoff_sigma * sqrtf(smax * smax * (a0 * a0 + a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
+      const float row0 = (float)(s.band_ty0 * s.tile_size), row1 = (float)(s.band_ty1 * s.tile_size);
+      if (isfinite(rb) && isfinite(v) && (v + rb < row0 || v - rb > row1)) survive = false;
+    }
+  }
+  keep[i] = survive ? 1u : 0u;
+  if (!survive) {
+    keys[i] = kCulledKey;
+    vals[i] = (uint32_t)i;
+    cnt[i] = 0;
+    sp_c[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+  }
+}
+
+__global__ void k_list_flagged(int64_t n, const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos,
+                               uint32_t* __restrict__ list) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flags[i]) list[pos[i]] = (uint32_t)i;
+}
+
+void launch_band_precull(const PreprocessArgs& a, uint32_t* keep, cudaStream_t stream) {
+  if (a.n == 0) return;
+  k_band_precull<<<(unsigned)((a.n + 255) / 256), 256, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.cam,
+                                                                    a.settings, a.sp_c, a.keys, a.vals, a.cnt, keep);
+  ++g_launches;
+}
+
+void launch_list_flagged(int64_t n, const uint32_t* flags, const uint32_t* pos, uint32_t* list, cudaStream_t stream) {
+  if (n == 0) return;
+  k_list_flagged<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, flags, pos, list);
   ++g_launches;
 }
 
