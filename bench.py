@@ -337,6 +337,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         fr2.destroy()
         c2.close()
 
+    aux = run_aux(args, ctx, dev, stream) if rank == 0 and not args.no_train else None
     train = None if args.no_train else run_train(args, ctx, rank, world, local_rank, dev, stream)
     large = None if args.no_large else run_large(args, ctx, rank, world, local_rank, dev, stream)
 
@@ -363,6 +364,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                     "path": f"odgs_render (host cloud, pinned) + odgs_frame_download (pinned), {E2E_LANES} "
                             f"contexts / streams / host threads pipelining frames"},
             "cpu_baseline": cpu,
+            "other_configs": aux,
             "train": train,
             "large_render": large,
             "gpu_launches": launches,
@@ -432,6 +434,56 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream):
             "steps": args.train_steps, "warmup": 2, "views_per_gpu": len(tr.mine), "n_gpus": world,
             "scaling": "strong", "loss": "photometric_loss, lambda_ssim = 0.2 (L1 + SSIM on the GPU)", "collective": "NCCL all-reduce (sum) of 16n+n values",
             "stage_ms_per_step": stages, "first_loss": losses[0], "last_loss": losses[-1]}
+
+
+def run_aux(args, ctx, dev, stream):
+    """The other BASELINE configs on this GPU (device-resident, CUDA events): C1 render
+    throughput (the reference's own test workload, 100K Gaussians at 1024x512) and the C2
+    forward + backward step (500K Gaussians, SH degree 3, 2048x1024)."""
+    import numpy as np
+    import torch
+    from paper_2410_20686_b200 import GaussianCloud, RenderOutput, RenderSettings, backward, render, scenes
+
+    def on_dev(c):
+        d = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        return GaussianCloud(d(c.means), d(c.rotations), d(c.log_scales), d(c.raw_opacities), d(c.colors),
+                             c.sh_degree, d(c.sh_rest))
+
+    def timed(fn, reps):
+        for k in range(2):
+            fn(k)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for k in range(reps):
+            fn(k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    s = RenderSettings()
+    fr = RenderOutput(ctx)
+    c1 = on_dev(scenes.cloud_c1())
+    ms1 = timed(lambda k: render(ctx, c1, scenes.yaw_camera(0.1 * k, 1024, 512), s, out=fr), 20)
+    c2 = on_dev(scenes.cloud_c2())
+    dl = torch.from_numpy(np.random.default_rng(2004).uniform(-1, 1, 3 * 2048 * 1024).astype(np.float32)).to(dev)
+    from paper_2410_20686_b200 import GradBuffers
+    n2 = c2.n
+    z = lambda *sh: torch.zeros(sh, dtype=torch.float32, device=dev)
+    g2 = GradBuffers(z(3, n2), z(4, n2), z(3, n2), z(n2), z(3, n2), z(n2), z(n2),
+                     torch.zeros(n2, dtype=torch.int32, device=dev), z(15, 3, n2))
+
+    def step2(k):
+        cam = scenes.yaw_camera(0.1 * k, 2048, 1024)
+        render(ctx, c2, cam, s, out=fr)
+        backward(ctx, c2, cam, fr, dl, s, grads=g2)
+
+    ms2 = timed(step2, 5)
+    fr.destroy()
+    return {"C1_render": {"workload": "100K Gaussians (default bounds), SH0, 1024x512", "ms": ms1,
+                          "frames_per_s": 1000.0 / ms1},
+            "C2_fwd_bwd": {"workload": "500K Gaussians, SH degree 3, 2048x1024, render + backward", "ms": ms2,
+                           "steps_per_s": 1000.0 / ms2}}
 
 
 def run_large(args, ctx, rank, world, local_rank, dev, stream):

@@ -55,6 +55,15 @@ def cloud_c1() -> GaussianCloud:
     return GaussianCloud(*random_cloud_arrays(77, 100_000))
 
 
+def cloud_c2(n: int = 500_000) -> GaussianCloud:
+    """C2: 500K Gaussians with SH degree 3 (bounds of test_backward.cpp:53-63's fd_cloud:
+    depth [0.8, 10], |elevation| <= 75 deg, opacity [0.1, 0.7], scale r * U[0.001, 0.01];
+    45 SH coefficients N(0, 0.05^2))."""
+    arrs = random_cloud_arrays(2002, n, CloudBounds(0.8, 10.0, math.radians(75.0), 0.1, 0.7, 0.001, 0.01))
+    sh = np.random.default_rng(2003).normal(0.0, 0.05, (15, 3, n)).astype(np.float32)
+    return GaussianCloud(*arrs, sh_degree=3, sh_rest=sh)
+
+
 def cloud_c3(n: int = 1_000_000) -> GaussianCloud:
     """C3: 50% uniform + 25% near the poles + 25% at the azimuth seam."""
     n_u, n_p = n // 2, n // 4
