@@ -196,8 +196,8 @@ odgs_status check_settings(odgs_ctx* ctx, const odgs_settings* s) {
   if (!s) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "settings: null");
   if (s->tile_size <= 0)
     return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "RenderSettings: tile_size must be positive");
-  if (s->tile_size > 64)
-    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "RenderSettings: tile_size > 64 is not supported on the GPU");
+  if (s->tile_size > 1024)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "RenderSettings: tile_size > 1024 is not supported");
   return ODGS_OK;
 }
 

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   __shared__ uint32_t s_pos[kBwdBatch];
   __shared__ float s_part[kBwdWarps][kBwdBatch][kRec];
   __shared__ int s_maxw[kBwdWarps];
+  __shared__ uint8_t s_had[kBwdBatch];  // record already written by an earlier pixel chunk
 
   const int tile = band_ty0 * tiles_x + blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -43,12 +44,15 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   const int area = tile_size * tile_size;
   const int64_t plane = (int64_t)width * height;
 
+  // Tiles larger than PPT * 256 pixels (tile_size > 64) are replayed in pixel chunks;
+  // each chunk's per-entry sums are added to the records the earlier chunks wrote.
+  for (int chunk = 0; chunk < area; chunk += PPT * kBwdThreads) {
   float px[PPT], py[PPT], t[PPT], d0[PPT], d1[PPT], d2v[PPT], suf0[PPT], suf1[PPT], suf2[PPT];
   int wk[PPT];
   int my_max = 0;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    const int lp = tid + q * kBwdThreads;
+    const int lp = chunk + tid + q * kBwdThreads;
     const int lx = lp / tile_size, ly = lp - lx * tile_size;
     const int x = tx * tile_size + lx, y = ty * tile_size + ly;
     const bool valid = lp < area && x < width && y < height;
@@ -175,15 +179,22 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
       }
     }
     __syncthreads();
+    if (chunk > 0) {
+      for (int j = tid; j < count; j += kBwdThreads) s_had[j] = touched[s_pos[j]];
+      __syncthreads();
+    }
     for (int idx = tid; idx < count * kRec; idx += kBwdThreads) {
       const int j = idx / kRec, c = idx - j * kRec;
       float s = 0.0f;
 #pragma unroll
       for (int w = 0; w < kBwdWarps; ++w) s += s_part[w][j][c];
-      records[(int64_t)s_pos[j] * kRec + c] = s;
+      float* r = records + (int64_t)s_pos[j] * kRec + c;
+      *r = (chunk > 0 && s_had[j]) ? *r + s : s;
       if (c == 0) touched[s_pos[j]] = 1;
     }
     __syncthreads();
+  }
+  __syncthreads();  // s_maxw and the shared batch are reused by the next chunk
   }
 }
 

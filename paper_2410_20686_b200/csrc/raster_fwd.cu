@@ -467,15 +467,17 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int e0 = offsets[tile], e1 = offsets[tile + 1];
   const int tid = threadIdx.x;
-
+  const int area = tile_size * tile_size;
+  // Tiles larger than PPT * 256 pixels (tile_size > 64) are blended in pixel chunks,
+  // each walking the tile's list again.
+  for (int chunk = 0; chunk < area; chunk += PPT * kBlendThreads) {
   float px[PPT], py[PPT], t[PPT], cr[PPT], cg[PPT], cb[PPT];
   int walked[PPT];
   bool done[PPT];
   int64_t pix[PPT];
-  const int area = tile_size * tile_size;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    const int lp = tid + q * kBlendThreads;
+    const int lp = chunk + tid + q * kBlendThreads;
     // Column-major pixel order inside the tile so a warp writes runs of y (the
     // images are column-major, y + x*H).
     const int lx = lp / tile_size, ly = lp - lx * tile_size;
@@ -572,6 +574,8 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
     image[2 * plane + pix[q]] = cb[q];
     trans_out[pix[q]] = t[q];
     walked_out[pix[q]] = walked[q];
+  }
+  __syncthreads();  // the next chunk restages the shared batch
   }
 }
 

@@ -58,6 +58,9 @@ CASES = [
     ("dense_512x256", lambda: oracle_lib.random_cloud(139, 3000), CameraPose(512, 256), {"cutoff_sigma": 8.0}),
     ("poles_seam_1024", lambda: oracle_lib.random_cloud(140, 5000, (0.5, 20.0, 1.55, 0.05, 0.95, 0.001, 0.01)),
      CameraPose(1024, 512), {"cutoff_sigma": 8.0}),
+    # tiles above 64 px: replayed in pixel chunks whose per-entry sums add up
+    ("tile96_chunks", lambda: oracle_lib.random_cloud(141, 1500), CameraPose(384, 192),
+     {"cutoff_sigma": 8.0, "tile_size": 96}),
 ]
 
 

@@ -36,6 +36,9 @@ SCENES = [
      {"tile_size": 8, "cutoff_sigma": 8.0}),
     ("tile32", lambda: oracle_lib.random_cloud(405, 500), CameraPose(512, 256), {"tile_size": 32}),
     ("tile20_ragged", lambda: oracle_lib.random_cloud(406, 300), CameraPose(250, 125), {"tile_size": 20}),
+    # tiles above 64 px: blended in 4096-pixel chunks per CTA
+    ("tile80_ragged", lambda: oracle_lib.random_cloud(408, 600), CameraPose(300, 150), {"tile_size": 80}),
+    ("tile128", lambda: oracle_lib.random_cloud(409, 600), CameraPose(512, 256), {"tile_size": 128}),
     ("near_far_shell", lambda: oracle_lib.random_cloud(407, 800), CameraPose(256, 128),
      {"near_radius": 3.0, "far_radius": 12.0}),
 ]
