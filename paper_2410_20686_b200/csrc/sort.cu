@@ -153,7 +153,10 @@ __global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
   hist[p * 256 + d] = off + incl - v;
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_onesweep_pass(
+// MinBlocks: 3 CTAs/SM (80 registers, no spills) for the depth sort; 4 (64 registers,
+// a few spills) for the long tile-entry sorts, where the extra occupancy wins.
+template <int MinBlocks>
+__global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
@@ -339,7 +342,8 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
     cudaMemsetAsync(status, 0, (size_t)nb * 256 * sizeof(uint32_t), stream);
-    k_onesweep_pass<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
+    auto pass = n > ((int64_t)1 << 22) ? k_onesweep_pass<4> : k_onesweep_pass<3>;
+    pass<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
                                                            plan.shift[p], plan.bits[p], hist + p * 256, status,
                                                            counters + p, p == passes - 1 ? gather_src : nullptr,
                                                            p == passes - 1 ? gather_dst : nullptr);
