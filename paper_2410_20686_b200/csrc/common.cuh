@@ -175,12 +175,22 @@ __device__ __forceinline__ float shift_of(int k, int width) {
   return k == 0 ? -(float)width : (k == 1 ? 0.0f : (float)width);
 }
 
+// x / d for 0 <= x < 2^32 / d (box coordinates: 0 <= x < image size), d >= 2, by a
+// multiply-high with m = ceil(2^32 / d): x m / 2^32 = x / d + x e / 2^32 with
+// 0 <= e < 1, and x / 2^32 < 1 / d keeps the floor exact. One integer division per
+// thread (hoisted: d is a kernel argument) instead of one per coordinate.
+__device__ __forceinline__ int div_tile(int x, int d) {
+  if (d == 1) return x;
+  const uint32_t m = 0xFFFFFFFFu / (uint32_t)d + 1u;
+  return (int)__umulhi((uint32_t)x, m);
+}
+
 // Tile span of shift k of a splat (box / tile_size); false if no instance.
 __device__ __forceinline__ bool instance_tiles(float mx, float my, float radius, int k, int width, int height,
                                                int tile_size, int span[4]) {
   int box[4];
   if (!instance_box(mx, my, radius, shift_of(k, width), width, height, box)) return false;
-  for (int q = 0; q < 4; ++q) span[q] = box[q] / tile_size;
+  for (int q = 0; q < 4; ++q) span[q] = div_tile(box[q], tile_size);
   return true;
 }
 
