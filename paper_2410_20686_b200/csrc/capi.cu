@@ -364,8 +364,10 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
       launch_band_precull(pa, keep, s);
       exclusive_scan_u32(keep, pos, n, f->scan_tmp.p, &ctx->d_err->n_precull, s);
       launch_list_flagged(n, keep, pos, list, s);
+      if ((st = read_errors(ctx)) != ODGS_OK) return st;
       pa.list = list;
       pa.list_len = &ctx->d_err->n_precull;
+      pa.list_host_len = (int64_t)ctx->h_err->n_precull;
     }
     launch_preprocess(pa, s);
   }
@@ -384,9 +386,13 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   if (band && n > 0) {
     uint32_t* flags = f->cnt_sorted.as<uint32_t>();  // free until the gather below
     uint32_t* pos = f->off_sorted.as<uint32_t>();
-    launch_band_flags(n, f->cnt.as<uint32_t>(), flags, s);
-    exclusive_scan_u32(flags, pos, n, f->scan_tmp.p, &ctx->d_err->n_band, s);
-    launch_compact_pairs(n, flags, pos, dk[0], dv[0], dk[1], dv[1], s);
+    // Only the pre-cull survivors (ascending, so the compaction stays stable) can
+    // have entries in the band.
+    const uint32_t* list = pa.list;
+    const int64_t rows = list ? pa.list_host_len : n;
+    launch_band_flags(rows, list, f->cnt.as<uint32_t>(), flags, s);
+    exclusive_scan_u32(flags, pos, rows, f->scan_tmp.p, &ctx->d_err->n_band, s);
+    launch_compact_pairs(rows, list, flags, pos, dk[0], dv[0], dk[1], dv[1], s);
     if ((st = read_errors(ctx)) != ODGS_OK) {
       delete depth_scope;
       return st;

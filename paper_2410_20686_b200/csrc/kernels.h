@@ -29,6 +29,7 @@ struct PreprocessArgs {
   DevErrors* err;
   const uint32_t* list = nullptr;                 // band pre-cull survivors (null: all n)
   const unsigned long long* list_len = nullptr;  // device count of `list`
+  int64_t list_host_len = 0;                      // the same count, read back (grid size)
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
 // Row-band renders: conservative pre-cull (keep[i] = 0 -> culled outputs written).
@@ -36,12 +37,14 @@ void launch_band_precull(const PreprocessArgs& a, uint32_t* keep, cudaStream_t s
 // list[pos[i]] = i for flagged i (pos = exclusive scan of flags).
 void launch_list_flagged(int64_t n, const uint32_t* flags, const uint32_t* pos, uint32_t* list, cudaStream_t stream);
 
-// Band renders: flags[i] = (cnt[i] > 0), the Gaussians that emit entries into the band.
-void launch_band_flags(int64_t n, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream);
-// Stable compaction of the flagged (key, value) pairs to the positions pos[i] (exclusive
-// scan of the flags).
-void launch_compact_pairs(int64_t n, const uint32_t* flags, const uint32_t* pos, const uint32_t* keys_in,
-                          const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream);
+// Band renders: flags[t] = (cnt[i] > 0) for i = list[t] (list null: i = t), the
+// Gaussians that emit entries into the band.
+void launch_band_flags(int64_t m, const uint32_t* list, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream);
+// Stable compaction of the flagged (key, value) pairs of rows list[t] to the positions
+// pos[t] (exclusive scan of the flags).
+void launch_compact_pairs(int64_t m, const uint32_t* list, const uint32_t* flags, const uint32_t* pos,
+                          const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out,
+                          cudaStream_t stream);
 struct EmitArgs {
   int64_t n;
   const uint32_t *sorted_idx, *cnt_sorted, *off_sorted;

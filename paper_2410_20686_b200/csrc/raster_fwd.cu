@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(256) k_preprocess(
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   if (a.n == 0) return;
   const int block = 256;
-  const int64_t grid = (a.n + block - 1) / block;
+  const int64_t rows = a.list ? a.list_host_len : a.n;
+  if (rows == 0) return;
+  const int64_t grid = (rows + block - 1) / block;
   k_preprocess<<<(unsigned)grid, block, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
                                                      a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
                                                      a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest, a.list, a.list_len);
@@ -244,31 +246,37 @@ void launch_list_flagged(int64_t n, const uint32_t* flags, const uint32_t* pos, 
 // A band render only needs the Gaussians that emit entries into its tile rows; the
 // others are dropped before the depth sort (their relative order is irrelevant: they
 // appear in no tile list of the band).
-__global__ void k_band_flags(int64_t n, const uint32_t* __restrict__ cnt, uint32_t* __restrict__ flags) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) flags[i] = cnt[i] > 0 ? 1u : 0u;
+// `list` (optional, ascending): the pre-cull survivors; the scan then runs over the m
+// survivors instead of all n Gaussians.
+__global__ void k_band_flags(int64_t m, const uint32_t* __restrict__ list, const uint32_t* __restrict__ cnt,
+                             uint32_t* __restrict__ flags) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) flags[t] = cnt[list ? list[t] : t] > 0 ? 1u : 0u;
 }
 
-__global__ void k_compact_pairs(int64_t n, const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos,
-                                const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && flags[i]) {
-    keys_out[pos[i]] = keys_in[i];
-    vals_out[pos[i]] = vals_in[i];
+__global__ void k_compact_pairs(int64_t m, const uint32_t* __restrict__ list, const uint32_t* __restrict__ flags,
+                                const uint32_t* __restrict__ pos, const uint32_t* __restrict__ keys_in,
+                                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+                                uint32_t* __restrict__ vals_out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m && flags[t]) {
+    const int64_t i = list ? (int64_t)list[t] : t;
+    keys_out[pos[t]] = keys_in[i];
+    vals_out[pos[t]] = vals_in[i];
   }
 }
 
-void launch_band_flags(int64_t n, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream) {
-  if (n == 0) return;
-  k_band_flags<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, cnt, flags);
+void launch_band_flags(int64_t m, const uint32_t* list, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream) {
+  if (m == 0) return;
+  k_band_flags<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(m, list, cnt, flags);
   ++g_launches;
 }
 
-void launch_compact_pairs(int64_t n, const uint32_t* flags, const uint32_t* pos, const uint32_t* keys_in,
-                          const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream) {
-  if (n == 0) return;
-  k_compact_pairs<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, flags, pos, keys_in, vals_in, keys_out,
+void launch_compact_pairs(int64_t m, const uint32_t* list, const uint32_t* flags, const uint32_t* pos,
+                          const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out,
+                          cudaStream_t stream) {
+  if (m == 0) return;
+  k_compact_pairs<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(m, list, flags, pos, keys_in, vals_in, keys_out,
                                                                     vals_out);
   ++g_launches;
 }
