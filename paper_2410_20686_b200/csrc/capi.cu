@@ -335,6 +335,7 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   ODGS_CUDA(ctx, ensure(f->offsets, sizeof(int32_t) * (n_tiles + 1), s));
   if ((st = reset_errors(ctx)) != ODGS_OK) return st;
 
+  const bool band = f->settings.band_ty0 > 0 || f->settings.band_ty1 < f->tiles_y;
   PreprocessArgs pa;
   pa.n = n;
   pa.means = cp.means;
@@ -355,59 +356,44 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   pa.err = ctx->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_PREPROCESS);
-    if (f->settings.band_ty0 > 0 || f->settings.band_ty1 < f->tiles_y) {
-      // Band pre-cull, then the exact projection on the compacted survivors only
-      // (flags / positions / list reuse buffers that are free until the depth sort).
-      uint32_t* keep = f->cnt_sorted.as<uint32_t>();
-      uint32_t* pos = f->off_sorted.as<uint32_t>();
-      uint32_t* list = f->ent_off_idx.as<uint32_t>();
-      launch_band_precull(pa, keep, s);
-      exclusive_scan_u32(keep, pos, n, f->scan_tmp.p, &ctx->d_err->n_precull, s);
-      launch_list_flagged(n, keep, pos, list, s);
-      if ((st = read_errors(ctx)) != ODGS_OK) return st;
-      pa.list = list;
-      pa.list_len = &ctx->d_err->n_precull;
-      pa.list_host_len = (int64_t)ctx->h_err->n_precull;
+    if (band) {
+      // Pre-cull, exact projection of the survivors and compaction of the Gaussians
+      // with entries in the band, in one pass (per-warp segments in keys[1] / vals[1],
+      // segment lengths / offsets in cnt_sorted / off_sorted, free until the gather).
+      uint32_t* seg_count = f->cnt_sorted.as<uint32_t>();
+      uint32_t* seg_off = f->off_sorted.as<uint32_t>();
+      launch_band_preprocess(pa, f->keys[1].as<uint32_t>(), f->vals[1].as<uint32_t>(), seg_count, s);
+      const int64_t n_seg = band_segments(n);
+      exclusive_scan_u32(seg_count, seg_off, n_seg, f->scan_tmp.p, &ctx->d_err->n_band, s);
+      launch_concat_segments(n, seg_count, seg_off, f->keys[1].as<uint32_t>(), f->vals[1].as<uint32_t>(),
+                             f->keys[0].as<uint32_t>(), f->vals[0].as<uint32_t>(), s);
+    } else {
+      launch_preprocess(pa, s);
     }
-    launch_preprocess(pa, s);
   }
 
   // Depth sort of the Gaussians (key: depth bits; culled sort last). A band render
-  // first compacts the Gaussians with entries in its rows (stable, so ties keep index
-  // order) and sorts only those: the tile lists are unchanged, the sort shrinks with
-  // the band (row bands over 8 GPUs sort ~1/8 of the cloud each).
-  const bool band = f->settings.band_ty0 > 0 || f->settings.band_ty1 < f->tiles_y;
+  // sorts only the Gaussians with entries in its rows, compacted in index order above
+  // (stable, so ties keep index order): the tile lists are unchanged, the sort shrinks
+  // with the band (row bands over 8 GPUs sort ~1/8 of the cloud each).
   ODGS_CUDA(ctx, ensure(f->sort_tmp, std::max(radix_sort_temp_bytes(n), (size_t)16), s));
   uint32_t* dk[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
   uint32_t* dv[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
   int64_t m = n;
-  bool swapped = false;
   StageScope* depth_scope = new StageScope(ctx, ODGS_STAGE_DEPTH_SORT);
   if (band && n > 0) {
-    uint32_t* flags = f->cnt_sorted.as<uint32_t>();  // free until the gather below
-    uint32_t* pos = f->off_sorted.as<uint32_t>();
-    // Only the pre-cull survivors (ascending, so the compaction stays stable) can
-    // have entries in the band.
-    const uint32_t* list = pa.list;
-    const int64_t rows = list ? pa.list_host_len : n;
-    launch_band_flags(rows, list, f->cnt.as<uint32_t>(), flags, s);
-    exclusive_scan_u32(flags, pos, rows, f->scan_tmp.p, &ctx->d_err->n_band, s);
-    launch_compact_pairs(rows, list, flags, pos, dk[0], dv[0], dk[1], dv[1], s);
     if ((st = read_errors(ctx)) != ODGS_OK) {
       delete depth_scope;
       return st;
     }
     m = (int64_t)ctx->h_err->n_band;
-    std::swap(dk[0], dk[1]);
-    std::swap(dv[0], dv[1]);
-    swapped = true;
   }
   {
     int which = 0;
     // The last pass also gathers each rank's tile count (cnt_sorted).
     radix_sort_pairs(dk, dv, m, 0, 32, f->sort_tmp.p, &which, s, f->cnt.as<uint32_t>(),
                      f->cnt_sorted.as<uint32_t>());
-    f->depth_which = swapped ? 1 - which : which;  // index into f->vals / f->keys
+    f->depth_which = which;  // index into f->vals / f->keys
   }
   delete depth_scope;
   f->n_sorted = m;

@@ -27,24 +27,17 @@ struct PreprocessArgs {
   uint32_t* vals;  // [n] iota
   uint32_t* cnt;   // [n] tile entries of the Gaussian
   DevErrors* err;
-  const uint32_t* list = nullptr;                 // band pre-cull survivors (null: all n)
-  const unsigned long long* list_len = nullptr;  // device count of `list`
-  int64_t list_host_len = 0;                      // the same count, read back (grid size)
 };
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
-// Row-band renders: conservative pre-cull (keep[i] = 0 -> culled outputs written).
-void launch_band_precull(const PreprocessArgs& a, uint32_t* keep, cudaStream_t stream);
-// list[pos[i]] = i for flagged i (pos = exclusive scan of flags).
-void launch_list_flagged(int64_t n, const uint32_t* flags, const uint32_t* pos, uint32_t* list, cudaStream_t stream);
-
-// Band renders: flags[t] = (cnt[i] > 0) for i = list[t] (list null: i = t), the
-// Gaussians that emit entries into the band.
-void launch_band_flags(int64_t m, const uint32_t* list, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream);
-// Stable compaction of the flagged (key, value) pairs of rows list[t] to the positions
-// pos[t] (exclusive scan of the flags).
-void launch_compact_pairs(int64_t m, const uint32_t* list, const uint32_t* flags, const uint32_t* pos,
-                          const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out,
-                          cudaStream_t stream);
+// Fused band path: pre-cull + exact preprocess of the survivors + compaction of the
+// Gaussians with band entries into per-warp segments (segment w at w * chunk,
+// seg_count[w] pairs; band_segments(n) segments).
+int64_t band_segments(int64_t n);
+void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_t* seg_vals, uint32_t* seg_count,
+                            cudaStream_t stream);
+// Concatenates the segments at seg_off (exclusive scan of seg_count).
+void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t* seg_off, const uint32_t* seg_keys,
+                            const uint32_t* seg_vals, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream);
 struct EmitArgs {
   int64_t n;
   const uint32_t *sorted_idx, *cnt_sorted, *off_sorted;

@@ -138,16 +138,12 @@ __global__ void __launch_bounds__(256) k_preprocess(
     const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
     float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
     uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, int sh_degree,
-    const float* __restrict__ sh_rest, const uint32_t* __restrict__ list,
-    const unsigned long long* __restrict__ list_len) {
+    const float* __restrict__ sh_rest) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool visible = false;
   uint32_t n_inst = 0;
-  // list: the band pre-cull's survivors (the others already hold their culled outputs).
-  const int64_t m = list ? (int64_t)*list_len : n;
-  if (t < m) {
-    const int64_t i = list ? (int64_t)list[t] : t;
-    n_inst = preprocess_one(i, n, means, rotations, log_scales, raw_opacities, colors, sh_degree, sh_rest, cam, s,
+  if (t < n) {
+    n_inst = preprocess_one(t, n, means, rotations, log_scales, raw_opacities, colors, sh_degree, sh_rest, cam, s,
                             sp_ab, sp_c, cov_out, keys, vals, cnt, err, &visible);
   }
   const uint32_t v_sum = __reduce_add_sync(0xffffffffu, visible ? 1u : 0u);
@@ -161,123 +157,209 @@ __global__ void __launch_bounds__(256) k_preprocess(
 void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   if (a.n == 0) return;
   const int block = 256;
-  const int64_t rows = a.list ? a.list_host_len : a.n;
-  if (rows == 0) return;
-  const int64_t grid = (rows + block - 1) / block;
+  const int64_t grid = (a.n + block - 1) / block;
   k_preprocess<<<(unsigned)grid, block, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
                                                      a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
-                                                     a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest, a.list, a.list_len);
+                                                     a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest);
   ++g_launches;
 }
 
 // ------------------------------------------------------------------ band pre-cull
 // Row-band renders: a conservative float test finds the Gaussians whose instance boxes
-// certainly miss the band's pixel rows; they get the culled outputs here and skip the
-// exact projection (binary64 transcendentals), which then runs only on the compacted
-// survivors. The box half-height is at most cutoff * sqrt(lambda_max(Sigma_2D)) <=
-// cutoff * sqrt(s_max^2 ||J||_F^2 + lowpass) (Sigma_2D = J R Sigma R^T J^T + lowpass I,
+// certainly miss the band's pixel rows; they get the culled outputs and skip the exact
+// projection (binary64 transcendentals), which then runs only on the survivors. The box
+// half-height is at most rb = cutoff * sqrt(lambda_max(Sigma_2D)) <= cutoff *
+// sqrt(s_max^2 ||J||_F^2 + lowpass) (Sigma_2D = J R Sigma R^T J^T + lowpass I,
 // lambda_max(Sigma) = s_max^2), with ||J||_F^2 = (W/2pi sec/r)^2 + (H/pi/r)^2
-// (projection.hpp:75-96); the centre row comes from float atan2f/hypotf, whose errors
-// are far inside the 2-pixel margin. Non-finite rows, near-zero quaternions and the
-// zero-direction case survive, so the exact path reports them as before.
-__global__ void __launch_bounds__(256) k_band_precull(int64_t n, const float* __restrict__ means,
-                                                      const float* __restrict__ rotations,
-                                                      const float* __restrict__ log_scales, DevCamera cam,
-                                                      DevSettings s, float4* __restrict__ sp_c,
-                                                      uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                      uint32_t* __restrict__ cnt, uint32_t* __restrict__ keep) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// (projection.hpp:75-96), padded by 1% and 2 pixels. The test runs in the sine domain,
+// with no inverse trigonometry: the centre row v = H/2 - H theta/pi lies above the band
+// by more than rb iff theta > theta_top + rb pi/H iff sin(theta) = -mu_y/|mu| > sin(that)
+// (both angles inside (-pi/2, pi/2)), likewise below. The fast-math errors (~1e-6 rad)
+// are far inside the padding; angles within 0.01 rad of a pole are never culled (sine is
+// flat there). Non-finite rows, near-zero quaternions and the zero-direction case survive,
+// so the exact path reports them as before.
+struct BandCull {
+  float sin_top, cos_top, sin_bot, cos_bot;  // band edge angles (top: row0, bottom: row1)
+  float top, bot;                            // the angles themselves
+  float sec_max;                             // 1 / cos(max_elevation)
+  float a0k, a1k, rad_per_px;                // W / 2pi, H / pi, pi / H
+};
+
+__device__ __forceinline__ BandCull make_band_cull(const DevCamera& cam, const DevSettings& s) {
+  BandCull b;
+  const float Hf = (float)cam.height;
+  b.top = (Hf / 2.0f - (float)(s.band_ty0 * s.tile_size)) * kPiF / Hf;
+  b.bot = (Hf / 2.0f - (float)(s.band_ty1 * s.tile_size)) * kPiF / Hf;
+  sincosf(b.top, &b.sin_top, &b.cos_top);
+  sincosf(b.bot, &b.sin_bot, &b.cos_bot);
+  b.sec_max = 1.0f / cosf(s.max_elevation);
+  b.a0k = (float)cam.width / (2.0f * kPiF);
+  b.a1k = Hf / kPiF;
+  b.rad_per_px = kPiF / Hf;
+  return b;
+}
+
+__device__ __forceinline__ bool band_survives(int64_t i, int64_t n, const float* __restrict__ means,
+                                              const float* __restrict__ rotations,
+                                              const float* __restrict__ log_scales, const DevCamera& cam,
+                                              const DevSettings& s, const BandCull& b) {
   const float p[3] = {__ldg(means + i), __ldg(means + n + i), __ldg(means + 2 * n + i)};
   const float q[4] = {__ldg(rotations + i), __ldg(rotations + n + i), __ldg(rotations + 2 * n + i),
                       __ldg(rotations + 3 * n + i)};
   const float ls[3] = {__ldg(log_scales + i), __ldg(log_scales + n + i), __ldg(log_scales + 2 * n + i)};
-  bool survive = true;
   float mu[3];
   to_camera(cam, p, mu);
   const float sq = sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]);
   const float depth = sqrtf(sq);
   const float qq = sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]);
-  if (sq > 0.0f && qq > 1e-20f && isfinite(depth)) {
-    if (!(depth >= s.near_radius && depth <= s.far_radius)) {
-      survive = false;  // shell-culled: the exact path would produce the same culled outputs
-    } else {
-      const float Wf = (float)cam.width, Hf = (float)cam.height;
-      const float th = atan2f(-mu[1], hypotf(mu[0], mu[2]));
-      const float v = -Hf / kPiF * th + Hf / 2.0f;
-      const float sec = 1.0f / cosf(fminf(fabsf(th), s.max_elevation));
-      const float a0 = Wf / (2.0f * kPiF) * sec / depth, a1 = Hf / kPiF / depth;
-      const float smax = expf(fmaxf(ls[0], fmaxf(ls[1], ls[2])));
-      const float rb =
-          s.cutoff_sigma * sqrtf(smax * smax * (a0 * a0 + a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
-      const float row0 = (float)(s.band_ty0 * s.tile_size), row1 = (float)(s.band_ty1 * s.tile_size);
-      if (isfinite(rb) && isfinite(v) && (v + rb < row0 || v - rb > row1)) survive = false;
+  if (!(sq > 0.0f && qq > 1e-20f && isfinite(depth))) return true;
+  // shell-culled: the exact path would produce the same culled outputs
+  if (!(depth >= s.near_radius && depth <= s.far_radius)) return false;
+  const float inv_d = 1.0f / depth;
+  const float rho = sqrtf(mu[0] * mu[0] + mu[2] * mu[2]);
+  const float sin_th = -mu[1] * inv_d;
+  const float sec = fminf(depth / rho, b.sec_max);  // rho = 0: +inf -> sec_max
+  const float a0 = b.a0k * sec * inv_d, a1 = b.a1k * inv_d;
+  const float smax = __expf(fmaxf(ls[0], fmaxf(ls[1], ls[2])));
+  const float rb = s.cutoff_sigma * sqrtf(smax * smax * (a0 * a0 + a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
+  const float rt = rb * b.rad_per_px;
+  if (!(rt < 1.0f)) return true;  // also non-finite rb
+  float sr, cr;
+  __sincosf(rt, &sr, &cr);
+  constexpr float kPoleGuard = 1.5607963f;  // pi/2 - 0.01
+  // above: theta > top + rt
+  if (b.top + rt < kPoleGuard && sin_th > b.sin_top * cr + b.cos_top * sr) return false;
+  // below: theta < bot - rt
+  if (b.bot - rt > -kPoleGuard && sin_th < b.sin_bot * cr - b.cos_bot * sr) return false;
+  return true;
+}
+
+// Fused band pre-cull + exact preprocess + band compaction, one warp per chunk of
+// kBandWarpChunk consecutive Gaussians. The warp streams its chunk with coalesced loads,
+// queues the pre-cull survivors in shared memory and projects them 32 at a time (full
+// warps, instead of one scattered gather per survivor), then appends the (depth key,
+// index) pairs of those with entries in the band, in index order, to its own segment
+// of seg_keys / seg_vals; seg_count[warp] is the segment length. Culled Gaussians get
+// the culled per-Gaussian outputs (cnt 0, sp_c 0); their keys / vals are not written
+// (only the compacted pairs are sorted).
+constexpr int kBandWarpChunk = 2048;
+constexpr int kBandUnroll = 4;
+constexpr int kBandQueue = 256;  // >= 31 + 32 * kBandUnroll, a power of two
+
+__global__ void __launch_bounds__(256, 3) k_band_preprocess(
+    int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
+    const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
+    const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
+    float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, int sh_degree,
+    const float* __restrict__ sh_rest, uint32_t* __restrict__ seg_keys, uint32_t* __restrict__ seg_vals,
+    uint32_t* __restrict__ seg_count) {
+  __shared__ uint32_t s_queue[8][kBandQueue];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t base = w * kBandWarpChunk;
+  if (base >= n) return;
+  const int64_t end = min(base + (int64_t)kBandWarpChunk, n);
+  uint32_t* q = s_queue[warp];  // ring buffer of survivor indices
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t head = 0, tail = 0;
+  uint32_t out_len = 0, n_surv = 0, n_vis = 0, n_inst = 0;
+  const BandCull bc = make_band_cull(cam, s);
+  // Projects the next `count` queued survivors (one per lane) and appends the pairs
+  // with band entries.
+  auto drain = [&](uint32_t count) {
+    bool visible = false, has = false;
+    uint32_t key = 0, idx = 0;
+    if (lane < count) {
+      idx = q[(head + lane) & (kBandQueue - 1)];
+      n_inst += preprocess_one(idx, n, means, rotations, log_scales, raw_opacities, colors, sh_degree, sh_rest, cam,
+                               s, sp_ab, sp_c, cov_out, keys, vals, cnt, err, &visible);
+      has = cnt[idx] > 0;
+      key = keys[idx];
     }
+    head += count;
+    n_vis += visible ? 1u : 0u;
+    const uint32_t hb = __ballot_sync(0xffffffffu, has);
+    if (has) {
+      const int64_t o = base + out_len + __popc(hb & lt);
+      seg_keys[o] = key;
+      seg_vals[o] = idx;
+    }
+    out_len += __popc(hb);
+  };
+  // The pre-cull streams kBandUnroll groups of 32 at a time (independent loads in
+  // flight), then the queue drains in full warps.
+  for (int64_t c = base; c < end; c += 32 * kBandUnroll) {
+    bool sv[kBandUnroll];
+#pragma unroll
+    for (int u = 0; u < kBandUnroll; ++u) {
+      const int64_t i = c + u * 32 + lane;
+      // clamped index: unconditional loads, all kBandUnroll groups in flight
+      sv[u] = band_survives(min(i, end - 1), n, means, rotations, log_scales, cam, s, bc) && i < end;
+    }
+#pragma unroll
+    for (int u = 0; u < kBandUnroll; ++u) {
+      const int64_t i = c + u * 32 + lane;
+      if (i < end && !sv[u]) {
+        cnt[i] = 0;
+        sp_c[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+      }
+      const uint32_t sb = __ballot_sync(0xffffffffu, sv[u]);
+      if (sv[u]) q[(tail + __popc(sb & lt)) & (kBandQueue - 1)] = (uint32_t)i;
+      tail += __popc(sb);
+      n_surv += __popc(sb);
+    }
+    __syncwarp();
+    while (tail - head >= 32) drain(32);
+    __syncwarp();
   }
-  keep[i] = survive ? 1u : 0u;
-  if (!survive) {
-    keys[i] = kCulledKey;
-    vals[i] = (uint32_t)i;
-    cnt[i] = 0;
-    sp_c[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+  if (tail != head) drain(tail - head);
+  const uint32_t vis = __reduce_add_sync(0xffffffffu, n_vis);
+  const uint32_t inst = __reduce_add_sync(0xffffffffu, n_inst);
+  if (lane == 0) {
+    seg_count[w] = out_len;
+    if (vis | inst) {
+      atomicAdd(&err->n_visible, (unsigned long long)vis);
+      atomicAdd(&err->n_instances, (unsigned long long)inst);
+    }
+    if (n_surv) atomicAdd(&err->n_precull, (unsigned long long)n_surv);
   }
 }
 
-__global__ void k_list_flagged(int64_t n, const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos,
-                               uint32_t* __restrict__ list) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && flags[i]) list[pos[i]] = (uint32_t)i;
+// Concatenates the warp segments (one warp per segment) at their scanned offsets.
+__global__ void k_concat_segments(int64_t n_seg, const uint32_t* __restrict__ seg_count,
+                                  const uint32_t* __restrict__ seg_off, const uint32_t* __restrict__ seg_keys,
+                                  const uint32_t* __restrict__ seg_vals, uint32_t* __restrict__ keys_out,
+                                  uint32_t* __restrict__ vals_out) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_seg) return;
+  const uint32_t len = seg_count[w], off = seg_off[w];
+  const int64_t src = w * kBandWarpChunk;
+  for (uint32_t k = lane; k < len; k += 32) {
+    keys_out[off + k] = seg_keys[src + k];
+    vals_out[off + k] = seg_vals[src + k];
+  }
 }
 
-void launch_band_precull(const PreprocessArgs& a, uint32_t* keep, cudaStream_t stream) {
+int64_t band_segments(int64_t n) { return (n + kBandWarpChunk - 1) / kBandWarpChunk; }
+
+void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_t* seg_vals, uint32_t* seg_count,
+                            cudaStream_t stream) {
   if (a.n == 0) return;
-  k_band_precull<<<(unsigned)((a.n + 255) / 256), 256, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.cam,
-                                                                    a.settings, a.sp_c, a.keys, a.vals, a.cnt, keep);
+  const int64_t n_seg = band_segments(a.n);
+  k_band_preprocess<<<(unsigned)((n_seg + 7) / 8), 256, 0, stream>>>(
+      a.n, a.means, a.rotations, a.log_scales, a.raw_opacities, a.colors, a.cam, a.settings, a.sp_ab, a.sp_c,
+      a.cov_out, a.keys, a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest, seg_keys, seg_vals, seg_count);
   ++g_launches;
 }
 
-void launch_list_flagged(int64_t n, const uint32_t* flags, const uint32_t* pos, uint32_t* list, cudaStream_t stream) {
-  if (n == 0) return;
-  k_list_flagged<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, flags, pos, list);
-  ++g_launches;
-}
-
-// ------------------------------------------------------------------ band compaction
-// A band render only needs the Gaussians that emit entries into its tile rows; the
-// others are dropped before the depth sort (their relative order is irrelevant: they
-// appear in no tile list of the band).
-// `list` (optional, ascending): the pre-cull survivors; the scan then runs over the m
-// survivors instead of all n Gaussians.
-__global__ void k_band_flags(int64_t m, const uint32_t* __restrict__ list, const uint32_t* __restrict__ cnt,
-                             uint32_t* __restrict__ flags) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < m) flags[t] = cnt[list ? list[t] : t] > 0 ? 1u : 0u;
-}
-
-__global__ void k_compact_pairs(int64_t m, const uint32_t* __restrict__ list, const uint32_t* __restrict__ flags,
-                                const uint32_t* __restrict__ pos, const uint32_t* __restrict__ keys_in,
-                                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-                                uint32_t* __restrict__ vals_out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < m && flags[t]) {
-    const int64_t i = list ? (int64_t)list[t] : t;
-    keys_out[pos[t]] = keys_in[i];
-    vals_out[pos[t]] = vals_in[i];
-  }
-}
-
-void launch_band_flags(int64_t m, const uint32_t* list, const uint32_t* cnt, uint32_t* flags, cudaStream_t stream) {
-  if (m == 0) return;
-  k_band_flags<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(m, list, cnt, flags);
-  ++g_launches;
-}
-
-void launch_compact_pairs(int64_t m, const uint32_t* list, const uint32_t* flags, const uint32_t* pos,
-                          const uint32_t* keys_in, const uint32_t* vals_in, uint32_t* keys_out, uint32_t* vals_out,
-                          cudaStream_t stream) {
-  if (m == 0) return;
-  k_compact_pairs<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(m, list, flags, pos, keys_in, vals_in, keys_out,
-                                                                    vals_out);
+void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t* seg_off, const uint32_t* seg_keys,
+                            const uint32_t* seg_vals, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream) {
+  const int64_t n_seg = band_segments(n);
+  if (n_seg == 0) return;
+  k_concat_segments<<<(unsigned)((n_seg * 32 + 255) / 256), 256, 0, stream>>>(n_seg, seg_count, seg_off, seg_keys,
+                                                                               seg_vals, keys_out, vals_out);
   ++g_launches;
 }
 

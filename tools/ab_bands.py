@@ -31,4 +31,5 @@ for b in range(8):
     e1.record()
     torch.cuda.synchronize()
     ms.append(e0.elapsed_time(e1) / reps)
+print("splats per band", [frs[b].info().n_splats for b in range(8)])
 print("bands ms", [round(v, 3) for v in ms], "mean", round(sum(ms) / 8, 4), "max", round(max(ms), 4))
