@@ -114,6 +114,7 @@ constexpr uint32_t kStatAgg = 1u << 30;
 constexpr uint32_t kStatPrefix = 2u << 30;
 constexpr uint32_t kStatMask = (1u << 30) - 1u;
 constexpr int kMaxPasses = 4;
+constexpr int kLookWindow = 8;
 
 struct PassPlan {
   int n_passes;
@@ -221,29 +222,16 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
   __syncthreads();
   uint32_t woff = 0;
   for (int w = 0; w < warp; ++w) woff += s_wsum[w];
-  if (threadIdx.x < radix) {
-    const int d = threadIdx.x;
-    const uint32_t start = woff + incl - digit_total;
-    s_start[d] = start;
-    const uint32_t real = (d == radix - 1) ? digit_total - (uint32_t)(kTile - valid_count) : digit_total;
-    // Publish, then look back over the predecessors for this digit's exclusive prefix.
-    volatile uint32_t* st = status;
-    if (tile == 0) {
-      st[d] = kStatPrefix | real;
-      s_gbase[d] = digit_start[d] - start;
-    } else {
-      st[(int64_t)tile * 256 + d] = kStatAgg | real;
-      uint32_t excl = 0;
-      for (int look = tile - 1; look >= 0;) {
-        const uint32_t w = st[(int64_t)look * 256 + d];
-        if ((w & ~kStatMask) == 0) continue;  // predecessor not published yet: spin
-        excl += w & kStatMask;
-        if (w & kStatPrefix) break;
-        --look;
-      }
-      st[(int64_t)tile * 256 + d] = kStatPrefix | (excl + real);
-      s_gbase[d] = digit_start[d] + excl - start;
-    }
+  // Publish this tile's per-digit counts first, so successors can look back past it
+  // while it scatters into shared memory.
+  const int d_own = threadIdx.x;
+  uint32_t start = 0, real = 0;
+  volatile uint32_t* st = status;
+  if (d_own < radix) {
+    start = woff + incl - digit_total;
+    s_start[d_own] = start;
+    real = (d_own == radix - 1) ? digit_total - (uint32_t)(kTile - valid_count) : digit_total;
+    st[(int64_t)tile * 256 + d_own] = (tile == 0 ? kStatPrefix : kStatAgg) | real;
   }
   __syncthreads();
 #pragma unroll
@@ -253,6 +241,37 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
     const uint32_t pos = s_start[d] + s_wcnt[warp][d] + rank[j];
     s_keys[pos] = key[j];
     s_vals[pos] = val[j];
+  }
+  if (d_own < radix) {
+    const int d = d_own;
+    if (tile == 0) {
+      s_gbase[d] = digit_start[d] - start;
+    } else {
+      // Windowed look-back: kLookWindow predecessors' words are loaded together (one
+      // round trip per window instead of per tile), then consumed newest first up to
+      // the first prefix; an unpublished word restarts the window there.
+      uint32_t excl = 0;
+      for (int look = tile - 1; look >= 0;) {
+        uint32_t w[kLookWindow];
+#pragma unroll
+        for (int j = 0; j < kLookWindow; ++j)
+          w[j] = look - j >= 0 ? st[(int64_t)(look - j) * 256 + d] : (uint32_t)kStatPrefix;
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < kLookWindow; ++j) {
+          if ((w[j] & ~kStatMask) == 0) break;  // predecessor not published yet: spin here
+          excl += w[j] & kStatMask;
+          --look;
+          if (w[j] & kStatPrefix) {
+            done = true;
+            break;
+          }
+        }
+        if (done) break;
+      }
+      st[(int64_t)tile * 256 + d] = kStatPrefix | (excl + real);
+      s_gbase[d] = digit_start[d] + excl - start;
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < valid_count; k += kThreads) {
