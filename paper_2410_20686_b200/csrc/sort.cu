@@ -156,10 +156,11 @@ __global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
 
 // MinBlocks: 3 CTAs/SM (80 registers, no spills) for the depth sort; 4 (64 registers,
 // a few spills) for the long tile-entry sorts, where the extra occupancy wins.
-template <int MinBlocks>
+// Bits: the digit width (a template argument, so the ranking's ballot loop unrolls).
+template <int MinBlocks, int Bits>
 __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-    uint32_t* __restrict__ vals_out, int64_t n, int shift, int bits, const uint32_t* __restrict__ digit_start,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
     uint32_t* __restrict__ gather_dst) {
   __shared__ uint32_t s_keys[kTile];
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
   __shared__ uint32_t s_wsum[kWarps];
   __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int radix = 1 << bits;
-  const uint32_t mask = (uint32_t)radix - 1u;
+  constexpr int radix = 1 << Bits;
+  constexpr uint32_t mask = (uint32_t)radix - 1u;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
   for (int k = threadIdx.x; k < kWarps * 256; k += kThreads) (&s_wcnt[0][0])[k] = 0;
   __syncthreads();
@@ -193,7 +194,8 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
     const bool valid = idx < n;
     const uint32_t d = valid ? (key[j] >> shift) & mask : mask;
     uint32_t peers = 0xffffffffu;
-    for (int b = 0; b < bits; ++b) {
+#pragma unroll
+    for (int b = 0; b < Bits; ++b) {
       const uint32_t bit = (d >> b) & 1u;
       const uint32_t bal = __ballot_sync(0xffffffffu, bit);
       peers &= bit ? bal : ~bal;
@@ -361,11 +363,21 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
     cudaMemsetAsync(status, 0, (size_t)nb * 256 * sizeof(uint32_t), stream);
-    auto pass = n > ((int64_t)1 << 22) ? k_onesweep_pass<4> : k_onesweep_pass<3>;
+    const bool big = n > ((int64_t)1 << 22);
+    decltype(&k_onesweep_pass<3, 8>) pass = nullptr;
+    switch (plan.bits[p]) {
+#define ODGS_PASS_CASE(B) \
+  case B:                 \
+    pass = big ? k_onesweep_pass<4, B> : k_onesweep_pass<3, B>; \
+    break;
+      ODGS_PASS_CASE(1) ODGS_PASS_CASE(2) ODGS_PASS_CASE(3) ODGS_PASS_CASE(4)
+      ODGS_PASS_CASE(5) ODGS_PASS_CASE(6) ODGS_PASS_CASE(7) ODGS_PASS_CASE(8)
+#undef ODGS_PASS_CASE
+    }
     pass<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
-                                                           plan.shift[p], plan.bits[p], hist + p * 256, status,
-                                                           counters + p, p == passes - 1 ? gather_src : nullptr,
-                                                           p == passes - 1 ? gather_dst : nullptr);
+                                                plan.shift[p], hist + p * 256, status, counters + p,
+                                                p == passes - 1 ? gather_src : nullptr,
+                                                p == passes - 1 ? gather_dst : nullptr);
     ++g_launches;
     cur ^= 1;
   }
