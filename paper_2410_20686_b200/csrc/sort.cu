@@ -25,6 +25,33 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kIPT = 16;
 constexpr int kTile = kThreads * kIPT;  // 4096
 constexpr int kWarpItems = 32 * kIPT;   // 512
+#ifndef ODGS_SORT_BIG_THREADS
+#define ODGS_SORT_BIG_THREADS 384
+#endif
+#ifndef ODGS_SORT_BIG_MINB
+#define ODGS_SORT_BIG_MINB 2
+#endif
+#ifndef ODGS_SORT_BIG_IPT
+#define ODGS_SORT_BIG_IPT 16
+#endif
+constexpr int kBigThreads = ODGS_SORT_BIG_THREADS;  // tile-entry sorts (n > 2^22)
+constexpr int kBigMinBlocks = ODGS_SORT_BIG_MINB;
+constexpr int kBigIPT = ODGS_SORT_BIG_IPT;
+#ifndef ODGS_SORT_SMALL_IPT
+#define ODGS_SORT_SMALL_IPT 16
+#endif
+#ifndef ODGS_SORT_SMALL_MINB
+#define ODGS_SORT_SMALL_MINB 3
+#endif
+constexpr int kSmallIPT = ODGS_SORT_SMALL_IPT;  // depth sorts (n <= 2^22), 256 threads
+constexpr int kSmallMinBlocks = ODGS_SORT_SMALL_MINB;
+constexpr int64_t kBigSort = (int64_t)1 << 22;  // n above this: the tile-entry sort shape
+
+// Onesweep tiles of a sort of n pairs.
+int64_t pass_tiles(int64_t n) {
+  const int64_t t = n > kBigSort ? kBigThreads * kBigIPT : kThreads * kSmallIPT;
+  return (n + t - 1) / t;
+}
 
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t v, int lane) {
 #pragma unroll
@@ -114,7 +141,10 @@ constexpr uint32_t kStatAgg = 1u << 30;
 constexpr uint32_t kStatPrefix = 2u << 30;
 constexpr uint32_t kStatMask = (1u << 30) - 1u;
 constexpr int kMaxPasses = 4;
-constexpr int kLookWindow = 8;
+#ifndef ODGS_SORT_LOOK_WINDOW
+#define ODGS_SORT_LOOK_WINDOW 8
+#endif
+constexpr int kLookWindow = ODGS_SORT_LOOK_WINDOW;
 
 struct PassPlan {
   int n_passes;
@@ -154,42 +184,47 @@ __global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
   hist[p * 256 + d] = off + incl - v;
 }
 
-// MinBlocks: 3 CTAs/SM (80 registers, no spills) for the depth sort; 4 (64 registers,
-// a few spills) for the long tile-entry sorts, where the extra occupancy wins.
+// Threads x IPT items per tile (shared memory: keys + values + per-warp digit counts,
+// dynamic). MinBlocks: 3 CTAs/SM (80 registers, no spills) for the depth sort; more
+// occupancy (a few spills) for the long tile-entry sorts, where it wins.
 // Bits: the digit width (a template argument, so the ranking's ballot loop unrolls).
-template <int MinBlocks, int Bits>
-__global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
+template <int Threads, int IPT, int MinBlocks, int Bits>
+__global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
     uint32_t* __restrict__ gather_dst) {
-  __shared__ uint32_t s_keys[kTile];
-  __shared__ uint32_t s_vals[kTile];
-  __shared__ uint32_t s_wcnt[kWarps][256];
+  constexpr int kW = Threads / 32;
+  constexpr int kT = Threads * IPT;
+  constexpr int kWI = 32 * IPT;
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_keys = s_dyn;                     // [kT]
+  uint32_t* s_vals = s_dyn + kT;                // [kT]
+  uint32_t(*s_wcnt)[256] = reinterpret_cast<uint32_t(*)[256]>(s_dyn + 2 * kT);  // [kW][256]
   __shared__ uint32_t s_start[256];
   __shared__ uint32_t s_gbase[256];
-  __shared__ uint32_t s_wsum[kWarps];
+  __shared__ uint32_t s_wsum[kW];
   __shared__ int s_tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int radix = 1 << Bits;
   constexpr uint32_t mask = (uint32_t)radix - 1u;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
-  for (int k = threadIdx.x; k < kWarps * 256; k += kThreads) (&s_wcnt[0][0])[k] = 0;
+  for (int k = threadIdx.x; k < kW * 256; k += Threads) (&s_wcnt[0][0])[k] = 0;
   __syncthreads();
   const int tile = s_tile;
-  const int64_t tile_base = (int64_t)tile * kTile;
-  const int64_t base = tile_base + (int64_t)warp * kWarpItems;
+  const int64_t tile_base = (int64_t)tile * kT;
+  const int64_t base = tile_base + (int64_t)warp * kWI;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  uint32_t key[kIPT], val[kIPT], rank[kIPT];
-  // All loads first, so the tile's 32 loads per thread are in flight together.
+  uint32_t key[IPT], val[IPT], rank[IPT];
+  // All loads first, so the tile's loads per thread are in flight together.
 #pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
+  for (int j = 0; j < IPT; ++j) {
     const int64_t idx = base + j * 32 + lane;
     key[j] = idx < n ? __ldcs(keys_in + idx) : 0u;
     val[j] = idx < n ? __ldcs(vals_in + idx) : 0u;
   }
 #pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
+  for (int j = 0; j < IPT; ++j) {
     const int64_t idx = base + j * 32 + lane;
     const bool valid = idx < n;
     const uint32_t d = valid ? (key[j] >> shift) & mask : mask;
@@ -209,11 +244,11 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
   __syncthreads();
   // Per-digit tile totals (padding excluded: it sits in the last digit, after every
   // real item, so subtract it from that digit's count).
-  const int64_t valid_count = n - tile_base < kTile ? n - tile_base : kTile;
+  const int64_t valid_count = n - tile_base < kT ? n - tile_base : kT;
   uint32_t digit_total = 0;
   if (threadIdx.x < radix) {
     const int d = threadIdx.x;
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < kW; ++w) {
       const uint32_t c = s_wcnt[w][d];
       s_wcnt[w][d] = digit_total;
       digit_total += c;
@@ -232,12 +267,12 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
   if (d_own < radix) {
     start = woff + incl - digit_total;
     s_start[d_own] = start;
-    real = (d_own == radix - 1) ? digit_total - (uint32_t)(kTile - valid_count) : digit_total;
+    real = (d_own == radix - 1) ? digit_total - (uint32_t)(kT - valid_count) : digit_total;
     st[(int64_t)tile * 256 + d_own] = (tile == 0 ? kStatPrefix : kStatAgg) | real;
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < kIPT; ++j) {
+  for (int j = 0; j < IPT; ++j) {
     const int64_t idx = base + j * 32 + lane;
     const uint32_t d = idx < n ? (key[j] >> shift) & mask : mask;
     const uint32_t pos = s_start[d] + s_wcnt[warp][d] + rank[j];
@@ -276,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocks) k_onesweep_pass(
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < valid_count; k += kThreads) {
+  for (int k = threadIdx.x; k < valid_count; k += Threads) {
     const uint32_t kk = s_keys[k];
     const uint32_t d = (kk >> shift) & mask;
     const uint32_t pos = s_gbase[d] + (uint32_t)k;
@@ -325,10 +360,56 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
 }
 
 size_t radix_sort_temp_bytes(int64_t n) {
-  const int64_t nb = blocks_for(n > 0 ? n : 1);
+  const int64_t nb = pass_tiles(n > 0 ? n : 1);
   // hist [kMaxPasses][256] + status [nb][256] + tile counters [kMaxPasses] (+ alignment)
   return (size_t)(kMaxPasses * 256 + nb * 256 + kMaxPasses + 64) * sizeof(uint32_t);
 }
+
+namespace {
+
+
+struct PassArgs {
+  const uint32_t *keys_in, *vals_in;
+  uint32_t *keys_out, *vals_out;
+  int64_t n;
+  int shift;
+  const uint32_t* digit_start;
+  uint32_t *status, *tile_counter;
+  const uint32_t* gather_src;
+  uint32_t* gather_dst;
+};
+
+template <int Threads, int IPT, int MinBlocks, int Bits>
+void launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
+  constexpr int kT = Threads * IPT;
+  constexpr size_t smem = (size_t)(2 * kT + (Threads / 32) * 256) * sizeof(uint32_t);
+  auto kern = k_onesweep_pass<Threads, IPT, MinBlocks, Bits>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int64_t tiles = (a.n + kT - 1) / kT;
+  kern<<<(unsigned)tiles, Threads, smem, stream>>>(a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n, a.shift,
+                                                   a.digit_start, a.status, a.tile_counter, a.gather_src,
+                                                   a.gather_dst);
+}
+
+template <int Threads, int IPT, int MinBlocks>
+void launch_pass(int bits, const PassArgs& a, cudaStream_t stream) {
+  switch (bits) {
+    case 1: launch_pass_bits<Threads, IPT, MinBlocks, 1>(a, stream); break;
+    case 2: launch_pass_bits<Threads, IPT, MinBlocks, 2>(a, stream); break;
+    case 3: launch_pass_bits<Threads, IPT, MinBlocks, 3>(a, stream); break;
+    case 4: launch_pass_bits<Threads, IPT, MinBlocks, 4>(a, stream); break;
+    case 5: launch_pass_bits<Threads, IPT, MinBlocks, 5>(a, stream); break;
+    case 6: launch_pass_bits<Threads, IPT, MinBlocks, 6>(a, stream); break;
+    case 7: launch_pass_bits<Threads, IPT, MinBlocks, 7>(a, stream); break;
+    default: launch_pass_bits<Threads, IPT, MinBlocks, 8>(a, stream); break;
+  }
+}
+
+}  // namespace
 
 void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
                       int* which, cudaStream_t stream, const uint32_t* gather_src, uint32_t* gather_dst) {
@@ -360,24 +441,16 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   ++g_launches;
   k_onesweep_hist_scan<<<passes, 256, 0, stream>>>(hist);
   ++g_launches;
+  const bool big = n > kBigSort;
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
-    cudaMemsetAsync(status, 0, (size_t)nb * 256 * sizeof(uint32_t), stream);
-    const bool big = n > ((int64_t)1 << 22);
-    decltype(&k_onesweep_pass<3, 8>) pass = nullptr;
-    switch (plan.bits[p]) {
-#define ODGS_PASS_CASE(B) \
-  case B:                 \
-    pass = big ? k_onesweep_pass<4, B> : k_onesweep_pass<3, B>; \
-    break;
-      ODGS_PASS_CASE(1) ODGS_PASS_CASE(2) ODGS_PASS_CASE(3) ODGS_PASS_CASE(4)
-      ODGS_PASS_CASE(5) ODGS_PASS_CASE(6) ODGS_PASS_CASE(7) ODGS_PASS_CASE(8)
-#undef ODGS_PASS_CASE
-    }
-    pass<<<(unsigned)nb, kThreads, 0, stream>>>(keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n,
-                                                plan.shift[p], hist + p * 256, status, counters + p,
-                                                p == passes - 1 ? gather_src : nullptr,
-                                                p == passes - 1 ? gather_dst : nullptr);
+    cudaMemsetAsync(status, 0, (size_t)pass_tiles(n) * 256 * sizeof(uint32_t), stream);
+    PassArgs pa{keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, plan.shift[p], hist + p * 256, status,
+                counters + p, p == passes - 1 ? gather_src : nullptr, p == passes - 1 ? gather_dst : nullptr};
+    if (big)
+      launch_pass<kBigThreads, kBigIPT, kBigMinBlocks>(plan.bits[p], pa, stream);
+    else
+      launch_pass<kThreads, kSmallIPT, kSmallMinBlocks>(plan.bits[p], pa, stream);
     ++g_launches;
     cur ^= 1;
   }
