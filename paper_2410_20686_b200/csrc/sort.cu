@@ -153,7 +153,11 @@ struct PassPlan {
 };
 
 __global__ void __launch_bounds__(kThreads) k_onesweep_hist(const uint32_t* __restrict__ keys, int64_t n,
-                                                            PassPlan plan, uint32_t* __restrict__ hist) {
+                                                            PassPlan plan, uint32_t* __restrict__ hist,
+                                                            uint32_t* __restrict__ status0, int64_t n_status) {
+  // Also clears the first pass's status words (each pass clears the next one's).
+  for (int64_t k = (int64_t)blockIdx.x * kThreads + threadIdx.x; k < n_status; k += (int64_t)gridDim.x * kThreads)
+    status0[k] = 0;
   __shared__ uint32_t s_cnt[kMaxPasses][256];
   for (int k = threadIdx.x; k < kMaxPasses * 256; k += kThreads) (&s_cnt[0][0])[k] = 0;
   __syncthreads();
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
-    uint32_t* __restrict__ gather_dst) {
+    uint32_t* __restrict__ gather_dst, uint32_t* __restrict__ status_next) {
   constexpr int kW = Threads / 32;
   constexpr int kT = Threads * IPT;
   constexpr int kWI = 32 * IPT;
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
   constexpr int radix = 1 << Bits;
   constexpr uint32_t mask = (uint32_t)radix - 1u;
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(tile_counter, 1u);
+  if (status_next && threadIdx.x < 256) status_next[(int64_t)blockIdx.x * 256 + threadIdx.x] = 0u;
   for (int k = threadIdx.x; k < kW * 256; k += Threads) (&s_wcnt[0][0])[k] = 0;
   __syncthreads();
   const int tile = s_tile;
@@ -360,9 +365,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
 }
 
 size_t radix_sort_temp_bytes(int64_t n) {
-  const int64_t nb = pass_tiles(n > 0 ? n : 1);
-  // hist [kMaxPasses][256] + status [nb][256] + tile counters [kMaxPasses] (+ alignment)
-  return (size_t)(kMaxPasses * 256 + nb * 256 + kMaxPasses + 64) * sizeof(uint32_t);
+  // Enough status words for any sort of <= n pairs (either tile shape).
+  constexpr int64_t min_tile = std::min(kThreads * kSmallIPT, kBigThreads * kBigIPT);
+  const int64_t nb = (std::max<int64_t>(n, 1) + min_tile - 1) / min_tile;
+  // hist [kMaxPasses][256] + tile counters [64] + status [2][nb][256] (alternating passes)
+  return (size_t)(kMaxPasses * 256 + 64 + 2 * nb * 256) * sizeof(uint32_t);
 }
 
 namespace {
@@ -377,6 +384,7 @@ struct PassArgs {
   uint32_t *status, *tile_counter;
   const uint32_t* gather_src;
   uint32_t* gather_dst;
+  uint32_t* status_next;
 };
 
 template <int Threads, int IPT, int MinBlocks, int Bits>
@@ -392,7 +400,7 @@ void launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
   const int64_t tiles = (a.n + kT - 1) / kT;
   kern<<<(unsigned)tiles, Threads, smem, stream>>>(a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n, a.shift,
                                                    a.digit_start, a.status, a.tile_counter, a.gather_src,
-                                                   a.gather_dst);
+                                                   a.gather_dst, a.status_next);
 }
 
 template <int Threads, int IPT, int MinBlocks>
@@ -434,19 +442,22 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   const int64_t nb = blocks_for(n);
   uint32_t* hist = static_cast<uint32_t*>(temp);
   uint32_t* counters = hist + kMaxPasses * 256;
-  uint32_t* status = counters + 64;
+  const int64_t tiles = pass_tiles(n);
+  uint32_t* status[2] = {counters + 64, counters + 64 + tiles * 256};
   cudaMemsetAsync(hist, 0, (kMaxPasses * 256 + 64) * sizeof(uint32_t), stream);
   int sms = 148;
-  k_onesweep_hist<<<(unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream>>>(keys[0], n, plan, hist);
+  k_onesweep_hist<<<(unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream>>>(keys[0], n, plan, hist,
+                                                                                      status[0], tiles * 256);
   ++g_launches;
   k_onesweep_hist_scan<<<passes, 256, 0, stream>>>(hist);
   ++g_launches;
   const bool big = n > kBigSort;
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
-    cudaMemsetAsync(status, 0, (size_t)pass_tiles(n) * 256 * sizeof(uint32_t), stream);
-    PassArgs pa{keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, plan.shift[p], hist + p * 256, status,
-                counters + p, p == passes - 1 ? gather_src : nullptr, p == passes - 1 ? gather_dst : nullptr};
+    const bool last = p == passes - 1;
+    PassArgs pa{keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, plan.shift[p], hist + p * 256,
+                status[p & 1], counters + p, last ? gather_src : nullptr, last ? gather_dst : nullptr,
+                last ? nullptr : status[(p + 1) & 1]};
     if (big)
       launch_pass<kBigThreads, kBigIPT, kBigMinBlocks>(plan.bits[p], pa, stream);
     else

@@ -161,6 +161,7 @@ def densify_and_prune(ctx: Context, cloud: GaussianCloud, state: TrainState, cfg
     ball = rng.unit_ball(2 * int(stats.split))
     ball_ptr = ball.ctypes.data_as(C.POINTER(C.c_float)) if ball.size else None
     p_out, s_out = params_of(out_cloud) if m > 0 else capi.Params(0), out_state.to_c()
+    ctx.wait_torch()  # the new tensors come from torch's allocator / stream
     ctx.check(ctx.lib.odgs_densify_apply(ctx.handle, C.byref(p_in), C.byref(s_in), ball_ptr, C.byref(p_out),
                                          C.byref(s_out)))
     # The old tensors are released below; the library stream must be done reading them

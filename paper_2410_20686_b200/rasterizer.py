@@ -141,13 +141,23 @@ class GaussianCloud:  # types.hpp:53-143
         return capi.Cloud(self.n, *ptrs[:5], mem, self.sh_degree, sh_ptr)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
 class Context:
     """One CUDA device + stream (odgs_ctx). Not thread-safe; one per host thread."""
 
     def __init__(self, device: int = 0, stream: Optional[int] = None):
         self.lib = capi.load_library()
         h = C.c_void_p()
-        st = self.lib.odgs_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h))
+        # stream: a cudaStream_t handle (e.g. torch.cuda.current_stream().cuda_stream); 0 is
+        # the legacy default stream (passed as cudaStreamLegacy, since a NULL handle asks the
+        # library for a private non-blocking stream). None: a private stream.
+        if stream is None:
+            handle = None
+        else:
+            handle = C.c_void_p(int(stream) if int(stream) != 0 else CUDA_STREAM_LEGACY)
+        st = self.lib.odgs_ctx_create(device, handle, C.byref(h))
         if st != 0:
             raise OdgsError(f"odgs_ctx_create failed with status {st}")
         self.handle = h
@@ -185,6 +195,33 @@ class Context:
     @property
     def stream(self) -> int:
         return int(self.lib.odgs_ctx_stream(self.handle) or 0)
+
+    def _torch_streams(self):
+        """(this context's stream, torch's current stream) as torch streams, or None when they
+        are the same stream (or torch / CUDA is absent)."""
+        import sys as _sys
+        torch = _sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_available():
+            return None
+        cur = torch.cuda.current_stream(self.device)
+        mine = self.stream
+        if mine == cur.cuda_stream or (mine == CUDA_STREAM_LEGACY and cur.cuda_stream == 0):
+            return None
+        return torch.cuda.ExternalStream(mine, device=torch.device("cuda", self.device)), cur
+
+    def wait_torch(self):
+        """Orders this context's stream after the work already queued on torch's current stream
+        (call before handing torch-produced device tensors to the library)."""
+        ss = self._torch_streams()
+        if ss:
+            ss[0].wait_stream(ss[1])
+
+    def torch_wait(self):
+        """Orders torch's current stream after the work queued on this context's stream (call
+        before torch reads device memory the library wrote)."""
+        ss = self._torch_streams()
+        if ss:
+            ss[1].wait_stream(ss[0])
 
     def set_profiling(self, enable: bool):
         self.check(self.lib.odgs_ctx_set_profiling(self.handle, int(enable)))
@@ -328,6 +365,8 @@ class GradBuffers:  # backward.hpp:342-374
 def prepare_render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings,
                    out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
     out = out or RenderOutput(ctx, flags)
+    if cloud.on_device:
+        ctx.wait_torch()
     cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
     ctx.check(ctx.lib.odgs_prepare_render(ctx.handle, C.byref(cc), C.byref(cam), C.byref(st), out.handle))
     return out
@@ -336,6 +375,8 @@ def prepare_render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, setti
 def render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings,
            out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
     out = out or RenderOutput(ctx, flags)
+    if cloud.on_device:
+        ctx.wait_torch()
     cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
     ctx.check(ctx.lib.odgs_render(ctx.handle, C.byref(cc), C.byref(cam), C.byref(st), out.handle))
     return out
@@ -345,6 +386,8 @@ def render_band(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings
                 row_end: int, out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
     """Rows [row_begin, row_end) of render(); bit-identical to the full render there."""
     out = out or RenderOutput(ctx, flags)
+    if cloud.on_device:
+        ctx.wait_torch()
     cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
     ctx.check(ctx.lib.odgs_render_band(ctx.handle, C.byref(cc), C.byref(cam), C.byref(st), row_begin, row_end,
                                        out.handle))
@@ -355,6 +398,8 @@ def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: Render
              settings: RenderSettings, signs=None, grads: Optional[GradBuffers] = None,
              accumulate: bool = False) -> GradBuffers:
     grads = grads or GradBuffers.zeros(cloud.n, cloud.sh_degree)
+    if cloud.on_device or (_is_torch(dl_dimage) and dl_dimage.is_cuda):
+        ctx.wait_torch()
     cc, cam, st, gc = cloud.to_c(), camera.to_c(), settings.to_c(), grads.to_c()
     if _is_torch(dl_dimage):
         dptr, dmem = dl_dimage.data_ptr(), (capi.MEM_DEVICE if dl_dimage.is_cuda else capi.MEM_HOST)
@@ -366,6 +411,8 @@ def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: Render
         sp = (C.c_double * 12)(*[float(s) for s in signs])
     ctx.check(ctx.lib.odgs_backward(ctx.handle, C.byref(cc), C.byref(cam), fwd.handle, C.c_void_p(dptr), dmem,
                                     C.byref(st), C.byref(gc), sp, capi.ACCUMULATE if accumulate else 0))
+    if _is_torch(grads.means) and grads.means.is_cuda:
+        ctx.torch_wait()  # torch may read the gradients next
     return grads
 
 

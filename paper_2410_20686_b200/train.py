@@ -129,6 +129,7 @@ class ViewShardedTrainer:
             loss_sum += loss.value
             backward(ctx, self.cloud, cam, self.frame, self.dl, self.settings, grads=self.grads, accumulate=True)
         allreduce_grads(self.flat, self.observed, self.group)
+        ctx.wait_torch()  # Adam reads the reduced gradients
         step = self.iteration + 1
         p = capi.Params(self.n, self.cloud.means.data_ptr(), self.cloud.rotations.data_ptr(),
                         self.cloud.log_scales.data_ptr(), self.cloud.raw_opacities.data_ptr(),
