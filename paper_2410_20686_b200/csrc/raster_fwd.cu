@@ -373,8 +373,10 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     uint32_t* __restrict__ out_vals, uint32_t* __restrict__ ent_off_idx) {
   __shared__ int s_span[kEmitWarps][32][12];
   __shared__ uint32_t s_area[kEmitWarps][32][3];
+  __shared__ uint32_t s_magic[kEmitWarps][32][3];  // ceil-ish 2^32 / span width (0: divide)
   __shared__ uint32_t s_excl[kEmitWarps][32];
   __shared__ uint32_t s_gid[kEmitWarps][32];
+  __shared__ uint8_t s_nz[kEmitWarps][32];  // lanes with entries, by rank
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = ((int64_t)blockIdx.x * kEmitWarps + warp) * 32;
   if (base >= n) return;
@@ -394,8 +396,11 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     for (int k = 0; k < 3; ++k) {
       int span[4];
       if (band_tiles(a.x, a.y, radius, k, width, height, tile_size, band_ty0, band_ty1, span)) {
-        areas[k] = (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
+        const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
+        areas[k] = w * (uint32_t)(span[3] - span[2] + 1);
         for (int q = 0; q < 4; ++q) s_span[warp][lane][4 * k + q] = span[q];
+        // j / w == umulhi(j, m) for m = floor((2^32 - 1) / w) + 1 when j * w < 2^32.
+        s_magic[warp][lane][k] = (uint64_t)areas[k] * w < (1ull << 32) ? 0xFFFFFFFFu / w + 1u : 0u;
       }
     }
   }
@@ -408,28 +413,40 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= d) incl += v;
   }
-  s_excl[warp][lane] = incl - c;
+  const uint32_t excl = incl - c;
+  s_excl[warp][lane] = excl;
   const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
   const uint32_t base_off = __shfl_sync(0xffffffffu, off, 0);
+  const uint32_t lt = (1u << lane) - 1u, le = (2u << lane) - 1u;
+  const uint32_t nz_mask = __ballot_sync(0xffffffffu, c > 0);
+  if (c > 0) s_nz[warp][__popc(nz_mask & lt)] = (uint8_t)lane;
   __syncwarp();
-  for (uint32_t p = lane; p < total; p += 32) {
-    int lo = 0, hi = 31;  // largest owner with excl <= p
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_excl[warp][mid] <= p) lo = mid;
-      else hi = mid - 1;
+  // Owner of entry p: the lanes with entries start their runs in increasing order, so
+  // in each chunk of 32 entries the owner rank advances by the starts at or before p
+  // (one OR-reduction of start bits per chunk instead of a binary search per entry).
+  int rank = -1;  // owner rank of the entry before the chunk
+  for (uint32_t P = 0; P < total; P += 32) {
+    const uint32_t o = excl - P;
+    const uint32_t bits = __reduce_or_sync(0xffffffffu, (c > 0 && o < 32u) ? (1u << o) : 0u);
+    const int rk = rank + __popc(bits & le);
+    rank += __popc(bits);
+    const uint32_t p = P + lane;
+    if (p < total) {
+      const int lo = s_nz[warp][rk];
+      uint32_t j = p - s_excl[warp][lo];
+      int k = 0;
+      while (j >= s_area[warp][lo][k]) {
+        j -= s_area[warp][lo][k];
+        ++k;
+      }
+      const int* span = s_span[warp][lo] + 4 * k;
+      const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
+      const uint32_t m = s_magic[warp][lo][k];
+      const uint32_t q = m ? __umulhi(j, m) : j / w;
+      const int ty = span[2] + (int)q, tx = span[0] + (int)(j - q * w);
+      out_keys[base_off + p] = (uint32_t)(ty * tiles_x + tx);
+      out_vals[base_off + p] = (s_gid[warp][lo] << 2) | (uint32_t)k;
     }
-    uint32_t j = p - s_excl[warp][lo];
-    int k = 0;
-    while (j >= s_area[warp][lo][k]) {
-      j -= s_area[warp][lo][k];
-      ++k;
-    }
-    const int* span = s_span[warp][lo] + 4 * k;
-    const uint32_t w = (uint32_t)(span[1] - span[0] + 1);
-    const int ty = span[2] + (int)(j / w), tx = span[0] + (int)(j % w);
-    out_keys[base_off + p] = (uint32_t)(ty * tiles_x + tx);
-    out_vals[base_off + p] = (s_gid[warp][lo] << 2) | (uint32_t)k;
   }
 }
 
