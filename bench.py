@@ -35,7 +35,7 @@ METRIC = "ERP frames/sec (1M Gaussians, 2048×1024)"
 UNIT = "frames/s"
 W_IMG, H_IMG = 2048, 1024
 N_GAUSS = 1_000_000
-E2E_LANES = 4  # frames in flight on the e2e path (contexts / streams / host threads)
+E2E_LANES = int(os.environ.get("ODGS_E2E_LANES", "4"))  # frames in flight on the e2e path (contexts / streams / host threads)
 WORKLOAD = ("C3: 1M synthetic Gaussians (50% uniform, 25% poles |elev| 75-89.5 deg, 25% azimuth seam), "
             "SH0, 2048x1024 ERP, camera yawed per step")
 
@@ -190,6 +190,48 @@ def run_reference(args, rank: int):
     print(json.dumps(line), flush=True)
 
 
+def pcie_peaks(torch, dev, h2d: int, d2h: int) -> dict:
+    """Pinned-host copy bandwidth of this box, one frame's bytes per copy (best of 10,
+    CUDA events): the ceiling of the e2e path, which moves h2d + d2h bytes per frame."""
+    hs = torch.empty(h2d, dtype=torch.uint8).pin_memory()
+    ds = torch.empty(h2d, dtype=torch.uint8, device=dev)
+    hd = torch.empty(d2h, dtype=torch.uint8).pin_memory()
+    dd = torch.empty(d2h, dtype=torch.uint8, device=dev)
+    out = {}
+    for key, dst, src, nbytes in (("h2d_gbs", ds, hs, h2d), ("d2h_gbs", hd, dd, d2h)):
+        best = None
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            dst.copy_(src, non_blocking=True)
+            b.record()
+            b.synchronize()
+            ms = a.elapsed_time(b)
+            best = ms if best is None else min(best, ms)
+        out[key] = nbytes / (best * 1e-3) / 1e9
+    # Both directions at once (as in the pipelined e2e frames): H2D rate while a D2H of
+    # a frame's image runs on another stream, per frame (h2d bytes + d2h bytes in flight).
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = None
+    for _ in range(10):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s1)
+        s2.wait_event(a)
+        with torch.cuda.stream(s1):
+            ds.copy_(hs, non_blocking=True)
+        with torch.cuda.stream(s2):
+            for _ in range(max(1, h2d // d2h)):
+                hd.copy_(dd, non_blocking=True)
+        b.record(s1)
+        b.synchronize()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    torch.cuda.synchronize()
+    out["h2d_gbs_with_d2h"] = h2d / (best * 1e-3) / 1e9
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_ours(args, rank: int, world: int, local_rank: int):
     import numpy as np
@@ -298,7 +340,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # End to end through the C ABI with host buffers: every frame uploads the cloud from
     # pinned host memory inside odgs_render (56 MB H2D) and downloads the image into
-    # pinned memory (25 MB D2H). E2E_LANES contexts (own CUDA streams) driven by as many host
+    # pinned memory (25 MB D2H); `pcie` reports this box's pinned copy rates and the frame-rate
+    # bound they set. E2E_LANES contexts (own CUDA streams) driven by as many host
     # threads pipeline the frames, so one frame's copies overlap another's kernels (4 lanes: 833 fps vs
     # 762 with 3, 703 with 2; 6 lanes no better — the 56 MB H2D per frame is then ~47 GB/s of PCIe Gen5).
     import threading as _th
@@ -347,6 +390,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for c2, fr2, _ in lanes:
         fr2.destroy()
         c2.close()
+    pcie = pcie_peaks(torch, dev, h2d, d2h)
 
     aux = run_aux(args, ctx, dev, stream) if rank == 0 and not args.no_train else None
     train = None if args.no_train else run_train(args, ctx, rank, world, local_rank, dev, stream)
@@ -373,7 +417,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "stage_rooflines": stage_roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": f"odgs_render (host cloud, pinned) + odgs_frame_download (pinned), {E2E_LANES} "
-                            f"contexts / streams / host threads pipelining frames"},
+                            f"contexts / streams / host threads pipelining frames",
+                    "pcie": dict(pcie, h2d_gbs_achieved=e2e_value * h2d / 1e9,
+                                 h2d_frac=e2e_value * h2d / 1e9 / pcie["h2d_gbs"],
+                                 h2d_frac_vs_bidirectional=e2e_value * h2d / 1e9 / pcie["h2d_gbs_with_d2h"],
+                                 fps_bound=pcie["h2d_gbs_with_d2h"] * 1e9 / h2d)},
             "cpu_baseline": cpu,
             "other_configs": aux,
             "train": train,
