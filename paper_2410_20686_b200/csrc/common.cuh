@@ -13,6 +13,30 @@
 #include "odgs_portable_math.h"
 
 namespace odgs_b200 {
+// Programmatic dependent launch (sm_90+): the kernel may be scheduled while its
+// predecessor in the stream drains (hides the ~1.5 us launch gap between dependent
+// kernels). Every kernel launched this way calls pdl_wait() first, before any global
+// memory access, so its semantics equal a plain stream-ordered launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}  // namespace odgs_b200
+
+namespace odgs_b200 {
 
 constexpr float kPiF = 3.14159274101257324f;  // std::numbers::pi_v<float>
 constexpr uint32_t kCulledKey = 0xFFFFFFFFu;

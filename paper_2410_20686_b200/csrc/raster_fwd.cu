@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(256) k_preprocess(
     float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
     uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, int sh_degree,
     const float* __restrict__ sh_rest) {
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool visible = false;
   uint32_t n_inst = 0;
@@ -158,7 +159,7 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   if (a.n == 0) return;
   const int block = 256;
   const int64_t grid = (a.n + block - 1) / block;
-  k_preprocess<<<(unsigned)grid, block, 0, stream>>>(a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
+  launch_pdl(k_preprocess, (unsigned)grid, block, 0, stream, a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
                                                      a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
                                                      a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest);
   ++g_launches;
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(256, 3) k_band_preprocess(
     uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err, int sh_degree,
     const float* __restrict__ sh_rest, uint32_t* __restrict__ seg_keys, uint32_t* __restrict__ seg_vals,
     uint32_t* __restrict__ seg_count) {
+  pdl_wait();
   __shared__ uint32_t s_queue[8][kBandQueue];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w = (int64_t)blockIdx.x * 8 + warp;
@@ -331,6 +333,7 @@ __global__ void k_concat_segments(int64_t n_seg, const uint32_t* __restrict__ se
                                   const uint32_t* __restrict__ seg_off, const uint32_t* __restrict__ seg_keys,
                                   const uint32_t* __restrict__ seg_vals, uint32_t* __restrict__ keys_out,
                                   uint32_t* __restrict__ vals_out) {
+  pdl_wait();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= n_seg) return;
@@ -348,7 +351,7 @@ void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_
                             cudaStream_t stream) {
   if (a.n == 0) return;
   const int64_t n_seg = band_segments(a.n);
-  k_band_preprocess<<<(unsigned)((n_seg + 7) / 8), 256, 0, stream>>>(
+  launch_pdl(k_band_preprocess, (unsigned)((n_seg + 7) / 8), 256, 0, stream, 
       a.n, a.means, a.rotations, a.log_scales, a.raw_opacities, a.colors, a.cam, a.settings, a.sp_ab, a.sp_c,
       a.cov_out, a.keys, a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest, seg_keys, seg_vals, seg_count);
   ++g_launches;
@@ -358,7 +361,7 @@ void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t
                             const uint32_t* seg_vals, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream) {
   const int64_t n_seg = band_segments(n);
   if (n_seg == 0) return;
-  k_concat_segments<<<(unsigned)((n_seg * 32 + 255) / 256), 256, 0, stream>>>(n_seg, seg_count, seg_off, seg_keys,
+  launch_pdl(k_concat_segments, (unsigned)((n_seg * 32 + 255) / 256), 256, 0, stream, n_seg, seg_count, seg_off, seg_keys,
                                                                                seg_vals, keys_out, vals_out);
   ++g_launches;
 }
@@ -371,6 +374,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     const uint32_t* __restrict__ off_sorted, const float4* __restrict__ sp_ab, const float4* __restrict__ sp_c,
     int width, int height, int tile_size, int tiles_x, int band_ty0, int band_ty1, uint32_t* __restrict__ out_keys,
     uint32_t* __restrict__ out_vals, uint32_t* __restrict__ ent_off_idx) {
+  pdl_wait();
   __shared__ int s_span[kEmitWarps][32][12];
   __shared__ uint32_t s_area[kEmitWarps][32][3];
   __shared__ uint32_t s_magic[kEmitWarps][32][3];  // ceil-ish 2^32 / span width (0: divide)
@@ -454,7 +458,7 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
   if (a.n == 0) return;
   const int64_t warps = (a.n + 31) / 32;
   const int64_t grid = (warps + kEmitWarps - 1) / kEmitWarps;
-  k_emit<<<(unsigned)grid, kEmitWarps * 32, 0, stream>>>(a.n, a.sorted_idx, a.cnt_sorted, a.off_sorted, a.sp_ab,
+  launch_pdl(k_emit, (unsigned)grid, kEmitWarps * 32, 0, stream, a.n, a.sorted_idx, a.cnt_sorted, a.off_sorted, a.sp_ab,
                                                          a.sp_c, a.width, a.height, a.tile_size, a.tiles_x,
                                                          a.band_ty0, a.band_ty1, a.out_keys, a.out_vals,
                                                          a.ent_off_idx);
@@ -470,6 +474,7 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
 // belongs to the thread whose range contains it).
 __global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ keys, uint32_t t0, uint32_t t1,
                               int32_t* __restrict__ offsets) {
+  pdl_wait();
   const uint32_t e_first = 4u * (blockIdx.x * blockDim.x + threadIdx.x);
   if (e_first > k_entries) return;
   uint32_t kv[4];
@@ -496,6 +501,7 @@ __global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ k
 
 __global__ void k_fill_outside(uint32_t k_entries, uint32_t n_tiles, uint32_t t0, uint32_t t1,
                                int32_t* __restrict__ offsets) {
+  pdl_wait();
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < t0) offsets[t] = 0;
   else if (t > t1 && t <= n_tiles) offsets[t] = (int32_t)k_entries;
@@ -508,10 +514,10 @@ void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_til
     return;
   }
   const uint32_t threads = k_entries / 4 + 1;
-  k_tile_ranges<<<(threads + 255) / 256, 256, 0, stream>>>(k_entries, keys, t0, t1, offsets);
+  launch_pdl(k_tile_ranges, (threads + 255) / 256, 256, 0, stream, k_entries, keys, t0, t1, offsets);
   ++g_launches;
   if (t0 > 0 || t1 < n_tiles) {
-    k_fill_outside<<<(n_tiles + 1 + 255) / 256, 256, 0, stream>>>(k_entries, n_tiles, t0, t1, offsets);
+    launch_pdl(k_fill_outside, (n_tiles + 1 + 255) / 256, 256, 0, stream, k_entries, n_tiles, t0, t1, offsets);
     ++g_launches;
   }
 }
@@ -534,6 +540,7 @@ __device__ __forceinline__ int order_bucket(int32_t len) {
 
 __global__ void __launch_bounds__(kOrderThreads) k_tile_order(const int32_t* __restrict__ offsets, int tile_base,
                                                               int n, uint32_t* __restrict__ order) {
+  pdl_wait();
   __shared__ uint32_t s_cnt[kOrderBuckets];
   for (int b = threadIdx.x; b < kOrderBuckets; b += kOrderThreads) s_cnt[b] = 0;
   __syncthreads();
@@ -555,7 +562,7 @@ __global__ void __launch_bounds__(kOrderThreads) k_tile_order(const int32_t* __r
 
 void launch_tile_order(const int32_t* offsets, int tile_base, int n, uint32_t* order, cudaStream_t stream) {
   if (n <= 0) return;
-  k_tile_order<<<1, kOrderThreads, 0, stream>>>(offsets, tile_base, n, order);
+  launch_pdl(k_tile_order, 1, kOrderThreads, 0, stream, offsets, tile_base, n, order);
   ++g_launches;
 }
 
@@ -698,6 +705,7 @@ __global__ void __launch_bounds__(kBlendThreads, 6) k_blend_cull(
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
     int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base,
     const uint32_t* __restrict__ order, PeerImages peers) {
+  pdl_wait();
   constexpr int kWarps = kBlendThreads / 32;
   // One 48-byte record per staged entry: the walk addresses all three parts from one
   // base with immediate offsets (separate arrays cost an address computation each).
@@ -869,7 +877,7 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
   if (!a.plain && a.tile_size <= 16) {
     const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
     auto kern = cutoff2 <= 172.0f ? k_blend_cull<true> : k_blend_cull<false>;
-    kern<<<n_band_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,
+    launch_pdl(kern, n_band_tiles, kBlendThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,
                                                       a.tile_size, a.tiles_x, a.alpha_clamp, a.transmittance_floor,
                                                       cutoff2, a.image, a.transmittance, a.walked, a.work,
                                                       a.band_ty0 * a.tiles_x, a.order, a.peers);

@@ -72,6 +72,7 @@ __device__ __forceinline__ uint32_t warp_reduce(uint32_t v) {
 __global__ void __launch_bounds__(kThreads) k_scan_reduce(const uint32_t* __restrict__ in, int64_t n,
                                                           uint32_t* __restrict__ block_sums,
                                                           unsigned long long* total64) {
+  pdl_wait();
   __shared__ uint32_t s_warp[kWarps];
   const int64_t base = (int64_t)blockIdx.x * kTile;
   uint32_t sum = 0;
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_downsweep(const uint32_t* __r
                                                              uint32_t* __restrict__ out, int64_t n,
                                                              const uint32_t* __restrict__ block_offsets,
                                                              unsigned long long* total64) {
+  pdl_wait();
   __shared__ uint32_t s_warp[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)warp * kWarpItems;
@@ -155,6 +157,7 @@ struct PassPlan {
 __global__ void __launch_bounds__(kThreads) k_onesweep_hist(const uint32_t* __restrict__ keys, int64_t n,
                                                             PassPlan plan, uint32_t* __restrict__ hist,
                                                             uint32_t* __restrict__ status0, int64_t n_status) {
+  pdl_wait();
   // Also clears the first pass's status words (each pass clears the next one's).
   for (int64_t k = (int64_t)blockIdx.x * kThreads + threadIdx.x; k < n_status; k += (int64_t)gridDim.x * kThreads)
     status0[k] = 0;
@@ -177,6 +180,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep_hist(const uint32_t* __re
 
 // Exclusive scan of each pass's 256 digit counts (one CTA of 256 threads per pass).
 __global__ void k_onesweep_hist_scan(uint32_t* __restrict__ hist) {
+  pdl_wait();
   __shared__ uint32_t s_w[8];
   const int p = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
   const uint32_t v = hist[p * 256 + d];
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
     uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
     uint32_t* __restrict__ gather_dst, uint32_t* __restrict__ status_next) {
+  pdl_wait();
   constexpr int kW = Threads / 32;
   constexpr int kT = Threads * IPT;
   constexpr int kWI = 32 * IPT;
@@ -331,6 +336,7 @@ int64_t blocks_for(int64_t n) { return (n + kTile - 1) / kTile; }
 
 __global__ void k_gather(int64_t n, const uint32_t* __restrict__ idx, const uint32_t* __restrict__ src,
                          uint32_t* __restrict__ dst) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = src[idx[i]];
 }
@@ -349,7 +355,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
                         cudaStream_t stream) {
   if (n <= 0) return;
   if (n <= kTile) {
-    k_scan_downsweep<<<1, kThreads, 0, stream>>>(in, out, n, nullptr, total64);
+    launch_pdl(k_scan_downsweep, 1, kThreads, 0, stream, in, out, n, nullptr, total64);
     ++g_launches;
     return;
   }
@@ -357,10 +363,10 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
   uint32_t* sums = static_cast<uint32_t*>(temp);
   uint32_t* offs = sums + nb;
   void* next = reinterpret_cast<char*>(temp) + (((size_t)(2 * nb) * sizeof(uint32_t) + 255) / 256) * 256;
-  k_scan_reduce<<<(unsigned)nb, kThreads, 0, stream>>>(in, n, sums, total64);
+  launch_pdl(k_scan_reduce, (unsigned)nb, kThreads, 0, stream, in, n, sums, total64);
   ++g_launches;
   exclusive_scan_u32(sums, offs, nb, next, nullptr, stream);
-  k_scan_downsweep<<<(unsigned)nb, kThreads, 0, stream>>>(in, out, n, offs, nullptr);
+  launch_pdl(k_scan_downsweep, (unsigned)nb, kThreads, 0, stream, in, out, n, offs, nullptr);
   ++g_launches;
 }
 
@@ -398,7 +404,7 @@ void launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
     configured = true;
   }
   const int64_t tiles = (a.n + kT - 1) / kT;
-  kern<<<(unsigned)tiles, Threads, smem, stream>>>(a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n, a.shift,
+  launch_pdl(kern, (unsigned)tiles, Threads, smem, stream, a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n, a.shift,
                                                    a.digit_start, a.status, a.tile_counter, a.gather_src,
                                                    a.gather_dst, a.status_next);
 }
@@ -424,7 +430,7 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   *which = 0;
   if (n <= 1 || end_bit <= begin_bit) {
     if (gather_dst && n > 0) {
-      k_gather<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(n, vals[0], gather_src, gather_dst);
+      launch_pdl(k_gather, (unsigned)((n + 255) / 256), 256, 0, stream, n, vals[0], gather_src, gather_dst);
       ++g_launches;
     }
     return;
@@ -446,10 +452,10 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   uint32_t* status[2] = {counters + 64, counters + 64 + tiles * 256};
   cudaMemsetAsync(hist, 0, (kMaxPasses * 256 + 64) * sizeof(uint32_t), stream);
   int sms = 148;
-  k_onesweep_hist<<<(unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream>>>(keys[0], n, plan, hist,
+  launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream, keys[0], n, plan, hist,
                                                                                       status[0], tiles * 256);
   ++g_launches;
-  k_onesweep_hist_scan<<<passes, 256, 0, stream>>>(hist);
+  launch_pdl(k_onesweep_hist_scan, passes, 256, 0, stream, hist);
   ++g_launches;
   const bool big = n > kBigSort;
   int cur = 0;
