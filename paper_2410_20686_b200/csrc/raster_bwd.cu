@@ -299,6 +299,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1,
     const uint32_t* __restrict__ order) {
+  pdl_wait();
   // One 48-byte record per staged entry (all parts addressed from one base).
   struct alignas(16) Staged {
     float4 geo;  // cx, cy, i00, 2*i01
@@ -551,7 +552,7 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
   const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
   const int area = a.tile_size * a.tile_size;
   if (!a.plain && a.tile_size <= 16) {
-    k_bwd_raster_cull<<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
+    launch_pdl(k_bwd_raster_cull, n_tiles, kBwdThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
                                                            a.transmittance, a.walked, a.dl_dimage, a.width,
                                                            a.height, a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2,
                                                            a.records, a.touched, a.band_ty0, a.band_ty1, a.order);
@@ -595,6 +596,7 @@ __device__ __forceinline__ M23 jacobian_factored_fast(float phi, float theta, fl
 }
 
 __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = a.n;
   if (i >= n) return;
@@ -837,6 +839,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
     int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
     const uint32_t* __restrict__ off_sorted, const uint8_t* __restrict__ touched, const float* __restrict__ records,
     float* __restrict__ folded) {
+  pdl_wait();
   __shared__ float s_rec[kFoldWarps][kFoldChunk * kRec];
   __shared__ uint8_t s_touch[kFoldWarps][kFoldChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -891,14 +894,14 @@ void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* 
                          cudaStream_t stream) {
   if (n == 0) return;
   const int64_t warps = (n + 31) / 32;
-  k_fold_records<<<(unsigned)((warps + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, stream>>>(
+  launch_pdl(k_fold_records, (unsigned)((warps + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, stream, 
       n, sorted_idx, cnt_sorted, off_sorted, touched, records, folded);
   ++g_launches;
 }
 
 void launch_bwd_splat(const BwdSplatArgs& a, cudaStream_t stream) {
   if (a.n == 0) return;
-  k_bwd_splat<<<(unsigned)((a.n + 255) / 256), 256, 0, stream>>>(a);
+  launch_pdl(k_bwd_splat, (unsigned)((a.n + 255) / 256), 256, 0, stream, a);
   ++g_launches;
 }
 

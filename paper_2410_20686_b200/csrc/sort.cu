@@ -334,6 +334,11 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
 
 int64_t blocks_for(int64_t n) { return (n + kTile - 1) / kTile; }
 
+__global__ void k_zero_u32(uint32_t* __restrict__ p, int n) {
+  pdl_wait();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) p[k] = 0u;
+}
+
 __global__ void k_gather(int64_t n, const uint32_t* __restrict__ idx, const uint32_t* __restrict__ src,
                          uint32_t* __restrict__ dst) {
   pdl_wait();
@@ -450,7 +455,8 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   uint32_t* counters = hist + kMaxPasses * 256;
   const int64_t tiles = pass_tiles(n);
   uint32_t* status[2] = {counters + 64, counters + 64 + tiles * 256};
-  cudaMemsetAsync(hist, 0, (kMaxPasses * 256 + 64) * sizeof(uint32_t), stream);
+  launch_pdl(k_zero_u32, 1, 256, 0, stream, hist, kMaxPasses * 256 + 64);  // hist + counters
+  ++g_launches;
   int sms = 148;
   launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream, keys[0], n, plan, hist,
                                                                                       status[0], tiles * 256);

@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(kLossThreads) k_l1_loss(const float* __restric
                                                           const float* __restrict__ target, int64_t count,
                                                           float scale, float pixels, float* __restrict__ grad,
                                                           double* __restrict__ partial) {
+  pdl_wait();
   __shared__ double s_warp[kLossThreads / 32];
   const int64_t base = (int64_t)blockIdx.x * kLossThreads * kLossItems;
   double sum = 0.0;
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(kLossThreads) k_l1_loss(const float* __restric
 }
 
 __global__ void k_sum_partials(const double* __restrict__ partial, int64_t n, double scale, double* out) {
+  pdl_wait();
   __shared__ double s[256];
   double t = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += 256) t += partial[i];
@@ -94,10 +96,10 @@ void launch_l1_loss(const float* rendered, const float* target, int64_t count, f
                     double* temp, cudaStream_t stream) {
   const int64_t blocks = (count + kLossThreads * kLossItems - 1) / (kLossThreads * kLossItems);
   const float pixels = (float)count;  // 3 * H * W, formed in Scalar as the reference does
-  k_l1_loss<<<(unsigned)blocks, kLossThreads, 0, stream>>>(rendered, target, count, 1.0f - lambda, pixels, grad,
+  launch_pdl(k_l1_loss, (unsigned)blocks, kLossThreads, 0, stream, rendered, target, count, 1.0f - lambda, pixels, grad,
                                                           temp + 1);
   ++g_launches;
-  k_sum_partials<<<1, 256, 0, stream>>>(temp + 1, blocks, (1.0 - (double)lambda) / (double)count, temp);
+  launch_pdl(k_sum_partials, 1, 256, 0, stream, temp + 1, blocks, (1.0 - (double)lambda) / (double)count, temp);
   ++g_launches;
 }
 
@@ -122,6 +124,7 @@ constexpr int kSsimThreads = 256;
 __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const float* __restrict__ a, const float* __restrict__ b,
                                                            int H, int W, SsimWindow win, double inv_windows,
                                                            float* __restrict__ gmaps, double* __restrict__ partial) {
+  pdl_wait();
   __shared__ float s_a[kSsimIX][kSsimIY], s_b[kSsimIX][kSsimIY];
   __shared__ float s_h[5][kSsimTX][kSsimIY];
   __shared__ double s_w[kSsimThreads / 32];
@@ -203,6 +206,7 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_bwd(const float* __restri
                                                            const float* __restrict__ a, const float* __restrict__ b,
                                                            int H, int W, SsimWindow win, float lambda, float pixels,
                                                            float* __restrict__ grad, double* __restrict__ l1_partial) {
+  pdl_wait();
   __shared__ float s_g[4][kSsimIX][kSsimIY];
   __shared__ float s_h[4][kSsimTX][kSsimIY];
   __shared__ double s_w[kSsimThreads / 32];
@@ -266,6 +270,7 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_bwd(const float* __restri
 // loss = (1 - lambda) sum|d| / pixels + lambda (1 - sum s / windows), fixed-order sums.
 __global__ void k_ssim_loss(const double* __restrict__ l1_partial, int64_t n_l1, const double* __restrict__ s_partial,
                             int64_t n_s, double lambda, double pixels, double windows, double* out) {
+  pdl_wait();
   __shared__ double s_a[256], s_b[256];
   double ta = 0.0, tb = 0.0;
   for (int64_t i = threadIdx.x; i < n_l1; i += 256) ta += l1_partial[i];
@@ -307,10 +312,10 @@ void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda
   const dim3 gb((unsigned)((H + kSsimTY - 1) / kSsimTY), (unsigned)((W + kSsimTX - 1) / kSsimTX), 3);
   double* l1_part = s_part + (int64_t)gf.x * gf.y * gf.z;
   const double windows = 3.0 * (double)Ho * (double)Wo;
-  k_ssim_fwd<<<gf, kSsimThreads, 0, stream>>>(a, b, H, W, win, 1.0 / windows, gmaps, s_part);
+  launch_pdl(k_ssim_fwd, gf, kSsimThreads, 0, stream, a, b, H, W, win, 1.0 / windows, gmaps, s_part);
   const float pixels = 3.0f * (float)H * (float)W;
-  k_ssim_bwd<<<gb, kSsimThreads, 0, stream>>>(gmaps, a, b, H, W, win, lambda, pixels, grad, l1_part);
-  k_ssim_loss<<<1, 256, 0, stream>>>(l1_part, (int64_t)gb.x * gb.y * gb.z, s_part, (int64_t)gf.x * gf.y * gf.z,
+  launch_pdl(k_ssim_bwd, gb, kSsimThreads, 0, stream, gmaps, a, b, H, W, win, lambda, pixels, grad, l1_part);
+  launch_pdl(k_ssim_loss, 1, 256, 0, stream, l1_part, (int64_t)gb.x * gb.y * gb.z, s_part, (int64_t)gf.x * gf.y * gf.z,
                                      (double)lambda, 3.0 * (double)H * (double)W, windows, loss_out);
   g_launches += 3;
 }
@@ -323,6 +328,7 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g, flo
 }
 
 __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = a.n;
   if (i >= n) return;
@@ -358,7 +364,7 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
 
 void launch_adam(const AdamArgs& a, cudaStream_t stream) {
   if (a.n == 0) return;
-  k_adam<<<(unsigned)((a.n + 255) / 256), 256, 0, stream>>>(a);
+  launch_pdl(k_adam, (unsigned)((a.n + 255) / 256), 256, 0, stream, a);
   ++g_launches;
 }
 
