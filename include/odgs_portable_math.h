@@ -36,6 +36,25 @@
 #define PM_HD static inline
 #endif
 
+/* Polynomial coefficient tables: on the device in constant memory, so each DFMA takes
+   its coefficient as a constant-bank operand (64-bit immediates otherwise cost two
+   uniform moves per coefficient); on the host a static array. Same values, same
+   evaluation order on both sides. */
+#if defined(__CUDACC__)
+#define PM_TABLE(name, n, ...)                                   \
+  static __constant__ double name##_dev[n] = {__VA_ARGS__};      \
+  static const double name##_host[n] = {__VA_ARGS__};
+#else
+#define PM_TABLE(name, n, ...) static const double name##_host[n] = {__VA_ARGS__};
+#endif
+#if defined(__CUDA_ARCH__)
+#define PM_COEF(name, k) (name##_dev[k])
+#define PM_UNROLL _Pragma("unroll")
+#else
+#define PM_COEF(name, k) (name##_host[k])
+#define PM_UNROLL
+#endif
+
 /* ---------------------------------------------------------------- primitives */
 
 PM_HD double pm_dadd(double a, double b) {
@@ -142,6 +161,8 @@ PM_HD double pm_rint_d(double x) {
 /* ---------------------------------------------------------------- exp */
 
 /* e^x in binary64 for -745 < x < 709 (only used on float-derived arguments). */
+PM_TABLE(pm_exp_tab, 14, 0x1.6124613a86d09p-33, 0x1.1eed8eff8d898p-29, 0x1.ae64567f544e4p-26, 0x1.27e4fb7789f5cp-22, 0x1.71de3a556c734p-19, 0x1.a01a01a01a01ap-16, 0x1.a01a01a01a01ap-13, 0x1.6c16c16c16c17p-10, 0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3, 0x1.0p-1, 0x1.0p+0, 0x1.0p+0)
+
 PM_HD double pm_exp_core_d(double x) {
   const double inv_ln2 = 0x1.71547652b82fep+0;
   const double ln2_hi = 0x1.62e42fefa39efp-1;
@@ -150,20 +171,9 @@ PM_HD double pm_exp_core_d(double x) {
   double r = pm_dfma(-kd, ln2_hi, x);
   r = pm_dfma(-kd, ln2_lo, r);
   /* Taylor to degree 13 on |r| <= 0.347: truncation < 5e-18 relative. */
-  double p = 0x1.6124613a86d09p-33;
-  p = pm_dfma(p, r, 0x1.1eed8eff8d898p-29);
-  p = pm_dfma(p, r, 0x1.ae64567f544e4p-26);
-  p = pm_dfma(p, r, 0x1.27e4fb7789f5cp-22);
-  p = pm_dfma(p, r, 0x1.71de3a556c734p-19);
-  p = pm_dfma(p, r, 0x1.a01a01a01a01ap-16);
-  p = pm_dfma(p, r, 0x1.a01a01a01a01ap-13);
-  p = pm_dfma(p, r, 0x1.6c16c16c16c17p-10);
-  p = pm_dfma(p, r, 0x1.1111111111111p-7);
-  p = pm_dfma(p, r, 0x1.5555555555555p-5);
-  p = pm_dfma(p, r, 0x1.5555555555555p-3);
-  p = pm_dfma(p, r, 0x1.0p-1);
-  p = pm_dfma(p, r, 0x1.0p+0);
-  p = pm_dfma(p, r, 0x1.0p+0);
+  double p = PM_COEF(pm_exp_tab, 0);
+  PM_UNROLL
+  for (int k_ = 1; k_ < 14; ++k_) p = pm_dfma(p, r, PM_COEF(pm_exp_tab, k_));
   return pm_dmul(p, pm_pow2i_d((int)kd));
 }
 
@@ -239,30 +249,23 @@ PM_HD double pm_reduce_pio2(double x, int* q) {
   return r;
 }
 
+PM_TABLE(pm_sin_tab, 8, 0x1.952c77030ad4ap-49, -0x1.ae7f3e733b81fp-41, 0x1.6124613a86d09p-33, -0x1.ae64567f544e4p-26, 0x1.71de3a556c734p-19, -0x1.a01a01a01a01ap-13, 0x1.1111111111111p-7, -0x1.5555555555555p-3)
+
 PM_HD double pm_sin_poly(double r) {
   const double s = pm_dmul(r, r);
-  double p = 0x1.952c77030ad4ap-49;
-  p = pm_dfma(p, s, -0x1.ae7f3e733b81fp-41);
-  p = pm_dfma(p, s, 0x1.6124613a86d09p-33);
-  p = pm_dfma(p, s, -0x1.ae64567f544e4p-26);
-  p = pm_dfma(p, s, 0x1.71de3a556c734p-19);
-  p = pm_dfma(p, s, -0x1.a01a01a01a01ap-13);
-  p = pm_dfma(p, s, 0x1.1111111111111p-7);
-  p = pm_dfma(p, s, -0x1.5555555555555p-3);
+  double p = PM_COEF(pm_sin_tab, 0);
+  PM_UNROLL
+  for (int k_ = 1; k_ < 8; ++k_) p = pm_dfma(p, s, PM_COEF(pm_sin_tab, k_));
   return pm_dfma(pm_dmul(r, s), p, r);
 }
 
+PM_TABLE(pm_cos_tab, 9, -0x1.6827863b97d97p-53, 0x1.ae7f3e733b81fp-45, -0x1.93974a8c07c9dp-37, 0x1.1eed8eff8d898p-29, -0x1.27e4fb7789f5cp-22, 0x1.a01a01a01a01ap-16, -0x1.6c16c16c16c17p-10, 0x1.5555555555555p-5, -0x1.0p-1)
+
 PM_HD double pm_cos_poly(double r) {
   const double s = pm_dmul(r, r);
-  double p = -0x1.6827863b97d97p-53;
-  p = pm_dfma(p, s, 0x1.ae7f3e733b81fp-45);
-  p = pm_dfma(p, s, -0x1.93974a8c07c9dp-37);
-  p = pm_dfma(p, s, 0x1.1eed8eff8d898p-29);
-  p = pm_dfma(p, s, -0x1.27e4fb7789f5cp-22);
-  p = pm_dfma(p, s, 0x1.a01a01a01a01ap-16);
-  p = pm_dfma(p, s, -0x1.6c16c16c16c17p-10);
-  p = pm_dfma(p, s, 0x1.5555555555555p-5);
-  p = pm_dfma(p, s, -0x1.0p-1);
+  double p = PM_COEF(pm_cos_tab, 0);
+  PM_UNROLL
+  for (int k_ = 1; k_ < 9; ++k_) p = pm_dfma(p, s, PM_COEF(pm_cos_tab, k_));
   return pm_dfma(s, p, 1.0);
 }
 
@@ -319,6 +322,8 @@ PM_HD void pm_sincosf(float x, float* s, float* c) {
 /* ---------------------------------------------------------------- atan2 / hypot */
 
 /* atan(t) for 0 <= t <= 1 in binary64. */
+PM_TABLE(pm_atan_tab, 22, 0x1.6c16c16c16c17p-6, -0x1.7d05f417d05f4p-6, 0x1.8f9c18f9c18fap-6, -0x1.a41a41a41a41ap-6, 0x1.bacf914c1bad0p-6, -0x1.d41d41d41d41dp-6, 0x1.f07c1f07c1f08p-6, -0x1.0842108421084p-5, 0x1.1a7b9611a7b96p-5, -0x1.2f684bda12f68p-5, 0x1.47ae147ae147bp-5, -0x1.642c8590b2164p-5, 0x1.8618618618618p-5, -0x1.af286bca1af28p-5, 0x1.e1e1e1e1e1e1ep-5, -0x1.1111111111111p-4, 0x1.3b13b13b13b14p-4, -0x1.745d1745d1746p-4, 0x1.c71c71c71c71cp-4, -0x1.2492492492492p-3, 0x1.999999999999ap-3, -0x1.5555555555555p-2)
+
 PM_HD double pm_atan_unit_d(double t) {
   const double tan_pi_8 = 0x1.a827999fcef32p-2;
   const double pi_4 = 0x1.921fb54442d18p-1;
@@ -329,28 +334,9 @@ PM_HD double pm_atan_unit_d(double t) {
   }
   /* Taylor in s = u^2 to u^45 on |u| <= tan(pi/8): truncation < 2e-19. */
   const double s = pm_dmul(u, u);
-  double p = 0x1.6c16c16c16c17p-6;
-  p = pm_dfma(p, s, -0x1.7d05f417d05f4p-6);
-  p = pm_dfma(p, s, 0x1.8f9c18f9c18fap-6);
-  p = pm_dfma(p, s, -0x1.a41a41a41a41ap-6);
-  p = pm_dfma(p, s, 0x1.bacf914c1bad0p-6);
-  p = pm_dfma(p, s, -0x1.d41d41d41d41dp-6);
-  p = pm_dfma(p, s, 0x1.f07c1f07c1f08p-6);
-  p = pm_dfma(p, s, -0x1.0842108421084p-5);
-  p = pm_dfma(p, s, 0x1.1a7b9611a7b96p-5);
-  p = pm_dfma(p, s, -0x1.2f684bda12f68p-5);
-  p = pm_dfma(p, s, 0x1.47ae147ae147bp-5);
-  p = pm_dfma(p, s, -0x1.642c8590b2164p-5);
-  p = pm_dfma(p, s, 0x1.8618618618618p-5);
-  p = pm_dfma(p, s, -0x1.af286bca1af28p-5);
-  p = pm_dfma(p, s, 0x1.e1e1e1e1e1e1ep-5);
-  p = pm_dfma(p, s, -0x1.1111111111111p-4);
-  p = pm_dfma(p, s, 0x1.3b13b13b13b14p-4);
-  p = pm_dfma(p, s, -0x1.745d1745d1746p-4);
-  p = pm_dfma(p, s, 0x1.c71c71c71c71cp-4);
-  p = pm_dfma(p, s, -0x1.2492492492492p-3);
-  p = pm_dfma(p, s, 0x1.999999999999ap-3);
-  p = pm_dfma(p, s, -0x1.5555555555555p-2);
+  double p = PM_COEF(pm_atan_tab, 0);
+  PM_UNROLL
+  for (int k_ = 1; k_ < 22; ++k_) p = pm_dfma(p, s, PM_COEF(pm_atan_tab, k_));
   return pm_dadd(base, pm_dfma(pm_dmul(u, s), p, u));
 }
 

@@ -298,7 +298,11 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
       // round trip per window instead of per tile), then consumed newest first up to
       // the first prefix; an unpublished word restarts the window there.
       uint32_t excl = 0;
+      uint32_t rounds = 0;
       for (int look = tile - 1; look >= 0;) {
+        // A predecessor that never publishes (a launch or memory fault upstream) would
+        // spin this loop forever: fail the kernel instead of hanging the device.
+        if (++rounds > (1u << 26)) __trap();
         uint32_t w[kLookWindow];
 #pragma unroll
         for (int j = 0; j < kLookWindow; ++j)
@@ -455,13 +459,14 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   uint32_t* counters = hist + kMaxPasses * 256;
   const int64_t tiles = pass_tiles(n);
   uint32_t* status[2] = {counters + 64, counters + 64 + tiles * 256};
-  launch_pdl(k_zero_u32, 1, 256, 0, stream, hist, kMaxPasses * 256 + 64);  // hist + counters
+  // The passes spin on look-back words: never launch them after a failed set-up launch.
+  if (launch_pdl(k_zero_u32, 1, 256, 0, stream, hist, kMaxPasses * 256 + 64) != cudaSuccess) return;
   ++g_launches;
   int sms = 148;
-  launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream, keys[0], n, plan, hist,
-                                                                                      status[0], tiles * 256);
+  const cudaError_t hist_err = launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0,
+                                          stream, keys[0], n, plan, hist, status[0], tiles * 256);
   ++g_launches;
-  launch_pdl(k_onesweep_hist_scan, passes, 256, 0, stream, hist);
+  if (hist_err != cudaSuccess || launch_pdl(k_onesweep_hist_scan, passes, 256, 0, stream, hist) != cudaSuccess) return;
   ++g_launches;
   const bool big = n > kBigSort;
   int cur = 0;
