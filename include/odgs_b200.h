@@ -151,7 +151,10 @@ typedef enum {
 odgs_settings odgs_default_settings(void);
 int odgs_abi_version(void);
 
-/* Creates a context on `device`. stream: a cudaStream_t, or NULL for a private one. */
+/* Creates a context on `device`. stream: a cudaStream_t, or NULL for a private
+   non-blocking one. The legacy default stream (handle 0, e.g. torch's default stream)
+   must be passed as cudaStreamLegacy ((void*)0x1), since NULL asks for a private stream.
+   Kernels are launched with programmatic dependent launch on that stream. */
 odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out);
 void odgs_ctx_destroy(odgs_ctx* ctx);
 odgs_status odgs_ctx_set_stream(odgs_ctx* ctx, void* stream);
