@@ -179,3 +179,35 @@ def test_band_gather_two_ranks_on_one_gpu(gpu_ctx):
     for r in range(2):
         assert not isinstance(res[r], str), res[r]
         assert np.array_equal(res[r].reshape(3, 512, 256), ref), r
+
+
+@pytest.mark.parametrize("tile,yaw", [(16, 0.0), (8, 0.7), (32, -1.3)])
+def test_bands_bit_identical_sh3_and_tile_sizes(gpu_ctx, tile, yaw):
+    # The fused band pass (pre-cull, survivor queues, segment compaction) on an SH
+    # degree-3 cloud, a yawed camera and tile sizes other than 16.
+    from paper_2410_20686_b200 import GaussianCloud
+    arrs = oracle_lib.random_cloud(930 + tile, 20000)
+    sh = np.random.default_rng(tile).normal(0, 0.05, (15, 3, 20000)).astype(np.float32)
+    cloud = GaussianCloud.from_numpy(*arrs, sh_degree=3, sh_rest=sh)
+    cam = scenes.yaw_camera(yaw, 512, 256)
+    s = RenderSettings(tile_size=tile)
+    full = render(gpu_ctx, cloud, cam, s)
+    img, wk = full.image, full.walked
+    rows = 256 // 4 if tile != 32 else 64
+    for r0 in range(0, 256, rows):
+        fr = render_band(gpu_ctx, cloud, cam, s, r0, r0 + rows)
+        assert np.array_equal(fr.image[:, :, r0:r0 + rows], img[:, :, r0:r0 + rows])
+        assert np.array_equal(fr.walked[:, r0:r0 + rows], wk[:, r0:r0 + rows])
+
+
+def test_band_reports_non_finite_like_the_full_render(gpu_ctx):
+    from paper_2410_20686_b200 import OdgsRuntimeError
+    arrs = [np.array(a, dtype=np.float32) for a in oracle_lib.random_cloud(940, 5000)]
+    arrs[0][1, 1234] = np.nan  # a NaN mean: the pre-cull must pass it to the exact path
+    cloud = to_cloud32(arrs)
+    cam, s = CameraPose(256, 128), RenderSettings()
+    with pytest.raises(OdgsRuntimeError) as full_err:
+        render(gpu_ctx, cloud, cam, s)
+    with pytest.raises(OdgsRuntimeError) as band_err:
+        render_band(gpu_ctx, cloud, cam, s, 64, 96)
+    assert full_err.value.index == band_err.value.index == 1234
