@@ -376,7 +376,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if errs:
             raise errs[0]
 
-    e2e_run(max(args.warmup, 2))
+    e2e_run(max(args.warmup, 2) * len(lanes))  # every lane allocates its buffers before timing
     barrier()
     torch.cuda.synchronize()
     e2e_launch0 = sum(l[0].launch_count for l in lanes)
