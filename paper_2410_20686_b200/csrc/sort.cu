@@ -9,9 +9,12 @@
 //     the per-tile lists equal the reference's (rasterizer.hpp:158-205).
 //
 // Onesweep LSD radix sort: one kernel histograms all passes' digits, then one kernel
-// per pass ranks a 4096-item tile with warp-level ballot matching (stable), finds its
-// global offsets by decoupled look-back, and scatters through shared memory so the
-// writes are runs per digit. 16 B of traffic per item per pass (+4 B once).
+// per pass ranks a tile (4096 items for depth sorts, 6144 for tile-entry sorts) with
+// warp-level ballot matching (stable), publishes its digit counts, scatters through
+// shared memory, finds its global offsets by decoupled look-back, and writes runs per
+// digit. 16 B of traffic per item per pass (+4 B once). Every kernel is launched with
+// programmatic dependent launch (launch_pdl); the tile shapes and the look-back window
+// are compile-time knobs (ODGS_SORT_*) for A/B builds, defaults measured on the B200.
 #include <algorithm>
 
 #include "kernels.h"
@@ -135,10 +138,11 @@ __global__ void __launch_bounds__(kThreads) k_scan_downsweep(const uint32_t* __r
 // ------------------------------------------------------------------ onesweep (one kernel per pass)
 // Merrill & Adinets' single-pass LSD scheme: one kernel histograms every pass's
 // digits up front; each pass is then a single kernel in which a CTA claims the next
-// tile id (atomic counter, so every predecessor is already resident), ranks its 4096
-// items exactly like k_radix_downsweep, publishes its per-digit counts, and derives
-// its per-digit global offsets by decoupled look-back over the predecessors' status
-// words (flag in the top 2 bits: 1 = tile aggregate, 2 = inclusive prefix).
+// tile id (atomic counter, so every predecessor is already resident), ranks its
+// items, publishes its per-digit counts, and derives its per-digit global offsets by
+// decoupled look-back over the predecessors' status words (flag in the top 2 bits:
+// 1 = tile aggregate, 2 = inclusive prefix). Status words alternate between two
+// buffers: the histogram kernel clears the first pass's, each pass the next one's.
 constexpr uint32_t kStatAgg = 1u << 30;
 constexpr uint32_t kStatPrefix = 2u << 30;
 constexpr uint32_t kStatMask = (1u << 30) - 1u;
