@@ -570,13 +570,23 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     # Should the peer set-up fail, NCCL's all_gather is the fallback.
     gather, gathered, collective = None, None, "none"
     if world > 1:
+        failure = None
         try:
             from paper_2410_20686_b200.peers import BandGather
             gather = BandGather(ctx, fr, W, H, dev)
-            collective = "fused: blend writes its band into every rank's image over NVLink (CUDA IPC), 1 barrier"
         except Exception as e:  # noqa: BLE001 — reported in the JSON line
+            failure = type(e).__name__
+        # Every rank must take the same path: the fused gather only if it set up everywhere.
+        ok = torch.tensor([0 if failure else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 1:
+            collective = "fused: blend writes its band into every rank's image over NVLink (CUDA IPC), 1 barrier"
+        else:
+            if gather is not None:
+                gather.close()
+                gather = None
             gathered = torch.empty((world, 3, W, rows), dtype=torch.float32, device=dev)
-            collective = f"NCCL all_gather of the band images (peer set-up failed: {type(e).__name__})"
+            collective = f"NCCL all_gather of the band images (peer set-up failed: {failure or 'on another rank'})"
 
     def frame(k):
         render_band(ctx, cloud, scenes.yaw_camera(2 * math.pi * k / 16, W, H), settings, r0, r1, out=fr)
