@@ -210,8 +210,12 @@ odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_e
    ODGS_FRAME_PLAIN_BLEND. The caller synchronises the ranks before reading. */
 odgs_status odgs_frame_set_image_peers(odgs_frame* frame, int32_t n, void* const* peer_images);
 
-/* CUDA IPC (one process per GPU on a node): export a device allocation, open a peer's. */
-#define ODGS_IPC_HANDLE_BYTES 64
+/* CUDA IPC (one process per GPU on a node): export device memory, open a peer's. The
+   pointer may lie inside a larger allocation (e.g. a caching allocator's block): the
+   handle carries the cudaIpcMemHandle_t of the enclosing allocation (64 bytes) and the
+   pointer's byte offset in it (8 bytes); odgs_ipc_open returns base + offset, and
+   odgs_ipc_close takes that pointer. */
+#define ODGS_IPC_HANDLE_BYTES 72
 odgs_status odgs_ipc_get_handle(const void* device_ptr, void* handle);
 odgs_status odgs_ipc_open(const void* handle, void** device_ptr);
 odgs_status odgs_ipc_close(void* device_ptr);

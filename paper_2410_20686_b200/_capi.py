@@ -26,7 +26,7 @@ FRAME_KEEP_SPLAT_GRADS = 0x4
  FRAME_SPLAT_CLAMPED, FRAME_SPLATGRAD_MEAN, FRAME_SPLATGRAD_COV2D, FRAME_SPLATGRAD_OPACITY,
  FRAME_SPLATGRAD_COLOR) = range(20)
 
-IPC_HANDLE_BYTES = 64
+IPC_HANDLE_BYTES = 72
 
 STATUS_OK = 0
 STATUS_INVALID_ARGUMENT = 1

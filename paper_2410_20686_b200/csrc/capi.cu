@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "kernels.h"
 #include "odgs_b200.h"
 
@@ -697,26 +699,56 @@ odgs_status odgs_frame_set_image_peers(odgs_frame* f, int32_t n, void* const* pe
   return ODGS_OK;
 }
 
+// The enclosing allocation of a device pointer: the driver's cuMemGetAddressRange (the
+// runtime has no such query), fetched through the runtime so the library does not link
+// libcuda itself (it must load on hosts without a driver for the CPU checks).
+static bool alloc_base(const void* p, char** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (Fn) nullptr;
+    return reinterpret_cast<Fn>(f);
+  }();
+  CUdeviceptr b = 0;
+  size_t size = 0;
+  if (!fn || fn(&b, &size, (CUdeviceptr)p) != CUDA_SUCCESS) return false;
+  *base = reinterpret_cast<char*>(b);
+  return true;
+}
+
 odgs_status odgs_ipc_get_handle(const void* device_ptr, void* handle) {
   if (!device_ptr || !handle) return ODGS_ERR_INVALID_ARGUMENT;
+  char* base = nullptr;
+  if (!alloc_base(device_ptr, &base)) return ODGS_ERR_CUDA;
   cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)) != cudaSuccess) return ODGS_ERR_CUDA;
-  static_assert(sizeof(h) == ODGS_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  if (cudaIpcGetMemHandle(&h, base) != cudaSuccess) return ODGS_ERR_CUDA;
+  static_assert(sizeof(h) + sizeof(uint64_t) == ODGS_IPC_HANDLE_BYTES, "handle + offset");
+  const uint64_t offset = (uint64_t)(static_cast<const char*>(device_ptr) - base);
   std::memcpy(handle, &h, sizeof h);
+  std::memcpy(static_cast<char*>(handle) + sizeof h, &offset, sizeof offset);
   return ODGS_OK;
 }
 
 odgs_status odgs_ipc_open(const void* handle, void** device_ptr) {
   if (!handle || !device_ptr) return ODGS_ERR_INVALID_ARGUMENT;
   cudaIpcMemHandle_t h;
+  uint64_t offset = 0;
   std::memcpy(&h, handle, sizeof h);
-  if (cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return ODGS_ERR_CUDA;
+  std::memcpy(&offset, static_cast<const char*>(handle) + sizeof h, sizeof offset);
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return ODGS_ERR_CUDA;
+  *device_ptr = static_cast<char*>(base) + offset;
   return ODGS_OK;
 }
 
 odgs_status odgs_ipc_close(void* device_ptr) {
   if (!device_ptr) return ODGS_ERR_INVALID_ARGUMENT;
-  return cudaIpcCloseMemHandle(device_ptr) == cudaSuccess ? ODGS_OK : ODGS_ERR_CUDA;
+  char* base = nullptr;
+  if (!alloc_base(device_ptr, &base)) return ODGS_ERR_CUDA;
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? ODGS_OK : ODGS_ERR_CUDA;
 }
 
 odgs_status odgs_frame_set_flags(odgs_frame* f, uint32_t flags) {

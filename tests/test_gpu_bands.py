@@ -111,13 +111,17 @@ def _ipc_child(handle, q):
         q.put(repr(e))
 
 
-def test_band_written_into_another_process_buffer(gpu_ctx):
+@pytest.mark.parametrize("pad", [0, 12345])
+def test_band_written_into_another_process_buffer(gpu_ctx, pad):
     """CUDA IPC path of the fused band all-gather, two processes on one GPU: the child
-    renders rows [64, 192) straight into the parent's buffer."""
+    renders rows [64, 192) straight into the parent's buffer. pad > 0 exports a pointer
+    inside a larger allocation (as a caching allocator hands out): the handle carries the
+    offset, and the floats before it stay untouched."""
     import multiprocessing as mp
     import torch
     from paper_2410_20686_b200.peers import ipc_handle
-    buf = torch.full((3 * 512 * 256,), -1.0, device="cuda")
+    whole = torch.full((pad + 3 * 512 * 256,), -1.0, device="cuda")
+    buf = whole[pad:]
     torch.cuda.synchronize()
     h = ipc_handle(gpu_ctx.lib, buf.data_ptr())
     ctx_mp = mp.get_context("spawn")
@@ -131,6 +135,7 @@ def test_band_written_into_another_process_buffer(gpu_ctx):
     got = buf.cpu().numpy().reshape(3, 512, 256)
     assert np.array_equal(got[:, :, 64:192], ref[:, :, 64:192])
     assert np.all(got[:, :, :64] == -1.0) and np.all(got[:, :, 192:] == -1.0)
+    assert np.all(whole[:pad].cpu().numpy() == -1.0)
 
 
 def _gather_rank(rank, world, port, q):
