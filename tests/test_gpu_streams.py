@@ -77,3 +77,45 @@ def test_torch_reads_gradients_after_the_library():
         assert late > 0 and early == late
     finally:
         ctx.close()
+
+
+def test_concurrent_contexts_match_serial_renders():
+    """The e2e path of bench.py: several contexts (own streams, programmatic dependent
+    launches) rendering concurrently from host threads with a host-resident cloud give
+    the same images as one context rendering the same cameras one after another."""
+    import threading
+
+    from paper_2410_20686_b200 import RenderOutput, scenes
+    arrs = oracle_lib.random_cloud(95, 20000)
+    cloud = GaussianCloud.from_numpy(*arrs)
+    s = RenderSettings()
+    cams = [scenes.yaw_camera(0.4 * k, 512, 256) for k in range(8)]
+    serial = Context(0)
+    try:
+        ref = [render(serial, cloud, c, s).image.copy() for c in cams]
+    finally:
+        serial.close()
+    lanes = [Context(0) for _ in range(4)]
+    out = [None] * len(cams)
+    errs = []
+
+    def worker(li):
+        try:
+            fr = RenderOutput(lanes[li])
+            for k in range(li, len(cams), len(lanes)):
+                for _ in range(3):  # repeated frames into the same output
+                    render(lanes[li], cloud, cams[k], s, out=fr)
+                out[k] = fr.image.copy()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(len(lanes))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for c in lanes:
+        c.close()
+    assert not errs, errs
+    for k in range(len(cams)):
+        assert np.array_equal(out[k], ref[k]), k
