@@ -206,8 +206,9 @@ odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_e
    renders into each of these n <= 8 image buffers ([3][W][H] float, the frame's
    layout) — typically the other ranks' full-image buffers opened with odgs_ipc_open —
    so a band render all-gathers its rows over NVLink as it produces them. Pointers stay
-   in effect for later renders into this frame; n = 0 clears them. Not with
-   ODGS_FRAME_PLAIN_BLEND. The caller synchronises the ranks before reading. */
+   in effect for later renders into this frame; n = 0 clears them. Every blend path
+   (warp-culled or ODGS_FRAME_PLAIN_BLEND, any tile size) writes them. The caller
+   synchronises the ranks before reading. */
 odgs_status odgs_frame_set_image_peers(odgs_frame* frame, int32_t n, void* const* peer_images);
 
 /* CUDA IPC (one process per GPU on a node): export device memory, open a peer's. The
@@ -242,6 +243,21 @@ odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camer
    backward on a band frame returns that band's share of the gradient (bands add). */
 odgs_status odgs_render_band(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
                              const odgs_settings* settings, int32_t row_begin, int32_t row_end, odgs_frame* frame);
+
+/* The rasterization half of render (rasterizer.hpp:141-267) on caller-supplied
+   projected splats — the Splat2D records of RenderOutput::splats (projection.hpp:163-174)
+   of a cloud of n_gaussians rows — instead of projecting a cloud: seam instances, the
+   (depth, index, shift) order, tile CSR and the front-to-back blend, exactly as render()
+   continues after project_gaussian. Host arrays, one row per splat in ascending cloud
+   index: pixel_mean [ns][2], cov2d_inv [ns][4] row-major ((0,1) is used, as the
+   reference's d2), depth, radius, opacity [ns], color [ns][3]. Lets a caller (or a test)
+   feed splats projected elsewhere — e.g. by the libm reference — to the GPU stages.
+   Synchronizes. ODGS_ERR_INVALID_ARGUMENT (index = splat row) for unsorted or
+   out-of-range indices, non-finite values, negative depth or radius. */
+odgs_status odgs_rasterize_splats(odgs_ctx* ctx, int64_t n_gaussians, int64_t n_splats, const int64_t* index,
+                                  const float* pixel_mean, const float* cov2d_inv, const float* depth,
+                                  const float* radius, const float* opacity, const float* color, int32_t width,
+                                  int32_t height, const odgs_settings* settings, odgs_frame* frame);
 
 /* backward (backward.hpp:380-448) incl. grad_pixels_to_splats (:208-339) for the view
    rendered into `frame` (same cloud, camera, settings — unchecked, as in the

@@ -604,6 +604,8 @@ inline bool instance_box(const Splat2D<S>& splat, S shift, int width, int height
   return true;
 }
 
+template <class S> inline void bin_splats(RenderOutput<S>& out, const Settings<S>& settings);
+
 template <class S, class M = StdMath>
 inline RenderOutput<S> prepare_render(const Cloud<S>& cloud, const Camera<S>& camera,
                                       const Settings<S>& settings) {  // rasterizer.hpp:129-207
@@ -616,7 +618,14 @@ inline RenderOutput<S> prepare_render(const Cloud<S>& cloud, const Camera<S>& ca
   out.height = height;
   for (int64_t i = 0; i < cloud.n; ++i)
     if (auto s = project_gaussian<S, M>(cloud, i, camera, settings)) out.splats.push_back(*s);
+  bin_splats(out, settings);
+  return out;
+}
 
+// The rest of prepare_render once out.splats is filled (rasterizer.hpp:141-205): seam
+// instances, the (depth, index, shift) order and the tile CSR.
+template <class S> inline void bin_splats(RenderOutput<S>& out, const Settings<S>& settings) {
+  const int width = out.width, height = out.height;
   const S shifts[3] = {-S(width), S(0), S(width)};
   for (int s = 0; s < static_cast<int>(out.splats.size()); ++s) {
     int box[4];
@@ -660,14 +669,11 @@ inline RenderOutput<S> prepare_render(const Cloud<S>& cloud, const Camera<S>& ca
       for (int tx = span[0]; tx <= span[1]; ++tx)
         out.tile_entries[(std::size_t)(cursor[(std::size_t)(ty * out.tiles_x + tx)]++)] = e;
   }
-  return out;
 }
 
-template <class S, class M = StdMath>
-inline RenderOutput<S> render(const Cloud<S>& cloud, const Camera<S>& camera,
-                              const Settings<S>& settings) {  // rasterizer.hpp:211-267
-  RenderOutput<S> out = prepare_render<S, M>(cloud, camera, settings);
-  const int width = camera.width, height = camera.height;
+// The blend of render (rasterizer.hpp:216-267) over a prepared output.
+template <class S, class M = StdMath> inline void blend_tiles(RenderOutput<S>& out, const Settings<S>& settings) {
+  const int width = out.width, height = out.height;
   out.image.assign((std::size_t)3 * width * height, S(0));
   out.transmittance.assign((std::size_t)width * height, S(1));
   out.walked.assign((std::size_t)width * height, 0);
@@ -718,6 +724,27 @@ inline RenderOutput<S> render(const Cloud<S>& cloud, const Camera<S>& camera,
   });
   out.e_exam = std::accumulate(tile_exam.begin(), tile_exam.end(), int64_t(0));
   out.e_contrib = std::accumulate(tile_contrib.begin(), tile_contrib.end(), int64_t(0));
+}
+
+template <class S, class M = StdMath>
+inline RenderOutput<S> render(const Cloud<S>& cloud, const Camera<S>& camera,
+                              const Settings<S>& settings) {  // rasterizer.hpp:211-267
+  RenderOutput<S> out = prepare_render<S, M>(cloud, camera, settings);
+  blend_tiles<S, M>(out, settings);
+  return out;
+}
+
+// Sort, bin and blend given splats (the stages of render after projection): what
+// odgs_rasterize_splats computes on the GPU.
+template <class S, class M = StdMath>
+inline RenderOutput<S> rasterize_splats(const std::vector<Splat2D<S>>& splats, int width, int height,
+                                        const Settings<S>& settings) {
+  RenderOutput<S> out;
+  out.width = width;
+  out.height = height;
+  out.splats = splats;
+  bin_splats(out, settings);
+  blend_tiles<S, M>(out, settings);
   return out;
 }
 

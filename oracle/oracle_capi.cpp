@@ -248,6 +248,26 @@ int64_t oracle_get(void* handle, const char* which, void* dst) {
   return get_from(h->rf, h->gf, h->sgf, h->have_grads, h->brute, w, dst);
 }
 
+// Sorts, bins and blends the splats of an existing float frame (rasterize_splats, i.e.
+// the stages after projection) with StdMath (portable = 0) or PortableMath blending.
+int oracle_rasterize_splats(void* handle, int portable, void** out, char* err, int errlen) {
+  Handle* src = static_cast<Handle*>(handle);
+  if (src->dbl) return fail(err, errlen, 1, "rasterize_splats: float frames only");
+  auto h = std::make_unique<Handle>();
+  const int rc = guarded(err, errlen, [&] {
+    h->portable = portable != 0;
+    h->sf = src->sf;
+    h->camf = src->camf;
+    h->cf = src->cf;
+    if (portable)
+      h->rf = rasterize_splats<float, PortableMath>(src->rf.splats, src->rf.width, src->rf.height, src->sf);
+    else
+      h->rf = rasterize_splats<float, StdMath>(src->rf.splats, src->rf.width, src->rf.height, src->sf);
+  });
+  if (rc == 0) *out = h.release();
+  return rc;
+}
+
 void oracle_free(void* handle) { delete static_cast<Handle*>(handle); }
 
 // scenes::random_cloud (proj/tests/scenes.hpp:20-51) with the given bounds

@@ -6,10 +6,10 @@ rasterizer API over that ABI.
 """
 from .rasterizer import (CameraPose, Context, DomainError, GaussianCloud, GradBuffers, InvalidArgument,
                          OdgsError, OdgsRuntimeError, RenderOutput, RenderSettings, backward, cull,
-                         prepare_render, render, render_band)
+                         prepare_render, rasterize_splats, render, render_band)
 from .densify import DensifyConfig, DensifyStats, Rng, TrainState, densify_and_prune, dynamic_threshold, reset_opacity
 
 __all__ = ["CameraPose", "Context", "DomainError", "GaussianCloud", "GradBuffers", "InvalidArgument",
            "OdgsError", "OdgsRuntimeError", "RenderOutput", "RenderSettings", "backward", "cull",
-           "prepare_render", "render", "render_band", "DensifyConfig", "DensifyStats", "Rng", "TrainState",
+           "prepare_render", "rasterize_splats", "render", "render_band", "DensifyConfig", "DensifyStats", "Rng", "TrainState",
            "densify_and_prune", "dynamic_threshold", "reset_opacity"]

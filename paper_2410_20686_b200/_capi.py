@@ -122,6 +122,8 @@ SIGNATURES = {
     "odgs_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
     "odgs_render_band": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), C.c_int32,
                                    C.c_int32, _P]),
+    "odgs_rasterize_splats": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, _P, _P, _P, _P, C.c_int32,
+                                        C.c_int32, C.POINTER(Settings), _P]),
     "odgs_backward": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), _P, _P, C.c_int32,
                                 C.POINTER(Settings), C.POINTER(Grads), C.POINTER(C.c_double), C.c_uint32]),
     "odgs_ctx_set_profiling": (C.c_int, [_P, C.c_int]),

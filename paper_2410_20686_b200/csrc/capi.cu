@@ -71,6 +71,7 @@ struct odgs_frame {
   int64_t n_splats = 0, n_instances = 0;
   int32_t row_begin = 0, row_end = 0;
   bool prepared = false, rendered = false, have_splat_grads = false;
+  bool from_splats = false;  // odgs_rasterize_splats: no cloud or camera behind the splats
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
   DevBuf ekeys[2], evals[2], offsets, tile_order, image, trans, walked, records, touched, folded, splat_grads, work;
   int depth_which = 0, tile_which = 0;
@@ -291,6 +292,27 @@ odgs_status reset_errors(odgs_ctx* ctx) {
   return ODGS_OK;
 }
 
+odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band);
+
+// Per-frame buffers of the projection stage (n Gaussians, n_tiles tiles).
+odgs_status ensure_frame_buffers(odgs_ctx* ctx, odgs_frame* f, int64_t n, uint32_t n_tiles) {
+  cudaStream_t s = ctx->stream;
+  ODGS_CUDA(ctx, ensure(f->sp_ab, sizeof(float4) * 2 * n, s));
+  ODGS_CUDA(ctx, ensure(f->sp_c, sizeof(float4) * n, s));
+  if (f->flags & ODGS_FRAME_KEEP_COV2D) ODGS_CUDA(ctx, ensure(f->cov, sizeof(float4) * n, s));
+  for (int k = 0; k < 2; ++k) {
+    ODGS_CUDA(ctx, ensure(f->keys[k], sizeof(uint32_t) * n, s));
+    ODGS_CUDA(ctx, ensure(f->vals[k], sizeof(uint32_t) * n, s));
+  }
+  ODGS_CUDA(ctx, ensure(f->cnt, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->cnt_sorted, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->off_sorted, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->ent_off_idx, sizeof(uint32_t) * n, s));
+  ODGS_CUDA(ctx, ensure(f->scan_tmp, scan_temp_bytes(n) + 256, s));
+  ODGS_CUDA(ctx, ensure(f->offsets, sizeof(int32_t) * (n_tiles + 1), s));
+  return ODGS_OK;
+}
+
 odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
                          const odgs_settings* settings, odgs_frame* f, int32_t row_begin = 0,
                          int32_t row_end = -1) {
@@ -302,6 +324,7 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   if ((st = resolve_cloud(ctx, cloud, &cp)) != ODGS_OK) return st;
   cudaStream_t s = ctx->stream;
   f->prepared = f->rendered = f->have_splat_grads = false;
+  f->from_splats = false;
   f->width = camera->width;
   f->height = camera->height;
   f->tile_size = settings->tile_size;
@@ -322,19 +345,7 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   const int64_t n = f->n;
   const uint32_t n_tiles = (uint32_t)(f->tiles_x * f->tiles_y);
 
-  ODGS_CUDA(ctx, ensure(f->sp_ab, sizeof(float4) * 2 * n, s));
-  ODGS_CUDA(ctx, ensure(f->sp_c, sizeof(float4) * n, s));
-  if (f->flags & ODGS_FRAME_KEEP_COV2D) ODGS_CUDA(ctx, ensure(f->cov, sizeof(float4) * n, s));
-  for (int k = 0; k < 2; ++k) {
-    ODGS_CUDA(ctx, ensure(f->keys[k], sizeof(uint32_t) * n, s));
-    ODGS_CUDA(ctx, ensure(f->vals[k], sizeof(uint32_t) * n, s));
-  }
-  ODGS_CUDA(ctx, ensure(f->cnt, sizeof(uint32_t) * n, s));
-  ODGS_CUDA(ctx, ensure(f->cnt_sorted, sizeof(uint32_t) * n, s));
-  ODGS_CUDA(ctx, ensure(f->off_sorted, sizeof(uint32_t) * n, s));
-  ODGS_CUDA(ctx, ensure(f->ent_off_idx, sizeof(uint32_t) * n, s));
-  ODGS_CUDA(ctx, ensure(f->scan_tmp, scan_temp_bytes(n) + 256, s));
-  ODGS_CUDA(ctx, ensure(f->offsets, sizeof(int32_t) * (n_tiles + 1), s));
+  if ((st = ensure_frame_buffers(ctx, f, n, n_tiles)) != ODGS_OK) return st;
   if ((st = reset_errors(ctx)) != ODGS_OK) return st;
 
   const bool band = f->settings.band_ty0 > 0 || f->settings.band_ty1 < f->tiles_y;
@@ -374,6 +385,17 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
     }
   }
 
+  return bin_impl(ctx, f, band);
+}
+
+// The part of prepare_render after projection (rasterizer.hpp:141-205): depth sort,
+// tile-entry emission, tile sort, CSR, launch order. f->sp_ab / sp_c / keys[0] / vals[0]
+// / cnt hold the projected splats (or, for a band, the compacted band survivors).
+odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
+  odgs_status st;
+  cudaStream_t s = ctx->stream;
+  const int64_t n = f->n;
+  const uint32_t n_tiles = (uint32_t)(f->tiles_x * f->tiles_y);
   // Depth sort of the Gaussians (key: depth bits; culled sort last). A band render
   // sorts only the Gaussians with entries in its rows, compacted in index order above
   // (stable, so ties keep index order): the tile lists are unchanged, the sort shrinks
@@ -393,8 +415,12 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   {
     int which = 0;
     // The last pass also gathers each rank's tile count (cnt_sorted).
-    radix_sort_pairs(dk, dv, m, 0, 32, f->sort_tmp.p, &which, s, f->cnt.as<uint32_t>(),
-                     f->cnt_sorted.as<uint32_t>());
+    const cudaError_t e = radix_sort_pairs(dk, dv, m, 0, 32, f->sort_tmp.p, &which, s, f->cnt.as<uint32_t>(),
+                                           f->cnt_sorted.as<uint32_t>());
+    if (e != cudaSuccess) {
+      delete depth_scope;
+      return cuda_fail(ctx, e, "depth sort");
+    }
     f->depth_which = which;  // index into f->vals / f->keys
   }
   delete depth_scope;
@@ -456,7 +482,7 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   uint32_t* ev[2] = {f->evals[0].as<uint32_t>(), f->evals[1].as<uint32_t>()};
   {
     StageScope sc(ctx, ODGS_STAGE_TILE_SORT);
-    radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s);
+    ODGS_CUDA(ctx, radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s));
   }
   {
     StageScope sc(ctx, ODGS_STAGE_RANGES);
@@ -792,6 +818,72 @@ odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camer
   return st;
 }
 
+odgs_status odgs_rasterize_splats(odgs_ctx* ctx, int64_t n_gaussians, int64_t n_splats, const int64_t* index,
+                                  const float* pixel_mean, const float* cov2d_inv, const float* depth,
+                                  const float* radius, const float* opacity, const float* color, int32_t width,
+                                  int32_t height, const odgs_settings* settings, odgs_frame* f) {
+  LaunchScope scope(ctx);
+  if (!ctx || !f) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  odgs_status st;
+  if ((st = check_settings(ctx, settings)) != ODGS_OK) return st;
+  if (width <= 0 || height <= 0 || width != 2 * height || (int64_t)width * height > ((int64_t)1 << 31))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "rasterize_splats: bad image size");
+  if (n_gaussians < 0 || n_gaussians >= ((int64_t)1 << 30) || n_splats < 0 || n_splats > n_gaussians)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "rasterize_splats: bad sizes");
+  if (n_splats > 0 && !(index && pixel_mean && cov2d_inv && depth && radius && opacity && color))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "rasterize_splats: null splat arrays");
+  // Host-side checks and packing (kSplatRecord floats per splat).
+  std::vector<float> rec((size_t)n_splats * kSplatRecord);
+  for (int64_t k = 0; k < n_splats; ++k) {
+    const int64_t i = index[k];
+    if (i < 0 || i >= n_gaussians || (k > 0 && i <= index[k - 1]))
+      return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, k, "rasterize_splats: indices must ascend inside the cloud");
+    const float v[11] = {pixel_mean[2 * k], pixel_mean[2 * k + 1], cov2d_inv[4 * k], cov2d_inv[4 * k + 1],
+                         cov2d_inv[4 * k + 3], depth[k], radius[k], opacity[k], color[3 * k], color[3 * k + 1],
+                         color[3 * k + 2]};
+    for (float x : v)
+      if (!std::isfinite(x))
+        return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, k, "rasterize_splats: non-finite splat");
+    if (!(depth[k] >= 0.0f) || !(radius[k] >= 0.0f))
+      return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, k, "rasterize_splats: negative depth or radius");
+    float* r = rec.data() + (size_t)k * kSplatRecord;
+    const uint32_t bits = (uint32_t)i;
+    std::memcpy(r, &bits, 4);
+    std::memcpy(r + 1, v, sizeof v);
+  }
+  cudaStream_t s = ctx->stream;
+  f->prepared = f->rendered = f->have_splat_grads = false;
+  f->from_splats = true;
+  f->width = width;
+  f->height = height;
+  f->tile_size = settings->tile_size;
+  f->tiles_x = (width + f->tile_size - 1) / f->tile_size;
+  f->tiles_y = (height + f->tile_size - 1) / f->tile_size;
+  f->n = n_gaussians;
+  f->cam = DevCamera{};
+  f->cam.width = width;
+  f->cam.height = height;
+  f->settings = to_dev(*settings);
+  f->row_begin = 0;
+  f->row_end = height;
+  f->settings.band_ty0 = 0;
+  f->settings.band_ty1 = f->tiles_y;
+  if ((st = ensure_frame_buffers(ctx, f, n_gaussians, (uint32_t)(f->tiles_x * f->tiles_y))) != ODGS_OK) return st;
+  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+  ODGS_CUDA(ctx, ensure(ctx->misc_buf, rec.size() * sizeof(float), s));
+  if (!rec.empty())
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->misc_buf.p, rec.data(), rec.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  launch_load_splats(n_gaussians, n_splats, ctx->misc_buf.as<float>(), width, height, f->tile_size, f->sp_ab.as<float4>(),
+                     f->sp_c.as<float4>(), f->keys[0].as<uint32_t>(), f->vals[0].as<uint32_t>(),
+                     f->cnt.as<uint32_t>(), ctx->d_err, s);
+  if ((st = bin_impl(ctx, f, false)) != ODGS_OK) return st;
+  ODGS_CUDA(ctx, cudaStreamSynchronize(s));  // the packed records live in host memory until here
+  st = blend_impl(ctx, f);
+  if (ctx->timers.enabled) resolve_timers(ctx);
+  return st;
+}
+
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_examined, int64_t* entries_composited) {
   if (!ctx || !f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not rendered");
   unsigned long long w[2];
@@ -951,6 +1043,8 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   if (!f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: frame not rendered");
+  if (f->from_splats)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: frame of odgs_rasterize_splats has no cloud");
   if (!grads || !dl_dimage) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: null buffers");
   odgs_status st;
   if ((st = check_camera(ctx, camera)) != ODGS_OK) return st;
@@ -1360,7 +1454,7 @@ odgs_status odgs_init_from_points(odgs_ctx* ctx, int64_t n, const double* positi
   uint32_t* kk[2] = {k0.as<uint32_t>(), k1.as<uint32_t>()};
   uint32_t* vv[2] = {v0.as<uint32_t>(), v1.as<uint32_t>()};
   int which = 0;
-  radix_sort_pairs(kk, vv, n, 0, bits_for(g.n_cells + 1u), tmp_b.p, &which, s);
+  ODGS_CUDA(ctx, radix_sort_pairs(kk, vv, n, 0, bits_for(g.n_cells + 1u), tmp_b.p, &which, s));
   launch_gather_xyz(n, vv[which], dpos, xyz_b.as<double>(), s);
   launch_cell_ranges(m, kk[which], g.n_cells, cells_b.as<uint32_t>(), s);
 

@@ -38,6 +38,12 @@ void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_
 // Concatenates the segments at seg_off (exclusive scan of seg_count).
 void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t* seg_off, const uint32_t* seg_keys,
                             const uint32_t* seg_vals, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream);
+// Caller-supplied splats (odgs_rasterize_splats): kSplatRecord floats per splat, the
+// first holding the cloud row's bits; rows without a splat are culled.
+constexpr int kSplatRecord = 12;
+void launch_load_splats(int64_t n, int64_t n_splats, const float* rec, int width, int height, int tile_size,
+                        float4* sp_ab, float4* sp_c, uint32_t* keys, uint32_t* vals, uint32_t* cnt, DevErrors* err,
+                        cudaStream_t stream);
 struct EmitArgs {
   int64_t n;
   const uint32_t *sorted_idx, *cnt_sorted, *off_sorted;
@@ -89,14 +95,19 @@ size_t scan_temp_bytes(int64_t n);
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp, unsigned long long* total64,
                         cudaStream_t stream);
 
+// Sorts hold fewer than 2^30 items: the onesweep look-back words carry 30-bit counts.
+constexpr unsigned long long kMaxSortItems = 1ull << 30;
+
 size_t radix_sort_temp_bytes(int64_t n);
 // Stable LSD radix sort of (key, value) pairs on key bits [begin_bit, end_bit).
 // keys/vals: [2] ping-pong buffers of n each; on return *which (0/1) holds the result.
 // Optional payload gather: gather_dst[r] = gather_src[sorted value r], written by the
 // last pass (saves a separate gather over the sorted values).
-void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
-                      int* which, cudaStream_t stream, const uint32_t* gather_src = nullptr,
-                      uint32_t* gather_dst = nullptr);
+// Returns the first failed launch's error (the remaining passes are then not launched:
+// they would look back over status words nobody cleared).
+cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit,
+                             void* temp, int* which, cudaStream_t stream, const uint32_t* gather_src = nullptr,
+                             uint32_t* gather_dst = nullptr);
 
 // ------------------------------------------------------------------ training step
 size_t l1_loss_temp_bytes(int64_t count);

@@ -733,6 +733,7 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
     }
     // means = R^T dmu
     for (int c = 0; c < 3; ++c) gm[c] = Rc.a[0][c] * dmu[0] + (Rc.a[1][c] * dmu[1] + Rc.a[2][c] * dmu[2]);
+    bool sh_finite = true;
     if (a.sh_degree > 0) {  // SH extension: coefficient gradients and the view-direction term
       const int nb = sh_count(a.sh_degree);
       float d[3], Y[15], dY[15][3];
@@ -744,6 +745,7 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
         for (int ch = 0; ch < 3; ++ch) {
           const int64_t idx = (int64_t)(3 * k + ch) * n + i;
           const float g = r[6 + ch] * Y[k];
+          sh_finite = sh_finite && isfinite(g);
           if (a.accumulate) a.g_sh_rest[idx] += g;
           else a.g_sh_rest[idx] = g;
           const float w = r[6 + ch] * a.sh_rest[idx];
@@ -800,7 +802,7 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
     for (int k = 0; k < 3; ++k) all[7 + k] = gls[k];
     all[10] = gop;
     for (int k = 0; k < 3; ++k) all[11 + k] = gcol[k];
-    if (!all_finite(all, 14)) atomic_min_error(&a.err->bwd_nonfinite, i, 2);
+    if (!all_finite(all, 14) || !sh_finite) atomic_min_error(&a.err->bwd_nonfinite, i, 2);
   }
   if (a.sh_degree > 0 && !(flags & kFlagVisible) && !a.accumulate)
     for (int k = 0; k < 3 * sh_count(a.sh_degree); ++k) a.g_sh_rest[(int64_t)k * n + i] = 0.0f;

@@ -165,6 +165,66 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   ++g_launches;
 }
 
+// ------------------------------------------------------------------ given splats
+// odgs_rasterize_splats: the per-Gaussian outputs of preprocess from caller-supplied
+// projected splats (Splat2D records, projection.hpp:163-174) instead of a projection.
+// k_clear_rows culls every row; k_load_splats then fills the rows of the splats.
+__global__ void k_clear_rows(int64_t n, float4* __restrict__ sp_c, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt) {
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  sp_c[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+  keys[i] = kCulledKey;
+  vals[i] = (uint32_t)i;
+  cnt[i] = 0;
+}
+
+__global__ void k_load_splats(int64_t n_splats, const float* __restrict__ rec, int width, int height,
+                              int tile_size, float4* __restrict__ sp_ab, float4* __restrict__ sp_c,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err) {
+  pdl_wait();
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t n_inst = 0;
+  if (s < n_splats) {
+    const float* r = rec + s * kSplatRecord;  // index bits, mx, my, i00, i01, i11, depth, radius, opacity, rgb
+    const uint32_t i = __float_as_uint(r[0]);
+    const float mx = r[1], my = r[2], radius = r[7];
+    uint32_t flags = kFlagVisible, total = 0;
+    for (int k = 0; k < 3; ++k) {
+      int span[4];
+      if (instance_tiles(mx, my, radius, k, width, height, tile_size, span)) {
+        flags |= kFlagShiftBase << k;
+        ++n_inst;
+        total += (uint32_t)(span[1] - span[0] + 1) * (uint32_t)(span[3] - span[2] + 1);
+      }
+    }
+    sp_ab[2 * (int64_t)i] = make_float4(mx, my, r[3], r[4]);
+    sp_ab[2 * (int64_t)i + 1] = make_float4(r[5], r[8], r[9], r[10]);
+    sp_c[i] = make_float4(r[11], r[6], radius, __uint_as_float(flags));
+    keys[i] = __float_as_uint(r[6]);
+    cnt[i] = total;
+  }
+  const uint32_t v_sum = __reduce_add_sync(0xffffffffu, s < n_splats ? 1u : 0u);
+  const uint32_t i_sum = __reduce_add_sync(0xffffffffu, n_inst);
+  if ((threadIdx.x & 31) == 0 && (v_sum | i_sum)) {
+    atomicAdd(&err->n_visible, (unsigned long long)v_sum);
+    atomicAdd(&err->n_instances, (unsigned long long)i_sum);
+  }
+}
+
+void launch_load_splats(int64_t n, int64_t n_splats, const float* rec, int width, int height, int tile_size,
+                        float4* sp_ab, float4* sp_c, uint32_t* keys, uint32_t* vals, uint32_t* cnt, DevErrors* err,
+                        cudaStream_t stream) {
+  if (n == 0) return;
+  launch_pdl(k_clear_rows, (unsigned)((n + 255) / 256), 256, 0, stream, n, sp_c, keys, vals, cnt);
+  ++g_launches;
+  if (n_splats == 0) return;
+  launch_pdl(k_load_splats, (unsigned)((n_splats + 255) / 256), 256, 0, stream, n_splats, rec, width, height,
+             tile_size, sp_ab, sp_c, keys, cnt, err);
+  ++g_launches;
+}
+
 // ------------------------------------------------------------------ band pre-cull
 // Row-band renders: a conservative float test finds the Gaussians whose instance boxes
 // certainly miss the band's pixel rows; they get the culled outputs and skip the exact
@@ -202,18 +262,29 @@ __device__ __forceinline__ BandCull make_band_cull(const DevCamera& cam, const D
 
 __device__ __forceinline__ bool band_survives(int64_t i, int64_t n, const float* __restrict__ means,
                                               const float* __restrict__ rotations,
-                                              const float* __restrict__ log_scales, const DevCamera& cam,
+                                              const float* __restrict__ log_scales,
+                                              const float* __restrict__ raw_opacities,
+                                              const float* __restrict__ colors, int n_sh,
+                                              const float* __restrict__ sh_rest, const DevCamera& cam,
                                               const DevSettings& s, const BandCull& b) {
   const float p[3] = {__ldg(means + i), __ldg(means + n + i), __ldg(means + 2 * n + i)};
   const float q[4] = {__ldg(rotations + i), __ldg(rotations + n + i), __ldg(rotations + 2 * n + i),
                       __ldg(rotations + 3 * n + i)};
   const float ls[3] = {__ldg(log_scales + i), __ldg(log_scales + n + i), __ldg(log_scales + 2 * n + i)};
+  // Every parameter of the row is checked (first_non_finite, rasterizer.hpp:133-136): a
+  // non-finite value anywhere sends the row to the exact path, which reports it, so a
+  // band render fails exactly where the full render does. A sum of the parameters is
+  // non-finite if any of them is (an overflow to inf only costs a needless survivor).
+  float fin = ((p[0] + p[1]) + (p[2] + q[0])) + ((q[1] + q[2]) + (q[3] + ls[0]));
+  fin += (ls[1] + ls[2]) + (__ldg(raw_opacities + i) +
+                            ((__ldg(colors + i) + __ldg(colors + n + i)) + __ldg(colors + 2 * n + i)));
+  for (int k = 0; k < n_sh; ++k) fin += __ldg(sh_rest + (int64_t)k * n + i);
   float mu[3];
   to_camera(cam, p, mu);
   const float sq = sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]);
   const float depth = sqrtf(sq);
   const float qq = sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]);
-  if (!(sq > 0.0f && qq > 1e-20f && isfinite(depth))) return true;
+  if (!(sq > 0.0f && qq > 1e-20f && isfinite(depth) && isfinite(fin))) return true;
   // shell-culled: the exact path would produce the same culled outputs
   if (!(depth >= s.near_radius && depth <= s.far_radius)) return false;
   const float inv_d = 1.0f / depth;
@@ -267,6 +338,7 @@ __global__ void __launch_bounds__(256, 3) k_band_preprocess(
   uint32_t head = 0, tail = 0;
   uint32_t out_len = 0, n_surv = 0, n_vis = 0, n_inst = 0;
   const BandCull bc = make_band_cull(cam, s);
+  const int n_sh = sh_degree > 0 ? 3 * sh_count(sh_degree) : 0;
   // Projects the next `count` queued survivors (one per lane) and appends the pairs
   // with band entries.
   auto drain = [&](uint32_t count) {
@@ -297,7 +369,8 @@ __global__ void __launch_bounds__(256, 3) k_band_preprocess(
     for (int u = 0; u < kBandUnroll; ++u) {
       const int64_t i = c + u * 32 + lane;
       // clamped index: unconditional loads, all kBandUnroll groups in flight
-      sv[u] = band_survives(min(i, end - 1), n, means, rotations, log_scales, cam, s, bc) && i < end;
+      sv[u] = band_survives(min(i, end - 1), n, means, rotations, log_scales, raw_opacities, colors, n_sh, sh_rest,
+                            cam, s, bc) && i < end;
     }
 #pragma unroll
     for (int u = 0; u < kBandUnroll; ++u) {

@@ -16,6 +16,7 @@
 // programmatic dependent launch (launch_pdl); the tile shapes and the look-back window
 // are compile-time knobs (ODGS_SORT_*) for A/B builds, defaults measured on the B200.
 #include <algorithm>
+#include <atomic>
 
 #include "kernels.h"
 
@@ -406,47 +407,59 @@ struct PassArgs {
   uint32_t* status_next;
 };
 
+// The dynamic shared-memory opt-in is a per-device function attribute: one flag bit per
+// device and instantiation, set once (racing threads at worst set it twice).
+template <class Kern> cudaError_t opt_in_smem(Kern kern, size_t smem) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 template <int Threads, int IPT, int MinBlocks, int Bits>
-void launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
+cudaError_t launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
   constexpr int kT = Threads * IPT;
   constexpr size_t smem = (size_t)(2 * kT + (Threads / 32) * 256) * sizeof(uint32_t);
   auto kern = k_onesweep_pass<Threads, IPT, MinBlocks, Bits>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  const cudaError_t e = opt_in_smem(kern, smem);
+  if (e != cudaSuccess) return e;
   const int64_t tiles = (a.n + kT - 1) / kT;
-  launch_pdl(kern, (unsigned)tiles, Threads, smem, stream, a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n, a.shift,
-                                                   a.digit_start, a.status, a.tile_counter, a.gather_src,
-                                                   a.gather_dst, a.status_next);
+  return launch_pdl(kern, (unsigned)tiles, Threads, smem, stream, a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n,
+                    a.shift, a.digit_start, a.status, a.tile_counter, a.gather_src, a.gather_dst, a.status_next);
 }
 
 template <int Threads, int IPT, int MinBlocks>
-void launch_pass(int bits, const PassArgs& a, cudaStream_t stream) {
+cudaError_t launch_pass(int bits, const PassArgs& a, cudaStream_t stream) {
   switch (bits) {
-    case 1: launch_pass_bits<Threads, IPT, MinBlocks, 1>(a, stream); break;
-    case 2: launch_pass_bits<Threads, IPT, MinBlocks, 2>(a, stream); break;
-    case 3: launch_pass_bits<Threads, IPT, MinBlocks, 3>(a, stream); break;
-    case 4: launch_pass_bits<Threads, IPT, MinBlocks, 4>(a, stream); break;
-    case 5: launch_pass_bits<Threads, IPT, MinBlocks, 5>(a, stream); break;
-    case 6: launch_pass_bits<Threads, IPT, MinBlocks, 6>(a, stream); break;
-    case 7: launch_pass_bits<Threads, IPT, MinBlocks, 7>(a, stream); break;
-    default: launch_pass_bits<Threads, IPT, MinBlocks, 8>(a, stream); break;
+    case 1: return launch_pass_bits<Threads, IPT, MinBlocks, 1>(a, stream);
+    case 2: return launch_pass_bits<Threads, IPT, MinBlocks, 2>(a, stream);
+    case 3: return launch_pass_bits<Threads, IPT, MinBlocks, 3>(a, stream);
+    case 4: return launch_pass_bits<Threads, IPT, MinBlocks, 4>(a, stream);
+    case 5: return launch_pass_bits<Threads, IPT, MinBlocks, 5>(a, stream);
+    case 6: return launch_pass_bits<Threads, IPT, MinBlocks, 6>(a, stream);
+    case 7: return launch_pass_bits<Threads, IPT, MinBlocks, 7>(a, stream);
+    default: return launch_pass_bits<Threads, IPT, MinBlocks, 8>(a, stream);
   }
 }
 
 }  // namespace
 
-void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit, void* temp,
-                      int* which, cudaStream_t stream, const uint32_t* gather_src, uint32_t* gather_dst) {
+cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit,
+                             void* temp, int* which, cudaStream_t stream, const uint32_t* gather_src,
+                             uint32_t* gather_dst) {
   *which = 0;
+  if (n >= (int64_t)kMaxSortItems) return cudaErrorInvalidValue;
   if (n <= 1 || end_bit <= begin_bit) {
     if (gather_dst && n > 0) {
-      launch_pdl(k_gather, (unsigned)((n + 255) / 256), 256, 0, stream, n, vals[0], gather_src, gather_dst);
       ++g_launches;
+      return launch_pdl(k_gather, (unsigned)((n + 255) / 256), 256, 0, stream, n, vals[0], gather_src, gather_dst);
     }
-    return;
+    return cudaSuccess;
   }
   PassPlan plan{};
   int passes = (end_bit - begin_bit + 7) / 8;
@@ -463,14 +476,17 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
   uint32_t* counters = hist + kMaxPasses * 256;
   const int64_t tiles = pass_tiles(n);
   uint32_t* status[2] = {counters + 64, counters + 64 + tiles * 256};
-  // The passes spin on look-back words: never launch them after a failed set-up launch.
-  if (launch_pdl(k_zero_u32, 1, 256, 0, stream, hist, kMaxPasses * 256 + 64) != cudaSuccess) return;
+  // The passes spin on look-back words: never launch one after a failed launch.
+  cudaError_t e = launch_pdl(k_zero_u32, 1, 256, 0, stream, hist, kMaxPasses * 256 + 64);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   int sms = 148;
-  const cudaError_t hist_err = launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0,
-                                          stream, keys[0], n, plan, hist, status[0], tiles * 256);
+  e = launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream, keys[0], n, plan,
+                 hist, status[0], tiles * 256);
+  if (e != cudaSuccess) return e;
   ++g_launches;
-  if (hist_err != cudaSuccess || launch_pdl(k_onesweep_hist_scan, passes, 256, 0, stream, hist) != cudaSuccess) return;
+  e = launch_pdl(k_onesweep_hist_scan, passes, 256, 0, stream, hist);
+  if (e != cudaSuccess) return e;
   ++g_launches;
   const bool big = n > kBigSort;
   int cur = 0;
@@ -479,14 +495,14 @@ void radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin
     PassArgs pa{keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, plan.shift[p], hist + p * 256,
                 status[p & 1], counters + p, last ? gather_src : nullptr, last ? gather_dst : nullptr,
                 last ? nullptr : status[(p + 1) & 1]};
-    if (big)
-      launch_pass<kBigThreads, kBigIPT, kBigMinBlocks>(plan.bits[p], pa, stream);
-    else
-      launch_pass<kThreads, kSmallIPT, kSmallMinBlocks>(plan.bits[p], pa, stream);
+    e = big ? launch_pass<kBigThreads, kBigIPT, kBigMinBlocks>(plan.bits[p], pa, stream)
+            : launch_pass<kThreads, kSmallIPT, kSmallMinBlocks>(plan.bits[p], pa, stream);
+    if (e != cudaSuccess) return e;
     ++g_launches;
     cur ^= 1;
   }
   *which = cur;
+  return cudaSuccess;
 }
 
 }  // namespace odgs_b200

@@ -382,6 +382,23 @@ def render(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: Ren
     return out
 
 
+def rasterize_splats(ctx: Context, n_gaussians: int, index, pixel_mean, cov2d_inv, depth, radius, opacity, color,
+                     width: int, height: int, settings: RenderSettings,
+                     out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
+    """The rasterization half of render() (rasterizer.hpp:141-267) on given projected
+    splats (RenderOutput::splats rows, ascending cloud index): seam instances, global
+    order, tile CSR and blend. Arrays: index (ns,), pixel_mean (ns, 2), cov2d_inv (ns, 4)
+    row-major, depth / radius / opacity (ns,), color (ns, 3)."""
+    out = out or RenderOutput(ctx, flags)
+    idx = np.ascontiguousarray(index, dtype=np.int64)
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+    arrs = [f(pixel_mean), f(cov2d_inv), f(depth), f(radius), f(opacity), f(color)]
+    st = settings.to_c()
+    ctx.check(ctx.lib.odgs_rasterize_splats(ctx.handle, int(n_gaussians), idx.shape[0], idx.ctypes.data,
+                                            *[a.ctypes.data for a in arrs], width, height, C.byref(st), out.handle))
+    return out
+
+
 def render_band(ctx: Context, cloud: GaussianCloud, camera: CameraPose, settings: RenderSettings, row_begin: int,
                 row_end: int, out: Optional[RenderOutput] = None, flags: int = 0) -> RenderOutput:
     """Rows [row_begin, row_end) of render(); bit-identical to the full render there."""
@@ -398,8 +415,9 @@ def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: Render
              settings: RenderSettings, signs=None, grads: Optional[GradBuffers] = None,
              accumulate: bool = False) -> GradBuffers:
     grads = grads or GradBuffers.zeros(cloud.n, cloud.sh_degree)
-    if cloud.on_device or (_is_torch(dl_dimage) and dl_dimage.is_cuda):
-        ctx.wait_torch()
+    if (cloud.on_device or (_is_torch(dl_dimage) and dl_dimage.is_cuda)
+            or (_is_torch(grads.means) and grads.means.is_cuda)):
+        ctx.wait_torch()  # torch-produced inputs or torch-zeroed gradient buffers
     cc, cam, st, gc = cloud.to_c(), camera.to_c(), settings.to_c(), grads.to_c()
     if _is_torch(dl_dimage):
         dptr, dmem = dl_dimage.data_ptr(), (capi.MEM_DEVICE if dl_dimage.is_cuda else capi.MEM_HOST)

@@ -40,6 +40,8 @@ def lib() -> C.CDLL:
         L.oracle_get.restype = C.c_int64
         L.oracle_get.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         L.oracle_free.argtypes = [C.c_void_p]
+        L.oracle_rasterize_splats.restype = C.c_int
+        L.oracle_rasterize_splats.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_int]
         L.oracle_random_cloud.argtypes = [C.c_uint32, C.c_int, dp, C.c_int, dp, dp, dp, dp, dp]
         L.oracle_photometric_loss.restype = C.c_double
         L.oracle_photometric_loss.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double, dp]
@@ -131,6 +133,16 @@ class OracleFrame:
         out = np.empty(n, dtype=dtype)
         L.oracle_get(self.h, which.encode(), out.ctypes.data)
         return out
+
+    def rasterize_splats(self, portable: bool) -> "OracleFrame":
+        """This (float) frame's splats sorted, binned and blended again (the stages after
+        projection), with PortableMath or StdMath blending."""
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = lib().oracle_rasterize_splats(self.h, int(portable), C.byref(h), err, 512)
+        if rc != 0:
+            raise OracleError(rc, err.value.decode())
+        return OracleFrame(h)
 
     def backward(self, dl_dimage: np.ndarray, mutate_term: int = -1):
         g = np.ascontiguousarray(dl_dimage, dtype=np.float64).ravel()

@@ -197,3 +197,39 @@ def test_culled_backward_matches_plain_backward(gpu_ctx):
     for k in GROUPS:
         assert group_rel(getattr(a, k), getattr(b, k)) < 1e-4, k
     assert np.array_equal(a.observed, b.observed)
+
+
+@pytest.mark.parametrize("bad", [np.inf, np.nan, 3e38])
+def test_non_finite_gradient_names_the_gaussian(gpu_ctx, bad):
+    """backward.hpp:440-446: a non-finite gradient raises std::runtime_error naming the
+    first offending Gaussian. An upstream gradient of inf / NaN / 3e38 (whose products
+    overflow) at one pixel poisons every Gaussian composited there; the lowest such index
+    is reported, as by the float oracle, which makes the same forward decisions."""
+    from paper_2410_20686_b200 import OdgsRuntimeError
+    arrs = oracle_lib.random_cloud(144, 2000)
+    cloud = to_cloud32(arrs)
+    W, H = 256, 128
+    cam = CameraPose(W, H)
+    gs, os_ = settings_pair()
+    fr = render(gpu_ctx, cloud, cam, gs)
+    walked = fr.walked
+    x, y = np.unravel_index(np.argmax(walked), walked.shape)  # the pixel with the longest walk
+    dl = probe(3, W, H)
+    dl[1, x, y] = bad
+    with pytest.raises(OdgsRuntimeError) as e:
+        backward(gpu_ctx, cloud, cam, fr, dl, gs)
+    r, t = cam32(cam)
+    of = oracle_lib.render(arrs, r, t, W, H, os_, portable=True)
+    with pytest.raises(oracle_lib.OracleError) as oe:
+        of.backward(dl.astype(np.float64))
+    assert str(oe.value) == str(e.value)
+    assert e.value.index == int(str(oe.value).rsplit(" ", 1)[1])
+    # the device-buffer path reports the same
+    import torch
+    n = cloud.n
+    z = lambda *s: torch.zeros(s, dtype=torch.float32, device="cuda")
+    dev = GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n),
+                      torch.zeros(n, dtype=torch.int32, device="cuda"))
+    with pytest.raises(OdgsRuntimeError) as e2:
+        backward(gpu_ctx, cloud, cam, fr, torch.from_numpy(dl).cuda(), gs, grads=dev)
+    assert e2.value.index == e.value.index

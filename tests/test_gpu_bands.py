@@ -216,3 +216,65 @@ def test_band_reports_non_finite_like_the_full_render(gpu_ctx):
     with pytest.raises(OdgsRuntimeError) as band_err:
         render_band(gpu_ctx, cloud, cam, s, 64, 96)
     assert full_err.value.index == band_err.value.index == 1234
+
+
+@pytest.mark.parametrize("field,row,col", [("raw_opacities", None, 4321), ("colors", 2, 4321),
+                                           ("log_scales", 1, 4321), ("rotations", 3, 4321)])
+@pytest.mark.parametrize("value", [np.nan, np.inf, -np.inf])
+def test_band_checks_every_parameter_outside_the_band(gpu_ctx, field, row, col, value):
+    """first_non_finite (rasterizer.hpp:133-136) covers every parameter of every row: a
+    Gaussian far outside the band with a non-finite opacity, colour, single log-scale or
+    quaternion component fails the band render exactly as it fails the full render."""
+    from paper_2410_20686_b200 import OdgsRuntimeError
+    arrs = [np.array(a, dtype=np.float32) for a in oracle_lib.random_cloud(941, 6000)]
+    arrs[0][:, col] = [0.0, -5.0, 1.0]  # high above the horizon: never in the bottom band
+    names = ["means", "rotations", "log_scales", "raw_opacities", "colors"]
+    a = arrs[names.index(field)]
+    if row is None:
+        a[col] = value
+    else:
+        a[row, col] = value
+    cloud = to_cloud32(arrs)
+    cam, s = CameraPose(256, 128), RenderSettings()
+    with pytest.raises(OdgsRuntimeError) as full_err:
+        render(gpu_ctx, cloud, cam, s)
+    with pytest.raises(OdgsRuntimeError) as band_err:
+        render_band(gpu_ctx, cloud, cam, s, 96, 128)
+    assert full_err.value.index == band_err.value.index == col
+
+
+def test_band_checks_sh_coefficients_outside_the_band(gpu_ctx):
+    from paper_2410_20686_b200 import GaussianCloud, OdgsRuntimeError
+    arrs = [np.array(a, dtype=np.float32) for a in oracle_lib.random_cloud(942, 3000)]
+    arrs[0][:, 77] = [0.0, -5.0, 1.0]
+    sh = np.zeros((3, 3, 3000), np.float32)
+    sh[2, 1, 77] = np.nan
+    cloud = GaussianCloud.from_numpy(*arrs, sh_degree=1, sh_rest=sh)
+    cam, s = CameraPose(256, 128), RenderSettings()
+    with pytest.raises(OdgsRuntimeError) as band_err:
+        render_band(gpu_ctx, cloud, cam, s, 96, 128)
+    assert band_err.value.index == 77
+
+
+@pytest.mark.parametrize("tile,plain", [(16, True), (32, False), (80, False)])
+def test_peer_images_written_on_every_blend_path(gpu_ctx, tile, plain):
+    """The fused band all-gather also runs in the un-culled blend (ODGS_FRAME_PLAIN_BLEND)
+    and for tiles above 16 px, set before or after the flags."""
+    import torch
+    from paper_2410_20686_b200 import RenderOutput
+    from paper_2410_20686_b200 import _capi as capi
+    c = scenes.cloud_c3(30_000)
+    W, H = 640, 320
+    cam = CameraPose(W, H)
+    s = RenderSettings(tile_size=tile)
+    full = render(gpu_ctx, c, cam, s).image
+    peer = torch.full((3 * W * H,), float("nan"), device="cuda")
+    fr = RenderOutput(gpu_ctx)
+    fr.set_image_peers([peer.data_ptr()])
+    if plain:
+        gpu_ctx.lib.odgs_frame_set_flags(fr.handle, capi.FRAME_PLAIN_BLEND)
+    rows = 160 if tile == 80 else tile * (160 // tile)
+    for r0 in range(0, H, rows):
+        render_band(gpu_ctx, c, cam, s, r0, min(H, r0 + rows), out=fr)
+    torch.cuda.synchronize()
+    assert np.array_equal(peer.cpu().numpy().reshape(3, W, H), full)
