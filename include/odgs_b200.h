@@ -259,6 +259,35 @@ odgs_status odgs_rasterize_splats(odgs_ctx* ctx, int64_t n_gaussians, int64_t n_
                                   const float* radius, const float* opacity, const float* color, int32_t width,
                                   int32_t height, const odgs_settings* settings, odgs_frame* frame);
 
+/* Splat2D (projection.hpp:163-174). */
+typedef struct {
+  float pixel_mean[2];
+  float cov2d[4];     /* row-major, incl. the low-pass dilation */
+  float cov2d_inv[4]; /* row-major */
+  float depth, radius, opacity;
+  float color[3];
+  int64_t index;
+  int32_t pole_clamped;
+} odgs_splat;
+
+/* project_gaussian (projection.hpp:178-216) of cloud row `index`: *projected = 0 for
+   std::nullopt (outside the near/far shell, or a non-positive / non-finite projected
+   covariance), else *out holds the splat. No first_non_finite pass, as in the reference:
+   ODGS_ERR_INVALID_ARGUMENT for a near-zero quaternion or a non-finite quaternion /
+   log-scale inside the shell (covariance.hpp:14-15, 31-32), ODGS_ERR_DOMAIN for a
+   zero-length direction. Synchronizes. */
+odgs_status odgs_project_gaussian(odgs_ctx* ctx, const odgs_cloud* cloud, int64_t index, const odgs_camera* camera,
+                                  const odgs_settings* settings, odgs_splat* out, int32_t* projected);
+
+/* grad_pixels_to_splats (backward.hpp:208-339): SplatGrads of every projected splat of a
+   rendered frame, in RenderOutput::splats order (n_splats rows; host arrays, any may be
+   NULL): pixel_mean [ns][2], cov2d [ns][4] (full-matrix convention), opacity [ns] (w.r.t.
+   the activated opacity), color [ns][3]. The alpha clamp and cutoff are read from
+   `settings`. Synchronizes. */
+odgs_status odgs_grad_pixels_to_splats(odgs_ctx* ctx, odgs_frame* frame, const float* dl_dimage, int32_t dl_memory,
+                                       const odgs_settings* settings, float* pixel_mean, float* cov2d, float* opacity,
+                                       float* color);
+
 /* backward (backward.hpp:380-448) incl. grad_pixels_to_splats (:208-339) for the view
    rendered into `frame` (same cloud, camera, settings — unchecked, as in the
    reference). dl_dimage: [3][W][H] in dl_memory. grad_t_signs: NULL or 12 signs

@@ -442,11 +442,14 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
     const int code = (int)(he.project & 15);
     if (code == 3)
       return set_error(ctx, ODGS_ERR_DOMAIN, idx, "to_spherical: degenerate zero-length direction");
+    if (code == 2) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "build_covariance: non-finite parameters");
     return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "normalize_quaternion: near-zero quaternion");
   }
   const unsigned long long total = n > 0 ? he.n_entries : 0ull;
-  if (total >= (1ull << 31))
-    return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: more than 2^31 tile entries");
+  // The onesweep look-back words carry 30-bit digit counts (sort.cu), so a sort holds
+  // fewer than 2^30 items.
+  if (total >= kMaxSortItems)
+    return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: 2^30 or more tile entries");
   f->n_entries = (uint32_t)total;
   f->n_splats = n > 0 ? (int64_t)he.n_visible : 0;
   f->n_instances = n > 0 ? (int64_t)he.n_instances : 0;
@@ -577,6 +580,62 @@ uint32_t flags_of(const float4& c) {
   uint32_t fl;
   std::memcpy(&fl, &c.w, 4);
   return fl;
+}
+
+// grad_pixels_to_splats' pixel half (backward.hpp:208-327) on a rendered frame: the
+// upstream gradient to the device (if on the host), the per-entry records of the back-
+// to-front replay, and their ordered fold per Gaussian into f->folded. The alpha clamp
+// and cutoff come from `settings`, as the reference's backward reads them.
+odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, int32_t dl_memory,
+                        const odgs_settings* settings) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = f->n;
+  const int64_t px = (int64_t)f->width * f->height;
+  const uint32_t K = f->n_entries;
+  const float* dl = dl_dimage;
+  if (dl_memory != ODGS_MEM_DEVICE) {
+    ODGS_CUDA(ctx, ensure(ctx->dl_buf, sizeof(float) * 3 * px, s));
+    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->dl_buf.p, dl_dimage, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, s));
+    dl = ctx->dl_buf.as<float>();
+  }
+  ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
+  ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
+  ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
+  {
+    StageScope sc(ctx, ODGS_STAGE_BWD_RASTER);
+    if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, (size_t)K, s));
+    BwdRasterArgs ra;
+    ra.offsets = f->offsets.as<int32_t>();
+    ra.vals = f->evals[f->tile_which].as<uint32_t>();
+    ra.sp_ab = f->sp_ab.as<float4>();
+    ra.sp_c = f->sp_c.as<float4>();
+    ra.ent_off_idx = f->ent_off_idx.as<uint32_t>();
+    ra.transmittance = f->trans.as<float>();
+    ra.walked = f->walked.as<int32_t>();
+    ra.dl_dimage = dl;
+    ra.width = f->width;
+    ra.height = f->height;
+    ra.tile_size = f->tile_size;
+    ra.tiles_x = f->tiles_x;
+    ra.tiles_y = f->tiles_y;
+    ra.band_ty0 = f->settings.band_ty0;
+    ra.band_ty1 = f->settings.band_ty1;
+    ra.alpha_clamp = settings->alpha_clamp;
+    ra.cutoff_sigma = settings->cutoff_sigma;
+    ra.records = f->records.as<float>();
+    ra.touched = f->touched.as<uint8_t>();
+    ra.order = f->tile_order.as<uint32_t>();
+    ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
+    launch_bwd_raster(ra, s);
+  }
+  {
+    StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
+    launch_fold_records(f->n_sorted, f->vals[f->depth_which].as<uint32_t>(), f->cnt_sorted.as<uint32_t>(),
+                        f->off_sorted.as<uint32_t>(), f->touched.as<uint8_t>(), f->records.as<float>(),
+                        f->folded.as<float>(), s);
+  }
+  ODGS_CUDA(ctx, cudaGetLastError());
+  return ODGS_OK;
 }
 
 }  // namespace
@@ -715,7 +774,6 @@ void odgs_frame_destroy(odgs_frame* f) {
 
 odgs_status odgs_frame_set_image_peers(odgs_frame* f, int32_t n, void* const* peer_images) {
   if (!f || n < 0 || n > kMaxPeers || (n > 0 && !peer_images)) return ODGS_ERR_INVALID_ARGUMENT;
-  if (n > 0 && (f->flags & ODGS_FRAME_PLAIN_BLEND)) return ODGS_ERR_INVALID_ARGUMENT;
   f->peers = PeerImages{};
   for (int k = 0; k < n; ++k) {
     if (!peer_images[k]) return ODGS_ERR_INVALID_ARGUMENT;
@@ -1043,8 +1101,6 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   if (!f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: frame not rendered");
-  if (f->from_splats)
-    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: frame of odgs_rasterize_splats has no cloud");
   if (!grads || !dl_dimage) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "backward: null buffers");
   odgs_status st;
   if ((st = check_camera(ctx, camera)) != ODGS_OK) return st;
@@ -1055,15 +1111,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   if ((st = resolve_cloud(ctx, cloud, &cp)) != ODGS_OK) return st;
   cudaStream_t s = ctx->stream;
   const int64_t n = f->n;
-  const int64_t px = (int64_t)f->width * f->height;
-  const uint32_t K = f->n_entries;
 
-  const float* dl = dl_dimage;
-  if (dl_memory != ODGS_MEM_DEVICE) {
-    ODGS_CUDA(ctx, ensure(ctx->dl_buf, sizeof(float) * 3 * px, s));
-    ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->dl_buf.p, dl_dimage, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, s));
-    dl = ctx->dl_buf.as<float>();
-  }
   const float* signs = ctx->d_unit_signs;
   if (grad_t_signs) {
     float sf[12];
@@ -1103,39 +1151,10 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     gomc = gomc ? dst[6] : nullptr;
     gobs = gobs ? reinterpret_cast<int32_t*>(dst[7]) : nullptr;
   }
-  ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
-  ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
-  ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
-  StageScope* bwd_scope = new StageScope(ctx, ODGS_STAGE_BWD_RASTER);
-  if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, (size_t)K, s));
   const bool keep_sg = (f->flags & ODGS_FRAME_KEEP_SPLAT_GRADS) != 0;
   if (keep_sg) ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
   if ((st = reset_errors(ctx)) != ODGS_OK) return st;
-
-  BwdRasterArgs ra;
-  ra.offsets = f->offsets.as<int32_t>();
-  ra.vals = f->evals[f->tile_which].as<uint32_t>();
-  ra.sp_ab = f->sp_ab.as<float4>();
-  ra.sp_c = f->sp_c.as<float4>();
-  ra.ent_off_idx = f->ent_off_idx.as<uint32_t>();
-  ra.transmittance = f->trans.as<float>();
-  ra.walked = f->walked.as<int32_t>();
-  ra.dl_dimage = dl;
-  ra.width = f->width;
-  ra.height = f->height;
-  ra.tile_size = f->tile_size;
-  ra.tiles_x = f->tiles_x;
-  ra.tiles_y = f->tiles_y;
-  ra.band_ty0 = f->settings.band_ty0;
-  ra.band_ty1 = f->settings.band_ty1;
-  ra.alpha_clamp = f->settings.alpha_clamp;
-  ra.cutoff_sigma = f->settings.cutoff_sigma;
-  ra.records = f->records.as<float>();
-  ra.touched = f->touched.as<uint8_t>();
-  ra.order = f->tile_order.as<uint32_t>();
-  ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
-  launch_bwd_raster(ra, s);
-  delete bwd_scope;
+  if ((st = raster_fold(ctx, f, dl_dimage, dl_memory, settings)) != ODGS_OK) return st;
 
   BwdSplatArgs sa;
   sa.n = n;
@@ -1146,8 +1165,13 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.sh_degree = cp.sh_degree;
   sa.sh_rest = cp.sh_rest;
   sa.g_sh_rest = gsh;
-  sa.cam = f->cam;
-  sa.settings = f->settings;
+  // The chain rule re-derives the projection from the camera and settings passed here,
+  // as the reference's backward does (backward.hpp:393-410): the frame supplies only
+  // the splats, tile lists and per-pixel state (also a frame of odgs_rasterize_splats).
+  sa.cam = to_dev(*camera);
+  sa.settings = to_dev(*settings);
+  sa.settings.band_ty0 = f->settings.band_ty0;
+  sa.settings.band_ty1 = f->settings.band_ty1;
   sa.sp_ab = f->sp_ab.as<float4>();
   sa.sp_c = f->sp_c.as<float4>();
   sa.cnt = f->cnt.as<uint32_t>();
@@ -1166,9 +1190,6 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.err = ctx->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
-    launch_fold_records(f->n_sorted, f->vals[f->depth_which].as<uint32_t>(), f->cnt_sorted.as<uint32_t>(),
-                        f->off_sorted.as<uint32_t>(), f->touched.as<uint8_t>(), f->records.as<float>(),
-                        f->folded.as<float>(), s);
     launch_bwd_splat(sa, s);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
@@ -1195,6 +1216,110 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
     const int64_t idx = (int64_t)(he.bwd_nonfinite >> 4);
     return set_error(ctx, ODGS_ERR_RUNTIME, idx, "backward: non-finite gradient for Gaussian " + std::to_string(idx));
   }
+  return ok(ctx);
+}
+
+odgs_status odgs_grad_pixels_to_splats(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, int32_t dl_memory,
+                                       const odgs_settings* settings, float* pixel_mean, float* cov2d, float* opacity,
+                                       float* color) {
+  LaunchScope scope(ctx);
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (!f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "grad_pixels_to_splats: frame not rendered");
+  if (!dl_dimage) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "grad_pixels_to_splats: null image gradient");
+  odgs_status st;
+  if ((st = check_settings(ctx, settings)) != ODGS_OK) return st;
+  cudaStream_t s = ctx->stream;
+  const int64_t n = f->n;
+  ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
+  if ((st = raster_fold(ctx, f, dl_dimage, dl_memory, settings)) != ODGS_OK) return st;
+  launch_splat_grads(n, f->sp_ab.as<float4>(), f->sp_c.as<float4>(), f->cnt.as<uint32_t>(), f->folded.as<float>(),
+                     f->splat_grads.as<float>(), s);
+  ODGS_CUDA(ctx, cudaGetLastError());
+  f->have_splat_grads = true;
+  // Compact to splat order (RenderOutput::splats: projected Gaussians, ascending row).
+  HostViews v;
+  if ((st = load_views(ctx, f, &v)) != ODGS_OK) return st;
+  std::vector<float> sg((size_t)n * 10);
+  if (n) ODGS_CUDA(ctx, cudaMemcpy(sg.data(), f->splat_grads.p, sizeof(float) * 10 * n, cudaMemcpyDeviceToHost));
+  for (size_t k = 0; k < v.visible.size(); ++k) {
+    const float* r = sg.data() + (size_t)v.visible[k] * 10;
+    if (pixel_mean) { pixel_mean[2 * k] = r[0]; pixel_mean[2 * k + 1] = r[1]; }
+    if (cov2d) for (int c = 0; c < 4; ++c) cov2d[4 * k + c] = r[2 + c];
+    if (opacity) opacity[k] = r[6];
+    if (color) for (int c = 0; c < 3; ++c) color[3 * k + c] = r[7 + c];
+  }
+  if (ctx->timers.enabled) resolve_timers(ctx);
+  return ok(ctx);
+}
+
+odgs_status odgs_project_gaussian(odgs_ctx* ctx, const odgs_cloud* cloud, int64_t index, const odgs_camera* camera,
+                                  const odgs_settings* settings, odgs_splat* out, int32_t* projected) {
+  LaunchScope scope(ctx);
+  if (!ctx || !out || !projected) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  *projected = 0;
+  odgs_status st;
+  if ((st = check_settings(ctx, settings)) != ODGS_OK) return st;
+  if (!camera || camera->width <= 0 || camera->height <= 0)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "project_gaussian: bad camera size");
+  if (!cloud || cloud->sh_degree < 0 || cloud->sh_degree > 3 || (cloud->sh_degree > 0 && !cloud->sh_rest))
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "project_gaussian: bad cloud");
+  if (index < 0 || index >= cloud->n)
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, index, "project_gaussian: index outside the cloud");
+  const int nb = cloud->sh_degree > 0 ? sh_count(cloud->sh_degree) : 0;
+  // Gather the row into a one-row cloud (means 3 | rotations 4 | log_scales 3 | opacity |
+  // colors 3 | sh_rest 3 nb) next to the one-row outputs.
+  const int row_len = 14 + 3 * nb;
+  const int64_t n = cloud->n;
+  const float* src[6] = {cloud->means, cloud->rotations, cloud->log_scales, cloud->raw_opacities, cloud->colors,
+                         cloud->sh_rest};
+  const int width[6] = {3, 4, 3, 1, 3, 3 * nb};
+  cudaStream_t s = ctx->stream;
+  constexpr size_t kOut = 256;  // sp_ab 32 | sp_c 16 | cov 16 | keys, vals, cnt
+  ODGS_CUDA(ctx, ensure(ctx->misc_buf, kOut + sizeof(float) * row_len, s));
+  char* base = ctx->misc_buf.as<char>();
+  float* d_row = reinterpret_cast<float*>(base + kOut);
+  std::vector<float> row((size_t)row_len);
+  const bool dev = cloud->memory == ODGS_MEM_DEVICE;
+  int off = 0;
+  for (int g = 0; g < 6; ++g)
+    for (int c = 0; c < width[g]; ++c, ++off) {
+      const float* p = src[g] + (int64_t)c * n + index;
+      if (dev) ODGS_CUDA(ctx, cudaMemcpyAsync(d_row + off, p, sizeof(float), cudaMemcpyDeviceToDevice, s));
+      else row[(size_t)off] = *p;
+    }
+  if (!dev) ODGS_CUDA(ctx, cudaMemcpyAsync(d_row, row.data(), sizeof(float) * row_len, cudaMemcpyHostToDevice, s));
+  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+  float4* d_ab = reinterpret_cast<float4*>(base);
+  float4* d_c = reinterpret_cast<float4*>(base + 32);
+  float4* d_cov = reinterpret_cast<float4*>(base + 48);
+  uint32_t* d_u = reinterpret_cast<uint32_t*>(base + 64);
+  DevSettings ds = to_dev(*settings);
+  ds.tile_size = 1;  // tile counts are not needed
+  launch_project_one(d_row, cloud->sh_degree, to_dev(*camera), ds, d_ab, d_c, d_cov, d_u, d_u + 1, d_u + 2, ctx->d_err, s);
+  float4 h[4];
+  ODGS_CUDA(ctx, cudaMemcpyAsync(h, base, sizeof h, cudaMemcpyDeviceToHost, s));
+  if ((st = read_errors(ctx)) != ODGS_OK) return st;
+  const DevErrors& he = *ctx->h_err;
+  if (he.project != kNoError) {
+    const int code = (int)(he.project & 15);
+    if (code == 3) return set_error(ctx, ODGS_ERR_DOMAIN, index, "to_spherical: degenerate zero-length direction");
+    if (code == 2) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, index, "build_covariance: non-finite parameters");
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, index, "normalize_quaternion: near-zero quaternion");
+  }
+  const uint32_t flags = flags_of(h[2]);
+  if (!(flags & kFlagVisible)) return ok(ctx);  // std::nullopt
+  out->pixel_mean[0] = h[0].x; out->pixel_mean[1] = h[0].y;
+  out->cov2d[0] = h[3].x; out->cov2d[1] = h[3].y; out->cov2d[2] = h[3].z; out->cov2d[3] = h[3].w;
+  out->cov2d_inv[0] = h[0].z; out->cov2d_inv[1] = h[0].w; out->cov2d_inv[2] = h[0].w; out->cov2d_inv[3] = h[1].x;
+  out->depth = h[2].y;
+  out->radius = h[2].z;
+  out->opacity = h[1].y;
+  out->color[0] = h[1].z; out->color[1] = h[1].w; out->color[2] = h[2].x;
+  out->index = index;
+  out->pole_clamped = (flags & kFlagClamped) ? 1 : 0;
+  *projected = 1;
   return ok(ctx);
 }
 

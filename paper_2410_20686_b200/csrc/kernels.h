@@ -38,6 +38,11 @@ void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_
 // Concatenates the segments at seg_off (exclusive scan of seg_count).
 void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t* seg_off, const uint32_t* seg_keys,
                             const uint32_t* seg_vals, uint32_t* keys_out, uint32_t* vals_out, cudaStream_t stream);
+// project_gaussian (projection.hpp:178-216) of a row gathered into a one-row cloud
+// (means 3 | rotations 4 | log_scales 3 | raw opacity | colors 3 | sh_rest 3 nb).
+void launch_project_one(const float* row, int sh_degree, const DevCamera& cam, const DevSettings& s, float4* sp_ab,
+                        float4* sp_c, float4* cov, uint32_t* keys, uint32_t* vals, uint32_t* cnt, DevErrors* err,
+                        cudaStream_t stream);
 // Caller-supplied splats (odgs_rasterize_splats): kSplatRecord floats per splat, the
 // first holding the cloud row's bits; rows without a splat are culled.
 constexpr int kSplatRecord = 12;
@@ -194,6 +199,10 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
 void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
                          const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
                          cudaStream_t stream);
+
+// SplatGrads of every projected Gaussian from the folded records (grad_pixels_to_splats).
+void launch_splat_grads(int64_t n, const float4* sp_ab, const float4* sp_c, const uint32_t* cnt, const float* folded,
+                        float* splat_grads, cudaStream_t stream);
 
 struct BwdSplatArgs {
   int64_t n;

@@ -827,6 +827,42 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ SplatGrads only
+// grad_pixels_to_splats (backward.hpp:208-339) without the per-splat chain rule: the
+// folded records of each projected Gaussian and the Sigma_2D transport, into
+// splat_grads[i][10] (mean 2, cov2d 4 full-matrix convention, opacity, colour 3).
+__global__ void k_splat_grads(int64_t n, const float4* __restrict__ sp_ab, const float4* __restrict__ sp_c,
+                              const uint32_t* __restrict__ cnt, const float* __restrict__ folded,
+                              float* __restrict__ splat_grads) {
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float r[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const uint32_t flags = __float_as_uint(sp_c[i].w);
+  if ((flags & kFlagVisible) && cnt[i] > 0)
+#pragma unroll
+    for (int c = 0; c < kRec; ++c) r[c] = folded[i * kRec + c];
+  const float4 ab0 = sp_ab[2 * i], ab1 = sp_ab[2 * i + 1];
+  const float inv[2][2] = {{ab0.z, ab0.w}, {ab0.w, ab1.x}};
+  const float ginv[2][2] = {{r[2], r[3]}, {r[3], r[4]}};
+  float tmp[2][2], dcov[2][2];
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) tmp[p][q] = (-inv[p][0]) * ginv[0][q] + (-inv[p][1]) * ginv[1][q];
+  for (int p = 0; p < 2; ++p)
+    for (int q = 0; q < 2; ++q) dcov[p][q] = tmp[p][0] * inv[0][q] + tmp[p][1] * inv[1][q];
+  float* o = splat_grads + i * 10;
+  o[0] = r[0]; o[1] = r[1];
+  o[2] = dcov[0][0]; o[3] = dcov[0][1]; o[4] = dcov[1][0]; o[5] = dcov[1][1];
+  o[6] = r[5]; o[7] = r[6]; o[8] = r[7]; o[9] = r[8];
+}
+
+void launch_splat_grads(int64_t n, const float4* sp_ab, const float4* sp_c, const uint32_t* cnt, const float* folded,
+                        float* splat_grads, cudaStream_t stream) {
+  if (n == 0) return;
+  launch_pdl(k_splat_grads, (unsigned)((n + 255) / 256), 256, 0, stream, n, sp_ab, sp_c, cnt, folded, splat_grads);
+  ++g_launches;
+}
+
 // ------------------------------------------------------------------ ordered fold
 // Lane l of a warp folds the records of depth rank r0 + l in emit order (the
 // reference's tile-entry order per splat, backward.hpp:310-327); records no warp

@@ -19,7 +19,11 @@ namespace odgs_b200 {
 
 // ------------------------------------------------------------------ preprocess
 // Projects Gaussian i; returns the number of seam instances (0 if culled) and sets
-// *visible. Error words get the lowest offending index.
+// *visible. Error words get the lowest offending index. kProjectOnly: the semantics of
+// project_gaussian alone (projection.hpp:178-216) — no first_non_finite pass; a
+// non-finite quaternion or log-scale of a Gaussian inside the shell is build_covariance's
+// invalid_argument (covariance.hpp:31-32), other non-finite values pass through.
+template <bool kProjectOnly = false>
 __device__ __forceinline__ uint32_t preprocess_one(
     int64_t i, int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
     const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
@@ -41,13 +45,15 @@ __device__ __forceinline__ uint32_t preprocess_one(
   cnt[i] = 0;
   sp_c[i] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
 
-  bool finite = isfinite(raw);
-  for (int c = 0; c < 3; ++c) finite = finite && isfinite(p[c]) && isfinite(ls[c]) && isfinite(col[c]);
-  for (int c = 0; c < 4; ++c) finite = finite && isfinite(q[c]);
-  for (int k = 0; k < 3 * nb; ++k) finite = finite && isfinite(__ldg(sh_rest + (int64_t)k * n + i));
-  if (!finite) {
-    atomic_min_error(&err->nonfinite, i, 2);
-    return 0;
+  if (!kProjectOnly) {
+    bool finite = isfinite(raw);
+    for (int c = 0; c < 3; ++c) finite = finite && isfinite(p[c]) && isfinite(ls[c]) && isfinite(col[c]);
+    for (int c = 0; c < 4; ++c) finite = finite && isfinite(q[c]);
+    for (int k = 0; k < 3 * nb; ++k) finite = finite && isfinite(__ldg(sh_rest + (int64_t)k * n + i));
+    if (!finite) {
+      atomic_min_error(&err->nonfinite, i, 2);
+      return 0;
+    }
   }
 
   float mu[3];
@@ -69,6 +75,15 @@ __device__ __forceinline__ uint32_t preprocess_one(
   const M23 J = jacobian_factored(phi, theta, depth, W, H, s.max_elevation, &clamped);
 
   // build_covariance (covariance.hpp:28-37)
+  if (kProjectOnly) {
+    bool finite = true;
+    for (int c = 0; c < 3; ++c) finite = finite && isfinite(ls[c]);
+    for (int c = 0; c < 4; ++c) finite = finite && isfinite(q[c]);
+    if (!finite) {
+      atomic_min_error(&err->project, i, 2);  // build_covariance: non-finite parameters
+      return 0;
+    }
+  }
   const float qn = sqrtf(sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]));
   if (!(qn > 1e-12f)) {
     atomic_min_error(&err->project, i, 1);  // normalize_quaternion invalid_argument
@@ -162,6 +177,26 @@ void launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
   launch_pdl(k_preprocess, (unsigned)grid, block, 0, stream, a.n, a.means, a.rotations, a.log_scales, a.raw_opacities,
                                                      a.colors, a.cam, a.settings, a.sp_ab, a.sp_c, a.cov_out, a.keys,
                                                      a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest);
+  ++g_launches;
+}
+
+// ------------------------------------------------------------------ project_gaussian
+// One Gaussian with project_gaussian's own semantics (odgs_project_gaussian): the row
+// was gathered into a one-row cloud.
+__global__ void k_project_one(const float* __restrict__ row, int sh_degree, DevCamera cam, DevSettings s,
+                              float4* __restrict__ sp_ab, float4* __restrict__ sp_c, float4* __restrict__ cov,
+                              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt,
+                              DevErrors* __restrict__ err) {
+  pdl_wait();
+  bool visible = false;
+  preprocess_one<true>(0, 1, row, row + 3, row + 7, row + 10, row + 11, sh_degree, sh_degree > 0 ? row + 14 : nullptr,
+                       cam, s, sp_ab, sp_c, cov, keys, vals, cnt, err, &visible);
+}
+
+void launch_project_one(const float* row, int sh_degree, const DevCamera& cam, const DevSettings& s, float4* sp_ab,
+                        float4* sp_c, float4* cov, uint32_t* keys, uint32_t* vals, uint32_t* cnt, DevErrors* err,
+                        cudaStream_t stream) {
+  launch_pdl(k_project_one, 1, 1, 0, stream, row, sh_degree, cam, s, sp_ab, sp_c, cov, keys, vals, cnt, err);
   ++g_launches;
 }
 
@@ -647,7 +682,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,
-    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base) {
+    int32_t* __restrict__ walked_out, unsigned long long* __restrict__ work, int tile_base, PeerImages peers) {
   __shared__ float s_cx[kBlendThreads], s_cy[kBlendThreads], s_i00[kBlendThreads], s_i01x2[kBlendThreads],
       s_i11[kBlendThreads], s_op[kBlendThreads], s_r[kBlendThreads], s_g[kBlendThreads], s_b[kBlendThreads];
   const int tile = tile_base + blockIdx.x;
@@ -761,6 +796,12 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
     image[2 * plane + pix[q]] = cb[q];
     trans_out[pix[q]] = t[q];
     walked_out[pix[q]] = walked[q];
+    for (int k = 0; k < peers.n; ++k) {  // fused band all-gather, as in k_blend_cull
+      float* o = peers.ptr[k];
+      o[pix[q]] = cr[q];
+      o[plane + pix[q]] = cg[q];
+      o[2 * plane + pix[q]] = cb[q];
+    }
   }
   __syncthreads();  // the next chunk restages the shared batch
   }
@@ -969,7 +1010,7 @@ void launch_blend_plain(const BlendArgs& a, cudaStream_t stream) {
   k_blend<PPT><<<n_tiles, kBlendThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,    \
                                                       a.tile_size, a.tiles_x, a.alpha_clamp,                    \
                                                       a.transmittance_floor, cutoff2, a.image, a.transmittance, \
-                                                      a.walked, a.work, a.band_ty0 * a.tiles_x)
+                                                      a.walked, a.work, a.band_ty0 * a.tiles_x, a.peers)
   if (area <= kBlendThreads) ODGS_BLEND(1);
   else if (area <= 4 * kBlendThreads) ODGS_BLEND(4);
   else ODGS_BLEND(16);

@@ -408,9 +408,9 @@ struct PassArgs {
 };
 
 // The dynamic shared-memory opt-in is a per-device function attribute: one flag bit per
-// device and instantiation, set once (racing threads at worst set it twice).
-template <class Kern> cudaError_t opt_in_smem(Kern kern, size_t smem) {
-  static std::atomic<uint64_t> done{0};
+// device in `done` (one word per kernel instantiation), set once (racing threads at worst
+// set it twice).
+template <class Kern> cudaError_t opt_in_smem(Kern kern, size_t smem, std::atomic<uint64_t>& done) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -426,7 +426,8 @@ cudaError_t launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
   constexpr int kT = Threads * IPT;
   constexpr size_t smem = (size_t)(2 * kT + (Threads / 32) * 256) * sizeof(uint32_t);
   auto kern = k_onesweep_pass<Threads, IPT, MinBlocks, Bits>;
-  const cudaError_t e = opt_in_smem(kern, smem);
+  static std::atomic<uint64_t> opted{0};  // per instantiation
+  const cudaError_t e = opt_in_smem(kern, smem, opted);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.n + kT - 1) / kT;
   return launch_pdl(kern, (unsigned)tiles, Threads, smem, stream, a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n,
