@@ -257,7 +257,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            rank_barrier(local_rank)
 
     for k in range(args.warmup):
         render(ctx, dcloud, camera(k, rank), settings, out=frame)
@@ -328,15 +328,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             gbs = b / (stage_ms[k] * 1e-3) / 1e9
             stage_roof[k] = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": gbs / hbm_peak, "ms": stage_ms[k]}
+    # FP32 lane-op peak: SMs x 128 FP32 lanes x the SM clock sampled under
+    # load in the timed region; the blend's ops are unfused (--fmad=false), one lane-op each.
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk = clocks.summary()
+    sm_mhz = clk["sm_mhz"] or clk["sm_max_mhz"] or 1965.0
+    lane_peak = sms * 128 * sm_mhz * 1e6 / 1e12
     if "blend" in stage_ms:
         tf = blend_flops / (stage_ms["blend"] * 1e-3) / 1e12
-        stage_roof["blend"] = {"bound": "fp32", "achieved": tf, "peak": fp32_peak, "unit": "TFLOP/s",
-                               "frac": tf / fp32_peak, "ms": stage_ms["blend"]}
+        stage_roof["blend"] = {"bound": "fp32 lane ops", "achieved": tf, "peak": lane_peak, "unit": "T lane-ops/s",
+                               "frac": tf / lane_peak, "ms": stage_ms["blend"],
+                               "peak_source": f"{sms} SMs x 128 lanes x {sm_mhz:.0f} MHz (median SM clock, timed region)",
+                               "frac_fma_convention": tf / fp32_peak,
+                               "fma_peak_tflops": fp32_peak,
+                               "work_model": "11 ops per examined entry + 12 per composited (SURVEY.md §8d)"}
     roof = dict(stage_roof[dominant]) if dominant in stage_roof else {"bound": "unknown"}
     roof["kernel"] = dominant
     roof["traffic"] = ncu_traffic(dominant)
-    roof["peak_source"] = (hbm_src if roof.get("unit") == "GB/s"
-                           else "measured FP32 FMA microbenchmark (odgs_measure_fp32_tflops), same run")
+    roof.setdefault("peak_source", hbm_src)
 
     # End to end through the C ABI with host buffers: every frame uploads the cloud from
     # pinned host memory inside odgs_render (56 MB H2D) and downloads the image into
@@ -393,7 +402,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pcie = pcie_peaks(torch, dev, h2d, d2h)
 
     aux = run_aux(args, ctx, dev, stream) if rank == 0 and not args.no_train else None
-    train = None if args.no_train else run_train(args, ctx, rank, world, local_rank, dev, stream)
+    train = None if args.no_train else run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak, hbm_peak)
     large = None if args.no_large else run_large(args, ctx, rank, world, local_rank, dev, stream)
 
     cpu = None
@@ -412,6 +421,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "tile_entries": K, "entries_examined": e_exam, "entries_composited": e_contrib,
                        "l2": "flushed between steps (256 MiB write, then a 256 MiB read that evicts its dirty lines; outside the step events)",
                        "parallelism": f"view-replicas x{world}"},
+            "distributed": {"world_size": world, "backend": (__import__("torch.distributed").distributed.get_backend()
+                                                             if world > 1 else None),
+                            "shared_gpu": SHARE_GPU},
             "roofline": roof,
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "stage_rooflines": stage_roof,
@@ -435,15 +447,17 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     ctx.close()
 
 
-def run_train(args, ctx, rank, world, local_rank, dev, stream):
+def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, hbm_peak):
     """BASELINE config 4: 3M Gaussians, a batch of 8 views at 2048x1024, views sharded
     over the ranks, NCCL all-reduce of the gradients, Adam. One step = the whole
-    batch (8 renders + L1 losses + 8 backward passes + all-reduce + Adam)."""
+    batch (8/G renders + photometric losses + backward passes per rank, all-reduce, Adam).
+    Timed unprofiled (CUDA events on the stream, max over ranks); stage times, work
+    counters and the all-reduce time come from separate passes."""
     import numpy as np
     import torch
     import torch.distributed as dist
     from paper_2410_20686_b200 import GaussianCloud, RenderSettings, render, scenes
-    from paper_2410_20686_b200.train import TrainConfig, ViewShardedTrainer
+    from paper_2410_20686_b200.train import FLAT_WIDTH, TrainConfig, ViewShardedTrainer, allreduce_grads
 
     n = 3_000_000
     views = scenes.c4_views(W_IMG, H_IMG, 8)
@@ -456,43 +470,166 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream):
     settings = RenderSettings()
     targets = []
     from paper_2410_20686_b200 import RenderOutput
-    from paper_2410_20686_b200 import _capi as capi
     tf = RenderOutput(ctx)
     for v in views:  # targets: renders of a second cloud
         render(ctx, tcloud, v, settings, out=tf)
-        img = torch.empty(3 * W_IMG * H_IMG, dtype=torch.float32, device=dev)
-        ptr = tf.device_ptr(capi.FRAME_IMAGE)
-        torch.cuda.synchronize()
-        img.copy_(torch.from_numpy(tf.image.ravel()).to(dev))
-        targets.append(img)
+        targets.append(torch.from_numpy(tf.image.ravel()).to(dev))
     tf.destroy()
     del tcloud
     extent = float(np.sqrt(((src.means - src.means.mean(axis=1, keepdims=True)) ** 2).sum(axis=0).max()))
     tr = ViewShardedTrainer(ctx, cloud, views, targets, settings, TrainConfig(), extent, rank, world)
-    for _ in range(2):
-        tr.step()
+
+    def barrier():
+        if world > 1:
+            rank_barrier(local_rank)
+
+    first_loss = tr.step()
+    tr.step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier(device_ids=[local_rank])
-    ctx.set_profiling(True)
-    ctx.reset_stage_times()
+    barrier()
+    torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    losses = [tr.step() for _ in range(args.train_steps)]
+    for _ in range(args.train_steps):
+        tr.step(read_loss=False)
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    stages = {k: round(v[0] / max(args.train_steps, 1), 4) for k, v in ctx.stage_times().items() if v[1] > 0}
-    ctx.set_profiling(False)
+    barrier()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    last_loss = tr.step()
+
+    # Separate pass: per-stage times (library CUDA events) and the work counters of every
+    # view of one step (forward examined / composited, backward replayed / contributing).
+    ctx.set_profiling(True)
+    ctx.reset_stage_times()
+    fwd_work, bwd_work = [0, 0], [0, 0]
+    orig_backward = tr.frame  # the trainer renders every view into tr.frame
+    import paper_2410_20686_b200.train as train_mod
+    real_backward = train_mod.backward
+
+    def counting_backward(*a, **kw):
+        out = real_backward(*a, **kw)
+        w = orig_backward.work()
+        b = orig_backward.backward_work()
+        fwd_work[0] += w[0]; fwd_work[1] += w[1]
+        bwd_work[0] += b[0]; bwd_work[1] += b[1]
+        return out
+    train_mod.backward = counting_backward
+    try:
+        tr.step(read_loss=False)
+    finally:
+        train_mod.backward = real_backward
+    torch.cuda.synchronize()
+    stages = {k: v[0] for k, v in ctx.stage_times().items() if v[1] > 0}
+    ctx.set_profiling(False)
+    nv = len(tr.mine)
+    stage_view = {k: v / nv for k, v in stages.items()}
+
+    # The all-reduce alone (the step's one exchange), and NCCL's bus bandwidth on a 1 GiB
+    # buffer as its roofline denominator (measured in the same run).
+    allreduce = None
+    if world > 1:
+        def time_ar(buf, obs, reps=5):
+            allreduce_grads(buf, obs)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                allreduce_grads(buf, obs)
+            b.record(stream)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+        ar_ms = time_ar(tr.flat, tr.observed)
+        big = torch.zeros(256 * 1024 * 1024, dtype=torch.float32, device=dev)
+        big_ms = time_ar(big, torch.zeros(1, dtype=torch.int32, device=dev), reps=3)
+        del big
+        factor = 2.0 * (world - 1) / world
+        grad_bytes = 4.0 * (FLAT_WIDTH + 1) * n
+        ar_busbw = factor * grad_bytes / (ar_ms * 1e-3) / 1e9
+        peak_busbw = factor * 4.0 * 256 * 1024 * 1024 / (big_ms * 1e-3) / 1e9
+        allreduce = {"bound": "nvlink", "ms": ar_ms, "bytes": grad_bytes, "achieved": ar_busbw,
+                     "peak": peak_busbw, "unit": "GB/s (bus bandwidth, 2(G-1)/G x bytes / time)",
+                     "frac": ar_busbw / peak_busbw,
+                     "peak_source": "NCCL all-reduce of a 1 GiB fp32 buffer, same run",
+                     "frac_vs_nominal_900": ar_busbw / 900.0}
+
+    # Rooflines of the training kernels, per view.
+    roof = {}
+    if "bwd_raster" in stage_view:
+        e_rep, e_con = bwd_work[0] / nv, bwd_work[1] / nv
+        ops = 11.0 * e_rep + 45.0 * e_con  # replay: the forward's d2 test; + ~45 ops per contribution
+        tops = ops / (stage_view["bwd_raster"] * 1e-3) / 1e12
+        roof["bwd_raster"] = {"bound": "fp32 lane ops", "ms_per_view": stage_view["bwd_raster"],
+                              "entries_replayed": e_rep, "contributions": e_con, "ops": ops,
+                              "achieved": tops, "peak": lane_peak_tops, "unit": "T lane-ops/s",
+                              "frac": tops / lane_peak_tops,
+                              "work_model": "11 ops per replayed entry + 45 per contribution (SURVEY.md §8d)"}
+    if "bwd_splat" in stage_view:
+        K = tr.frame.info().n_entries
+        byts = 56.0 * n + 36.0 * K + 4.0 * 14 * n + 12.0 * n
+        gbs = byts / (stage_view["bwd_splat"] * 1e-3) / 1e9
+        roof["fold_and_splat"] = {"bound": "hbm", "ms_per_view": stage_view["bwd_splat"], "bytes": byts,
+                                  "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                                  "work_model": "N (56 B cloud + 4x14 B grads + 12 B stats) + 36 B per tile entry "
+                                                "(SURVEY.md §8d)"}
+    if allreduce:
+        roof["allreduce"] = allreduce
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = train_cpu_baseline(src, tsrc, views[0])
     return {"metric": "train iters/sec (C4: 3M Gaussians, batch of 8 ERP views at 2048x1024)",
             "value": args.train_steps / (ms_max / 1000.0), "unit": "iters/s", "ms_per_step": ms_max / args.train_steps,
-            "steps": args.train_steps, "warmup": 2, "views_per_gpu": len(tr.mine), "n_gpus": world,
-            "scaling": "strong", "loss": "photometric_loss, lambda_ssim = 0.2 (L1 + SSIM on the GPU)", "collective": "NCCL all-reduce (sum) of 16n+n values",
-            "stage_ms_per_step": stages, "first_loss": losses[0], "last_loss": losses[-1]}
+            "steps": args.train_steps, "warmup": 2, "views_per_gpu": nv, "n_gpus": world,
+            "scaling": "strong", "loss": "photometric_loss, lambda_ssim = 0.2 (L1 + SSIM on the GPU)",
+            "timing": "CUDA events around the unprofiled steps (no host loss readback), max over ranks",
+            "collective": "NCCL all-reduce (sum) of 16n floats + n int32" if world > 1 else "none (1 rank)",
+            "stage_ms_per_step": {k: round(v, 4) for k, v in stages.items()},
+            "work_per_view": {"fwd_examined": fwd_work[0] / nv, "fwd_composited": fwd_work[1] / nv,
+                              "bwd_replayed": bwd_work[0] / nv, "bwd_contributions": bwd_work[1] / nv},
+            "roofline": roof, "cpu_baseline": cpu, "first_loss": first_loss, "last_loss": last_loss}
+
+
+def train_cpu_baseline(src, tsrc, cam):
+    """The reference algorithm on the host (oracle restatement, StdMath double — the
+    reference CLI trains in double, tools/odgs.cpp:242; its float isZero() would skip
+    every pixel of a photometric gradient — all host threads): render + photometric
+    loss + backward of one C4 view, timed; iters/s = 1 / (8 x that) — the CPU's step is
+    8 such views (Adam is negligible next to them)."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ctypes as C
+    import oracle_lib  # the CPU restatement (only the baseline leg may run it)
+    L = oracle_lib.lib()
+    cores = L.oracle_hardware_concurrency()
+    arrs = [np.asarray(getattr(src, k), dtype=np.float64) for k in ("means", "rotations", "log_scales",
+                                                                    "raw_opacities", "colors")]
+    tarrs = [np.asarray(getattr(tsrc, k), dtype=np.float64) for k in ("means", "rotations", "log_scales",
+                                                                      "raw_opacities", "colors")]
+    r, t = np.asarray(cam.rotation, np.float32).astype(np.float64), np.asarray(cam.translation, np.float32).astype(
+        np.float64)
+    target = oracle_lib.render(tarrs, r, t, W_IMG, H_IMG, dbl=True).get("image")
+    t0 = time.perf_counter()
+    fr = oracle_lib.render(arrs, r, t, W_IMG, H_IMG, dbl=True)
+    t1 = time.perf_counter()
+    img = fr.get("image")
+    g = np.empty_like(img)
+    dp = C.POINTER(C.c_double)
+    L.oracle_photometric_loss(img.ctypes.data_as(dp), target.ctypes.data_as(dp), H_IMG, W_IMG, 0.2,
+                              g.ctypes.data_as(dp))
+    t2 = time.perf_counter()
+    fr.backward(g)
+    t3 = time.perf_counter()
+    view_s = t3 - t0
+    return {"value": 1.0 / (8.0 * view_s), "unit": "iters/s", "cores": cores, "kind": "port",
+            "render_s": t1 - t0, "loss_s": t2 - t1, "backward_s": t3 - t2,
+            "sample": f"1 of the 8 C4 views (3M Gaussians, 2048x1024): oracle render + photometric loss "
+                      f"(lambda 0.2) + backward, StdMath double, threads = all {cores} host threads; "
+                      f"iters/s = 1 / (8 x view time)"}
 
 
 def run_aux(args, ctx, dev, stream):
@@ -589,6 +726,8 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
             collective = f"NCCL all_gather of the band images (peer set-up failed: {failure or 'on another rank'})"
 
     def frame(k):
+        if gather is not None:
+            gather.begin()  # this frame's bands go to the other image buffer of every rank
         render_band(ctx, cloud, scenes.yaw_camera(2 * math.pi * k / 16, W, H), settings, r0, r1, out=fr)
         if gather is not None:
             gather.sync(local_rank)
@@ -602,8 +741,6 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     if world > 1:
         dist.barrier(device_ids=[local_rank])
     steps = max(3, min(args.steps, 10))
-    ctx.set_profiling(True)
-    ctx.reset_stage_times()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for k in range(steps):
@@ -611,7 +748,13 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    stages = {k: round(v[0] / steps, 4) for k, v in ctx.stage_times().items() if v[1] > 0}
+    # stage times from a separate profiled pass (its event readbacks stay out of the timing)
+    ctx.set_profiling(True)
+    ctx.reset_stage_times()
+    for k in range(2):
+        frame(k)
+    torch.cuda.synchronize()
+    stages = {k: round(v[0] / 2, 4) for k, v in ctx.stage_times().items() if v[1] > 0}
     ctx.set_profiling(False)
     info = fr.info()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -659,19 +802,54 @@ def _device_view(ptr: int, numel: int, dev):
     return torch.as_tensor(h, device=dev)
 
 
+SHARE_GPU = os.environ.get("ODGS_BENCH_SHARE_GPU") == "1"  # test mode: every rank on GPU 0, gloo
+
+
+def rank_barrier(local_rank: int) -> None:
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.barrier(device_ids=[local_rank])
+    else:
+        dist.barrier()
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` started without a launcher: re-executes itself under
+    torch.distributed.run with N ranks (one process per GPU) on 127.0.0.1."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    local_rank = 0 if SHARE_GPU else int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}")
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if SHARE_GPU:  # NCCL refuses two ranks on one GPU; gloo moves the CUDA tensors
+            dist.init_process_group("gloo")
+        else:
+            if torch.cuda.device_count() < world:
+                raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nRanks) on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        assert dist.get_world_size() == world
     try:
         run_ours(args, rank, world, local_rank)
     finally:

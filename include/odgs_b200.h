@@ -202,6 +202,12 @@ odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, voi
    and entries composited. Synchronizes. */
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_examined,
                             int64_t* entries_composited);
+/* Backward work of the last odgs_backward / odgs_grad_pixels_to_splats on `frame` (for
+   rooflines): entries replayed (sum over pixels with a non-zero image gradient of their
+   walk length — the reference's replay loop, backward.hpp:251-269) and contributions
+   (replayed entries inside the cutoff, :271-305). Synchronizes. */
+odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_replayed,
+                                     int64_t* entries_contributing);
 /* Row bands over several GPUs: the blend also writes every pixel it
    renders into each of these n <= 8 image buffers ([3][W][H] float, the frame's
    layout) — typically the other ranks' full-image buffers opened with odgs_ipc_open —
@@ -330,6 +336,12 @@ typedef struct {
    [3][W][H] device buffers; lambda in [0, 1); SSIM needs W, H >= 11. */
 odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
                                   int32_t height, float lambda_ssim, float* dl_dimage, double* loss);
+
+/* As odgs_photometric_loss, without a host readback: the loss is added to
+   *device_loss_sum (a device double, may be NULL) on the context's stream, so a training
+   step can read its summed loss once. Does not synchronize. */
+odgs_status odgs_photometric_loss_async(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
+                                        int32_t height, float lambda_ssim, float* dl_dimage, double* device_loss_sum);
 
 /* The update half of train_step (optimizer.hpp:114-139): densify-window
    accumulation, Adam (b1 0.9, b2 0.999, eps 1e-15) on the five groups, quaternion

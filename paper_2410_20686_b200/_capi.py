@@ -92,6 +92,12 @@ class Cloud64(C.Structure):
                 ("raw_opacities", C.c_void_p), ("colors", C.c_void_p)]
 
 
+class Splat(C.Structure):  # odgs_splat (Splat2D, projection.hpp:163-174)
+    _fields_ = [("pixel_mean", C.c_float * 2), ("cov2d", C.c_float * 4), ("cov2d_inv", C.c_float * 4),
+                ("depth", C.c_float), ("radius", C.c_float), ("opacity", C.c_float), ("color", C.c_float * 3),
+                ("index", C.c_int64), ("pole_clamped", C.c_int32)]
+
+
 class FrameInfo(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32),
                 ("tiles_y", C.c_int32), ("n_gaussians", C.c_int64), ("n_splats", C.c_int64),
@@ -117,6 +123,7 @@ SIGNATURES = {
     "odgs_frame_get_info": (C.c_int, [_P, C.POINTER(FrameInfo)]),
     "odgs_frame_download": (C.c_int, [_P, _P, C.c_int, _P, C.c_size_t]),
     "odgs_frame_work": (C.c_int, [_P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "odgs_frame_backward_work": (C.c_int, [_P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "odgs_frame_device_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "odgs_prepare_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
     "odgs_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
@@ -124,6 +131,9 @@ SIGNATURES = {
                                    C.c_int32, _P]),
     "odgs_rasterize_splats": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, _P, _P, _P, _P, C.c_int32,
                                         C.c_int32, C.POINTER(Settings), _P]),
+    "odgs_project_gaussian": (C.c_int, [_P, C.POINTER(Cloud), C.c_int64, C.POINTER(Camera), C.POINTER(Settings),
+                                        C.POINTER(Splat), C.POINTER(C.c_int32)]),
+    "odgs_grad_pixels_to_splats": (C.c_int, [_P, _P, _P, C.c_int32, C.POINTER(Settings), _P, _P, _P, _P]),
     "odgs_backward": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), _P, _P, C.c_int32,
                                 C.POINTER(Settings), C.POINTER(Grads), C.POINTER(C.c_double), C.c_uint32]),
     "odgs_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
@@ -132,6 +142,7 @@ SIGNATURES = {
     "odgs_stage_name": (C.c_char_p, [C.c_int]),
     "odgs_measure_fp32_tflops": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "odgs_photometric_loss": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float, _P, C.POINTER(C.c_double)]),
+    "odgs_photometric_loss_async": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P]),
     "odgs_adam_step": (C.c_int, [_P, C.POINTER(Params), C.POINTER(Grads), C.POINTER(TrainState),
                                  C.POINTER(AdamParams)]),
     "odgs_default_densify_config": (None, [C.POINTER(DensifyConfig)]),

@@ -74,6 +74,7 @@ struct odgs_frame {
   bool from_splats = false;  // odgs_rasterize_splats: no cloud or camera behind the splats
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
   DevBuf ekeys[2], evals[2], offsets, tile_order, image, trans, walked, records, touched, folded, splat_grads, work;
+  DevBuf bwd_work;  // [2] backward work counters of the last backward
   int depth_which = 0, tile_which = 0;
   int64_t n_sorted = 0;  // depth-sorted ranks: n, or the band's Gaussians (band compaction)
   PeerImages peers{};    // odgs_frame_set_image_peers
@@ -601,6 +602,8 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
   ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
   ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
   ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
+  ODGS_CUDA(ctx, ensure(f->bwd_work, 2 * sizeof(unsigned long long), s));
+  ODGS_CUDA(ctx, cudaMemsetAsync(f->bwd_work.p, 0, 2 * sizeof(unsigned long long), s));
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_RASTER);
     if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, (size_t)K, s));
@@ -626,6 +629,7 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
     ra.touched = f->touched.as<uint8_t>();
     ra.order = f->tile_order.as<uint32_t>();
     ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
+    ra.work = f->bwd_work.as<unsigned long long>();
     launch_bwd_raster(ra, s);
   }
   {
@@ -766,7 +770,7 @@ void odgs_frame_destroy(odgs_frame* f) {
   DevBuf* bufs[] = {&f->sp_ab, &f->sp_c, &f->cov, &f->keys[0], &f->keys[1], &f->vals[0], &f->vals[1], &f->cnt,
                     &f->cnt_sorted, &f->off_sorted, &f->ent_off_idx, &f->sort_tmp, &f->scan_tmp, &f->ekeys[0],
                     &f->ekeys[1], &f->evals[0], &f->evals[1], &f->offsets, &f->tile_order, &f->image, &f->trans, &f->walked,
-                    &f->records, &f->touched, &f->folded, &f->splat_grads, &f->work};
+                    &f->records, &f->touched, &f->folded, &f->splat_grads, &f->work, &f->bwd_work};
   for (DevBuf* b : bufs) release(*b, s);
   cudaStreamSynchronize(s);
   delete f;
@@ -874,6 +878,17 @@ odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camer
   st = blend_impl(ctx, frame);
   if (ctx->timers.enabled) resolve_timers(ctx);
   return st;
+}
+
+odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_replayed,
+                                     int64_t* entries_contributing) {
+  if (!ctx || !f || !f->bwd_work.p) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "no backward on this frame");
+  unsigned long long w[2];
+  ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->bwd_work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (entries_replayed) *entries_replayed = (int64_t)w[0];
+  if (entries_contributing) *entries_contributing = (int64_t)w[1];
+  return ok(ctx);
 }
 
 odgs_status odgs_rasterize_splats(odgs_ctx* ctx, int64_t n_gaussians, int64_t n_splats, const int64_t* index,
@@ -1323,9 +1338,9 @@ odgs_status odgs_project_gaussian(odgs_ctx* ctx, const odgs_cloud* cloud, int64_
   return ok(ctx);
 }
 
-odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
-                                  int32_t height, float lambda_ssim, float* dl_dimage, double* loss) {
-  LaunchScope scope(ctx);
+namespace {
+odgs_status loss_impl(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width, int32_t height,
+                      float lambda_ssim, float* dl_dimage, double* loss, double* device_accum) {
   if (!ctx || !rendered || !target || !dl_dimage) return ODGS_ERR_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   if (!(lambda_ssim >= 0.0f) || !(lambda_ssim < 1.0f))
@@ -1338,10 +1353,11 @@ odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const fl
     ODGS_CUDA(ctx, ensure(ctx->loss_buf, ssim_temp_bytes(height, width) + 64, ctx->stream));
     char* base = ctx->loss_buf.as<char>();
     launch_ssim_loss(rendered, target, height, width, lambda_ssim, dl_dimage, base + 64,
-                     reinterpret_cast<double*>(base), ctx->stream);
+                     reinterpret_cast<double*>(base), device_accum, ctx->stream);
   } else {
     ODGS_CUDA(ctx, ensure(ctx->loss_buf, l1_loss_temp_bytes(count), ctx->stream));
-    launch_l1_loss(rendered, target, count, lambda_ssim, dl_dimage, ctx->loss_buf.as<double>(), ctx->stream);
+    launch_l1_loss(rendered, target, count, lambda_ssim, dl_dimage, ctx->loss_buf.as<double>(), device_accum,
+                   ctx->stream);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
   if (loss) {
@@ -1351,6 +1367,19 @@ odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const fl
     std::memcpy(loss, ctx->h_scratch, sizeof(double));
   }
   return ok(ctx);
+}
+}  // namespace
+
+odgs_status odgs_photometric_loss(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
+                                  int32_t height, float lambda_ssim, float* dl_dimage, double* loss) {
+  LaunchScope scope(ctx);
+  return loss_impl(ctx, rendered, target, width, height, lambda_ssim, dl_dimage, loss, nullptr);
+}
+
+odgs_status odgs_photometric_loss_async(odgs_ctx* ctx, const float* rendered, const float* target, int32_t width,
+                                        int32_t height, float lambda_ssim, float* dl_dimage, double* device_loss_sum) {
+  LaunchScope scope(ctx);
+  return loss_impl(ctx, rendered, target, width, height, lambda_ssim, dl_dimage, nullptr, device_loss_sum);
 }
 
 odgs_status odgs_adam_step(odgs_ctx* ctx, const odgs_params* p, const odgs_grads* g, const odgs_train_state* st,

@@ -116,14 +116,15 @@ cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, in
 
 // ------------------------------------------------------------------ training step
 size_t l1_loss_temp_bytes(int64_t count);
-// temp[0] <- loss (double); grad <- (1 - lambda) sign(rendered - target) / count.
+// temp[0] <- loss (double), *accum += loss (if accum); grad <- (1 - lambda)
+// sign(rendered - target) / count.
 void launch_l1_loss(const float* rendered, const float* target, int64_t count, float lambda, float* grad,
-                    double* temp, cudaStream_t stream);
+                    double* temp, double* accum, cudaStream_t stream);
 
 size_t ssim_temp_bytes(int H, int W);
 // photometric_loss with lambda > 0 (metrics.hpp:152-184): image gradient and *loss_out.
 void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda, float* grad, void* temp,
-                      double* loss_out, cudaStream_t stream);
+                      double* loss_out, double* accum, cudaStream_t stream);
 
 struct AdamArgs {
   int64_t n;
@@ -190,6 +191,7 @@ struct BwdRasterArgs {
   uint8_t* touched;  // [K] 1 where a record was written (cleared before the launch)
   const uint32_t* order;  // launch order of the band's tiles or null
   bool plain;        // un-culled reference kernel (A/B checks)
+  unsigned long long* work;  // [2] += entries replayed, contributions (or null)
 };
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
 

@@ -23,13 +23,26 @@ constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kBwdBatch = 128;
 constexpr int kRec = 9;  // mx, my, m00, m01, m11, op, c0, c1, c2
 
+// Backward work counters for the roofline (bench.py): entries replayed (sum over pixels
+// with a gradient of their walk, the reference's replay loop, backward.hpp:251-269) and
+// contributions (replayed entries inside the cutoff, :271-305).
+__device__ __forceinline__ void bwd_count_work(unsigned long long* work, uint32_t exam, uint32_t contrib) {
+  const uint32_t we = __reduce_add_sync(0xffffffffu, exam);
+  const uint32_t wc = __reduce_add_sync(0xffffffffu, contrib);
+  if ((threadIdx.x & 31) == 0 && (we | wc)) {
+    atomicAdd(work, (unsigned long long)we);
+    atomicAdd(work + 1, (unsigned long long)wc);
+  }
+}
+
 template <int PPT>
 __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
-    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1) {
+    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1,
+    unsigned long long* __restrict__ work) {
   __shared__ float s_cx[kBwdBatch], s_cy[kBwdBatch], s_i00[kBwdBatch], s_i01[kBwdBatch], s_i11[kBwdBatch],
       s_op[kBwdBatch], s_col[3][kBwdBatch];
   __shared__ uint32_t s_pos[kBwdBatch];
@@ -50,6 +63,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
   float px[PPT], py[PPT], t[PPT], d0[PPT], d1[PPT], d2v[PPT], suf0[PPT], suf1[PPT], suf2[PPT];
   int wk[PPT];
   int my_max = 0;
+  uint32_t n_exam = 0, n_contrib = 0;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int lp = chunk + tid + q * kBwdThreads;
@@ -75,6 +89,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
       }
     }
     my_max = max(my_max, wk[q]);
+    n_exam += (uint32_t)wk[q];
   }
   // CTA-wide max walk: entries at or beyond it are never replayed.
 #pragma unroll
@@ -151,6 +166,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
         suf2[q] += c2 * at;
         t[q] = t_here;
         any = true;
+        ++n_contrib;
         if (raw_alpha > alpha_clamp) continue;  // clamped: no alpha gradient (:289)
         acc[5] += dl_dalpha * G;
         const float dl_dd2 = dl_dalpha * op * (-G / 2.0f);
@@ -194,6 +210,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
     }
     __syncthreads();
   }
+  if (work) bwd_count_work(work, n_exam, n_contrib);
   __syncthreads();  // s_maxw and the shared batch are reused by the next chunk
   }
 }
@@ -298,7 +315,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
     const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1,
-    const uint32_t* __restrict__ order) {
+    const uint32_t* __restrict__ order, unsigned long long* __restrict__ work) {
   pdl_wait();
   // One 48-byte record per staged entry (all parts addressed from one base).
   struct alignas(16) Staged {
@@ -349,6 +366,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
       t = transmittance[p];
     }
   }
+  uint32_t n_contrib = 0;
   // Warp box over the pixels that replay anything; max walk over the CTA.
   const bool active = wk > 0;
   float bx0 = active ? px : INFINITY, bx1 = active ? px : -INFINITY;
@@ -489,6 +507,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
+        n_contrib += (uint32_t)any_a + (uint32_t)any_b;
         ma = __ballot_sync(0xffffffffu, any_a);
         mb = __ballot_sync(0xffffffffu, any_b);
         if (ma | mb) pair_level16(A, B, upper, K1);
@@ -511,6 +530,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) D[c] = 0.0f;
+        n_contrib += (uint32_t)any_c + (uint32_t)any_d;
         mc = __ballot_sync(0xffffffffu, any_c);
         md = __ballot_sync(0xffffffffu, any_d);
         if (mc | md) pair_level16(C, D, upper, K2);
@@ -544,6 +564,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     prev_count = count;
     buf ^= 1;
   }
+  if (work) bwd_count_work(work, (uint32_t)wk, n_contrib);
 }
 
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
@@ -555,7 +576,8 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
     launch_pdl(k_bwd_raster_cull, n_tiles, kBwdThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
                                                            a.transmittance, a.walked, a.dl_dimage, a.width,
                                                            a.height, a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2,
-                                                           a.records, a.touched, a.band_ty0, a.band_ty1, a.order);
+                                                           a.records, a.touched, a.band_ty0, a.band_ty1, a.order,
+                                                           a.work);
     ++g_launches;
     return;
   }
@@ -563,7 +585,7 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
   k_bwd_raster<PPT><<<n_tiles, kBwdThreads, 0, stream>>>(a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,       \
                                                          a.transmittance, a.walked, a.dl_dimage, a.width, a.height, \
                                                          a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2, a.records, a.touched, \
-                                                         a.band_ty0, a.band_ty1)
+                                                         a.band_ty0, a.band_ty1, a.work)
   if (area <= kBwdThreads) ODGS_BWD(1);
   else if (area <= 4 * kBwdThreads) ODGS_BWD(4);
   else ODGS_BWD(16);

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kLossThreads) k_l1_loss(const float* __restric
   }
 }
 
-__global__ void k_sum_partials(const double* __restrict__ partial, int64_t n, double scale, double* out) {
+__global__ void k_sum_partials(const double* __restrict__ partial, int64_t n, double scale, double* out,
+                               double* accum) {
   pdl_wait();
   __shared__ double s[256];
   double t = 0.0;
@@ -84,7 +85,10 @@ __global__ void k_sum_partials(const double* __restrict__ partial, int64_t n, do
     if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = s[0] * scale;
+  if (threadIdx.x == 0) {
+    *out = s[0] * scale;
+    if (accum) *accum += s[0] * scale;  // device-side loss sum (one readback per step)
+  }
 }
 
 size_t l1_loss_temp_bytes(int64_t count) {
@@ -93,13 +97,14 @@ size_t l1_loss_temp_bytes(int64_t count) {
 }
 
 void launch_l1_loss(const float* rendered, const float* target, int64_t count, float lambda, float* grad,
-                    double* temp, cudaStream_t stream) {
+                    double* temp, double* accum, cudaStream_t stream) {
   const int64_t blocks = (count + kLossThreads * kLossItems - 1) / (kLossThreads * kLossItems);
   const float pixels = (float)count;  // 3 * H * W, formed in Scalar as the reference does
   launch_pdl(k_l1_loss, (unsigned)blocks, kLossThreads, 0, stream, rendered, target, count, 1.0f - lambda, pixels, grad,
                                                           temp + 1);
   ++g_launches;
-  launch_pdl(k_sum_partials, 1, 256, 0, stream, temp + 1, blocks, (1.0 - (double)lambda) / (double)count, temp);
+  launch_pdl(k_sum_partials, 1, 256, 0, stream, temp + 1, blocks, (1.0 - (double)lambda) / (double)count, temp,
+             accum);
   ++g_launches;
 }
 
@@ -269,7 +274,8 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_bwd(const float* __restri
 
 // loss = (1 - lambda) sum|d| / pixels + lambda (1 - sum s / windows), fixed-order sums.
 __global__ void k_ssim_loss(const double* __restrict__ l1_partial, int64_t n_l1, const double* __restrict__ s_partial,
-                            int64_t n_s, double lambda, double pixels, double windows, double* out) {
+                            int64_t n_s, double lambda, double pixels, double windows, double* out,
+                            double* accum) {
   pdl_wait();
   __shared__ double s_a[256], s_b[256];
   double ta = 0.0, tb = 0.0;
@@ -285,7 +291,11 @@ __global__ void k_ssim_loss(const double* __restrict__ l1_partial, int64_t n_l1,
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = (1.0 - lambda) * s_a[0] / pixels + lambda * (1.0 - s_b[0] / windows);
+  if (threadIdx.x == 0) {
+    const double v = (1.0 - lambda) * s_a[0] / pixels + lambda * (1.0 - s_b[0] / windows);
+    *out = v;
+    if (accum) *accum += v;
+  }
 }
 
 size_t ssim_temp_bytes(int H, int W) {
@@ -296,7 +306,7 @@ size_t ssim_temp_bytes(int H, int W) {
 }
 
 void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda, float* grad, void* temp,
-                      double* loss_out, cudaStream_t stream) {
+                      double* loss_out, double* accum, cudaStream_t stream) {
   SsimWindow win;
   float sum = 0.0f;
   for (int i = 0; i < 11; ++i) {  // metrics.hpp:31-39 (libm exp on the host, in float)
@@ -316,7 +326,7 @@ void launch_ssim_loss(const float* a, const float* b, int H, int W, float lambda
   const float pixels = 3.0f * (float)H * (float)W;
   launch_pdl(k_ssim_bwd, gb, kSsimThreads, 0, stream, gmaps, a, b, H, W, win, lambda, pixels, grad, l1_part);
   launch_pdl(k_ssim_loss, 1, 256, 0, stream, l1_part, (int64_t)gb.x * gb.y * gb.z, s_part, (int64_t)gf.x * gf.y * gf.z,
-                                     (double)lambda, 3.0 * (double)H * (double)W, windows, loss_out);
+                                     (double)lambda, 3.0 * (double)H * (double)W, windows, loss_out, accum);
   g_launches += 3;
 }
 

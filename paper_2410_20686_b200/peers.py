@@ -34,27 +34,50 @@ def ipc_open(lib, handle: bytes) -> int:
 
 
 class BandGather:
-    """Full-image buffers of all ranks, wired into `frame` as blend outputs."""
+    """Full-image buffers of all ranks, wired into `frame` as blend outputs.
+
+    Double-buffered: frame k's bands are written into every rank's buffer k % 2, so a
+    rank may still read frame k's image (`full`) while the others already render frame
+    k + 1 into the other buffer. The rule: read a frame's image before calling sync() of
+    the next frame — that sync's barrier then orders the reads before any rank's frame
+    k + 2 writes into the same buffer. Call begin() before each band render."""
 
     def __init__(self, ctx, frame, width: int, height: int, device, group=None):
         import torch
         import torch.distributed as dist
         self.ctx, self.frame = ctx, frame
-        self.full = torch.zeros(3 * width * height, dtype=torch.float32, device=device)
+        self.buffers = [torch.zeros(3 * width * height, dtype=torch.float32, device=device) for _ in range(2)]
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.opened: List[int] = []
-        ptrs = [self.full.data_ptr()]
+        self.ptrs = [[b.data_ptr()] for b in self.buffers]  # per parity: own buffer first, then the peers'
         if world > 1:
-            handles = [None] * world
-            dist.all_gather_object(handles, ipc_handle(ctx.lib, self.full.data_ptr()), group=group)
-            for r, h in enumerate(handles):
-                if r != rank:
-                    p = ipc_open(ctx.lib, h)
-                    self.opened.append(p)
-                    ptrs.append(p)
-        frame.set_image_peers(ptrs)
+            for par, b in enumerate(self.buffers):
+                handles = [None] * world
+                dist.all_gather_object(handles, ipc_handle(ctx.lib, b.data_ptr()), group=group)
+                for r, h in enumerate(handles):
+                    if r != rank:
+                        p = ipc_open(ctx.lib, h)
+                        self.opened.append(p)
+                        self.ptrs[par].append(p)
         self.world, self.group = world, group
+        self.parity = 1
+        self._fresh = False
+        self.begin()
+
+    @property
+    def full(self):
+        """This rank's copy of the current frame (all bands after sync())."""
+        return self.buffers[self.parity]
+
+    def begin(self) -> None:
+        """Starts the next frame: its bands go into the other buffer of every rank (a no-op
+        until the current frame has been synced, so calling it before every render is safe)."""
+        if self._fresh:
+            return
+        self.parity ^= 1
+        self.frame.set_image_peers(self.ptrs[self.parity])
+        self._fresh = True
 
     def sync(self, device_id: int) -> None:
         """After every rank's band render: all full images are complete. With NCCL the
@@ -62,6 +85,7 @@ class BandGather:
         backends the device is synchronised first."""
         import torch
         import torch.distributed as dist
+        self._fresh = False
         if self.world > 1:
             if dist.get_backend(self.group) == "nccl":
                 dist.barrier(group=self.group, device_ids=[device_id])

@@ -282,6 +282,12 @@ class RenderOutput:
         self.ctx.check(self.ctx.lib.odgs_frame_work(self.ctx.handle, self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def backward_work(self):
+        """(entries replayed, contributions) of the last backward on this frame."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        self.ctx.check(self.ctx.lib.odgs_frame_backward_work(self.ctx.handle, self.handle, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def set_image_peers(self, ptrs) -> None:
         """odgs_frame_set_image_peers: the blend also writes each rendered pixel into
         these [3][W][H] float device buffers (fused band all-gather)."""
@@ -432,6 +438,64 @@ def backward(ctx: Context, cloud: GaussianCloud, camera: CameraPose, fwd: Render
     if _is_torch(grads.means) and grads.means.is_cuda:
         ctx.torch_wait()  # torch may read the gradients next
     return grads
+
+
+@dataclass
+class Splat2D:  # projection.hpp:163-174
+    pixel_mean: np.ndarray
+    cov2d: np.ndarray
+    cov2d_inv: np.ndarray
+    depth: float
+    radius: float
+    opacity: float
+    color: np.ndarray
+    index: int
+    pole_clamped: bool
+
+
+def project_gaussian(ctx: Context, cloud: GaussianCloud, i: int, camera: CameraPose,
+                     settings: RenderSettings) -> Optional[Splat2D]:
+    """projection.hpp:178-216: the splat of cloud row i, or None (std::nullopt)."""
+    if cloud.on_device:
+        ctx.wait_torch()
+    cc, cam, st = cloud.to_c(), camera.to_c(), settings.to_c()
+    out, projected = capi.Splat(), C.c_int32(0)
+    ctx.check(ctx.lib.odgs_project_gaussian(ctx.handle, C.byref(cc), int(i), C.byref(cam), C.byref(st),
+                                            C.byref(out), C.byref(projected)))
+    if not projected.value:
+        return None
+    f = lambda a: np.array(a[:], dtype=np.float32)
+    return Splat2D(f(out.pixel_mean), f(out.cov2d).reshape(2, 2), f(out.cov2d_inv).reshape(2, 2),
+                   np.float32(out.depth), np.float32(out.radius), np.float32(out.opacity), f(out.color),
+                   int(out.index), bool(out.pole_clamped))
+
+
+@dataclass
+class SplatGrads:  # backward.hpp:19-25, one row per splat of the frame
+    pixel_mean: np.ndarray  # (ns, 2)
+    cov2d: np.ndarray       # (ns, 2, 2), full-matrix convention
+    opacity: np.ndarray     # (ns,), w.r.t. the activated opacity
+    color: np.ndarray       # (ns, 3)
+
+
+def grad_pixels_to_splats(ctx: Context, fwd: RenderOutput, dl_dimage, settings: RenderSettings) -> SplatGrads:
+    """backward.hpp:208-339: per-splat gradients of a rendered frame (fwd) for the image
+    gradient dl_dimage (3, W, H)."""
+    ns = fwd.info().n_splats
+    out = SplatGrads(np.zeros((ns, 2), np.float32), np.zeros((ns, 2, 2), np.float32), np.zeros(ns, np.float32),
+                     np.zeros((ns, 3), np.float32))
+    if _is_torch(dl_dimage):
+        if dl_dimage.is_cuda:
+            ctx.wait_torch()
+        dptr, dmem = dl_dimage.data_ptr(), (capi.MEM_DEVICE if dl_dimage.is_cuda else capi.MEM_HOST)
+    else:
+        dl_dimage = np.ascontiguousarray(dl_dimage, dtype=np.float32)
+        dptr, dmem = dl_dimage.ctypes.data, capi.MEM_HOST
+    st = settings.to_c()
+    ctx.check(ctx.lib.odgs_grad_pixels_to_splats(ctx.handle, fwd.handle, C.c_void_p(dptr), dmem, C.byref(st),
+                                                 out.pixel_mean.ctypes.data, out.cov2d.ctypes.data,
+                                                 out.opacity.ctypes.data, out.color.ctypes.data))
+    return out
 
 
 def cull(ctx: Context, cloud: GaussianCloud, camera: CameraPose, near: float, far: float) -> np.ndarray:

@@ -98,6 +98,7 @@ class ViewShardedTrainer:
         self.last_densify: Optional[DensifyStats] = None
         H, W = views[0].height, views[0].width
         self.dl = self.torch.empty(3 * W * H, dtype=self.torch.float32, device=cloud.means.device)
+        self.loss_sum = self.torch.zeros(1, dtype=self.torch.float64, device=cloud.means.device)
         self.frame = RenderOutput(ctx)
         self.iteration = 0
         self._alloc_grads()
@@ -112,21 +113,22 @@ class ViewShardedTrainer:
         self.grads = GradBuffers(fv["means"], fv["rotations"], fv["log_scales"], fv["raw_opacities"],
                                  fv["colors"], fv["pixel_grad_norm"], fv["one_minus_cos"], self.observed)
 
-    def step(self) -> float:
+    def step(self, read_loss: bool = True) -> Optional[float]:
+        """One training step; returns this rank's summed photometric loss over its views
+        (one device-to-host read per step), or None with read_loss=False."""
         torch = self.torch
         ctx, lib = self.ctx, self.ctx.lib
         self.flat.zero_()
         self.observed.zero_()
-        loss_sum = 0.0
+        self.loss_sum.zero_()
         for k, v in enumerate(self.mine):
             cam = self.views[v]
             render(ctx, self.cloud, cam, self.settings, out=self.frame)
             img = self.frame.device_ptr(capi.FRAME_IMAGE)
-            loss = C_double()
-            ctx.check(lib.odgs_photometric_loss(ctx.handle, C_void(img), C_void(self.targets[v].data_ptr()),
-                                                cam.width, cam.height, self.cfg.lambda_ssim,
-                                                C_void(self.dl.data_ptr()), byref(loss)))
-            loss_sum += loss.value
+            # The loss stays on the device (added into loss_sum on the context's stream).
+            ctx.check(lib.odgs_photometric_loss_async(ctx.handle, C_void(img), C_void(self.targets[v].data_ptr()),
+                                                      cam.width, cam.height, self.cfg.lambda_ssim,
+                                                      C_void(self.dl.data_ptr()), C_void(self.loss_sum.data_ptr())))
             backward(ctx, self.cloud, cam, self.frame, self.dl, self.settings, grads=self.grads, accumulate=True)
         allreduce_grads(self.flat, self.observed, self.group)
         ctx.wait_torch()  # Adam reads the reduced gradients
@@ -149,7 +151,10 @@ class ViewShardedTrainer:
                 self._alloc_grads()
             if d.opacity_reset_interval > 0 and step % d.opacity_reset_interval == 0:
                 reset_opacity(ctx, self.cloud, self.state)
-        return loss_sum
+        if not read_loss:
+            return None
+        ctx.torch_wait()
+        return float(self.loss_sum.item())
 
 
 # ctypes shorthands

@@ -350,7 +350,7 @@ int main() {
     odgs::GradTSigns flip;
     flip.sign[3] = -1.0;
     const GradF gflip = odgs::backward(ra, small, fa, probe, s8, &flip);
-    CHECK(!(gflip.rotations.v == ga.rotations.v));
+    CHECK(!(gflip.means.v == ga.means.v));  // dL/dT feeds the mean gradient (backward.hpp:413-418)
     CHECK(gflip.colors.v == ga.colors.v);
     // the reference-style template caller routes to the GPU (argument-dependent lookup)
     const GradF gv = odgs::view_step(ra, small, probe, s8);

@@ -152,10 +152,14 @@ def _gather_rank(rank, world, port, q):
         W, H = 512, 256
         g = BandGather(ctx, fr, W, H, torch.device("cuda", 0))
         rows = H // world
-        render_band(ctx, scenes.cloud_c3(20_000), CameraPose(W, H), RenderSettings(), rank * rows, (rank + 1) * rows,
-                    out=fr)
-        g.sync(0)
-        q.put((rank, g.full.cpu().numpy()))
+        frames = []
+        for k in range(3):  # consecutive frames alternate between the two image buffers
+            g.begin()
+            render_band(ctx, scenes.cloud_c3(20_000), scenes.yaw_camera(0.5 * k, W, H), RenderSettings(),
+                        rank * rows, (rank + 1) * rows, out=fr)
+            g.sync(0)
+            frames.append(g.full.cpu().numpy())
+        q.put((rank, frames))
         dist.barrier()
         g.close()
         dist.destroy_process_group()
@@ -180,10 +184,12 @@ def test_band_gather_two_ranks_on_one_gpu(gpu_ctx):
     res = dict(q.get(timeout=300) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
-    ref = render(gpu_ctx, scenes.cloud_c3(20_000), CameraPose(512, 256), RenderSettings()).image
     for r in range(2):
         assert not isinstance(res[r], str), res[r]
-        assert np.array_equal(res[r].reshape(3, 512, 256), ref), r
+    for k in range(3):
+        ref = render(gpu_ctx, scenes.cloud_c3(20_000), scenes.yaw_camera(0.5 * k, 512, 256), RenderSettings()).image
+        for r in range(2):
+            assert np.array_equal(res[r][k].reshape(3, 512, 256), ref), (r, k)
 
 
 @pytest.mark.parametrize("tile,yaw", [(16, 0.0), (8, 0.7), (32, -1.3)])

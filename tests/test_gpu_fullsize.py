@@ -116,20 +116,26 @@ def test_c4_full_size_train_step(gpu_ctx):
             gpu_ctx.handle, C.c_void_p(fr.device_ptr(capi.FRAME_IMAGE)), C.c_void_p(tgt.data_ptr()), W, H,
             cfg.lambda_ssim, C.c_void_p(dl.data_ptr()), C.byref(loss)))
         g = backward(gpu_ctx, cloud, cam, fr, dl, gs)  # host GradBuffers
+        # The float oracle's isZero() skips pixels with |dL/dpixel| <= 1e-5
+        # (backward.hpp:248); the photometric gradient is ~1e-7 per pixel, so the oracle
+        # would drop every pixel. The comparison runs on dl * 2^20 (an
+        # exact scaling; the gradients are linear in dl) on both sides.
+        dl_big = dl * float(2 ** 20)
+        g_big = backward(gpu_ctx, cloud, cam, fr, dl_big, gs)
         r, t = cam32(cam)
         of = oracle_lib.render(arrs, r, t, W, H, os_, portable=True)
         assert np.array_equal(fr.walked.ravel(), of.get("walked")), v
         assert np.array_equal(fr.image.ravel(), of.get("image").astype(np.float32)), v
-        of.backward(dl.cpu().numpy().astype(np.float64))
+        of.backward(dl_big.cpu().numpy().astype(np.float64))
         o = {"means": of.get("g_means"), "rotations": of.get("g_rotations"), "log_scales": of.get("g_log_scales"),
              "raw_opacities": of.get("g_raw_opacities"), "colors": of.get("g_colors")}
         for k in GROUPS:
-            assert group_rel(getattr(g, k), o[k]) < 1e-3, (v, k, group_rel(getattr(g, k), o[k]))
-        assert np.array_equal(g.observed, of.get("g_observed")), v
-        assert np.abs(g.one_minus_cos - of.get("g_one_minus_cos")).max() < 1e-5, v
-        assert group_rel(g.pixel_grad_norm, of.get("g_pixel_grad_norm")) < 1e-3, v
+            assert group_rel(getattr(g_big, k), o[k]) < 1e-3, (v, k, group_rel(getattr(g_big, k), o[k]))
+        assert np.array_equal(g_big.observed, of.get("g_observed")), v
+        assert np.abs(g_big.one_minus_cos - of.get("g_one_minus_cos")).max() < 1e-5, v
+        assert group_rel(g_big.pixel_grad_norm, of.get("g_pixel_grad_norm")) < 1e-3, v
         cur = {k: getattr(g, k).copy() for k in GROUPS + ["pixel_grad_norm", "one_minus_cos", "observed"]}
-        osum = {k: o[k].astype(np.float32).reshape(cur[k].shape) for k in GROUPS}
+        osum = {k: (o[k] / 2.0 ** 20).astype(np.float32).reshape(cur[k].shape) for k in GROUPS}
         if gpu_sum is None:
             gpu_sum, oracle_sum = cur, osum
         else:

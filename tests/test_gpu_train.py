@@ -158,3 +158,72 @@ def test_photometric_loss_with_ssim_matches_oracle(gpu_ctx, lam):
     assert abs(loss.value - oloss) <= 1e-5 * abs(oloss)
     g = grad.cpu().numpy().astype(np.float64)
     assert np.abs(g - g64).max() <= 1e-4 * np.abs(g64).max()
+
+
+def _trainer_setup(ctx, world, rank, group=None):
+    arrs = oracle_lib.random_cloud(303, 6000)
+    host = to_cloud32(arrs)
+    cloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(host, k))).cuda()
+                            for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")])
+    W, H = 512, 256
+    from paper_2410_20686_b200 import scenes
+    views = scenes.c4_views(W, H, 2)
+    tcloud = to_cloud32(oracle_lib.random_cloud(304, 6000))
+    targets = [torch.from_numpy(render(ctx, tcloud, v, RenderSettings()).image.ravel()).cuda() for v in views]
+    return ViewShardedTrainer(ctx, cloud, views, targets, RenderSettings(), TrainConfig(), extent=10.0, rank=rank,
+                              world=world, group=group)
+
+
+def _sharded_rank(rank, world, port, q):
+    try:
+        import os
+        import torch.distributed as dist
+        from paper_2410_20686_b200 import Context
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ctx = Context(0)
+        tr = _trainer_setup(ctx, world, rank)
+        losses = [tr.step() for _ in range(2)]
+        torch.cuda.synchronize()
+        out = {k: getattr(tr.cloud, k).cpu().numpy() for k in ("means", "rotations", "log_scales", "raw_opacities",
+                                                               "colors")}
+        q.put((rank, (out, losses, tr.mine)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+def test_view_sharded_trainer_two_ranks_matches_one_process(gpu_ctx):
+    """ViewShardedTrainer.step() on two ranks (two processes on GPU 0, gloo all-reduce of
+    the CUDA gradient buffers): after two steps every rank's cloud equals the
+    single-process trainer's over both views, bit for bit (the all-reduced sum g0 + g1
+    adds the same floats as the local accumulation 0 + g0 + g1, and every rank runs the
+    identical Adam step)."""
+    import multiprocessing as mp
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    procs = [ctx_mp.Process(target=_sharded_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert not isinstance(res[r], str), res[r]
+    assert res[0][2] == [0] and res[1][2] == [1]
+    tr = _trainer_setup(gpu_ctx, 1, 0)
+    losses = [tr.step() for _ in range(2)]
+    torch.cuda.synchronize()
+    for k in ("means", "rotations", "log_scales", "raw_opacities", "colors"):
+        ref = getattr(tr.cloud, k).cpu().numpy()
+        for r in range(2):
+            assert np.array_equal(res[r][0][k], ref), (r, k)
+    # the per-rank losses add up to the single-process loss (each rank sums its views)
+    for step in range(2):
+        assert abs(res[0][1][step] + res[1][1][step] - losses[step]) <= 1e-12 * abs(losses[step])
