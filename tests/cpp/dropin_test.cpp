@@ -348,7 +348,7 @@ int main() {
     CHECK(threw);
     // GradTSigns reaches the T-gradient stage (backward.hpp:32-34)
     odgs::GradTSigns flip;
-    flip.sign[3] = -1.0;
+    flip.sign[0] = -1.0;  // entry (1,1): reaches dJ(0,0), hence the mean gradient
     const GradF gflip = odgs::backward(ra, small, fa, probe, s8, &flip);
     CHECK(!(gflip.means.v == ga.means.v));  // dL/dT feeds the mean gradient (backward.hpp:413-418)
     CHECK(gflip.colors.v == ga.colors.v);
