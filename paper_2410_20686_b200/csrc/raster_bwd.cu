@@ -13,10 +13,24 @@
 //                 Sigma_2D transport (:329-337), then the per-splat chain rule
 //                 (:393-438) incl. the densify statistics, plus the error checks
 //                 (pole axis :79-80, non-finite gradient :440-446).
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace odgs_b200 {
+
+// The warp-specialised pipelined kernel (k_bwd_raster_pipe) unless ODGS_BWD_KERNEL=barrier
+// selects the previous two-barrier kernel (A/B measurements).
+static bool use_pipe_kernel() {
+  static const bool pipe = [] {
+    const char* e = std::getenv("ODGS_BWD_KERNEL");
+    return !(e && std::strcmp(e, "barrier") == 0);
+  }();
+  return pipe;
+}
 
 constexpr int kBwdThreads = 256;
 constexpr int kBwdWarps = kBwdThreads / 32;
@@ -567,11 +581,363 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
   if (work) bwd_count_work(work, (uint32_t)wk, n_contrib);
 }
 
+// ------------------------------------------------------------------ warp-specialised backward raster
+// One CTA per tile (up to 16x16): kPipeWarps compute warps each own an 8x8 pixel block
+// (two pixels per lane, so one warp reduction covers 64 pixels) and one producer warp
+// feeds them through a ring of kPipeStages shared-memory slots of kPipeBatch entries,
+// synchronised with mbarriers instead of CTA barriers:
+//   producer  per batch (back to front): wait until every compute warp released the
+//             slot (empty), sum the slot's previous per-warp partials in warp order and
+//             write their records, stage the new batch (entry data, per-warp cull masks,
+//             emit positions), arrive on full;
+//   compute   per batch: wait full, compact the warp's entries, walk them four at a time
+//             (two pixels per lane, reduce-scatter of the 4 x 9 sums over the warp),
+//             store the warp's partials in the slot, arrive on empty.
+// A warp can run up to kPipeStages - 1 batches ahead of the slowest one, so per-batch
+// imbalance between the warps' lists no longer stalls the CTA (the previous kernel's two
+// __syncthreads per batch). Records and their fixed summation order are as before:
+// deterministic, no atomics.
+constexpr int kPipeWarps = 4;
+constexpr int kPipeThreads = (kPipeWarps + 1) * 32;
+constexpr int kPipeBatch = 64;
+constexpr int kPipeStages = 4;
+
+struct alignas(16) PipeEntry {
+  float4 geo;  // cx, cy, i00, 2*i01
+  float4 att;  // i11, opacity, r, g
+  float4 b;    // b, -, -, -
+};
+struct PipeSlot {
+  PipeEntry ent[kPipeBatch];
+  float part[kPipeWarps][kRec][kPipeBatch];  // per-warp sums, component-major
+  uint32_t pos[kPipeBatch];                  // emit position of the entry
+  uint8_t mask[kPipeBatch];                  // warps whose block the entry can touch
+  uint8_t wrote[kPipeWarps][kPipeBatch];     // warp stored a partial (cleared by the producer)
+};
+struct PipeSmem {
+  PipeSlot slot[kPipeStages];
+  unsigned long long full[kPipeStages], empty[kPipeStages];
+  float4 wbox[kPipeWarps];
+  int maxw[kPipeWarps];
+  uint8_t list[kPipeWarps][kPipeBatch];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// bwd_contrib for both pixels of a lane, summed into acc; true if either contributed.
+__device__ __forceinline__ bool bwd_contrib2(const PipeEntry& en, int rel, const int wk[2], const float px[2],
+                                             const float py[2], float cutoff2, float alpha_clamp, const float d0[2],
+                                             const float d1[2], const float d2v[2], float t[2], float sd[2],
+                                             float acc[kRec]) {
+  float a1[kRec];
+  const bool c0 = bwd_contrib(en.geo, en.att, en.b.x, rel, wk[0], px[0], py[0], cutoff2, alpha_clamp, d0[0], d1[0],
+                              d2v[0], t[0], sd[0], acc);
+  const bool c1 = bwd_contrib(en.geo, en.att, en.b.x, rel, wk[1], px[1], py[1], cutoff2, alpha_clamp, d0[1], d1[1],
+                              d2v[1], t[1], sd[1], a1);
+#pragma unroll
+  for (int c = 0; c < kRec; ++c) acc[c] += a1[c];
+  return c0 || c1;
+}
+
+__global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
+    const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
+    const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
+    const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
+    const float* __restrict__ dl_dimage, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
+    float cutoff2, float* __restrict__ records, uint8_t* __restrict__ touched, int band_ty0, int band_ty1,
+    const uint32_t* __restrict__ order, unsigned long long* __restrict__ work) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(s_raw);
+  const int tile = band_ty0 * tiles_x + (int)(order ? order[blockIdx.x] : blockIdx.x);
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const int e0 = offsets[tile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == kPipeWarps;
+  const int64_t plane = (int64_t)width * height;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+
+  // Compute warps: two pixels per lane. 16x16 tiles: warp w owns the 8x8 block at
+  // (8 (w & 1), 8 (w >> 1)); lanes run down a column in fours (the image is column-major),
+  // the second pixel 4 rows lower. Smaller tiles: slots warp*64 + 32q + lane, column-major.
+  float px[2], py[2], t[2] = {1.0f, 1.0f}, d0[2] = {0.0f, 0.0f}, d1[2] = {0.0f, 0.0f}, d2v[2] = {0.0f, 0.0f};
+  float sd[2] = {0.0f, 0.0f};
+  int wk[2] = {0, 0};
+  uint32_t n_contrib = 0;
+  if (!producer) {
+    float bx0 = INFINITY, bx1 = -INFINITY, by0 = INFINITY, by1 = -INFINITY;
+    int my_max = 0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      int lx, ly;
+      bool valid;
+      if (tile_size == 16) {
+        lx = (warp & 1) * 8 + (lane >> 2);
+        ly = (warp >> 1) * 8 + (lane & 3) + 4 * q;
+        valid = true;
+      } else {
+        const int sl = warp * 64 + q * 32 + lane;
+        lx = sl / tile_size;
+        ly = sl - lx * tile_size;
+        valid = sl < tile_size * tile_size;
+      }
+      const int x = tx * tile_size + lx, y = ty * tile_size + ly;
+      valid = valid && x < width && y < height;
+      px[q] = (float)x + 0.5f;
+      py[q] = (float)y + 0.5f;
+      if (valid) {
+        const int64_t p = (int64_t)x * height + y;
+        d0[q] = dl_dimage[p];
+        d1[q] = dl_dimage[plane + p];
+        d2v[q] = dl_dimage[2 * plane + p];
+        // Only exact zeros are skipped (the reference's float isZero()).
+        if (d0[q] != 0.0f || d1[q] != 0.0f || d2v[q] != 0.0f) {
+          wk[q] = walked_in[p];
+          t[q] = transmittance[p];
+        }
+      }
+      if (wk[q] > 0) {  // the warp box covers the pixels that replay anything
+        bx0 = fminf(bx0, px[q]);
+        bx1 = fmaxf(bx1, px[q]);
+        by0 = fminf(by0, py[q]);
+        by1 = fmaxf(by1, py[q]);
+      }
+      my_max = max(my_max, wk[q]);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, d));
+      bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, d));
+      by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, d));
+      by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, d));
+      my_max = max(my_max, __shfl_xor_sync(0xffffffffu, my_max, d));
+    }
+    if (lane == 0) {
+      S.maxw[warp] = my_max;
+      S.wbox[warp] = make_float4(bx0, bx1, by0, by1);
+    }
+  } else {
+    if (lane < kPipeStages) {
+      mbar_init(&S.full[lane], 32);                 // the producer warp's lanes
+      mbar_init(&S.empty[lane], kPipeWarps * 32);   // every compute lane
+    }
+    for (int k = lane; k < kPipeStages * kPipeWarps * kPipeBatch; k += 32)
+      (&S.slot[k / (kPipeWarps * kPipeBatch)].wrote[0][0])[k % (kPipeWarps * kPipeBatch)] = 0;
+  }
+  __syncthreads();  // pixel boxes, walks, barrier initialisation
+  int max_walked = 0;
+#pragma unroll
+  for (int w = 0; w < kPipeWarps; ++w) max_walked = max(max_walked, S.maxw[w]);
+  const int n_batches = (max_walked + kPipeBatch - 1) / kPipeBatch;
+
+  if (producer) {
+    for (int i = 0; i < n_batches + kPipeStages; ++i) {
+      const int st = i % kPipeStages;
+      PipeSlot& sl = S.slot[st];
+      const int prev = i - kPipeStages;
+      if (prev >= 0 && prev < n_batches) {
+        // Records of batch `prev`: the per-warp partials summed in warp order.
+        mbar_wait(&S.empty[st], (uint32_t)(prev / kPipeStages) & 1u);
+        const int hi = max_walked - prev * kPipeBatch;
+        const int count = min(kPipeBatch, hi);
+        for (int k = lane; k < count; k += 32) {
+          if (!sl.mask[k]) continue;
+          float sum[kRec];
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) sum[c] = 0.0f;
+          bool any = false;
+#pragma unroll
+          for (int w = 0; w < kPipeWarps; ++w)
+            if (sl.wrote[w][k]) {
+              sl.wrote[w][k] = 0;
+              any = true;
+#pragma unroll
+              for (int c = 0; c < kRec; ++c) sum[c] += sl.part[w][c][k];
+            }
+          if (any) {
+            const uint32_t pos = sl.pos[k];
+            float* r = records + (int64_t)pos * kRec;
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) r[c] = sum[c];
+            touched[pos] = 1;
+          }
+        }
+      }
+      if (i < n_batches) {
+        // Stage batch i: entries [lo, hi) of the tile list, back to front.
+        const int hi = max_walked - i * kPipeBatch;
+        const int lo = max(0, hi - kPipeBatch);
+        const int count = hi - lo;
+        for (int k = lane; k < kPipeBatch; k += 32) {
+          uint32_t mask = 0;
+          if (k < count) {
+            const int rel = lo + k;
+            const uint32_t v = vals[e0 + rel];
+            const uint32_t g = v >> 2;
+            const int sk = (int)(v & 3u);
+            const float4 a = __ldg(sp_ab + 2 * (int64_t)g);
+            const float4 b = __ldg(sp_ab + 2 * (int64_t)g + 1);
+            const float4 c = __ldg(sp_c + g);
+            const float cx = a.x + shift_of(sk, width), cy = a.y;
+            sl.ent[k].geo = make_float4(cx, cy, a.z, 2.0f * a.w);
+            sl.ent[k].att = b;
+            sl.ent[k].b.x = c.x;
+            float ex, ey;
+            const bool cullable = cull_extents(a.z, a.w, b.x, cutoff2, &ex, &ey);
+#pragma unroll
+            for (int w = 0; w < kPipeWarps; ++w) {
+              const float4 bx = S.wbox[w];
+              const bool out = rel >= S.maxw[w] || (cullable && ((bx.x - cx > ex) || (bx.y - cx < -ex) ||
+                                                                 (bx.z - cy > ey) || (bx.w - cy < -ey)));
+              mask |= out ? 0u : (1u << w);
+            }
+            if (mask) {
+              // Emit position of (tile, g, shift): first entry of g + earlier shifts' areas +
+              // row-major offset inside this shift's (band-clipped) tile rectangle.
+              uint32_t pos = __ldg(ent_off_idx + g);
+              for (int kk = 0; kk <= sk; ++kk) {
+                int span[4];
+                if (!band_tiles(a.x, a.y, c.z, kk, width, height, tile_size, band_ty0, band_ty1, span)) continue;
+                const uint32_t wd = (uint32_t)(span[1] - span[0] + 1);
+                if (kk < sk) pos += wd * (uint32_t)(span[3] - span[2] + 1);
+                else pos += (uint32_t)(ty - span[2]) * wd + (uint32_t)(tx - span[0]);
+              }
+              sl.pos[k] = pos;
+            }
+          }
+          sl.mask[k] = (uint8_t)mask;
+        }
+        mbar_arrive(&S.full[st]);
+      }
+    }
+  } else {
+    const bool upper = lane & 16, mid = lane & 8;
+    for (int i = 0; i < n_batches; ++i) {
+      const int st = i % kPipeStages;
+      PipeSlot& sl = S.slot[st];
+      mbar_wait(&S.full[st], (uint32_t)(i / kPipeStages) & 1u);
+      const int lo = max(0, max_walked - i * kPipeBatch - kPipeBatch);
+      int n_list = 0;
+#pragma unroll
+      for (int cidx = 0; cidx < kPipeBatch / 32; ++cidx) {
+        const bool mine = (sl.mask[cidx * 32 + lane] >> warp) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (mine) S.list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(cidx * 32 + lane);
+        n_list += __popc(bal);
+      }
+      __syncwarp();
+      // Back to front over this warp's entries, four at a time: the 4 x 9 per-lane sums
+      // (two pixels each) are reduce-scattered over the warp; the totals land on lanes 0
+      // (A), 8 (C), 16 (B) and 24 (D).
+      for (int qi = n_list - 1; qi >= 0; qi -= 4) {
+        const int ja = S.list[warp][qi];
+        const int jb = qi >= 1 ? S.list[warp][qi - 1] : -1;
+        const int jc = qi >= 2 ? S.list[warp][qi - 2] : -1;
+        const int jd = qi >= 3 ? S.list[warp][qi - 3] : -1;
+        float K1[kRec], K2[kRec];
+        unsigned ma, mb, mc, md;
+        {
+          float A[kRec], B[kRec];
+          const bool any_a = bwd_contrib2(sl.ent[ja], lo + ja, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v, t, sd, A);
+          bool any_b = false;
+          if (jb >= 0)
+            any_b = bwd_contrib2(sl.ent[jb], lo + jb, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v, t, sd, B);
+          else
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
+          n_contrib += (uint32_t)any_a + (uint32_t)any_b;
+          ma = __ballot_sync(0xffffffffu, any_a);
+          mb = __ballot_sync(0xffffffffu, any_b);
+          if (ma | mb) pair_level16(A, B, upper, K1);
+          else
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) K1[c] = 0.0f;
+        }
+        {
+          float Cc[kRec], D[kRec];
+          bool any_c = false, any_d = false;
+          if (jc >= 0)
+            any_c = bwd_contrib2(sl.ent[jc], lo + jc, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v, t, sd, Cc);
+          else
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) Cc[c] = 0.0f;
+          if (jd >= 0)
+            any_d = bwd_contrib2(sl.ent[jd], lo + jd, wk, px, py, cutoff2, alpha_clamp, d0, d1, d2v, t, sd, D);
+          else
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) D[c] = 0.0f;
+          n_contrib += (uint32_t)any_c + (uint32_t)any_d;
+          mc = __ballot_sync(0xffffffffu, any_c);
+          md = __ballot_sync(0xffffffffu, any_d);
+          if (mc | md) pair_level16(Cc, D, upper, K2);
+          else
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) K2[c] = 0.0f;
+        }
+        if (ma | mb | mc | md) {
+          float L[kRec];
+#pragma unroll
+          for (int c = 0; c < kRec; ++c) {
+            const float r = __shfl_xor_sync(0xffffffffu, mid ? K1[c] : K2[c], 8);
+            L[c] = (mid ? K2[c] : K1[c]) + r;
+          }
+#pragma unroll
+          for (int d = 4; d > 0; d >>= 1)
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) L[c] += __shfl_xor_sync(0xffffffffu, L[c], d);
+          const int grp = lane >> 3;  // 0: A, 1: C, 2: B, 3: D
+          const unsigned mine = grp == 0 ? ma : (grp == 1 ? mc : (grp == 2 ? mb : md));
+          if ((lane & 7) == 0 && mine) {
+            const int j = grp == 0 ? ja : (grp == 1 ? jc : (grp == 2 ? jb : jd));
+            mean_grad_from_moments(sl.ent[j].geo, sl.ent[j].att.x, L[0], L[1]);
+#pragma unroll
+            for (int c = 0; c < kRec; ++c) sl.part[warp][c][j] = L[c];
+            sl.wrote[warp][j] = 1;
+          }
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&S.empty[st]);
+    }
+  }
+  if (work && !producer) bwd_count_work(work, (uint32_t)(wk[0] + wk[1]), n_contrib);
+}
+
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
   const int n_tiles = a.tiles_x * (a.band_ty1 - a.band_ty0);
   if (n_tiles <= 0) return;
   const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
   const int area = a.tile_size * a.tile_size;
+  if (!a.plain && a.tile_size <= 16 && use_pipe_kernel()) {
+    constexpr size_t smem = sizeof(PipeSmem);
+    static std::atomic<uint64_t> opted{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(opted.load() & (1ull << (dev & 63)))) {
+      cudaFuncSetAttribute(k_bwd_raster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      opted.fetch_or(1ull << (dev & 63));
+    }
+    launch_pdl(k_bwd_raster_pipe, n_tiles, kPipeThreads, smem, stream, a.offsets, a.vals, a.sp_ab, a.sp_c,
+               a.ent_off_idx, a.transmittance, a.walked, a.dl_dimage, a.width, a.height, a.tile_size, a.tiles_x,
+               a.alpha_clamp, cutoff2, a.records, a.touched, a.band_ty0, a.band_ty1, a.order, a.work);
+    ++g_launches;
+    return;
+  }
   if (!a.plain && a.tile_size <= 16) {
     launch_pdl(k_bwd_raster_cull, n_tiles, kBwdThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
                                                            a.transmittance, a.walked, a.dl_dimage, a.width,
