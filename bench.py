@@ -506,7 +506,7 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
     # view of one step (forward examined / composited, backward replayed / contributing).
     ctx.set_profiling(True)
     ctx.reset_stage_times()
-    fwd_work, bwd_work = [0, 0], [0, 0]
+    fwd_work, bwd_work = [0, 0], [0, 0, 0, 0]
     orig_backward = tr.frame  # the trainer renders every view into tr.frame
     import paper_2410_20686_b200.train as train_mod
     real_backward = train_mod.backward
@@ -516,7 +516,8 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
         w = orig_backward.work()
         b = orig_backward.backward_work()
         fwd_work[0] += w[0]; fwd_work[1] += w[1]
-        bwd_work[0] += b[0]; bwd_work[1] += b[1]
+        for j in range(4):
+            bwd_work[j] += b[j]
         return out
     train_mod.backward = counting_backward
     try:
@@ -590,7 +591,8 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
             "collective": "NCCL all-reduce (sum) of 16n floats + n int32" if world > 1 else "none (1 rank)",
             "stage_ms_per_step": {k: round(v, 4) for k, v in stages.items()},
             "work_per_view": {"fwd_examined": fwd_work[0] / nv, "fwd_composited": fwd_work[1] / nv,
-                              "bwd_replayed": bwd_work[0] / nv, "bwd_contributions": bwd_work[1] / nv},
+                              "bwd_replayed": bwd_work[0] / nv, "bwd_contributions": bwd_work[1] / nv,
+                              "bwd_warp_entries": bwd_work[2] / nv, "bwd_warp_entries_live": bwd_work[3] / nv},
             "roofline": roof, "cpu_baseline": cpu, "first_loss": first_loss, "last_loss": last_loss}
 
 

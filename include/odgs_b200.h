@@ -203,11 +203,12 @@ odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, voi
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_examined,
                             int64_t* entries_composited);
 /* Backward work of the last odgs_backward / odgs_grad_pixels_to_splats on `frame` (for
-   rooflines): entries replayed (sum over pixels with a non-zero image gradient of their
-   walk length — the reference's replay loop, backward.hpp:251-269) and contributions
-   (replayed entries inside the cutoff, :271-305). Synchronizes. */
-odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_replayed,
-                                     int64_t* entries_contributing);
+   rooflines), up to n_counters (<= 4) values: [0] entries replayed (sum over pixels with
+   a non-zero image gradient of their walk length — the reference's replay loop,
+   backward.hpp:251-269), [1] contributions (replayed entries inside the cutoff,
+   :271-305), [2] warp-entries walked by the culled kernel (sum of its warps' list
+   lengths), [3] warp-entries with at least one contributing pixel. Synchronizes. */
+odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* counters, int32_t n_counters);
 /* Row bands over several GPUs: the blend also writes every pixel it
    renders into each of these n <= 8 image buffers ([3][W][H] float, the frame's
    layout) — typically the other ranks' full-image buffers opened with odgs_ipc_open —

@@ -123,7 +123,7 @@ SIGNATURES = {
     "odgs_frame_get_info": (C.c_int, [_P, C.POINTER(FrameInfo)]),
     "odgs_frame_download": (C.c_int, [_P, _P, C.c_int, _P, C.c_size_t]),
     "odgs_frame_work": (C.c_int, [_P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
-    "odgs_frame_backward_work": (C.c_int, [_P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "odgs_frame_backward_work": (C.c_int, [_P, _P, C.POINTER(C.c_int64), C.c_int32]),
     "odgs_frame_device_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "odgs_prepare_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),
     "odgs_render": (C.c_int, [_P, C.POINTER(Cloud), C.POINTER(Camera), C.POINTER(Settings), _P]),

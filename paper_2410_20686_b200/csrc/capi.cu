@@ -602,8 +602,8 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
   ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
   ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
   ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
-  ODGS_CUDA(ctx, ensure(f->bwd_work, 2 * sizeof(unsigned long long), s));
-  ODGS_CUDA(ctx, cudaMemsetAsync(f->bwd_work.p, 0, 2 * sizeof(unsigned long long), s));
+  ODGS_CUDA(ctx, ensure(f->bwd_work, 4 * sizeof(unsigned long long), s));
+  ODGS_CUDA(ctx, cudaMemsetAsync(f->bwd_work.p, 0, 4 * sizeof(unsigned long long), s));
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_RASTER);
     if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, (size_t)K, s));
@@ -880,14 +880,12 @@ odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camer
   return st;
 }
 
-odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_replayed,
-                                     int64_t* entries_contributing) {
+odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* f, int64_t* counters, int32_t n_counters) {
   if (!ctx || !f || !f->bwd_work.p) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "no backward on this frame");
-  unsigned long long w[2];
+  unsigned long long w[4];
   ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->bwd_work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
   ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  if (entries_replayed) *entries_replayed = (int64_t)w[0];
-  if (entries_contributing) *entries_contributing = (int64_t)w[1];
+  for (int k = 0; k < n_counters && k < 4; ++k) counters[k] = (int64_t)w[k];
   return ok(ctx);
 }
 

@@ -40,12 +40,17 @@ constexpr int kRec = 9;  // mx, my, m00, m01, m11, op, c0, c1, c2
 // Backward work counters for the roofline (bench.py): entries replayed (sum over pixels
 // with a gradient of their walk, the reference's replay loop, backward.hpp:251-269) and
 // contributions (replayed entries inside the cutoff, :271-305).
-__device__ __forceinline__ void bwd_count_work(unsigned long long* work, uint32_t exam, uint32_t contrib) {
+// work[2..3] (culled kernels): warp-entries walked (sum of the warps' list lengths) and
+// warp-entries with at least one contributing lane — the culling's efficiency.
+__device__ __forceinline__ void bwd_count_work(unsigned long long* work, uint32_t exam, uint32_t contrib,
+                                               uint32_t warp_entries = 0, uint32_t warp_live = 0) {
   const uint32_t we = __reduce_add_sync(0xffffffffu, exam);
   const uint32_t wc = __reduce_add_sync(0xffffffffu, contrib);
-  if ((threadIdx.x & 31) == 0 && (we | wc)) {
+  if ((threadIdx.x & 31) == 0 && (we | wc | warp_entries)) {
     atomicAdd(work, (unsigned long long)we);
     atomicAdd(work + 1, (unsigned long long)wc);
+    atomicAdd(work + 2, (unsigned long long)warp_entries);
+    atomicAdd(work + 3, (unsigned long long)warp_live);
   }
 }
 
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
       t = transmittance[p];
     }
   }
-  uint32_t n_contrib = 0;
+  uint32_t n_contrib = 0, n_wentries = 0, n_wlive = 0;
   // Warp box over the pixels that replay anything; max walk over the CTA.
   const bool active = wk > 0;
   float bx0 = active ? px : INFINITY, bx1 = active ? px : -INFINITY;
@@ -503,6 +508,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     // level 8 splits AB|CD, levels 4-2-1 finish) — 54 shuffles per 4 entries. The
     // totals land on lanes 0 (A), 8 (C), 16 (B) and 24 (D).
     const bool upper = lane & 16, mid = lane & 8;
+    n_wentries += (uint32_t)n_list;
     for (int qi = n_list - 1; qi >= 0; qi -= 4) {
       const int ja = s_list[warp][qi];
       const int jb = qi >= 1 ? s_list[warp][qi - 1] : -1;
@@ -552,6 +558,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
 #pragma unroll
           for (int c = 0; c < kRec; ++c) K2[c] = 0.0f;
       }
+      n_wlive += (uint32_t)(ma != 0) + (uint32_t)(mb != 0) + (uint32_t)(mc != 0) + (uint32_t)(md != 0);
       if (ma | mb | mc | md) {
         float L[kRec];
 #pragma unroll
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     prev_count = count;
     buf ^= 1;
   }
-  if (work) bwd_count_work(work, (uint32_t)wk, n_contrib);
+  if (work) bwd_count_work(work, (uint32_t)wk, n_contrib, n_wentries, n_wlive);
 }
 
 // ------------------------------------------------------------------ warp-specialised backward raster
@@ -597,10 +604,23 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
 // imbalance between the warps' lists no longer stalls the CTA (the previous kernel's two
 // __syncthreads per batch). Records and their fixed summation order are as before:
 // deterministic, no atomics.
+#ifndef ODGS_PIPE_STAGES
+#define ODGS_PIPE_STAGES 4
+#endif
+#ifndef ODGS_PIPE_MINB
+#define ODGS_PIPE_MINB 4
+#endif
+#ifndef ODGS_PIPE_WIDE
+#define ODGS_PIPE_WIDE 0
+#endif
+#ifndef ODGS_PIPE_SLEEP
+#define ODGS_PIPE_SLEEP 0
+#endif
 constexpr int kPipeWarps = 4;
 constexpr int kPipeThreads = (kPipeWarps + 1) * 32;
 constexpr int kPipeBatch = 64;
-constexpr int kPipeStages = 4;
+constexpr int kPipeStages = ODGS_PIPE_STAGES;
+constexpr bool kPipeWide = ODGS_PIPE_WIDE;  // 16x4 warp blocks instead of 8x8
 
 struct alignas(16) PipeEntry {
   float4 geo;  // cx, cy, i00, 2*i01
@@ -629,6 +649,23 @@ __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t coun
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The producer's wait: try_wait with a nanosleep back-off, so an idle producer does not
+// take issue slots from the compute warps.
+__device__ __forceinline__ void mbar_wait_backoff(unsigned long long* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (ODGS_PIPE_SLEEP > 0) __nanosleep(ODGS_PIPE_SLEEP);
+  }
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred done;\n"
@@ -654,7 +691,7 @@ __device__ __forceinline__ bool bwd_contrib2(const PipeEntry& en, int rel, const
   return c0 || c1;
 }
 
-__global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
+__global__ void __launch_bounds__(kPipeThreads, ODGS_PIPE_MINB) k_bwd_raster_pipe(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
     const float* __restrict__ transmittance, const int32_t* __restrict__ walked_in,
@@ -678,7 +715,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
   float px[2], py[2], t[2] = {1.0f, 1.0f}, d0[2] = {0.0f, 0.0f}, d1[2] = {0.0f, 0.0f}, d2v[2] = {0.0f, 0.0f};
   float sd[2] = {0.0f, 0.0f};
   int wk[2] = {0, 0};
-  uint32_t n_contrib = 0;
+  uint32_t n_contrib = 0, n_wentries = 0, n_wlive = 0;
   if (!producer) {
     float bx0 = INFINITY, bx1 = -INFINITY, by0 = INFINITY, by1 = -INFINITY;
     int my_max = 0;
@@ -687,8 +724,13 @@ __global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
       int lx, ly;
       bool valid;
       if (tile_size == 16) {
-        lx = (warp & 1) * 8 + (lane >> 2);
-        ly = (warp >> 1) * 8 + (lane & 3) + 4 * q;
+        if (kPipeWide) {
+          lx = (lane >> 2) + 8 * q;
+          ly = warp * 4 + (lane & 3);
+        } else {
+          lx = (warp & 1) * 8 + (lane >> 2);
+          ly = (warp >> 1) * 8 + (lane & 3) + 4 * q;
+        }
         valid = true;
       } else {
         const int sl = warp * 64 + q * 32 + lane;
@@ -752,7 +794,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
       const int prev = i - kPipeStages;
       if (prev >= 0 && prev < n_batches) {
         // Records of batch `prev`: the per-warp partials summed in warp order.
-        mbar_wait(&S.empty[st], (uint32_t)(prev / kPipeStages) & 1u);
+        mbar_wait_backoff(&S.empty[st], (uint32_t)(prev / kPipeStages) & 1u);
         const int hi = max_walked - prev * kPipeBatch;
         const int count = min(kPipeBatch, hi);
         for (int k = lane; k < count; k += 32) {
@@ -841,6 +883,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
         n_list += __popc(bal);
       }
       __syncwarp();
+      n_wentries += (uint32_t)n_list;
       // Back to front over this warp's entries, four at a time: the 4 x 9 per-lane sums
       // (two pixels each) are reduce-scattered over the warp; the totals land on lanes 0
       // (A), 8 (C), 16 (B) and 24 (D).
@@ -889,6 +932,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
 #pragma unroll
             for (int c = 0; c < kRec; ++c) K2[c] = 0.0f;
         }
+        n_wlive += (uint32_t)(ma != 0) + (uint32_t)(mb != 0) + (uint32_t)(mc != 0) + (uint32_t)(md != 0);
         if (ma | mb | mc | md) {
           float L[kRec];
 #pragma unroll
@@ -915,7 +959,7 @@ __global__ void __launch_bounds__(kPipeThreads, 4) k_bwd_raster_pipe(
       mbar_arrive(&S.empty[st]);
     }
   }
-  if (work && !producer) bwd_count_work(work, (uint32_t)(wk[0] + wk[1]), n_contrib);
+  if (work && !producer) bwd_count_work(work, (uint32_t)(wk[0] + wk[1]), n_contrib, n_wentries, n_wlive);
 }
 
 void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {

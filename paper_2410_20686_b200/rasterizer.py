@@ -283,10 +283,11 @@ class RenderOutput:
         return a.value, b.value
 
     def backward_work(self):
-        """(entries replayed, contributions) of the last backward on this frame."""
-        a, b = C.c_int64(0), C.c_int64(0)
-        self.ctx.check(self.ctx.lib.odgs_frame_backward_work(self.ctx.handle, self.handle, C.byref(a), C.byref(b)))
-        return a.value, b.value
+        """(entries replayed, contributions, warp-entries walked, warp-entries with a
+        contribution) of the last backward on this frame."""
+        out = (C.c_int64 * 4)()
+        self.ctx.check(self.ctx.lib.odgs_frame_backward_work(self.ctx.handle, self.handle, out, 4))
+        return tuple(int(v) for v in out)
 
     def set_image_peers(self, ptrs) -> None:
         """odgs_frame_set_image_peers: the blend also writes each rendered pixel into

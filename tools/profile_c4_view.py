@@ -26,5 +26,5 @@ for _ in range(iters):
     fr = render(ctx, cloud, cam, s)
     g = backward(ctx, cloud, cam, fr, dl, s)
 torch.cuda.synchronize()
-print("n_entries", fr.info().n_entries, "work", fr.work())
+print("n_entries", fr.info().n_entries, "work", fr.work(), "bwd_work", fr.backward_work())
 print({k: round(v[0] / max(v[1], 1), 4) for k, v in ctx.stage_times().items() if v[1]})
