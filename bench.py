@@ -246,6 +246,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream(dev)
     ctx = Context(local_rank, stream=stream.cuda_stream)
+    # Asynchronous renders: no host round trip inside or between frames (errors and
+    # entry-buffer overflows surface at frame.check()).
+    ctx.set_async(True)
     settings = RenderSettings()
     arrs = cloud_arrays()
     dcloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in arrs])
@@ -261,12 +264,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     for k in range(args.warmup):
         render(ctx, dcloud, camera(k, rank), settings, out=frame)
+    frame.check()
     torch.cuda.synchronize()
 
-    # Timed region: K renders, L2 flushed between steps (outside the step events).
+    # Timed region: K renders queued back to back on the stream (no host synchronisation),
+    # L2 flushed between steps (outside the step events).
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    work = []
     launches0 = ctx.launch_count
     barrier()
     torch.cuda.synchronize()
@@ -277,8 +281,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             starts[k].record(stream)
             render(ctx, dcloud, camera(k, rank), settings, out=frame)
             ends[k].record(stream)
-            work.append(frame.work())
         torch.cuda.synchronize()
+    if frame.check():  # an entry-buffer overflow would have re-rendered the last frame
+        raise RuntimeError("bench: a timed frame overflowed its entry buffers")
     barrier()
     launches = ctx.launch_count - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -294,6 +299,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     stages = ctx.stage_times()
     ctx.set_profiling(False)
+    # Work counters of the same frames (a separate pass: each read synchronises).
+    work = []
+    for k in range(args.steps):
+        render(ctx, dcloud, camera(k, rank), settings, out=frame)
+        work.append(frame.work())
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -520,10 +530,13 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
             bwd_work[j] += b[j]
         return out
     train_mod.backward = counting_backward
+    from paper_2410_20686_b200 import _capi as capi
+    ctx.lib.odgs_frame_set_flags(tr.frame.handle, capi.FRAME_COUNT_WORK)
     try:
         tr.step(read_loss=False)
     finally:
         train_mod.backward = real_backward
+        ctx.lib.odgs_frame_set_flags(tr.frame.handle, 0)
     torch.cuda.synchronize()
     stages = {k: v[0] for k, v in ctx.stage_times().items() if v[1] > 0}
     ctx.set_profiling(False)
@@ -677,6 +690,7 @@ def run_aux(args, ctx, dev, stream):
         backward(ctx, c2, cam, fr, dl, s, grads=g2)
 
     ms2 = timed(step2, 5)
+    fr.check()
     fr.destroy()
     return {"C1_render": {"workload": "100K Gaussians (default bounds), SH0, 1024x512", "ms": ms1,
                           "frames_per_s": 1000.0 / ms1},
@@ -750,6 +764,8 @@ def run_large(args, ctx, rank, world, local_rank, dev, stream):
     ev1.record(stream)
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    if fr.check():
+        raise RuntimeError("bench: a C5 frame overflowed its entry buffers")
     # stage times from a separate profiled pass (its event readbacks stay out of the timing)
     ctx.set_profiling(True)
     ctx.reset_stage_times()

@@ -143,6 +143,7 @@ typedef enum {
 #define ODGS_FRAME_KEEP_COV2D 0x1u   /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
 #define ODGS_FRAME_PLAIN_BLEND 0x2u  /* disable warp culling in the blend (A/B checks) */
 #define ODGS_FRAME_KEEP_SPLAT_GRADS 0x4u /* backward also stores SplatGrads (SPLATGRAD_* fields) */
+#define ODGS_FRAME_COUNT_WORK 0x8u  /* backward counts its work (odgs_frame_backward_work); costs time */
 
 /* odgs_backward flags */
 #define ODGS_ACCUMULATE 0x1u /* add into the gradient buffers (GradBuffers::accumulate) */
@@ -160,6 +161,22 @@ void odgs_ctx_destroy(odgs_ctx* ctx);
 odgs_status odgs_ctx_set_stream(odgs_ctx* ctx, void* stream);
 void* odgs_ctx_stream(odgs_ctx* ctx);
 odgs_status odgs_synchronize(odgs_ctx* ctx);
+/* Asynchronous mode (enable != 0): odgs_render / odgs_render_band / odgs_prepare_render
+   and odgs_backward with device gradient buffers return without synchronising the stream
+   — no host round trip inside or between them, so frames and training views queue back
+   to back (after a frame's first render, which sizes its buffers). Their errors (the
+   reference's exceptions) are reported at the frame's check point: odgs_frame_check, or
+   any call that reads the frame on the host (downloads, odgs_frame_get_info,
+   odgs_frame_work). Inputs must stay valid until then. Default: synchronous, errors
+   returned by the call itself as the reference throws. */
+odgs_status odgs_ctx_set_async(odgs_ctx* ctx, int enable);
+/* The frame's check point: synchronises, and reports a deferred error of the operations
+   enqueued on the frame since the last check. If a render produced more tile entries
+   than the frame's entry buffers held (they are sized 1.25x the entries of the frame's
+   first render and grow on demand), the frame's last render is re-run synchronously with
+   room for them, so the frame holds the correct result; *rerendered (optional) is then
+   1, and a backward enqueued on the overflowed render must be repeated. */
+odgs_status odgs_frame_check(odgs_ctx* ctx, odgs_frame* frame, int32_t* rerendered);
 /* Code of the last failed call on ctx; *gaussian_index = offending row or -1. */
 odgs_status odgs_last_error(const odgs_ctx* ctx, int64_t* gaussian_index, char* message, size_t message_len);
 /* Number of kernels this context has launched since creation. */
@@ -203,7 +220,7 @@ odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, voi
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_examined,
                             int64_t* entries_composited);
 /* Backward work of the last odgs_backward / odgs_grad_pixels_to_splats on `frame` (for
-   rooflines), up to n_counters (<= 4) values: [0] entries replayed (sum over pixels with
+   rooflines; zeros unless the frame has ODGS_FRAME_COUNT_WORK), up to n_counters (<= 4) values: [0] entries replayed (sum over pixels with
    a non-zero image gradient of their walk length — the reference's replay loop,
    backward.hpp:251-269), [1] contributions (replayed entries inside the cutoff,
    :271-305), [2] warp-entries walked by the culled kernel (sum of its warps' list

@@ -19,6 +19,7 @@ ACCUMULATE = 0x1
 FRAME_KEEP_COV2D = 0x1
 FRAME_PLAIN_BLEND = 0x2
 FRAME_KEEP_SPLAT_GRADS = 0x4
+FRAME_COUNT_WORK = 0x8
 
 (FRAME_IMAGE, FRAME_TRANSMITTANCE, FRAME_WALKED, FRAME_TILE_OFFSETS, FRAME_TILE_ENTRIES,
  FRAME_INSTANCE_SPLAT, FRAME_INSTANCE_SHIFT, FRAME_SPLAT_INDEX, FRAME_SPLAT_MEAN, FRAME_SPLAT_COV2D,
@@ -117,6 +118,8 @@ SIGNATURES = {
     "odgs_synchronize": (C.c_int, [_P]),
     "odgs_last_error": (C.c_int, [_P, C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
     "odgs_ctx_launch_count": (C.c_int64, [_P]),
+    "odgs_ctx_set_async": (C.c_int, [_P, C.c_int]),
+    "odgs_frame_check": (C.c_int, [_P, _P, C.POINTER(C.c_int32)]),
     "odgs_frame_create": (C.c_int, [_P, C.POINTER(_P)]),
     "odgs_frame_destroy": (None, [_P]),
     "odgs_frame_set_flags": (C.c_int, [_P, C.c_uint32]),

@@ -51,6 +51,7 @@ struct odgs_ctx {
   DevBuf cloud_buf, dl_buf, grads_buf, signs_buf, cull_buf, loss_buf;
   float* d_unit_signs = nullptr;
   int64_t launches = 0;
+  bool async_mode = false;  // odgs_ctx_set_async: renders / backward passes return without synchronising
   // densify_and_prune plan (odgs_densify_plan -> odgs_densify_apply)
   DevBuf densify_buf, unit_ball_buf, misc_buf;
   struct {
@@ -72,9 +73,30 @@ struct odgs_frame {
   int32_t row_begin = 0, row_end = 0;
   bool prepared = false, rendered = false, have_splat_grads = false;
   bool from_splats = false;  // odgs_rasterize_splats: no cloud or camera behind the splats
+  bool band = false;         // a row-band render (compacted depth sort)
   DevBuf sp_ab, sp_c, cov, keys[2], vals[2], cnt, cnt_sorted, off_sorted, ent_off_idx, sort_tmp, scan_tmp;
   DevBuf ekeys[2], evals[2], offsets, tile_order, image, trans, walked, records, touched, folded, splat_grads, work;
-  DevBuf bwd_work;  // [2] backward work counters of the last backward
+  DevBuf bwd_work;  // [4] backward work counters of the last backward
+  // Per-frame device error words and their pinned host copy: several frames can be in
+  // flight on one context (asynchronous renders), each checked at its own sync point.
+  DevErrors* d_err = nullptr;
+  DevErrors* h_err = nullptr;
+  // Capacity of the tile-entry buffers (entries). 0: unknown — the next render learns the
+  // entry count with a host synchronisation after the offsets scan (the "exact" path);
+  // afterwards renders run without any synchronisation, with the entry count kept on the
+  // device, and an overflow (more entries than the capacity) is detected at the frame's
+  // check point and re-rendered with room for them.
+  uint32_t k_cap = 0;
+  bool pending = false;      // enqueued work whose error words / counts are not read yet
+  bool bwd_pending = false;  // a backward whose error words are not read yet
+  // The last render request, for the re-run after an overflow (pointers are the caller's).
+  struct Request {
+    int kind = 0;  // 0 none, 1 render, 2 prepare, 3 band
+    odgs_cloud cloud{};
+    odgs_camera camera{};
+    odgs_settings settings{};
+    int32_t row_begin = 0, row_end = 0;
+  } req;
   int depth_which = 0, tile_which = 0;
   int64_t n_sorted = 0;  // depth-sorted ranks: n, or the band's Gaussians (band compaction)
   PeerImages peers{};    // odgs_frame_set_image_peers
@@ -293,6 +315,61 @@ odgs_status reset_errors(odgs_ctx* ctx) {
   return ODGS_OK;
 }
 
+// A render starts: its counters are reset; the sticky words too, unless earlier
+// asynchronous work on the frame is still unchecked (its errors must survive to the check).
+odgs_status reset_frame_errors(odgs_ctx* ctx, odgs_frame* f) {
+  if (f->pending || f->bwd_pending) {
+    char* d = reinterpret_cast<char*>(f->d_err) + kDevErrorsSticky;
+    ODGS_CUDA(ctx, cudaMemcpyAsync(d, reinterpret_cast<const char*>(ctx->h_err_init) + kDevErrorsSticky,
+                                   sizeof(DevErrors) - kDevErrorsSticky, cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    ODGS_CUDA(ctx, cudaMemcpyAsync(f->d_err, ctx->h_err_init, sizeof(DevErrors), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  return ODGS_OK;
+}
+
+// Reads the frame's device error words (synchronizing the stream).
+odgs_status read_frame_errors(odgs_ctx* ctx, odgs_frame* f) {
+  ODGS_CUDA(ctx, cudaMemcpyAsync(f->h_err, f->d_err, sizeof(DevErrors), cudaMemcpyDeviceToHost, ctx->stream));
+  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return ODGS_OK;
+}
+
+// The reference's exceptions for projection-stage error words (rasterizer.hpp:133-136,
+// covariance.hpp:14-15, 31-32, projection.hpp:23-24).
+odgs_status projection_error(odgs_ctx* ctx, const DevErrors& he) {
+  if (he.nonfinite != kNoError) {
+    const int64_t idx = (int64_t)(he.nonfinite >> 4);
+    return set_error(ctx, ODGS_ERR_RUNTIME, idx, "render: non-finite parameter in Gaussian " + std::to_string(idx));
+  }
+  if (he.project != kNoError) {
+    const int64_t idx = (int64_t)(he.project >> 4);
+    const int code = (int)(he.project & 15);
+    if (code == 3) return set_error(ctx, ODGS_ERR_DOMAIN, idx, "to_spherical: degenerate zero-length direction");
+    if (code == 2) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "build_covariance: non-finite parameters");
+    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "normalize_quaternion: near-zero quaternion");
+  }
+  return ODGS_OK;
+}
+
+odgs_status backward_error(odgs_ctx* ctx, const DevErrors& he) {
+  if (he.bwd_domain != kNoError) {
+    const int64_t idx = (int64_t)(he.bwd_domain >> 4);
+    return set_error(ctx, ODGS_ERR_DOMAIN, idx, "grad_position: undefined at the pole axis");
+  }
+  if (he.bwd_nonfinite != kNoError) {
+    const int64_t idx = (int64_t)(he.bwd_nonfinite >> 4);
+    return set_error(ctx, ODGS_ERR_RUNTIME, idx, "backward: non-finite gradient for Gaussian " + std::to_string(idx));
+  }
+  return ODGS_OK;
+}
+
+// Entry capacity the frame's tile-entry buffers hold.
+uint32_t entry_capacity(const odgs_frame* f) {
+  const size_t c = std::min({f->ekeys[0].cap, f->ekeys[1].cap, f->evals[0].cap, f->evals[1].cap}) / sizeof(uint32_t);
+  return (uint32_t)std::min<size_t>(c, (size_t)kMaxSortItems - 1);
+}
+
 odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band);
 
 // Per-frame buffers of the projection stage (n Gaussians, n_tiles tiles).
@@ -347,9 +424,11 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   const uint32_t n_tiles = (uint32_t)(f->tiles_x * f->tiles_y);
 
   if ((st = ensure_frame_buffers(ctx, f, n, n_tiles)) != ODGS_OK) return st;
-  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+  if ((st = reset_frame_errors(ctx, f)) != ODGS_OK) return st;
+  f->pending = true;
 
   const bool band = f->settings.band_ty0 > 0 || f->settings.band_ty1 < f->tiles_y;
+  f->band = band;
   PreprocessArgs pa;
   pa.n = n;
   pa.means = cp.means;
@@ -367,7 +446,7 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
   pa.keys = f->keys[0].as<uint32_t>();
   pa.vals = f->vals[0].as<uint32_t>();
   pa.cnt = f->cnt.as<uint32_t>();
-  pa.err = ctx->d_err;
+  pa.err = f->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_PREPROCESS);
     if (band) {
@@ -378,7 +457,7 @@ odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_came
       uint32_t* seg_off = f->off_sorted.as<uint32_t>();
       launch_band_preprocess(pa, f->keys[1].as<uint32_t>(), f->vals[1].as<uint32_t>(), seg_count, s);
       const int64_t n_seg = band_segments(n);
-      exclusive_scan_u32(seg_count, seg_off, n_seg, f->scan_tmp.p, &ctx->d_err->n_band, s);
+      exclusive_scan_u32(seg_count, seg_off, n_seg, f->scan_tmp.p, &f->d_err->n_band, s);
       launch_concat_segments(n, seg_count, seg_off, f->keys[1].as<uint32_t>(), f->vals[1].as<uint32_t>(),
                              f->keys[0].as<uint32_t>(), f->vals[0].as<uint32_t>(), s);
     } else {
@@ -397,6 +476,10 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
   cudaStream_t s = ctx->stream;
   const int64_t n = f->n;
   const uint32_t n_tiles = (uint32_t)(f->tiles_x * f->tiles_y);
+  // Exact path (entry capacity unknown): read the entry count (and a band's Gaussian
+  // count) on the host. Capacity path: every count stays on the device and the launches
+  // are sized for the capacities; no synchronisation.
+  const bool exact = f->k_cap == 0 || n == 0;
   // Depth sort of the Gaussians (key: depth bits; culled sort last). A band render
   // sorts only the Gaussians with entries in its rows, compacted in index order above
   // (stable, so ties keep index order): the tile lists are unchanged, the sort shrinks
@@ -405,19 +488,22 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
   uint32_t* dk[2] = {f->keys[0].as<uint32_t>(), f->keys[1].as<uint32_t>()};
   uint32_t* dv[2] = {f->vals[0].as<uint32_t>(), f->vals[1].as<uint32_t>()};
   int64_t m = n;
+  // the band's Gaussian count on the device (low word of the 64-bit counter)
+  const uint32_t* m_dev = band ? reinterpret_cast<const uint32_t*>(&f->d_err->n_band) : nullptr;
   StageScope* depth_scope = new StageScope(ctx, ODGS_STAGE_DEPTH_SORT);
-  if (band && n > 0) {
-    if ((st = read_errors(ctx)) != ODGS_OK) {
+  if (band && n > 0 && exact) {
+    if ((st = read_frame_errors(ctx, f)) != ODGS_OK) {
       delete depth_scope;
       return st;
     }
-    m = (int64_t)ctx->h_err->n_band;
+    m = (int64_t)f->h_err->n_band;
+    m_dev = nullptr;
   }
   {
     int which = 0;
     // The last pass also gathers each rank's tile count (cnt_sorted).
     const cudaError_t e = radix_sort_pairs(dk, dv, m, 0, 32, f->sort_tmp.p, &which, s, f->cnt.as<uint32_t>(),
-                                           f->cnt_sorted.as<uint32_t>());
+                                           f->cnt_sorted.as<uint32_t>(), m_dev);
     if (e != cudaSuccess) {
       delete depth_scope;
       return cuda_fail(ctx, e, "depth sort");
@@ -425,41 +511,38 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
     f->depth_which = which;  // index into f->vals / f->keys
   }
   delete depth_scope;
-  f->n_sorted = m;
+  f->n_sorted = m;  // the sorted ranks: m, or at most m (band, capacity path: m_dev on the device)
   const uint32_t* sorted_idx = f->vals[f->depth_which].as<uint32_t>();
   {
     StageScope sc(ctx, ODGS_STAGE_SCAN);
     exclusive_scan_u32(f->cnt_sorted.as<uint32_t>(), f->off_sorted.as<uint32_t>(), m, f->scan_tmp.p,
-                       &ctx->d_err->n_entries, s);
+                       &f->d_err->n_entries, s, m_dev);
   }
-  if ((st = read_errors(ctx)) != ODGS_OK) return st;
-  const DevErrors& he = *ctx->h_err;
-  if (he.nonfinite != kNoError) {
-    const int64_t idx = (int64_t)(he.nonfinite >> 4);
-    return set_error(ctx, ODGS_ERR_RUNTIME, idx, "render: non-finite parameter in Gaussian " + std::to_string(idx));
+  uint32_t K = 0;
+  if (exact) {
+    if ((st = read_frame_errors(ctx, f)) != ODGS_OK) return st;
+    const DevErrors& he = *f->h_err;
+    if ((st = projection_error(ctx, he)) != ODGS_OK) return st;
+    const unsigned long long total = n > 0 ? he.n_entries : 0ull;
+    // The onesweep look-back words carry 30-bit digit counts (sort.cu), so a sort holds
+    // fewer than 2^30 items.
+    if (total >= kMaxSortItems)
+      return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: 2^30 or more tile entries");
+    f->n_entries = (uint32_t)total;
+    f->n_splats = n > 0 ? (int64_t)he.n_visible : 0;
+    f->n_instances = n > 0 ? (int64_t)he.n_instances : 0;
+    K = f->n_entries;
+    for (int k = 0; k < 2; ++k) {
+      ODGS_CUDA(ctx, ensure(f->ekeys[k], sizeof(uint32_t) * K, s));
+      ODGS_CUDA(ctx, ensure(f->evals[k], sizeof(uint32_t) * K, s));
+    }
+  } else {
+    K = f->k_cap;
   }
-  if (he.project != kNoError) {
-    const int64_t idx = (int64_t)(he.project >> 4);
-    const int code = (int)(he.project & 15);
-    if (code == 3)
-      return set_error(ctx, ODGS_ERR_DOMAIN, idx, "to_spherical: degenerate zero-length direction");
-    if (code == 2) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "build_covariance: non-finite parameters");
-    return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, idx, "normalize_quaternion: near-zero quaternion");
-  }
-  const unsigned long long total = n > 0 ? he.n_entries : 0ull;
-  // The onesweep look-back words carry 30-bit digit counts (sort.cu), so a sort holds
-  // fewer than 2^30 items.
-  if (total >= kMaxSortItems)
-    return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: 2^30 or more tile entries");
-  f->n_entries = (uint32_t)total;
-  f->n_splats = n > 0 ? (int64_t)he.n_visible : 0;
-  f->n_instances = n > 0 ? (int64_t)he.n_instances : 0;
-  const uint32_t K = f->n_entries;
+  const uint32_t cap = entry_capacity(f);
+  // The capacity path sorts / bins min(entries, capacity) entries, counted on the device.
+  const uint32_t* k_dev = exact ? nullptr : reinterpret_cast<const uint32_t*>(&f->d_err->k_sort);
 
-  for (int k = 0; k < 2; ++k) {
-    ODGS_CUDA(ctx, ensure(f->ekeys[k], sizeof(uint32_t) * K, s));
-    ODGS_CUDA(ctx, ensure(f->evals[k], sizeof(uint32_t) * K, s));
-  }
   EmitArgs ea;
   ea.n = m;
   ea.sorted_idx = sorted_idx;
@@ -476,6 +559,11 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
   ea.out_keys = f->ekeys[0].as<uint32_t>();
   ea.out_vals = f->evals[0].as<uint32_t>();
   ea.ent_off_idx = f->ent_off_idx.as<uint32_t>();
+  ea.n_dev = m_dev;
+  ea.total = &f->d_err->n_entries;
+  ea.capacity = exact ? K : cap;
+  ea.k_sort = exact ? nullptr : &f->d_err->k_sort;
+  ea.overflow = &f->d_err->overflow;
   {
     StageScope sc(ctx, ODGS_STAGE_EMIT);
     launch_emit(ea, s);
@@ -486,18 +574,22 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
   uint32_t* ev[2] = {f->evals[0].as<uint32_t>(), f->evals[1].as<uint32_t>()};
   {
     StageScope sc(ctx, ODGS_STAGE_TILE_SORT);
-    ODGS_CUDA(ctx, radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s));
+    ODGS_CUDA(ctx, radix_sort_pairs(ek, ev, K, 0, bits_for(n_tiles), f->sort_tmp.p, &f->tile_which, s, nullptr,
+                                    nullptr, k_dev));
   }
   {
     StageScope sc(ctx, ODGS_STAGE_RANGES);
     launch_tile_ranges(K, ek[f->tile_which], n_tiles, (uint32_t)(f->settings.band_ty0 * f->tiles_x),
-                       (uint32_t)(f->settings.band_ty1 * f->tiles_x), f->offsets.as<int32_t>(), s);
+                       (uint32_t)(f->settings.band_ty1 * f->tiles_x), f->offsets.as<int32_t>(), s, k_dev);
     const int band_tiles = f->tiles_x * (f->settings.band_ty1 - f->settings.band_ty0);
     ODGS_CUDA(ctx, ensure(f->tile_order, sizeof(uint32_t) * std::max(band_tiles, 1), s));
     launch_tile_order(f->offsets.as<int32_t>(), f->settings.band_ty0 * f->tiles_x, band_tiles,
                       f->tile_order.as<uint32_t>(), s);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
+  // Later renders of this frame run on the capacity path.
+  f->k_cap = n > 0 ? std::max<uint32_t>(cap, 1u) : f->k_cap;
+  f->pending = !exact;
   f->prepared = true;
   return ok(ctx);
 }
@@ -592,7 +684,8 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
   cudaStream_t s = ctx->stream;
   const int64_t n = f->n;
   const int64_t px = (int64_t)f->width * f->height;
-  const uint32_t K = f->n_entries;
+  // Entry buffers: the capacity covers every emit position of a capacity-path frame.
+  const uint32_t K = std::max(f->n_entries, f->k_cap);
   const float* dl = dl_dimage;
   if (dl_memory != ODGS_MEM_DEVICE) {
     ODGS_CUDA(ctx, ensure(ctx->dl_buf, sizeof(float) * 3 * px, s));
@@ -629,16 +722,78 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
     ra.touched = f->touched.as<uint8_t>();
     ra.order = f->tile_order.as<uint32_t>();
     ra.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
-    ra.work = f->bwd_work.as<unsigned long long>();
+    ra.work = (f->flags & ODGS_FRAME_COUNT_WORK) ? f->bwd_work.as<unsigned long long>() : nullptr;
     launch_bwd_raster(ra, s);
   }
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
+    // A band's sorted ranks are counted on the device (capacity path: n_sorted = n).
+    const uint32_t* m_dev = f->band ? reinterpret_cast<const uint32_t*>(&f->d_err->n_band) : nullptr;
     launch_fold_records(f->n_sorted, f->vals[f->depth_which].as<uint32_t>(), f->cnt_sorted.as<uint32_t>(),
                         f->off_sorted.as<uint32_t>(), f->touched.as<uint8_t>(), f->records.as<float>(),
-                        f->folded.as<float>(), s);
+                        f->folded.as<float>(), s, m_dev);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
+  return ODGS_OK;
+}
+
+odgs_status prepare_impl(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
+                         const odgs_settings* settings, odgs_frame* f, int32_t row_begin, int32_t row_end);
+odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f);
+
+// Runs the frame's recorded render request (render, prepare_render or a band).
+odgs_status run_request(odgs_ctx* ctx, odgs_frame* f) {
+  const odgs_frame::Request r = f->req;
+  odgs_status st;
+  if (r.kind == 3) st = prepare_impl(ctx, &r.cloud, &r.camera, &r.settings, f, r.row_begin, r.row_end);
+  else st = prepare_impl(ctx, &r.cloud, &r.camera, &r.settings, f, 0, -1);
+  if (st != ODGS_OK) return st;
+  if (r.kind != 2) st = blend_impl(ctx, f);
+  return st;
+}
+
+// The frame's check point: synchronises, reads the frame's error words and counts, and
+// reports deferred errors as the synchronous call would have. An overflow of the entry
+// buffers re-runs the frame's last render request with room for every entry (the exact
+// path), so the frame holds the correct result; *rerun (optional) tells the caller that
+// work enqueued on the overflowed frame since (a backward) must be repeated.
+odgs_status finish_frame(odgs_ctx* ctx, odgs_frame* f, int32_t* rerun = nullptr) {
+  if (rerun) *rerun = 0;
+  if (!f->pending && !f->bwd_pending) return ODGS_OK;
+  odgs_status st;
+  if ((st = read_frame_errors(ctx, f)) != ODGS_OK) return st;
+  const DevErrors he = *f->h_err;
+  const bool fwd = f->pending, bwd = f->bwd_pending;
+  f->pending = f->bwd_pending = false;
+  // the host has the sticky words now: clear them for the next operations
+  ODGS_CUDA(ctx, cudaMemcpyAsync(f->d_err, ctx->h_err_init, kDevErrorsSticky, cudaMemcpyHostToDevice, ctx->stream));
+  if ((st = projection_error(ctx, he)) != ODGS_OK) return st;
+  if (fwd) {
+    const unsigned long long total = f->n > 0 ? he.n_entries : 0ull;
+    if (total >= kMaxSortItems)
+      return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: 2^30 or more tile entries");
+    f->n_entries = (uint32_t)total;
+    f->n_splats = f->n > 0 ? (int64_t)he.n_visible : 0;
+    f->n_instances = f->n > 0 ? (int64_t)he.n_instances : 0;
+    if (f->band) f->n_sorted = (int64_t)he.n_band;  // the capacity path sorted the band's Gaussians
+  }
+  if (he.overflow) {
+    if (he.overflow >= kMaxSortItems)
+      return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "prepare_render: 2^30 or more tile entries");
+    if (f->req.kind == 0) return set_error(ctx, ODGS_ERR_RUNTIME, -1, "tile-entry overflow without a request");
+    // Room for the largest entry count seen since the last check (the overflow word
+    // keeps the maximum), then the exact path re-runs the last request.
+    const size_t want = (size_t)he.overflow;
+    for (int k = 0; k < 2; ++k) {
+      ODGS_CUDA(ctx, ensure(f->ekeys[k], sizeof(uint32_t) * want, ctx->stream));
+      ODGS_CUDA(ctx, ensure(f->evals[k], sizeof(uint32_t) * want, ctx->stream));
+    }
+    f->k_cap = 0;  // the exact path: the entry count read on the host, buffers grown to fit
+    if ((st = run_request(ctx, f)) != ODGS_OK) return st;
+    if (rerun) *rerun = 1;
+    return finish_frame(ctx, f);
+  }
+  if (bwd && (st = backward_error(ctx, he)) != ODGS_OK) return st;
   return ODGS_OK;
 }
 
@@ -699,6 +854,8 @@ odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out) {
   ctx->h_err_init->n_instances = 0;
   ctx->h_err_init->n_band = 0;
   ctx->h_err_init->n_precull = 0;
+  ctx->h_err_init->k_sort = 0;
+  ctx->h_err_init->overflow = 0;
   *out = ctx;
   return ODGS_OK;
 }
@@ -760,6 +917,17 @@ odgs_status odgs_frame_create(odgs_ctx* ctx, odgs_frame** out) {
   odgs_frame* f = new (std::nothrow) odgs_frame();
   if (!f) return set_error(ctx, ODGS_ERR_OUT_OF_MEMORY, -1, "frame allocation");
   f->ctx = ctx;
+  cudaSetDevice(ctx->device);
+  cudaError_t e = cudaMalloc(&f->d_err, sizeof(DevErrors));
+  if (e == cudaSuccess) e = cudaMallocHost(&f->h_err, sizeof(DevErrors));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(f->d_err, ctx->h_err_init, sizeof(DevErrors), cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) {
+    if (f->d_err) cudaFree(f->d_err);
+    if (f->h_err) cudaFreeHost(f->h_err);
+    delete f;
+    return cuda_fail(ctx, e, "frame error words");
+  }
   *out = f;
   return ok(ctx);
 }
@@ -773,6 +941,8 @@ void odgs_frame_destroy(odgs_frame* f) {
                     &f->records, &f->touched, &f->folded, &f->splat_grads, &f->work, &f->bwd_work};
   for (DevBuf* b : bufs) release(*b, s);
   cudaStreamSynchronize(s);
+  if (f->d_err) cudaFree(f->d_err);
+  if (f->h_err) cudaFreeHost(f->h_err);
   delete f;
 }
 
@@ -845,8 +1015,14 @@ odgs_status odgs_frame_set_flags(odgs_frame* f, uint32_t flags) {
   return ODGS_OK;
 }
 
-odgs_status odgs_frame_get_info(const odgs_frame* f, odgs_frame_info* info) {
-  if (!f || !info) return ODGS_ERR_INVALID_ARGUMENT;
+odgs_status odgs_frame_get_info(const odgs_frame* cf, odgs_frame_info* info) {
+  if (!cf || !info) return ODGS_ERR_INVALID_ARGUMENT;
+  odgs_frame* f = const_cast<odgs_frame*>(cf);  // the counts of an asynchronous render are read here
+  if (f->pending || f->bwd_pending) {
+    cudaSetDevice(f->ctx->device);
+    const odgs_status st = finish_frame(f->ctx, f);
+    if (st != ODGS_OK) return st;
+  }
   info->width = f->width;
   info->height = f->height;
   info->tiles_x = f->tiles_x;
@@ -860,24 +1036,56 @@ odgs_status odgs_frame_get_info(const odgs_frame* f, odgs_frame_info* info) {
   return ODGS_OK;
 }
 
+// A render-type entry point: records the request (for an overflow re-run), runs it and,
+// unless the context is asynchronous, checks the frame right away (the reference's
+// synchronous exceptions).
+static odgs_status render_entry(odgs_ctx* ctx, odgs_frame* frame, int kind) {
+  frame->req.kind = kind;
+  odgs_status st = run_request(ctx, frame);
+  if (st == ODGS_OK && !ctx->async_mode) st = finish_frame(ctx, frame);
+  if (ctx->timers.enabled) resolve_timers(ctx);
+  return st == ODGS_OK ? ok(ctx) : st;
+}
+
 odgs_status odgs_prepare_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
                                 const odgs_settings* settings, odgs_frame* frame) {
   LaunchScope scope(ctx);
-  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  if (!ctx || !frame) return ODGS_ERR_INVALID_ARGUMENT;
+  if (!cloud || !camera || !settings) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "null argument");
   cudaSetDevice(ctx->device);
-  return prepare_impl(ctx, cloud, camera, settings, frame);
+  frame->req.cloud = *cloud;
+  frame->req.camera = *camera;
+  frame->req.settings = *settings;
+  frame->req.row_begin = 0;
+  frame->req.row_end = -1;
+  return render_entry(ctx, frame, 2);
 }
 
 odgs_status odgs_render(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
                         const odgs_settings* settings, odgs_frame* frame) {
   LaunchScope scope(ctx);
-  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  if (!ctx || !frame) return ODGS_ERR_INVALID_ARGUMENT;
+  if (!cloud || !camera || !settings) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "null argument");
   cudaSetDevice(ctx->device);
-  odgs_status st = prepare_impl(ctx, cloud, camera, settings, frame);
-  if (st != ODGS_OK) return st;
-  st = blend_impl(ctx, frame);
-  if (ctx->timers.enabled) resolve_timers(ctx);
-  return st;
+  frame->req.cloud = *cloud;
+  frame->req.camera = *camera;
+  frame->req.settings = *settings;
+  frame->req.row_begin = 0;
+  frame->req.row_end = -1;
+  return render_entry(ctx, frame, 1);
+}
+
+odgs_status odgs_ctx_set_async(odgs_ctx* ctx, int enable) {
+  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  ctx->async_mode = enable != 0;
+  return ok(ctx);
+}
+
+odgs_status odgs_frame_check(odgs_ctx* ctx, odgs_frame* frame, int32_t* rerendered) {
+  if (!ctx || !frame) return ODGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  const odgs_status st = finish_frame(ctx, frame, rerendered);
+  return st == ODGS_OK ? ok(ctx) : st;
 }
 
 odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* f, int64_t* counters, int32_t n_counters) {
@@ -941,13 +1149,18 @@ odgs_status odgs_rasterize_splats(odgs_ctx* ctx, int64_t n_gaussians, int64_t n_
   f->settings.band_ty0 = 0;
   f->settings.band_ty1 = f->tiles_y;
   if ((st = ensure_frame_buffers(ctx, f, n_gaussians, (uint32_t)(f->tiles_x * f->tiles_y))) != ODGS_OK) return st;
-  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+  if ((st = finish_frame(ctx, f)) != ODGS_OK) return st;  // earlier asynchronous work on this frame
+  if ((st = reset_frame_errors(ctx, f)) != ODGS_OK) return st;
+  f->req.kind = 0;  // no re-run: the exact path below cannot overflow
+  f->k_cap = 0;
+  f->band = false;
+  f->pending = true;
   ODGS_CUDA(ctx, ensure(ctx->misc_buf, rec.size() * sizeof(float), s));
   if (!rec.empty())
     ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->misc_buf.p, rec.data(), rec.size() * sizeof(float), cudaMemcpyHostToDevice, s));
   launch_load_splats(n_gaussians, n_splats, ctx->misc_buf.as<float>(), width, height, f->tile_size, f->sp_ab.as<float4>(),
                      f->sp_c.as<float4>(), f->keys[0].as<uint32_t>(), f->vals[0].as<uint32_t>(),
-                     f->cnt.as<uint32_t>(), ctx->d_err, s);
+                     f->cnt.as<uint32_t>(), f->d_err, s);
   if ((st = bin_impl(ctx, f, false)) != ODGS_OK) return st;
   ODGS_CUDA(ctx, cudaStreamSynchronize(s));  // the packed records live in host memory until here
   st = blend_impl(ctx, f);
@@ -957,6 +1170,8 @@ odgs_status odgs_rasterize_splats(odgs_ctx* ctx, int64_t n_gaussians, int64_t n_
 
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_examined, int64_t* entries_composited) {
   if (!ctx || !f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not rendered");
+  odgs_status st;
+  if ((st = finish_frame(ctx, f)) != ODGS_OK) return st;
   unsigned long long w[2];
   ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
   ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -968,13 +1183,15 @@ odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_exami
 odgs_status odgs_render_band(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_camera* camera,
                              const odgs_settings* settings, int32_t row_begin, int32_t row_end, odgs_frame* frame) {
   LaunchScope scope(ctx);
-  if (!ctx) return ODGS_ERR_INVALID_ARGUMENT;
+  if (!ctx || !frame) return ODGS_ERR_INVALID_ARGUMENT;
+  if (!cloud || !camera || !settings) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "null argument");
   cudaSetDevice(ctx->device);
-  odgs_status st = prepare_impl(ctx, cloud, camera, settings, frame, row_begin, row_end);
-  if (st != ODGS_OK) return st;
-  st = blend_impl(ctx, frame);
-  if (ctx->timers.enabled) resolve_timers(ctx);
-  return st;
+  frame->req.cloud = *cloud;
+  frame->req.camera = *camera;
+  frame->req.settings = *settings;
+  frame->req.row_begin = row_begin;
+  frame->req.row_end = row_end;
+  return render_entry(ctx, frame, 3);
 }
 
 odgs_status odgs_frame_device_ptr(odgs_frame* f, int field, void** device_ptr) {
@@ -992,6 +1209,10 @@ odgs_status odgs_frame_device_ptr(odgs_frame* f, int field, void** device_ptr) {
 odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* f, int field, void* host_dst, size_t bytes) {
   if (!ctx || !f || !f->prepared) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not prepared");
   cudaSetDevice(ctx->device);
+  {
+    const odgs_status fs = finish_frame(ctx, f);  // an asynchronous render's errors and counts
+    if (fs != ODGS_OK) return fs;
+  }
   cudaStream_t s = ctx->stream;
   const int64_t px = (int64_t)f->width * f->height;
   const int64_t n_tiles = (int64_t)f->tiles_x * f->tiles_y;
@@ -1166,7 +1387,11 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   }
   const bool keep_sg = (f->flags & ODGS_FRAME_KEEP_SPLAT_GRADS) != 0;
   if (keep_sg) ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));
-  if ((st = reset_errors(ctx)) != ODGS_OK) return st;
+  // The backward's error words live in the frame's sticky section: cleared here unless
+  // an earlier operation on the frame is still unchecked (then they accumulate until the
+  // check point).
+  if (!f->pending && !f->bwd_pending)
+    ODGS_CUDA(ctx, cudaMemcpyAsync(f->d_err, ctx->h_err_init, kDevErrorsSticky, cudaMemcpyHostToDevice, s));
   if ((st = raster_fold(ctx, f, dl_dimage, dl_memory, settings)) != ODGS_OK) return st;
 
   BwdSplatArgs sa;
@@ -1200,7 +1425,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.g_one_minus_cos = gomc;
   sa.g_observed = gobs;
   sa.splat_grads = keep_sg ? f->splat_grads.as<float>() : nullptr;
-  sa.err = ctx->d_err;
+  sa.err = f->d_err;
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
     launch_bwd_splat(sa, s);
@@ -1218,17 +1443,12 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
       if (dsth[k]) ODGS_CUDA(ctx, cudaMemcpyAsync(dsth[k], srcd[k], 4 * width[k] * n, cudaMemcpyDeviceToHost, s));
     if (nb > 0) ODGS_CUDA(ctx, cudaMemcpyAsync(grads->sh_rest, gsh, 4 * 3 * nb * n, cudaMemcpyDeviceToHost, s));
   }
-  if ((st = read_errors(ctx)) != ODGS_OK) return st;
+  f->bwd_pending = true;
   if (ctx->timers.enabled) resolve_timers(ctx);
-  const DevErrors& he = *ctx->h_err;
-  if (he.bwd_domain != kNoError) {
-    const int64_t idx = (int64_t)(he.bwd_domain >> 4);
-    return set_error(ctx, ODGS_ERR_DOMAIN, idx, "grad_position: undefined at the pole axis");
-  }
-  if (he.bwd_nonfinite != kNoError) {
-    const int64_t idx = (int64_t)(he.bwd_nonfinite >> 4);
-    return set_error(ctx, ODGS_ERR_RUNTIME, idx, "backward: non-finite gradient for Gaussian " + std::to_string(idx));
-  }
+  // Asynchronous contexts report the errors at the frame's check point; host gradient
+  // buffers are only complete after a synchronisation, so they always check here.
+  if (ctx->async_mode && !host_out) return ok(ctx);
+  if ((st = finish_frame(ctx, f)) != ODGS_OK) return st;
   return ok(ctx);
 }
 
@@ -1242,6 +1462,7 @@ odgs_status odgs_grad_pixels_to_splats(odgs_ctx* ctx, odgs_frame* f, const float
   if (!dl_dimage) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "grad_pixels_to_splats: null image gradient");
   odgs_status st;
   if ((st = check_settings(ctx, settings)) != ODGS_OK) return st;
+  if ((st = finish_frame(ctx, f)) != ODGS_OK) return st;
   cudaStream_t s = ctx->stream;
   const int64_t n = f->n;
   ODGS_CUDA(ctx, ensure(f->splat_grads, sizeof(float) * 10 * n, s));

@@ -43,17 +43,26 @@ constexpr uint32_t kCulledKey = 0xFFFFFFFFu;
 
 // Per-call device error words. Each holds min over offenders of (index << 4 | code)
 // so the lowest Gaussian index wins, as in the reference's serial loops.
+//
+// Two sections. The sticky words (errors, overflow) keep their first value across
+// asynchronous operations until the host reads them at a check point; the counters are
+// per render and reset by every render.
 struct DevErrors {
+  // -- sticky: reset only after the host has read them
   unsigned long long nonfinite;    // first_non_finite (rasterizer.hpp:134-136)
   unsigned long long project;      // project_gaussian throws (code 1 invalid_argument, 3 domain)
   unsigned long long bwd_domain;   // grad_position*/jacobian_omni_direct pole axis (backward.hpp:79-80)
   unsigned long long bwd_nonfinite;  // non-finite gradient (backward.hpp:440-446)
+  unsigned long long overflow;     // max n_entries that exceeded the entry buffers' capacity, else 0
+  // -- per-render counters
   unsigned long long n_entries;    // total tile entries K (written by the offsets scan)
   unsigned long long n_visible;    // projected splats (RenderOutput::splats.size())
   unsigned long long n_instances;  // seam instances (RenderOutput::instances.size())
   unsigned long long n_band;       // band renders: Gaussians with entries in the band
   unsigned long long n_precull;    // band renders: pre-cull survivors
+  unsigned long long k_sort;       // tile entries sorted and binned: min(n_entries, capacity)
 };
+constexpr size_t kDevErrorsSticky = 5 * sizeof(unsigned long long);  // bytes of the sticky section
 constexpr unsigned long long kNoError = ~0ull;
 
 struct DevCamera {

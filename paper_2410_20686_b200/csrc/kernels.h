@@ -55,6 +55,11 @@ struct EmitArgs {
   const float4 *sp_ab, *sp_c;
   int width, height, tile_size, tiles_x, band_ty0, band_ty1;
   uint32_t *out_keys, *out_vals, *ent_off_idx;
+  const uint32_t* n_dev;            // device-side rank count (<= n) or null
+  const unsigned long long* total;  // total tile entries (the offsets scan's total)
+  uint32_t capacity;                // entries the output buffers hold
+  unsigned long long* k_sort;       // <- min(total, capacity) (or null)
+  unsigned long long* overflow;     // <- total when it exceeds the capacity
 };
 void launch_emit(const EmitArgs& a, cudaStream_t stream);
 
@@ -63,7 +68,7 @@ void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, flo
 
 // Tile CSR offsets [n_tiles + 1]; entries lie in tiles [t0, t1) (a row band), t1 <= n_tiles.
 void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, uint32_t t0, uint32_t t1,
-                        int32_t* offsets, cudaStream_t stream);
+                        int32_t* offsets, cudaStream_t stream, const uint32_t* k_dev = nullptr);
 
 // Peer image buffers ([3][W][H], the frame's layout) that the blend epilogue also writes
 // its pixels to: an all-gather of row bands fused into the kernel that produces them
@@ -97,8 +102,9 @@ void launch_blend_plain(const BlendArgs& a, cudaStream_t stream);
 // Scratch needed by exclusive_scan_u32 for n items.
 size_t scan_temp_bytes(int64_t n);
 // out[k] = sum_{j<k} in[k]; optionally atomically adds the 64-bit total to *total64.
+// n_dev: optional device-side item count <= n (the launch is sized for n).
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp, unsigned long long* total64,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const uint32_t* n_dev = nullptr);
 
 // Sorts hold fewer than 2^30 items: the onesweep look-back words carry 30-bit counts.
 constexpr unsigned long long kMaxSortItems = 1ull << 30;
@@ -109,10 +115,12 @@ size_t radix_sort_temp_bytes(int64_t n);
 // Optional payload gather: gather_dst[r] = gather_src[sorted value r], written by the
 // last pass (saves a separate gather over the sorted values).
 // Returns the first failed launch's error (the remaining passes are then not launched:
-// they would look back over status words nobody cleared).
+// they would look back over status words nobody cleared). n_dev: optional device-side
+// item count <= n; the kernels are then launched for n (the capacity) and read the count
+// on the device, so no host synchronisation is needed to learn it.
 cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit,
                              void* temp, int* which, cudaStream_t stream, const uint32_t* gather_src = nullptr,
-                             uint32_t* gather_dst = nullptr);
+                             uint32_t* gather_dst = nullptr, const uint32_t* n_dev = nullptr);
 
 // ------------------------------------------------------------------ training step
 size_t l1_loss_temp_bytes(int64_t count);
@@ -200,7 +208,7 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
 // Gaussian with entries.
 void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
                          const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
-                         cudaStream_t stream);
+                         cudaStream_t stream, const uint32_t* n_dev = nullptr);
 
 // SplatGrads of every projected Gaussian from the folded records (grad_pixels_to_splats).
 void launch_splat_grads(int64_t n, const float4* sp_ab, const float4* sp_c, const uint32_t* cnt, const float* folded,

@@ -42,10 +42,11 @@ constexpr int kRec = 9;  // mx, my, m00, m01, m11, op, c0, c1, c2
 // contributions (replayed entries inside the cutoff, :271-305).
 // work[2..3] (culled kernels): warp-entries walked (sum of the warps' list lengths) and
 // warp-entries with at least one contributing lane — the culling's efficiency.
+// exam is per lane; contrib, warp_entries and warp_live are warp totals (uniform).
 __device__ __forceinline__ void bwd_count_work(unsigned long long* work, uint32_t exam, uint32_t contrib,
                                                uint32_t warp_entries = 0, uint32_t warp_live = 0) {
   const uint32_t we = __reduce_add_sync(0xffffffffu, exam);
-  const uint32_t wc = __reduce_add_sync(0xffffffffu, contrib);
+  const uint32_t wc = contrib;
   if ((threadIdx.x & 31) == 0 && (we | wc | warp_entries)) {
     atomicAdd(work, (unsigned long long)we);
     atomicAdd(work + 1, (unsigned long long)wc);
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
     }
     __syncthreads();
   }
-  if (work) bwd_count_work(work, n_exam, n_contrib);
+  if (work) bwd_count_work(work, n_exam, __reduce_add_sync(0xffffffffu, n_contrib));
   __syncthreads();  // s_maxw and the shared batch are reused by the next chunk
   }
 }
@@ -328,6 +329,7 @@ __device__ __forceinline__ void pair_level16(const float A[kRec], const float B[
 // keep their zero record (the buffer is cleared before the launch). Skipping is
 // exact: a culled entry has computed d2 > cutoff^2 at every pixel of the warp, so
 // its contribution there is zero and it does not change t or the suffix.
+template <bool kCount>
 __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, const uint32_t* __restrict__ ent_off_idx,
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     // level 8 splits AB|CD, levels 4-2-1 finish) — 54 shuffles per 4 entries. The
     // totals land on lanes 0 (A), 8 (C), 16 (B) and 24 (D).
     const bool upper = lane & 16, mid = lane & 8;
-    n_wentries += (uint32_t)n_list;
+    if (kCount) n_wentries += (uint32_t)n_list;
     for (int qi = n_list - 1; qi >= 0; qi -= 4) {
       const int ja = s_list[warp][qi];
       const int jb = qi >= 1 ? s_list[warp][qi - 1] : -1;
@@ -527,7 +529,6 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
-        n_contrib += (uint32_t)any_a + (uint32_t)any_b;
         ma = __ballot_sync(0xffffffffu, any_a);
         mb = __ballot_sync(0xffffffffu, any_b);
         if (ma | mb) pair_level16(A, B, upper, K1);
@@ -550,7 +551,6 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
         else
 #pragma unroll
           for (int c = 0; c < kRec; ++c) D[c] = 0.0f;
-        n_contrib += (uint32_t)any_c + (uint32_t)any_d;
         mc = __ballot_sync(0xffffffffu, any_c);
         md = __ballot_sync(0xffffffffu, any_d);
         if (mc | md) pair_level16(C, D, upper, K2);
@@ -558,7 +558,10 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
 #pragma unroll
           for (int c = 0; c < kRec; ++c) K2[c] = 0.0f;
       }
-      n_wlive += (uint32_t)(ma != 0) + (uint32_t)(mb != 0) + (uint32_t)(mc != 0) + (uint32_t)(md != 0);
+      if (kCount) {
+        n_wlive += (uint32_t)(ma != 0) + (uint32_t)(mb != 0) + (uint32_t)(mc != 0) + (uint32_t)(md != 0);
+        n_contrib += __popc(ma) + __popc(mb) + __popc(mc) + __popc(md);
+      }
       if (ma | mb | mc | md) {
         float L[kRec];
 #pragma unroll
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
     prev_count = count;
     buf ^= 1;
   }
-  if (work) bwd_count_work(work, (uint32_t)wk, n_contrib, n_wentries, n_wlive);
+  if (kCount) bwd_count_work(work, (uint32_t)wk, n_contrib, n_wentries, n_wlive);
 }
 
 // ------------------------------------------------------------------ warp-specialised backward raster
@@ -903,7 +906,6 @@ __global__ void __launch_bounds__(kPipeThreads, ODGS_PIPE_MINB) k_bwd_raster_pip
           else
 #pragma unroll
             for (int c = 0; c < kRec; ++c) B[c] = 0.0f;
-          n_contrib += (uint32_t)any_a + (uint32_t)any_b;
           ma = __ballot_sync(0xffffffffu, any_a);
           mb = __ballot_sync(0xffffffffu, any_b);
           if (ma | mb) pair_level16(A, B, upper, K1);
@@ -924,7 +926,6 @@ __global__ void __launch_bounds__(kPipeThreads, ODGS_PIPE_MINB) k_bwd_raster_pip
           else
 #pragma unroll
             for (int c = 0; c < kRec; ++c) D[c] = 0.0f;
-          n_contrib += (uint32_t)any_c + (uint32_t)any_d;
           mc = __ballot_sync(0xffffffffu, any_c);
           md = __ballot_sync(0xffffffffu, any_d);
           if (mc | md) pair_level16(Cc, D, upper, K2);
@@ -933,6 +934,7 @@ __global__ void __launch_bounds__(kPipeThreads, ODGS_PIPE_MINB) k_bwd_raster_pip
             for (int c = 0; c < kRec; ++c) K2[c] = 0.0f;
         }
         n_wlive += (uint32_t)(ma != 0) + (uint32_t)(mb != 0) + (uint32_t)(mc != 0) + (uint32_t)(md != 0);
+        n_contrib += __popc(ma) + __popc(mb) + __popc(mc) + __popc(md);  // lanes (of 2 pixels) contributing
         if (ma | mb | mc | md) {
           float L[kRec];
 #pragma unroll
@@ -983,7 +985,8 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream) {
     return;
   }
   if (!a.plain && a.tile_size <= 16) {
-    launch_pdl(k_bwd_raster_cull, n_tiles, kBwdThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
+    // The counting instantiation only when counters are requested (they cost registers).
+    launch_pdl(a.work ? k_bwd_raster_cull<true> : k_bwd_raster_cull<false>, n_tiles, kBwdThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.ent_off_idx,
                                                            a.transmittance, a.walked, a.dl_dimage, a.width,
                                                            a.height, a.tile_size, a.tiles_x, a.alpha_clamp, cutoff2,
                                                            a.records, a.touched, a.band_ty0, a.band_ty1, a.order,
@@ -1308,8 +1311,9 @@ constexpr int kFoldChunk = 128;
 __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
     int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
     const uint32_t* __restrict__ off_sorted, const uint8_t* __restrict__ touched, const float* __restrict__ records,
-    float* __restrict__ folded) {
+    float* __restrict__ folded, const uint32_t* __restrict__ n_dev) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // a band's ranks counted on the device
   __shared__ float s_rec[kFoldWarps][kFoldChunk * kRec];
   __shared__ uint8_t s_touch[kFoldWarps][kFoldChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1361,11 +1365,11 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
 
 void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
                          const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, const uint32_t* n_dev) {
   if (n == 0) return;
   const int64_t warps = (n + 31) / 32;
-  launch_pdl(k_fold_records, (unsigned)((warps + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, stream, 
-      n, sorted_idx, cnt_sorted, off_sorted, touched, records, folded);
+  launch_pdl(k_fold_records, (unsigned)((warps + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, stream, n,
+             sorted_idx, cnt_sorted, off_sorted, touched, records, folded, n_dev);
   ++g_launches;
 }
 

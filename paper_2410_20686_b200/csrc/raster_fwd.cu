@@ -481,8 +481,18 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
     int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
     const uint32_t* __restrict__ off_sorted, const float4* __restrict__ sp_ab, const float4* __restrict__ sp_c,
     int width, int height, int tile_size, int tiles_x, int band_ty0, int band_ty1, uint32_t* __restrict__ out_keys,
-    uint32_t* __restrict__ out_vals, uint32_t* __restrict__ ent_off_idx) {
+    uint32_t* __restrict__ out_vals, uint32_t* __restrict__ ent_off_idx, const uint32_t* __restrict__ n_dev,
+    const unsigned long long* __restrict__ k_total, uint32_t capacity, unsigned long long* __restrict__ k_sort,
+    unsigned long long* __restrict__ overflow) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // depth-sorted ranks counted on the device
+  if (k_sort && blockIdx.x == 0 && threadIdx.x == 0) {
+    // Entries to sort / bin: all of them, or the capacity if they do not fit (the
+    // overflow word then makes the host re-run the frame with enough room).
+    const unsigned long long t = *k_total;
+    *k_sort = t <= capacity ? t : capacity;
+    if (t > capacity) atomicMax(overflow, t);
+  }
   __shared__ int s_span[kEmitWarps][32][12];
   __shared__ uint32_t s_area[kEmitWarps][32][3];
   __shared__ uint32_t s_magic[kEmitWarps][32][3];  // ceil-ish 2^32 / span width (0: divide)
@@ -556,8 +566,10 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit(
       const uint32_t m = s_magic[warp][lo][k];
       const uint32_t q = m ? __umulhi(j, m) : j / w;
       const int ty = span[2] + (int)q, tx = span[0] + (int)(j - q * w);
-      out_keys[base_off + p] = (uint32_t)(ty * tiles_x + tx);
-      out_vals[base_off + p] = (s_gid[warp][lo] << 2) | (uint32_t)k;
+      if (base_off + p < capacity) {
+        out_keys[base_off + p] = (uint32_t)(ty * tiles_x + tx);
+        out_vals[base_off + p] = (s_gid[warp][lo] << 2) | (uint32_t)k;
+      }
     }
   }
 }
@@ -567,9 +579,8 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
   const int64_t warps = (a.n + 31) / 32;
   const int64_t grid = (warps + kEmitWarps - 1) / kEmitWarps;
   launch_pdl(k_emit, (unsigned)grid, kEmitWarps * 32, 0, stream, a.n, a.sorted_idx, a.cnt_sorted, a.off_sorted, a.sp_ab,
-                                                         a.sp_c, a.width, a.height, a.tile_size, a.tiles_x,
-                                                         a.band_ty0, a.band_ty1, a.out_keys, a.out_vals,
-                                                         a.ent_off_idx);
+             a.sp_c, a.width, a.height, a.tile_size, a.tiles_x, a.band_ty0, a.band_ty1, a.out_keys, a.out_vals,
+             a.ent_off_idx, a.n_dev, a.total, a.capacity, a.k_sort, a.overflow);
   ++g_launches;
 }
 
@@ -581,8 +592,9 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream) {
 // Thread i covers entries 4i .. 4i+3 (one 16-byte key load; the sentinel position K
 // belongs to the thread whose range contains it).
 __global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ keys, uint32_t t0, uint32_t t1,
-                              int32_t* __restrict__ offsets) {
+                              int32_t* __restrict__ offsets, const uint32_t* __restrict__ k_dev) {
   pdl_wait();
+  if (k_dev) k_entries = min(k_entries, *k_dev);  // capacity-sized launch, count on the device
   const uint32_t e_first = 4u * (blockIdx.x * blockDim.x + threadIdx.x);
   if (e_first > k_entries) return;
   uint32_t kv[4];
@@ -608,24 +620,26 @@ __global__ void k_tile_ranges(uint32_t k_entries, const uint32_t* __restrict__ k
 }
 
 __global__ void k_fill_outside(uint32_t k_entries, uint32_t n_tiles, uint32_t t0, uint32_t t1,
-                               int32_t* __restrict__ offsets) {
+                               int32_t* __restrict__ offsets, const uint32_t* __restrict__ k_dev) {
   pdl_wait();
+  if (k_dev) k_entries = min(k_entries, *k_dev);
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < t0) offsets[t] = 0;
   else if (t > t1 && t <= n_tiles) offsets[t] = (int32_t)k_entries;
 }
 
 void launch_tile_ranges(uint32_t k_entries, const uint32_t* keys, uint32_t n_tiles, uint32_t t0, uint32_t t1,
-                        int32_t* offsets, cudaStream_t stream) {
+                        int32_t* offsets, cudaStream_t stream, const uint32_t* k_dev) {
   if (k_entries == 0) {
     cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (n_tiles + 1), stream);
     return;
   }
   const uint32_t threads = k_entries / 4 + 1;
-  launch_pdl(k_tile_ranges, (threads + 255) / 256, 256, 0, stream, k_entries, keys, t0, t1, offsets);
+  launch_pdl(k_tile_ranges, (threads + 255) / 256, 256, 0, stream, k_entries, keys, t0, t1, offsets, k_dev);
   ++g_launches;
   if (t0 > 0 || t1 < n_tiles) {
-    launch_pdl(k_fill_outside, (n_tiles + 1 + 255) / 256, 256, 0, stream, k_entries, n_tiles, t0, t1, offsets);
+    launch_pdl(k_fill_outside, (n_tiles + 1 + 255) / 256, 256, 0, stream, k_entries, n_tiles, t0, t1, offsets,
+               k_dev);
     ++g_launches;
   }
 }

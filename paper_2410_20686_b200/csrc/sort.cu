@@ -75,8 +75,9 @@ __device__ __forceinline__ uint32_t warp_reduce(uint32_t v) {
 // ------------------------------------------------------------------ scan
 __global__ void __launch_bounds__(kThreads) k_scan_reduce(const uint32_t* __restrict__ in, int64_t n,
                                                           uint32_t* __restrict__ block_sums,
-                                                          unsigned long long* total64) {
+                                                          unsigned long long* total64, const uint32_t* n_dev) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // device-side item count (capacity-sized launch)
   __shared__ uint32_t s_warp[kWarps];
   const int64_t base = (int64_t)blockIdx.x * kTile;
   uint32_t sum = 0;
@@ -104,8 +105,9 @@ __global__ void __launch_bounds__(kThreads) k_scan_reduce(const uint32_t* __rest
 __global__ void __launch_bounds__(kThreads) k_scan_downsweep(const uint32_t* __restrict__ in,
                                                              uint32_t* __restrict__ out, int64_t n,
                                                              const uint32_t* __restrict__ block_offsets,
-                                                             unsigned long long* total64) {
+                                                             unsigned long long* total64, const uint32_t* n_dev) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   __shared__ uint32_t s_warp[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)warp * kWarpItems;
@@ -161,8 +163,10 @@ struct PassPlan {
 
 __global__ void __launch_bounds__(kThreads) k_onesweep_hist(const uint32_t* __restrict__ keys, int64_t n,
                                                             PassPlan plan, uint32_t* __restrict__ hist,
-                                                            uint32_t* __restrict__ status0, int64_t n_status) {
+                                                            uint32_t* __restrict__ status0, int64_t n_status,
+                                                            const uint32_t* n_dev) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // device-side item count (capacity-sized launch)
   // Also clears the first pass's status words (each pass clears the next one's).
   for (int64_t k = (int64_t)blockIdx.x * kThreads + threadIdx.x; k < n_status; k += (int64_t)gridDim.x * kThreads)
     status0[k] = 0;
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, const uint32_t* __restrict__ digit_start,
     uint32_t* __restrict__ status, uint32_t* __restrict__ tile_counter, const uint32_t* __restrict__ gather_src,
-    uint32_t* __restrict__ gather_dst, uint32_t* __restrict__ status_next) {
+    uint32_t* __restrict__ gather_dst, uint32_t* __restrict__ status_next, const uint32_t* n_dev) {
   pdl_wait();
   constexpr int kW = Threads / 32;
   constexpr int kT = Threads * IPT;
@@ -228,20 +232,27 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
   __syncthreads();
   const int tile = s_tile;
   const int64_t tile_base = (int64_t)tile * kT;
+  // The items of this tile: [0, valid_count). With a device-side count (capacity-sized
+  // grid) the tiles past it have nothing to sort; they claim the highest ids, so no tile
+  // with items ever looks back at them. Only this 32-bit count stays live below.
+  const int64_t n_items = n_dev ? min(n, (int64_t)*n_dev) : n;
+  if (tile_base >= n_items && tile > 0) return;
+  const int valid_count = (int)min((int64_t)kT, n_items - tile_base);
   const int64_t base = tile_base + (int64_t)warp * kWI;
+  const int wbase = warp * kWI;  // tile-relative
   const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t key[IPT], val[IPT], rank[IPT];
   // All loads first, so the tile's loads per thread are in flight together.
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
     const int64_t idx = base + j * 32 + lane;
-    key[j] = idx < n ? __ldcs(keys_in + idx) : 0u;
-    val[j] = idx < n ? __ldcs(vals_in + idx) : 0u;
+    const bool ok = wbase + j * 32 + lane < valid_count;
+    key[j] = ok ? __ldcs(keys_in + idx) : 0u;
+    val[j] = ok ? __ldcs(vals_in + idx) : 0u;
   }
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
-    const int64_t idx = base + j * 32 + lane;
-    const bool valid = idx < n;
+    const bool valid = wbase + j * 32 + lane < valid_count;
     const uint32_t d = valid ? (key[j] >> shift) & mask : mask;
     uint32_t peers = 0xffffffffu;
 #pragma unroll
@@ -259,7 +270,6 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
   __syncthreads();
   // Per-digit tile totals (padding excluded: it sits in the last digit, after every
   // real item, so subtract it from that digit's count).
-  const int64_t valid_count = n - tile_base < kT ? n - tile_base : kT;
   uint32_t digit_total = 0;
   if (threadIdx.x < radix) {
     const int d = threadIdx.x;
@@ -288,8 +298,7 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
-    const int64_t idx = base + j * 32 + lane;
-    const uint32_t d = idx < n ? (key[j] >> shift) & mask : mask;
+    const uint32_t d = wbase + j * 32 + lane < valid_count ? (key[j] >> shift) & mask : mask;
     const uint32_t pos = s_start[d] + s_wcnt[warp][d] + rank[j];
     s_keys[pos] = key[j];
     s_vals[pos] = val[j];
@@ -349,8 +358,9 @@ __global__ void k_zero_u32(uint32_t* __restrict__ p, int n) {
 }
 
 __global__ void k_gather(int64_t n, const uint32_t* __restrict__ idx, const uint32_t* __restrict__ src,
-                         uint32_t* __restrict__ dst) {
+                         uint32_t* __restrict__ dst, const uint32_t* n_dev) {
   pdl_wait();
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = src[idx[i]];
 }
@@ -366,10 +376,10 @@ size_t scan_temp_bytes(int64_t n) {
 }
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp, unsigned long long* total64,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, const uint32_t* n_dev) {
   if (n <= 0) return;
   if (n <= kTile) {
-    launch_pdl(k_scan_downsweep, 1, kThreads, 0, stream, in, out, n, nullptr, total64);
+    launch_pdl(k_scan_downsweep, 1, kThreads, 0, stream, in, out, n, nullptr, total64, n_dev);
     ++g_launches;
     return;
   }
@@ -377,10 +387,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* temp
   uint32_t* sums = static_cast<uint32_t*>(temp);
   uint32_t* offs = sums + nb;
   void* next = reinterpret_cast<char*>(temp) + (((size_t)(2 * nb) * sizeof(uint32_t) + 255) / 256) * 256;
-  launch_pdl(k_scan_reduce, (unsigned)nb, kThreads, 0, stream, in, n, sums, total64);
+  // Blocks past the device-side count write zero sums, so the block scan needs no count.
+  launch_pdl(k_scan_reduce, (unsigned)nb, kThreads, 0, stream, in, n, sums, total64, n_dev);
   ++g_launches;
-  exclusive_scan_u32(sums, offs, nb, next, nullptr, stream);
-  launch_pdl(k_scan_downsweep, (unsigned)nb, kThreads, 0, stream, in, out, n, offs, nullptr);
+  exclusive_scan_u32(sums, offs, nb, next, nullptr, stream, nullptr);
+  launch_pdl(k_scan_downsweep, (unsigned)nb, kThreads, 0, stream, in, out, n, offs, nullptr, n_dev);
   ++g_launches;
 }
 
@@ -405,6 +416,7 @@ struct PassArgs {
   const uint32_t* gather_src;
   uint32_t* gather_dst;
   uint32_t* status_next;
+  const uint32_t* n_dev;
 };
 
 // The dynamic shared-memory opt-in is a per-device function attribute: one flag bit per
@@ -431,7 +443,8 @@ cudaError_t launch_pass_bits(const PassArgs& a, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   const int64_t tiles = (a.n + kT - 1) / kT;
   return launch_pdl(kern, (unsigned)tiles, Threads, smem, stream, a.keys_in, a.vals_in, a.keys_out, a.vals_out, a.n,
-                    a.shift, a.digit_start, a.status, a.tile_counter, a.gather_src, a.gather_dst, a.status_next);
+                    a.shift, a.digit_start, a.status, a.tile_counter, a.gather_src, a.gather_dst, a.status_next,
+                    a.n_dev);
 }
 
 template <int Threads, int IPT, int MinBlocks>
@@ -452,13 +465,14 @@ cudaError_t launch_pass(int bits, const PassArgs& a, cudaStream_t stream) {
 
 cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int begin_bit, int end_bit,
                              void* temp, int* which, cudaStream_t stream, const uint32_t* gather_src,
-                             uint32_t* gather_dst) {
+                             uint32_t* gather_dst, const uint32_t* n_dev) {
   *which = 0;
   if (n >= (int64_t)kMaxSortItems) return cudaErrorInvalidValue;
-  if (n <= 1 || end_bit <= begin_bit) {
+  if ((n <= 1 && !n_dev) || n <= 0 || end_bit <= begin_bit) {
     if (gather_dst && n > 0) {
       ++g_launches;
-      return launch_pdl(k_gather, (unsigned)((n + 255) / 256), 256, 0, stream, n, vals[0], gather_src, gather_dst);
+      return launch_pdl(k_gather, (unsigned)((n + 255) / 256), 256, 0, stream, n, vals[0], gather_src, gather_dst,
+                        n_dev);
     }
     return cudaSuccess;
   }
@@ -483,7 +497,7 @@ cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, in
   ++g_launches;
   int sms = 148;
   e = launch_pdl(k_onesweep_hist, (unsigned)std::min<int64_t>(nb, 4 * sms), kThreads, 0, stream, keys[0], n, plan,
-                 hist, status[0], tiles * 256);
+                 hist, status[0], tiles * 256, n_dev);
   if (e != cudaSuccess) return e;
   ++g_launches;
   e = launch_pdl(k_onesweep_hist_scan, passes, 256, 0, stream, hist);
@@ -495,7 +509,7 @@ cudaError_t radix_sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, in
     const bool last = p == passes - 1;
     PassArgs pa{keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, plan.shift[p], hist + p * 256,
                 status[p & 1], counters + p, last ? gather_src : nullptr, last ? gather_dst : nullptr,
-                last ? nullptr : status[(p + 1) & 1]};
+                last ? nullptr : status[(p + 1) & 1], n_dev};
     e = big ? launch_pass<kBigThreads, kBigIPT, kBigMinBlocks>(plan.bits[p], pa, stream)
             : launch_pass<kThreads, kSmallIPT, kSmallMinBlocks>(plan.bits[p], pa, stream);
     if (e != cudaSuccess) return e;

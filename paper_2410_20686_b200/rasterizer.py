@@ -223,6 +223,11 @@ class Context:
         if ss:
             ss[1].wait_stream(ss[0])
 
+    def set_async(self, enable: bool = True):
+        """odgs_ctx_set_async: renders and device-buffer backward passes return without
+        synchronising; errors surface at RenderOutput.check() (or any host read)."""
+        self.check(self.lib.odgs_ctx_set_async(self.handle, int(enable)))
+
     def set_profiling(self, enable: bool):
         self.check(self.lib.odgs_ctx_set_profiling(self.handle, int(enable)))
 
@@ -267,8 +272,16 @@ class RenderOutput:
 
     def info(self) -> capi.FrameInfo:
         i = capi.FrameInfo()
-        self.ctx.lib.odgs_frame_get_info(self.handle, C.byref(i))
+        self.ctx.check(self.ctx.lib.odgs_frame_get_info(self.handle, C.byref(i)))
         return i
+
+    def check(self) -> bool:
+        """The frame's check point (odgs_frame_check): raises the deferred error of
+        asynchronous work; True if the frame had to be re-rendered (an entry-buffer
+        overflow), in which case a backward enqueued on it must be repeated."""
+        rr = C.c_int32(0)
+        self.ctx.check(self.ctx.lib.odgs_frame_check(self.ctx.handle, self.handle, C.byref(rr)))
+        return bool(rr.value)
 
     def _download(self, fld: int, dtype, shape) -> np.ndarray:
         out = np.empty(shape, dtype=dtype)

@@ -118,18 +118,26 @@ class ViewShardedTrainer:
         (one device-to-host read per step), or None with read_loss=False."""
         torch = self.torch
         ctx, lib = self.ctx, self.ctx.lib
-        self.flat.zero_()
-        self.observed.zero_()
-        self.loss_sum.zero_()
-        for k, v in enumerate(self.mine):
-            cam = self.views[v]
-            render(ctx, self.cloud, cam, self.settings, out=self.frame)
-            img = self.frame.device_ptr(capi.FRAME_IMAGE)
-            # The loss stays on the device (added into loss_sum on the context's stream).
-            ctx.check(lib.odgs_photometric_loss_async(ctx.handle, C_void(img), C_void(self.targets[v].data_ptr()),
-                                                      cam.width, cam.height, self.cfg.lambda_ssim,
-                                                      C_void(self.dl.data_ptr()), C_void(self.loss_sum.data_ptr())))
-            backward(ctx, self.cloud, cam, self.frame, self.dl, self.settings, grads=self.grads, accumulate=True)
+        for attempt in range(3):
+            self.flat.zero_()
+            self.observed.zero_()
+            self.loss_sum.zero_()
+            for k, v in enumerate(self.mine):
+                cam = self.views[v]
+                render(ctx, self.cloud, cam, self.settings, out=self.frame)
+                img = self.frame.device_ptr(capi.FRAME_IMAGE)
+                # The loss stays on the device (added into loss_sum on the context's stream).
+                ctx.check(lib.odgs_photometric_loss_async(ctx.handle, C_void(img),
+                                                          C_void(self.targets[v].data_ptr()), cam.width, cam.height,
+                                                          self.cfg.lambda_ssim, C_void(self.dl.data_ptr()),
+                                                          C_void(self.loss_sum.data_ptr())))
+                backward(ctx, self.cloud, cam, self.frame, self.dl, self.settings, grads=self.grads,
+                         accumulate=True)
+            # Asynchronous contexts: one check point per step (deferred errors). An
+            # entry-buffer overflow in any view invalidates the step's gradients: the
+            # views run again, with buffers grown to the largest view's entries.
+            if not self.frame.check():
+                break
         allreduce_grads(self.flat, self.observed, self.group)
         ctx.wait_torch()  # Adam reads the reduced gradients
         step = self.iteration + 1

@@ -25,6 +25,12 @@ ctx.reset_stage_times()
 for _ in range(iters):
     fr = render(ctx, cloud, cam, s)
     g = backward(ctx, cloud, cam, fr, dl, s)
+from paper_2410_20686_b200 import _capi as capi  # noqa: E402
+torch.cuda.synchronize()
+stages = {k: round(v[0] / max(v[1], 1), 4) for k, v in ctx.stage_times().items() if v[1]}
+ctx.lib.odgs_frame_set_flags(fr.handle, capi.FRAME_COUNT_WORK)
+fr = render(ctx, cloud, cam, s, out=fr)
+g = backward(ctx, cloud, cam, fr, dl, s)
 torch.cuda.synchronize()
 print("n_entries", fr.info().n_entries, "work", fr.work(), "bwd_work", fr.backward_work())
-print({k: round(v[0] / max(v[1], 1), 4) for k, v in ctx.stage_times().items() if v[1]})
+print(stages)
