@@ -522,7 +522,12 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
   if (exact) {
     if ((st = read_frame_errors(ctx, f)) != ODGS_OK) return st;
     const DevErrors& he = *f->h_err;
-    if ((st = projection_error(ctx, he)) != ODGS_OK) return st;
+    if ((st = projection_error(ctx, he)) != ODGS_OK) {
+      // reported: the frame starts clean (its sticky words read and cleared)
+      f->pending = f->bwd_pending = false;
+      ODGS_CUDA(ctx, cudaMemcpyAsync(f->d_err, ctx->h_err_init, kDevErrorsSticky, cudaMemcpyHostToDevice, s));
+      return st;
+    }
     const unsigned long long total = n > 0 ? he.n_entries : 0ull;
     // The onesweep look-back words carry 30-bit digit counts (sort.cu), so a sort holds
     // fewer than 2^30 items.

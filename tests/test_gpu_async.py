@@ -86,7 +86,7 @@ def test_async_overflow_rerenders(gpu_ctx):
 
 def test_async_errors_at_the_check_point(gpu_ctx):
     arrs = [np.array(a, dtype=np.float32) for a in oracle_lib.random_cloud(950, 3000)]
-    good = to_cloud32(arrs)
+    good = to_cloud32([a.copy() for a in arrs])
     arrs[3][1777] = np.nan
     bad = to_cloud32(arrs)
     cam, s = CameraPose(256, 128), RenderSettings()
