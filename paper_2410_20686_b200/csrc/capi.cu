@@ -1420,6 +1420,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   sa.cnt = f->cnt.as<uint32_t>();
   sa.folded = f->folded.as<float>();
   sa.signs = signs;
+  sa.sec_max = 1.0f / std::cos(settings->max_elevation);
   sa.accumulate = (flags & ODGS_ACCUMULATE) ? 1 : 0;
   sa.g_means = gm;
   sa.g_rotations = gq;

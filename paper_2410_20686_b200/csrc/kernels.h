@@ -226,6 +226,7 @@ struct BwdSplatArgs {
   const uint32_t* cnt;
   const float* folded;  // [n][9] folded records (launch_fold_records), read where cnt > 0
   const float* signs;  // [12] GradTSigns
+  float sec_max;       // 1 / cos(max_elevation): the clamped Jacobian's secant
   int accumulate;
   float *g_means, *g_rotations, *g_log_scales, *g_raw_opacities, *g_colors, *g_pixel_grad_norm, *g_one_minus_cos;
   int32_t* g_observed;

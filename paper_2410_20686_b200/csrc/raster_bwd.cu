@@ -1014,20 +1014,42 @@ __device__ __forceinline__ bool all_finite(const float* v, int n) {
   return ok;
 }
 
-// jacobian_omni_factored with library float trig (closed form of the factored
-// product, projection.hpp:75-96): rows (kw sec / r)(cp, 0, -sp), (kh / r)(st sp, ct, st cp).
-__device__ __forceinline__ M23 jacobian_factored_fast(float phi, float theta, float r, float W, float H,
-                                                      float max_elevation, bool* clamped) {
-  const bool clamp = fabsf(theta) > max_elevation;
-  *clamped = clamp;
-  const float sec = 1.0f / cosf(clamp ? max_elevation : fabsf(theta));
-  float sp, cp, st, ct;
-  sincosf(phi, &sp, &cp);
-  sincosf(theta, &st, &ct);
-  const float a0 = W / (2.0f * kPiF) * sec / r, a1 = H / kPiF / r;
+// jacobian_omni_factored (projection.hpp:75-96) in closed form from the camera-space
+// components, without trigonometry: with rho = hypot(x, z) and r = |mu|, sin / cos of the
+// azimuth are x / rho, z / rho and of the elevation -y / r, rho / r, and sec(elevation) =
+// r / rho — or 1 / cos(max_elevation) where the forward clamped it (its flag decides, so
+// the branch matches the forward's). Rows (kw sec / r)(cp, 0, -sp), (kh / r)(st sp, ct,
+// st cp). Tolerance-checked like the rest of the per-splat backward.
+struct Angles {
+  float sp, cp, st, ct, rho, rho2, r, r2, inv_rho, inv_r;
+};
+
+__device__ __forceinline__ Angles angles_of(float x, float y, float z) {
+  Angles g;
+  g.rho2 = x * x + z * z;
+  g.rho = sqrtf(g.rho2);
+  g.r2 = g.rho2 + y * y;
+  g.r = sqrtf(g.r2);
+  g.inv_rho = __frcp_rn(g.rho);
+  g.inv_r = __frcp_rn(g.r);
+  if (g.rho > 0.0f) {
+    g.sp = x * g.inv_rho;
+    g.cp = z * g.inv_rho;
+  } else {  // atan2(0, 0) = 0, as the forward's azimuth
+    g.sp = 0.0f;
+    g.cp = 1.0f;
+  }
+  g.st = -y * g.inv_r;
+  g.ct = g.rho * g.inv_r;
+  return g;
+}
+
+__device__ __forceinline__ M23 jacobian_from_angles(const Angles& g, float W, float H, bool clamped, float sec_max) {
+  const float sec = clamped ? sec_max : g.r * g.inv_rho;
+  const float a0 = W / (2.0f * kPiF) * sec * g.inv_r, a1 = H / kPiF * g.inv_r;
   M23 j;
-  j.a[0][0] = a0 * cp; j.a[0][1] = 0.0f; j.a[0][2] = -a0 * sp;
-  j.a[1][0] = a1 * st * sp; j.a[1][1] = a1 * ct; j.a[1][2] = a1 * st * cp;
+  j.a[0][0] = a0 * g.cp; j.a[0][1] = 0.0f; j.a[0][2] = -a0 * g.sp;
+  j.a[1][0] = a1 * g.st * g.sp; j.a[1][1] = a1 * g.ct; j.a[1][2] = a1 * g.st * g.cp;
   return j;
 }
 
@@ -1038,6 +1060,19 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
   if (i >= n) return;
   const float4 c4 = a.sp_c[i];
   const uint32_t flags = __float_as_uint(c4.w);
+  if (a.accumulate && !(flags & kFlagVisible)) return;  // adds nothing: no read-modify-write
+  if (a.accumulate) {
+    // The accumulators are read only after the chain rule: fetch their lines into L2
+    // now, so the final read-modify-write does not wait on DRAM.
+    const float* acc_rows[6] = {a.g_means, a.g_rotations, a.g_log_scales, a.g_raw_opacities, a.g_colors, nullptr};
+    const int widths[5] = {3, 4, 3, 1, 3};
+    for (int k = 0; k < 5; ++k)
+      for (int c = 0; c < widths[k]; ++c)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(acc_rows[k] + (int64_t)c * n + i));
+    if (a.g_pixel_grad_norm) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.g_pixel_grad_norm + i));
+    if (a.g_one_minus_cos) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.g_one_minus_cos + i));
+    if (a.g_observed) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.g_observed + i));
+  }
   float gm[3] = {0, 0, 0}, gq[4] = {0, 0, 0, 0}, gls[3] = {0, 0, 0}, gop = 0, gcol[3] = {0, 0, 0};
   float pgn = 0, omc = 0;
   int observed = 0;
@@ -1075,21 +1110,17 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
     to_camera(a.cam, p, mu);
     const float x = mu[0], y = mu[1], z = mu[2];
     const float W = (float)a.cam.width, H = (float)a.cam.height;
-    // The backward is tolerance-checked (not bit-exact), so it uses the fast float
-    // library functions rather than the forward's portable binary64 ones.
-    const float phi = atan2f(x, z);
-    const float rho_h = hypotf(x, z);
-    const float theta = atan2f(-y, rho_h);
-    float st_, ct_;
-    sincosf(theta, &st_, &ct_);
-    omc = 1.0f - ct_;
-    const float depth = sqrtf(sum3(x * x, y * y, z * z));
-    bool clamped;
-    const M23 J = jacobian_factored_fast(phi, theta, depth, W, H, a.settings.max_elevation, &clamped);
+    // The backward is tolerance-checked (not bit-exact): angles from the components, fast
+    // exponentials and reciprocals rather than the forward's portable binary64 functions.
+    const Angles ang = angles_of(x, y, z);
+    omc = 1.0f - ang.ct;
+    const bool clamped = (flags & kFlagClamped) != 0;  // the forward's pole-clamp decision
+    const M23 J = jacobian_from_angles(ang, W, H, clamped, a.sec_max);
     const float qn = sqrtf(sum4(qraw[0] * qraw[0], qraw[1] * qraw[1], qraw[2] * qraw[2], qraw[3] * qraw[3]));
-    const float qq[4] = {qraw[0] / qn, qraw[1] / qn, qraw[2] / qn, qraw[3] / qn};
+    const float inv_qn = __frcp_rn(qn);
+    const float qq[4] = {qraw[0] * inv_qn, qraw[1] * inv_qn, qraw[2] * inv_qn, qraw[3] * inv_qn};
     const M3 Rq = quaternion_matrix(qq[0], qq[1], qq[2], qq[3]);
-    const float sc[3] = {expf(ls[0]), expf(ls[1]), expf(ls[2])};
+    const float sc[3] = {__expf(ls[0]), __expf(ls[1]), __expf(ls[2])};
     M3 m;
     for (int rr = 0; rr < 3; ++rr)
       for (int k = 0; k < 3; ++k) m.a[rr][k] = Rq.a[rr][k] * sc[k];
@@ -1119,35 +1150,34 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
         dJ[rr][c] = dT[rr][0] * Rc.a[c][0] + dT[rr][1] * Rc.a[c][1] + dT[rr][2] * Rc.a[c][2];
 
     float dmu[3] = {0, 0, 0};
-    const float rho2 = x * x + z * z;
+    const float rho2 = ang.rho2;
     if (!(rho2 > 0.0f)) {
       atomic_min_error(&a.err->bwd_domain, i, 3);
     } else {
-      const float rho = sqrtf(rho2);
-      const float r2 = rho2 + y * y;
+      const float rho = ang.rho, r2 = ang.r2;
+      const float inv_rho2 = __frcp_rn(rho2), inv_r2 = __frcp_rn(r2);
       const float kw0 = W / (2.0f * kPiF), kh0 = H / kPiF;
       if (!clamped) {  // grad_position (backward.hpp:73-105)
-        const float r4 = r2 * r2;
+        const float inv_r4 = inv_r2 * inv_r2;
+        const float inv_rho3 = inv_rho2 * ang.inv_rho;
         const float g11 = dJ[0][0], g13 = dJ[0][2], g21 = dJ[1][0], g22 = dJ[1][1], g23 = dJ[1][2];
-        const float xz_over_rho4 = x * z / (rho2 * rho2);
-        const float xx_minus_zz = (x * x - z * z) / (rho2 * rho2);
-        const float mixed = x * y * z * (2.0f * rho2 + r2) / (r4 * rho2 * rho);
-        const float straight = (r2 - 2.0f * y * y) / (r4 * rho);
+        const float xz_over_rho4 = x * z * (inv_rho2 * inv_rho2);
+        const float xx_minus_zz = (x * x - z * z) * (inv_rho2 * inv_rho2);
+        const float mixed = x * y * z * (2.0f * rho2 + r2) * (inv_r4 * inv_rho3);
+        const float straight = (r2 - 2.0f * y * y) * (inv_r4 * ang.inv_rho);
         dmu[0] = -2.0f * kw0 * xz_over_rho4 * g11 + kw0 * xx_minus_zz * g13 -
-                 kh0 * y * (z * z * r2 - 2.0f * x * x * rho2) / (r4 * rho2 * rho) * g21 - kh0 * x * straight * g22 +
+                 kh0 * y * (z * z * r2 - 2.0f * x * x * rho2) * (inv_r4 * inv_rho3) * g21 - kh0 * x * straight * g22 +
                  kh0 * mixed * g23;
-        dmu[1] = -kh0 * x * straight * g21 - 2.0f * kh0 * y * rho / r4 * g22 - kh0 * z * straight * g23;
+        dmu[1] = -kh0 * x * straight * g21 - 2.0f * kh0 * y * rho * inv_r4 * g22 - kh0 * z * straight * g23;
         dmu[2] = kw0 * xx_minus_zz * g11 + 2.0f * kw0 * xz_over_rho4 * g13 + kh0 * mixed * g21 -
-                 kh0 * z * straight * g22 - kh0 * y * (x * x * r2 - 2.0f * z * z * rho2) / (r4 * rho2 * rho) * g23;
+                 kh0 * z * straight * g22 - kh0 * y * (x * x * r2 - 2.0f * z * z * rho2) * (inv_r4 * inv_rho3) * g23;
       } else {  // grad_position_clamped (backward.hpp:111-150)
-        const float r = sqrtf(r2);
-        float cp, sp;
-        sincosf(phi, &sp, &cp);
-        const float ct = ct_, st = st_;
-        const float sec = 1.0f / cosf(a.settings.max_elevation);
-        const float kw = W / (2.0f * kPiF) * sec / r;
-        const float kh = H / kPiF / r;
-        const float djr[2][3] = {{-kw * cp / r, 0.0f, kw * sp / r}, {-kh * st * sp / r, -kh * ct / r, -kh * st * cp / r}};
+        const float inv_r = ang.inv_r;
+        const float cp = ang.cp, sp = ang.sp, ct = ang.ct, st = ang.st;
+        const float kw = W / (2.0f * kPiF) * a.sec_max * inv_r;
+        const float kh = H / kPiF * inv_r;
+        const float djr[2][3] = {{-kw * cp * inv_r, 0.0f, kw * sp * inv_r},
+                                 {-kh * st * sp * inv_r, -kh * ct * inv_r, -kh * st * cp * inv_r}};
         const float djp[2][3] = {{-kw * sp, 0.0f, -kw * cp}, {kh * st * cp, 0.0f, -kh * st * sp}};
         const float djt[2][3] = {{0.0f, 0.0f, 0.0f}, {kh * ct * sp, -kh * st, kh * ct * cp}};
         float cr = 0, cph = 0, cth = 0;
@@ -1157,14 +1187,16 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
             cph += dJ[rr][c] * djp[rr][c];
             cth += dJ[rr][c] * djt[rr][c];
           }
-        const float drdt[3] = {x / r, y / r, z / r};
-        const float dphidt[3] = {z / rho2, 0.0f, -x / rho2};
-        const float dthdt[3] = {x * y / (rho * r2), -rho / r2, z * y / (rho * r2)};
+        const float drdt[3] = {x * inv_r, y * inv_r, z * inv_r};
+        const float dphidt[3] = {z * inv_rho2, 0.0f, -x * inv_rho2};
+        const float k3 = ang.inv_rho * inv_r2;
+        const float dthdt[3] = {x * y * k3, -rho * inv_r2, z * y * k3};
         for (int c = 0; c < 3; ++c) dmu[c] = cr * drdt[c] + cph * dphidt[c] + cth * dthdt[c];
       }
       // Mean path: unclamped direct Jacobian (projection.hpp:118-133, backward.hpp:420-423)
-      const float jd[2][3] = {{kw0 * z / rho2, 0.0f, -kw0 * x / rho2},
-                              {-kh0 * x * y / (rho * r2), kh0 * rho / r2, -kh0 * y * z / (rho * r2)}};
+      const float k3 = ang.inv_rho * inv_r2;
+      const float jd[2][3] = {{kw0 * z * inv_rho2, 0.0f, -kw0 * x * inv_rho2},
+                              {-kh0 * x * y * k3, kh0 * rho * inv_r2, -kh0 * y * z * k3}};
       for (int c = 0; c < 3; ++c) dmu[c] += jd[0][c] * sg_mean[0] + jd[1][c] * sg_mean[1];
     }
     // means = R^T dmu
@@ -1225,7 +1257,7 @@ __global__ void __launch_bounds__(256, 4) k_bwd_splat(BwdSplatArgs a) {
       }
     for (int k = 0; k < 4; ++k) gu[k] *= 2.0f;
     const float qd = (qq[0] * gu[0] + qq[1] * gu[1]) + (qq[2] * gu[2] + qq[3] * gu[3]);
-    for (int k = 0; k < 4; ++k) gq[k] = (gu[k] - qq[k] * qd) / qn;
+    for (int k = 0; k < 4; ++k) gq[k] = (gu[k] - qq[k] * qd) * inv_qn;
 
     const float o = ab1.y;
     gop = sg_op * o * (1.0f - o);
@@ -1300,14 +1332,21 @@ void launch_splat_grads(int64_t n, const float4* sp_ab, const float4* sp_c, cons
 }
 
 // ------------------------------------------------------------------ ordered fold
-// Lane l of a warp folds the records of depth rank r0 + l in emit order (the
-// reference's tile-entry order per splat, backward.hpp:310-327); records no warp
-// wrote (touched == 0) are zero and skipped. The 32 ranks own one contiguous record
-// range, which the warp streams through shared memory in coalesced chunks of
-// kFoldChunk records; each lane then adds the part of its own range inside the chunk,
-// in order.
+// Per-Gaussian sum of its entry records (backward.hpp:310-327); a Gaussian's records are
+// contiguous in emit order ([off_sorted[r], +cnt_sorted[r]) for depth rank r). A warp owns
+// 32 consecutive ranks. Ranks with at most kFoldSmall records are summed by their own
+// lane, in record order; larger ranks (pole and seam splats, up to thousands of tiles)
+// are summed by the whole warp — lane l takes records l, l + 32, ... (coalesced 36-byte
+// records), then a fixed xor tree — so one long list no longer serialises its warp.
+// Records no warp wrote (touched == 0) are zero and skipped. Deterministic: every sum has
+// a fixed order.
 constexpr int kFoldWarps = 8;
-constexpr int kFoldChunk = 128;
+constexpr uint32_t kFoldSmall = 16;
+
+__device__ __forceinline__ void fold_add(const float* __restrict__ rec, float acc[kRec]) {
+#pragma unroll
+  for (int c = 0; c < kRec; ++c) acc[c] += __ldcs(rec + c);
+}
 
 __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
     int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
@@ -1315,53 +1354,70 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
     float* __restrict__ folded, const uint32_t* __restrict__ n_dev) {
   pdl_wait();
   if (n_dev) n = min(n, (int64_t)*n_dev);  // a band's ranks counted on the device
-  __shared__ float s_rec[kFoldWarps][kFoldChunk * kRec];
-  __shared__ uint8_t s_touch[kFoldWarps][kFoldChunk];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = ((int64_t)blockIdx.x * kFoldWarps + warp) * 32;
   if (r0 >= n) return;
   const int64_t r = r0 + lane;
   const uint32_t cnt = r < n ? cnt_sorted[r] : 0u;
   const uint32_t off = r < n ? off_sorted[r] : 0u;
-  // The warp's range: from its first rank's offset to the end of its last rank's.
-  const uint32_t beg = __shfl_sync(0xffffffffu, off, 0);
-  const int last = n - r0 >= 32 ? 31 : (int)(n - 1 - r0);
-  const uint32_t end = __shfl_sync(0xffffffffu, off + cnt, last);
-  float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (uint32_t c0 = beg; c0 < end; c0 += kFoldChunk) {
-    const uint32_t m = min((uint32_t)kFoldChunk, end - c0);
-    __syncwarp();
-    for (uint32_t k = lane; k < m; k += 32) s_touch[warp][k] = touched[c0 + k];
-    __syncwarp();
-    // Only written records are read (untouched ones hold stale data).
-    const float* src = records + (int64_t)c0 * kRec;
-    const uint32_t mf = m * kRec;
-    for (uint32_t k0 = 0; k0 < mf; k0 += 32 * 12) {  // 12 loads in flight per lane
-      float v[12];
+  const uint32_t g = r < n ? sorted_idx[r] : 0u;
+  // small ranks: the lane's own records, in order, four in flight at a time
+  if (cnt > 0 && cnt <= kFoldSmall) {
+    float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const uint32_t end = off + cnt;
+    for (uint32_t e = off; e < end; e += 4) {
+      float v[4][kRec];
 #pragma unroll
-      for (int u = 0; u < 12; ++u) {
-        const uint32_t k = k0 + lane + 32 * u;
-        v[u] = (k < mf && s_touch[warp][k / kRec]) ? __ldcs(src + k) : 0.0f;
+      for (int u = 0; u < 4; ++u) {
+        const bool live = e + u < end && touched[e + u];
+        const float* rec = records + (int64_t)(e + u) * kRec;
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) v[u][c] = live ? __ldcs(rec + c) : 0.0f;
       }
 #pragma unroll
-      for (int u = 0; u < 12; ++u) {
-        const uint32_t k = k0 + lane + 32 * u;
-        if (k < mf) s_rec[warp][k] = v[u];
-      }
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) acc[c] += v[u][c];
     }
-    __syncwarp();
-    const uint32_t lo = max(off, c0), hi = min(off + cnt, c0 + m);
-    for (uint32_t e = lo; e < hi; ++e) {
-      if (!s_touch[warp][e - c0]) continue;
-      const float* rec = &s_rec[warp][(e - c0) * kRec];
+    float* o = folded + (int64_t)g * kRec;
 #pragma unroll
-      for (int c = 0; c < kRec; ++c) acc[c] += rec[c];
+    for (int c = 0; c < kRec; ++c) o[c] = acc[c];
+  }
+  // large ranks: one at a time with the whole warp
+  uint32_t big = __ballot_sync(0xffffffffu, cnt > kFoldSmall);
+  while (big) {
+    const int src = __ffs(big) - 1;
+    big &= big - 1;
+    const uint32_t boff = __shfl_sync(0xffffffffu, off, src);
+    const uint32_t bcnt = __shfl_sync(0xffffffffu, cnt, src);
+    const uint32_t bg = __shfl_sync(0xffffffffu, g, src);
+    float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t k0 = lane; k0 < bcnt; k0 += 4 * 32) {  // four records in flight per lane
+      float v[4][kRec];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t k = k0 + 32 * u;
+        const bool live = k < bcnt && touched[boff + k];
+        const float* rec = records + (int64_t)(boff + k) * kRec;
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) v[u][c] = live ? __ldcs(rec + c) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int c = 0; c < kRec; ++c) acc[c] += v[u][c];
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1)
+#pragma unroll
+      for (int c = 0; c < kRec; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], d);
+    if (lane < kRec) {
+      float v = 0.0f;
+#pragma unroll
+      for (int c = 0; c < kRec; ++c) v = lane == c ? acc[c] : v;
+      folded[(int64_t)bg * kRec + lane] = v;
     }
   }
-  if (cnt == 0) return;
-  float* o = folded + (int64_t)sorted_idx[r] * kRec;
-#pragma unroll
-  for (int c = 0; c < kRec; ++c) o[c] = acc[c];
 }
 
 void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,

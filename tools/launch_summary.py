@@ -21,7 +21,7 @@ for r in rows[1:]:
     name = r[ix["Kernel Name"]].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("odgs_b200::", "").split("(")[0].split("<")[0]
     v = float(r[ix["Metric Value"]].replace(",", ""))
     unit = r[ix["Metric Unit"]]
-    v = v / 1000.0 if unit == "nsecond" else (v if unit == "usecond" else v * 1000.0)
+    v = v / 1000.0 if unit in ("nsecond", "ns") else (v if unit in ("usecond", "us") else v * 1000.0)
     tot[name] += v
     cnt[name] += 1
 T = sum(tot.values())
