@@ -23,6 +23,15 @@ namespace odgs_b200 {
 // project_gaussian alone (projection.hpp:178-216) — no first_non_finite pass; a
 // non-finite quaternion or log-scale of a Gaussian inside the shell is build_covariance's
 // invalid_argument (covariance.hpp:31-32), other non-finite values pass through.
+// The row's parameters as values (v: mean 3, quaternion 4, log-scales 3, raw opacity,
+// colour 3): preprocess_one after its loads, for callers that already hold them.
+template <bool kProjectOnly = false>
+__device__ __forceinline__ uint32_t preprocess_vals(
+    int64_t i, int64_t n, const float v[14], int sh_degree, const float* __restrict__ sh_rest, const DevCamera& cam,
+    const DevSettings& s, float4* __restrict__ sp_ab, float4* __restrict__ sp_c, float4* __restrict__ cov_out,
+    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err,
+    bool* visible);
+
 template <bool kProjectOnly = false>
 __device__ __forceinline__ uint32_t preprocess_one(
     int64_t i, int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
@@ -31,13 +40,27 @@ __device__ __forceinline__ uint32_t preprocess_one(
     const DevSettings& s, float4* __restrict__ sp_ab, float4* __restrict__ sp_c, float4* __restrict__ cov_out,
     uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err,
     bool* visible) {
+  const float v[14] = {__ldg(means + i),          __ldg(means + n + i),          __ldg(means + 2 * n + i),
+                       __ldg(rotations + i),      __ldg(rotations + n + i),      __ldg(rotations + 2 * n + i),
+                       __ldg(rotations + 3 * n + i), __ldg(log_scales + i),      __ldg(log_scales + n + i),
+                       __ldg(log_scales + 2 * n + i), __ldg(raw_opacities + i),  __ldg(colors + i),
+                       __ldg(colors + n + i),     __ldg(colors + 2 * n + i)};
+  return preprocess_vals<kProjectOnly>(i, n, v, sh_degree, sh_rest, cam, s, sp_ab, sp_c, cov_out, keys, vals, cnt,
+                                       err, visible);
+}
+
+template <bool kProjectOnly>
+__device__ __forceinline__ uint32_t preprocess_vals(
+    int64_t i, int64_t n, const float v[14], int sh_degree, const float* __restrict__ sh_rest, const DevCamera& cam,
+    const DevSettings& s, float4* __restrict__ sp_ab, float4* __restrict__ sp_c, float4* __restrict__ cov_out,
+    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err,
+    bool* visible) {
   *visible = false;
-  const float p[3] = {__ldg(means + i), __ldg(means + n + i), __ldg(means + 2 * n + i)};
-  const float q[4] = {__ldg(rotations + i), __ldg(rotations + n + i), __ldg(rotations + 2 * n + i),
-                      __ldg(rotations + 3 * n + i)};
-  const float ls[3] = {__ldg(log_scales + i), __ldg(log_scales + n + i), __ldg(log_scales + 2 * n + i)};
-  const float raw = __ldg(raw_opacities + i);
-  float col[3] = {__ldg(colors + i), __ldg(colors + n + i), __ldg(colors + 2 * n + i)};
+  const float p[3] = {v[0], v[1], v[2]};
+  const float q[4] = {v[3], v[4], v[5], v[6]};
+  const float ls[3] = {v[7], v[8], v[9]};
+  const float raw = v[10];
+  float col[3] = {v[11], v[12], v[13]};
   const int nb = sh_degree > 0 ? sh_count(sh_degree) : 0;
 
   keys[i] = kCulledKey;
@@ -295,6 +318,34 @@ __device__ __forceinline__ BandCull make_band_cull(const DevCamera& cam, const D
   return b;
 }
 
+// The pre-cull test on one row's values (p: mean, q: quaternion, ls: log-scales; fin: a
+// sum of every parameter of the row, non-finite iff one of them is).
+__device__ __forceinline__ bool band_survives_v(const float p[3], const float q[4], const float ls[3], float fin,
+                                                const DevCamera& cam, const DevSettings& s, const BandCull& b) {
+  float mu[3];
+  to_camera(cam, p, mu);
+  const float sq = sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]);
+  const float depth = sqrtf(sq);
+  const float qq = sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]);
+  if (!(sq > 0.0f && qq > 1e-20f && isfinite(depth) && isfinite(fin))) return true;
+  if (!(depth >= s.near_radius && depth <= s.far_radius)) return false;
+  const float inv_d = 1.0f / depth;
+  const float rho = sqrtf(mu[0] * mu[0] + mu[2] * mu[2]);
+  const float sin_th = -mu[1] * inv_d;
+  const float sec = fminf(depth / rho, b.sec_max);
+  const float a0 = b.a0k * sec * inv_d, a1 = b.a1k * inv_d;
+  const float smax = __expf(fmaxf(ls[0], fmaxf(ls[1], ls[2])));
+  const float rb = s.cutoff_sigma * sqrtf(smax * smax * (a0 * a0 + a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
+  const float rt = rb * b.rad_per_px;
+  if (!(rt < 1.0f)) return true;
+  float sr, cr;
+  __sincosf(rt, &sr, &cr);
+  constexpr float kPoleGuard = 1.5607963f;  // pi/2 - 0.01
+  if (b.top + rt < kPoleGuard && sin_th > b.sin_top * cr + b.cos_top * sr) return false;
+  if (b.bot - rt > -kPoleGuard && sin_th < b.sin_bot * cr - b.cos_bot * sr) return false;
+  return true;
+}
+
 __device__ __forceinline__ bool band_survives(int64_t i, int64_t n, const float* __restrict__ means,
                                               const float* __restrict__ rotations,
                                               const float* __restrict__ log_scales,
@@ -314,31 +365,7 @@ __device__ __forceinline__ bool band_survives(int64_t i, int64_t n, const float*
   fin += (ls[1] + ls[2]) + (__ldg(raw_opacities + i) +
                             ((__ldg(colors + i) + __ldg(colors + n + i)) + __ldg(colors + 2 * n + i)));
   for (int k = 0; k < n_sh; ++k) fin += __ldg(sh_rest + (int64_t)k * n + i);
-  float mu[3];
-  to_camera(cam, p, mu);
-  const float sq = sum3(mu[0] * mu[0], mu[1] * mu[1], mu[2] * mu[2]);
-  const float depth = sqrtf(sq);
-  const float qq = sum4(q[0] * q[0], q[1] * q[1], q[2] * q[2], q[3] * q[3]);
-  if (!(sq > 0.0f && qq > 1e-20f && isfinite(depth) && isfinite(fin))) return true;
-  // shell-culled: the exact path would produce the same culled outputs
-  if (!(depth >= s.near_radius && depth <= s.far_radius)) return false;
-  const float inv_d = 1.0f / depth;
-  const float rho = sqrtf(mu[0] * mu[0] + mu[2] * mu[2]);
-  const float sin_th = -mu[1] * inv_d;
-  const float sec = fminf(depth / rho, b.sec_max);  // rho = 0: +inf -> sec_max
-  const float a0 = b.a0k * sec * inv_d, a1 = b.a1k * inv_d;
-  const float smax = __expf(fmaxf(ls[0], fmaxf(ls[1], ls[2])));
-  const float rb = s.cutoff_sigma * sqrtf(smax * smax * (a0 * a0 + a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
-  const float rt = rb * b.rad_per_px;
-  if (!(rt < 1.0f)) return true;  // also non-finite rb
-  float sr, cr;
-  __sincosf(rt, &sr, &cr);
-  constexpr float kPoleGuard = 1.5607963f;  // pi/2 - 0.01
-  // above: theta > top + rt
-  if (b.top + rt < kPoleGuard && sin_th > b.sin_top * cr + b.cos_top * sr) return false;
-  // below: theta < bot - rt
-  if (b.bot - rt > -kPoleGuard && sin_th < b.sin_bot * cr - b.cos_bot * sr) return false;
-  return true;
+  return band_survives_v(p, q, ls, fin, cam, s, b);
 }
 
 // Fused band pre-cull + exact preprocess + band compaction, one warp per chunk of
@@ -436,6 +463,124 @@ __global__ void __launch_bounds__(256, 3) k_band_preprocess(
   }
 }
 
+// The same pass for SH degree 0 clouds with n % 4 == 0 and 16-byte aligned rows, at HBM
+// speed: lane l takes the four consecutive rows 4l..4l+3 of each group of 128 with one
+// 16-byte load per parameter row (14 loads per lane in flight); the pre-cull runs on the
+// loaded values, and each survivor is queued with its 14 parameters, so the exact path
+// reads shared memory instead of re-gathering the row (scattered survivor rows would cost
+// a 32-byte sector per 4-byte parameter). Survivors are queued in index order (a warp
+// prefix sum over the lanes' counts); the group's cnt / sp_c are cleared with vector
+// stores first (the exact path overwrites the survivors' after the __syncwarp).
+constexpr int kBandVecWarps = 4;
+constexpr uint32_t kBandVecQueue = 160;  // >= 31 + 128
+
+__global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
+    int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
+    const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
+    const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
+    float4* __restrict__ sp_c, float4* __restrict__ cov_out, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err,
+    uint32_t* __restrict__ seg_keys, uint32_t* __restrict__ seg_vals, uint32_t* __restrict__ seg_count) {
+  pdl_wait();
+  __shared__ uint32_t s_idx[kBandVecWarps][kBandVecQueue];
+  __shared__ float s_val[kBandVecWarps][14][kBandVecQueue];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w = (int64_t)blockIdx.x * kBandVecWarps + warp;
+  const int64_t base = w * kBandWarpChunk;
+  if (base >= n) return;
+  const int64_t end = min(base + (int64_t)kBandWarpChunk, n);
+  uint32_t head = 0, tail = 0;
+  uint32_t out_len = 0, n_surv = 0, n_vis = 0, n_inst = 0;
+  const uint32_t lt = (1u << lane) - 1u;
+  const BandCull bc = make_band_cull(cam, s);
+  auto drain = [&](uint32_t count) {
+    bool visible = false, has = false;
+    uint32_t key = 0, idx = 0;
+    if (lane < count) {
+      const uint32_t slot = (head + lane) % kBandVecQueue;
+      idx = s_idx[warp][slot];
+      float v[14];
+#pragma unroll
+      for (int k = 0; k < 14; ++k) v[k] = s_val[warp][k][slot];
+      n_inst += preprocess_vals(idx, n, v, 0, nullptr, cam, s, sp_ab, sp_c, cov_out, keys, vals, cnt, err, &visible);
+      has = cnt[idx] > 0;
+      key = keys[idx];
+    }
+    head += count;
+    n_vis += visible ? 1u : 0u;
+    const uint32_t hb = __ballot_sync(0xffffffffu, has);
+    if (has) {
+      const int64_t o = base + out_len + __popc(hb & lt);
+      seg_keys[o] = key;
+      seg_vals[o] = idx;
+    }
+    out_len += __popc(hb);
+  };
+  const float* rows[14] = {means,     means + n,          means + 2 * n,      rotations,          rotations + n,
+                           rotations + 2 * n, rotations + 3 * n, log_scales,  log_scales + n,     log_scales + 2 * n,
+                           raw_opacities, colors,         colors + n,         colors + 2 * n};
+  for (int64_t c = base; c < end; c += 128) {
+    const int64_t i0 = c + 4 * lane;
+    const bool any = i0 < end;  // end - base is a multiple of 4
+    float4 v[14];
+#pragma unroll
+    for (int k = 0; k < 14; ++k)
+      v[k] = any ? __ldcs(reinterpret_cast<const float4*>(rows[k] + i0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t m = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      auto el = [&](int k) { return u == 0 ? v[k].x : u == 1 ? v[k].y : u == 2 ? v[k].z : v[k].w; };
+      const float p[3] = {el(0), el(1), el(2)};
+      const float qv[4] = {el(3), el(4), el(5), el(6)};
+      const float ls[3] = {el(7), el(8), el(9)};
+      // every parameter of the row: non-finite anywhere -> the exact path reports it
+      const float fin = (((p[0] + p[1]) + (p[2] + qv[0])) + ((qv[1] + qv[2]) + (qv[3] + ls[0]))) +
+                        ((ls[1] + ls[2]) + (el(10) + ((el(11) + el(12)) + el(13))));
+      if (any && band_survives_v(p, qv, ls, fin, cam, s, bc)) m |= 1u << u;
+    }
+    if (any) {
+      reinterpret_cast<uint4*>(cnt + i0)[0] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sp_c[i0 + u] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+    }
+    const uint32_t cnt_l = __popc(m);
+    uint32_t incl = cnt_l;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    uint32_t pos = tail + incl - cnt_l;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (m & (1u << u)) {
+        const uint32_t slot = pos % kBandVecQueue;
+        s_idx[warp][slot] = (uint32_t)(i0 + u);
+#pragma unroll
+        for (int k = 0; k < 14; ++k)
+          s_val[warp][k][slot] = u == 0 ? v[k].x : u == 1 ? v[k].y : u == 2 ? v[k].z : v[k].w;
+        ++pos;
+      }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    tail += total;
+    n_surv += total;
+    __syncwarp();
+    while (tail - head >= 32) drain(32);
+    __syncwarp();
+  }
+  if (tail != head) drain(tail - head);
+  const uint32_t vis = __reduce_add_sync(0xffffffffu, n_vis);
+  const uint32_t inst = __reduce_add_sync(0xffffffffu, n_inst);
+  if (lane == 0) {
+    seg_count[w] = out_len;
+    if (vis | inst) {
+      atomicAdd(&err->n_visible, (unsigned long long)vis);
+      atomicAdd(&err->n_instances, (unsigned long long)inst);
+    }
+    if (n_surv) atomicAdd(&err->n_precull, (unsigned long long)n_surv);
+  }
+}
+
 // Concatenates the warp segments (one warp per segment) at their scanned offsets.
 __global__ void k_concat_segments(int64_t n_seg, const uint32_t* __restrict__ seg_count,
                                   const uint32_t* __restrict__ seg_off, const uint32_t* __restrict__ seg_keys,
@@ -459,6 +604,16 @@ void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_
                             cudaStream_t stream) {
   if (a.n == 0) return;
   const int64_t n_seg = band_segments(a.n);
+  auto aligned = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  const bool vec = a.sh_degree == 0 && a.n % 4 == 0 && aligned(a.means) && aligned(a.rotations) &&
+                   aligned(a.log_scales) && aligned(a.raw_opacities) && aligned(a.colors);
+  if (vec) {
+    launch_pdl(k_band_preprocess_vec, (unsigned)((n_seg + kBandVecWarps - 1) / kBandVecWarps), kBandVecWarps * 32, 0,
+               stream, a.n, a.means, a.rotations, a.log_scales, a.raw_opacities, a.colors, a.cam, a.settings, a.sp_ab,
+               a.sp_c, a.cov_out, a.keys, a.vals, a.cnt, a.err, seg_keys, seg_vals, seg_count);
+    ++g_launches;
+    return;
+  }
   launch_pdl(k_band_preprocess, (unsigned)((n_seg + 7) / 8), 256, 0, stream, 
       a.n, a.means, a.rotations, a.log_scales, a.raw_opacities, a.colors, a.cam, a.settings, a.sp_ab, a.sp_c,
       a.cov_out, a.keys, a.vals, a.cnt, a.err, a.sh_degree, a.sh_rest, seg_keys, seg_vals, seg_count);
