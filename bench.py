@@ -590,6 +590,10 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
                                   "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                                   "work_model": "N (56 B cloud + 4x14 B grads + 12 B stats) + 36 B per tile entry "
                                                 "(SURVEY.md §8d)"}
+    for k in ("bwd_raster", "fold_and_splat"):
+        if k in roof:
+            roof[k]["traffic"] = ncu_traffic(k)
+            roof[k]["traffic_source"] = "profiles/ncu_traffic.json (one ncu --set full capture of a C4 view)"
     if allreduce:
         roof["allreduce"] = allreduce
 
