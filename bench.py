@@ -512,10 +512,15 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
     ms_max = float(t.item())
     last_loss = tr.step()
 
-    # Separate pass: per-stage times (library CUDA events) and the work counters of every
-    # view of one step (forward examined / composited, backward replayed / contributing).
+    # Separate passes: per-stage times (library CUDA events), then the work counters of
+    # every view of one step (forward examined / composited, backward replayed /
+    # contributing; the counting backward is a separate, slower instantiation).
     ctx.set_profiling(True)
     ctx.reset_stage_times()
+    tr.step(read_loss=False)
+    torch.cuda.synchronize()
+    stages = {k: v[0] for k, v in ctx.stage_times().items() if v[1] > 0}
+    ctx.set_profiling(False)
     fwd_work, bwd_work = [0, 0], [0, 0, 0, 0]
     orig_backward = tr.frame  # the trainer renders every view into tr.frame
     import paper_2410_20686_b200.train as train_mod
@@ -538,8 +543,6 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
         train_mod.backward = real_backward
         ctx.lib.odgs_frame_set_flags(tr.frame.handle, 0)
     torch.cuda.synchronize()
-    stages = {k: v[0] for k, v in ctx.stage_times().items() if v[1] > 0}
-    ctx.set_profiling(False)
     nv = len(tr.mine)
     stage_view = {k: v / nv for k, v in stages.items()}
 
