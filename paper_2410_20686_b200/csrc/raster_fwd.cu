@@ -376,7 +376,7 @@ __device__ __forceinline__ bool band_survives(int64_t i, int64_t n, const float*
 // of seg_keys / seg_vals; seg_count[warp] is the segment length. Culled Gaussians get
 // the culled per-Gaussian outputs (cnt 0, sp_c 0); their keys / vals are not written
 // (only the compacted pairs are sorted).
-constexpr int kBandWarpChunk = 2048;
+constexpr int kBandWarpChunk = 512;  // 2048: 2.7% slower C5 bands (tail wave of long warps)
 constexpr int kBandUnroll = 4;
 constexpr int kBandQueue = 256;  // >= 31 + 32 * kBandUnroll, a power of two
 

@@ -268,3 +268,41 @@ def test_default_cutoff_gradients_match_fp64_oracle_masked(gpu_ctx, name, make, 
     for k in GROUPS:
         err = group_rel(getattr(g, k), o[k])
         assert err < 1e-3, (k, err)
+
+
+def _pipe_child(q):
+    import os
+    os.environ["ODGS_BWD_KERNEL"] = "pipe"
+    try:
+        from paper_2410_20686_b200 import Context, scenes
+        ctx = Context(0)
+        c = scenes.cloud_c3(50_000)
+        cam = scenes.yaw_camera(0.3, 1024, 512)
+        gs, _ = settings_pair()
+        dl = probe(13, 1024, 512)
+        g = backward(ctx, c, cam, render(ctx, c, cam, gs), dl, gs)
+        q.put({k: getattr(g, k) for k in GROUPS + ["observed"]})
+    except Exception as e:  # reported to the parent
+        q.put(repr(e))
+
+
+def test_pipelined_backward_kernel_matches_default(gpu_ctx):
+    """The warp-specialised backward raster (ODGS_BWD_KERNEL=pipe: producer warp, mbarrier
+    ring, two pixels per lane) gives the default kernel's gradients (summation order
+    differs: group-relative 1e-5)."""
+    import multiprocessing as mp
+    from paper_2410_20686_b200 import scenes
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    p = ctx_mp.Process(target=_pipe_child, args=(q,))
+    p.start()
+    got = q.get(timeout=300)
+    p.join(timeout=60)
+    assert not isinstance(got, str), got
+    c = scenes.cloud_c3(50_000)
+    cam = scenes.yaw_camera(0.3, 1024, 512)
+    gs, _ = settings_pair()
+    ref = backward(gpu_ctx, c, cam, render(gpu_ctx, c, cam, gs), probe(13, 1024, 512), gs)
+    for k in GROUPS:
+        assert group_rel(got[k], getattr(ref, k)) < 1e-5, k
+    assert np.array_equal(got["observed"], ref.observed)
