@@ -965,7 +965,9 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
     image[2 * plane + pix[q]] = cb[q];
     trans_out[pix[q]] = t[q];
     walked_out[pix[q]] = walked[q];
-    for (int k = 0; k < peers.n; ++k) {  // fused band all-gather, as in k_blend_cull
+#pragma unroll
+    for (int k = 0; k < kMaxPeers; ++k) {  // fused band all-gather, as in k_blend_cull
+      if (k >= peers.n) break;
       float* o = peers.ptr[k];
       o[pix[q]] = cr[q];
       o[plane + pix[q]] = cg[q];
@@ -1025,7 +1027,7 @@ __global__ void __launch_bounds__(kBlendThreads, 7) k_blend_cull(
   }
   const int x = tx * tile_size + lx, y = ty * tile_size + ly;
   valid = valid && x < width && y < height;
-  const float px = (float)x + 0.5f, py = (float)y + 0.5f;
+  const float px = valid ? (float)x + 0.5f : -1.0f, py = (float)y + 0.5f;  // px < 0: no pixel
   {
     float xmin = valid ? px : INFINITY, xmax = valid ? px : -INFINITY;
     float ymin = valid ? py : INFINITY, ymax = valid ? py : -INFINITY;
@@ -1130,22 +1132,30 @@ __global__ void __launch_bounds__(kBlendThreads, 7) k_blend_cull(
     }
   }
 
-  const uint32_t exam = valid ? (uint32_t)min(walked + 1, e1 - e0) : 0u;
+  // The pixel again from its centre (exact: coordinates < 2^23), so x, y and the valid
+  // flag need no registers across the walk.
+  const bool valid_px = px >= 0.0f;
+  const uint32_t exam = valid_px ? (uint32_t)min(walked + 1, e1 - e0) : 0u;
   const uint32_t w_exam = __reduce_add_sync(0xffffffffu, exam);
   const uint32_t w_contrib = __reduce_add_sync(0xffffffffu, contrib);
   if (lane == 0 && work) {
     atomicAdd(work, (unsigned long long)w_exam);
     atomicAdd(work + 1, (unsigned long long)w_contrib);
   }
-  if (valid) {
+  if (valid_px) {
     const int64_t plane = (int64_t)width * height;
-    const int64_t p = (int64_t)x * height + y;
+    const int64_t p = (int64_t)(int)px * height + (int)py;
     image[p] = cr;
     image[plane + p] = cg;
     image[2 * plane + p] = cb;
     trans_out[p] = t;
     walked_out[p] = walked;
-    for (int k = 0; k < peers.n; ++k) {  // fused all-gather: the same pixel into every peer's image
+    // Fused all-gather: the same pixel into every peer's image. Unrolled, so the peer
+    // pointers are read from the parameter bank (a runtime index would copy the array
+    // to local memory).
+#pragma unroll
+    for (int k = 0; k < kMaxPeers; ++k) {
+      if (k >= peers.n) break;
       float* q = peers.ptr[k];
       q[p] = cr;
       q[plane + p] = cg;
