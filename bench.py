@@ -515,33 +515,41 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
     # Separate passes: per-stage times (library CUDA events), then the work counters of
     # every view of one step (forward examined / composited, backward replayed /
     # contributing; the counting backward is a separate, slower instantiation).
-    ctx.set_profiling(True)
-    ctx.reset_stage_times()
+    # (stage times summed over the trainer's contexts: its views alternate between two)
+    for c in tr.contexts:
+        c.set_profiling(True)
+        c.reset_stage_times()
     tr.step(read_loss=False)
     torch.cuda.synchronize()
-    stages = {k: v[0] for k, v in ctx.stage_times().items() if v[1] > 0}
-    ctx.set_profiling(False)
+    stages = {}
+    for c in tr.contexts:
+        for k, v in c.stage_times().items():
+            if v[1] > 0:
+                stages[k] = stages.get(k, 0.0) + v[0]
+        c.set_profiling(False)
     fwd_work, bwd_work = [0, 0], [0, 0, 0, 0]
-    orig_backward = tr.frame  # the trainer renders every view into tr.frame
     import paper_2410_20686_b200.train as train_mod
     real_backward = train_mod.backward
 
     def counting_backward(*a, **kw):
         out = real_backward(*a, **kw)
-        w = orig_backward.work()
-        b = orig_backward.backward_work()
+        fr = a[3]  # the view's frame
+        w = fr.work()
+        b = fr.backward_work()
         fwd_work[0] += w[0]; fwd_work[1] += w[1]
         for j in range(4):
             bwd_work[j] += b[j]
         return out
     train_mod.backward = counting_backward
     from paper_2410_20686_b200 import _capi as capi
-    ctx.lib.odgs_frame_set_flags(tr.frame.handle, capi.FRAME_COUNT_WORK)
+    for ln in tr.lanes:
+        ln.ctx.lib.odgs_frame_set_flags(ln.frame.handle, capi.FRAME_COUNT_WORK)
     try:
         tr.step(read_loss=False)
     finally:
         train_mod.backward = real_backward
-        ctx.lib.odgs_frame_set_flags(tr.frame.handle, 0)
+        for ln in tr.lanes:
+            ln.ctx.lib.odgs_frame_set_flags(ln.frame.handle, 0)
     torch.cuda.synchronize()
     nv = len(tr.mine)
     stage_view = {k: v / nv for k, v in stages.items()}
@@ -606,6 +614,7 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
     return {"metric": "train iters/sec (C4: 3M Gaussians, batch of 8 ERP views at 2048x1024)",
             "value": args.train_steps / (ms_max / 1000.0), "unit": "iters/s", "ms_per_step": ms_max / args.train_steps,
             "steps": args.train_steps, "warmup": 2, "views_per_gpu": nv, "n_gpus": world,
+            "view_pipeline": f"{len(tr.lanes)} contexts (view k + 1 renders while view k back-propagates)",
             "scaling": "strong", "loss": "photometric_loss, lambda_ssim = 0.2 (L1 + SSIM on the GPU)",
             "timing": "CUDA events around the unprofiled steps (no host loss readback), max over ranks",
             "collective": "NCCL all-reduce (sum) of 16n floats + n int32" if world > 1 else "none (1 rank)",

@@ -21,8 +21,8 @@ import numpy as np
 
 from . import _capi as capi
 from .densify import DensifyConfig, DensifyStats, Rng, TrainState, densify_and_prune, reset_opacity
-from .rasterizer import (CameraPose, Context, GaussianCloud, GradBuffers, RenderOutput, RenderSettings, backward,
-                         render)
+from .rasterizer import (CUDA_STREAM_LEGACY, CameraPose, Context, GaussianCloud, GradBuffers, RenderOutput,
+                         RenderSettings, backward, render)
 
 FLAT_LAYOUT = (("means", 3), ("rotations", 4), ("log_scales", 3), ("raw_opacities", 1), ("colors", 3),
                ("pixel_grad_norm", 1), ("one_minus_cos", 1))
@@ -81,12 +81,37 @@ def allreduce_grads(flat, observed, group=None):
         dist.all_reduce(observed, op=dist.ReduceOp.SUM, group=group)
 
 
+class _Lane:
+    """One context of the trainer's view pipeline: its stream, frame, upstream-gradient
+    buffer and device-side loss sum."""
+
+    def __init__(self, torch, ctx: Context, n_px: int, device):
+        self.ctx = ctx
+        h = ctx.stream
+        if h in (0, CUDA_STREAM_LEGACY):  # the legacy default stream: torch's default stream
+            self.stream = torch.cuda.default_stream(device)
+        elif h == torch.cuda.current_stream(device).cuda_stream:
+            self.stream = torch.cuda.current_stream(device)
+        else:
+            self.stream = torch.cuda.ExternalStream(h, device=device)
+        self.frame = RenderOutput(ctx)
+        self.dl = torch.empty(3 * n_px, dtype=torch.float32, device=device)
+        self.loss_sum = torch.zeros(1, dtype=torch.float64, device=device)
+
+
 class ViewShardedTrainer:
     """C4 training step: render + photometric loss (L1 + SSIM) + backward for this rank's views, gradient
-    all-reduce, Adam. Everything stays on the device."""
+    all-reduce, Adam. Everything stays on the device.
+
+    pipeline=True: views alternate between two contexts (two streams), so view k + 1's
+    render, loss and front end run while view k's backward does; the backward passes —
+    the only steps that touch the shared gradient buffer — stay in view order (each waits
+    on the previous one's event), so the accumulated gradients are bit-identical to the
+    sequential loop's."""
 
     def __init__(self, ctx: Context, cloud: GaussianCloud, views: Sequence[CameraPose], targets, settings,
-                 cfg: TrainConfig, extent: float, rank: int = 0, world: int = 1, group=None):
+                 cfg: TrainConfig, extent: float, rank: int = 0, world: int = 1, group=None,
+                 pipeline: bool = True):
         import torch
         self.torch = torch
         self.ctx, self.cloud, self.views, self.targets = ctx, cloud, list(views), list(targets)
@@ -97,11 +122,19 @@ class ViewShardedTrainer:
         self.rng = Rng(cfg.seed)
         self.last_densify: Optional[DensifyStats] = None
         H, W = views[0].height, views[0].width
-        self.dl = self.torch.empty(3 * W * H, dtype=self.torch.float32, device=cloud.means.device)
-        self.loss_sum = self.torch.zeros(1, dtype=self.torch.float64, device=cloud.means.device)
-        self.frame = RenderOutput(ctx)
+        dev = cloud.means.device
+        self.lanes = [_Lane(torch, ctx, W * H, dev)]
+        if pipeline and len(self.mine) > 1:
+            ctx2 = Context(ctx.device, stream=torch.cuda.Stream(device=dev).cuda_stream)
+            ctx2.set_async(True)
+            self.lanes.append(_Lane(torch, ctx2, W * H, dev))
+        self.frame, self.dl, self.loss_sum = self.lanes[0].frame, self.lanes[0].dl, self.lanes[0].loss_sum
         self.iteration = 0
         self._alloc_grads()
+
+    @property
+    def contexts(self) -> List[Context]:
+        return [ln.ctx for ln in self.lanes]
 
     def _alloc_grads(self) -> None:
         torch = self.torch
@@ -121,23 +154,44 @@ class ViewShardedTrainer:
         for attempt in range(3):
             self.flat.zero_()
             self.observed.zero_()
-            self.loss_sum.zero_()
+            for ln in self.lanes:
+                ln.loss_sum.zero_()
+            start = torch.cuda.Event()
+            start.record()  # the zeroed buffers, on the caller's stream
+            for ln in self.lanes:
+                ln.stream.wait_event(start)
+            prev_bwd = None
             for k, v in enumerate(self.mine):
+                ln = self.lanes[k % len(self.lanes)]
                 cam = self.views[v]
-                render(ctx, self.cloud, cam, self.settings, out=self.frame)
-                img = self.frame.device_ptr(capi.FRAME_IMAGE)
-                # The loss stays on the device (added into loss_sum on the context's stream).
-                ctx.check(lib.odgs_photometric_loss_async(ctx.handle, C_void(img),
-                                                          C_void(self.targets[v].data_ptr()), cam.width, cam.height,
-                                                          self.cfg.lambda_ssim, C_void(self.dl.data_ptr()),
-                                                          C_void(self.loss_sum.data_ptr())))
-                backward(ctx, self.cloud, cam, self.frame, self.dl, self.settings, grads=self.grads,
-                         accumulate=True)
+                # The lane's stream is torch's current stream here, so the wrappers'
+                # stream-ordering calls are no-ops and only the events below order lanes.
+                with torch.cuda.stream(ln.stream):
+                    render(ln.ctx, self.cloud, cam, self.settings, out=ln.frame)
+                    img = ln.frame.device_ptr(capi.FRAME_IMAGE)
+                    # The loss stays on the device (added into the lane's loss sum).
+                    ln.ctx.check(ln.ctx.lib.odgs_photometric_loss_async(
+                        ln.ctx.handle, C_void(img), C_void(self.targets[v].data_ptr()), cam.width, cam.height,
+                        self.cfg.lambda_ssim, C_void(ln.dl.data_ptr()), C_void(ln.loss_sum.data_ptr())))
+                    if prev_bwd is not None:
+                        ln.stream.wait_event(prev_bwd)  # gradient accumulation in view order
+                    backward(ln.ctx, self.cloud, cam, ln.frame, ln.dl, self.settings, grads=self.grads,
+                             accumulate=True)
+                    prev_bwd = torch.cuda.Event()
+                    prev_bwd.record(ln.stream)
+            cur = torch.cuda.current_stream(self.cloud.means.device)
+            for ln in self.lanes:
+                cur.wait_stream(ln.stream)
             # Asynchronous contexts: one check point per step (deferred errors). An
             # entry-buffer overflow in any view invalidates the step's gradients: the
             # views run again, with buffers grown to the largest view's entries.
-            if not self.frame.check():
+            rerun = False
+            for ln in self.lanes:
+                rerun = ln.frame.check() or rerun
+            if not rerun:
                 break
+        if len(self.lanes) > 1:
+            self.loss_sum += self.lanes[1].loss_sum
         allreduce_grads(self.flat, self.observed, self.group)
         ctx.wait_torch()  # Adam reads the reduced gradients
         step = self.iteration + 1

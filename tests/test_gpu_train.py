@@ -227,3 +227,32 @@ def test_view_sharded_trainer_two_ranks_matches_one_process(gpu_ctx):
     # the per-rank losses add up to the single-process loss (each rank sums its views)
     for step in range(2):
         assert abs(res[0][1][step] + res[1][1][step] - losses[step]) <= 1e-12 * abs(losses[step])
+
+
+def test_pipelined_trainer_matches_sequential(gpu_ctx):
+    """pipeline=True (views alternate between two contexts / streams; the backward passes
+    stay in view order through events) gives the sequential trainer's clouds bit for bit
+    after two steps of four views; the losses agree up to the order of the two lanes'
+    float64 sums."""
+    arrs = oracle_lib.random_cloud(305, 6000)
+    host = to_cloud32(arrs)
+    W, H = 512, 256
+    from paper_2410_20686_b200 import scenes
+    views = scenes.c4_views(W, H, 4)
+    tcloud = to_cloud32(oracle_lib.random_cloud(306, 6000))
+    targets = [torch.from_numpy(render(gpu_ctx, tcloud, v, RenderSettings()).image.ravel()).cuda() for v in views]
+    out = []
+    for pipe in (False, True):
+        cloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(getattr(host, k))).cuda()
+                                for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")])
+        tr = ViewShardedTrainer(gpu_ctx, cloud, views, targets, RenderSettings(), TrainConfig(), extent=10.0,
+                                pipeline=pipe)
+        assert len(tr.lanes) == (2 if pipe else 1)
+        losses = [tr.step() for _ in range(2)]
+        torch.cuda.synchronize()
+        out.append(({k: getattr(cloud, k).cpu().numpy() for k in ("means", "rotations", "log_scales",
+                                                                   "raw_opacities", "colors")}, losses))
+    for k in out[0][0]:
+        assert np.array_equal(out[0][0][k], out[1][0][k]), k
+    for a, b in zip(out[0][1], out[1][1]):
+        assert abs(a - b) <= 1e-12 * abs(a)
