@@ -697,7 +697,7 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
     ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->dl_buf.p, dl_dimage, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, s));
     dl = ctx->dl_buf.as<float>();
   }
-  ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 9 * (size_t)K, s));
+  ODGS_CUDA(ctx, ensure(f->records, sizeof(float) * 12 * (size_t)K, s));  // kRecStride floats per entry
   ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
   ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
   ODGS_CUDA(ctx, ensure(f->bwd_work, 4 * sizeof(unsigned long long), s));

@@ -195,7 +195,7 @@ struct BwdRasterArgs {
   const float* dl_dimage;
   int width, height, tile_size, tiles_x, tiles_y, band_ty0, band_ty1;
   float alpha_clamp, cutoff_sigma;
-  float* records;    // [K][9] per tile entry, at the entry's emit position
+  float* records;    // [K][12] per tile entry (9 sums + pad), at the entry's emit position
   uint8_t* touched;  // [K] 1 where a record was written (cleared before the launch)
   const uint32_t* order;  // launch order of the band's tiles or null
   bool plain;        // un-culled reference kernel (A/B checks)

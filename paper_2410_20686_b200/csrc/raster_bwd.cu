@@ -37,6 +37,21 @@ constexpr int kBwdThreads = 256;
 constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kBwdBatch = 128;
 constexpr int kRec = 9;  // mx, my, m00, m01, m11, op, c0, c1, c2
+constexpr int kRecStride = 12;  // floats per entry record in memory: 9 sums + 3 pad (three 16-byte vectors)
+
+__device__ __forceinline__ void store_record(float* r, const float v[kRec]) {
+  float4* o = reinterpret_cast<float4*>(r);
+  o[0] = make_float4(v[0], v[1], v[2], v[3]);
+  o[1] = make_float4(v[4], v[5], v[6], v[7]);
+  o[2] = make_float4(v[8], 0.0f, 0.0f, 0.0f);
+}
+__device__ __forceinline__ void load_record(const float* r, float v[kRec]) {
+  const float4* o = reinterpret_cast<const float4*>(r);
+  const float4 a = __ldcs(o), b = __ldcs(o + 1), c = __ldcs(o + 2);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  v[8] = c.x;
+}
 
 // Backward work counters for the roofline (bench.py): entries replayed (sum over pixels
 // with a gradient of their walk, the reference's replay loop, backward.hpp:251-269) and
@@ -225,7 +240,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_raster(
       float s = 0.0f;
 #pragma unroll
       for (int w = 0; w < kBwdWarps; ++w) s += s_part[w][j][c];
-      float* r = records + (int64_t)s_pos[j] * kRec + c;
+      float* r = records + (int64_t)s_pos[j] * kRecStride + c;
       *r = (chunk > 0 && s_had[j]) ? *r + s : s;
       if (c == 0) touched[s_pos[j]] = 1;
     }
@@ -488,9 +503,7 @@ __global__ void __launch_bounds__(kBwdThreads, 4) k_bwd_raster_cull(
           }
         if (any_w) {
           const uint32_t pos = s_pos[buf ^ 1][j];
-          float* r = records + (int64_t)pos * kRec;
-#pragma unroll
-          for (int c = 0; c < kRec; ++c) r[c] = sum[c];
+          store_record(records + (int64_t)pos * kRecStride, sum);
           touched[pos] = 1;
         }
       }
@@ -817,9 +830,7 @@ __global__ void __launch_bounds__(kPipeThreads, ODGS_PIPE_MINB) k_bwd_raster_pip
             }
           if (any) {
             const uint32_t pos = sl.pos[k];
-            float* r = records + (int64_t)pos * kRec;
-#pragma unroll
-            for (int c = 0; c < kRec; ++c) r[c] = sum[c];
+            store_record(records + (int64_t)pos * kRecStride, sum);
             touched[pos] = 1;
           }
         }
@@ -1336,7 +1347,7 @@ void launch_splat_grads(int64_t n, const float4* sp_ab, const float4* sp_c, cons
 // contiguous in emit order ([off_sorted[r], +cnt_sorted[r]) for depth rank r). A warp owns
 // 32 consecutive ranks. Ranks with at most kFoldSmall records are summed by their own
 // lane, in record order; larger ranks (pole and seam splats, up to thousands of tiles)
-// are summed by the whole warp — lane l takes records l, l + 32, ... (coalesced 36-byte
+// are summed by the whole warp — lane l takes records l, l + 32, ... (coalesced 48-byte
 // records), then a fixed xor tree — so one long list no longer serialises its warp.
 // Records no warp wrote (touched == 0) are zero and skipped. Deterministic: every sum has
 // a fixed order.
@@ -1370,9 +1381,10 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const bool live = e + u < end && touched[e + u];
-        const float* rec = records + (int64_t)(e + u) * kRec;
+        if (live) load_record(records + (int64_t)(e + u) * kRecStride, v[u]);
+        else
 #pragma unroll
-        for (int c = 0; c < kRec; ++c) v[u][c] = live ? __ldcs(rec + c) : 0.0f;
+          for (int c = 0; c < kRec; ++c) v[u][c] = 0.0f;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -1398,9 +1410,10 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
       for (int u = 0; u < 4; ++u) {
         const uint32_t k = k0 + 32 * u;
         const bool live = k < bcnt && touched[boff + k];
-        const float* rec = records + (int64_t)(boff + k) * kRec;
+        if (live) load_record(records + (int64_t)(boff + k) * kRecStride, v[u]);
+        else
 #pragma unroll
-        for (int c = 0; c < kRec; ++c) v[u][c] = live ? __ldcs(rec + c) : 0.0f;
+          for (int c = 0; c < kRec; ++c) v[u][c] = 0.0f;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
