@@ -246,15 +246,22 @@ __device__ __forceinline__ bool band_tiles(float mx, float my, float radius, int
 //   margin:   delta = 64 eps kappa covers that, and the rounding of det and Sigma00
 //             (each <= 3 eps kappa); extents are inflated by (1 + 4 delta) in Q.
 // Ill-conditioned entries (delta >= 0.25) are never culled.
+// The reciprocal and square roots are the approximate MUFU ones (relative error a few
+// 1e-7); the 2e-5 relative inflation of the extents covers them.
 __device__ __forceinline__ bool cull_extents(float i00, float i01, float i11, float cutoff2, float* ex, float* ey) {
   const float det = i00 * i11 - i01 * i01;
   if (!(det > 0.0f) || !(i00 > 0.0f) || !(i11 > 0.0f)) return false;
-  const float kappa = (fmaxf(i00, i11) + fabsf(i01)) * (i00 + i11) / det;
+  float rdet;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rdet) : "f"(det));
+  const float kappa = (fmaxf(i00, i11) + fabsf(i01)) * (i00 + i11) * rdet;
   const float delta = 64.0f * 1.1920929e-7f * kappa;
   if (!(delta < 0.25f)) return false;
-  const float f = cutoff2 * (1.0f + 4.0f * delta);
-  *ex = sqrtf(i11 / det * f) * 1.00001f + 1e-4f;
-  *ey = sqrtf(i00 / det * f) * 1.00001f + 1e-4f;
+  const float f = cutoff2 * (1.0f + 4.0f * delta) * rdet;
+  float sx, sy;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sx) : "f"(i11 * f));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sy) : "f"(i00 * f));
+  *ex = sx * 1.00002f + 1e-4f;
+  *ey = sy * 1.00002f + 1e-4f;
   return true;
 }
 
