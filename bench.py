@@ -487,7 +487,8 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
     tf.destroy()
     del tcloud
     extent = float(np.sqrt(((src.means - src.means.mean(axis=1, keepdims=True)) ** 2).sum(axis=0).max()))
-    tr = ViewShardedTrainer(ctx, cloud, views, targets, settings, TrainConfig(), extent, rank, world)
+    lanes = int(os.environ.get("ODGS_TRAIN_LANES", "2"))  # A/B knob: contexts in the view pipeline
+    tr = ViewShardedTrainer(ctx, cloud, views, targets, settings, TrainConfig(), extent, rank, world, pipeline=lanes)
 
     def barrier():
         if world > 1:

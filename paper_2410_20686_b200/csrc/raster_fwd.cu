@@ -984,7 +984,10 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
 // exponential's underflow branch is dead: pm_expf_blend(x) == pm_expf_blend_core(
 // fminf(x, 88)) there, bit for bit, without a branch in the walk.
 template <bool kSmallCutoff>
-__global__ void __launch_bounds__(kBlendThreads, 7) k_blend_cull(
+#ifndef ODGS_BLEND_MINB
+#define ODGS_BLEND_MINB 7
+#endif
+__global__ void __launch_bounds__(kBlendThreads, ODGS_BLEND_MINB) k_blend_cull(
     const int32_t* __restrict__ offsets, const uint32_t* __restrict__ vals, const float4* __restrict__ sp_ab,
     const float4* __restrict__ sp_c, int width, int height, int tile_size, int tiles_x, float alpha_clamp,
     float transmittance_floor, float cutoff2, float* __restrict__ image, float* __restrict__ trans_out,

@@ -103,15 +103,15 @@ class ViewShardedTrainer:
     """C4 training step: render + photometric loss (L1 + SSIM) + backward for this rank's views, gradient
     all-reduce, Adam. Everything stays on the device.
 
-    pipeline=True: views alternate between two contexts (two streams), so view k + 1's
-    render, loss and front end run while view k's backward does; the backward passes —
+    pipeline=True (or a lane count): views alternate between two contexts (two streams), so
+    view k + 1's render, loss and front end run while view k's backward does; the backward passes —
     the only steps that touch the shared gradient buffer — stay in view order (each waits
     on the previous one's event), so the accumulated gradients are bit-identical to the
     sequential loop's."""
 
     def __init__(self, ctx: Context, cloud: GaussianCloud, views: Sequence[CameraPose], targets, settings,
                  cfg: TrainConfig, extent: float, rank: int = 0, world: int = 1, group=None,
-                 pipeline: bool = True):
+                 pipeline=True):
         import torch
         self.torch = torch
         self.ctx, self.cloud, self.views, self.targets = ctx, cloud, list(views), list(targets)
@@ -124,10 +124,11 @@ class ViewShardedTrainer:
         H, W = views[0].height, views[0].width
         dev = cloud.means.device
         self.lanes = [_Lane(torch, ctx, W * H, dev)]
-        if pipeline and len(self.mine) > 1:
-            ctx2 = Context(ctx.device, stream=torch.cuda.Stream(device=dev).cuda_stream)
-            ctx2.set_async(True)
-            self.lanes.append(_Lane(torch, ctx2, W * H, dev))
+        n_lanes = min(int(pipeline) if not isinstance(pipeline, bool) else (2 if pipeline else 1), len(self.mine))
+        for _ in range(1, n_lanes):
+            c = Context(ctx.device, stream=torch.cuda.Stream(device=dev).cuda_stream)
+            c.set_async(True)
+            self.lanes.append(_Lane(torch, c, W * H, dev))
         self.frame, self.dl, self.loss_sum = self.lanes[0].frame, self.lanes[0].dl, self.lanes[0].loss_sum
         self.iteration = 0
         self._alloc_grads()
@@ -190,8 +191,8 @@ class ViewShardedTrainer:
                 rerun = ln.frame.check() or rerun
             if not rerun:
                 break
-        if len(self.lanes) > 1:
-            self.loss_sum += self.lanes[1].loss_sum
+        for ln in self.lanes[1:]:
+            self.loss_sum += ln.loss_sum
         allreduce_grads(self.flat, self.observed, self.group)
         ctx.wait_torch()  # Adam reads the reduced gradients
         step = self.iteration + 1
