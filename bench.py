@@ -618,7 +618,8 @@ def run_train(args, ctx, rank, world, local_rank, dev, stream, lane_peak_tops, h
             "view_pipeline": f"{len(tr.lanes)} contexts (view k + 1 renders while view k back-propagates)",
             "scaling": "strong", "loss": "photometric_loss, lambda_ssim = 0.2 (L1 + SSIM on the GPU)",
             "timing": "CUDA events around the unprofiled steps (no host loss readback), max over ranks",
-            "collective": "NCCL all-reduce (sum) of 16n floats + n int32" if world > 1 else "none (1 rank)",
+            "collective": (f"{dist.get_backend().upper()} all-reduce (sum) of 16n floats + n int32" if world > 1
+                           else "none (1 rank)"),
             "stage_ms_per_step": {k: round(v, 4) for k, v in stages.items()},
             "work_per_view": {"fwd_examined": fwd_work[0] / nv, "fwd_composited": fwd_work[1] / nv,
                               "bwd_replayed": bwd_work[0] / nv, "bwd_contributions": bwd_work[1] / nv,

@@ -288,9 +288,11 @@ void launch_load_splats(int64_t n, int64_t n_splats, const float* rec, int width
 // certainly miss the band's pixel rows; they get the culled outputs and skip the exact
 // projection (binary64 transcendentals), which then runs only on the survivors. The box
 // half-height is at most rb = cutoff * sqrt(lambda_max(Sigma_2D)) <= cutoff *
-// sqrt(s_max^2 ||J||_F^2 + lowpass) (Sigma_2D = J R Sigma R^T J^T + lowpass I,
-// lambda_max(Sigma) = s_max^2), with ||J||_F^2 = (W/2pi sec/r)^2 + (H/pi/r)^2
-// (projection.hpp:75-96), padded by 1% and 2 pixels. The test runs in the sine domain,
+// sqrt(s_max^2 lambda_max(J J^T) + lowpass) (Sigma_2D = J Sigma J^T + lowpass I,
+// lambda_max(Sigma) = s_max^2). J's rows are a0 = W/2pi sec/r and a1 = H/pi/r times two
+// orthonormal rows of the tangent-frame rotation (projection.hpp:75-96), so J J^T =
+// diag(a0^2, a1^2) and lambda_max(J J^T) = max(a0^2, a1^2); padded by 1% and 2 pixels.
+// The test runs in the sine domain,
 // with no inverse trigonometry: the centre row v = H/2 - H theta/pi lies above the band
 // by more than rb iff theta > theta_top + rb pi/H iff sin(theta) = -mu_y/|mu| > sin(that)
 // (both angles inside (-pi/2, pi/2)), likewise below. The fast-math errors (~1e-6 rad)
@@ -335,7 +337,7 @@ __device__ __forceinline__ bool band_survives_v(const float p[3], const float q[
   const float sec = fminf(depth / rho, b.sec_max);
   const float a0 = b.a0k * sec * inv_d, a1 = b.a1k * inv_d;
   const float smax = __expf(fmaxf(ls[0], fmaxf(ls[1], ls[2])));
-  const float rb = s.cutoff_sigma * sqrtf(smax * smax * (a0 * a0 + a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
+  const float rb = s.cutoff_sigma * sqrtf(smax * smax * fmaxf(a0 * a0, a1 * a1) + s.lowpass_dilation) * 1.01f + 2.0f;
   const float rt = rb * b.rad_per_px;
   if (!(rt < 1.0f)) return true;
   float sr, cr;

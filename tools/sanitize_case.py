@@ -1,6 +1,6 @@
 """Small workloads for compute-sanitizer (racecheck / synccheck / memcheck): every kernel
 of the render, backward, band, async and training paths at sizes the instrumented run
-finishes in minutes. `python tools/sanitize_case.py [small|bigsort]`."""
+finishes in minutes. `python tools/sanitize_case.py [small|bigsort|train]`."""
 import sys
 from pathlib import Path
 
@@ -53,5 +53,16 @@ if mode == "small":
     grad = torch.empty_like(img)
     ctx.check(ctx.lib.odgs_photometric_loss(ctx.handle, C.c_void_p(img.data_ptr()), C.c_void_p(tgt.data_ptr()),
                                             W, H, 0.2, C.c_void_p(grad.data_ptr()), C.byref(loss)))
+if mode == "train":
+    # the two-stream view pipeline of the trainer (four views, two steps): loss, Adam and
+    # the backward passes accumulating into one buffer from two contexts
+    from paper_2410_20686_b200.train import TrainConfig, ViewShardedTrainer
+    views = scenes.c4_views(W, H, 4)
+    targets = [img_t for img_t in (torch.from_numpy(render(ctx, cloud, scenes.yaw_camera(0.3 * k, W, H), s).image
+                                                    .ravel()).to(dev) for k in range(4))]
+    tr = ViewShardedTrainer(ctx, cloud, views, targets, s, TrainConfig(), extent=10.0, pipeline=2)
+    assert len(tr.lanes) == 2
+    for _ in range(2):
+        tr.step()
 torch.cuda.synchronize()
 print("ok", mode)
