@@ -126,9 +126,12 @@ class ViewShardedTrainer:
         self.lanes = [_Lane(torch, ctx, W * H, dev)]
         n_lanes = min(int(pipeline) if not isinstance(pipeline, bool) else (2 if pipeline else 1), len(self.mine))
         for _ in range(1, n_lanes):
-            c = Context(ctx.device, stream=torch.cuda.Stream(device=dev).cuda_stream)
+            st = torch.cuda.Stream(device=dev)
+            c = Context(ctx.device, stream=st.cuda_stream)
             c.set_async(True)
-            self.lanes.append(_Lane(torch, c, W * H, dev))
+            ln = _Lane(torch, c, W * H, dev)
+            ln.stream = st  # the lane's torch stream (kept alive with the lane)
+            self.lanes.append(ln)
         self.frame, self.dl, self.loss_sum = self.lanes[0].frame, self.lanes[0].dl, self.lanes[0].loss_sum
         self.iteration = 0
         self._alloc_grads()
