@@ -88,6 +88,7 @@ struct odgs_frame {
   // check point and re-rendered with room for them.
   uint32_t k_cap = 0;
   bool pending = false;      // enqueued work whose error words / counts are not read yet
+  bool cap_path = false;     // the last render ran on the capacity path (entry count on the device)
   bool bwd_pending = false;  // a backward whose error words are not read yet
   // The last render request, for the re-run after an overflow (pointers are the caller's).
   struct Request {
@@ -595,6 +596,7 @@ odgs_status bin_impl(odgs_ctx* ctx, odgs_frame* f, bool band) {
   // Later renders of this frame run on the capacity path.
   f->k_cap = n > 0 ? std::max<uint32_t>(cap, 1u) : f->k_cap;
   f->pending = !exact;
+  f->cap_path = !exact;
   f->prepared = true;
   return ok(ctx);
 }
@@ -734,9 +736,12 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
     StageScope sc(ctx, ODGS_STAGE_BWD_SPLAT);
     // A band's sorted ranks are counted on the device (capacity path: n_sorted = n).
     const uint32_t* m_dev = f->band ? reinterpret_cast<const uint32_t*>(&f->d_err->n_band) : nullptr;
+    // Capacity path: records exist only below the sorted entry count (an overflowed frame
+    // is re-rendered at its check point; until then its fold must stay inside the buffers).
+    const unsigned long long* k_lim = f->cap_path ? &f->d_err->k_sort : nullptr;
     launch_fold_records(f->n_sorted, f->vals[f->depth_which].as<uint32_t>(), f->cnt_sorted.as<uint32_t>(),
                         f->off_sorted.as<uint32_t>(), f->touched.as<uint8_t>(), f->records.as<float>(),
-                        f->folded.as<float>(), s, m_dev);
+                        f->folded.as<float>(), s, m_dev, k_lim);
   }
   ODGS_CUDA(ctx, cudaGetLastError());
   return ODGS_OK;

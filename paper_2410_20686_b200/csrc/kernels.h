@@ -206,9 +206,11 @@ void launch_bwd_raster(const BwdRasterArgs& a, cudaStream_t stream);
 // Ordered per-Gaussian fold of the entry records (backward.hpp:310-327), one thread per
 // depth rank so a warp reads one contiguous record range: folded[g][9] for every
 // Gaussian with entries.
+// k_limit (capacity path): records at emit positions >= *k_limit were not written.
 void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
                          const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
-                         cudaStream_t stream, const uint32_t* n_dev = nullptr);
+                         cudaStream_t stream, const uint32_t* n_dev = nullptr,
+                         const unsigned long long* k_limit = nullptr);
 
 // SplatGrads of every projected Gaussian from the folded records (grad_pixels_to_splats).
 void launch_splat_grads(int64_t n, const float4* sp_ab, const float4* sp_c, const uint32_t* cnt, const float* folded,

@@ -1362,9 +1362,10 @@ __device__ __forceinline__ void fold_add(const float* __restrict__ rec, float ac
 __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
     int64_t n, const uint32_t* __restrict__ sorted_idx, const uint32_t* __restrict__ cnt_sorted,
     const uint32_t* __restrict__ off_sorted, const uint8_t* __restrict__ touched, const float* __restrict__ records,
-    float* __restrict__ folded, const uint32_t* __restrict__ n_dev) {
+    float* __restrict__ folded, const uint32_t* __restrict__ n_dev, const unsigned long long* __restrict__ k_limit) {
   pdl_wait();
   if (n_dev) n = min(n, (int64_t)*n_dev);  // a band's ranks counted on the device
+  const uint32_t kmax = k_limit ? (uint32_t)min(*k_limit, 0xFFFFFFFFull) : 0xFFFFFFFFu;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = ((int64_t)blockIdx.x * kFoldWarps + warp) * 32;
   if (r0 >= n) return;
@@ -1375,7 +1376,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
   // small ranks: the lane's own records, in order, four in flight at a time
   if (cnt > 0 && cnt <= kFoldSmall) {
     float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    const uint32_t end = off + cnt;
+    const uint32_t end = min(off + cnt, max(off, kmax));
     for (uint32_t e = off; e < end; e += 4) {
       float v[4][kRec];
 #pragma unroll
@@ -1401,7 +1402,7 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
     const int src = __ffs(big) - 1;
     big &= big - 1;
     const uint32_t boff = __shfl_sync(0xffffffffu, off, src);
-    const uint32_t bcnt = __shfl_sync(0xffffffffu, cnt, src);
+    const uint32_t bcnt = min(__shfl_sync(0xffffffffu, cnt, src), boff < kmax ? kmax - boff : 0u);
     const uint32_t bg = __shfl_sync(0xffffffffu, g, src);
     float acc[kRec] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (uint32_t k0 = lane; k0 < bcnt; k0 += 4 * 32) {  // four records in flight per lane
@@ -1435,11 +1436,11 @@ __global__ void __launch_bounds__(kFoldWarps * 32) k_fold_records(
 
 void launch_fold_records(int64_t n, const uint32_t* sorted_idx, const uint32_t* cnt_sorted,
                          const uint32_t* off_sorted, const uint8_t* touched, const float* records, float* folded,
-                         cudaStream_t stream, const uint32_t* n_dev) {
+                         cudaStream_t stream, const uint32_t* n_dev, const unsigned long long* k_limit) {
   if (n == 0) return;
   const int64_t warps = (n + 31) / 32;
   launch_pdl(k_fold_records, (unsigned)((warps + kFoldWarps - 1) / kFoldWarps), kFoldWarps * 32, 0, stream, n,
-             sorted_idx, cnt_sorted, off_sorted, touched, records, folded, n_dev);
+             sorted_idx, cnt_sorted, off_sorted, touched, records, folded, n_dev, k_limit);
   ++g_launches;
 }
 

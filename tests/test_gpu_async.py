@@ -134,3 +134,35 @@ def test_async_backward_and_bands_equal_sync(gpu_ctx):
             render_band(actx, c, cam, s, r0, r0 + 128, out=bf)
             assert np.array_equal(bf.image[:, :, r0:r0 + 128], full[:, :, r0:r0 + 128]), (it, r0)
     actx.close()
+
+
+def test_async_backward_on_overflowed_frame_is_memory_safe(gpu_ctx):
+    """A backward enqueued on a frame whose render overflowed its entry buffers (before the
+    check point) must stay inside the buffers: the fold clamps its record ranges to the
+    entries actually sorted. After the check re-renders the frame, the backward equals the
+    synchronous one bit for bit."""
+    n = 60_000
+    base = scenes.cloud_c3(n)
+    arrs = [np.array(getattr(base, k)) for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")]
+    small = [a.copy() for a in arrs]
+    small[2] = small[2] - 3.0
+    s = RenderSettings()
+    cam = CameraPose(1024, 512)
+    actx = Context(0)
+    actx.set_async(True)
+    fr = RenderOutput(actx)
+    render(actx, dev_cloud(GaussianCloud(*small)), cam, s, out=fr)
+    big = dev_cloud(GaussianCloud(*arrs))
+    dl = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, 3 * 1024 * 512).astype(np.float32)).cuda()
+    z = lambda *sh: torch.zeros(sh, dtype=torch.float32, device="cuda")
+    g = GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n), torch.zeros(n, dtype=torch.int32,
+                                                                                      device="cuda"))
+    render(actx, big, cam, s, out=fr)
+    backward(actx, big, cam, fr, dl, s, grads=g)  # on the overflowed frame
+    assert fr.check()  # re-rendered
+    backward(actx, big, cam, fr, dl, s, grads=g)
+    torch.cuda.synchronize()
+    ref = backward(gpu_ctx, big, cam, render(gpu_ctx, big, cam, s), dl, s)
+    for k in ("means", "rotations", "log_scales", "raw_opacities", "colors", "observed"):
+        assert np.array_equal(getattr(g, k).cpu().numpy(), getattr(ref, k)), k
+    actx.close()

@@ -11,7 +11,7 @@ import torch
 
 import oracle_lib
 from helpers import to_cloud32
-from paper_2410_20686_b200 import CameraPose, GaussianCloud, GradBuffers, RenderSettings, backward, render
+from paper_2410_20686_b200 import CameraPose, Context, GaussianCloud, GradBuffers, RenderSettings, backward, render
 from paper_2410_20686_b200 import _capi as capi
 from paper_2410_20686_b200.train import TrainConfig, ViewShardedTrainer, means_lr_at
 
@@ -256,3 +256,39 @@ def test_pipelined_trainer_matches_sequential(gpu_ctx):
         assert np.array_equal(out[0][0][k], out[1][0][k]), k
     for a, b in zip(out[0][1], out[1][1]):
         assert abs(a - b) <= 1e-12 * abs(a)
+
+
+def test_pipelined_trainer_overflow_rerun_matches_sequential(gpu_ctx):
+    """A step whose views need more tile entries than the lanes' frames were sized for
+    (log-scales grown by 2 after the first step): both lanes' check points report the
+    overflow, the step runs again with grown buffers, and the pipelined trainer still
+    ends with the sequential trainer's cloud bit for bit."""
+    arrs = oracle_lib.random_cloud(307, 5000)
+    host = to_cloud32(arrs)
+    W, H = 512, 256
+    from paper_2410_20686_b200 import scenes
+    views = scenes.c4_views(W, H, 4)
+    tcloud = to_cloud32(oracle_lib.random_cloud(308, 5000))
+    targets = [torch.from_numpy(render(gpu_ctx, tcloud, v, RenderSettings()).image.ravel()).cuda() for v in views]
+    out = []
+    for pipe in (False, True):
+        ls = np.ascontiguousarray(host.log_scales) - 2.0  # small splats: few entries per view
+        cloud = GaussianCloud(*[torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                                for a in (host.means, host.rotations, ls, host.raw_opacities, host.colors)])
+        ctx = Context(0)
+        ctx.set_async(True)
+        tr = ViewShardedTrainer(ctx, cloud, views, targets, RenderSettings(), TrainConfig(), extent=10.0,
+                                pipeline=pipe)
+        tr.step()
+        k0 = [ln.frame.info().n_entries for ln in tr.lanes]
+        with torch.no_grad():
+            cloud.log_scales += 2.0  # many more entries than the frames hold
+        tr.step()
+        torch.cuda.synchronize()
+        k1 = [ln.frame.info().n_entries for ln in tr.lanes]
+        assert all(b > 2 * a for a, b in zip(k0, k1)), (k0, k1)
+        out.append({k: getattr(cloud, k).cpu().numpy() for k in ("means", "rotations", "log_scales",
+                                                                  "raw_opacities", "colors")})
+        ctx.close()
+    for k in out[0]:
+        assert np.array_equal(out[0][k], out[1][k]), k

@@ -1,6 +1,6 @@
 """Small workloads for compute-sanitizer (racecheck / synccheck / memcheck): every kernel
 of the render, backward, band, async and training paths at sizes the instrumented run
-finishes in minutes. `python tools/sanitize_case.py [small|bigsort|train]`."""
+finishes in minutes. `python tools/sanitize_case.py [small|bigsort|train|overflow]`."""
 import sys
 from pathlib import Path
 
@@ -53,6 +53,19 @@ if mode == "small":
     grad = torch.empty_like(img)
     ctx.check(ctx.lib.odgs_photometric_loss(ctx.handle, C.c_void_p(img.data_ptr()), C.c_void_p(tgt.data_ptr()),
                                             W, H, 0.2, C.c_void_p(grad.data_ptr()), C.byref(loss)))
+if mode == "overflow":
+    # a backward enqueued on an asynchronous frame whose render overflowed its entry
+    # buffers (before the check point): the fold must stay inside the record buffers
+    actx = Context(0)
+    actx.set_async(True)
+    fo = RenderOutput(actx)
+    small = GaussianCloud(cloud.means, cloud.rotations, cloud.log_scales - 3.0, cloud.raw_opacities, cloud.colors)
+    render(actx, small, cam, s, out=fo)
+    render(actx, cloud, cam, s, out=fo)
+    backward(actx, cloud, cam, fo, dl, s, grads=g)
+    assert fo.check()
+    backward(actx, cloud, cam, fo, dl, s, grads=g)
+    actx.close()
 if mode == "train":
     # the two-stream view pipeline of the trainer (four views, two steps): loss, Adam and
     # the backward passes accumulating into one buffer from two contexts
