@@ -12,6 +12,8 @@
 //                 staged in shared memory and CTA-wide early exit (rasterizer.hpp:211-267)
 //
 // Compiled with --fmad=false: see common.cuh for the numerics contract.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -465,18 +467,38 @@ __global__ void __launch_bounds__(256, 3) k_band_preprocess(
   }
 }
 
-// The same pass for SH degree 0 clouds with n % 4 == 0 and 16-byte aligned rows, at HBM
-// speed: lane l takes the four consecutive rows 4l..4l+3 of each group of 128 with one
-// 16-byte load per parameter row (14 loads per lane in flight); the pre-cull runs on the
+// The same pass for SH degree 0 clouds with n % 4 == 0 and 16-byte aligned rows: lane l
+// takes kRows consecutive rows (default 2: one 8-byte load per parameter row, 14 loads
+// per lane in flight, 64 + registers at 6 CTAs/SM; 4 rows with 16-byte loads need 111
+// registers, 4 CTAs/SM, and are 6 % slower at C5); the pre-cull runs on the
 // loaded values, and each survivor is queued with its 14 parameters, so the exact path
 // reads shared memory instead of re-gathering the row (scattered survivor rows would cost
 // a 32-byte sector per 4-byte parameter). Survivors are queued in index order (a warp
 // prefix sum over the lanes' counts); the group's cnt / sp_c are cleared with vector
 // stores first (the exact path overwrites the survivors' after the __syncwarp).
+#ifndef ODGS_BANDVEC_ROWS
+#define ODGS_BANDVEC_ROWS 2
+#endif
+#ifndef ODGS_BANDVEC_MINB
+#define ODGS_BANDVEC_MINB 6
+#endif
 constexpr int kBandVecWarps = 4;
-constexpr uint32_t kBandVecQueue = 160;  // >= 31 + 128
 
-__global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
+// kRows consecutive rows per lane (float4: 4, float2: 2); the queue holds a warp's
+// leftover survivors (< 32) plus one group of 32 kRows rows.
+template <int kRows>
+struct BandVec {
+  static constexpr uint32_t kQueue = 32 + 32 * kRows;
+  using V = typename std::conditional<kRows == 4, float4, typename std::conditional<kRows == 2, float2, float>::type>::type;
+  __device__ static float el(const V& v, int u) {
+    if constexpr (kRows == 4) return u == 0 ? v.x : u == 1 ? v.y : u == 2 ? v.z : v.w;
+    else if constexpr (kRows == 2) return u == 0 ? v.x : v.y;
+    else return v;
+  }
+};
+
+template <int kRows, int kMinBlocks>
+__global__ void __launch_bounds__(kBandVecWarps * 32, kMinBlocks) k_band_preprocess_vec(
     int64_t n, const float* __restrict__ means, const float* __restrict__ rotations,
     const float* __restrict__ log_scales, const float* __restrict__ raw_opacities,
     const float* __restrict__ colors, DevCamera cam, DevSettings s, float4* __restrict__ sp_ab,
@@ -484,8 +506,12 @@ __global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
     uint32_t* __restrict__ vals, uint32_t* __restrict__ cnt, DevErrors* __restrict__ err,
     uint32_t* __restrict__ seg_keys, uint32_t* __restrict__ seg_vals, uint32_t* __restrict__ seg_count) {
   pdl_wait();
-  __shared__ uint32_t s_idx[kBandVecWarps][kBandVecQueue];
-  __shared__ float s_val[kBandVecWarps][14][kBandVecQueue];
+  using BV = BandVec<kRows>;
+  using V = typename BV::V;
+  constexpr uint32_t kQ = BV::kQueue;
+  constexpr int kGroup = 32 * kRows;
+  __shared__ uint32_t s_idx[kBandVecWarps][kQ];
+  __shared__ float s_val[kBandVecWarps][14][kQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t w = (int64_t)blockIdx.x * kBandVecWarps + warp;
   const int64_t base = w * kBandWarpChunk;
@@ -499,7 +525,7 @@ __global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
     bool visible = false, has = false;
     uint32_t key = 0, idx = 0;
     if (lane < count) {
-      const uint32_t slot = (head + lane) % kBandVecQueue;
+      const uint32_t slot = (head + lane) % kQ;
       idx = s_idx[warp][slot];
       float v[14];
 #pragma unroll
@@ -521,17 +547,16 @@ __global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
   const float* rows[14] = {means,     means + n,          means + 2 * n,      rotations,          rotations + n,
                            rotations + 2 * n, rotations + 3 * n, log_scales,  log_scales + n,     log_scales + 2 * n,
                            raw_opacities, colors,         colors + n,         colors + 2 * n};
-  for (int64_t c = base; c < end; c += 128) {
-    const int64_t i0 = c + 4 * lane;
-    const bool any = i0 < end;  // end - base is a multiple of 4
-    float4 v[14];
+  for (int64_t c = base; c < end; c += kGroup) {
+    const int64_t i0 = c + kRows * lane;
+    const bool any = i0 < end;  // end - base is a multiple of kRows
+    V v[14];
 #pragma unroll
-    for (int k = 0; k < 14; ++k)
-      v[k] = any ? __ldcs(reinterpret_cast<const float4*>(rows[k] + i0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < 14; ++k) v[k] = any ? __ldcs(reinterpret_cast<const V*>(rows[k] + i0)) : V{};
     uint32_t m = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      auto el = [&](int k) { return u == 0 ? v[k].x : u == 1 ? v[k].y : u == 2 ? v[k].z : v[k].w; };
+    for (int u = 0; u < kRows; ++u) {
+      auto el = [&](int k) { return BV::el(v[k], u); };
       const float p[3] = {el(0), el(1), el(2)};
       const float qv[4] = {el(3), el(4), el(5), el(6)};
       const float ls[3] = {el(7), el(8), el(9)};
@@ -541,9 +566,11 @@ __global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
       if (any && band_survives_v(p, qv, ls, fin, cam, s, bc)) m |= 1u << u;
     }
     if (any) {
-      reinterpret_cast<uint4*>(cnt + i0)[0] = make_uint4(0u, 0u, 0u, 0u);
+      if constexpr (kRows == 4) reinterpret_cast<uint4*>(cnt + i0)[0] = make_uint4(0u, 0u, 0u, 0u);
+      else if constexpr (kRows == 2) reinterpret_cast<uint2*>(cnt + i0)[0] = make_uint2(0u, 0u);
+      else cnt[i0] = 0u;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) sp_c[i0 + u] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
+      for (int u = 0; u < kRows; ++u) sp_c[i0 + u] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(0u));
     }
     const uint32_t cnt_l = __popc(m);
     uint32_t incl = cnt_l;
@@ -554,13 +581,12 @@ __global__ void __launch_bounds__(kBandVecWarps * 32, 4) k_band_preprocess_vec(
     }
     uint32_t pos = tail + incl - cnt_l;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kRows; ++u)
       if (m & (1u << u)) {
-        const uint32_t slot = pos % kBandVecQueue;
+        const uint32_t slot = pos % kQ;
         s_idx[warp][slot] = (uint32_t)(i0 + u);
 #pragma unroll
-        for (int k = 0; k < 14; ++k)
-          s_val[warp][k][slot] = u == 0 ? v[k].x : u == 1 ? v[k].y : u == 2 ? v[k].z : v[k].w;
+        for (int k = 0; k < 14; ++k) s_val[warp][k][slot] = BV::el(v[k], u);
         ++pos;
       }
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
@@ -610,7 +636,8 @@ void launch_band_preprocess(const PreprocessArgs& a, uint32_t* seg_keys, uint32_
   const bool vec = a.sh_degree == 0 && a.n % 4 == 0 && aligned(a.means) && aligned(a.rotations) &&
                    aligned(a.log_scales) && aligned(a.raw_opacities) && aligned(a.colors);
   if (vec) {
-    launch_pdl(k_band_preprocess_vec, (unsigned)((n_seg + kBandVecWarps - 1) / kBandVecWarps), kBandVecWarps * 32, 0,
+    launch_pdl(k_band_preprocess_vec<ODGS_BANDVEC_ROWS, ODGS_BANDVEC_MINB>,
+               (unsigned)((n_seg + kBandVecWarps - 1) / kBandVecWarps), kBandVecWarps * 32, 0,
                stream, a.n, a.means, a.rotations, a.log_scales, a.raw_opacities, a.colors, a.cam, a.settings, a.sp_ab,
                a.sp_c, a.cov_out, a.keys, a.vals, a.cnt, a.err, seg_keys, seg_vals, seg_count);
     ++g_launches;
