@@ -166,3 +166,42 @@ def test_async_backward_on_overflowed_frame_is_memory_safe(gpu_ctx):
     for k in ("means", "rotations", "log_scales", "raw_opacities", "colors", "observed"):
         assert np.array_equal(getattr(g, k).cpu().numpy(), getattr(ref, k)), k
     actx.close()
+
+
+def test_async_random_sequence_equals_sync(gpu_ctx):
+    """A random sequence of clouds (sizes 0 to 40K, log-scales shifted by -3 to +1.5, so the
+    entry count jumps up and down past the frame's capacity) rendered and back-propagated
+    on one asynchronous frame, checked after every step against the synchronous path."""
+    rng = np.random.default_rng(42)
+    base = scenes.cloud_c3(40_000)
+    arrs = [np.array(getattr(base, k)) for k in ("means", "rotations", "log_scales", "raw_opacities", "colors")]
+    s = RenderSettings()
+    actx = Context(0)
+    actx.set_async(True)
+    fr = RenderOutput(actx)
+    W, H = 512, 256
+    for step in range(10):
+        n = int(rng.choice([0, 1, 37, 5000, 40_000]))
+        sub = [a[..., :n].copy() for a in arrs]
+        sub[2] = sub[2] + float(rng.uniform(-3.0, 1.5))
+        cloud = dev_cloud(GaussianCloud(*sub))
+        cam = scenes.yaw_camera(float(rng.uniform(0, 6.28)), W, H)
+        render(actx, cloud, cam, s, out=fr)
+        dl = torch.from_numpy(rng.uniform(-1, 1, 3 * W * H).astype(np.float32)).cuda()
+        z = lambda *sh: torch.zeros(sh, dtype=torch.float32, device="cuda")
+        g = GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n),
+                        torch.zeros(n, dtype=torch.int32, device="cuda"))
+        backward(actx, cloud, cam, fr, dl, s, grads=g)
+        if fr.check():  # re-rendered: the backward ran on the overflowed frame; repeat it
+            g = GradBuffers(z(3, n), z(4, n), z(3, n), z(n), z(3, n), z(n), z(n),
+                            torch.zeros(n, dtype=torch.int32, device="cuda"))
+            backward(actx, cloud, cam, fr, dl, s, grads=g)
+        torch.cuda.synchronize()
+        ref_fr = render(gpu_ctx, cloud, cam, s)
+        for a, b in zip(fields(fr), fields(ref_fr)):
+            assert np.array_equal(a, b), step
+        if n:
+            ref = backward(gpu_ctx, cloud, cam, ref_fr, dl, s)
+            for k in ("means", "colors", "observed"):
+                assert np.array_equal(getattr(g, k).cpu().numpy(), getattr(ref, k)), (step, k)
+    actx.close()
