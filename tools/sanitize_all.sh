@@ -1,4 +1,7 @@
-cd /root/repo
+#!/bin/bash
+# compute-sanitizer over the product kernels (tools/sanitize_case.py small / train) and a
+# 2-rank shared-GPU bench run; outputs under gpurun_out/san_final/.
+cd "$(dirname "$0")/.."
 D=gpurun_out/san_final; mkdir -p $D
 for tool in racecheck synccheck memcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_case.py small > $D/small_$tool.txt 2>&1; tail -3 $D/small_$tool.txt
