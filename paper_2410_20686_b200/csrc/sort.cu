@@ -173,9 +173,37 @@ __global__ void __launch_bounds__(kThreads) k_onesweep_hist(const uint32_t* __re
   __shared__ uint32_t s_cnt[kMaxPasses][256];
   for (int k = threadIdx.x; k < kMaxPasses * 256; k += kThreads) (&s_cnt[0][0])[k] = 0;
   __syncthreads();
+  // Four consecutive keys per thread and step (one 16-byte load, two in flight), each
+  // pass's digits merged into runs before the shared adds: consecutive tile entries of
+  // one Gaussian share their tile row, and the high depth digits few values.
+  const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15u) == 0;
+  const int64_t n4 = aligned ? n >> 2 : 0;
+  const uint4* keys4 = reinterpret_cast<const uint4*>(keys);
   const int64_t stride = (int64_t)gridDim.x * kThreads;
-  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
-    const uint32_t key = keys[i];
+  auto count4 = [&](const uint4 q) {
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p) {
+      if (p < plan.n_passes) {
+        const uint32_t m = (1u << plan.bits[p]) - 1u;
+        const int sh = plan.shift[p];
+        const uint32_t d0 = (q.x >> sh) & m, d1 = (q.y >> sh) & m, d2 = (q.z >> sh) & m, d3 = (q.w >> sh) & m;
+        uint32_t cur = d0, c = 1;
+        if (d1 == cur) ++c; else { atomicAdd(&s_cnt[p][cur], c); cur = d1; c = 1; }
+        if (d2 == cur) ++c; else { atomicAdd(&s_cnt[p][cur], c); cur = d2; c = 1; }
+        if (d3 == cur) ++c; else { atomicAdd(&s_cnt[p][cur], c); cur = d3; c = 1; }
+        atomicAdd(&s_cnt[p][cur], c);
+      }
+    }
+  };
+  int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  for (; i + stride < n4; i += 2 * stride) {
+    const uint4 a = keys4[i], b = keys4[i + stride];  // default policy: the passes re-read them
+    count4(a);
+    count4(b);
+  }
+  for (; i < n4; i += stride) count4(keys4[i]);
+  for (int64_t t = 4 * n4 + (int64_t)blockIdx.x * kThreads + threadIdx.x; t < n; t += stride) {
+    const uint32_t key = keys[t];
 #pragma unroll
     for (int p = 0; p < kMaxPasses; ++p)
       if (p < plan.n_passes) atomicAdd(&s_cnt[p][(key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u)], 1u);
