@@ -847,19 +847,25 @@ __device__ __forceinline__ int order_bucket(int32_t len) {
 __global__ void __launch_bounds__(kOrderThreads) k_tile_order(const int32_t* __restrict__ offsets, int tile_base,
                                                               int n, uint32_t* __restrict__ order) {
   pdl_wait();
-  __shared__ uint32_t s_cnt[kOrderBuckets];
+  __shared__ __align__(16) uint32_t s_cnt[kOrderBuckets];
   for (int b = threadIdx.x; b < kOrderBuckets; b += kOrderThreads) s_cnt[b] = 0;
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += kOrderThreads)
     atomicAdd(&s_cnt[order_bucket(offsets[tile_base + t + 1] - offsets[tile_base + t])], 1u);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t acc = 0;
-    for (int b = 0; b < kOrderBuckets; ++b) {
-      const uint32_t c = s_cnt[b];
-      s_cnt[b] = acc;
-      acc += c;
+  if (threadIdx.x < 32) {  // exclusive scan of the buckets: 4 per lane, then over the warp
+    static_assert(kOrderBuckets == 128, "4 buckets per lane");
+    const int lane = threadIdx.x;
+    const uint4 c = *reinterpret_cast<const uint4*>(&s_cnt[4 * lane]);
+    const uint32_t own = c.x + c.y + c.z + c.w;
+    uint32_t incl = own;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
     }
+    const uint32_t e = incl - own;
+    *reinterpret_cast<uint4*>(&s_cnt[4 * lane]) = make_uint4(e, e + c.x, e + c.x + c.y, e + c.x + c.y + c.z);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += kOrderThreads)

@@ -269,14 +269,13 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
   const int64_t base = tile_base + (int64_t)warp * kWI;
   const int wbase = warp * kWI;  // tile-relative
   const uint32_t lt_mask = (1u << lane) - 1u;
-  uint32_t key[IPT], val[IPT], rank[IPT];
-  // All loads first, so the tile's loads per thread are in flight together.
+  uint32_t key[IPT], rank[IPT];  // the values are loaded at the shared-memory scatter
+  // All key loads first, so the tile's loads per thread are in flight together.
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
     const int64_t idx = base + j * 32 + lane;
     const bool ok = wbase + j * 32 + lane < valid_count;
     key[j] = ok ? __ldcs(keys_in + idx) : 0u;
-    val[j] = ok ? __ldcs(vals_in + idx) : 0u;
   }
 #pragma unroll
   for (int j = 0; j < IPT; ++j) {
@@ -329,7 +328,7 @@ __global__ void __launch_bounds__(Threads, MinBlocks) k_onesweep_pass(
     const uint32_t d = wbase + j * 32 + lane < valid_count ? (key[j] >> shift) & mask : mask;
     const uint32_t pos = s_start[d] + s_wcnt[warp][d] + rank[j];
     s_keys[pos] = key[j];
-    s_vals[pos] = val[j];
+    if (wbase + j * 32 + lane < valid_count) s_vals[pos] = __ldcs(vals_in + base + j * 32 + lane);
   }
   if (d_own < radix) {
     const int d = d_own;
