@@ -118,10 +118,59 @@ struct SsimWindow {
 
 // Two tiled kernels, each doing both separable passes in shared memory (no full-size
 // intermediate maps): a tile covers kSsimTY rows (y, contiguous) x kSsimTX columns (x)
-// of its output grid plus the 10-pixel halo of the 11-tap window.
-constexpr int kSsimTY = 56, kSsimTX = 16;
+// of its output grid plus the 10-pixel halo of the 11-tap window. Each thread computes
+// kSsimG = 4 neighbouring outputs of a pass from one sliding run of 14 inputs (the loads
+// and the moment products shared), with FMAs: the loss is tolerance-checked against the
+// fp64 oracle, not part of the bit-exact contract.
+constexpr int kSsimTY = 56, kSsimTX = 16, kSsimG = 4;
 constexpr int kSsimIY = kSsimTY + 10, kSsimIX = kSsimTX + 10;
+constexpr int kSsimHY = kSsimIY + 2;  // horizontal-pass rows padded to a float4 multiple
 constexpr int kSsimThreads = 256;
+static_assert(kSsimTX % kSsimG == 0 && kSsimTY % kSsimG == 0 && kSsimHY % 4 == 0, "tile shape");
+static_assert(kSsimTY - kSsimG + 16 <= kSsimHY, "the vertical pass's float4 runs stay in the row");
+
+// Horizontal pass of one row iy: the 11-tap correlations of NQ input planes at the
+// kSsimG columns tx0 .. tx0 + 3 (inputs tx0 .. tx0 + 13).
+template <int NQ, class Load>
+__device__ __forceinline__ void ssim_hpass(const SsimWindow& win, Load load, float m[kSsimG][NQ]) {
+#pragma unroll
+  for (int o = 0; o < kSsimG; ++o)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) m[o][q] = 0.0f;
+#pragma unroll
+  for (int j = 0; j < kSsimG + 10; ++j) {
+    float v[NQ];
+    load(j, v);
+#pragma unroll
+    for (int o = 0; o < kSsimG; ++o) {
+      const int i = j - o;
+      if (i >= 0 && i < 11)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) m[o][q] = fmaf(win.w[i], v[q], m[o][q]);
+    }
+  }
+}
+
+// Vertical pass of column tx: the 11-tap correlations of row run ty0 .. ty0 + 13 of one
+// horizontal-result plane at the kSsimG rows ty0 .. ty0 + 3 (four float4 loads).
+__device__ __forceinline__ void ssim_vpass(const SsimWindow& win, const float* row, float out[kSsimG]) {
+  float in[16];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float4 t = reinterpret_cast<const float4*>(row)[r];
+    in[4 * r] = t.x;
+    in[4 * r + 1] = t.y;
+    in[4 * r + 2] = t.z;
+    in[4 * r + 3] = t.w;
+  }
+#pragma unroll
+  for (int o = 0; o < kSsimG; ++o) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 11; ++i) acc = fmaf(win.w[i], in[o + i], acc);
+    out[o] = acc;
+  }
+}
 
 // Forward: per window (metrics.hpp:106-122) the five windowed moments of (a, b) —
 // horizontal 11-tap correlation then vertical — the SSIM value (block partial sums)
@@ -131,7 +180,7 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const float* __restri
                                                            float* __restrict__ gmaps, double* __restrict__ partial) {
   pdl_wait();
   __shared__ float s_a[kSsimIX][kSsimIY], s_b[kSsimIX][kSsimIY];
-  __shared__ float s_h[5][kSsimTX][kSsimIY];
+  __shared__ __align__(16) float s_h[5][kSsimTX][kSsimHY];
   __shared__ double s_w[kSsimThreads / 32];
   const int Ho = H - 10, Wo = W - 10;
   const int y0 = blockIdx.x * kSsimTY, x0 = blockIdx.y * kSsimTX, c = blockIdx.z;
@@ -146,51 +195,56 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_fwd(const float* __restri
     s_b[ix][iy] = in ? pb[(int64_t)x * H + y] : 0.0f;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kSsimTX * kSsimIY; k += kSsimThreads) {
-    const int tx = k / kSsimIY, iy = k - tx * kSsimIY;
-    float m[5] = {0, 0, 0, 0, 0};
+  for (int k = threadIdx.x; k < (kSsimTX / kSsimG) * kSsimIY; k += kSsimThreads) {
+    const int g = k / kSsimIY, iy = k - g * kSsimIY, tx0 = kSsimG * g;
+    float m[kSsimG][5];
+    ssim_hpass<5>(win,
+                  [&](int j, float v[5]) {
+                    const float va = s_a[tx0 + j][iy], vb = s_b[tx0 + j][iy];
+                    v[0] = va;
+                    v[1] = vb;
+                    v[2] = va * va;
+                    v[3] = vb * vb;
+                    v[4] = va * vb;
+                  },
+                  m);
 #pragma unroll
-    for (int i = 0; i < 11; ++i) {
-      const float va = s_a[tx + i][iy], vb = s_b[tx + i][iy], w = win.w[i];
-      m[0] += w * va;
-      m[1] += w * vb;
-      m[2] += w * (va * va);
-      m[3] += w * (vb * vb);
-      m[4] += w * (va * vb);
-    }
+    for (int o = 0; o < kSsimG; ++o)
 #pragma unroll
-    for (int q = 0; q < 5; ++q) s_h[q][tx][iy] = m[q];
+      for (int q = 0; q < 5; ++q) s_h[q][tx0 + o][iy] = m[o][q];
   }
   __syncthreads();
   double sval = 0.0;
   const int64_t gplane = (int64_t)Wo * Ho, gstride = 3 * gplane;
   const float c1 = 0.01f * 0.01f, c2 = 0.03f * 0.03f, iw = (float)inv_windows;
-  for (int k = threadIdx.x; k < kSsimTX * kSsimTY; k += kSsimThreads) {
-    const int tx = k / kSsimTY, ty = k - tx * kSsimTY;
-    const int xo = x0 + tx, yo = y0 + ty;
-    if (xo >= Wo || yo >= Ho) continue;
-    float v[5];
+  constexpr int kGy = kSsimTY / kSsimG;
+  for (int k = threadIdx.x; k < kSsimTX * kGy; k += kSsimThreads) {
+    const int tx = k / kGy, ty0 = kSsimG * (k - tx * kGy);
+    const int xo = x0 + tx;
+    if (xo >= Wo) continue;
+    float v[5][kSsimG];
 #pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      float acc = 0.0f;
+    for (int q = 0; q < 5; ++q) ssim_vpass(win, &s_h[q][tx][ty0], v[q]);
 #pragma unroll
-      for (int i = 0; i < 11; ++i) acc += win.w[i] * s_h[q][tx][ty + i];
-      v[q] = acc;
+    for (int o = 0; o < kSsimG; ++o) {
+      const int yo = y0 + ty0 + o;
+      if (yo >= Ho) break;
+      const float mu_a = v[0][o], mu_b = v[1][o];
+      const float var_a = v[2][o] - mu_a * mu_a, var_b = v[3][o] - mu_b * mu_b, cov = v[4][o] - mu_a * mu_b;
+      const float n1 = 2.0f * mu_a * mu_b + c1, n2 = 2.0f * cov + c2;
+      const float d1 = mu_a * mu_a + mu_b * mu_b + c1, d2 = var_a + var_b + c2;
+      const float inv12 = 1.0f / (d1 * d2);  // one division: 1 / d2 = d1 inv12
+      const float sc = n1 * n2 * inv12;
+      sval += sc;
+      const float d_mu_a = (2.0f * mu_b * n2 - 2.0f * mu_a * sc * d2) * inv12 * iw;
+      const float d_var_a = -sc * (d1 * inv12) * iw;
+      const float d_cov = 2.0f * n1 * inv12 * iw;
+      const int64_t idx = c * gplane + (int64_t)xo * Ho + yo;
+      gmaps[0 * gstride + idx] = d_mu_a;
+      gmaps[1 * gstride + idx] = d_var_a;
+      gmaps[2 * gstride + idx] = d_cov;
+      gmaps[3 * gstride + idx] = 2.0f * d_var_a * mu_a + d_cov * mu_b;
     }
-    const float mu_a = v[0], mu_b = v[1];
-    const float var_a = v[2] - mu_a * mu_a, var_b = v[3] - mu_b * mu_b, cov = v[4] - mu_a * mu_b;
-    const float n1 = 2.0f * mu_a * mu_b + c1, n2 = 2.0f * cov + c2;
-    const float d1 = mu_a * mu_a + mu_b * mu_b + c1, d2 = var_a + var_b + c2;
-    const float sc = (n1 * n2) / (d1 * d2);
-    sval += sc;
-    const float d_mu_a = (2.0f * mu_b * n2 - 2.0f * mu_a * sc * d2) / (d1 * d2) * iw;
-    const float d_var_a = (-sc / d2) * iw;
-    const float d_cov = (2.0f * (n1 / d1) / d2) * iw;
-    const int64_t idx = c * gplane + (int64_t)xo * Ho + yo;
-    gmaps[0 * gstride + idx] = d_mu_a;
-    gmaps[1 * gstride + idx] = d_var_a;
-    gmaps[2 * gstride + idx] = d_cov;
-    gmaps[3 * gstride + idx] = 2.0f * d_var_a * mu_a + d_cov * mu_b;
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) sval += __shfl_xor_sync(0xffffffffu, sval, d);
@@ -213,7 +267,7 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_bwd(const float* __restri
                                                            float* __restrict__ grad, double* __restrict__ l1_partial) {
   pdl_wait();
   __shared__ float s_g[4][kSsimIX][kSsimIY];
-  __shared__ float s_h[4][kSsimTX][kSsimIY];
+  __shared__ __align__(16) float s_h[4][kSsimTX][kSsimHY];
   __shared__ double s_w[kSsimThreads / 32];
   const int Ho = H - 10, Wo = W - 10;
   const int y0 = blockIdx.x * kSsimTY, x0 = blockIdx.y * kSsimTX, c = blockIdx.z;
@@ -228,38 +282,43 @@ __global__ void __launch_bounds__(kSsimThreads) k_ssim_bwd(const float* __restri
     for (int q = 0; q < 4; ++q) s_g[q][ix][iy] = in ? gmaps[q * gstride + idx] : 0.0f;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kSsimTX * kSsimIY; k += kSsimThreads) {
-    const int tx = k / kSsimIY, iy = k - tx * kSsimIY;
+  for (int k = threadIdx.x; k < (kSsimTX / kSsimG) * kSsimIY; k += kSsimThreads) {
+    const int g = k / kSsimIY, iy = k - g * kSsimIY, tx0 = kSsimG * g;
+    float m[kSsimG][4];
+    ssim_hpass<4>(win,
+                  [&](int j, float v[4]) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float acc = 0.0f;
+                    for (int q = 0; q < 4; ++q) v[q] = s_g[q][tx0 + j][iy];
+                  },
+                  m);
 #pragma unroll
-      for (int i = 0; i < 11; ++i) acc += win.w[i] * s_g[q][tx + i][iy];
-      s_h[q][tx][iy] = acc;
-    }
+    for (int o = 0; o < kSsimG; ++o)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s_h[q][tx0 + o][iy] = m[o][q];
   }
   __syncthreads();
   double l1 = 0.0;
   const int64_t plane = (int64_t)W * H;
-  for (int k = threadIdx.x; k < kSsimTX * kSsimTY; k += kSsimThreads) {
-    const int tx = k / kSsimTY, ty = k - tx * kSsimTY;
-    const int x = x0 + tx, y = y0 + ty;
-    if (x >= W || y >= H) continue;
-    float S[4];
+  constexpr int kGy = kSsimTY / kSsimG;
+  for (int k = threadIdx.x; k < kSsimTX * kGy; k += kSsimThreads) {
+    const int tx = k / kGy, ty0 = kSsimG * (k - tx * kGy);
+    const int x = x0 + tx;
+    if (x >= W) continue;
+    float S[4][kSsimG];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float acc = 0.0f;
+    for (int q = 0; q < 4; ++q) ssim_vpass(win, &s_h[q][tx][ty0], S[q]);
 #pragma unroll
-      for (int i = 0; i < 11; ++i) acc += win.w[i] * s_h[q][tx][ty + i];
-      S[q] = acc;
+    for (int o = 0; o < kSsimG; ++o) {
+      const int y = y0 + ty0 + o;
+      if (y >= H) break;
+      const int64_t p = c * plane + (int64_t)x * H + y;
+      const float va = a[p], vb = b[p];
+      const float d = va - vb;
+      l1 += (double)fabsf(d);
+      const float sign = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
+      const float g_ssim = S[0][o] + (2.0f * va * S[1][o] + vb * S[2][o]) - S[3][o];
+      grad[p] = (1.0f - lambda) * sign / pixels - lambda * g_ssim;
     }
-    const int64_t p = c * plane + (int64_t)x * H + y;
-    const float va = a[p], vb = b[p];
-    const float d = va - vb;
-    l1 += (double)fabsf(d);
-    const float sign = d > 0.0f ? 1.0f : (d < 0.0f ? -1.0f : 0.0f);
-    const float g_ssim = S[0] + (2.0f * va * S[1] + vb * S[2]) - S[3];
-    grad[p] = (1.0f - lambda) * sign / pixels - lambda * g_ssim;
   }
 #pragma unroll
   for (int dd = 16; dd > 0; dd >>= 1) l1 += __shfl_xor_sync(0xffffffffu, l1, dd);

@@ -137,10 +137,10 @@ def test_view_sharded_step_sums_views_on_one_gpu(gpu_ctx):
     assert not torch.equal(before, cloud.means)
 
 
-@pytest.mark.parametrize("lam", [0.2, 0.5])
-def test_photometric_loss_with_ssim_matches_oracle(gpu_ctx, lam):
-    """metrics.hpp:83-184 (SSIM window 11, sigma 1.5, K1 .01, K2 .03) vs the fp64 oracle."""
-    W, H = 256, 128
+@pytest.mark.parametrize("lam,W,H", [(0.2, 256, 128), (0.5, 256, 128), (0.2, 203, 77), (0.2, 1030, 515)])
+def test_photometric_loss_with_ssim_matches_oracle(gpu_ctx, lam, W, H):
+    """metrics.hpp:83-184 (SSIM window 11, sigma 1.5, K1 .01, K2 .03) vs the fp64 oracle;
+    sizes off the kernels' 56 x 16 tiles and 4-output runs included."""
     rng = np.random.default_rng(11)
     a = rng.random(3 * W * H, dtype=np.float32)
     b = np.clip(a + rng.normal(0, 0.1, a.shape).astype(np.float32), 0, 1).astype(np.float32)
