@@ -299,11 +299,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     stages = ctx.stage_times()
     ctx.set_profiling(False)
-    # Work counters of the same frames (a separate pass: each read synchronises).
+    # Work counters of the same frames (a separate pass: each read synchronises; the
+    # timed frames do not count).
     work = []
+    ctx.lib.odgs_frame_set_flags(frame.handle, capi.FRAME_COUNT_WORK)
     for k in range(args.steps):
         render(ctx, dcloud, camera(k, rank), settings, out=frame)
         work.append(frame.work())
+    ctx.lib.odgs_frame_set_flags(frame.handle, 0)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

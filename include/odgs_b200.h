@@ -143,7 +143,8 @@ typedef enum {
 #define ODGS_FRAME_KEEP_COV2D 0x1u   /* also store Sigma_2D (for ODGS_FRAME_SPLAT_COV2D) */
 #define ODGS_FRAME_PLAIN_BLEND 0x2u  /* disable warp culling in the blend (A/B checks) */
 #define ODGS_FRAME_KEEP_SPLAT_GRADS 0x4u /* backward also stores SplatGrads (SPLATGRAD_* fields) */
-#define ODGS_FRAME_COUNT_WORK 0x8u  /* backward counts its work (odgs_frame_backward_work); costs time */
+#define ODGS_FRAME_COUNT_WORK 0x8u  /* blend and backward count their work (odgs_frame_work,
+                                       odgs_frame_backward_work); costs time */
 
 /* odgs_backward flags */
 #define ODGS_ACCUMULATE 0x1u /* add into the gradient buffers (GradBuffers::accumulate) */
@@ -216,7 +217,8 @@ odgs_status odgs_frame_get_info(const odgs_frame* frame, odgs_frame_info* info);
 odgs_status odgs_frame_download(odgs_ctx* ctx, odgs_frame* frame, int field, void* host_dst, size_t bytes);
 /* Blend work of the last render into `frame` (for rooflines): pixel-entry
    evaluations examined (sum over pixels of walked, +1 when the walk stopped early)
-   and entries composited. Synchronizes. */
+   and entries composited; zeros unless the frame has ODGS_FRAME_COUNT_WORK.
+   Synchronizes. */
 odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* frame, int64_t* entries_examined,
                             int64_t* entries_composited);
 /* Backward work of the last odgs_backward / odgs_grad_pixels_to_splats on `frame` (for

@@ -99,6 +99,7 @@ struct odgs_frame {
     int32_t row_begin = 0, row_end = 0;
   } req;
   int depth_which = 0, tile_which = 0;
+  bool work_counted = false;  // the last blend counted its work (ODGS_FRAME_COUNT_WORK)
   int64_t n_sorted = 0;  // depth-sorted ranks: n, or the band's Gaussians (band compaction)
   PeerImages peers{};    // odgs_frame_set_image_peers
   DevCamera cam{};
@@ -607,8 +608,13 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ODGS_CUDA(ctx, ensure(f->image, sizeof(float) * 3 * px, s));
   ODGS_CUDA(ctx, ensure(f->trans, sizeof(float) * px, s));
   ODGS_CUDA(ctx, ensure(f->walked, sizeof(int32_t) * px, s));
-  ODGS_CUDA(ctx, ensure(f->work, 2 * sizeof(unsigned long long), s));
-  ODGS_CUDA(ctx, cudaMemsetAsync(f->work.p, 0, 2 * sizeof(unsigned long long), s));
+  // Work counters only for frames that ask for them (a memset in the stream would also
+  // break the programmatic-launch chain into the blend).
+  f->work_counted = (f->flags & ODGS_FRAME_COUNT_WORK) != 0;
+  if (f->work_counted) {
+    ODGS_CUDA(ctx, ensure(f->work, 2 * sizeof(unsigned long long), s));
+    ODGS_CUDA(ctx, cudaMemsetAsync(f->work.p, 0, 2 * sizeof(unsigned long long), s));
+  }
   BlendArgs ba;
   ba.offsets = f->offsets.as<int32_t>();
   ba.vals = f->evals[f->tile_which].as<uint32_t>();
@@ -627,7 +633,7 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   ba.image = f->image.as<float>();
   ba.transmittance = f->trans.as<float>();
   ba.walked = f->walked.as<int32_t>();
-  ba.work = f->work.as<unsigned long long>();
+  ba.work = f->work_counted ? f->work.as<unsigned long long>() : nullptr;
   ba.order = f->tile_order.as<uint32_t>();
   ba.peers = f->peers;
   ba.plain = (f->flags & ODGS_FRAME_PLAIN_BLEND) != 0;
@@ -1182,9 +1188,11 @@ odgs_status odgs_frame_work(odgs_ctx* ctx, odgs_frame* f, int64_t* entries_exami
   if (!ctx || !f || !f->rendered) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "frame not rendered");
   odgs_status st;
   if ((st = finish_frame(ctx, f)) != ODGS_OK) return st;
-  unsigned long long w[2];
-  ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
-  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  unsigned long long w[2] = {0, 0};
+  if (f->work_counted) {
+    ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
+    ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   if (entries_examined) *entries_examined = (int64_t)w[0];
   if (entries_composited) *entries_composited = (int64_t)w[1];
   return ok(ctx);

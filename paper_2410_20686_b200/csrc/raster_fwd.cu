@@ -1018,7 +1018,7 @@ __global__ void __launch_bounds__(kBlendThreads) k_blend(
 // kSmallCutoff: cutoff^2 <= 172, so every composited entry has -d2/2 >= -86 and the
 // exponential's underflow branch is dead: pm_expf_blend(x) == pm_expf_blend_core(
 // fminf(x, 88)) there, bit for bit, without a branch in the walk.
-template <bool kSmallCutoff>
+template <bool kSmallCutoff, bool kCount>
 #ifndef ODGS_BLEND_MINB
 #define ODGS_BLEND_MINB 7
 #endif
@@ -1039,7 +1039,9 @@ __global__ void __launch_bounds__(kBlendThreads, ODGS_BLEND_MINB) k_blend_cull(
   };
   __shared__ Staged s_ent[kBlendThreads];
   __shared__ uint8_t s_mask[kBlendThreads];
-  __shared__ uint8_t s_list[kWarps][kBlendThreads];
+  // Per-warp lists of byte offsets into s_ent (the walk addresses a record without a
+  // multiply).
+  __shared__ uint16_t s_list[kWarps][kBlendThreads];
   __shared__ float4 s_wbox[kWarps];  // pixel-centre bbox of each warp: xmin, xmax, ymin, ymax
 
   const int tile = tile_base + (int)(order ? order[blockIdx.x] : blockIdx.x);
@@ -1137,17 +1139,18 @@ __global__ void __launch_bounds__(kBlendThreads, ODGS_BLEND_MINB) k_blend_cull(
     for (int c = 0; c < kBlendThreads / 32; ++c) {
       const bool mine = (s_mask[c * 32 + lane] >> warp) & 1u;
       const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-      if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint8_t)(c * 32 + lane);
+      if (mine) s_list[warp][n_list + __popc(bal & lt_mask)] = (uint16_t)((c * 32 + lane) * sizeof(Staged));
       n_list += __popc(bal);
     }
     __syncwarp();
     if (!done) {
-      for (int q = 0; q < n_list; ++q) {
-        const int j = s_list[warp][q];
-        const float4 geo = s_ent[j].geo;
+      const char* ent_base = reinterpret_cast<const char*>(s_ent);
+      for (const uint16_t *lp = s_list[warp], *lend = s_list[warp] + n_list; lp != lend; ++lp) {
+        const Staged& ent = *reinterpret_cast<const Staged*>(ent_base + *lp);
+        const float4 geo = ent.geo;
         const float dx = px - geo.x;
         const float dy = py - geo.y;
-        const float4 att = s_ent[j].att;
+        const float4 att = ent.att;
         const float d2 = geo.z * dx * dx + geo.w * dx * dy + att.x * dy * dy;
         if (d2 > cutoff2) continue;
         const float x = -d2 / 2.0f;
@@ -1156,15 +1159,15 @@ __global__ void __launch_bounds__(kBlendThreads, ODGS_BLEND_MINB) k_blend_cull(
         const float alpha = fminf(alpha_clamp, att.y * G);
         const float t_next = t * (1.0f - alpha);
         if (t_next < transmittance_floor) {
-          walked = base + j - e0;
+          walked = base + (int)(*lp / sizeof(Staged)) - e0;
           done = true;
           break;
         }
         const float wgt = alpha * t;
-        ++contrib;
+        if (kCount) ++contrib;
         cr = cr + att.z * wgt;
         cg = cg + att.w * wgt;
-        cb = cb + s_ent[j].b.x * wgt;
+        cb = cb + ent.b.x * wgt;
         t = t_next;
       }
     }
@@ -1173,12 +1176,14 @@ __global__ void __launch_bounds__(kBlendThreads, ODGS_BLEND_MINB) k_blend_cull(
   // The pixel again from its centre (exact: coordinates < 2^23), so x, y and the valid
   // flag need no registers across the walk.
   const bool valid_px = px >= 0.0f;
-  const uint32_t exam = valid_px ? (uint32_t)min(walked + 1, e1 - e0) : 0u;
-  const uint32_t w_exam = __reduce_add_sync(0xffffffffu, exam);
-  const uint32_t w_contrib = __reduce_add_sync(0xffffffffu, contrib);
-  if (lane == 0 && work) {
-    atomicAdd(work, (unsigned long long)w_exam);
-    atomicAdd(work + 1, (unsigned long long)w_contrib);
+  if (kCount) {
+    const uint32_t exam = valid_px ? (uint32_t)min(walked + 1, e1 - e0) : 0u;
+    const uint32_t w_exam = __reduce_add_sync(0xffffffffu, exam);
+    const uint32_t w_contrib = __reduce_add_sync(0xffffffffu, contrib);
+    if (lane == 0) {
+      atomicAdd(work, (unsigned long long)w_exam);
+      atomicAdd(work + 1, (unsigned long long)w_contrib);
+    }
   }
   if (valid_px) {
     const int64_t plane = (int64_t)width * height;
@@ -1207,7 +1212,9 @@ void launch_blend(const BlendArgs& a, cudaStream_t stream) {
   if (n_band_tiles <= 0) return;
   if (!a.plain && a.tile_size <= 16) {
     const float cutoff2 = a.cutoff_sigma * a.cutoff_sigma;
-    auto kern = cutoff2 <= 172.0f ? k_blend_cull<true> : k_blend_cull<false>;
+    // Work counters (examined / composited entries) only when the frame asks for them.
+    auto kern = cutoff2 <= 172.0f ? (a.work ? k_blend_cull<true, true> : k_blend_cull<true, false>)
+                                  : (a.work ? k_blend_cull<false, true> : k_blend_cull<false, false>);
     launch_pdl(kern, n_band_tiles, kBlendThreads, 0, stream, a.offsets, a.vals, a.sp_ab, a.sp_c, a.width, a.height,
                                                       a.tile_size, a.tiles_x, a.alpha_clamp, a.transmittance_floor,
                                                       cutoff2, a.image, a.transmittance, a.walked, a.work,

@@ -223,9 +223,14 @@ def test_warp_culled_blend_equals_plain_blend(gpu_ctx, tile):
     c = scenes.cloud_c3(200_000)
     cam = CameraPose(2048, 1024, rot_yaw(0.3))
     s = RenderSettings(tile_size=tile)
-    a = render(gpu_ctx, c, cam, s)
-    b = render(gpu_ctx, c, cam, s, flags=capi.FRAME_PLAIN_BLEND)
+    a = render(gpu_ctx, c, cam, s, flags=capi.FRAME_COUNT_WORK)
+    b = render(gpu_ctx, c, cam, s, flags=capi.FRAME_PLAIN_BLEND | capi.FRAME_COUNT_WORK)
     assert np.array_equal(a.image, b.image)
     assert np.array_equal(a.walked, b.walked)
     assert np.array_equal(a.transmittance, b.transmittance)
     assert a.work() == b.work()
+    assert a.work()[1] > 0
+    # without ODGS_FRAME_COUNT_WORK the blend counts nothing (and its outputs are the same)
+    d = render(gpu_ctx, c, cam, s)
+    assert d.work() == (0, 0)
+    assert np.array_equal(a.image, d.image) and np.array_equal(a.walked, d.walked)
