@@ -99,7 +99,8 @@ struct odgs_frame {
     int32_t row_begin = 0, row_end = 0;
   } req;
   int depth_which = 0, tile_which = 0;
-  bool work_counted = false;  // the last blend counted its work (ODGS_FRAME_COUNT_WORK)
+  bool work_counted = false;      // the last blend counted its work (ODGS_FRAME_COUNT_WORK)
+  bool bwd_work_counted = false;  // the last backward did
   int64_t n_sorted = 0;  // depth-sorted ranks: n, or the band's Gaussians (band compaction)
   PeerImages peers{};    // odgs_frame_set_image_peers
   DevCamera cam{};
@@ -313,20 +314,16 @@ odgs_status read_errors(odgs_ctx* ctx) {
 }
 
 odgs_status reset_errors(odgs_ctx* ctx) {
-  ODGS_CUDA(ctx, cudaMemcpyAsync(ctx->d_err, ctx->h_err_init, sizeof(DevErrors), cudaMemcpyHostToDevice, ctx->stream));
+  launch_reset_errors(ctx->d_err, false, ctx->stream);
+  ODGS_CUDA(ctx, cudaGetLastError());
   return ODGS_OK;
 }
 
 // A render starts: its counters are reset; the sticky words too, unless earlier
 // asynchronous work on the frame is still unchecked (its errors must survive to the check).
 odgs_status reset_frame_errors(odgs_ctx* ctx, odgs_frame* f) {
-  if (f->pending || f->bwd_pending) {
-    char* d = reinterpret_cast<char*>(f->d_err) + kDevErrorsSticky;
-    ODGS_CUDA(ctx, cudaMemcpyAsync(d, reinterpret_cast<const char*>(ctx->h_err_init) + kDevErrorsSticky,
-                                   sizeof(DevErrors) - kDevErrorsSticky, cudaMemcpyHostToDevice, ctx->stream));
-  } else {
-    ODGS_CUDA(ctx, cudaMemcpyAsync(f->d_err, ctx->h_err_init, sizeof(DevErrors), cudaMemcpyHostToDevice, ctx->stream));
-  }
+  launch_reset_errors(f->d_err, f->pending || f->bwd_pending, ctx->stream);
+  ODGS_CUDA(ctx, cudaGetLastError());
   return ODGS_OK;
 }
 
@@ -613,7 +610,7 @@ odgs_status blend_impl(odgs_ctx* ctx, odgs_frame* f) {
   f->work_counted = (f->flags & ODGS_FRAME_COUNT_WORK) != 0;
   if (f->work_counted) {
     ODGS_CUDA(ctx, ensure(f->work, 2 * sizeof(unsigned long long), s));
-    ODGS_CUDA(ctx, cudaMemsetAsync(f->work.p, 0, 2 * sizeof(unsigned long long), s));
+    launch_zero_bytes(f->work.p, 2 * sizeof(unsigned long long), s);
   }
   BlendArgs ba;
   ba.offsets = f->offsets.as<int32_t>();
@@ -709,10 +706,11 @@ odgs_status raster_fold(odgs_ctx* ctx, odgs_frame* f, const float* dl_dimage, in
   ODGS_CUDA(ctx, ensure(f->touched, (size_t)K + 16, s));
   ODGS_CUDA(ctx, ensure(f->folded, sizeof(float) * 9 * (size_t)n + 16, s));
   ODGS_CUDA(ctx, ensure(f->bwd_work, 4 * sizeof(unsigned long long), s));
-  ODGS_CUDA(ctx, cudaMemsetAsync(f->bwd_work.p, 0, 4 * sizeof(unsigned long long), s));
+  f->bwd_work_counted = (f->flags & ODGS_FRAME_COUNT_WORK) != 0;
+  if (f->bwd_work_counted) launch_zero_bytes(f->bwd_work.p, 4 * sizeof(unsigned long long), s);
   {
     StageScope sc(ctx, ODGS_STAGE_BWD_RASTER);
-    if (K) ODGS_CUDA(ctx, cudaMemsetAsync(f->touched.p, 0, (size_t)K, s));
+    if (K) launch_zero_bytes(f->touched.p, (size_t)K, s);
     BwdRasterArgs ra;
     ra.offsets = f->offsets.as<int32_t>();
     ra.vals = f->evals[f->tile_which].as<uint32_t>();
@@ -861,6 +859,7 @@ odgs_status odgs_ctx_create(int device, void* stream, odgs_ctx** out) {
     odgs_ctx_destroy(ctx);
     return e == cudaErrorMemoryAllocation ? ODGS_ERR_OUT_OF_MEMORY : ODGS_ERR_CUDA;
   }
+  std::memset(ctx->h_err_init, 0, sizeof(DevErrors));  // overflow, counters, k_sort: 0
   ctx->h_err_init->nonfinite = kNoError;
   ctx->h_err_init->project = kNoError;
   ctx->h_err_init->bwd_domain = kNoError;
@@ -1106,9 +1105,11 @@ odgs_status odgs_frame_check(odgs_ctx* ctx, odgs_frame* frame, int32_t* rerender
 
 odgs_status odgs_frame_backward_work(odgs_ctx* ctx, odgs_frame* f, int64_t* counters, int32_t n_counters) {
   if (!ctx || !f || !f->bwd_work.p) return set_error(ctx, ODGS_ERR_INVALID_ARGUMENT, -1, "no backward on this frame");
-  unsigned long long w[4];
-  ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->bwd_work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
-  ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  unsigned long long w[4] = {0, 0, 0, 0};
+  if (f->bwd_work_counted) {
+    ODGS_CUDA(ctx, cudaMemcpyAsync(w, f->bwd_work.p, sizeof w, cudaMemcpyDeviceToHost, ctx->stream));
+    ODGS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   for (int k = 0; k < n_counters && k < 4; ++k) counters[k] = (int64_t)w[k];
   return ok(ctx);
 }

@@ -63,6 +63,12 @@ struct EmitArgs {
 };
 void launch_emit(const EmitArgs& a, cudaStream_t stream);
 
+// Stream-ordered resets as kernels (they join the programmatic-launch chain; a memcpy or
+// memset node would break it): the per-render counters (and, unless keep_sticky, the
+// sticky error words) to their initial values; `bytes` zero bytes at a cudaMalloc base.
+void launch_reset_errors(DevErrors* e, bool keep_sticky, cudaStream_t stream);
+void launch_zero_bytes(void* p, size_t bytes, cudaStream_t stream);
+
 void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, float far_r, uint8_t* keep,
                  cudaStream_t stream);
 

@@ -658,6 +658,48 @@ void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t
   ++g_launches;
 }
 
+// ------------------------------------------------------------------ stream-ordered resets
+// Kernels instead of memcpy / memset nodes, so they join the programmatic-launch chain.
+__global__ void k_reset_errors(DevErrors* __restrict__ e, int keep_sticky) {
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  if (!keep_sticky) {
+    e->nonfinite = kNoError;
+    e->project = kNoError;
+    e->bwd_domain = kNoError;
+    e->bwd_nonfinite = kNoError;
+    e->overflow = 0;
+  }
+  e->n_entries = 0;
+  e->n_visible = 0;
+  e->n_instances = 0;
+  e->n_band = 0;
+  e->n_precull = 0;
+  e->k_sort = 0;
+}
+
+void launch_reset_errors(DevErrors* e, bool keep_sticky, cudaStream_t stream) {
+  launch_pdl(k_reset_errors, 1, 32, 0, stream, e, keep_sticky ? 1 : 0);
+  ++g_launches;
+}
+
+__global__ void k_zero_bytes(uint4* __restrict__ p, int64_t n16, uint8_t* __restrict__ tail, int n_tail) {
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) p[i] = make_uint4(0, 0, 0, 0);
+  if (blockIdx.x == 0 && (int)threadIdx.x < n_tail) tail[threadIdx.x] = 0;
+}
+
+void launch_zero_bytes(void* p, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return;
+  // p is a cudaMalloc base (256-byte aligned)
+  const int64_t n16 = (int64_t)(bytes / 16);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, 148 * 8));
+  launch_pdl(k_zero_bytes, grid, 256, 0, stream, static_cast<uint4*>(p), n16,
+             static_cast<uint8_t*>(p) + 16 * n16, (int)(bytes - 16 * (size_t)n16));
+  ++g_launches;
+}
+
 // ------------------------------------------------------------------ emit tile entries
 constexpr int kEmitWarps = 8;
 
