@@ -306,3 +306,25 @@ def test_pipelined_backward_kernel_matches_default(gpu_ctx):
     for k in GROUPS:
         assert group_rel(got[k], getattr(ref, k)) < 1e-5, k
     assert np.array_equal(got["observed"], ref.observed)
+
+
+def test_work_counters_are_opt_in_and_do_not_change_results(gpu_ctx):
+    """ODGS_FRAME_COUNT_WORK: the blend and backward count their work only on frames that
+    ask (zeros otherwise, also after a counting pass), and counting changes no output."""
+    from paper_2410_20686_b200 import scenes
+    c = scenes.cloud_c3(50_000)
+    cam = CameraPose(512, 256)
+    gs, _ = settings_pair()
+    dl = probe(5, 512, 256)
+    fr = render(gpu_ctx, c, cam, gs, flags=capi.FRAME_COUNT_WORK)
+    g1 = backward(gpu_ctx, c, cam, fr, dl, gs)
+    w1, b1 = fr.work(), fr.backward_work()
+    assert w1[0] > 0 and w1[1] > 0 and b1[0] > 0 and b1[1] > 0
+    img1 = fr.image.copy()
+    gpu_ctx.lib.odgs_frame_set_flags(fr.handle, 0)
+    render(gpu_ctx, c, cam, gs, out=fr)
+    g0 = backward(gpu_ctx, c, cam, fr, dl, gs)
+    assert fr.work() == (0, 0) and fr.backward_work() == (0, 0, 0, 0)
+    assert np.array_equal(fr.image, img1)
+    for k in GROUPS:
+        assert np.array_equal(getattr(g0, k), getattr(g1, k)), k
