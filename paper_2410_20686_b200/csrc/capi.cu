@@ -1409,8 +1409,7 @@ odgs_status odgs_backward(odgs_ctx* ctx, const odgs_cloud* cloud, const odgs_cam
   // The backward's error words live in the frame's sticky section: cleared here unless
   // an earlier operation on the frame is still unchecked (then they accumulate until the
   // check point).
-  if (!f->pending && !f->bwd_pending)
-    ODGS_CUDA(ctx, cudaMemcpyAsync(f->d_err, ctx->h_err_init, kDevErrorsSticky, cudaMemcpyHostToDevice, s));
+  if (!f->pending && !f->bwd_pending) launch_reset_sticky(f->d_err, s);
   if ((st = raster_fold(ctx, f, dl_dimage, dl_memory, settings)) != ODGS_OK) return st;
 
   BwdSplatArgs sa;

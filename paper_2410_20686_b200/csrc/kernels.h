@@ -67,6 +67,7 @@ void launch_emit(const EmitArgs& a, cudaStream_t stream);
 // memset node would break it): the per-render counters (and, unless keep_sticky, the
 // sticky error words) to their initial values; `bytes` zero bytes at a cudaMalloc base.
 void launch_reset_errors(DevErrors* e, bool keep_sticky, cudaStream_t stream);
+void launch_reset_sticky(DevErrors* e, cudaStream_t stream);  // the sticky words only
 void launch_zero_bytes(void* p, size_t bytes, cudaStream_t stream);
 
 void launch_cull(int64_t n, const float* means, DevCamera cam, float near_r, float far_r, uint8_t* keep,

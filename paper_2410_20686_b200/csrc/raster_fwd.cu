@@ -660,16 +660,18 @@ void launch_concat_segments(int64_t n, const uint32_t* seg_count, const uint32_t
 
 // ------------------------------------------------------------------ stream-ordered resets
 // Kernels instead of memcpy / memset nodes, so they join the programmatic-launch chain.
-__global__ void k_reset_errors(DevErrors* __restrict__ e, int keep_sticky) {
+// mode 0: everything; 1: the counters (sticky words kept); 2: the sticky words only.
+__global__ void k_reset_errors(DevErrors* __restrict__ e, int mode) {
   pdl_wait();
   if (threadIdx.x != 0) return;
-  if (!keep_sticky) {
+  if (mode != 1) {
     e->nonfinite = kNoError;
     e->project = kNoError;
     e->bwd_domain = kNoError;
     e->bwd_nonfinite = kNoError;
     e->overflow = 0;
   }
+  if (mode == 2) return;
   e->n_entries = 0;
   e->n_visible = 0;
   e->n_instances = 0;
@@ -680,6 +682,11 @@ __global__ void k_reset_errors(DevErrors* __restrict__ e, int keep_sticky) {
 
 void launch_reset_errors(DevErrors* e, bool keep_sticky, cudaStream_t stream) {
   launch_pdl(k_reset_errors, 1, 32, 0, stream, e, keep_sticky ? 1 : 0);
+  ++g_launches;
+}
+
+void launch_reset_sticky(DevErrors* e, cudaStream_t stream) {
+  launch_pdl(k_reset_errors, 1, 32, 0, stream, e, 2);
   ++g_launches;
 }
 
